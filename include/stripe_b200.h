@@ -1,0 +1,138 @@
+/*
+ * stripe_b200.h — C ABI of the B200-native Stripe block executor.
+ *
+ * Drop-in boundary for the reference's block executor (Stripe Kit,
+ * arXiv 1903.06498 reference).  The reference exposes a C++ free-function API
+ * with no FFI; each entry point below replaces one reference interface, cited
+ * file:line relative to /root/reference/proj:
+ *
+ *   sb_program_parse / sb_program_print    parse_program / print_program   include/stripe/text.h:20-25
+ *   sb_program_buffer_*                    Program::buffers, rebind_buffers include/stripe/ir.h:146-160
+ *   sb_program_output_identity             prepare_outputs' fill value      include/stripe/interp.h:70-73
+ *   sb_execute                             execute(Program, BufferStore*, ExecOptions)
+ *                                                                           include/stripe/interp.h:68
+ *   sb_execute_device                      same, buffers already resident in HBM (benchmarks)
+ *   sb_exec_options                        ExecOptions / IterOrder          include/stripe/interp.h:58-64
+ *   sb_last_error / SB_ERR_*               ExecError{code}                  include/stripe/interp.h:22-26
+ *
+ * Plain C types only: no C++ or torch types cross this boundary, and no
+ * exceptions: every call returns an SB_ERR_* status and sb_last_error()
+ * holds "Code: message" for the calling thread.  There is no CPU fallback:
+ * without a usable sm_100 device, sb_context_create fails.
+ */
+#ifndef STRIPE_B200_H
+#define STRIPE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SB_ABI_VERSION 1
+
+/* Status codes; names match the reference's ExecError / ParseError codes. */
+enum {
+  SB_OK = 0,
+  SB_ERR_MISSING_BUFFER = 1,     /* "MissingBuffer"      interp.cpp:187-192, 312 */
+  SB_ERR_UNKNOWN_INTRINSIC = 2,  /* "UnknownIntrinsic"   interp.cpp:270 */
+  SB_ERR_UNKNOWN_SPECIAL = 3,    /* "UnknownSpecial"     interp.cpp:289-293, 546-549 */
+  SB_ERR_UNDEFINED_TEMP = 4,     /* "UndefinedTemp"      interp.cpp:321 */
+  SB_ERR_OUT_OF_BOUNDS = 5,      /* "OutOfBoundsAccess"  interp.cpp:463-478, 560-578 */
+  SB_ERR_UNBOUND_INDEX = 6,      /* "UnboundIndex"       affine.h:46-50 */
+  SB_ERR_SYNTAX = 7,             /* "SyntaxError"        text.h:12-18 */
+  SB_ERR_SCOPE = 8,              /* "ScopeError"         text.h:12-18 */
+  SB_ERR_UNSUPPORTED = 9,        /* outside this executor's contract (e.g. observers) */
+  SB_ERR_CUDA = 10,              /* CUDA runtime / driver failure */
+  SB_ERR_NCCL = 11,              /* NCCL failure (split aggregations) */
+  SB_ERR_INVALID = 12            /* bad argument at the ABI */
+};
+
+/* Element dtypes (bit widths; ir.h:25) plus the fp32 extension. */
+enum { SB_I8 = 8, SB_I16 = 16, SB_I32 = 32, SB_F32 = 0x20F };
+
+/* Buffer directions of root refinements. */
+enum { SB_IN = 0, SB_OUT = 1, SB_INOUT = 2 };
+
+/* Host carriers: the reference's int64 BufferStore vectors (interp.h:14-20),
+ * or native-width arrays (int8/int16/int32/float). */
+enum { SB_CARRIER_I64 = 0, SB_CARRIER_NATIVE = 1 };
+
+/* Buffer flags. */
+enum {
+  SB_BUF_PREPARE = 1 /* output absent from the store: create it with prepare_outputs' identity
+                        (interp.cpp:617-642) on the device; input contents are ignored */
+};
+
+typedef struct sb_host_buffer {
+  const char* name;
+  int32_t carrier; /* SB_CARRIER_* */
+  int32_t flags;   /* SB_BUF_* */
+  void* data;      /* int64_t[count] or native[count]; outputs are written back in place */
+  int64_t count;   /* element count; must equal the program's buffer table entry */
+} sb_host_buffer;
+
+typedef struct sb_device_buffer {
+  const char* name;
+  int32_t flags; /* SB_BUF_* */
+  int32_t reserved;
+  void* dptr;    /* native-width device array; allocation padded to 16 bytes */
+  int64_t count;
+} sb_device_buffer;
+
+typedef struct sb_exec_options {
+  int32_t order;     /* IterOrder: 0 Lex, 1 Reversed, 2 Shuffled — accepted, result is order-free */
+  int32_t observer;  /* nonzero = caller wants an ExecObserver: rejected (SB_ERR_UNSUPPORTED) */
+  uint64_t seed;     /* Shuffled seed (ignored) */
+  int32_t disable_tensor_cores; /* force the generic kernel family (testing) */
+  int32_t reserved;
+} sb_exec_options;
+
+typedef struct sb_context sb_context;
+typedef struct sb_program sb_program;
+
+const char* sb_last_error(void);
+const char* sb_status_name(int status);
+int sb_abi_version(void);
+
+/* ---- programs (host only; no GPU needed) ---- */
+int sb_program_parse(const char* text, sb_program** out);
+void sb_program_free(sb_program* p);
+int sb_program_print(const sb_program* p, char* buf, size_t cap, size_t* len);
+int sb_program_buffer_count(const sb_program* p);
+int sb_program_buffer_info(const sb_program* p, int i, const char** name, int* dtype,
+                           int64_t* elements, int* dir);
+int sb_program_output_identity(const sb_program* p, const char* name, int64_t* value);
+/* Human-readable launch plan (which kernel family / execution mode per block). */
+int sb_program_describe_plan(sb_program* p, int fresh_outputs, int disable_tensor_cores, char* buf,
+                             size_t cap, size_t* len);
+
+/* ---- device contexts ---- */
+int sb_context_create(int device, sb_context** out);
+void sb_context_destroy(sb_context* ctx);
+/* Launch on an external cudaStream_t (e.g. torch's current stream); NULL = own stream. */
+int sb_context_set_stream(sb_context* ctx, void* cuda_stream);
+void* sb_context_stream(sb_context* ctx);
+/* Waits for the stream and reports any device-side error (OutOfBoundsAccess ...). */
+int sb_context_sync(sb_context* ctx);
+/* Number of kernels this library launched on the context so far. */
+uint64_t sb_context_launch_count(sb_context* ctx);
+int sb_device_alloc(sb_context* ctx, int64_t bytes, void** dptr);
+int sb_device_free(sb_context* ctx, void* dptr);
+int sb_host_alloc_pinned(int64_t bytes, void** ptr);
+int sb_host_free_pinned(void* ptr);
+
+/* ---- execution ---- */
+/* Reference-compatible execute: host buffers in, outputs written back; synchronous. */
+int sb_execute(sb_context* ctx, sb_program* p, sb_host_buffer* bufs, int n,
+               const sb_exec_options* opts);
+/* HBM-resident execute: enqueues on the context stream and returns (call sb_context_sync). */
+int sb_execute_device(sb_context* ctx, sb_program* p, const sb_device_buffer* bufs, int n,
+                      const sb_exec_options* opts);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STRIPE_B200_H */

@@ -1,0 +1,518 @@
+// C ABI + device executor (see include/stripe_b200.h).
+//
+// sb_execute is the B200 counterpart of stripe::execute (interp.h:68,
+// interp.cpp:613-615): the buffer-table check of Executor::run
+// (interp.cpp:183-198) happens on the host, the Program is lowered once into a
+// cached plan (planner.cpp), buffers are moved to HBM at native width, the
+// plan's steps run in stream order, and outputs come back.  Errors map 1:1 to
+// the reference's ExecError codes.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/stripe_b200.h"
+#include "ir.hpp"
+#include "kernels.hpp"
+#include "plan.hpp"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int status_of(const std::string& code) {
+  static const std::map<std::string, int> m = {
+      {"MissingBuffer", SB_ERR_MISSING_BUFFER},   {"UnknownIntrinsic", SB_ERR_UNKNOWN_INTRINSIC},
+      {"UnknownSpecial", SB_ERR_UNKNOWN_SPECIAL}, {"UndefinedTemp", SB_ERR_UNDEFINED_TEMP},
+      {"OutOfBoundsAccess", SB_ERR_OUT_OF_BOUNDS}, {"UnboundIndex", SB_ERR_UNBOUND_INDEX},
+      {"SyntaxError", SB_ERR_SYNTAX},             {"ScopeError", SB_ERR_SCOPE},
+      {"Unsupported", SB_ERR_UNSUPPORTED},        {"CudaError", SB_ERR_CUDA},
+      {"NcclError", SB_ERR_NCCL},                 {"Invalid", SB_ERR_INVALID}};
+  auto it = m.find(code);
+  return it == m.end() ? SB_ERR_INVALID : it->second;
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return SB_OK;
+  } catch (const sb::Error& e) {
+    g_last_error = e.code + ": " + e.what();
+    return status_of(e.code);
+  } catch (const std::exception& e) {
+    g_last_error = std::string("Invalid: ") + e.what();
+    return SB_ERR_INVALID;
+  }
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw sb::Error("CudaError", std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+std::size_t kind_bytes(int kind) {
+  switch (kind) {
+    case sb::kI8: return 1;
+    case sb::kI16: return 2;
+    case sb::kI64: return 8;
+    default: return 4;
+  }
+}
+
+std::size_t padded(std::size_t bytes) { return (bytes + 15) / 16 * 16; }
+
+struct Compiled {
+  sb::Plan plan;
+  std::vector<sb::GenericDesc> descs;
+  std::vector<std::vector<int>> bufmaps;
+  std::vector<int> desc_of_step;
+};
+
+}  // namespace
+
+struct sb_program {
+  sb::Program prog;
+  std::mutex mu;
+  std::map<std::string, std::unique_ptr<Compiled>> plans;
+};
+
+struct sb_context {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  sb::DevError* d_err = nullptr;
+  sb::DevError* h_err = nullptr;
+  std::uint64_t launches = 0;
+  struct State {
+    sb::GenericDesc* d_descs = nullptr;
+    std::vector<void*> scratch;  // by plan buffer id (scratch only)
+  };
+  std::map<const Compiled*, State> states;
+  std::vector<std::pair<void*, std::size_t>> roots;  // host-path device buffers
+  std::vector<std::pair<void*, std::size_t>> pinned;  // host-path staging
+
+  ~sb_context() {
+    cudaSetDevice(device);
+    for (auto& [c, st] : states) {
+      cudaFree(st.d_descs);
+      for (void* p : st.scratch) cudaFree(p);
+    }
+    for (auto& r : roots) cudaFree(r.first);
+    for (auto& r : pinned) cudaFreeHost(r.first);
+    cudaFree(d_err);
+    cudaFreeHost(h_err);
+    if (own) cudaStreamDestroy(own);
+  }
+};
+
+namespace {
+
+Compiled* get_plan(sb_program* p, const std::vector<bool>& fresh, bool tc) {
+  std::string key(tc ? "T" : "G");
+  for (bool f : fresh) key += f ? '1' : '0';
+  std::lock_guard<std::mutex> lock(p->mu);
+  auto it = p->plans.find(key);
+  if (it != p->plans.end()) return it->second.get();
+  auto c = std::make_unique<Compiled>();
+  sb::PlanOptions opt;
+  opt.enable_tc = tc;
+  opt.fresh_outputs = fresh;
+  c->plan = sb::build_plan(p->prog, opt);
+  for (const auto& s : c->plan.steps) {
+    if (s.kind == sb::PStep::Launch && s.launch.kernel == sb::KernelKind::Generic) {
+      c->desc_of_step.push_back(static_cast<int>(c->descs.size()));
+      c->descs.emplace_back();
+      c->bufmaps.emplace_back();
+      sb::to_desc(s.launch, &c->descs.back(), &c->bufmaps.back());
+    } else {
+      c->desc_of_step.push_back(-1);
+    }
+  }
+  Compiled* raw = c.get();
+  p->plans[key] = std::move(c);
+  return raw;
+}
+
+sb_context::State& ensure_state(sb_context* ctx, const Compiled* c) {
+  auto it = ctx->states.find(c);
+  if (it != ctx->states.end()) return it->second;
+  sb_context::State st;
+  if (!c->descs.empty()) {
+    cuda_check(cudaMalloc(&st.d_descs, sizeof(sb::GenericDesc) * c->descs.size()), "cudaMalloc(desc)");
+    cuda_check(cudaMemcpy(st.d_descs, c->descs.data(), sizeof(sb::GenericDesc) * c->descs.size(),
+                          cudaMemcpyHostToDevice),
+               "upload desc");
+  }
+  st.scratch.assign(c->plan.bufs.size(), nullptr);
+  for (std::size_t b = 0; b < c->plan.bufs.size(); b++) {
+    const auto& pb = c->plan.bufs[b];
+    if (pb.root) continue;
+    cuda_check(cudaMalloc(&st.scratch[b], padded(pb.elements * kind_bytes(pb.kind))), "cudaMalloc(scratch)");
+  }
+  return ctx->states.emplace(c, std::move(st)).first->second;
+}
+
+// Runs every plan step on the context stream.  root_ptr/root_elems indexed by root buffer.
+void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root_ptr) {
+  auto& st = ensure_state(ctx, c);
+  const auto& plan = c->plan;
+  auto ptr_of = [&](int b) { return plan.bufs[b].root ? root_ptr[plan.bufs[b].root_index] : st.scratch[b]; };
+  for (std::size_t i = 0; i < plan.steps.size(); i++) {
+    const auto& s = plan.steps[i];
+    if (s.kind == sb::PStep::Fill) {
+      const auto& pb = plan.bufs[s.buf];
+      cuda_check(sb::launch_fill(ptr_of(s.buf), pb.kind, pb.elements, s.value, ctx->stream), "fill");
+      ctx->launches++;
+      continue;
+    }
+    const sb::PLaunch& l = s.launch;
+    if (l.kernel == sb::KernelKind::ConvI8TC) {
+      sb::ConvArgs a;
+      a.a = ptr_of(l.conv.a_buf);
+      a.b = ptr_of(l.conv.b_buf);
+      a.c = ptr_of(l.conv.c_buf);
+      a.a_elems = plan.bufs[l.conv.a_buf].elements;
+      a.b_elems = plan.bufs[l.conv.b_buf].elements;
+      a.c_elems = plan.bufs[l.conv.c_buf].elements;
+      cuda_check(sb::launch_conv_tc(l.conv, a, ctx->stream, ctx->num_sms), "conv_tc");
+      ctx->launches++;
+      continue;
+    }
+    int di = c->desc_of_step[i];
+    sb::BufTable t;
+    std::memset(&t, 0, sizeof(t));
+    const auto& map = c->bufmaps[di];
+    for (std::size_t k = 0; k < map.size(); k++) {
+      t.ptr[k] = ptr_of(map[k]);
+      t.elems[k] = plan.bufs[map[k]].elements;
+      t.kind[k] = plan.bufs[map[k]].kind;
+    }
+    cuda_check(sb::launch_generic(st.d_descs + di, l.pcount, t, ctx->d_err, static_cast<int>(i), ctx->stream),
+               "generic");
+    ctx->launches++;
+  }
+}
+
+void check_device_error(sb_context* ctx, const Compiled* c) {
+  cuda_check(cudaStreamSynchronize(ctx->stream), "stream sync");
+  if (ctx->h_err->code == 0) return;
+  cuda_check(cudaMemcpy(ctx->h_err, ctx->d_err, sizeof(sb::DevError), cudaMemcpyDeviceToHost), "err read");
+  sb::DevError e = *ctx->h_err;
+  sb::DevError zero{};
+  cudaMemcpy(ctx->d_err, &zero, sizeof(zero), cudaMemcpyHostToDevice);
+  ctx->h_err->code = 0;
+  if (e.code == 0) return;
+  std::string where = c && e.launch >= 0 && e.launch < static_cast<int>(c->plan.steps.size())
+                          ? c->plan.steps[e.launch].launch.path
+                          : "?";
+  if (e.code == 2)
+    throw sb::Error("OutOfBoundsAccess", "gather/scatter index " + std::to_string(e.addr) +
+                                             " outside range in block " + where);
+  throw sb::Error("OutOfBoundsAccess", "access at element " + std::to_string(e.addr) +
+                                           " outside buffer in block " + where);
+}
+
+std::vector<bool> fresh_flags(const sb::Program& prog, const std::vector<int>& slot_of_root,
+                              const std::vector<int>& flags) {
+  std::vector<bool> fresh(prog.buffers.size(), false);
+  for (std::size_t r = 0; r < prog.buffers.size(); r++)
+    fresh[r] = slot_of_root[r] >= 0 && (flags[slot_of_root[r]] & SB_BUF_PREPARE) &&
+               prog.buffers[r].dir != sb::Dir::In;
+  return fresh;
+}
+
+void check_opts(const sb_exec_options* o) {
+  if (o && o->observer)
+    throw sb::Error("Unsupported", "execution observers are not supported by the device executor");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sb_last_error(void) { return g_last_error.c_str(); }
+int sb_abi_version(void) { return SB_ABI_VERSION; }
+
+const char* sb_status_name(int s) {
+  static const char* names[] = {"Ok",           "MissingBuffer",  "UnknownIntrinsic", "UnknownSpecial",
+                                "UndefinedTemp", "OutOfBoundsAccess", "UnboundIndex",   "SyntaxError",
+                                "ScopeError",   "Unsupported",    "CudaError",        "NcclError",
+                                "Invalid"};
+  return s >= 0 && s <= 12 ? names[s] : "Invalid";
+}
+
+int sb_program_parse(const char* text, sb_program** out) {
+  return guarded([&] {
+    if (!text || !out) throw sb::Error("Invalid", "null argument");
+    auto p = std::make_unique<sb_program>();
+    p->prog = sb::parse_program(text);
+    *out = p.release();
+  });
+}
+
+void sb_program_free(sb_program* p) { delete p; }
+
+int sb_program_print(const sb_program* p, char* buf, size_t cap, size_t* len) {
+  return guarded([&] {
+    std::string s = sb::print_program(p->prog);
+    if (len) *len = s.size();
+    if (buf && cap) {
+      std::size_t n = std::min(s.size(), cap - 1);
+      std::memcpy(buf, s.data(), n);
+      buf[n] = 0;
+    }
+  });
+}
+
+int sb_program_buffer_count(const sb_program* p) { return static_cast<int>(p->prog.buffers.size()); }
+
+int sb_program_buffer_info(const sb_program* p, int i, const char** name, int* dtype,
+                           int64_t* elements, int* dir) {
+  return guarded([&] {
+    if (i < 0 || i >= static_cast<int>(p->prog.buffers.size())) throw sb::Error("Invalid", "buffer index");
+    const auto& b = p->prog.buffers[i];
+    if (name) *name = b.name.c_str();
+    if (dtype) *dtype = b.dtype == sb::DType::F32 ? SB_F32 : sb::dtype_bits(b.dtype);
+    if (elements) *elements = b.elements;
+    if (dir) *dir = static_cast<int>(b.dir);
+  });
+}
+
+int sb_program_output_identity(const sb_program* p, const char* name, int64_t* value) {
+  return guarded([&] { *value = sb::output_identity(p->prog, name); });
+}
+
+int sb_program_describe_plan(sb_program* p, int fresh_outputs, int disable_tc, char* buf, size_t cap,
+                             size_t* len) {
+  return guarded([&] {
+    std::vector<bool> fresh(p->prog.buffers.size(), false);
+    for (std::size_t r = 0; r < fresh.size(); r++) fresh[r] = fresh_outputs && p->prog.buffers[r].dir != sb::Dir::In;
+    Compiled* c = get_plan(p, fresh, !disable_tc);
+    std::string s = c->plan.describe();
+    if (len) *len = s.size();
+    if (buf && cap) {
+      std::size_t n = std::min(s.size(), cap - 1);
+      std::memcpy(buf, s.data(), n);
+      buf[n] = 0;
+    }
+  });
+}
+
+int sb_context_create(int device, sb_context** out) {
+  return guarded([&] {
+    int count = 0;
+    cuda_check(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+    if (device < 0 || device >= count) throw sb::Error("CudaError", "no such device");
+    cudaDeviceProp prop;
+    cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major != 10)
+      throw sb::Error("CudaError", std::string("device is not sm_100 (Blackwell): ") + prop.name);
+    auto ctx = std::make_unique<sb_context>();
+    ctx->device = device;
+    ctx->num_sms = prop.multiProcessorCount;
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    cuda_check(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking), "cudaStreamCreate");
+    ctx->stream = ctx->own;
+    cuda_check(cudaMalloc(&ctx->d_err, sizeof(sb::DevError)), "cudaMalloc(err)");
+    cuda_check(cudaMemset(ctx->d_err, 0, sizeof(sb::DevError)), "memset(err)");
+    cuda_check(cudaMallocHost(&ctx->h_err, sizeof(sb::DevError)), "cudaMallocHost");
+    // h_err->code doubles as a "maybe dirty" hint; the authoritative copy is read on sync.
+    ctx->h_err->code = 1;
+    *out = ctx.release();
+  });
+}
+
+void sb_context_destroy(sb_context* ctx) { delete ctx; }
+
+int sb_context_set_stream(sb_context* ctx, void* s) {
+  return guarded([&] { ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own; });
+}
+
+void* sb_context_stream(sb_context* ctx) { return ctx->stream; }
+
+int sb_context_sync(sb_context* ctx) {
+  return guarded([&] {
+    cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    ctx->h_err->code = 1;
+    check_device_error(ctx, nullptr);
+  });
+}
+
+uint64_t sb_context_launch_count(sb_context* ctx) { return ctx->launches; }
+
+int sb_device_alloc(sb_context* ctx, int64_t bytes, void** dptr) {
+  return guarded([&] {
+    cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cuda_check(cudaMalloc(dptr, padded(static_cast<std::size_t>(bytes))), "cudaMalloc");
+  });
+}
+
+int sb_device_free(sb_context* ctx, void* dptr) {
+  return guarded([&] {
+    cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cuda_check(cudaFree(dptr), "cudaFree");
+  });
+}
+
+int sb_host_alloc_pinned(int64_t bytes, void** ptr) {
+  return guarded([&] { cuda_check(cudaMallocHost(ptr, padded(static_cast<std::size_t>(bytes))), "cudaMallocHost"); });
+}
+
+int sb_host_free_pinned(void* ptr) { return guarded([&] { cuda_check(cudaFreeHost(ptr), "cudaFreeHost"); }); }
+
+int sb_execute_device(sb_context* ctx, sb_program* p, const sb_device_buffer* bufs, int n,
+                      const sb_exec_options* opts) {
+  return guarded([&] {
+    check_opts(opts);
+    cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const auto& prog = p->prog;
+    std::vector<int> slot(prog.buffers.size(), -1);
+    std::vector<int> flags(n);
+    for (int i = 0; i < n; i++) {
+      flags[i] = bufs[i].flags;
+      int r = prog.buffer_index(bufs[i].name ? bufs[i].name : "");
+      if (r >= 0) slot[r] = i;
+    }
+    std::vector<void*> ptrs(prog.buffers.size(), nullptr);
+    for (std::size_t r = 0; r < prog.buffers.size(); r++) {
+      if (slot[r] < 0)
+        throw sb::Error("MissingBuffer", "buffer '" + prog.buffers[r].name + "' not present in store");
+      if (bufs[slot[r]].count != prog.buffers[r].elements)
+        throw sb::Error("MissingBuffer", "buffer '" + prog.buffers[r].name + "' has " +
+                                             std::to_string(bufs[slot[r]].count) + " elements, expected " +
+                                             std::to_string(prog.buffers[r].elements));
+      ptrs[r] = bufs[slot[r]].dptr;
+    }
+    Compiled* c = get_plan(p, fresh_flags(prog, slot, flags), !(opts && opts->disable_tensor_cores));
+    for (std::size_t r = 0; r < prog.buffers.size(); r++) {
+      if ((flags[slot[r]] & SB_BUF_PREPARE) && prog.buffers[r].dir != sb::Dir::In) {
+        const auto& b = prog.buffers[r];
+        bool consumed = false;  // a matched kernel overwrites fresh outputs itself
+        for (const auto& s : c->plan.steps)
+          if (s.kind == sb::PStep::Launch && s.launch.kernel == sb::KernelKind::ConvI8TC &&
+              s.launch.conv.fresh_output && c->plan.bufs[s.launch.conv.c_buf].root_index == static_cast<int>(r))
+            consumed = true;
+        if (!consumed) {
+          cuda_check(sb::launch_fill(ptrs[r], c->plan.bufs[r].kind, b.elements, sb::output_identity(prog, b.name),
+                                     ctx->stream),
+                     "prepare_outputs");
+          ctx->launches++;
+        }
+      }
+    }
+    run_plan(ctx, c, ptrs);
+  });
+}
+
+int sb_execute(sb_context* ctx, sb_program* p, sb_host_buffer* bufs, int n, const sb_exec_options* opts) {
+  return guarded([&] {
+    check_opts(opts);
+    cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const auto& prog = p->prog;
+    std::vector<int> slot(prog.buffers.size(), -1);
+    std::vector<int> flags(n);
+    for (int i = 0; i < n; i++) {
+      flags[i] = bufs[i].flags;
+      int r = prog.buffer_index(bufs[i].name ? bufs[i].name : "");
+      if (r >= 0) slot[r] = i;
+    }
+    // Executor::run's buffer-table check (interp.cpp:184-194).
+    for (std::size_t r = 0; r < prog.buffers.size(); r++) {
+      if (slot[r] < 0)
+        throw sb::Error("MissingBuffer", "buffer '" + prog.buffers[r].name + "' not present in store");
+      if (bufs[slot[r]].count != prog.buffers[r].elements)
+        throw sb::Error("MissingBuffer", "buffer '" + prog.buffers[r].name + "' has " +
+                                             std::to_string(bufs[slot[r]].count) + " elements, expected " +
+                                             std::to_string(prog.buffers[r].elements));
+    }
+    Compiled* c = get_plan(p, fresh_flags(prog, slot, flags), !(opts && opts->disable_tensor_cores));
+    const std::size_t nr = prog.buffers.size();
+    if (ctx->roots.size() < nr) ctx->roots.resize(nr, {nullptr, 0});
+    if (ctx->pinned.size() < nr) ctx->pinned.resize(nr, {nullptr, 0});
+    std::vector<void*> ptrs(nr);
+    std::vector<sb_device_buffer> dev(nr);
+    for (std::size_t r = 0; r < nr; r++) {
+      const auto& b = prog.buffers[r];
+      const sb_host_buffer& hb = bufs[slot[r]];
+      int kind = c->plan.bufs[r].kind;
+      std::size_t bytes = padded(b.elements * kind_bytes(kind));
+      if (ctx->roots[r].second < bytes) {
+        cudaFree(ctx->roots[r].first);
+        cuda_check(cudaMalloc(&ctx->roots[r].first, bytes), "cudaMalloc(root)");
+        ctx->roots[r].second = bytes;
+      }
+      ptrs[r] = ctx->roots[r].first;
+      dev[r] = sb_device_buffer{b.name.c_str(), hb.flags, 0, ptrs[r], b.elements};
+      if ((hb.flags & SB_BUF_PREPARE) && b.dir != sb::Dir::In) continue;
+      const void* src = hb.data;
+      if (hb.carrier == SB_CARRIER_I64) {
+        if (ctx->pinned[r].second < bytes) {
+          cudaFreeHost(ctx->pinned[r].first);
+          cuda_check(cudaMallocHost(&ctx->pinned[r].first, bytes), "cudaMallocHost");
+          ctx->pinned[r].second = bytes;
+        }
+        const auto* in = static_cast<const std::int64_t*>(hb.data);
+        void* st = ctx->pinned[r].first;
+        for (std::int64_t e = 0; e < b.elements; e++) {
+          switch (kind) {
+            case sb::kI8: static_cast<std::int8_t*>(st)[e] = static_cast<std::int8_t>(in[e]); break;
+            case sb::kI16: static_cast<std::int16_t*>(st)[e] = static_cast<std::int16_t>(in[e]); break;
+            default: static_cast<std::int32_t*>(st)[e] = static_cast<std::int32_t>(in[e]); break;
+          }
+        }
+        src = st;
+      }
+      cuda_check(cudaMemcpyAsync(ptrs[r], src, b.elements * kind_bytes(kind), cudaMemcpyHostToDevice, ctx->stream),
+                 "H2D");
+    }
+    {
+      // reuse the device path for prepare-fills + plan execution
+      int rc = sb_execute_device(ctx, p, dev.data(), static_cast<int>(nr), opts);
+      if (rc != SB_OK) throw sb::Error(sb_status_name(rc), g_last_error);
+    }
+    for (std::size_t r = 0; r < nr; r++) {
+      const auto& b = prog.buffers[r];
+      if (b.dir == sb::Dir::In) continue;
+      sb_host_buffer& hb = bufs[slot[r]];
+      int kind = c->plan.bufs[r].kind;
+      void* dst = hb.data;
+      if (hb.carrier == SB_CARRIER_I64) {
+        std::size_t bytes = padded(b.elements * kind_bytes(kind));
+        if (ctx->pinned[r].second < bytes) {
+          cudaFreeHost(ctx->pinned[r].first);
+          cuda_check(cudaMallocHost(&ctx->pinned[r].first, bytes), "cudaMallocHost");
+          ctx->pinned[r].second = bytes;
+        }
+        dst = ctx->pinned[r].first;
+      }
+      cuda_check(cudaMemcpyAsync(dst, ptrs[r], b.elements * kind_bytes(kind), cudaMemcpyDeviceToHost, ctx->stream),
+                 "D2H");
+    }
+    ctx->h_err->code = 1;
+    check_device_error(ctx, c);
+    for (std::size_t r = 0; r < nr; r++) {
+      const auto& b = prog.buffers[r];
+      if (b.dir == sb::Dir::In) continue;
+      sb_host_buffer& hb = bufs[slot[r]];
+      if (hb.carrier != SB_CARRIER_I64) continue;
+      int kind = c->plan.bufs[r].kind;
+      auto* out = static_cast<std::int64_t*>(hb.data);
+      const void* st = ctx->pinned[r].first;
+      for (std::int64_t e = 0; e < b.elements; e++) {
+        switch (kind) {
+          case sb::kI8: out[e] = static_cast<const std::int8_t*>(st)[e]; break;
+          case sb::kI16: out[e] = static_cast<const std::int16_t*>(st)[e]; break;
+          default: out[e] = static_cast<const std::int32_t*>(st)[e]; break;
+        }
+      }
+    }
+  });
+}
+
+}  // extern "C"

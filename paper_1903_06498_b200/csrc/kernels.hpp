@@ -1,0 +1,28 @@
+// Host-callable launchers of the sm_100a kernels (kernels/*.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "desc.hpp"
+#include "plan.hpp"
+
+namespace sb {
+
+cudaError_t launch_generic(const GenericDesc* d_desc, std::int64_t pcount, const BufTable& t,
+                           DevError* err, int launch_id, cudaStream_t s);
+cudaError_t launch_fill(void* p, int kind, std::int64_t n, std::int64_t v, cudaStream_t s);
+
+// tcgen05 implicit-GEMM convolution, i8 x i8 -> i32 accumulate (kernels/conv_tc.cu).
+struct ConvArgs {
+  const void* a;  // input activations (i8)
+  const void* b;  // filter (i8)
+  void* c;        // output (i8/i16/i32)
+  std::int64_t a_elems, b_elems, c_elems;
+};
+// Host-side checks that the plan fits the kernel's tiling; empty string = ok.
+const char* conv_tc_unsupported(const ConvPlan& cp);
+cudaError_t launch_conv_tc(const ConvPlan& cp, const ConvArgs& args, cudaStream_t s, int num_sms);
+
+}  // namespace sb

@@ -1,0 +1,132 @@
+// Host-side execution plan: the lowering of a Stripe Program into a serial
+// list of device steps (identity fills and kernel launches).
+//
+// This is the B200 replacement for the reference's Executor::compile
+// (proj/src/interp.cpp:201-347): instead of a slot-form tree walked per point
+// on one CPU thread, each root-to-leaf chain of blocks becomes ONE flat launch
+// whose dims are every ranged index on the chain, whose constraints are all the
+// chain's predicates, and whose accesses are the composed refinement chains
+// (flat base = sum over levels of stride*offset, interp.cpp:227-233, 449-451).
+// Multi-statement blocks become consecutive launches (kernel boundaries are
+// the phase barriers); per-iteration local allocations become per-point
+// slices of a zero-filled scratch buffer (interp.cpp:239-247, 442-447).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "desc.hpp"
+#include "ir.hpp"
+
+namespace sb {
+
+struct FAff {
+  std::int64_t c = 0;
+  std::vector<std::int64_t> k;  // dense over the launch dims
+  std::int64_t at(std::size_t d) const { return d < k.size() ? k[d] : 0; }
+  bool uses(std::size_t d) const { return at(d) != 0; }
+  bool operator==(const FAff& o) const;
+};
+
+struct PDim {
+  std::string name;
+  std::int64_t range = 1;
+  bool pinned = false;  // host-unrolled (serial fallback); value folded into constants
+  std::int64_t value = 0;
+};
+
+struct PBuffer {
+  std::string name;
+  DType dtype = DType::I32;
+  std::int8_t kind = kI32;  // device storage kind (kI64 for temp spills)
+  std::int64_t elements = 0;
+  bool root = false;
+  int root_index = -1;  // index into Program::buffers
+  Dir dir = Dir::In;
+};
+
+struct PAccess {
+  int buf = 0;
+  FAff addr;
+};
+
+struct PSpecial {
+  bool gather = true;
+  int dst = 0, src = 0, idx = 0;  // access indices
+  std::vector<std::int64_t> walk, sdst, ssrc, sidx;
+  std::int64_t bound = 0;
+  Agg dst_agg = Agg::Assign;
+  DType dst_dtype = DType::I32;
+};
+
+// Specialised kernel families the matcher can route a launch to.
+enum class KernelKind { Generic, ConvI8TC, Reduce };
+
+// Parameters of the tcgen05 implicit-GEMM convolution (kernels/conv_tc.cu).
+struct ConvPlan {
+  int a_buf = -1, b_buf = -1, c_buf = -1;
+  DType c_dtype = DType::I32;
+  std::int64_t N = 1, H = 1, W = 1, C = 1, K = 1, R = 1, S = 1;
+  // A (input) element address = a_n*n + a_x*u + a_y*v + c + a0, u = x + i + ox, v = y + j + oy
+  std::int64_t a_n = 0, a_x = 0, a_y = 0, a0 = 0;
+  std::int64_t ox = 0, oy = 0;
+  std::int64_t u_lo = 0, u_hi = 0, v_lo = 0, v_hi = 0;  // valid input window from constraints
+  // B (filter) element address = b_i*i + b_j*j + b_k*k + b_c*c + b0
+  std::int64_t b_i = 0, b_j = 0, b_k = 0, b_c = 0, b0 = 0;
+  // C (output) element address = c_n*n + c_x*x + c_y*y + k + c0
+  std::int64_t c_n = 0, c_x = 0, c_y = 0, c0 = 0;
+  bool fresh_output = false;  // output known identity-filled: overwrite instead of accumulate
+};
+
+struct PLaunch {
+  std::string path;  // dot path of the leaf block ("0.1.0")
+  std::vector<PDim> dims;
+  std::vector<FAff> cons;
+  std::vector<PAccess> acc;
+  std::vector<DInstr> code;
+  std::vector<std::int64_t> consts;
+  std::vector<PSpecial> specials;
+  std::vector<std::pair<Agg, DType>> priv;  // leaf-level private allocs
+  int ntemps = 0;
+  bool has_spill = false;
+
+  // analysis (analyze())
+  std::int8_t mode = kModeOwner;
+  std::vector<int> pdims, rdims;
+  std::vector<std::int8_t> acc_mode, acc_cell;
+  int ncells = 0;
+  std::int64_t pcount = 1, points = 1;
+  std::string why;  // reason for a non-owner mode
+
+  KernelKind kernel = KernelKind::Generic;
+  ConvPlan conv;
+};
+
+struct PStep {
+  enum Kind { Fill, Launch } kind = Launch;
+  int buf = -1;
+  std::int64_t value = 0;
+  PLaunch launch;
+};
+
+struct Plan {
+  std::vector<PBuffer> bufs;  // roots first (Program::buffers order), then scratch
+  std::vector<PStep> steps;
+  std::vector<std::string> notes;
+  std::string describe() const;  // human-readable plan dump (tests / logs)
+};
+
+struct PlanOptions {
+  bool enable_tc = true;           // route matched contractions to tcgen05 kernels
+  std::vector<bool> fresh_outputs; // per root buffer: contents are prepare_outputs' identity
+  std::int64_t max_unroll = 1 << 16;
+};
+
+Plan build_plan(const Program& p, const PlanOptions& opt);
+
+// Fills a device descriptor for a generic launch.
+// bufmap receives the plan buffer id of every launch-local buffer slot.
+void to_desc(const PLaunch& l, GenericDesc* d, std::vector<int>* bufmap);
+
+}  // namespace sb
