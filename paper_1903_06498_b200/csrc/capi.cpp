@@ -8,7 +8,9 @@
 // the reference's ExecError codes.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstring>
+#include <set>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -67,6 +69,7 @@ std::size_t kind_bytes(int kind) {
 std::size_t padded(std::size_t bytes) { return (bytes + 15) / 16 * 16; }
 
 struct Compiled {
+  std::uint64_t id = 0;  // unique: device state is keyed by it, never by address
   sb::Plan plan;
   std::vector<sb::GenericDesc> descs;
   std::vector<std::vector<int>> bufmaps;
@@ -79,6 +82,7 @@ struct sb_program {
   sb::Program prog;
   std::mutex mu;
   std::map<std::string, std::unique_ptr<Compiled>> plans;
+  ~sb_program();
 };
 
 struct sb_context {
@@ -93,16 +97,18 @@ struct sb_context {
     sb::GenericDesc* d_descs = nullptr;
     std::vector<void*> scratch;  // by plan buffer id (scratch only)
   };
-  std::map<const Compiled*, State> states;
+  std::map<std::uint64_t, State> states;  // by Compiled::id
   std::vector<std::pair<void*, std::size_t>> roots;  // host-path device buffers
   std::vector<std::pair<void*, std::size_t>> pinned;  // host-path staging
 
-  ~sb_context() {
+  static void release(State& st) {
+    cudaFree(st.d_descs);
+    for (void* p : st.scratch) cudaFree(p);
+  }
+  ~sb_context();
+  void body_dtor() {
     cudaSetDevice(device);
-    for (auto& [c, st] : states) {
-      cudaFree(st.d_descs);
-      for (void* p : st.scratch) cudaFree(p);
-    }
+    for (auto& [c, st] : states) release(st);
     for (auto& r : roots) cudaFree(r.first);
     for (auto& r : pinned) cudaFreeHost(r.first);
     cudaFree(d_err);
@@ -113,6 +119,37 @@ struct sb_context {
 
 namespace {
 
+std::mutex g_registry_mu;
+std::set<sb_context*> g_contexts;
+std::atomic<std::uint64_t> g_next_plan_id{1};
+
+}  // namespace
+
+sb_context::~sb_context() {
+  {
+    std::lock_guard<std::mutex> lock(g_registry_mu);
+    g_contexts.erase(this);
+  }
+  body_dtor();
+}
+
+sb_program::~sb_program() {
+  // drop the device state every context holds for this program's plans
+  std::lock_guard<std::mutex> lock(g_registry_mu);
+  for (auto& [key, c] : plans) {
+    for (sb_context* ctx : g_contexts) {
+      auto it = ctx->states.find(c->id);
+      if (it == ctx->states.end()) continue;
+      cudaSetDevice(ctx->device);
+      cudaStreamSynchronize(ctx->stream);
+      sb_context::release(it->second);
+      ctx->states.erase(it);
+    }
+  }
+}
+
+namespace {
+
 Compiled* get_plan(sb_program* p, const std::vector<bool>& fresh, bool tc) {
   std::string key(tc ? "T" : "G");
   for (bool f : fresh) key += f ? '1' : '0';
@@ -120,6 +157,7 @@ Compiled* get_plan(sb_program* p, const std::vector<bool>& fresh, bool tc) {
   auto it = p->plans.find(key);
   if (it != p->plans.end()) return it->second.get();
   auto c = std::make_unique<Compiled>();
+  c->id = g_next_plan_id++;
   sb::PlanOptions opt;
   opt.enable_tc = tc;
   opt.fresh_outputs = fresh;
@@ -140,7 +178,7 @@ Compiled* get_plan(sb_program* p, const std::vector<bool>& fresh, bool tc) {
 }
 
 sb_context::State& ensure_state(sb_context* ctx, const Compiled* c) {
-  auto it = ctx->states.find(c);
+  auto it = ctx->states.find(c->id);
   if (it != ctx->states.end()) return it->second;
   sb_context::State st;
   if (!c->descs.empty()) {
@@ -155,7 +193,7 @@ sb_context::State& ensure_state(sb_context* ctx, const Compiled* c) {
     if (pb.root) continue;
     cuda_check(cudaMalloc(&st.scratch[b], padded(pb.elements * kind_bytes(pb.kind))), "cudaMalloc(scratch)");
   }
-  return ctx->states.emplace(c, std::move(st)).first->second;
+  return ctx->states.emplace(c->id, std::move(st)).first->second;
 }
 
 // Runs every plan step on the context stream.  root_ptr/root_elems indexed by root buffer.
@@ -324,6 +362,10 @@ int sb_context_create(int device, sb_context** out) {
     cuda_check(cudaMallocHost(&ctx->h_err, sizeof(sb::DevError)), "cudaMallocHost");
     // h_err->code doubles as a "maybe dirty" hint; the authoritative copy is read on sync.
     ctx->h_err->code = 1;
+    {
+      std::lock_guard<std::mutex> lock(g_registry_mu);
+      g_contexts.insert(ctx.get());
+    }
     *out = ctx.release();
   });
 }
