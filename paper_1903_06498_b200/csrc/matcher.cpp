@@ -1,14 +1,213 @@
-// Kernel matcher: routes launches whose leaf body is a recognised contraction
-// to the specialised sm_100a kernels; everything else stays on the generic
-// block kernel.  (Filled in by the tensor-core path.)
+// Kernel matcher: routes launches whose leaf body is a dense contraction of the
+// convolution family to the tcgen05 implicit-GEMM kernel (kernels/conv_tc.cu).
+// Everything else stays on the generic block kernel.
+//
+// Recognised body (the reference's conv leaf, tests/support.cpp:79-124):
+//   $a = load(A); $b = load(B); $p = mul($a, $b) | mul($b, $a); C = store($p)  with C:add
+// Index roles are read off the composed affine accesses:
+//   k  (N)   : in B and C only                      -> output channel
+//   c  (K)   : in A and B, coefficient 1 in A       -> input channel
+//   i, j     : in A and B, same A coefficient as x/y -> filter taps
+//   n, x, y  : in A and C only                      -> batch and spatial output dims
+// Constraints must be exactly interval bounds on u = x + i and v = y + j: the
+// kernel realises them as TMA out-of-bounds zero fill, which reproduces the
+// skip-predicate semantics (interp.cpp:426-428) for a multiply-accumulate.
+#include <algorithm>
+#include <cstdlib>
+#include <limits>
+
+#include "kernels.hpp"
 #include "plan.hpp"
 
 namespace sb {
+namespace {
+
+bool match_conv(const Plan& plan, const PLaunch& l, const Program& prog, const PlanOptions& opt, std::size_t step,
+                ConvPlan* cp, std::string* why) {
+  if (l.mode != kModeOwner || !l.priv.empty() || l.has_spill || !l.specials.empty() || !l.consts.empty()) return false;
+  if (l.code.size() != 4) return false;
+  const DInstr& la = l.code[0];
+  const DInstr& lb = l.code[1];
+  const DInstr& mu = l.code[2];
+  const DInstr& st = l.code[3];
+  if (la.op != kOpLoad || lb.op != kOpLoad || mu.op != kOpMul || st.op != kOpStore) return false;
+  bool order_ok = (mu.a == la.dst && mu.b == lb.dst) || (mu.a == lb.dst && mu.b == la.dst);
+  if (!order_ok || st.a != mu.dst || la.dst == lb.dst) return false;
+  if (st.agg != static_cast<std::int8_t>(Agg::Add)) return false;
+  const PAccess* A = &l.acc[la.acc];
+  const PAccess* B = &l.acc[lb.acc];
+  const PAccess& C = l.acc[st.acc];
+  if (A->buf == C.buf || B->buf == C.buf) return false;
+  if (plan.bufs[A->buf].dtype != DType::I8 || plan.bufs[B->buf].dtype != DType::I8) return false;
+  if (plan.bufs[A->buf].kind != kI8 || plan.bufs[B->buf].kind != kI8) return false;
+  DType cdt = static_cast<DType>(st.dtype);
+  if (cdt == DType::F32 || plan.bufs[C.buf].dtype != cdt) return false;
+
+  const int nd = static_cast<int>(l.dims.size());
+  auto roles = [&](const PAccess* a, const PAccess* b, int* kdim, int* cdim, std::vector<int>* mdims,
+                   std::vector<int>* taps) {
+    for (int d = 0; d < nd; d++) {
+      bool ia = a->addr.uses(d), ib = b->addr.uses(d), ic = C.addr.uses(d);
+      if (!ia && ib && ic) {
+        if (*kdim >= 0) return false;
+        *kdim = d;
+      } else if (ia && ib && !ic) {
+        taps->push_back(d);
+      } else if (ia && !ib && ic) {
+        mdims->push_back(d);
+      } else {
+        return false;
+      }
+    }
+    return true;
+  };
+  int kdim = -1, cdim = -1;
+  std::vector<int> mdims, taps;
+  if (!roles(A, B, &kdim, &cdim, &mdims, &taps)) {
+    // maybe the loads are in the other order (filter first)
+    std::swap(A, B);
+    kdim = -1;
+    mdims.clear();
+    taps.clear();
+    if (!roles(A, B, &kdim, &cdim, &mdims, &taps)) return false;
+  }
+  if (kdim < 0 || mdims.empty() || mdims.size() > 3) return false;
+  // input channel: the tap-role dim with A coefficient 1
+  for (std::size_t t = 0; t < taps.size(); t++)
+    if (A->addr.at(taps[t]) == 1) {
+      cdim = taps[t];
+      taps.erase(taps.begin() + static_cast<long>(t));
+      break;
+    }
+  if (cdim < 0 || taps.size() > 2) return false;
+  // spatial dims: the M dims ordered by A coefficient (y smallest, then x, then n)
+  std::sort(mdims.begin(), mdims.end(), [&](int a, int b) { return A->addr.at(a) < A->addr.at(b); });
+  int ydim = mdims[0];
+  int xdim = mdims.size() > 1 ? mdims[1] : -1;
+  int ndim = mdims.size() > 2 ? mdims[2] : -1;
+  int idim = -1, jdim = -1;
+  for (int t : taps) {
+    if (A->addr.at(t) == A->addr.at(ydim) && jdim < 0) jdim = t;
+    else if (xdim >= 0 && A->addr.at(t) == A->addr.at(xdim) && idim < 0) idim = t;
+    else return false;
+  }
+  // with a single M dim that has a tap but no batch: fine; taps must pair
+  auto coef = [&](const PAccess* a, int d) -> std::int64_t { return d < 0 ? 0 : a->addr.at(d); };
+  auto range = [&](int d) -> std::int64_t { return d < 0 ? 1 : l.dims[d].range; };
+  for (int d = 0; d < nd; d++)
+    if (A->addr.at(d) < 0 || B->addr.at(d) < 0 || C.addr.at(d) < 0) return false;
+  if (C.addr.at(kdim) != 1) return false;
+
+  ConvPlan c;
+  c.a_buf = A->buf;
+  c.b_buf = B->buf;
+  c.c_buf = C.buf;
+  c.c_dtype = cdt;
+  c.N = range(ndim);
+  c.H = range(xdim);
+  c.W = range(ydim);
+  c.C = range(cdim);
+  c.K = range(kdim);
+  c.R = range(idim);
+  c.S = range(jdim);
+  c.a_n = coef(A, ndim);
+  c.a_x = coef(A, xdim);
+  c.a_y = coef(A, ydim);
+  c.a0 = A->addr.c;
+  if (c.a_n == 0) c.a_n = std::max<std::int64_t>(16, (c.a_x ? c.a_x : c.a_y) * 1024);  // unused (N == 1)
+  if (c.a_x == 0) c.a_x = std::max<std::int64_t>(16, c.a_y * c.W * 4);                // unused (H == 1)
+  c.b_i = coef(B, idim);
+  c.b_j = coef(B, jdim);
+  c.b_k = coef(B, kdim);
+  c.b_c = coef(B, cdim);
+  c.b0 = B->addr.c;
+  c.c_n = coef(&C, ndim);
+  c.c_x = coef(&C, xdim);
+  c.c_y = coef(&C, ydim);
+  c.c0 = C.addr.c;
+  // valid input window: u = x + i in [u_lo, u_hi], v = y + j in [v_lo, v_hi]
+  c.u_lo = 0;
+  c.u_hi = c.H - 1 + c.R - 1;
+  c.v_lo = 0;
+  c.v_hi = c.W - 1 + c.S - 1;
+  for (const auto& con : l.cons) {
+    int used = 0;
+    for (int d = 0; d < nd; d++) used += con.uses(d) ? 1 : 0;
+    std::int64_t ax = con.at(xdim < 0 ? 0 : xdim), ai = idim < 0 ? 0 : con.at(idim);
+    std::int64_t ay = con.at(ydim), aj = jdim < 0 ? 0 : con.at(jdim);
+    bool on_u = xdim >= 0 && ax != 0 && (idim < 0 ? used == 1 : (ai == ax && used == 2));
+    bool on_v = ay != 0 && (jdim < 0 ? used == 1 : (aj == ay && used == 2));
+    if (xdim < 0) ax = 0;
+    if (on_u && (ax == 1 || ax == -1)) {
+      // ax*(x+i) + c >= 0
+      if (ax == 1) c.u_lo = std::max(c.u_lo, -con.c);
+      else c.u_hi = std::min(c.u_hi, con.c);
+    } else if (on_v && (ay == 1 || ay == -1)) {
+      if (ay == 1) c.v_lo = std::max(c.v_lo, -con.c);
+      else c.v_hi = std::min(c.v_hi, con.c);
+    } else {
+      *why = "constraint is not an interval on an input coordinate";
+      return false;
+    }
+  }
+  if (c.u_lo > c.u_hi || c.v_lo > c.v_hi) return false;  // empty: leave to the generic kernel
+  // every address the kernel touches must lie inside its buffer (else the
+  // reference would raise OutOfBoundsAccess; the generic kernel reports it)
+  std::int64_t a_min = c.a0 + c.a_x * c.u_lo + c.a_y * c.v_lo;
+  std::int64_t a_max = c.a0 + c.a_n * (c.N - 1) + c.a_x * c.u_hi + c.a_y * c.v_hi + (c.C - 1);
+  if (a_min < 0 || a_max >= plan.bufs[c.a_buf].elements) return false;
+  std::int64_t b_max = c.b0 + c.b_i * (c.R - 1) + c.b_j * (c.S - 1) + c.b_k * (c.K - 1) + c.b_c * (c.C - 1);
+  if (c.b0 < 0 || b_max >= plan.bufs[c.b_buf].elements) return false;
+  std::int64_t o_max = c.c0 + c.c_n * (c.N - 1) + c.c_x * (c.H - 1) + c.c_y * (c.W - 1) + (c.K - 1);
+  if (c.c0 < 0 || o_max >= plan.bufs[c.c_buf].elements) return false;
+  // exactness of the s32 accumulation
+  if (c.R * c.S * c.C * 128 * 128 >= (std::int64_t{1} << 31)) {
+    *why = "reduction too long for exact s32 accumulation";
+    return false;
+  }
+  // fused prepare_outputs: the first writer of a fresh root output that covers
+  // it exactly once may overwrite instead of accumulate into the identity (0).
+  const PBuffer& cb = plan.bufs[c.c_buf];
+  if (cb.root && cb.root_index < static_cast<int>(opt.fresh_outputs.size()) && opt.fresh_outputs[cb.root_index] &&
+      output_identity(prog, cb.name) == 0) {
+    bool first = true;
+    for (std::size_t s = 0; s < step; s++) {
+      const PStep& ps = plan.steps[s];
+      if (ps.kind != PStep::Launch) continue;
+      for (const auto& ins : ps.launch.code)
+        if ((ins.op == kOpStore && ps.launch.acc[ins.acc].buf == c.c_buf)) first = false;
+      for (const auto& sp : ps.launch.specials)
+        if (ps.launch.acc[sp.dst].buf == c.c_buf) first = false;
+    }
+    bool dense = c.c0 == 0 && c.c_y == c.K && (c.H == 1 || c.c_x == c.W * c.K) &&
+                 (c.N == 1 || c.c_n == c.H * c.W * c.K) && c.N * c.H * c.W * c.K == cb.elements;
+    c.fresh_output = first && dense;
+  }
+  const char* bad = conv_tc_unsupported(c);
+  if (bad) {
+    *why = bad;
+    return false;
+  }
+  *cp = c;
+  return true;
+}
+
+}  // namespace
 
 void match_kernels(Plan* plan, const Program& p, const PlanOptions& opt) {
-  (void)plan;
-  (void)p;
-  (void)opt;
+  if (!opt.enable_tc) return;
+  for (std::size_t s = 0; s < plan->steps.size(); s++) {
+    PStep& st = plan->steps[s];
+    if (st.kind != PStep::Launch) continue;
+    ConvPlan cp;
+    std::string why;
+    if (match_conv(*plan, st.launch, p, opt, s, &cp, &why)) {
+      st.launch.kernel = KernelKind::ConvI8TC;
+      st.launch.conv = cp;
+    } else if (!why.empty()) {
+      plan->notes.push_back("launch " + st.launch.path + ": contraction kept on the generic kernel (" + why + ")");
+    }
+  }
 }
 
 }  // namespace sb
