@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 Stripe block executor (BASELINE.json contract).
+
+Workload (N=1): BASELINE config 2 — a 3x3 conv2d NHWC 56x56x64->64, batch 32,
+with padding constraints, as ONE Stripe block (paper_1903_06498_b200.workloads.conv2d),
+i8 x i8 -> i32 (the reference's integer semantics; bit-exact vs its interpreter).
+A step = prepare_outputs + execute of that program over one batch (the identity
+fill of the output is fused into the conv epilogue).  Multi-GPU: weak scaling,
+each rank runs its own batch-32 shard (the batch index partitions with no
+data-path collective).
+
+value  : useful GFLOP/s (2 x constraint-satisfying MAC points, tile.cpp:338-370),
+         inputs resident in HBM, max-over-ranks device time.
+e2e    : same metric through the public API (sb_execute) from pinned host
+         buffers: H2D of I and F and D2H of O inside the timed region.
+--impl reference: the reference interpreter (oracle/_ref, stripe::execute) on
+         the host cores over a bounded sample of the same workload.
+"""
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Stripe-kernel GFLOP/s & GB/s vs B200 roofline at 1/2/4/8 GPU; x vs CPU ref"
+N_IMG, H, W, C, K = 32, 56, 56, 64, 64
+L2_BYTES = 126 * 1024 * 1024
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def wait_first_sample(self, timeout=3.0):
+        t0 = time.time()
+        while self.proc and time.time() - t0 < timeout:
+            if os.path.getsize(self.path) > 0:
+                return
+            time.sleep(0.02)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 9:
+                    continue
+                try:
+                    sm.append(float(f[1]))
+                    smax.append(float(f[2]))
+                except ValueError:
+                    continue
+                for n, v in zip(names, f[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(n)
+            os.unlink(self.path)
+        except Exception:
+            pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ------------------------------------------------------------------------------------------
+def cpu_reference(samples_rows=8, threads=None, steps=1, warmup=0):
+    """Reference interpreter (unmodified stripe::execute from oracle/_ref) on host cores.
+    One step = `threads` concurrent executions (one per host thread, execute is reentrant,
+    SPEC.md:263) of a row-band sample of config 2: 1 image x `samples_rows` output rows."""
+    import numpy as np
+
+    from oracle import Ref, random_inputs
+    from paper_1903_06498_b200 import workloads as Wk
+    threads = threads or os.cpu_count() or 1
+    text = Wk.conv2d(1, samples_rows, W, C, K)
+    macs = Wk.conv_useful_macs(1, samples_rows, W, C, K)
+    L = Ref.lib()
+    prog = Ref.parse(text)
+    bufs = prog.buffers()
+    inputs = random_inputs(bufs, 1001)
+    times = []
+    for it in range(warmup + steps):
+        progs = (ctypes.c_void_p * threads)(*([prog.h] * threads))
+        stores = []
+        for t in range(threads):
+            s = L.sr_store_new()
+            for n, bits, el, d in bufs:
+                arr = inputs[n] if n in inputs else np.zeros(el, np.int64)
+                L.sr_store_set(s, n.encode(), bits, arr.ctypes.data, arr.size)
+            stores.append(s)
+        st = (ctypes.c_void_p * threads)(*stores)
+        t0 = time.perf_counter()
+        bad = L.sr_execute_many(progs, st, threads, threads)
+        dt = time.perf_counter() - t0
+        for s in stores:
+            L.sr_store_free(s)
+        if bad:
+            raise RuntimeError("reference execute failed")
+        if it >= warmup:
+            times.append(dt)
+    gflops = 2.0 * macs * threads / (sum(times) / len(times)) / 1e9
+    sample = (f"{threads} concurrent stripe::execute runs (one per host thread) of config 2 restricted to "
+              f"1 image x {samples_rows} output rows ({macs} useful MACs each), reference built -O2 from "
+              f"/root/reference/proj/src")
+    return gflops, threads, sample, times
+
+
+def run_reference_arm(args):
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    from oracle import Ref
+    if not Ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libstripe_ref.so not built"}))
+        return
+    gflops, cores, sample, times = cpu_reference(samples_rows=8, steps=args.steps, warmup=args.warmup)
+    print(json.dumps({
+        "metric": METRIC, "value": round(gflops, 4), "unit": "GFLOP/s", "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1000 * sum(times) / len(times), 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "i8xi8->i32 (int64 carriers)",
+        "data": "synthetic (splitmix64 random_inputs, seed 1001)",
+        "config": {"workload": "BASELINE config 2: conv2d 3x3 NHWC 56x56x64->64 batch 32, padding constraints",
+                   "sample": "row band"},
+        "cpu_baseline": {"value": round(gflops, 4), "unit": "GFLOP/s", "cores": cores, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": round(gflops, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+# ------------------------------------------------------------------------------------------
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1903_06498_b200 as sb
+    from paper_1903_06498_b200 import workloads as Wk
+
+    world, rank, local = dist_setup()
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+
+    text = Wk.conv2d(N_IMG, H, W, C, K)
+    prog = sb.parse_program(text)
+    plan = prog.describe_plan(fresh_outputs=True)
+    assert "conv_i8_tc" in plan, plan
+    ctx = sb.Context(local)
+    ctx.set_stream(stream.cuda_stream)
+
+    macs = Wk.conv_useful_macs(N_IMG, H, W, C, K)
+    flops_step = 2.0 * macs
+    in_bytes = N_IMG * H * W * C + 3 * 3 * K * C
+    out_bytes = N_IMG * H * W * K * 4
+    alg_bytes = in_bytes + out_bytes
+
+    # rotate through enough input/output sets that the working set exceeds L2
+    nsets = max(4, int(3 * L2_BYTES // alg_bytes) + 1)
+    g = torch.Generator(device=dev).manual_seed(1001 + rank)
+    sets = []
+    for _ in range(nsets):
+        I = torch.randint(-128, 128, (N_IMG, H, W, C), dtype=torch.int8, device=dev, generator=g)
+        F = torch.randint(-128, 128, (3, 3, K, C), dtype=torch.int8, device=dev, generator=g)
+        O = torch.empty((N_IMG, H, W, K), dtype=torch.int32, device=dev)
+        sets.append({"I": (I.data_ptr(), I.numel(), 0), "F": (F.data_ptr(), F.numel(), 0),
+                     "O": (O.data_ptr(), O.numel(), sb.SB_BUF_PREPARE), "_keep": (I, F, O)})
+
+    bound = [ctx.bind_device(prog, {k: v for k, v in s.items() if not k.startswith("_")}) for s in sets]
+
+    def step(i):
+        bound[i % nsets]()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    with torch.cuda.stream(stream):
+        clk = ClockSampler(local).__enter__()
+        clk.wait_first_sample()
+        for i in range(args.warmup):
+            step(i)
+        # keep the GPU busy ~1 s before the timed region so the sampled clocks reflect load
+        settle = 0
+        t_settle = time.perf_counter()
+        while time.perf_counter() - t_settle < 1.0:
+            for _ in range(20):
+                step(args.warmup + settle)
+                settle += 1
+            torch.cuda.synchronize(dev)
+        ctx.sync()
+        barrier()
+        torch.cuda.synchronize(dev)
+        launches0 = ctx.launch_count
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        if True:
+            t_start = torch.cuda.Event(enable_timing=True)
+            t_end = torch.cuda.Event(enable_timing=True)
+            t_start.record(stream)
+            for i in range(args.steps):
+                ev[i][0].record(stream)
+                step(args.warmup + i)
+                ev[i][1].record(stream)
+            t_end.record(stream)
+            torch.cuda.synchronize(dev)
+        clk.__exit__(None, None, None)
+        ctx.sync()
+        barrier()
+        launches = ctx.launch_count - launches0
+        elapsed_ms = t_start.elapsed_time(t_end)
+        kernel_ms = [a.elapsed_time(b) for a, b in ev]
+
+    t = torch.tensor([elapsed_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(t.item())
+    ms_per_step = elapsed_ms / args.steps
+    value = flops_step * world * args.steps / (elapsed_ms / 1e3) / 1e9
+
+    # ---- end-to-end through the public API (host buffers, H2D + D2H inside the region) ----
+    ctx.set_stream(None)
+    e2e = None
+    e2e_steps = max(3, min(args.steps, 20))
+    hI = np.empty(N_IMG * H * W * C, np.int8)
+    hF = np.empty(3 * 3 * K * C, np.int8)
+    hO = np.empty(N_IMG * H * W * K, np.int32)
+    pins = []
+    for a in (hI, hF, hO):
+        p = ctypes.c_void_p()  # pinned host memory from the library's own allocator
+        sb._check(sb.lib().sb_host_alloc_pinned(a.nbytes, ctypes.byref(p)))
+        pins.append(p)
+    hI = np.ctypeslib.as_array((ctypes.c_int8 * hI.size).from_address(pins[0].value))
+    hF = np.ctypeslib.as_array((ctypes.c_int8 * hF.size).from_address(pins[1].value))
+    hO = np.ctypeslib.as_array((ctypes.c_int32 * hO.size).from_address(pins[2].value))
+    rng = np.random.default_rng(7 + rank)
+    hI[:] = rng.integers(-128, 128, hI.size, dtype=np.int8)
+    hF[:] = rng.integers(-128, 128, hF.size, dtype=np.int8)
+    for _ in range(2):
+        ctx.execute_native(prog, {"I": hI, "F": hF, "O": hO}, prepare=("O",))
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        ctx.execute_native(prog, {"I": hI, "F": hF, "O": hO}, prepare=("O",))
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e = {"value": round(flops_step * world * e2e_steps / float(te.item()) / 1e9, 3), "unit": "GFLOP/s",
+           "h2d_bytes_per_step": int(hI.nbytes + hF.nbytes), "d2h_bytes_per_step": int(hO.nbytes),
+           "steps": e2e_steps, "timer": "host wall clock around synchronous sb_execute calls"}
+    for p in pins:
+        sb.lib().sb_host_free_pinned(p)
+
+    hbm_peak, bf16_peak, peak_kind = peaks()
+    avg_kernel_ms = statistics.mean(kernel_ms)
+    achieved_gbs = alg_bytes / (avg_kernel_ms / 1e3) / 1e9
+    tensor_tops = flops_step / (avg_kernel_ms / 1e3) / 1e12
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "conv_tc_traffic.json")) as f:
+            traffic = json.load(f).get("bytes_per_launch")
+    except Exception:
+        pass
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
+        try:
+            from oracle import Ref
+            if Ref.available():
+                gf, cores, sample, _ = cpu_reference(samples_rows=8, steps=1, warmup=0)
+                cpu = {"value": round(gf, 4), "unit": "GFLOP/s", "cores": cores, "kind": "reference",
+                       "sample": sample}
+        except Exception as e:  # reported, never silently substituted
+            cpu = {"value": None, "unit": "GFLOP/s", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "i8xi8->i32",
+            "data": "synthetic (uniform random int8 inputs in HBM)",
+            "config": {"workload": "BASELINE config 2: conv2d 3x3 NHWC 56x56x64->64, batch 32 per GPU, "
+                                   "padding constraints, one Stripe block",
+                       "global_batch": N_IMG * world, "parallelism": f"batch-sharded x{world} (no collective)",
+                       "l2": f"{nsets} rotating input/output sets ({nsets * alg_bytes / 2**20:.0f} MiB > L2)"},
+            "roofline": {"bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                         "frac": round(achieved_gbs / hbm_peak, 4), "traffic": traffic,
+                         "peak_kind": peak_kind, "algorithmic_bytes_per_launch": alg_bytes,
+                         "kernel_ms": round(avg_kernel_ms, 5),
+                         "tensor": {"achieved_tops": round(tensor_tops, 2),
+                                    "int8_peak_tops_derived": round(2 * bf16_peak, 1),
+                                    "frac": round(tensor_tops / (2 * bf16_peak), 4)}},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clock_settle_steps": settle,
+            "clocks": clocks,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -286,10 +286,23 @@ class Context:
 
     def execute_device(self, program: Program, buffers: Dict[str, tuple], opts: Optional[ExecOptions] = None) -> None:
         """buffers: name -> (device_ptr, count, flags).  Asynchronous on the context stream."""
+        self.bind_device(program, buffers, opts)()
+
+    def bind_device(self, program: Program, buffers: Dict[str, tuple], opts: Optional[ExecOptions] = None):
+        """Pre-marshals an HBM-resident execute; the returned callable enqueues it."""
         opts = opts or ExecOptions()
-        db = [DeviceBuffer(n.encode(), int(f), 0, int(p), int(c)) for n, (p, c, f) in buffers.items()]
+        names = [n.encode() for n in buffers]
+        db = [DeviceBuffer(nm, int(f), 0, int(p), int(c)) for nm, (p, c, f) in zip(names, buffers.values())]
         arr = (DeviceBuffer * len(db))(*db)
-        _check(lib().sb_execute_device(self._h, program.handle, arr, len(db), ctypes.byref(opts._c())))
+        copts = opts._c()
+        fn, h, ph, n, po = lib().sb_execute_device, self._h, program.handle, len(db), ctypes.byref(copts)
+
+        def run():
+            rc = fn(h, ph, arr, n, po)
+            if rc:
+                _check(rc)
+        run._keep = (names, arr, copts, program)
+        return run
 
 
 _default_ctx: Dict[int, Context] = {}

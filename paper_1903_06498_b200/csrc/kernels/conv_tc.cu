@@ -49,6 +49,10 @@ struct ConvKParams {
   int out_kind;             // kI8/kI16/kI32
   int fresh;                // overwrite (prepare_outputs identity is fused) vs accumulate
   int vec_out;              // i32 output, 16-byte aligned rows -> int4 stores
+  int filt_vec;             // filter channels contiguous and 16-byte aligned -> uint4 loads
+  int tma_out;              // fresh i32 output written through swizzled staging + TMA stores
+  int nstg;                 // staging buffers (1 or 2)
+  std::uint32_t staging_bytes;
   std::uint32_t strip_bytes, plane_bytes, filt_bytes;
   std::uint32_t tmem_cols;
   std::uint32_t idesc;
@@ -133,11 +137,12 @@ __device__ __forceinline__ void tmem_ld32(std::uint32_t taddr, std::uint32_t (&v
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-    conv_i8_tc_kernel(const __grid_constant__ CUtensorMap amap, const std::int8_t* __restrict__ filt,
-                      void* __restrict__ out, const ConvKParams p) {
+    conv_i8_tc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap omap,
+                      const std::int8_t* __restrict__ filt, void* __restrict__ out, const ConvKParams p) {
   extern __shared__ __align__(1024) std::uint8_t smem_raw[];
-  // carve: [stages strips][filter][barriers]
-  std::uint8_t* strips = smem_raw;
+  // carve: [output staging (1024-aligned, 128B swizzle)][stages strips][filter][barriers]
+  std::uint8_t* staging = reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t{1023});
+  std::uint8_t* strips = staging + p.staging_bytes;
   std::uint8_t* fsm = strips + kStages * p.strip_bytes + 1024;  // +slack: junk rows read past a strip
   std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(fsm + ((p.filt_bytes + 127) / 128) * 128);
   std::uint64_t* full = bars;
@@ -151,7 +156,23 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // Filter -> shared memory in the UMMA K-major layout:
   // byte (tap, plane, k, c%16) at ((tap * C/16 + plane) * K + k) * 16 + c%16.
-  {
+  if (p.filt_vec) {
+    // 16-byte rows of contiguous input channels: one cp.async per (tap, plane, k); k fastest so
+    // consecutive threads fill consecutive 16-byte smem slots (conflict-free).
+    const std::uint32_t planes = static_cast<std::uint32_t>(p.C / 16), K = static_cast<std::uint32_t>(p.K);
+    const std::uint32_t S = static_cast<std::uint32_t>(p.S);
+    const std::uint32_t total = static_cast<std::uint32_t>(p.R * p.S) * K * planes;
+    for (std::uint32_t e = threadIdx.x; e < total; e += kThreads) {
+      std::uint32_t k = e % K;
+      std::uint32_t rest = e / K;
+      std::uint32_t pl = rest % planes;
+      std::uint32_t tap = rest / planes;
+      std::uint32_t i = tap / S, j = tap % S;
+      const std::int8_t* src = filt + (p.b_i * i + p.b_j * j + p.b_k * k + 16 * pl + p.b0);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(fsm + e * 16)), "l"(src) : "memory");
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  } else {
     const int planes = static_cast<int>(p.C / 16);
     const std::int64_t total = p.R * p.S * p.K * p.C;
     for (std::int64_t e = threadIdx.x; e < total; e += kThreads) {
@@ -262,6 +283,54 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int xl = row / p.P;
     const int y = row % p.P;
     int iter = 0;
+    if (p.tma_out) {
+      // Fresh i32 output: TMEM -> registers -> 128B-swizzled smem staging (conflict-free,
+      // row = TMEM lane) -> TMA tensor stores of full lines; rows outside the image are
+      // clipped by the tensor map bounds.
+      const bool leader = threadIdx.x == 64;
+      const int halves = static_cast<int>(p.K / 32);
+      for (int t = blockIdx.x; t < p.tiles; t += gridDim.x, iter++) {
+        int acc = iter & 1;
+        std::uint32_t aphase = (iter >> 1) & 1;
+        int sb = p.nstg == 2 ? (iter & 1) : 0;
+        if (leader) {
+          if (p.nstg == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // staging buffer sb is free again
+        mbar_wait(&tfull[acc], aphase);
+        tc_fence_after();
+        std::uint8_t* stg = staging + static_cast<std::uint32_t>(sb * halves) * 16384u;
+        for (int h = 0; h < halves; h++) {
+          std::uint32_t v[32];
+          tmem_ld32(tmem_base + (static_cast<std::uint32_t>(quarter * 32) << 16) +
+                        static_cast<std::uint32_t>(acc * p.K + h * 32),
+                    v);
+          std::uint32_t rbase = smem_u32(stg + h * 16384 + row * 128);
+#pragma unroll
+          for (int q = 0; q < 8; q++)
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rbase + ((q ^ (row & 7)) << 4)),
+                         "r"(v[4 * q]), "r"(v[4 * q + 1]), "r"(v[4 * q + 2]), "r"(v[4 * q + 3])
+                         : "memory");
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);  // accumulator drained: MMA may reuse it
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (leader) {
+          int n = t / p.tiles_x;
+          int x0 = (t % p.tiles_x) * p.TX;
+          for (int h = 0; h < halves; h++)
+            asm volatile(
+                "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                    reinterpret_cast<std::uint64_t>(&omap)),
+                "r"(smem_u32(stg + h * 16384)), "r"(h * 32), "r"(0), "r"(x0), "r"(n)
+                : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      }
+      if (leader) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    } else
     for (int t = blockIdx.x; t < p.tiles; t += gridDim.x, iter++) {
       int acc = iter & 1;
       std::uint32_t aphase = (iter >> 1) & 1;
@@ -345,7 +414,8 @@ int pitch_for(std::int64_t W, std::int64_t S) {
 }
 
 std::size_t smem_bytes(const ConvKParams& kp) {
-  return 1024 /*align*/ + kStages * kp.strip_bytes + 1024 + ((kp.filt_bytes + 127) / 128) * 128 + 256;
+  return 1024 /*align*/ + kp.staging_bytes + kStages * kp.strip_bytes + 1024 + ((kp.filt_bytes + 127) / 128) * 128 +
+         256;
 }
 
 bool fill_params(const ConvPlan& cp, ConvKParams* kp) {
@@ -379,9 +449,22 @@ bool fill_params(const ConvPlan& cp, ConvKParams* kp) {
   kp->out_kind = cp.c_dtype == DType::I8 ? kI8 : cp.c_dtype == DType::I16 ? kI16 : kI32;
   kp->fresh = cp.fresh_output ? 1 : 0;
   kp->vec_out = kp->out_kind == kI32 && cp.c_n % 4 == 0 && cp.c_x % 4 == 0 && cp.c_y % 4 == 0 && cp.c0 % 4 == 0;
+  kp->filt_vec = cp.b_c == 1 && cp.b_i % 16 == 0 && cp.b_j % 16 == 0 && cp.b_k % 16 == 0 && cp.b0 % 16 == 0;
   kp->plane_bytes = static_cast<std::uint32_t>((kp->TX + cp.R - 1) * kp->P * 16);
   kp->strip_bytes = kp->plane_bytes * (kp->CH / 16);
   kp->filt_bytes = static_cast<std::uint32_t>(cp.R * cp.S * cp.K * cp.C);
+  kp->tma_out = kp->fresh && kp->out_kind == kI32 && cp.c_y % 4 == 0 && cp.c_x % 4 == 0 && cp.c_n % 4 == 0 &&
+                cp.c0 % 4 == 0 && cp.K % 32 == 0;
+  kp->nstg = 2;
+  kp->staging_bytes = kp->tma_out ? static_cast<std::uint32_t>(kp->nstg * (cp.K / 32) * 16384) : 0;
+  if (kp->tma_out && smem_bytes(*kp) > 220 * 1024) {
+    kp->nstg = 1;
+    kp->staging_bytes = static_cast<std::uint32_t>((cp.K / 32) * 16384);
+  }
+  if (kp->tma_out && smem_bytes(*kp) > 220 * 1024) {
+    kp->tma_out = 0;
+    kp->staging_bytes = 0;
+  }
   std::uint32_t cols = 32;
   while (cols < 2 * cp.K) cols *= 2;
   kp->tmem_cols = cols;
@@ -422,6 +505,20 @@ cudaError_t launch_conv_tc(const ConvPlan& cp, const ConvArgs& args, cudaStream_
                       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                       CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  CUtensorMap omap;
+  std::memset(&omap, 0, sizeof(omap));
+  if (kp.tma_out) {
+    std::int32_t* obase = static_cast<std::int32_t*>(args.c) + cp.c0;
+    if (reinterpret_cast<std::uintptr_t>(obase) % 16 != 0) return cudaErrorMisalignedAddress;
+    cuuint64_t odims[4] = {static_cast<cuuint64_t>(cp.K), static_cast<cuuint64_t>(cp.W),
+                           static_cast<cuuint64_t>(cp.H), static_cast<cuuint64_t>(cp.N)};
+    cuuint64_t ostr[3] = {static_cast<cuuint64_t>(cp.c_y * 4), static_cast<cuuint64_t>((cp.c_x ? cp.c_x : cp.c_y * cp.W) * 4),
+                          static_cast<cuuint64_t>((cp.c_n ? cp.c_n : cp.c_y * cp.W * cp.H) * 4)};
+    cuuint32_t obox[4] = {32u, static_cast<cuuint32_t>(kp.P), static_cast<cuuint32_t>(kp.TX), 1u};
+    r = encode(&omap, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, obase, odims, ostr, obox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  }
   std::size_t smem = smem_bytes(kp);
   static bool attr = false;
   if (!attr) {
@@ -430,7 +527,7 @@ cudaError_t launch_conv_tc(const ConvPlan& cp, const ConvArgs& args, cudaStream_
     attr = true;
   }
   int grid = kp.tiles < num_sms ? kp.tiles : num_sms;
-  conv_i8_tc_kernel<<<grid, kThreads, smem, s>>>(map, static_cast<const std::int8_t*>(args.b), args.c, kp);
+  conv_i8_tc_kernel<<<grid, kThreads, smem, s>>>(map, omap, static_cast<const std::int8_t*>(args.b), args.c, kp);
   return cudaGetLastError();
 }
 
