@@ -131,6 +131,15 @@ int sb_execute(sb_context* ctx, sb_program* p, sb_host_buffer* bufs, int n,
 int sb_execute_device(sb_context* ctx, sb_program* p, const sb_device_buffer* bufs, int n,
                       const sb_exec_options* opts);
 
+/* ---- CUDA graphs (launch overhead off the critical path) ---- */
+typedef struct sb_graph sb_graph;
+/* Starts capturing everything this thread enqueues on the context stream
+ * (sb_execute_device calls; plans must have run once outside capture). */
+int sb_graph_begin(sb_context* ctx);
+int sb_graph_end(sb_context* ctx, sb_graph** out);
+int sb_graph_launch(sb_context* ctx, sb_graph* g);
+void sb_graph_free(sb_graph* g);
+
 #ifdef __cplusplus
 }
 #endif

@@ -45,6 +45,7 @@ EXPORTED = [
     "sb_context_create", "sb_context_destroy", "sb_context_set_stream", "sb_context_stream",
     "sb_context_sync", "sb_context_launch_count", "sb_device_alloc", "sb_device_free",
     "sb_host_alloc_pinned", "sb_host_free_pinned", "sb_execute", "sb_execute_device",
+    "sb_graph_begin", "sb_graph_end", "sb_graph_launch", "sb_graph_free",
 ]
 
 
@@ -101,6 +102,11 @@ def lib() -> ctypes.CDLL:
         L.sb_host_free_pinned.argtypes = [vp]
         L.sb_execute.argtypes = [vp, vp, ctypes.POINTER(HostBuffer), i32, ctypes.POINTER(_Opts)]
         L.sb_execute_device.argtypes = [vp, vp, ctypes.POINTER(DeviceBuffer), i32, ctypes.POINTER(_Opts)]
+        L.sb_graph_begin.argtypes = [vp]
+        L.sb_graph_end.argtypes = [vp, ctypes.POINTER(vp)]
+        L.sb_graph_launch.argtypes = [vp, vp]
+        L.sb_graph_free.argtypes = [vp]
+        L.sb_graph_free.restype = None
         _lib = L
     return _lib
 
@@ -303,6 +309,29 @@ class Context:
                 _check(rc)
         run._keep = (names, arr, copts, program)
         return run
+
+
+class Graph:
+    """A captured sequence of HBM-resident executes (sb_graph_*), replayed with one launch."""
+
+    def __init__(self, ctx: "Context", fn):
+        self.ctx = ctx
+        _check(lib().sb_graph_begin(ctx.handle))
+        try:
+            fn()
+        finally:
+            h = ctypes.c_void_p()
+            rc = lib().sb_graph_end(ctx.handle, ctypes.byref(h))
+        _check(rc)
+        self._h = h
+
+    def launch(self) -> None:
+        _check(lib().sb_graph_launch(self.ctx.handle, self._h))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.sb_graph_free(self._h)
+            self._h = None
 
 
 _default_ctx: Dict[int, Context] = {}

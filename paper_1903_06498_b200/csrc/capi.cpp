@@ -558,3 +558,50 @@ int sb_execute(sb_context* ctx, sb_program* p, sb_host_buffer* bufs, int n, cons
 }
 
 }  // extern "C"
+
+// ---- CUDA graphs -----------------------------------------------------------------
+struct sb_graph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  std::uint64_t kernels = 0;  // library kernels per launch of this graph
+  ~sb_graph() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+  }
+};
+
+namespace {
+thread_local std::uint64_t g_capture_mark = 0;
+}
+
+extern "C" {
+
+int sb_graph_begin(sb_context* ctx) {
+  return guarded([&] {
+    cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    g_capture_mark = ctx->launches;
+    cuda_check(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+  });
+}
+
+int sb_graph_end(sb_context* ctx, sb_graph** out) {
+  return guarded([&] {
+    auto g = std::make_unique<sb_graph>();
+    cuda_check(cudaStreamEndCapture(ctx->stream, &g->graph), "cudaStreamEndCapture");
+    cuda_check(cudaGraphInstantiate(&g->exec, g->graph, 0), "cudaGraphInstantiate");
+    g->kernels = ctx->launches - g_capture_mark;
+    ctx->launches = g_capture_mark;  // captured, not launched
+    *out = g.release();
+  });
+}
+
+int sb_graph_launch(sb_context* ctx, sb_graph* g) {
+  return guarded([&] {
+    cuda_check(cudaGraphLaunch(g->exec, ctx->stream), "cudaGraphLaunch");
+    ctx->launches += g->kernels;
+  });
+}
+
+void sb_graph_free(sb_graph* g) { delete g; }
+
+}  // extern "C"

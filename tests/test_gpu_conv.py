@@ -46,12 +46,13 @@ SHAPES = [
     # N, H, W, C, K, out dtype
     (2, 16, 16, 64, 64, "i32"),
     (1, 7, 7, 64, 128, "i32"),
-    (3, 14, 14, 32, 32, "i32"),
+    (3, 14, 14, 64, 32, "i32"),
     (2, 13, 20, 64, 96, "i32"),
     (1, 9, 30, 128, 64, "i32"),
     (2, 8, 8, 64, 64, "i8"),
     (2, 8, 8, 64, 32, "i16"),
-    (1, 3, 60, 32, 256, "i32"),
+    (1, 3, 60, 64, 256, "i32"),
+    (2, 5, 7, 192, 64, "i32"),
 ]
 
 
