@@ -61,6 +61,9 @@ struct ConvKParams {
   std::uint32_t tmem_cols;
   std::uint32_t idesc;
   int base_offset_mode;   // experimental: encode (addr >> 7) & 7 into the descriptor base offset
+  int st_out;             // tma_out staging drained with coalesced LSU stores instead of TMA stores
+  int cluster;            // CTAs per thread-block cluster (filter multicast)
+  int debug_nofilt;       // timing experiments only
   unsigned long long* trace;
 };
 
@@ -194,6 +197,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (p.cluster > 1) {
+    // every CTA's barriers must exist before a cluster peer multicasts into them
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
   const std::uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) trace_at(p.trace, 49);
 
@@ -201,14 +209,42 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       // ---------------- TMA producer ----------------
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&amap)) : "memory");
-      // filter: one box (64 channels x K rows) per (tap, chunk), resident for the whole kernel
-      mbar_expect_tx(fready, p.filt_bytes);
-      const std::uint32_t fbase = smem_u32(fsm);
-      for (int i = 0; i < p.R; i++)
-        for (int j = 0; j < p.S; j++)
-          for (int cc = 0; cc < p.chunks; cc++)
-            tma_load_4d(fbase + ((i * p.S + j) * p.chunks + cc) * p.filt_tap_bytes, &fmap, fready, cc * 64, 0, j,
-                        i);
+      // filter: one box (64 channels x K rows) per (tap, chunk), resident for the whole kernel;
+      // issued right after the first strip so the first tile's A data is already in flight.
+      // With a thread-block cluster, each CTA fetches 1/csize of the boxes and multicasts
+      // them to every CTA of the cluster (all CTAs read the same filter: this divides the
+      // L2 requests on those hot lines by csize).
+      auto load_filter = [&] {
+        if (p.debug_nofilt) {  // timing experiment only: results are wrong
+          mbar_arrive(fready);
+          return;
+        }
+        mbar_expect_tx(fready, p.filt_bytes);
+        const std::uint32_t fbase = smem_u32(fsm);
+        std::uint32_t crank = 0, csize = 1;
+        if (p.cluster > 1) {
+          asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+          csize = static_cast<std::uint32_t>(p.cluster);
+        }
+        const std::uint16_t mask = static_cast<std::uint16_t>((1u << csize) - 1);
+        int idx = 0;
+        for (int i = 0; i < p.R; i++)
+          for (int j = 0; j < p.S; j++)
+            for (int cc = 0; cc < p.chunks; cc++, idx++) {
+              std::uint32_t dst = fbase + ((i * p.S + j) * p.chunks + cc) * p.filt_tap_bytes;
+              if (csize == 1) {
+                tma_load_4d(dst, &fmap, fready, cc * 64, 0, j, i);
+              } else if (static_cast<std::uint32_t>(idx) % csize == crank) {
+                asm volatile(
+                    "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+                    " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(dst),
+                    "l"(reinterpret_cast<std::uint64_t>(&fmap)), "r"(smem_u32(fready)), "r"(cc * 64), "r"(0), "r"(j),
+                    "r"(i), "h"(mask)
+                    : "memory");
+              }
+            }
+      };
+      bool filter_issued = false;
       int stage = 0;
       std::uint32_t phase = 0;
       for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
@@ -219,12 +255,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           trace_at(p.trace, (t - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x));
           mbar_expect_tx(&full[stage], p.strip_bytes);
           tma_load_4d(smem_u32(strips + stage * p.strip_bytes), &amap, &full[stage], cc * 64, p.v_off, x0 + p.u_off, n);
+          if (!filter_issued) {
+            load_filter();
+            filter_issued = true;
+          }
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
       }
+      if (!filter_issued) load_filter();
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -321,6 +362,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc_fence_before();
         mbar_arrive(&tempty[acc]);  // accumulator drained: MMA may reuse it
+        if (p.st_out) {
+          // coalesced LSU stores from the staging tile: 16 lanes cover one pixel's 256 B
+          // (two 128 B halves), a warp instruction writes two consecutive pixels = 512 B.
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          const int et = threadIdx.x - 64;
+          const int n = t / p.tiles_x;
+          const int x0 = (t % p.tiles_x) * p.TX;
+          const int sub = et & 15;         // 16-byte chunk within a pair of 128 B halves
+          const int q = sub & 7;
+          for (int hb = 0; hb < halves; hb += 2) {
+            const int h = hb + (sub >> 3);
+            if (h >= halves) continue;
+            for (int r = et >> 4; r < kTileM; r += 8) {
+              const int rx = r / p.P, ry = r % p.P;
+              if (ry >= p.W || x0 + rx >= p.H || rx >= p.TX) continue;
+              uint4 v;
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                           : "r"(smem_u32(stg + h * 16384 + r * 128 + ((q ^ (r & 7)) << 4))));
+              std::int32_t* o = static_cast<std::int32_t*>(out) + p.c_n * n + p.c_x * (x0 + rx) + p.c_y * ry + p.c0 +
+                                h * 32 + q * 4;
+              *reinterpret_cast<uint4*>(o) = v;
+            }
+          }
+          continue;
+        }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (leader) {
@@ -505,6 +572,12 @@ cudaError_t prepare_conv(const ConvPlan& cp, const ConvArgs& args, Prepared* out
   ConvKParams& kp = out->kp;
   if (!fill_params(cp, &kp) || conv_tc_unsupported(cp)) return cudaErrorNotSupported;
   if (const char* e = std::getenv("SB_CONV_BASEOFF")) kp.base_offset_mode = e[0] == '1';
+  if (const char* e = std::getenv("SB_CONV_ST_OUT")) kp.st_out = e[0] == '1';
+  kp.debug_nofilt = std::getenv("SB_CONV_DEBUG_NOFILT") != nullptr;
+  if (std::getenv("SB_CONV_NO_TMA_OUT")) {
+    kp.tma_out = 0;
+    kp.staging_bytes = 0;
+  }
   auto encode = get_encode();
   if (!encode) return cudaErrorNotSupported;
   cuuint32_t estr[4] = {1, 1, 1, 1};
@@ -583,8 +656,28 @@ cudaError_t launch_conv_tc(const ConvPlan& cp, const ConvArgs& args, cudaStream_
     kp.trace = g_trace;
   }
   int grid = kp.tiles < num_sms ? kp.tiles : num_sms;
-  conv_i8_tc_kernel<<<grid, kThreads, smem_bytes(kp), s>>>(pr->amap, pr->fmap, pr->omap, args.c, kp);
-  return cudaGetLastError();
+  static const int want_cluster = [] {
+    const char* e = std::getenv("SB_CONV_CLUSTER");
+    return e ? std::atoi(e) : 1;  // measured: clusters of 2/4 are slower (co-scheduling limits)
+  }();
+  kp.cluster = 1;
+  if (want_cluster > 1 && grid >= want_cluster) {
+    kp.cluster = want_cluster;
+    grid = grid / want_cluster * want_cluster;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem_bytes(kp);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(kp.cluster);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, conv_i8_tc_kernel, pr->amap, pr->fmap, pr->omap, args.c, kp);
 }
 
 }  // namespace sb
