@@ -218,6 +218,7 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
       a.a_elems = plan.bufs[l.conv.a_buf].elements;
       a.b_elems = plan.bufs[l.conv.b_buf].elements;
       a.c_elems = plan.bufs[l.conv.c_buf].elements;
+      a.b_immutable = l.conv.b_immutable;
       cuda_check(sb::launch_conv_tc(l.conv, a, ctx->stream, ctx->num_sms), "conv_tc");
       ctx->launches++;
       continue;

@@ -20,6 +20,7 @@ struct ConvArgs {
   const void* b;  // filter (i8)
   void* c;        // output (i8/i16/i32)
   std::int64_t a_elems, b_elems, c_elems;
+  bool b_immutable = false;  // filter is a root `in` buffer no plan step writes
 };
 // Host-side checks that the plan fits the kernel's tiling; empty string = ok.
 const char* conv_tc_unsupported(const ConvPlan& cp);

@@ -64,6 +64,8 @@ struct ConvKParams {
   int st_out;             // tma_out staging drained with coalesced LSU stores instead of TMA stores
   int cluster;            // CTAs per thread-block cluster (filter multicast)
   int debug_nofilt;       // timing experiments only
+  int pdl;                // launched with programmatic stream serialization
+  int filter_early;       // filter is immutable input: fetch before griddepcontrol.wait
   unsigned long long* trace;
 };
 
@@ -204,6 +206,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   const std::uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) trace_at(p.trace, 49);
+  // the next kernel in the stream may start its prologue as soon as SMs free up
+  if (p.pdl && threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0) {
     if (lane == 0) {
@@ -245,6 +249,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
       };
       bool filter_issued = false;
+      if (p.pdl) {
+        // Programmatic dependent launch: this prologue overlapped the previous kernel's tail.
+        // An immutable filter (a root `in` buffer nothing in the plan writes) may be fetched
+        // before the dependency resolves; the activations only after it.
+        if (p.filter_early) {
+          load_filter();
+          filter_issued = true;
+        }
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+      }
       int stage = 0;
       std::uint32_t phase = 0;
       for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
@@ -670,13 +684,21 @@ cudaError_t launch_conv_tc(const ConvPlan& cp, const ConvArgs& args, cudaStream_
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem_bytes(kp);
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  static const bool pdl = [] {
+    const char* e = std::getenv("SB_CONV_PDL");
+    return e ? e[0] == '1' : true;
+  }();
+  kp.pdl = pdl ? 1 : 0;
+  kp.filter_early = args.b_immutable ? 1 : 0;
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = static_cast<unsigned>(kp.cluster);
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, conv_i8_tc_kernel, pr->amap, pr->fmap, pr->omap, args.c, kp);
 }
 

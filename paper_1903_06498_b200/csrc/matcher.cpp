@@ -183,6 +183,19 @@ bool match_conv(const Plan& plan, const PLaunch& l, const Program& prog, const P
                  (c.N == 1 || c.c_n == c.H * c.W * c.K) && c.N * c.H * c.W * c.K == cb.elements;
     c.fresh_output = first && dense;
   }
+  {
+    const PBuffer& bb = plan.bufs[c.b_buf];
+    bool written = false;
+    for (const auto& ps : plan.steps) {
+      if (ps.kind == PStep::Fill) written |= ps.buf == c.b_buf;
+      if (ps.kind != PStep::Launch) continue;
+      for (const auto& ins : ps.launch.code)
+        if (ins.op == kOpStore && ps.launch.acc[ins.acc].buf == c.b_buf) written = true;
+      for (const auto& sp : ps.launch.specials)
+        if (ps.launch.acc[sp.dst].buf == c.b_buf) written = true;
+    }
+    c.b_immutable = bb.root && bb.dir == Dir::In && !written;
+  }
   const char* bad = conv_tc_unsupported(c);
   if (bad) {
     *why = bad;

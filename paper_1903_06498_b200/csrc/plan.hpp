@@ -77,6 +77,7 @@ struct ConvPlan {
   // C (output) element address = c_n*n + c_x*x + c_y*y + k + c0
   std::int64_t c_n = 0, c_x = 0, c_y = 0, c0 = 0;
   bool fresh_output = false;  // output known identity-filled: overwrite instead of accumulate
+  bool b_immutable = false;   // filter is a root `in` buffer that no plan step writes
 };
 
 struct PLaunch {

@@ -102,8 +102,9 @@ def test_live_tilings():
     rng = np.random.default_rng(3131)
     for kind, args, bits in [("matmul", (20, 18, 22), 32), ("conv", (9, 11, 3, 5), 8), ("maxpool", (12, 10, 3), 16)]:
         base = Ref.gen(kind, *args, bits=bits)
-        idx = {"matmul": dict(m=args[0], n=args[1], k=args[2]), "conv": dict(x=args[0], y=args[1], c=args[2], k=args[3]),
-               "maxpool": dict(x=args[0] // 2, y=args[1] // 2, c=args[2])}[kind]
+        idx = {"matmul": lambda: dict(m=args[0], n=args[1], k=args[2]),
+               "conv": lambda: dict(x=args[0], y=args[1], c=args[2], k=args[3]),
+               "maxpool": lambda: dict(x=args[0] // 2, y=args[1] // 2, c=args[2])}[kind]()
         for t in range(6):
             tiles = ",".join(f"{n}:{int(rng.integers(1, min(6, r) + 1))}" for n, r in idx.items() if rng.random() < 0.7)
             tiles = tiles or f"{next(iter(idx))}:2"
