@@ -93,3 +93,10 @@ def conv_useful_macs(N, H, W, C, K, R=3, S=3, pad=1):
     def axis(L, T):
         return sum(1 for x in range(L) for t in range(T) if 0 <= x + t - pad < L)
     return N * axis(H, R) * axis(W, S) * C * K
+
+
+def shard_range(total, world, rank):
+    """Contiguous split of a partitioned (batch) index across ranks: [lo, hi)."""
+    base, extra = divmod(total, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
