@@ -163,7 +163,8 @@ Compiled* get_plan(sb_program* p, const std::vector<bool>& fresh, bool tc) {
   opt.fresh_outputs = fresh;
   c->plan = sb::build_plan(p->prog, opt);
   for (const auto& s : c->plan.steps) {
-    if (s.kind == sb::PStep::Launch && s.launch.kernel == sb::KernelKind::Generic) {
+    if (s.kind == sb::PStep::Launch &&
+        (s.launch.kernel == sb::KernelKind::Generic || s.launch.kernel == sb::KernelKind::Map)) {
       c->desc_of_step.push_back(static_cast<int>(c->descs.size()));
       c->descs.emplace_back();
       c->bufmaps.emplace_back();
@@ -223,6 +224,36 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
       ctx->launches++;
       continue;
     }
+    if (l.kernel == sb::KernelKind::Reduce) {
+      sb::ReduceArgs a;
+      std::memset(&a, 0, sizeof(a));
+      const sb::ReducePlan& r = l.reduce;
+      a.in = ptr_of(r.in_buf);
+      a.out = ptr_of(r.out_buf);
+      a.in_kind = r.in_kind;
+      a.out_kind = r.out_kind;
+      a.agg = r.agg;
+      a.fresh = r.fresh ? 1 : 0;
+      a.identity = r.identity;
+      a.np = r.np;
+      a.nr = r.nr;
+      a.rcount = r.rcount;
+      for (int k = 0; k < r.np; k++) {
+        a.prange[k] = r.prange[k];
+        a.pin[k] = r.pin[k];
+        a.pout[k] = r.pout[k];
+      }
+      for (int k = 0; k < r.nr; k++) {
+        a.rrange[k] = r.rrange[k];
+        a.rstep[k] = r.rstep[k];
+      }
+      a.in_c = r.in_c;
+      a.out_c = r.out_c;
+      a.pcount = r.pcount;
+      cuda_check(sb::launch_reduce(a, ctx->stream), "reduce");
+      ctx->launches++;
+      continue;
+    }
     int di = c->desc_of_step[i];
     sb::BufTable t;
     std::memset(&t, 0, sizeof(t));
@@ -232,8 +263,11 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
       t.elems[k] = plan.bufs[map[k]].elements;
       t.kind[k] = plan.bufs[map[k]].kind;
     }
-    cuda_check(sb::launch_generic(st.d_descs + di, l.pcount, t, ctx->d_err, static_cast<int>(i), ctx->stream),
-               "generic");
+    if (l.kernel == sb::KernelKind::Map)
+      cuda_check(sb::launch_map(st.d_descs + di, l.vcount, t, ctx->d_err, static_cast<int>(i), ctx->stream), "map");
+    else
+      cuda_check(sb::launch_generic(st.d_descs + di, l.pcount, t, ctx->d_err, static_cast<int>(i), ctx->stream),
+                 "generic");
     ctx->launches++;
   }
 }
@@ -438,9 +472,7 @@ int sb_execute_device(sb_context* ctx, sb_program* p, const sb_device_buffer* bu
         const auto& b = prog.buffers[r];
         bool consumed = false;  // a matched kernel overwrites fresh outputs itself
         for (const auto& s : c->plan.steps)
-          if (s.kind == sb::PStep::Launch && s.launch.kernel == sb::KernelKind::ConvI8TC &&
-              s.launch.conv.fresh_output && c->plan.bufs[s.launch.conv.c_buf].root_index == static_cast<int>(r))
-            consumed = true;
+          if (s.kind == sb::PStep::Launch && s.launch.fused_fill_root == static_cast<int>(r)) consumed = true;
         if (!consumed) {
           cuda_check(sb::launch_fill(ptrs[r], c->plan.bufs[r].kind, b.elements, sb::output_identity(prog, b.name),
                                      ctx->stream),

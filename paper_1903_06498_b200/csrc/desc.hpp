@@ -89,7 +89,16 @@ struct GenericDesc {
   DInstr code[kMaxCode];
   std::int64_t consts[kMaxConsts];
   DSpecial special[kMaxSpecial];
+  // vectorised owner-mode variant (kernels/map.cu): one thread owns kVec consecutive
+  // points of the fastest thread dim `vdim`
+  std::int8_t vdim;
+  std::int8_t vkind[kMaxAccess];  // 0 broadcast (coef 0), 1 contiguous aligned vector, 2 per-lane
+  std::int64_t vcount;            // threads: pcount / range[vdim] * ceil(range[vdim] / kVec)
 };
+
+constexpr int kVec = 4;            // lanes per thread in the map kernel
+constexpr int kVecMaxTemps = 8;
+constexpr int kVecMaxCells = 4;
 
 // Per-run buffer table (kernel parameter, by value).
 struct BufTable {

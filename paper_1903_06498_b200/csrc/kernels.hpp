@@ -13,6 +13,23 @@ namespace sb {
 cudaError_t launch_generic(const GenericDesc* d_desc, std::int64_t pcount, const BufTable& t,
                            DevError* err, int launch_id, cudaStream_t s);
 cudaError_t launch_fill(void* p, int kind, std::int64_t n, std::int64_t v, cudaStream_t s);
+// Vectorised owner-mode block kernel (kernels/map.cu): memory-bound map / reduce blocks.
+cudaError_t launch_map(const GenericDesc* d_desc, std::int64_t vcount, const BufTable& t, DevError* err,
+                       int launch_id, cudaStream_t s);
+
+// Streaming reduce/copy (kernels/reduce.cu).
+struct ReduceArgs {
+  const void* in;
+  void* out;
+  int in_kind, out_kind, agg, fresh;
+  std::int64_t identity;
+  int np, nr, rcount;
+  std::int64_t prange[kMaxDims], pin[kMaxDims], pout[kMaxDims];
+  std::int64_t rrange[kMaxDims], rstep[kMaxDims];
+  std::int64_t in_c, out_c, pcount;
+};
+int reduce_vec_lanes(int in_kind);
+cudaError_t launch_reduce(const ReduceArgs& a, cudaStream_t s);
 
 // tcgen05 implicit-GEMM convolution, i8 x i8 -> i32 accumulate (kernels/conv_tc.cu).
 struct ConvArgs {

@@ -205,6 +205,148 @@ bool match_conv(const Plan& plan, const PLaunch& l, const Program& prog, const P
   return true;
 }
 
+// True when no step before `step` writes plan buffer `buf`.
+bool first_writer(const Plan& plan, std::size_t step, int buf) {
+  for (std::size_t s = 0; s < step; s++) {
+    const PStep& ps = plan.steps[s];
+    if (ps.kind == PStep::Fill) {
+      if (ps.buf == buf) return false;
+      continue;
+    }
+    for (const auto& ins : ps.launch.code)
+      if (ins.op == kOpStore && ps.launch.acc[ins.acc].buf == buf) return false;
+    for (const auto& sp : ps.launch.specials)
+      if (ps.launch.acc[sp.dst].buf == buf) return false;
+  }
+  return true;
+}
+
+// The address function maps the given dims one-to-one onto [0, elements).
+bool covers_exactly(const FAff& a, const std::vector<int>& dims, const std::vector<PDim>& rng, std::int64_t elements) {
+  if (a.c != 0) return false;
+  std::vector<std::pair<std::int64_t, std::int64_t>> t;
+  std::int64_t count = 1, span = 0;
+  for (int d : dims) {
+    std::int64_t k = a.at(d);
+    if (k <= 0) return false;
+    t.emplace_back(k, rng[d].range);
+    count *= rng[d].range;
+    span += k * (rng[d].range - 1);
+  }
+  std::sort(t.begin(), t.end());
+  std::int64_t run = 0;
+  for (auto& [k, r] : t) {
+    if (k <= run) return false;
+    run += k * (r - 1);
+  }
+  return count == elements && span == elements - 1;
+}
+
+// $v = load(I); O = store($v) with no constraints: streaming reduce/copy (kernels/reduce.cu).
+bool match_reduce(const Plan& plan, PLaunch& l, const Program& prog, const PlanOptions& opt, std::size_t step) {
+  if (l.mode != kModeOwner || l.pdims.empty() || !l.cons.empty() || !l.priv.empty() || l.has_spill ||
+      !l.specials.empty() || l.code.size() != 2)
+    return false;
+  const DInstr& ld = l.code[0];
+  const DInstr& st = l.code[1];
+  if (ld.op != kOpLoad || st.op != kOpStore || st.a != ld.dst || ld.acc == st.acc) return false;
+  if (l.acc_mode[ld.acc] != kAccRead || l.acc_mode[st.acc] != kAccOwned) return false;
+  const PAccess& A = l.acc[ld.acc];
+  const PAccess& O = l.acc[st.acc];
+  const PBuffer& ib = plan.bufs[A.buf];
+  const PBuffer& ob = plan.bufs[O.buf];
+  auto intk = [](std::int8_t k) { return k == kI8 || k == kI16 || k == kI32; };
+  if (!intk(ib.kind) || !intk(ob.kind) || st.dtype != static_cast<std::int8_t>(ob.dtype)) return false;
+  const int V = reduce_vec_lanes(ib.kind);
+  const int obytes = ob.kind == kI8 ? 1 : ob.kind == kI16 ? 2 : 4;
+  if (V * obytes < 16) return false;
+  const int v = l.pdims[0];
+  if (A.addr.at(v) != 1 || O.addr.at(v) != 1 || l.dims[v].range % V != 0) return false;
+  if (A.addr.c % V != 0 || O.addr.c % V != 0) return false;
+  for (std::size_t d = 0; d < l.dims.size(); d++) {
+    if (static_cast<int>(d) == v) continue;
+    if (A.addr.at(d) % V != 0 || O.addr.at(d) % V != 0) return false;
+  }
+  ReducePlan r;
+  r.in_buf = A.buf;
+  r.out_buf = O.buf;
+  r.in_kind = ib.kind;
+  r.out_kind = ob.kind;
+  r.agg = st.agg;
+  r.np = static_cast<int>(l.pdims.size());
+  for (int i = 0; i < r.np; i++) {
+    int d = l.pdims[i];
+    r.prange[i] = l.dims[d].range;
+    r.pin[i] = A.addr.at(d);
+    r.pout[i] = O.addr.at(d);
+  }
+  r.nr = static_cast<int>(l.rdims.size());
+  std::int64_t rc = 1;
+  for (int i = 0; i < r.nr; i++) {
+    int d = l.rdims[i];
+    r.rrange[i] = l.dims[d].range;
+    r.rstep[i] = A.addr.at(d);
+    rc *= r.rrange[i];
+  }
+  if (rc > 6144) return false;
+  r.rcount = static_cast<int>(rc);
+  r.in_c = A.addr.c;
+  r.out_c = O.addr.c;
+  r.pcount = l.pcount;
+  // bounds: the whole box must be inside both buffers (affine extremes)
+  auto extremes = [&](const FAff& a, std::int64_t* lo, std::int64_t* hi) {
+    *lo = *hi = a.c;
+    for (std::size_t d = 0; d < l.dims.size(); d++) {
+      std::int64_t k = a.at(d) * (l.dims[d].range - 1);
+      (k < 0 ? *lo : *hi) += k;
+    }
+  };
+  std::int64_t lo, hi;
+  extremes(A.addr, &lo, &hi);
+  if (lo < 0 || hi >= ib.elements) return false;
+  extremes(O.addr, &lo, &hi);
+  if (lo < 0 || hi >= ob.elements) return false;
+  if (ob.root && ob.root_index < static_cast<int>(opt.fresh_outputs.size()) && opt.fresh_outputs[ob.root_index] &&
+      first_writer(plan, step, O.buf) && covers_exactly(O.addr, l.pdims, l.dims, ob.elements)) {
+    r.fresh = true;
+    r.identity = output_identity(prog, ob.name);
+    l.fused_fill_root = ob.root_index;
+  }
+  l.reduce = r;
+  return true;
+}
+
+// Vectorised owner-mode launch (kernels/map.cu): the fastest thread dim becomes kVec
+// lanes; every access is broadcast (coefficient 0), an aligned contiguous vector
+// (coefficient 1, everything else a multiple of kVec) or a per-lane gather.  Written
+// buffers must be aligned contiguous vectors so each thread owns whole vectors.
+bool match_map(PLaunch& l) {
+  if (l.mode != kModeOwner || l.pdims.empty() || !l.specials.empty()) return false;
+  if (l.ntemps > kVecMaxTemps || l.ncells > kVecMaxCells || l.priv.size() > static_cast<std::size_t>(kVecMaxCells))
+    return false;
+  const int v = l.pdims[0];
+  const std::int64_t rv = l.dims[v].range;
+  if (rv < kVec || l.pcount < 4096) return false;
+  std::vector<std::int8_t> kind(l.acc.size(), 2);
+  for (std::size_t i = 0; i < l.acc.size(); i++) {
+    const FAff& a = l.acc[i].addr;
+    std::int64_t k = a.at(v);
+    if (k == 0) {
+      kind[i] = 0;
+    } else if (k == 1) {
+      bool aligned = a.c % kVec == 0;
+      for (std::size_t d = 0; d < l.dims.size(); d++)
+        if (static_cast<int>(d) != v && a.at(d) % kVec != 0) aligned = false;
+      kind[i] = aligned ? 1 : 2;
+    }
+    if (l.acc_mode[i] != kAccRead && kind[i] != 1) return false;
+  }
+  l.vdim = v;
+  l.vkind = kind;
+  l.vcount = l.pcount / rv * ((rv + kVec - 1) / kVec);
+  return true;
+}
+
 }  // namespace
 
 void match_kernels(Plan* plan, const Program& p, const PlanOptions& opt) {
@@ -217,9 +359,13 @@ void match_kernels(Plan* plan, const Program& p, const PlanOptions& opt) {
     if (match_conv(*plan, st.launch, p, opt, s, &cp, &why)) {
       st.launch.kernel = KernelKind::ConvI8TC;
       st.launch.conv = cp;
-    } else if (!why.empty()) {
-      plan->notes.push_back("launch " + st.launch.path + ": contraction kept on the generic kernel (" + why + ")");
+      if (cp.fresh_output) st.launch.fused_fill_root = plan->bufs[cp.c_buf].root_index;
+      continue;
     }
+    if (!why.empty())
+      plan->notes.push_back("launch " + st.launch.path + ": contraction kept on the generic kernel (" + why + ")");
+    if (match_reduce(*plan, st.launch, p, opt, s)) st.launch.kernel = KernelKind::Reduce;
+    else if (match_map(st.launch)) st.launch.kernel = KernelKind::Map;
   }
 }
 

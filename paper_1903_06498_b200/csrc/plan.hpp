@@ -61,7 +61,20 @@ struct PSpecial {
 };
 
 // Specialised kernel families the matcher can route a launch to.
-enum class KernelKind { Generic, ConvI8TC, Reduce };
+enum class KernelKind { Generic, ConvI8TC, Map, Reduce };
+
+// Streaming reduce/copy ($v = load(I); O = store($v)): kernels/reduce.cu.
+struct ReducePlan {
+  int in_buf = -1, out_buf = -1;
+  int in_kind = 0, out_kind = 0, agg = 0;
+  bool fresh = false;
+  std::int64_t identity = 0;
+  int np = 0, nr = 0;
+  std::int64_t prange[kMaxDims] = {}, pin[kMaxDims] = {}, pout[kMaxDims] = {};
+  std::int64_t rrange[kMaxDims] = {}, rstep[kMaxDims] = {};
+  std::int64_t in_c = 0, out_c = 0, pcount = 0;
+  int rcount = 0;
+};
 
 // Parameters of the tcgen05 implicit-GEMM convolution (kernels/conv_tc.cu).
 struct ConvPlan {
@@ -102,6 +115,12 @@ struct PLaunch {
 
   KernelKind kernel = KernelKind::Generic;
   ConvPlan conv;
+  ReducePlan reduce;
+  int fused_fill_root = -1;  // root buffer whose prepare_outputs fill this launch performs itself
+  // map kernel (vectorised owner mode): vdim = thread dim split into kVec-lane vectors
+  int vdim = -1;
+  std::vector<std::int8_t> vkind;
+  std::int64_t vcount = 0;
 };
 
 struct PStep {

@@ -712,7 +712,7 @@ Plan build_plan(const Program& p, const PlanOptions& opt) {
 std::string Plan::describe() const {
   std::ostringstream os;
   static const char* modes[] = {"owner", "atomic", "serial"};
-  static const char* kinds[] = {"generic", "conv_i8_tc", "reduce"};
+  static const char* kinds[] = {"generic", "conv_i8_tc", "map", "reduce"};
   for (const auto& s : steps) {
     if (s.kind == PStep::Fill) {
       os << "fill " << bufs[s.buf].name << " = " << s.value << " (" << bufs[s.buf].elements
@@ -769,6 +769,9 @@ void to_desc(const PLaunch& l, GenericDesc* d, std::vector<int>* bufmap) {
   d->ncells = l.ncells;
   d->npriv = static_cast<int>(l.priv.size());
   d->nspecial = static_cast<int>(l.specials.size());
+  d->vdim = static_cast<std::int8_t>(l.vdim);
+  d->vcount = l.vcount;
+  for (std::size_t i = 0; i < l.vkind.size() && i < static_cast<std::size_t>(kMaxAccess); i++) d->vkind[i] = l.vkind[i];
   d->mode = l.mode;
   d->npdims = static_cast<std::int8_t>(l.pdims.size());
   d->nrdims = static_cast<std::int8_t>(l.rdims.size());
