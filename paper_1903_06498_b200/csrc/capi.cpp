@@ -204,6 +204,7 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
   auto ptr_of = [&](int b) { return plan.bufs[b].root ? root_ptr[plan.bufs[b].root_index] : st.scratch[b]; };
   for (std::size_t i = 0; i < plan.steps.size(); i++) {
     const auto& s = plan.steps[i];
+    if (s.elided) continue;
     if (s.kind == sb::PStep::Fill) {
       const auto& pb = plan.bufs[s.buf];
       cuda_check(sb::launch_fill(ptr_of(s.buf), pb.kind, pb.elements, s.value, ctx->stream), "fill");
@@ -220,6 +221,10 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
       a.b_elems = plan.bufs[l.conv.b_buf].elements;
       a.c_elems = plan.bufs[l.conv.c_buf].elements;
       a.b_immutable = l.conv.b_immutable;
+      if (l.conv.epi_vec) {
+        a.vec = ptr_of(l.conv.vec_buf);
+        a.vec_kind = plan.bufs[l.conv.vec_buf].kind;
+      }
       cuda_check(sb::launch_conv_tc(l.conv, a, ctx->stream, ctx->num_sms), "conv_tc");
       ctx->launches++;
       continue;

@@ -38,6 +38,8 @@ struct ConvArgs {
   void* c;        // output (i8/i16/i32)
   std::int64_t a_elems, b_elems, c_elems;
   bool b_immutable = false;  // filter is a root `in` buffer no plan step writes
+  const void* vec = nullptr;  // fused-epilogue per-channel vector buffer
+  int vec_kind = 0;
 };
 // Host-side checks that the plan fits the kernel's tiling; empty string = ok.
 const char* conv_tc_unsupported(const ConvPlan& cp);

@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <climits>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -66,6 +67,12 @@ struct ConvKParams {
   int debug_nofilt;       // timing experiments only
   int pdl;                // launched with programmatic stream serialization
   int filter_early;       // filter is immutable input: fetch before griddepcontrol.wait
+  // fused epilogue: out = wrap(max(acc + vec[k], lo)) (optional parts), int64 arithmetic
+  int epi, epi_vec, epi_lo;
+  long long lo;
+  const void* vec;
+  int vec_kind;
+  long long vec_c, vec_k;
   unsigned long long* trace;
 };
 
@@ -174,6 +181,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   std::uint64_t* tempty = bars + 2 * kStages + 2;
   std::uint64_t* fready = bars + 2 * kStages + 4;
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 2 * kStages + 5);
+  int* vec_s = reinterpret_cast<int*>(reinterpret_cast<std::uint8_t*>(bars) + 256);  // [K] epilogue vector
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -344,6 +352,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int xl = row / p.P;
     const int y = row % p.P;
     int iter = 0;
+    if (p.epi_vec) {
+      // per-output-channel vector of the fused epilogue (e.g. the bias), as int32 in smem
+      for (int k = threadIdx.x - 64; k < p.K; k += 128) {
+        long long a = p.vec_c + p.vec_k * k;
+        vec_s[k] = p.vec_kind == kI8 ? static_cast<const std::int8_t*>(p.vec)[a]
+                   : p.vec_kind == kI16 ? static_cast<const std::int16_t*>(p.vec)[a]
+                                        : static_cast<const std::int32_t*>(p.vec)[a];
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+    }
+    // fused epilogue on the exact s32 accumulator, int64 arithmetic, wrap at the i32 store
+    auto epilogue = [&](int k, std::uint32_t acc_bits) -> std::uint32_t {
+      if (!p.epi) return acc_bits;
+      long long x = static_cast<std::int32_t>(acc_bits);
+      if (p.epi_vec) x += vec_s[k];
+      if (p.epi_lo && x < p.lo) x = p.lo;
+      return static_cast<std::uint32_t>(x);
+    };
     if (p.tma_out) {
       // TMEM -> registers -> 128B-swizzled staging (row = TMEM lane, conflict-free) ->
       // TMA tensor stores of full lines; rows outside the image are clipped by the map.
@@ -367,12 +393,32 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld32(tmem_base + (static_cast<std::uint32_t>(quarter * 32) << 16) +
                         static_cast<std::uint32_t>(acc * p.K + h * 32),
                     v);
+          if (p.epi) {
+            // the 32 vector values of this half first (8 x ld.shared.v4, one latency), then
+            // the element-wise transform on registers (no memory traffic in between)
+            int bv[32];
+            const std::uint32_t vaddr = smem_u32(vec_s + h * 32);
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+              if (p.epi_vec)
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(bv[4 * q]), "=r"(bv[4 * q + 1]), "=r"(bv[4 * q + 2]), "=r"(bv[4 * q + 3])
+                             : "r"(vaddr + q * 16));
+              else
+                bv[4 * q] = bv[4 * q + 1] = bv[4 * q + 2] = bv[4 * q + 3] = 0;
+            }
+            const long long lo = p.epi_lo ? p.lo : LLONG_MIN;
+#pragma unroll
+            for (int q = 0; q < 32; q++) {
+              long long x = static_cast<long long>(static_cast<std::int32_t>(v[q])) + bv[q];
+              v[q] = static_cast<std::uint32_t>(x < lo ? lo : x);
+            }
+          }
           std::uint32_t rbase = smem_u32(stg + h * 16384 + row * 128);
 #pragma unroll
           for (int q = 0; q < 8; q++)
             asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rbase + ((q ^ (row & 7)) << 4)),
-                         "r"(v[4 * q]), "r"(v[4 * q + 1]), "r"(v[4 * q + 2]), "r"(v[4 * q + 3])
-                         : "memory");
+                         "r"(v[4 * q]), "r"(v[4 * q + 1]), "r"(v[4 * q + 2]), "r"(v[4 * q + 3]));
         }
         tc_fence_before();
         mbar_arrive(&tempty[acc]);  // accumulator drained: MMA may reuse it
@@ -439,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             std::int32_t* o = static_cast<std::int32_t*>(out) + obase + k0;
 #pragma unroll
             for (int q = 0; q < 32; q++)
-              o[q] = static_cast<std::int32_t>(p.fresh ? v[q] : static_cast<std::uint32_t>(o[q]) + v[q]);
+              o[q] = static_cast<std::int32_t>(p.fresh ? epilogue(k0 + q, v[q]) : static_cast<std::uint32_t>(o[q]) + v[q]);
           } else if (p.out_kind == kI16) {
             std::int16_t* o = static_cast<std::int16_t*>(out) + obase + k0;
 #pragma unroll
@@ -488,7 +534,8 @@ int pitch_for(std::int64_t W, std::int64_t S) {
 }
 
 std::size_t smem_bytes(const ConvKParams& kp) {
-  return 1024 /*align*/ + kp.staging_bytes + kStages * kp.strip_bytes + 1024 + kp.filt_bytes + 256;
+  return 1024 /*align*/ + kp.staging_bytes + kStages * kp.strip_bytes + 1024 + kp.filt_bytes + 256 +
+         static_cast<std::size_t>(kp.K) * 8;
 }
 
 bool fill_params(const ConvPlan& cp, ConvKParams* kp) {
@@ -690,6 +737,14 @@ cudaError_t launch_conv_tc(const ConvPlan& cp, const ConvArgs& args, cudaStream_
   }();
   kp.pdl = pdl ? 1 : 0;
   kp.filter_early = args.b_immutable ? 1 : 0;
+  kp.epi = cp.epi ? 1 : 0;
+  kp.epi_vec = cp.epi_vec ? 1 : 0;
+  kp.epi_lo = cp.epi_lo ? 1 : 0;
+  kp.lo = cp.lo;
+  kp.vec = args.vec;
+  kp.vec_kind = args.vec_kind;
+  kp.vec_c = cp.vec_c;
+  kp.vec_k = cp.vec_k;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = static_cast<unsigned>(kp.cluster);

@@ -347,19 +347,173 @@ bool match_map(PLaunch& l) {
   return true;
 }
 
+// K3e: a conv launch writing a per-point local accumulator T (scratch, zero-filled) whose
+// only consumer is the next phase  O = f(T, vec[k])  with f in the bias/ReLU family
+// (conv_relu.stripe after fuse+localize, test_passes.cpp:357-379): the epilogue applies f
+// on the s32 accumulator and writes O directly; T never reaches HBM.
+void fuse_conv_epilogue(Plan* plan, std::size_t s, const Program& prog, const PlanOptions& opt) {
+  PLaunch& cl = plan->steps[s].launch;
+  ConvPlan& c = cl.conv;
+  const int T = c.c_buf;
+  if (plan->bufs[T].root || c.fresh_output) return;
+  // T is touched only by: one zero Fill before s, the conv, and the consumer s2 after s
+  int fill_step = -1, s2 = -1;
+  for (std::size_t k = 0; k < plan->steps.size(); k++) {
+    if (k == s) continue;
+    const PStep& ps = plan->steps[k];
+    bool touches = false;
+    if (ps.kind == PStep::Fill) {
+      if (ps.buf == T) {
+        if (k > s || ps.value != 0 || fill_step >= 0) return;
+        fill_step = static_cast<int>(k);
+      }
+      continue;
+    }
+    for (const auto& a : ps.launch.acc) touches |= a.buf == T;
+    if (!touches) continue;
+    if (k < s || s2 >= 0) return;
+    s2 = static_cast<int>(k);
+  }
+  if (fill_step < 0 || s2 < 0) return;
+  for (std::size_t k = s + 1; k < static_cast<std::size_t>(s2); k++)  // nothing in between
+    if (!plan->steps[k].elided) return;
+  PLaunch& el = plan->steps[s2].launch;
+  if (el.mode != kModeOwner || !el.cons.empty() || !el.priv.empty() || el.has_spill || !el.specials.empty()) return;
+  // T must be dense [n][x][y][k] for the conv and read back at the same element
+  const std::int64_t K = c.K, HW = c.H * c.W, NHW = c.N * HW;
+  if (!(c.c0 == 0 && c.c_y == K && (c.H == 1 || c.c_x == c.W * K) && (c.N == 1 || c.c_n == HW * K))) return;
+  if (el.dims.size() != 2) return;
+  int pd = -1, kd = -1;
+  for (int d = 0; d < 2; d++) (el.dims[d].range == K ? kd : pd) = d;
+  if (pd < 0 || kd < 0 || el.dims[pd].range != NHW) return;
+  // symbolic evaluation of the body: each temp is ACC, VEC (per-k vector), CONST or an op on them
+  struct Sym {
+    int kind = -1;  // 0 ACC, 1 VEC, 2 CONST, 3 ADD(a,b), 4 MAX(a,b)
+    int a = -1, b = -1;
+    std::int64_t c = 0;
+  };
+  std::vector<Sym> nodes;
+  std::vector<int> temp(el.ntemps, -1);
+  int vec_acc = -1, out_acc = -1, out_node = -1;
+  auto operand = [&](int x) -> int {
+    if (x >= 0) return temp[x];
+    Sym s;
+    s.kind = 2;
+    s.c = el.consts[-1 - x];
+    nodes.push_back(s);
+    return static_cast<int>(nodes.size()) - 1;
+  };
+  for (const auto& ins : el.code) {
+    Sym s;
+    if (ins.op == kOpLoad) {
+      const PAccess& a = el.acc[ins.acc];
+      if (a.buf == T) {
+        if (!(a.addr.c == 0 && a.addr.at(pd) == K && a.addr.at(kd) == 1)) return;
+        s.kind = 0;
+      } else {
+        if (a.addr.at(pd) != 0 || el.acc_mode[ins.acc] != kAccRead) return;
+        if (vec_acc >= 0 && !(el.acc[vec_acc].buf == a.buf && el.acc[vec_acc].addr == a.addr)) return;
+        vec_acc = ins.acc;
+        s.kind = 1;
+      }
+    } else if (ins.op == kOpConst) {
+      int o = operand(ins.a);
+      if (o < 0) return;
+      temp[ins.dst] = o;
+      continue;
+    } else if (ins.op == kOpAdd || ins.op == kOpMax) {
+      s.kind = ins.op == kOpAdd ? 3 : 4;
+      s.a = operand(ins.a);
+      s.b = operand(ins.b);
+      if (s.a < 0 || s.b < 0) return;
+    } else if (ins.op == kOpStore) {
+      if (out_acc >= 0) return;
+      out_acc = ins.acc;
+      out_node = temp[ins.a];
+      if (out_node < 0) return;
+      if (static_cast<DType>(ins.dtype) != DType::I32) return;  // TMA-store epilogue writes i32
+      if (ins.agg != static_cast<std::int8_t>(Agg::Assign) && ins.agg != static_cast<std::int8_t>(Agg::Add)) return;
+      continue;
+    } else {
+      return;
+    }
+    nodes.push_back(s);
+    temp[ins.dst] = static_cast<int>(nodes.size()) - 1;
+  }
+  if (out_acc < 0) return;
+  // match out = MAX(x, CONST) | x ;  x = ADD(ACC, VEC) | ADD(VEC, ACC) | ACC
+  ConvPlan e = c;
+  int n = out_node;
+  e.epi_lo = false;
+  if (nodes[n].kind == 4) {
+    int a = nodes[n].a, b = nodes[n].b;
+    if (nodes[b].kind != 2) std::swap(a, b);
+    if (nodes[b].kind != 2) return;
+    e.epi_lo = true;
+    e.lo = nodes[b].c;
+    n = a;
+  }
+  e.epi_vec = false;
+  if (nodes[n].kind == 3) {
+    int a = nodes[n].a, b = nodes[n].b;
+    if (nodes[a].kind == 1) std::swap(a, b);
+    if (nodes[a].kind != 0 || nodes[b].kind != 1) return;
+    e.epi_vec = true;
+    const PAccess& va = el.acc[vec_acc];
+    e.vec_buf = va.buf;
+    e.vec_c = va.addr.c;
+    e.vec_k = va.addr.at(kd);
+    if (plan->bufs[va.buf].kind != kI32 && plan->bufs[va.buf].kind != kI16 && plan->bufs[va.buf].kind != kI8) return;
+    if (e.vec_c < 0 || e.vec_k < 0 || e.vec_c + e.vec_k * (K - 1) >= plan->bufs[va.buf].elements) return;
+  } else if (nodes[n].kind != 0) {
+    return;
+  }
+  // output O: address = o_pix * pix + k + o_c over the consumer's dims
+  const PAccess& O = el.acc[out_acc];
+  const PBuffer& ob = plan->bufs[O.buf];
+  if (O.addr.at(kd) != 1 || O.addr.at(pd) <= 0 || ob.kind != kI32) return;
+  const std::int64_t op = O.addr.at(pd);
+  if (O.addr.c < 0 || O.addr.c + op * (NHW - 1) + K - 1 >= ob.elements) return;
+  bool overwrite = el.code.back().agg == static_cast<std::int8_t>(Agg::Assign);
+  const bool fresh_root = ob.root && ob.root_index < static_cast<int>(opt.fresh_outputs.size()) &&
+                          opt.fresh_outputs[ob.root_index] && output_identity(prog, ob.name) == 0 &&
+                          first_writer(*plan, static_cast<std::size_t>(s2), O.buf);
+  const bool covers = O.addr.c == 0 && op == K && NHW * K == ob.elements;
+  if (!overwrite && !(fresh_root && covers)) return;
+  e.epi = e.epi_vec || e.epi_lo;
+  e.c_buf = O.buf;
+  e.c_dtype = ob.dtype;
+  e.c_y = op;
+  e.c_x = op * c.W;
+  e.c_n = op * HW;
+  e.c0 = O.addr.c;
+  e.fresh_output = true;  // the consumer overwrites (assign) or adds onto the fused identity 0
+  if (const char* bad = conv_tc_unsupported(e)) {
+    (void)bad;
+    return;
+  }
+  c = e;
+  plan->steps[fill_step].elided = true;
+  plan->steps[s2].elided = true;
+  if (fresh_root && covers) cl.fused_fill_root = ob.root_index;
+  plan->notes.push_back("launch " + cl.path + ": epilogue of " + el.path + " fused; local buffer " + plan->bufs[T].name +
+                        " never materialised");
+}
+
 }  // namespace
 
 void match_kernels(Plan* plan, const Program& p, const PlanOptions& opt) {
   if (!opt.enable_tc) return;
   for (std::size_t s = 0; s < plan->steps.size(); s++) {
     PStep& st = plan->steps[s];
-    if (st.kind != PStep::Launch) continue;
+    if (st.kind != PStep::Launch || st.elided) continue;
     ConvPlan cp;
     std::string why;
     if (match_conv(*plan, st.launch, p, opt, s, &cp, &why)) {
       st.launch.kernel = KernelKind::ConvI8TC;
       st.launch.conv = cp;
       if (cp.fresh_output) st.launch.fused_fill_root = plan->bufs[cp.c_buf].root_index;
+      fuse_conv_epilogue(plan, s, p, opt);
       continue;
     }
     if (!why.empty())

@@ -91,6 +91,10 @@ struct ConvPlan {
   std::int64_t c_n = 0, c_x = 0, c_y = 0, c0 = 0;
   bool fresh_output = false;  // output known identity-filled: overwrite instead of accumulate
   bool b_immutable = false;   // filter is a root `in` buffer that no plan step writes
+  // fused element-wise epilogue (K3e): out = wrap(max(acc + vec[k], lo)) with the optional parts
+  bool epi = false, epi_vec = false, epi_lo = false;
+  int vec_buf = -1;
+  std::int64_t vec_c = 0, vec_k = 0, lo = 0;
 };
 
 struct PLaunch {
@@ -125,6 +129,7 @@ struct PLaunch {
 
 struct PStep {
   enum Kind { Fill, Launch } kind = Launch;
+  bool elided = false;  // absorbed into another step (fused epilogue / fused identity fill)
   int buf = -1;
   std::int64_t value = 0;
   PLaunch launch;

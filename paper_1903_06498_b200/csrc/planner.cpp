@@ -585,9 +585,39 @@ class Lowerer {
       l.cons.push_back(f);
     }
     for (auto& a : l.acc) a.addr = compact(a.addr);
+    coalesce(l);
     if (l.dims.size() > static_cast<std::size_t>(kMaxDims))
       throw Error("Unsupported", "nest at " + l.path + " has more than 24 non-trivial indexes");
     analyze(l);
+  }
+
+  // Loop coalescing: adjacent dims (d outer, d+1 inner) with k[d] == k[d+1] * range[d+1]
+  // in every access and constraint are one index of range r_d * r_{d+1} (a tiled index
+  // after tile_rewrite, tile.cpp:100-235, becomes untiled again).  Adjacency keeps the
+  // lexicographic order, so execution semantics are unchanged.
+  static void coalesce(PLaunch& l) {
+    bool changed = true;
+    while (changed) {
+      changed = false;
+      for (std::size_t d = 0; d + 1 < l.dims.size(); d++) {
+        const std::int64_t r1 = l.dims[d + 1].range;
+        auto ok = [&](const FAff& f) { return f.at(d) == f.at(d + 1) * r1; };
+        bool all = true;
+        for (const auto& a : l.acc) all &= ok(a.addr);
+        for (const auto& c : l.cons) all &= ok(c);
+        if (!all) continue;
+        auto drop = [&](FAff& f) {
+          if (d < f.k.size()) f.k.erase(f.k.begin() + static_cast<long>(d));
+        };
+        for (auto& a : l.acc) drop(a.addr);
+        for (auto& c : l.cons) drop(c);
+        l.dims[d + 1].name = l.dims[d].name + "*" + l.dims[d + 1].name;
+        l.dims[d + 1].range *= l.dims[d].range;
+        l.dims.erase(l.dims.begin() + static_cast<long>(d));
+        changed = true;
+        break;
+      }
+    }
   }
 
   void analyze(PLaunch& l) {
@@ -714,6 +744,7 @@ std::string Plan::describe() const {
   static const char* modes[] = {"owner", "atomic", "serial"};
   static const char* kinds[] = {"generic", "conv_i8_tc", "map", "reduce"};
   for (const auto& s : steps) {
+    if (s.elided) os << "(elided) ";
     if (s.kind == PStep::Fill) {
       os << "fill " << bufs[s.buf].name << " = " << s.value << " (" << bufs[s.buf].elements
          << " elems)\n";

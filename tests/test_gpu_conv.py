@@ -117,3 +117,31 @@ def test_conv_tc_full_config2_exact():
     ref = ref.permute(0, 2, 3, 1).to(torch.int64)
     assert torch.equal(O.to(torch.int64), ref)
     ctx.set_stream(None)
+
+
+@pytest.mark.parametrize("shape", [(2, 8, 8, 64, 64), (1, 6, 20, 128, 32), (3, 4, 9, 64, 96)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_fused_conv_bias_relu(shape):
+    """BASELINE config 3 structure: conv into a per-tile local accumulator, then
+    O = max(T + Bias[k], 0); the epilogue is fused into the tcgen05 kernel."""
+    import paper_1903_06498_b200 as sb
+    N, H, Wd, C, K = shape
+    text = W.conv_bias_relu(N, H, Wd, C, K)
+    plan = sb.parse_program(text).describe_plan(True)
+    assert "epilogue of" in plan and "conv_i8_tc" in plan, plan
+    _, inp = inputs_for(text, 77 + N)
+    exp = expected(text, inp)
+    got = run_device(text, inp)
+    np.testing.assert_array_equal(got["O"], exp["O"])
+
+
+def test_fused_epilogue_int64_semantics_near_overflow():
+    """max(T + Bias, 0) is evaluated on unwrapped int64 temps (interp.cpp:515-537) and
+    wrapped only at the store: biases near 2^31 must wrap exactly like the reference."""
+    text = W.conv_bias_relu(1, 4, 8, 64, 32)
+    p, inp = inputs_for(text, 5)
+    inp["Bias"] = (32, np.array([2**31 - 1 - 3 * i for i in range(16)] + [-(2**31) + 7 * i for i in range(16)],
+                                dtype=np.int64))
+    exp = expected(text, inp)
+    got = run_device(text, inp)
+    np.testing.assert_array_equal(got["O"], exp["O"])
