@@ -229,6 +229,12 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
       ctx->launches++;
       continue;
     }
+    if (l.kernel == sb::KernelKind::GemmI8TC) {
+      sb::GemmArgs a{ptr_of(l.gemm.a_buf), ptr_of(l.gemm.b_buf), ptr_of(l.gemm.c_buf)};
+      cuda_check(sb::launch_gemm_tc(l.gemm, a, ctx->stream, ctx->num_sms), "gemm_tc");
+      ctx->launches++;
+      continue;
+    }
     if (l.kernel == sb::KernelKind::Reduce) {
       sb::ReduceArgs a;
       std::memset(&a, 0, sizeof(a));

@@ -31,6 +31,15 @@ struct ReduceArgs {
 int reduce_vec_lanes(int in_kind);
 cudaError_t launch_reduce(const ReduceArgs& a, cudaStream_t s);
 
+// tcgen05 GEMM (kernels/gemm_tc.cu).
+struct GemmArgs {
+  const void* a;
+  const void* b;
+  void* c;
+};
+const char* gemm_tc_unsupported(const GemmPlan& g);
+cudaError_t launch_gemm_tc(const GemmPlan& g, const GemmArgs& args, cudaStream_t s, int num_sms);
+
 // tcgen05 implicit-GEMM convolution, i8 x i8 -> i32 accumulate (kernels/conv_tc.cu).
 struct ConvArgs {
   const void* a;  // input activations (i8)

@@ -1,0 +1,412 @@
+// tcgen05 GEMM for Stripe matmul-shaped contraction blocks (K3):
+//     $a = load(A); $b = load(B); $p = mul($a, $b); C = store($p)   C:add
+// with i8 operands: C[m, n] (+)= sum_k A[m, k] * B[k, n]  (gen_matmul, support.cpp:50-77;
+// matmul64.stripe).  A is K-major (k contiguous), B either N-major (n contiguous, the
+// reference generator's layout) or K-major.
+//
+// B200 mapping: persistent CTAs over 128x128 output tiles; warp 0 = TMA producer
+// (128-byte-swizzled boxes: A 128 m x 128 k, B 128 k x 128 n or 128 n x 128 k), 4-stage
+// mbarrier ring; warp 1 = one thread issuing tcgen05.mma.cta_group::1.kind::i8 (M=128,
+// N=128, K=32 per instruction); warps 2-5 = epilogue: tcgen05.ld -> registers ->
+// 128B-swizzled smem -> TMA tensor store (out-of-range rows/cols clipped), or a direct
+// read-modify-write when the output accumulates into existing contents.  TMA zero-fill
+// of the K tail contributes exact zeros.  Exactness: s32 accumulation with
+// K * 128 * 128 < 2^31 (checked by the planner) equals the reference's int64 sum.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../kernels.hpp"
+
+namespace sb {
+namespace {
+
+constexpr int kThreads = 192;
+constexpr int kStages = 4;
+constexpr int BM = 128, BN = 128, BK = 128;
+constexpr std::uint32_t kStageA = BM * BK, kStageB = BK * BN;  // bytes (i8)
+
+struct GemmKParams {
+  int M, N, K;
+  int tiles_m, tiles_n, kblocks;
+  int b_kmajor;
+  int fresh, tma_out, out_kind;
+  void* c;
+  long long ldc;  // elements
+  std::uint32_t idesc;
+  int pdl, b_early;
+};
+
+__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
+  return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(std::uint64_t* bar, std::uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(std::uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(std::uint64_t* bar, std::uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(std::uint32_t dst, const CUtensorMap* map, std::uint64_t* bar, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<std::uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void umma_i8(std::uint32_t d, std::uint32_t a_lo, std::uint32_t a_hi, std::uint32_t b_lo,
+                                        std::uint32_t b_hi, std::uint32_t idesc, std::uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 da, db;\n\t"
+      "mov.b64 da, {%1, %2};\n\t"
+      "mov.b64 db, {%3, %4};\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], da, db, %5, p;\n\t}" ::"r"(d),
+      "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(std::uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld32(std::uint32_t taddr, std::uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// SWIZZLE_128B descriptors (version 1, layout 2 in bits 61-63).
+// K-major: rows of 128 B, 8-row atoms (SBO = 1024 B), LBO unused (16 B).
+// MN-major: 128-element MN rows per k, 8-k-row atoms (SBO = 1024 B), LBO = next 128-element MN block.
+constexpr std::uint32_t kHiSW128 = (1024u >> 4) | (1u << 14) | (2u << 29);
+
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_i8_tc_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
+                      const __grid_constant__ CUtensorMap cmap, const GemmKParams p) {
+  extern __shared__ __align__(1024) std::uint8_t smem_raw[];
+  std::uint8_t* base =
+      reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t{1023});
+  std::uint8_t* sa = base;                              // kStages x 16 KB
+  std::uint8_t* sbm = sa + kStages * kStageA;           // kStages x 16 KB
+  std::uint8_t* stg = sbm + kStages * kStageB;          // 64 KB output staging (4 x 16 KB column quarters)
+  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(stg + BM * BN * 4);
+  std::uint64_t* full = bars;
+  std::uint64_t* empty = bars + kStages;
+  std::uint64_t* tfull = bars + 2 * kStages;
+  std::uint64_t* tempty = bars + 2 * kStages + 2;
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 2 * kStages + 4);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int tiles = p.tiles_m * p.tiles_n;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; a++) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const std::uint32_t tmem_base = *tmem_slot;
+  if (p.pdl && threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+  if (warp == 0) {
+    if (lane == 0) {
+      if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+      int stage = 0;
+      std::uint32_t phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * BN;
+        for (int kb = 0; kb < p.kblocks; kb++) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], kStageA + kStageB);
+          tma_load_2d(smem_u32(sa + stage * kStageA), &amap, &full[stage], kb * BK, m0);
+          if (p.b_kmajor) tma_load_2d(smem_u32(sbm + stage * kStageB), &bmap, &full[stage], kb * BK, n0);
+          else tma_load_2d(smem_u32(sbm + stage * kStageB), &bmap, &full[stage], n0, kb * BK);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0, iter = 0;
+      std::uint32_t phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, iter++) {
+        const int acc = iter & 1;
+        mbar_wait(&tempty[acc], ((iter >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const std::uint32_t d = tmem_base + static_cast<std::uint32_t>(acc * BN);
+        for (int kb = 0; kb < p.kblocks; kb++) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const std::uint32_t a0 = (smem_u32(sa + stage * kStageA) >> 4) | (1u << 16);
+          const std::uint32_t bsm = smem_u32(sbm + stage * kStageB);
+#pragma unroll
+          for (int ks = 0; ks < BK / 32; ks++) {
+            // A: +32 bytes along the 128-byte K row; B: K-major +32 bytes, N-major +32 rows (4 KB)
+            std::uint32_t b_lo = p.b_kmajor ? (((bsm + ks * 32) >> 4) | (1u << 16))
+                                            : (((bsm + ks * 32 * 128) >> 4) | ((static_cast<std::uint32_t>(BK * 128) >> 4) << 16));
+            umma_i8(d, a0 + ks * 2, kHiSW128, b_lo, kHiSW128, p.idesc, (kb | ks) != 0);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const bool leader = threadIdx.x == 64;
+    int iter = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, iter++) {
+      const int acc = iter & 1;
+      const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * BN;
+      if (p.tma_out) {
+        if (leader) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+      mbar_wait(&tfull[acc], (iter >> 1) & 1);
+      tc_fence_after();
+      for (int h = 0; h < BN / 32; h++) {
+        std::uint32_t v[32];
+        tmem_ld32(tmem_base + (static_cast<std::uint32_t>(quarter * 32) << 16) + static_cast<std::uint32_t>(acc * BN + h * 32),
+                  v);
+        if (p.tma_out) {
+          std::uint32_t rbase = smem_u32(stg + h * 16384 + row * 128);
+#pragma unroll
+          for (int q = 0; q < 8; q++)
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rbase + ((q ^ (row & 7)) << 4)),
+                         "r"(v[4 * q]), "r"(v[4 * q + 1]), "r"(v[4 * q + 2]), "r"(v[4 * q + 3]));
+        } else if (m0 + row < p.M) {
+          for (int q = 0; q < 32; q++) {
+            int n = n0 + h * 32 + q;
+            if (n >= p.N) break;
+            long long idx = static_cast<long long>(m0 + row) * p.ldc + n;
+            if (p.out_kind == kI32) {
+              std::int32_t* o = static_cast<std::int32_t*>(p.c) + idx;
+              *o = static_cast<std::int32_t>(p.fresh ? v[q] : static_cast<std::uint32_t>(*o) + v[q]);
+            } else if (p.out_kind == kI16) {
+              std::int16_t* o = static_cast<std::int16_t*>(p.c) + idx;
+              *o = static_cast<std::int16_t>(p.fresh ? v[q] : static_cast<std::uint32_t>(*o) + v[q]);
+            } else {
+              std::int8_t* o = static_cast<std::int8_t*>(p.c) + idx;
+              *o = static_cast<std::int8_t>(p.fresh ? v[q] : static_cast<std::uint32_t>(*o) + v[q]);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (p.tma_out) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (leader) {
+          for (int h = 0; h < BN / 32; h++)
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                             reinterpret_cast<std::uint64_t>(&cmap)),
+                         "r"(smem_u32(stg + h * 16384)), "r"(n0 + h * 32), "r"(m0)
+                         : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      }
+    }
+    if (p.tma_out && leader) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(256));
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+constexpr std::size_t kSmem = 1024 + kStages * (kStageA + kStageB) + BM * BN * 4 + 256;
+
+struct Prepared {
+  GemmPlan gp;
+  const void *a, *b;
+  void* c;
+  GemmKParams kp;
+  CUtensorMap amap, bmap, cmap;
+};
+
+bool same(const GemmPlan& x, const GemmPlan& y) {
+  return std::memcmp(&x.M, &y.M, sizeof(long long) * 9) == 0 && x.b_kmajor == y.b_kmajor && x.fresh == y.fresh &&
+         x.c_dtype == y.c_dtype;
+}
+
+std::mutex g_mu;
+std::vector<Prepared>* g_prep = nullptr;
+
+cudaError_t prepare(const GemmPlan& g, const GemmArgs& args, Prepared* out) {
+  out->gp = g;
+  out->a = args.a;
+  out->b = args.b;
+  out->c = args.c;
+  auto encode = get_encode();
+  if (!encode) return cudaErrorNotSupported;
+  GemmKParams& kp = out->kp;
+  std::memset(&kp, 0, sizeof(kp));
+  kp.M = static_cast<int>(g.M);
+  kp.N = static_cast<int>(g.N);
+  kp.K = static_cast<int>(g.K);
+  kp.tiles_m = static_cast<int>((g.M + BM - 1) / BM);
+  kp.tiles_n = static_cast<int>((g.N + BN - 1) / BN);
+  kp.kblocks = static_cast<int>((g.K + BK - 1) / BK);
+  kp.b_kmajor = g.b_kmajor ? 1 : 0;
+  kp.fresh = g.fresh ? 1 : 0;
+  kp.out_kind = g.c_dtype == DType::I8 ? kI8 : g.c_dtype == DType::I16 ? kI16 : kI32;
+  kp.ldc = g.ldc;
+  kp.c = static_cast<char*>(args.c) + g.c0 * (kp.out_kind == kI8 ? 1 : kp.out_kind == kI16 ? 2 : 4);
+  kp.tma_out = kp.fresh && kp.out_kind == kI32 && g.ldc % 4 == 0 &&
+               reinterpret_cast<std::uintptr_t>(kp.c) % 16 == 0;
+  // idesc: S32 accumulate, signed A/B, A K-major, B K- or MN-major, N = 128, M = 128
+  kp.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((kp.b_kmajor ? 0u : 1u) << 16) | ((128u >> 3) << 17) |
+             ((128u >> 4) << 24);
+  cuuint32_t es[2] = {1, 1};
+  const std::int8_t* a = static_cast<const std::int8_t*>(args.a) + g.a0;
+  const std::int8_t* b = static_cast<const std::int8_t*>(args.b) + g.b0;
+  if (reinterpret_cast<std::uintptr_t>(a) % 16 || reinterpret_cast<std::uintptr_t>(b) % 16) return cudaErrorMisalignedAddress;
+  cuuint64_t adim[2] = {static_cast<cuuint64_t>(g.K), static_cast<cuuint64_t>(g.M)};
+  cuuint64_t astr[1] = {static_cast<cuuint64_t>(g.lda)};
+  cuuint32_t abox[2] = {BK, BM};
+  if (encode(&out->amap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<std::int8_t*>(a), adim, astr, abox, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  cuuint64_t bdim[2], bstr[1] = {static_cast<cuuint64_t>(g.ldb)};
+  cuuint32_t bbox[2];
+  if (g.b_kmajor) {
+    bdim[0] = static_cast<cuuint64_t>(g.K);
+    bdim[1] = static_cast<cuuint64_t>(g.N);
+    bbox[0] = BK;
+    bbox[1] = BN;
+  } else {
+    bdim[0] = static_cast<cuuint64_t>(g.N);
+    bdim[1] = static_cast<cuuint64_t>(g.K);
+    bbox[0] = BN;
+    bbox[1] = BK;
+  }
+  if (encode(&out->bmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<std::int8_t*>(b), bdim, bstr, bbox, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  std::memset(&out->cmap, 0, sizeof(out->cmap));
+  if (kp.tma_out) {
+    cuuint64_t cdim[2] = {static_cast<cuuint64_t>(g.N), static_cast<cuuint64_t>(g.M)};
+    cuuint64_t cstr[1] = {static_cast<cuuint64_t>(g.ldc * 4)};
+    cuuint32_t cbox[2] = {32, BM};
+    if (encode(&out->cmap, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, kp.c, cdim, cstr, cbox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_i8_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kSmem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace
+
+const char* gemm_tc_unsupported(const GemmPlan& g) {
+  if (g.K * 128 * 128 >= (1ll << 31)) return "reduction too long for exact s32 accumulation";
+  if (g.lda % 16 || g.ldb % 16 || g.a0 % 16 || g.b0 % 16) return "operand rows not 16-byte aligned";
+  if (g.M < 1 || g.N < 1 || g.K < 1) return "empty";
+  if (g.lda < g.K || (g.b_kmajor ? g.ldb < g.K : g.ldb < g.N)) return "overlapping operand rows";
+  return nullptr;
+}
+
+cudaError_t launch_gemm_tc(const GemmPlan& g, const GemmArgs& args, cudaStream_t s, int num_sms) {
+  Prepared* pr = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(g_mu);
+    if (!g_prep) g_prep = new std::vector<Prepared>();
+    for (auto& e : *g_prep)
+      if (e.a == args.a && e.b == args.b && e.c == args.c && same(e.gp, g)) pr = &e;
+    if (!pr) {
+      if (g_prep->size() >= 256) g_prep->clear();
+      Prepared fresh;
+      cudaError_t err = prepare(g, args, &fresh);
+      if (err != cudaSuccess) return err;
+      g_prep->push_back(fresh);
+      pr = &g_prep->back();
+    }
+  }
+  GemmKParams kp = pr->kp;
+  kp.pdl = 1;
+  int tiles = kp.tiles_m * kp.tiles_n;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(tiles < num_sms ? tiles : num_sms));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gemm_i8_tc_kernel, pr->amap, pr->bmap, pr->cmap, kp);
+}
+
+}  // namespace sb

@@ -347,6 +347,79 @@ bool match_map(PLaunch& l) {
   return true;
 }
 
+// Plain matmul leaf (gen_matmul, support.cpp:50-77): exactly one m, n and k dim,
+// no constraints, A k-contiguous, B n- or k-contiguous, C n-contiguous.
+bool match_gemm(const Plan& plan, PLaunch& l, const Program& prog, const PlanOptions& opt, std::size_t step) {
+  if (l.mode != kModeOwner || !l.priv.empty() || l.has_spill || !l.specials.empty() || !l.consts.empty() ||
+      !l.cons.empty() || l.code.size() != 4)
+    return false;
+  const DInstr &la = l.code[0], &lb = l.code[1], &mu = l.code[2], &st = l.code[3];
+  if (la.op != kOpLoad || lb.op != kOpLoad || mu.op != kOpMul || st.op != kOpStore) return false;
+  if (!((mu.a == la.dst && mu.b == lb.dst) || (mu.a == lb.dst && mu.b == la.dst)) || st.a != mu.dst) return false;
+  if (st.agg != static_cast<std::int8_t>(Agg::Add)) return false;
+  const PAccess* A = &l.acc[la.acc];
+  const PAccess* B = &l.acc[lb.acc];
+  const PAccess& C = l.acc[st.acc];
+  if (A->buf == C.buf || B->buf == C.buf || plan.bufs[A->buf].kind != kI8 || plan.bufs[B->buf].kind != kI8) return false;
+  DType cdt = static_cast<DType>(st.dtype);
+  if (cdt == DType::F32 || plan.bufs[C.buf].dtype != cdt) return false;
+  if (l.dims.size() != 3) return false;
+  auto roles = [&](const PAccess* a, const PAccess* b, int* m, int* n, int* k) {
+    *m = *n = *k = -1;
+    for (int d = 0; d < 3; d++) {
+      bool ia = a->addr.uses(d), ib = b->addr.uses(d), ic = C.addr.uses(d);
+      if (ia && !ib && ic) *m = d;
+      else if (!ia && ib && ic) *n = d;
+      else if (ia && ib && !ic) *k = d;
+    }
+    return *m >= 0 && *n >= 0 && *k >= 0 && a->addr.at(*k) == 1;
+  };
+  int m, n, k;
+  if (!roles(A, B, &m, &n, &k)) {
+    std::swap(A, B);
+    if (!roles(A, B, &m, &n, &k)) return false;
+  }
+  GemmPlan g;
+  g.M = l.dims[m].range;
+  g.N = l.dims[n].range;
+  g.K = l.dims[k].range;
+  g.lda = A->addr.at(m);
+  g.a0 = A->addr.c;
+  if (B->addr.at(n) == 1) {
+    g.b_kmajor = false;
+    g.ldb = B->addr.at(k);
+  } else if (B->addr.at(k) == 1) {
+    g.b_kmajor = true;
+    g.ldb = B->addr.at(n);
+  } else {
+    return false;
+  }
+  g.b0 = B->addr.c;
+  if (C.addr.at(n) != 1) return false;
+  g.ldc = C.addr.at(m);
+  g.c0 = C.addr.c;
+  g.c_dtype = cdt;
+  g.a_buf = A->buf;
+  g.b_buf = B->buf;
+  g.c_buf = C.buf;
+  if (g.lda <= 0 || g.ldb <= 0 || g.ldc < g.N || g.a0 < 0 || g.b0 < 0 || g.c0 < 0) return false;
+  if (g.a0 + g.lda * (g.M - 1) + g.K - 1 >= plan.bufs[A->buf].elements) return false;
+  long long bmax = g.b_kmajor ? g.b0 + g.ldb * (g.N - 1) + g.K - 1 : g.b0 + g.ldb * (g.K - 1) + g.N - 1;
+  if (bmax >= plan.bufs[B->buf].elements) return false;
+  if (g.c0 + g.ldc * (g.M - 1) + g.N - 1 >= plan.bufs[C.buf].elements) return false;
+  if (gemm_tc_unsupported(g)) return false;
+  const PBuffer& cb = plan.bufs[C.buf];
+  std::vector<int> pd = {m, n};
+  if (cb.root && cb.root_index < static_cast<int>(opt.fresh_outputs.size()) && opt.fresh_outputs[cb.root_index] &&
+      output_identity(prog, cb.name) == 0 && first_writer(plan, step, C.buf) &&
+      covers_exactly(C.addr, pd, l.dims, cb.elements)) {
+    g.fresh = true;
+    l.fused_fill_root = cb.root_index;
+  }
+  l.gemm = g;
+  return true;
+}
+
 // K3e: a conv launch writing a per-point local accumulator T (scratch, zero-filled) whose
 // only consumer is the next phase  O = f(T, vec[k])  with f in the bias/ReLU family
 // (conv_relu.stripe after fuse+localize, test_passes.cpp:357-379): the epilogue applies f
@@ -514,6 +587,10 @@ void match_kernels(Plan* plan, const Program& p, const PlanOptions& opt) {
       st.launch.conv = cp;
       if (cp.fresh_output) st.launch.fused_fill_root = plan->bufs[cp.c_buf].root_index;
       fuse_conv_epilogue(plan, s, p, opt);
+      continue;
+    }
+    if (match_gemm(*plan, st.launch, p, opt, s)) {
+      st.launch.kernel = KernelKind::GemmI8TC;
       continue;
     }
     if (!why.empty())

@@ -61,7 +61,15 @@ struct PSpecial {
 };
 
 // Specialised kernel families the matcher can route a launch to.
-enum class KernelKind { Generic, ConvI8TC, Map, Reduce };
+enum class KernelKind { Generic, ConvI8TC, Map, Reduce, GemmI8TC };
+
+// tcgen05 GEMM (kernels/gemm_tc.cu): C[m,n] (+)= sum_k A[m,k] B[k,n], i8 operands.
+struct GemmPlan {
+  long long M = 0, N = 0, K = 0, lda = 0, ldb = 0, ldc = 0, a0 = 0, b0 = 0, c0 = 0;  // keep first, contiguous
+  bool b_kmajor = false, fresh = false;
+  DType c_dtype = DType::I32;
+  int a_buf = -1, b_buf = -1, c_buf = -1;
+};
 
 // Streaming reduce/copy ($v = load(I); O = store($v)): kernels/reduce.cu.
 struct ReducePlan {
@@ -120,6 +128,7 @@ struct PLaunch {
   KernelKind kernel = KernelKind::Generic;
   ConvPlan conv;
   ReducePlan reduce;
+  GemmPlan gemm;
   int fused_fill_root = -1;  // root buffer whose prepare_outputs fill this launch performs itself
   // map kernel (vectorised owner mode): vdim = thread dim split into kVec-lane vectors
   int vdim = -1;

@@ -180,3 +180,10 @@ def conv_bias_relu(N, H, W, C, K, tx=2, in_dtype="i8", acc_dtype="i32", out_dtyp
 	}}
 }}
 """
+
+
+def matmul_bt(M, N, K, in_dtype="i8", out_dtype="i32"):
+    """C[m,n] += A[m,k] * B[n,k] (B stored k-contiguous, i.e. transposed)."""
+    return matmul(M, N, K, in_dtype, out_dtype).replace(
+        f"in B[0, 0] {in_dtype}({K}, {N}):({N}, 1)", f"in B[0, 0] {in_dtype}({N}, {K}):({K}, 1)").replace(
+        f"in B[k, n] {in_dtype}(1, 1):({N}, 1)", f"in B[n, k] {in_dtype}(1, 1):({K}, 1)")

@@ -1,0 +1,67 @@
+"""tcgen05 GEMM path (kernels/gemm_tc.cu) vs the reference semantics, bit-exact."""
+import numpy as np
+import pytest
+
+from harness import gpu_available, run_device
+from oracle import Port, Ref, random_inputs
+from paper_1903_06498_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not gpu_available():
+        pytest.skip("no B200")
+
+
+def check(text, seed=3, provide_out=False):
+    import paper_1903_06498_b200 as sb
+    p = sb.parse_program(text)
+    assert "gemm_i8_tc" in p.describe_plan(not provide_out), p.describe_plan(True)
+    bufs = [(n, d.dtype, d.elements, int(d.dir)) for n, d in p.buffers.items()]
+    inp = {n: (p.buffers[n].dtype, a) for n, a in random_inputs(bufs, seed).items()}
+    if provide_out:
+        rng = np.random.default_rng(seed)
+        d = p.buffers["C"]
+        lim = 2 ** (d.dtype - 1)
+        inp["C"] = (d.dtype, rng.integers(-lim, lim, size=d.elements).astype(np.int64))
+    store = {n: a for n, (b, a) in inp.items()}
+    for n, d in p.buffers.items():
+        if n not in store:
+            store[n] = np.full(d.elements, p.output_identity(n), np.int64)
+    if Ref.available():
+        exp = {n: v[1] for n, v in Ref.execute(Ref.parse(text), {n: (p.buffers[n].dtype, a) for n, a in store.items()}).items()}
+    else:
+        exp = Port.execute(text, store)
+    got = run_device(text, inp)
+    np.testing.assert_array_equal(got["C"], exp["C"])
+
+
+@pytest.mark.parametrize("mnk", [(64, 64, 64), (256, 128, 512), (200, 176, 320), (130, 304, 48), (3, 16, 16)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_matmul_i8_to_i32(mnk):
+    check(W.matmul(*mnk, in_dtype="i8", out_dtype="i32"))
+
+
+@pytest.mark.parametrize("od", ["i8", "i16"])
+def test_matmul_narrow_outputs_wrap(od):
+    check(W.matmul(128, 128, 256, in_dtype="i8", out_dtype=od))
+
+
+def test_matmul_b_k_major():
+    check(W.matmul_bt(192, 160, 256))
+
+
+def test_matmul_accumulates_into_existing():
+    check(W.matmul(128, 256, 128, in_dtype="i8", out_dtype="i32"), provide_out=True)
+
+
+def test_matmul_config1_shape_exact():
+    """BASELINE config 1 shape (1024^3) in the i8 integer mode, checked against numpy int64."""
+    import paper_1903_06498_b200 as sb
+    rng = np.random.default_rng(1)
+    A = rng.integers(-128, 128, size=(1024, 1024)).astype(np.int64)
+    B = rng.integers(-128, 128, size=(1024, 1024)).astype(np.int64)
+    got = run_device(W.matmul(1024, 1024, 1024, "i8", "i32"), {"A": (8, A.ravel()), "B": (8, B.ravel())})
+    np.testing.assert_array_equal(got["C"].reshape(1024, 1024), A @ B)
