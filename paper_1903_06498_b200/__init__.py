@@ -203,7 +203,9 @@ def print_program(p: Program) -> str:
 
 @dataclass
 class Buffer:
-    """interp.h:14-17: dtype plus int64 carriers (values always wrapped to dtype)."""
+    """interp.h:14-17: dtype plus int64 carriers (values always wrapped to dtype).
+
+    f32 extension: an F32 buffer carries float32 values instead."""
     dtype: int
     data: np.ndarray
 
@@ -234,7 +236,12 @@ def prepare_outputs(program: Program, store: BufferStore) -> None:
     for name, decl in program.buffers.items():
         if decl.dir == Dir.In or name in store:
             continue
-        store[name] = Buffer(decl.dtype, np.full(decl.elements, program.output_identity(name), dtype=np.int64))
+        ident = program.output_identity(name)
+        if decl.dtype == SB_F32:  # f32 extension: identity returned as IEEE-754 bits
+            data = np.full(decl.elements, ident & 0xFFFFFFFF, dtype=np.uint32).view(np.float32)
+        else:
+            data = np.full(decl.elements, ident, dtype=np.int64)
+        store[name] = Buffer(decl.dtype, data)
 
 
 class Context:
@@ -269,6 +276,11 @@ class Context:
         opts = opts or ExecOptions()
         arrs, hb = [], []
         for name, buf in store.items():
+            if buf.dtype == SB_F32:  # f32 buffers travel as native float32 carriers
+                a = np.ascontiguousarray(buf.data, dtype=np.float32)
+                arrs.append(a)
+                hb.append(HostBuffer(name.encode(), SB_CARRIER_NATIVE, 0, a.ctypes.data, a.size))
+                continue
             a = np.ascontiguousarray(buf.data, dtype=np.int64)
             arrs.append(a)
             hb.append(HostBuffer(name.encode(), SB_CARRIER_I64, 0, a.ctypes.data, a.size))

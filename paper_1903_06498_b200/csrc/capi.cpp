@@ -274,7 +274,10 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
       t.elems[k] = plan.bufs[map[k]].elements;
       t.kind[k] = plan.bufs[map[k]].kind;
     }
-    if (l.kernel == sb::KernelKind::Map)
+    if (l.is_float)
+      cuda_check(sb::launch_generic_f32(st.d_descs + di, l.pcount, t, ctx->d_err, static_cast<int>(i), ctx->stream),
+                 "generic_f32");
+    else if (l.kernel == sb::KernelKind::Map)
       cuda_check(sb::launch_map(st.d_descs + di, l.vcount, t, ctx->d_err, static_cast<int>(i), ctx->stream), "map");
     else
       cuda_check(sb::launch_generic(st.d_descs + di, l.pcount, t, ctx->d_err, static_cast<int>(i), ctx->stream),

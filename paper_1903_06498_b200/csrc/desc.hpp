@@ -94,6 +94,7 @@ struct GenericDesc {
   std::int8_t vdim;
   std::int8_t vkind[kMaxAccess];  // 0 broadcast (coef 0), 1 contiguous aligned vector, 2 per-lane
   std::int64_t vcount;            // threads: pcount / range[vdim] * ceil(range[vdim] / kVec)
+  std::int8_t is_float;           // f32 numeric mode: temps, cells and aggregation in fp32
 };
 
 constexpr int kVec = 4;            // lanes per thread in the map kernel

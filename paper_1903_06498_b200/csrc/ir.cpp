@@ -261,9 +261,18 @@ std::int64_t output_identity(const Program& p, const std::string& name) {
     for (const auto& s : b->stmts)
       if (s.kind == StmtKind::Block) stack.push_back(s.block.get());
   }
+  if (is_float(root_ref->dtype)) {
+    // f32 extension: the identity's IEEE-754 bit pattern (-inf, +inf, 1.0f, 0.0f)
+    switch (agg) {
+      case Agg::Max: return static_cast<std::int32_t>(0xFF800000u);
+      case Agg::Min: return 0x7F800000;
+      case Agg::Mul: return 0x3F800000;
+      default: return 0;
+    }
+  }
   switch (agg) {
-    case Agg::Max: return is_float(root_ref->dtype) ? 0 : dtype_min(root_ref->dtype);
-    case Agg::Min: return is_float(root_ref->dtype) ? 0 : dtype_max(root_ref->dtype);
+    case Agg::Max: return dtype_min(root_ref->dtype);
+    case Agg::Min: return dtype_max(root_ref->dtype);
     case Agg::Mul: return 1;
     default: return 0;
   }

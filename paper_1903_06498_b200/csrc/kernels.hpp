@@ -10,6 +10,9 @@
 
 namespace sb {
 
+// fp32 numeric mode (kernels/generic_f32.cu)
+cudaError_t launch_generic_f32(const GenericDesc* d_desc, std::int64_t pcount, const BufTable& t, DevError* err,
+                               int launch_id, cudaStream_t s);
 cudaError_t launch_generic(const GenericDesc* d_desc, std::int64_t pcount, const BufTable& t,
                            DevError* err, int launch_id, cudaStream_t s);
 cudaError_t launch_fill(void* p, int kind, std::int64_t n, std::int64_t v, cudaStream_t s);

@@ -321,7 +321,7 @@ bool match_reduce(const Plan& plan, PLaunch& l, const Program& prog, const PlanO
 // (coefficient 1, everything else a multiple of kVec) or a per-lane gather.  Written
 // buffers must be aligned contiguous vectors so each thread owns whole vectors.
 bool match_map(PLaunch& l) {
-  if (l.mode != kModeOwner || l.pdims.empty() || !l.specials.empty()) return false;
+  if (l.is_float || l.mode != kModeOwner || l.pdims.empty() || !l.specials.empty()) return false;
   if (l.ntemps > kVecMaxTemps || l.ncells > kVecMaxCells || l.priv.size() > static_cast<std::size_t>(kVecMaxCells))
     return false;
   const int v = l.pdims[0];

@@ -119,6 +119,7 @@ struct PLaunch {
 
   // analysis (analyze())
   std::int8_t mode = kModeOwner;
+  bool is_float = false;  // f32 numeric mode (every data buffer F32)
   std::vector<int> pdims, rdims;
   std::vector<std::int8_t> acc_mode, acc_cell;
   int ncells = 0;

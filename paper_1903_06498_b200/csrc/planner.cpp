@@ -649,6 +649,20 @@ class Lowerer {
         l.acc_mode[i] = written.count(l.acc[i].buf) ? kAccDirect : kAccRead;
       l.pcount = 1;
     };
+    // numeric mode: a launch over F32 buffers runs in fp32 (generic_f32.cu); the
+    // integer semantics of interp.cpp never mix with it inside one launch
+    {
+      int nf = 0, ni = 0;
+      for (const auto& a : l.acc) {
+        const PBuffer& b = plan_->bufs[a.buf];
+        if (b.kind == kI64) continue;  // temp spill: carries either mode's value
+        (b.dtype == DType::F32 ? nf : ni)++;
+      }
+      for (const auto& pr : l.priv) (pr.second == DType::F32 ? nf : ni)++;
+      if (nf && ni) throw Error("Unsupported", "launch " + l.path + " mixes f32 and integer buffers");
+      l.is_float = nf > 0;
+      if (l.is_float && special) throw Error("Unsupported", "gather/scatter over f32 buffers");
+    }
     if (special) return serial("gather/scatter");
     // every access of a written buffer must use one address function
     std::map<int, int> rep;  // buf -> representative access
@@ -761,6 +775,7 @@ std::string Plan::describe() const {
     for (std::size_t i = 0; i < l.rdims.size(); i++) os << (i ? "," : "") << l.dims[l.rdims[i]].name;
     os << "] cons=" << l.cons.size() << " acc=" << l.acc.size() << " code=" << l.code.size()
        << " points=" << l.points;
+    if (l.is_float) os << " f32";
     if (!l.why.empty()) os << " why=\"" << l.why << "\"";
     os << "\n";
   }
@@ -804,6 +819,7 @@ void to_desc(const PLaunch& l, GenericDesc* d, std::vector<int>* bufmap) {
   d->vcount = l.vcount;
   for (std::size_t i = 0; i < l.vkind.size() && i < static_cast<std::size_t>(kMaxAccess); i++) d->vkind[i] = l.vkind[i];
   d->mode = l.mode;
+  d->is_float = l.is_float ? 1 : 0;
   d->npdims = static_cast<std::int8_t>(l.pdims.size());
   d->nrdims = static_cast<std::int8_t>(l.rdims.size());
   for (std::size_t i = 0; i < l.pdims.size(); i++) d->pdims[i] = static_cast<std::int8_t>(l.pdims[i]);
