@@ -212,7 +212,7 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
       continue;
     }
     const sb::PLaunch& l = s.launch;
-    if (l.kernel == sb::KernelKind::ConvI8TC) {
+    if (l.kernel == sb::KernelKind::ConvI8TC || l.kernel == sb::KernelKind::ConvIgemmTC) {
       sb::ConvArgs a;
       a.a = ptr_of(l.conv.a_buf);
       a.b = ptr_of(l.conv.b_buf);
@@ -225,7 +225,10 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
         a.vec = ptr_of(l.conv.vec_buf);
         a.vec_kind = plan.bufs[l.conv.vec_buf].kind;
       }
-      cuda_check(sb::launch_conv_tc(l.conv, a, ctx->stream, ctx->num_sms), "conv_tc");
+      if (l.kernel == sb::KernelKind::ConvI8TC)
+        cuda_check(sb::launch_conv_tc(l.conv, a, ctx->stream, ctx->num_sms), "conv_tc");
+      else
+        cuda_check(sb::launch_conv_igemm(l.conv, a, ctx->stream, ctx->num_sms), "conv_igemm");
       ctx->launches++;
       continue;
     }

@@ -56,5 +56,8 @@ struct ConvArgs {
 // Host-side checks that the plan fits the kernel's tiling; empty string = ok.
 const char* conv_tc_unsupported(const ConvPlan& cp);
 cudaError_t launch_conv_tc(const ConvPlan& cp, const ConvArgs& args, cudaStream_t s, int num_sms);
+// General im2col-TMA implicit GEMM (kernels/conv_igemm.cu): strides, 1x1, streamed filters.
+const char* conv_igemm_unsupported(const ConvPlan& cp);
+cudaError_t launch_conv_igemm(const ConvPlan& cp, const ConvArgs& args, cudaStream_t s, int num_sms);
 
 }  // namespace sb

@@ -1,0 +1,533 @@
+// General tcgen05 implicit-GEMM convolution (K3) for conv leaves the
+// resident-filter kernel (conv_tc.cu) does not take: strided convs, 1x1 convs, wide
+// filters that do not fit shared memory (3x3x512x512 = 2.4 MB), any output-channel count.
+//
+//     O[n, x, y, k] (+)= sum_{i, j, c} I[n, sx*x + i + ox, sy*y + j + oy, c] * F[i, j, k, c]
+//
+// GEMM view: M = output pixels in (n, x, y) order, N = output channels k, reduction =
+// (i, j, c).  The A operand is produced by TMA in im2col mode: one
+// cp.async.bulk.tensor.4d...im2col load brings 128 consecutive output pixels' input rows
+// for one filter tap (im2col offsets) and one 64/128-channel slice, walking (y, x, n) with
+// the conv strides and zero-filling the padding halo.  The Stripe constraints that skip
+// out-of-window taps (interp.cpp:426-428) become exactly that zero fill: a skipped point
+// contributes nothing to an add aggregation, a zero product contributes nothing either.
+// The filter B (k rows, c contiguous) streams through the same mbarrier ring.
+//
+// Warp roles as in gemm_tc.cu: warp 0 TMA producer, warp 1 single-thread
+// tcgen05.mma.kind::i8 issuer (M=128, N=128, K=32 per instruction), warps 2-5 epilogue
+// (tcgen05.ld -> 128B-swizzled staging -> TMA tensor store, or read-modify-write).
+// Double-buffered TMEM accumulators let the epilogue of tile t overlap the MMAs of t+1.
+// Exactness: s32 accumulation with R*S*C*128*128 < 2^31 (planner check).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../kernels.hpp"
+
+namespace sb {
+namespace {
+
+constexpr int kThreads = 192;
+constexpr int BM = 128, BN = 128;
+constexpr int kRingBytes = 128 * 1024;  // A+B stage ring
+
+struct IgKParams {
+  int M, N;           // GEMM rows (output pixels) and cols (output channels)
+  int P, Q;           // output rows / cols per image (x, y extents)
+  int sx, sy;         // conv strides (traversal strides of the im2col map)
+  int lower_h, lower_w;
+  int S, cblocks, kblocks;
+  int tiles_m, tiles_n;
+  int bk, stages;     // channels per k-block (64 or 128), ring depth
+  int fresh, tma_out, out_kind;
+  void* c;
+  long long ldc;      // elements between consecutive output pixels
+  std::uint32_t idesc, desc_hi;
+  int pdl;
+  // fused epilogue: out = wrap(max(acc + vec[k], lo))
+  int epi, epi_vec, epi_lo, vec_kind;
+  const void* vec;
+  long long vec_k;
+  long long lo;
+};
+
+__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
+  return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(std::uint64_t* bar, std::uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, std::uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(std::uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(std::uint64_t* bar, std::uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_im2col(std::uint32_t dst, const CUtensorMap* map, std::uint64_t* bar, int c,
+                                                int w, int h, int n, std::uint16_t ow, std::uint16_t oh) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(dst),
+      "l"(reinterpret_cast<std::uint64_t>(map)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ow), "h"(oh)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(std::uint32_t dst, const CUtensorMap* map, std::uint64_t* bar, int c0,
+                                            int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::
+          "r"(dst),
+      "l"(reinterpret_cast<std::uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void umma_i8(std::uint32_t d, std::uint32_t a_lo, std::uint32_t a_hi, std::uint32_t b_lo,
+                                        std::uint32_t b_hi, std::uint32_t idesc, std::uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 da, db;\n\t"
+      "mov.b64 da, {%1, %2};\n\t"
+      "mov.b64 db, {%3, %4};\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], da, db, %5, p;\n\t}" ::"r"(d),
+      "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(std::uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld32(std::uint32_t taddr, std::uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// fused epilogue on the exact s32 accumulator: int64 arithmetic (the reference's temps),
+// wrapped to the output dtype by the store
+__device__ __forceinline__ std::uint32_t epi_value(const IgKParams& p, int k, std::uint32_t acc) {
+  long long v = static_cast<std::int32_t>(acc);
+  if (p.epi_vec) {
+    long long vi = static_cast<long long>(k) * p.vec_k;
+    v += p.vec_kind == kI8 ? static_cast<const std::int8_t*>(p.vec)[vi]
+         : p.vec_kind == kI16 ? static_cast<const std::int16_t*>(p.vec)[vi]
+                              : static_cast<const std::int32_t*>(p.vec)[vi];
+  }
+  if (p.epi_lo && v < p.lo) v = p.lo;
+  return static_cast<std::uint32_t>(v);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_igemm_i8_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
+                         const __grid_constant__ CUtensorMap cmap, const IgKParams p) {
+  extern __shared__ __align__(1024) std::uint8_t smem_raw[];
+  std::uint8_t* base =
+      reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t{1023});
+  const std::uint32_t stage_a = BM * p.bk, stage_b = BN * p.bk;
+  std::uint8_t* ring = base;                    // stages x (A | B)
+  std::uint8_t* stg = ring + kRingBytes;        // 64 KB output staging (4 x 16 KB column quarters)
+  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(stg + BM * BN * 4);
+  std::uint64_t* full = bars;
+  std::uint64_t* empty = bars + 16;
+  std::uint64_t* tfull = bars + 32;
+  std::uint64_t* tempty = bars + 34;
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 36);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int tiles = p.tiles_m * p.tiles_n;
+  const int stages = p.stages;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; a++) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const std::uint32_t tmem_base = *tmem_slot;
+  if (p.pdl && threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+  if (warp == 0) {
+    if (lane == 0) {
+      if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+      const int PQ = p.P * p.Q;
+      int stage = 0;
+      std::uint32_t phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        // n-tiles of one m-tile are adjacent in t: the A strip stays hot in L2
+        const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * BN;
+        const int img = m0 / PQ, rem = m0 - img * PQ;
+        const int ox = rem / p.Q, oy = rem - ox * p.Q;
+        const int h0 = p.lower_h + ox * p.sx, w0 = p.lower_w + oy * p.sy;
+        int cb = 0, tap = 0;
+        for (int kb = 0; kb < p.kblocks; kb++) {
+          const int r = tap / p.S, s = tap - r * p.S;
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], stage_a + stage_b);
+          const std::uint32_t sa = smem_u32(ring + stage * (stage_a + stage_b));
+          tma_load_im2col(sa, &amap, &full[stage], cb * p.bk, w0, h0, img, static_cast<std::uint16_t>(s),
+                          static_cast<std::uint16_t>(r));
+          tma_load_4d(sa + stage_a, &bmap, &full[stage], cb * p.bk, n0, s, r);
+          if (++cb == p.cblocks) {
+            cb = 0;
+            tap++;
+          }
+          if (++stage == stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0, iter = 0;
+      std::uint32_t phase = 0;
+      const int ksteps = p.bk / 32;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, iter++) {
+        const int acc = iter & 1;
+        mbar_wait(&tempty[acc], ((iter >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const std::uint32_t d = tmem_base + static_cast<std::uint32_t>(acc * BN);
+        for (int kb = 0; kb < p.kblocks; kb++) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const std::uint32_t sa = smem_u32(ring + stage * (stage_a + stage_b));
+          const std::uint32_t a_lo = (sa >> 4) | (1u << 16);
+          const std::uint32_t b_lo = ((sa + stage_a) >> 4) | (1u << 16);
+          for (int ks = 0; ks < ksteps; ks++)  // +32 bytes along the K-major rows
+            umma_i8(d, a_lo + ks * 2, p.desc_hi, b_lo + ks * 2, p.desc_hi, p.idesc, (kb | ks) != 0);
+          umma_commit(&empty[stage]);
+          if (++stage == stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const bool leader = threadIdx.x == 64;
+    int iter = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, iter++) {
+      const int acc = iter & 1;
+      const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * BN;
+      if (p.tma_out) {
+        if (leader) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+      mbar_wait(&tfull[acc], (iter >> 1) & 1);
+      tc_fence_after();
+      const int m = m0 + row;
+      for (int h = 0; h < BN / 32; h++) {
+        std::uint32_t v[32];
+        tmem_ld32(tmem_base + (static_cast<std::uint32_t>(quarter * 32) << 16) +
+                      static_cast<std::uint32_t>(acc * BN + h * 32),
+                  v);
+        const int kbase = n0 + h * 32;
+        if (p.epi) {
+#pragma unroll
+          for (int q = 0; q < 32; q++)
+            if (kbase + q < p.N) v[q] = epi_value(p, kbase + q, v[q]);
+        }
+        if (p.tma_out) {
+          std::uint32_t rbase = smem_u32(stg + h * 16384 + row * 128);
+#pragma unroll
+          for (int q = 0; q < 8; q++)
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rbase + ((q ^ (row & 7)) << 4)),
+                         "r"(v[4 * q]), "r"(v[4 * q + 1]), "r"(v[4 * q + 2]), "r"(v[4 * q + 3]));
+        } else if (m < p.M) {
+          const long long rowbase = static_cast<long long>(m) * p.ldc;
+          if (p.fresh && p.out_kind == kI8 && kbase + 32 <= p.N &&
+              (reinterpret_cast<std::uintptr_t>(p.c) + rowbase + kbase) % 16 == 0) {
+            // packed: 32 wrapped bytes as two 16-byte stores
+            std::uint32_t w[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++)
+              w[q] = (v[4 * q] & 0xFF) | ((v[4 * q + 1] & 0xFF) << 8) | ((v[4 * q + 2] & 0xFF) << 16) |
+                     (v[4 * q + 3] << 24);
+            uint4* o = reinterpret_cast<uint4*>(static_cast<std::int8_t*>(p.c) + rowbase + kbase);
+            o[0] = make_uint4(w[0], w[1], w[2], w[3]);
+            o[1] = make_uint4(w[4], w[5], w[6], w[7]);
+          } else {
+            for (int q = 0; q < 32; q++) {
+              const int n = kbase + q;
+              if (n >= p.N) break;
+              const long long idx = rowbase + n;
+              if (p.out_kind == kI32) {
+                std::int32_t* o = static_cast<std::int32_t*>(p.c) + idx;
+                *o = static_cast<std::int32_t>(p.fresh ? v[q] : static_cast<std::uint32_t>(*o) + v[q]);
+              } else if (p.out_kind == kI16) {
+                std::int16_t* o = static_cast<std::int16_t*>(p.c) + idx;
+                *o = static_cast<std::int16_t>(p.fresh ? v[q] : static_cast<std::uint32_t>(*o) + v[q]);
+              } else {
+                std::int8_t* o = static_cast<std::int8_t*>(p.c) + idx;
+                *o = static_cast<std::int8_t>(p.fresh ? v[q] : static_cast<std::uint32_t>(*o) + v[q]);
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (p.tma_out) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (leader) {
+          for (int h = 0; h < BN / 32; h++)
+            if (n0 + h * 32 < p.N)
+              asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                               reinterpret_cast<std::uint64_t>(&cmap)),
+                           "r"(smem_u32(stg + h * 16384)), "r"(n0 + h * 32), "r"(m0)
+                           : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      }
+    }
+    if (p.tma_out && leader) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(256));
+  }
+}
+
+template <class F>
+F driver_fn(const char* name) {
+  cudaDriverEntryPointQueryResult q;
+  void* f = nullptr;
+  if (cudaGetDriverEntryPoint(name, &f, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess)
+    return reinterpret_cast<F>(f);
+  return nullptr;
+}
+
+constexpr std::size_t kSmem = 1024 + kRingBytes + BM * BN * 4 + 512;
+
+struct Geometry {
+  std::int64_t Hin, Win;       // input window extents (tensor map dims)
+  int lower_h, lower_w, upper_h, upper_w;
+  int bk;
+};
+
+bool geometry(const ConvPlan& cp, Geometry* g) {
+  g->Hin = cp.u_hi - cp.u_lo + 1;
+  g->Win = cp.v_hi - cp.v_lo + 1;
+  // the window origin of output x is u = sx*x (+ tap i); relative to the map origin u_lo
+  g->lower_h = static_cast<int>(-cp.u_lo);
+  g->lower_w = static_cast<int>(-cp.v_lo);
+  g->upper_h = static_cast<int>(cp.sx * (cp.H - 1) - cp.u_lo - (g->Hin - 1));
+  g->upper_w = static_cast<int>(cp.sy * (cp.W - 1) - cp.v_lo - (g->Win - 1));
+  g->bk = cp.C % 128 == 0 ? 128 : 64;
+  auto corner = [](std::int64_t v) { return v >= -128 && v <= 127; };
+  return corner(-cp.u_lo) && corner(-cp.v_lo) && corner(cp.sx * (cp.H - 1) - cp.u_lo - (g->Hin - 1)) &&
+         corner(cp.sy * (cp.W - 1) - cp.v_lo - (g->Win - 1));
+}
+
+struct Prepared {
+  ConvPlan cp;
+  const void *a, *b, *vec;
+  void* c;
+  IgKParams kp;
+  CUtensorMap amap, bmap, cmap;
+};
+
+std::mutex g_mu;
+std::vector<Prepared>* g_prep = nullptr;
+
+bool same(const ConvPlan& x, const ConvPlan& y) {
+  return x.N == y.N && x.H == y.H && x.W == y.W && x.C == y.C && x.K == y.K && x.R == y.R && x.S == y.S &&
+         x.sx == y.sx && x.sy == y.sy && x.a_n == y.a_n && x.a_x == y.a_x && x.a_y == y.a_y && x.a0 == y.a0 &&
+         x.u_lo == y.u_lo && x.u_hi == y.u_hi && x.v_lo == y.v_lo && x.v_hi == y.v_hi && x.b_i == y.b_i &&
+         x.b_j == y.b_j && x.b_k == y.b_k && x.b0 == y.b0 && x.c_n == y.c_n && x.c_x == y.c_x && x.c_y == y.c_y &&
+         x.c0 == y.c0 && x.c_dtype == y.c_dtype && x.fresh_output == y.fresh_output && x.epi == y.epi &&
+         x.epi_vec == y.epi_vec && x.epi_lo == y.epi_lo && x.vec_k == y.vec_k && x.vec_c == y.vec_c && x.lo == y.lo;
+}
+
+int kind_of(DType d) { return d == DType::I8 ? kI8 : d == DType::I16 ? kI16 : kI32; }
+
+cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
+  out->cp = cp;
+  out->a = args.a;
+  out->b = args.b;
+  out->c = args.c;
+  out->vec = args.vec;
+  auto enc_tiled = driver_fn<PFN_cuTensorMapEncodeTiled_v12000>("cuTensorMapEncodeTiled");
+  auto enc_im2col = driver_fn<PFN_cuTensorMapEncodeIm2col_v12000>("cuTensorMapEncodeIm2col");
+  if (!enc_tiled || !enc_im2col) return cudaErrorNotSupported;
+  Geometry g;
+  if (!geometry(cp, &g)) return cudaErrorNotSupported;
+  IgKParams& kp = out->kp;
+  std::memset(&kp, 0, sizeof(kp));
+  kp.M = static_cast<int>(cp.N * cp.H * cp.W);
+  kp.N = static_cast<int>(cp.K);
+  kp.P = static_cast<int>(cp.H);
+  kp.Q = static_cast<int>(cp.W);
+  kp.sx = static_cast<int>(cp.sx);
+  kp.sy = static_cast<int>(cp.sy);
+  kp.lower_h = g.lower_h;
+  kp.lower_w = g.lower_w;
+  kp.S = static_cast<int>(cp.S);
+  kp.bk = g.bk;
+  kp.cblocks = static_cast<int>(cp.C / g.bk);
+  kp.kblocks = static_cast<int>(cp.R * cp.S) * kp.cblocks;
+  kp.stages = static_cast<int>(kRingBytes / (2 * BM * g.bk));
+  kp.tiles_m = (kp.M + BM - 1) / BM;
+  kp.tiles_n = (kp.N + BN - 1) / BN;
+  kp.fresh = cp.fresh_output ? 1 : 0;
+  kp.out_kind = kind_of(cp.c_dtype);
+  kp.ldc = cp.c_y;
+  const int ob = kp.out_kind == kI8 ? 1 : kp.out_kind == kI16 ? 2 : 4;
+  kp.c = static_cast<char*>(args.c) + cp.c0 * ob;
+  kp.epi = cp.epi ? 1 : 0;
+  kp.epi_vec = cp.epi_vec ? 1 : 0;
+  kp.epi_lo = cp.epi_lo ? 1 : 0;
+  kp.lo = cp.lo;
+  kp.vec_k = cp.vec_k;
+  kp.vec_kind = args.vec_kind;
+  if (cp.epi_vec) {
+    const int vb = args.vec_kind == kI8 ? 1 : args.vec_kind == kI16 ? 2 : 4;
+    kp.vec = static_cast<const char*>(args.vec) + cp.vec_c * vb;
+  }
+  kp.tma_out = kp.fresh && kp.out_kind == kI32 && (kp.ldc * 4) % 16 == 0 &&
+               reinterpret_cast<std::uintptr_t>(kp.c) % 16 == 0;
+  // idesc: S32 accumulate, signed A/B, both K-major, N = 128, M = 128
+  kp.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+  // descriptor high word: SBO = 8 rows x row bytes, version 1, swizzle 128B (2) / 64B (4)
+  kp.desc_hi = g.bk == 128 ? ((1024u >> 4) | (1u << 14) | (2u << 29)) : ((512u >> 4) | (1u << 14) | (4u << 29));
+  const CUtensorMapSwizzle sw = g.bk == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+
+  // A: im2col over (c, v, u, n) from the window corner (u_lo, v_lo)
+  const std::int8_t* abase = static_cast<const std::int8_t*>(args.a) + cp.a0 + cp.a_x * cp.u_lo + cp.a_y * cp.v_lo;
+  if (reinterpret_cast<std::uintptr_t>(abase) % 16) return cudaErrorMisalignedAddress;
+  cuuint64_t adim[4] = {static_cast<cuuint64_t>(cp.C), static_cast<cuuint64_t>(g.Win), static_cast<cuuint64_t>(g.Hin),
+                        static_cast<cuuint64_t>(cp.N)};
+  cuuint64_t astr[3] = {static_cast<cuuint64_t>(cp.a_y), static_cast<cuuint64_t>(cp.a_x),
+                        static_cast<cuuint64_t>(cp.a_n)};
+  int lower[2] = {g.lower_h, g.lower_w};  // {H, W}
+  int upper[2] = {g.upper_h, g.upper_w};
+  cuuint32_t aes[4] = {1, static_cast<cuuint32_t>(cp.sy), static_cast<cuuint32_t>(cp.sx), 1};
+  if (enc_im2col(&out->amap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<std::int8_t*>(abase), adim, astr, lower,
+                 upper, static_cast<cuuint32_t>(g.bk), BM, aes, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  // B: filter as (c, k, j, i), box (bk, 128, 1, 1)
+  const std::int8_t* bbase = static_cast<const std::int8_t*>(args.b) + cp.b0;
+  if (reinterpret_cast<std::uintptr_t>(bbase) % 16) return cudaErrorMisalignedAddress;
+  cuuint64_t bdim[4] = {static_cast<cuuint64_t>(cp.C), static_cast<cuuint64_t>(cp.K), static_cast<cuuint64_t>(cp.S),
+                        static_cast<cuuint64_t>(cp.R)};
+  cuuint64_t bstr[3] = {static_cast<cuuint64_t>(cp.b_k), static_cast<cuuint64_t>(cp.S > 1 ? cp.b_j : cp.b_k * cp.K),
+                        static_cast<cuuint64_t>(cp.R > 1 ? cp.b_i : cp.b_k * cp.K * cp.S)};
+  cuuint32_t bbox[4] = {static_cast<cuuint32_t>(g.bk), BN, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  if (enc_tiled(&out->bmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<std::int8_t*>(bbase), bdim, bstr, bbox, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  std::memset(&out->cmap, 0, sizeof(out->cmap));
+  if (kp.tma_out) {
+    cuuint64_t cdim[2] = {static_cast<cuuint64_t>(kp.N), static_cast<cuuint64_t>(kp.M)};
+    cuuint64_t cstr[1] = {static_cast<cuuint64_t>(kp.ldc * 4)};
+    cuuint32_t cbox[2] = {32, BM};
+    if (enc_tiled(&out->cmap, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, kp.c, cdim, cstr, cbox, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(conv_igemm_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kSmem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace
+
+const char* conv_igemm_unsupported(const ConvPlan& cp) {
+  Geometry g;
+  if (!geometry(cp, &g)) return "padding halo outside the im2col corner range";
+  if (cp.C % 64 != 0) return "channels not a multiple of 64";
+  if (cp.sx < 1 || cp.sx > 8 || cp.sy < 1 || cp.sy > 8) return "stride outside [1, 8]";
+  if (cp.R > 16 || cp.S > 16) return "filter taps beyond 16";
+  if (cp.a_y % 16 || cp.a_x % 16 || cp.a_n % 16) return "input strides not 16-byte multiples";
+  if (cp.b_c != 1 || cp.b_k % 16 || (cp.S > 1 && cp.b_j % 16) || (cp.R > 1 && cp.b_i % 16) || cp.b0 % 16)
+    return "filter layout not channel-contiguous with 16-byte aligned rows";
+  if (cp.N * cp.H * cp.W >= (1ll << 31) || cp.K >= (1 << 20)) return "extent too large";
+  // output rows must follow the (n, x, y) pixel order with a uniform pitch
+  if (cp.c_y < cp.K || (cp.H > 1 && cp.c_x != cp.W * cp.c_y) || (cp.N > 1 && cp.c_n != cp.H * cp.W * cp.c_y))
+    return "output not pixel-major";
+  if (cp.R * cp.S * cp.C * 128 * 128 >= (1ll << 31)) return "reduction too long for exact s32 accumulation";
+  return nullptr;
+}
+
+cudaError_t launch_conv_igemm(const ConvPlan& cp, const ConvArgs& args, cudaStream_t s, int num_sms) {
+  Prepared* pr = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(g_mu);
+    if (!g_prep) g_prep = new std::vector<Prepared>();
+    for (auto& e : *g_prep)
+      if (e.a == args.a && e.b == args.b && e.c == args.c && e.vec == args.vec && same(e.cp, cp)) pr = &e;
+    if (!pr) {
+      if (g_prep->size() >= 512) g_prep->clear();
+      Prepared fresh;
+      cudaError_t err = prepare(cp, args, &fresh);
+      if (err != cudaSuccess) return err;
+      g_prep->push_back(fresh);
+      pr = &g_prep->back();
+    }
+  }
+  IgKParams kp = pr->kp;
+  kp.pdl = 1;
+  const int tiles = kp.tiles_m * kp.tiles_n;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(tiles < num_sms ? tiles : num_sms));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, conv_igemm_i8_kernel, pr->amap, pr->bmap, pr->cmap, kp);
+}
+
+}  // namespace sb

@@ -85,10 +85,23 @@ bool match_conv(const Plan& plan, const PLaunch& l, const Program& prog, const P
   int ydim = mdims[0];
   int xdim = mdims.size() > 1 ? mdims[1] : -1;
   int ndim = mdims.size() > 2 ? mdims[2] : -1;
+  // taps: the smaller A coefficient pairs with y (j), the other with x (i); a spatial
+  // coefficient that is s times its tap's is a stride-s conv (s in [1, 8])
   int idim = -1, jdim = -1;
-  for (int t : taps) {
-    if (A->addr.at(t) == A->addr.at(ydim) && jdim < 0) jdim = t;
-    else if (xdim >= 0 && A->addr.at(t) == A->addr.at(xdim) && idim < 0) idim = t;
+  std::sort(taps.begin(), taps.end(), [&](int a, int b) { return A->addr.at(a) < A->addr.at(b); });
+  auto stride_of = [&](int sp, int tp) -> std::int64_t {
+    if (sp < 0 || tp < 0) return 0;
+    std::int64_t a = A->addr.at(sp), t = A->addr.at(tp);
+    if (t <= 0 || a % t != 0 || a / t < 1 || a / t > 8) return 0;
+    return a / t;
+  };
+  if (taps.size() == 2) {
+    jdim = taps[0];
+    idim = taps[1];
+    if (!stride_of(ydim, jdim) || !stride_of(xdim, idim)) return false;
+  } else if (taps.size() == 1) {
+    if (stride_of(ydim, taps[0])) jdim = taps[0];
+    else if (stride_of(xdim, taps[0])) idim = taps[0];
     else return false;
   }
   // with a single M dim that has a tap but no batch: fine; taps must pair
@@ -110,9 +123,11 @@ bool match_conv(const Plan& plan, const PLaunch& l, const Program& prog, const P
   c.K = range(kdim);
   c.R = range(idim);
   c.S = range(jdim);
+  c.sx = idim >= 0 ? stride_of(xdim, idim) : 1;
+  c.sy = jdim >= 0 ? stride_of(ydim, jdim) : 1;
   c.a_n = coef(A, ndim);
-  c.a_x = coef(A, xdim);
-  c.a_y = coef(A, ydim);
+  c.a_x = idim >= 0 ? coef(A, idim) : coef(A, xdim);  // one input row
+  c.a_y = jdim >= 0 ? coef(A, jdim) : coef(A, ydim);  // one input pixel
   c.a0 = A->addr.c;
   if (c.a_n == 0) c.a_n = std::max<std::int64_t>(16, (c.a_x ? c.a_x : c.a_y) * 1024);  // unused (N == 1)
   if (c.a_x == 0) c.a_x = std::max<std::int64_t>(16, c.a_y * c.W * 4);                // unused (H == 1)
@@ -125,25 +140,28 @@ bool match_conv(const Plan& plan, const PLaunch& l, const Program& prog, const P
   c.c_x = coef(&C, xdim);
   c.c_y = coef(&C, ydim);
   c.c0 = C.addr.c;
-  // valid input window: u = x + i in [u_lo, u_hi], v = y + j in [v_lo, v_hi]
+  // valid input window: u = sx*x + i in [u_lo, u_hi], v = sy*y + j in [v_lo, v_hi]
   c.u_lo = 0;
-  c.u_hi = c.H - 1 + c.R - 1;
+  c.u_hi = c.sx * (c.H - 1) + c.R - 1;
   c.v_lo = 0;
-  c.v_hi = c.W - 1 + c.S - 1;
+  c.v_hi = c.sy * (c.W - 1) + c.S - 1;
   for (const auto& con : l.cons) {
     int used = 0;
     for (int d = 0; d < nd; d++) used += con.uses(d) ? 1 : 0;
-    std::int64_t ax = con.at(xdim < 0 ? 0 : xdim), ai = idim < 0 ? 0 : con.at(idim);
-    std::int64_t ay = con.at(ydim), aj = jdim < 0 ? 0 : con.at(jdim);
-    bool on_u = xdim >= 0 && ax != 0 && (idim < 0 ? used == 1 : (ai == ax && used == 2));
-    bool on_v = ay != 0 && (jdim < 0 ? used == 1 : (aj == ay && used == 2));
-    if (xdim < 0) ax = 0;
-    if (on_u && (ax == 1 || ax == -1)) {
-      // ax*(x+i) + c >= 0
-      if (ax == 1) c.u_lo = std::max(c.u_lo, -con.c);
+    // unit coefficient of u (resp. v) in the constraint: the tap's, or the spatial one
+    std::int64_t cx = xdim < 0 ? 0 : con.at(xdim), ci = idim < 0 ? 0 : con.at(idim);
+    std::int64_t cy = con.at(ydim), cj = jdim < 0 ? 0 : con.at(jdim);
+    std::int64_t au = idim >= 0 ? ci : cx, av = jdim >= 0 ? cj : cy;
+    bool on_u = xdim >= 0 && cx != 0 && (au == 1 || au == -1) && cx == c.sx * au &&
+                used == (idim >= 0 ? 2 : 1) && (idim < 0 || ci != 0);
+    bool on_v = cy != 0 && (av == 1 || av == -1) && cy == c.sy * av && used == (jdim >= 0 ? 2 : 1) &&
+                (jdim < 0 || cj != 0);
+    if (on_u) {
+      // au*u + c >= 0
+      if (au == 1) c.u_lo = std::max(c.u_lo, -con.c);
       else c.u_hi = std::min(c.u_hi, con.c);
-    } else if (on_v && (ay == 1 || ay == -1)) {
-      if (ay == 1) c.v_lo = std::max(c.v_lo, -con.c);
+    } else if (on_v) {
+      if (av == 1) c.v_lo = std::max(c.v_lo, -con.c);
       else c.v_hi = std::min(c.v_hi, con.c);
     } else {
       *why = "constraint is not an interval on an input coordinate";
@@ -195,11 +213,6 @@ bool match_conv(const Plan& plan, const PLaunch& l, const Program& prog, const P
         if (ps.launch.acc[sp.dst].buf == c.b_buf) written = true;
     }
     c.b_immutable = bb.root && bb.dir == Dir::In && !written;
-  }
-  const char* bad = conv_tc_unsupported(c);
-  if (bad) {
-    *why = bad;
-    return false;
   }
   *cp = c;
   return true;
@@ -424,11 +437,11 @@ bool match_gemm(const Plan& plan, PLaunch& l, const Program& prog, const PlanOpt
 // only consumer is the next phase  O = f(T, vec[k])  with f in the bias/ReLU family
 // (conv_relu.stripe after fuse+localize, test_passes.cpp:357-379): the epilogue applies f
 // on the s32 accumulator and writes O directly; T never reaches HBM.
-void fuse_conv_epilogue(Plan* plan, std::size_t s, const Program& prog, const PlanOptions& opt) {
+bool fuse_conv_epilogue(Plan* plan, std::size_t s, const Program& prog, const PlanOptions& opt) {
   PLaunch& cl = plan->steps[s].launch;
   ConvPlan& c = cl.conv;
   const int T = c.c_buf;
-  if (plan->bufs[T].root || c.fresh_output) return;
+  if (plan->bufs[T].root || c.fresh_output) return false;
   // T is touched only by: one zero Fill before s, the conv, and the consumer s2 after s
   int fill_step = -1, s2 = -1;
   for (std::size_t k = 0; k < plan->steps.size(); k++) {
@@ -437,28 +450,28 @@ void fuse_conv_epilogue(Plan* plan, std::size_t s, const Program& prog, const Pl
     bool touches = false;
     if (ps.kind == PStep::Fill) {
       if (ps.buf == T) {
-        if (k > s || ps.value != 0 || fill_step >= 0) return;
+        if (k > s || ps.value != 0 || fill_step >= 0) return false;
         fill_step = static_cast<int>(k);
       }
       continue;
     }
     for (const auto& a : ps.launch.acc) touches |= a.buf == T;
     if (!touches) continue;
-    if (k < s || s2 >= 0) return;
+    if (k < s || s2 >= 0) return false;
     s2 = static_cast<int>(k);
   }
-  if (fill_step < 0 || s2 < 0) return;
+  if (fill_step < 0 || s2 < 0) return false;
   for (std::size_t k = s + 1; k < static_cast<std::size_t>(s2); k++)  // nothing in between
-    if (!plan->steps[k].elided) return;
+    if (!plan->steps[k].elided) return false;
   PLaunch& el = plan->steps[s2].launch;
-  if (el.mode != kModeOwner || !el.cons.empty() || !el.priv.empty() || el.has_spill || !el.specials.empty()) return;
+  if (el.mode != kModeOwner || !el.cons.empty() || !el.priv.empty() || el.has_spill || !el.specials.empty()) return false;
   // T must be dense [n][x][y][k] for the conv and read back at the same element
   const std::int64_t K = c.K, HW = c.H * c.W, NHW = c.N * HW;
-  if (!(c.c0 == 0 && c.c_y == K && (c.H == 1 || c.c_x == c.W * K) && (c.N == 1 || c.c_n == HW * K))) return;
-  if (el.dims.size() != 2) return;
+  if (!(c.c0 == 0 && c.c_y == K && (c.H == 1 || c.c_x == c.W * K) && (c.N == 1 || c.c_n == HW * K))) return false;
+  if (el.dims.size() != 2) return false;
   int pd = -1, kd = -1;
   for (int d = 0; d < 2; d++) (el.dims[d].range == K ? kd : pd) = d;
-  if (pd < 0 || kd < 0 || el.dims[pd].range != NHW) return;
+  if (pd < 0 || kd < 0 || el.dims[pd].range != NHW) return false;
   // symbolic evaluation of the body: each temp is ACC, VEC (per-k vector), CONST or an op on them
   struct Sym {
     int kind = -1;  // 0 ACC, 1 VEC, 2 CONST, 3 ADD(a,b), 4 MAX(a,b)
@@ -468,6 +481,7 @@ void fuse_conv_epilogue(Plan* plan, std::size_t s, const Program& prog, const Pl
   std::vector<Sym> nodes;
   std::vector<int> temp(el.ntemps, -1);
   int vec_acc = -1, out_acc = -1, out_node = -1;
+  DInstr store_ins{};
   auto operand = [&](int x) -> int {
     if (x >= 0) return temp[x];
     Sym s;
@@ -481,39 +495,41 @@ void fuse_conv_epilogue(Plan* plan, std::size_t s, const Program& prog, const Pl
     if (ins.op == kOpLoad) {
       const PAccess& a = el.acc[ins.acc];
       if (a.buf == T) {
-        if (!(a.addr.c == 0 && a.addr.at(pd) == K && a.addr.at(kd) == 1)) return;
+        if (!(a.addr.c == 0 && a.addr.at(pd) == K && a.addr.at(kd) == 1)) return false;
         s.kind = 0;
       } else {
-        if (a.addr.at(pd) != 0 || el.acc_mode[ins.acc] != kAccRead) return;
-        if (vec_acc >= 0 && !(el.acc[vec_acc].buf == a.buf && el.acc[vec_acc].addr == a.addr)) return;
+        if (a.addr.at(pd) != 0 || el.acc_mode[ins.acc] != kAccRead) return false;
+        if (vec_acc >= 0 && !(el.acc[vec_acc].buf == a.buf && el.acc[vec_acc].addr == a.addr)) return false;
         vec_acc = ins.acc;
         s.kind = 1;
       }
     } else if (ins.op == kOpConst) {
       int o = operand(ins.a);
-      if (o < 0) return;
+      if (o < 0) return false;
       temp[ins.dst] = o;
       continue;
     } else if (ins.op == kOpAdd || ins.op == kOpMax) {
       s.kind = ins.op == kOpAdd ? 3 : 4;
       s.a = operand(ins.a);
       s.b = operand(ins.b);
-      if (s.a < 0 || s.b < 0) return;
+      if (s.a < 0 || s.b < 0) return false;
     } else if (ins.op == kOpStore) {
-      if (out_acc >= 0) return;
+      if (out_acc >= 0) return false;
       out_acc = ins.acc;
+      store_ins = ins;
       out_node = temp[ins.a];
-      if (out_node < 0) return;
-      if (static_cast<DType>(ins.dtype) != DType::I32) return;  // TMA-store epilogue writes i32
-      if (ins.agg != static_cast<std::int8_t>(Agg::Assign) && ins.agg != static_cast<std::int8_t>(Agg::Add)) return;
+      if (out_node < 0) return false;
+      // the resident-filter kernel's TMA-store epilogue writes i32; the im2col one any width
+      if (static_cast<DType>(ins.dtype) != DType::I32 && cl.kernel != KernelKind::ConvIgemmTC) return false;
+      if (ins.agg != static_cast<std::int8_t>(Agg::Assign) && ins.agg != static_cast<std::int8_t>(Agg::Add)) return false;
       continue;
     } else {
-      return;
+      return false;
     }
     nodes.push_back(s);
     temp[ins.dst] = static_cast<int>(nodes.size()) - 1;
   }
-  if (out_acc < 0) return;
+  if (out_acc < 0) return false;
   // match out = MAX(x, CONST) | x ;  x = ADD(ACC, VEC) | ADD(VEC, ACC) | ACC
   ConvPlan e = c;
   int n = out_node;
@@ -521,7 +537,7 @@ void fuse_conv_epilogue(Plan* plan, std::size_t s, const Program& prog, const Pl
   if (nodes[n].kind == 4) {
     int a = nodes[n].a, b = nodes[n].b;
     if (nodes[b].kind != 2) std::swap(a, b);
-    if (nodes[b].kind != 2) return;
+    if (nodes[b].kind != 2) return false;
     e.epi_lo = true;
     e.lo = nodes[b].c;
     n = a;
@@ -530,29 +546,31 @@ void fuse_conv_epilogue(Plan* plan, std::size_t s, const Program& prog, const Pl
   if (nodes[n].kind == 3) {
     int a = nodes[n].a, b = nodes[n].b;
     if (nodes[a].kind == 1) std::swap(a, b);
-    if (nodes[a].kind != 0 || nodes[b].kind != 1) return;
+    if (nodes[a].kind != 0 || nodes[b].kind != 1) return false;
     e.epi_vec = true;
     const PAccess& va = el.acc[vec_acc];
     e.vec_buf = va.buf;
     e.vec_c = va.addr.c;
     e.vec_k = va.addr.at(kd);
-    if (plan->bufs[va.buf].kind != kI32 && plan->bufs[va.buf].kind != kI16 && plan->bufs[va.buf].kind != kI8) return;
-    if (e.vec_c < 0 || e.vec_k < 0 || e.vec_c + e.vec_k * (K - 1) >= plan->bufs[va.buf].elements) return;
+    if (plan->bufs[va.buf].kind != kI32 && plan->bufs[va.buf].kind != kI16 && plan->bufs[va.buf].kind != kI8) return false;
+    if (e.vec_c < 0 || e.vec_k < 0 || e.vec_c + e.vec_k * (K - 1) >= plan->bufs[va.buf].elements) return false;
   } else if (nodes[n].kind != 0) {
-    return;
+    return false;
   }
   // output O: address = o_pix * pix + k + o_c over the consumer's dims
   const PAccess& O = el.acc[out_acc];
   const PBuffer& ob = plan->bufs[O.buf];
-  if (O.addr.at(kd) != 1 || O.addr.at(pd) <= 0 || ob.kind != kI32) return;
+  if (O.addr.at(kd) != 1 || O.addr.at(pd) <= 0) return false;
+  if (ob.kind != kI32 && !(cl.kernel == KernelKind::ConvIgemmTC && (ob.kind == kI8 || ob.kind == kI16))) return false;
+  if (static_cast<std::int8_t>(ob.dtype) != store_ins.dtype) return false;
   const std::int64_t op = O.addr.at(pd);
-  if (O.addr.c < 0 || O.addr.c + op * (NHW - 1) + K - 1 >= ob.elements) return;
-  bool overwrite = el.code.back().agg == static_cast<std::int8_t>(Agg::Assign);
+  if (O.addr.c < 0 || O.addr.c + op * (NHW - 1) + K - 1 >= ob.elements) return false;
+  bool overwrite = store_ins.agg == static_cast<std::int8_t>(Agg::Assign);
   const bool fresh_root = ob.root && ob.root_index < static_cast<int>(opt.fresh_outputs.size()) &&
                           opt.fresh_outputs[ob.root_index] && output_identity(prog, ob.name) == 0 &&
                           first_writer(*plan, static_cast<std::size_t>(s2), O.buf);
   const bool covers = O.addr.c == 0 && op == K && NHW * K == ob.elements;
-  if (!overwrite && !(fresh_root && covers)) return;
+  if (!overwrite && !(fresh_root && covers)) return false;
   e.epi = e.epi_vec || e.epi_lo;
   e.c_buf = O.buf;
   e.c_dtype = ob.dtype;
@@ -561,16 +579,92 @@ void fuse_conv_epilogue(Plan* plan, std::size_t s, const Program& prog, const Pl
   e.c_n = op * HW;
   e.c0 = O.addr.c;
   e.fresh_output = true;  // the consumer overwrites (assign) or adds onto the fused identity 0
-  if (const char* bad = conv_tc_unsupported(e)) {
-    (void)bad;
-    return;
-  }
+  e.overwrites = overwrite;
+  if (cl.kernel == KernelKind::ConvIgemmTC ? conv_igemm_unsupported(e) != nullptr : conv_tc_unsupported(e) != nullptr)
+    return false;
   c = e;
   plan->steps[fill_step].elided = true;
   plan->steps[s2].elided = true;
   if (fresh_root && covers) cl.fused_fill_root = ob.root_index;
   plan->notes.push_back("launch " + cl.path + ": epilogue of " + el.path + " fused; local buffer " + plan->bufs[T].name +
                         " never materialised");
+  return true;
+}
+
+// The conv writes every element of its output exactly once (pixel-major, dense).
+bool conv_covers(const ConvPlan& c, std::int64_t elements) {
+  return c.c0 == 0 && c.c_y == c.K && (c.H == 1 || c.c_x == c.W * c.K) && (c.N == 1 || c.c_n == c.H * c.W * c.K) &&
+         c.N * c.H * c.W * c.K == elements;
+}
+
+// A conv accumulating (add) into a local whose only earlier touch is its zero fill
+// (interp.cpp:433-447: locals start at zero) may overwrite instead; the fill goes.
+void fresh_scratch_output(Plan* plan, std::size_t s) {
+  PLaunch& l = plan->steps[s].launch;
+  ConvPlan& c = l.conv;
+  const PBuffer& ob = plan->bufs[c.c_buf];
+  if (ob.root || c.fresh_output || !conv_covers(c, ob.elements)) return;
+  int fill = -1;
+  for (std::size_t k = 0; k < s; k++) {
+    const PStep& ps = plan->steps[k];
+    if (ps.elided) continue;
+    if (ps.kind == PStep::Fill) {
+      if (ps.buf == c.c_buf) {
+        if (ps.value != 0) return;
+        fill = static_cast<int>(k);
+      }
+      continue;
+    }
+    for (const auto& a : ps.launch.acc)
+      if (a.buf == c.c_buf) return;
+  }
+  if (fill < 0) return;
+  c.fresh_output = true;
+  plan->steps[fill].elided = true;
+}
+
+// Zero fills of locals that the next step touching them overwrites completely before
+// reading (a fused conv epilogue with assign, or an owner-mode assign over every element).
+void elide_dead_fills(Plan* plan) {
+  for (std::size_t f = 0; f < plan->steps.size(); f++) {
+    PStep& fs = plan->steps[f];
+    if (fs.kind != PStep::Fill || fs.elided || plan->bufs[fs.buf].root) continue;
+    const int B = fs.buf;
+    const std::int64_t elems = plan->bufs[B].elements;
+    for (std::size_t k = f + 1; k < plan->steps.size(); k++) {
+      const PStep& ps = plan->steps[k];
+      if (ps.elided) continue;
+      if (ps.kind == PStep::Fill) {
+        if (ps.buf == B) break;
+        continue;
+      }
+      const PLaunch& l = ps.launch;
+      bool conv = l.kernel == KernelKind::ConvI8TC || l.kernel == KernelKind::ConvIgemmTC;
+      bool touches = conv && (l.conv.c_buf == B || l.conv.a_buf == B || l.conv.b_buf == B ||
+                              (l.conv.epi_vec && l.conv.vec_buf == B));
+      for (const auto& a : l.acc) touches |= a.buf == B;
+      if (!touches) continue;
+      bool dead = false;
+      if (conv) {
+        dead = l.conv.c_buf == B && l.conv.a_buf != B && l.conv.b_buf != B && l.conv.fresh_output &&
+               l.conv.overwrites && conv_covers(l.conv, elems);
+      } else if ((l.kernel == KernelKind::Generic || l.kernel == KernelKind::Map) && l.mode == kModeOwner &&
+                 l.cons.empty() && l.specials.empty()) {
+        dead = true;
+        int acc = -1;
+        for (const auto& ins : l.code) {
+          if (ins.op == kOpLoad && l.acc[ins.acc].buf == B) dead = false;
+          if (ins.op == kOpStore && l.acc[ins.acc].buf == B) {
+            if (ins.agg != static_cast<std::int8_t>(Agg::Assign) || acc >= 0) dead = false;
+            acc = ins.acc;
+          }
+        }
+        dead = dead && acc >= 0 && covers_exactly(l.acc[acc].addr, l.pdims, l.dims, elems) && l.rdims.empty();
+      }
+      if (dead) fs.elided = true;
+      break;
+    }
+  }
 }
 
 }  // namespace
@@ -583,11 +677,24 @@ void match_kernels(Plan* plan, const Program& p, const PlanOptions& opt) {
     ConvPlan cp;
     std::string why;
     if (match_conv(*plan, st.launch, p, opt, s, &cp, &why)) {
-      st.launch.kernel = KernelKind::ConvI8TC;
-      st.launch.conv = cp;
-      if (cp.fresh_output) st.launch.fused_fill_root = plan->bufs[cp.c_buf].root_index;
-      fuse_conv_epilogue(plan, s, p, opt);
-      continue;
+      const char* bad_tc = conv_tc_unsupported(cp);
+      const char* bad_ig = bad_tc ? conv_igemm_unsupported(cp) : nullptr;
+      if (!bad_tc || !bad_ig) {
+        st.launch.kernel = bad_tc ? KernelKind::ConvIgemmTC : KernelKind::ConvI8TC;
+        st.launch.conv = cp;
+        if (cp.fresh_output) st.launch.fused_fill_root = plan->bufs[cp.c_buf].root_index;
+        bool fused = fuse_conv_epilogue(plan, s, p, opt);
+        if (!fused && !bad_tc && !bad_ig) {
+          // the im2col kernel stores any output width: it may take an epilogue the
+          // resident-filter kernel (i32 TMA-store only) cannot
+          plan->steps[s].launch.kernel = KernelKind::ConvIgemmTC;
+          fused = fuse_conv_epilogue(plan, s, p, opt);
+          if (!fused) plan->steps[s].launch.kernel = KernelKind::ConvI8TC;
+        }
+        if (!fused) fresh_scratch_output(plan, s);
+        continue;
+      }
+      why = std::string(bad_tc) + "; " + bad_ig;
     }
     if (match_gemm(*plan, st.launch, p, opt, s)) {
       st.launch.kernel = KernelKind::GemmI8TC;
@@ -598,6 +705,7 @@ void match_kernels(Plan* plan, const Program& p, const PlanOptions& opt) {
     if (match_reduce(*plan, st.launch, p, opt, s)) st.launch.kernel = KernelKind::Reduce;
     else if (match_map(st.launch)) st.launch.kernel = KernelKind::Map;
   }
+  elide_dead_fills(plan);
 }
 
 }  // namespace sb

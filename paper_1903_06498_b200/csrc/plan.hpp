@@ -61,7 +61,7 @@ struct PSpecial {
 };
 
 // Specialised kernel families the matcher can route a launch to.
-enum class KernelKind { Generic, ConvI8TC, Map, Reduce, GemmI8TC };
+enum class KernelKind { Generic, ConvI8TC, Map, Reduce, GemmI8TC, ConvIgemmTC };
 
 // tcgen05 GEMM (kernels/gemm_tc.cu): C[m,n] (+)= sum_k A[m,k] B[k,n], i8 operands.
 struct GemmPlan {
@@ -89,7 +89,8 @@ struct ConvPlan {
   int a_buf = -1, b_buf = -1, c_buf = -1;
   DType c_dtype = DType::I32;
   std::int64_t N = 1, H = 1, W = 1, C = 1, K = 1, R = 1, S = 1;
-  // A (input) element address = a_n*n + a_x*u + a_y*v + c + a0, u = x + i + ox, v = y + j + oy
+  std::int64_t sx = 1, sy = 1;  // conv strides (input rows/cols per output row/col)
+  // A (input) element address = a_n*n + a_x*u + a_y*v + c + a0, u = sx*x + i + ox, v = sy*y + j + oy
   std::int64_t a_n = 0, a_x = 0, a_y = 0, a0 = 0;
   std::int64_t ox = 0, oy = 0;
   std::int64_t u_lo = 0, u_hi = 0, v_lo = 0, v_hi = 0;  // valid input window from constraints
@@ -98,6 +99,7 @@ struct ConvPlan {
   // C (output) element address = c_n*n + c_x*x + c_y*y + k + c0
   std::int64_t c_n = 0, c_x = 0, c_y = 0, c0 = 0;
   bool fresh_output = false;  // output known identity-filled: overwrite instead of accumulate
+  bool overwrites = false;    // fused epilogue stores with assign (program semantics overwrite)
   bool b_immutable = false;   // filter is a root `in` buffer that no plan step writes
   // fused element-wise epilogue (K3e): out = wrap(max(acc + vec[k], lo)) with the optional parts
   bool epi = false, epi_vec = false, epi_lo = false;

@@ -13,32 +13,28 @@ All return canonical .stripe text that both the reference parser and ours accept
 """
 
 
-def conv2d(N, H, W, C, K, R=3, S=3, in_dtype="i8", out_dtype="i32", pad=1):
-    """O[n,x,y,k] += I[n, x+i-pad, y+j-pad, c] * F[i,j,k,c], constraints keep taps in bounds."""
+def conv2d(N, H, W, C, K, R=3, S=3, in_dtype="i8", out_dtype="i32", pad=1, stride=1):
+    """O[n,x,y,k] += I[n, s*x+i-pad, s*y+j-pad, c] * F[i,j,k,c], constraints keep taps in bounds."""
+    P = (H + 2 * pad - R) // stride + 1
+    Q = (W + 2 * pad - S) // stride + 1
     sI = (H * W * C, W * C, C, 1)
     sF = (S * K * C, K * C, C, 1)
-    sO = (H * W * K, W * K, K, 1)
-    pts = N * H * W * R * S * C * K
-
-    def aff(idx, off):
-        if off == 0:
-            return f"{idx[1]} + {idx[0]}"
-        return f"{idx[1]} + {idx[0]} - {off}" if off > 0 else f"{idx[1]} + {idx[0]} + {-off}"
-
+    sO = (P * Q * K, Q * K, K, 1)
+    pts = N * P * Q * R * S * C * K
     cons = []
     if pad:
-        cons = [f"i + x - {pad} >= 0", f"-i - x + {H - 1 + pad} >= 0",
-                f"j + y - {pad} >= 0", f"-j - y + {W - 1 + pad} >= 0"]
+        cons = [f"{_aff((stride, 'x'), (1, 'i'), -pad)} >= 0", f"{_aff((-stride, 'x'), (-1, 'i'), H - 1 + pad)} >= 0",
+                f"{_aff((stride, 'y'), (1, 'j'), -pad)} >= 0", f"{_aff((-stride, 'y'), (-1, 'j'), W - 1 + pad)} >= 0"]
     lines = "\n".join("\t\t" + c for c in cons)
     return f"""block []:1 (
 	in I[0, 0, 0, 0] {in_dtype}({N}, {H}, {W}, {C}):{sI}
 	in F[0, 0, 0, 0] {in_dtype}({R}, {S}, {K}, {C}):{sF} #untiled
-	out O[0, 0, 0, 0]:assign {out_dtype}({N}, {H}, {W}, {K}):{sO}
+	out O[0, 0, 0, 0]:assign {out_dtype}({N}, {P}, {Q}, {K}):{sO}
 ) {{
 	0:
-	block [n:{N}, x:{H}, y:{W}, i:{R}, j:{S}, c:{C}, k:{K}]:{pts} (
+	block [n:{N}, x:{P}, y:{Q}, i:{R}, j:{S}, c:{C}, k:{K}]:{pts} (
 {lines}
-		in I[n, {aff(('x', 'i'), pad)}, {aff(('y', 'j'), pad)}, c] {in_dtype}(1, 1, 1, 1):{sI}
+		in I[n, {_aff((stride, 'x'), (1, 'i'), -pad)}, {_aff((stride, 'y'), (1, 'j'), -pad)}, c] {in_dtype}(1, 1, 1, 1):{sI}
 		in F[i, j, k, c] {in_dtype}(1, 1, 1, 1):{sF} #untiled
 		out O[n, x, y, k]:add {out_dtype}(1, 1, 1, 1):{sO}
 	) {{
@@ -49,6 +45,20 @@ def conv2d(N, H, W, C, K, R=3, S=3, in_dtype="i8", out_dtype="i32", pad=1):
 	}}
 }}
 """.replace("\n\n", "\n")
+
+
+def conv_fused(N, H, W, C, K, R=3, S=3, stride=1, pad=1, relu=True, residual=False, out_dtype="i8"):
+    """One conv layer in the fused/localized form (conv_layer): O = wrap(max(conv + Bias (+ Res), 0))."""
+    P = (H + 2 * pad - R) // stride + 1
+    Q = (W + 2 * pad - S) // stride + 1
+    I = Buf("I", "i8", (N, H, W, C))
+    F = Buf("F", "i8", (R, S, K, C), tag="untiled")
+    B = Buf("Bias", "i32", (K,))
+    O = Buf("O", out_dtype, (N, P, Q, K))
+    Rz = Buf("Res", "i8", (N, P, Q, K)) if residual else None
+    body, _ = conv_layer(I, O, F, B, N, H, W, C, K, R, S, stride, pad, relu, Rz, ind=1)
+    refs = [I.ref("in"), F.ref("in"), B.ref("in")] + ([Rz.ref("in")] if Rz else []) + [O.ref("out", agg="assign")]
+    return "\n".join(["block []:1 ("] + [f"\t{r}" for r in refs] + [") {", "\t0:", f"\t{body}", "}", ""])
 
 
 def maxpool2x2(N, H, W, C, dtype="i32"):
@@ -187,3 +197,218 @@ def matmul_bt(M, N, K, in_dtype="i8", out_dtype="i32"):
     return matmul(M, N, K, in_dtype, out_dtype).replace(
         f"in B[0, 0] {in_dtype}({K}, {N}):({N}, 1)", f"in B[0, 0] {in_dtype}({N}, {K}):({K}, 1)").replace(
         f"in B[k, n] {in_dtype}(1, 1):({N}, 1)", f"in B[n, k] {in_dtype}(1, 1):({K}, 1)")
+
+
+# ---- composable program builder (config 5: ResNet-50 and single conv layers) -------------
+
+def _tup(xs):
+    return "(" + ", ".join(str(x) for x in xs) + ")"
+
+
+def _dense(shape):
+    st, acc = [], 1
+    for d in reversed(shape):
+        st.append(acc)
+        acc *= d
+    return tuple(reversed(st))
+
+
+def _aff(*terms):
+    """Affine text from (coef, name) / int terms, e.g. _aff((2, 'x'), (1, 'i'), -3) -> '2*x + i - 3'."""
+    out = []
+    const = 0
+    for t in terms:
+        if isinstance(t, int):
+            const += t
+            continue
+        k, n = t
+        if k == 0:
+            continue
+        s = n if abs(k) == 1 else f"{abs(k)}*{n}"
+        out.append(("- " if k < 0 else "+ ") + s)
+    if const:
+        out.append(("- " if const < 0 else "+ ") + str(abs(const)))
+    if not out:
+        return "0"
+    txt = " ".join(out)
+    return txt[2:] if txt.startswith("+ ") else "-" + txt[2:]
+
+
+class Buf:
+    def __init__(self, name, dtype, shape, tag=""):
+        self.name, self.dtype, self.shape, self.tag = name, dtype, tuple(shape), tag
+        self.strides = _dense(shape)
+
+    @property
+    def elements(self):
+        n = 1
+        for s in self.shape:
+            n *= s
+        return n
+
+    def ref(self, direction, offsets=None, agg=None, sizes=None):
+        offs = offsets if offsets is not None else ["0"] * len(self.shape)
+        a = f":{agg}" if agg else ""
+        sz = sizes if sizes is not None else self.shape
+        tag = f" #{self.tag}" if self.tag else ""
+        return f"{direction} {self.name}[{', '.join(offs)}]{a} {self.dtype}{_tup(sz)}:{_tup(self.strides)}{tag}"
+
+    def point(self, direction, offsets, agg=None):
+        return self.ref(direction, offsets, agg, sizes=[1] * len(self.shape))
+
+
+def _block(idx, cons, refs, body, ind):
+    """idx: list of (name, range) or alias strings."""
+    pts = 1
+    names = []
+    for i in idx:
+        if isinstance(i, tuple):
+            names.append(f"{i[0]}:{i[1]}")
+            pts *= i[1]
+        else:
+            names.append(i)
+    t = "\t" * ind
+    lines = [f"block [{', '.join(names)}]:{pts} ("]
+    lines += [f"{t}\t{c}" for c in cons]
+    lines += [f"{t}\t{r}" for r in refs]
+    lines.append(f"{t}) {{")
+    for k, s in enumerate(body):
+        if s.startswith("block"):
+            lines.append(f"{t}\t{k}:")
+            lines.append(f"{t}\t{s}")
+        else:
+            lines.append(f"{t}\t{k}: {s}")
+    lines.append(f"{t}}}")
+    return "\n".join(lines)
+
+
+def conv_layer(src, dst, w, b, N, H, W, C, K, R, S, stride, pad, relu=True, residual=None, ind=1,
+               acc_dtype="i32", tname="T"):
+    """One conv + bias (+ residual) (+ ReLU) as the fuse/localize passes leave it
+    (test_passes.cpp:357-379): a wrapper block owning the local accumulator T,
+    statement 0 the conv leaf into T (add), statement 1 the element-wise epilogue
+    writing dst (assign)."""
+    P = (H + 2 * pad - R) // stride + 1
+    Q = (W + 2 * pad - S) // stride + 1
+    T = Buf(tname, acc_dtype, (N, P, Q, K))
+    cons = []
+    if pad:
+        # padding halo: the input row/col of every counted tap lies inside the image
+        cons.append(f"{_aff((stride, 'x'), (1, 'i'), -pad)} >= 0")
+        cons.append(f"{_aff((-stride, 'x'), (-1, 'i'), H - 1 + pad)} >= 0")
+        cons.append(f"{_aff((stride, 'y'), (1, 'j'), -pad)} >= 0")
+        cons.append(f"{_aff((-stride, 'y'), (-1, 'j'), W - 1 + pad)} >= 0")
+    conv_refs = [src.point("in", ["n", _aff((stride, "x"), (1, "i"), -pad), _aff((stride, "y"), (1, "j"), -pad), "c"]),
+                 w.point("in", ["i", "j", "k", "c"]),
+                 T.point("out", ["n", "x", "y", "k"], "add")]
+    conv = _block([("n", N), ("x", P), ("y", Q), ("i", R), ("j", S), ("c", C), ("k", K)], cons, conv_refs,
+                  [f"$I = load({src.name})", f"$F = load({w.name})", "$O = mul($I, $F)", f"{T.name} = store($O)"],
+                  ind + 1)
+    epi_refs = [T.point("in", ["n", "x", "y", "k"]), b.point("in", ["k"])]
+    body = [f"$t = load({T.name})", f"$b = load({b.name})", "$s = add($t, $b)"]
+    v = "$s"
+    if residual is not None:
+        epi_refs.append(residual.point("in", ["n", "x", "y", "k"]))
+        body += [f"$r = load({residual.name})", "$u = add($s, $r)"]
+        v = "$u"
+    if relu:
+        body += ["$z = constant(0)", f"$o = max({v}, $z)"]
+        v = "$o"
+    epi_refs.append(dst.point("out", ["n", "x", "y", "k"], "assign"))
+    body.append(f"{dst.name} = store({v})")
+    epi = _block([("n", N), ("x", P), ("y", Q), ("k", K)], [], epi_refs, body, ind + 1)
+    outer_refs = [src.ref("in"), w.ref("in"), b.ref("in")]
+    if residual is not None:
+        outer_refs.append(residual.ref("in"))
+    outer_refs += [T.ref("inout", agg="add"), dst.ref("out", agg="assign")]
+    return _block([], [], outer_refs, [conv, epi], ind), (P, Q)
+
+
+def resnet50(N, image=224, width=64, stages=(3, 4, 6, 3), classes=1000, in_ch=3):
+    """BASELINE config 5: a ResNet-50 v1.5-shaped Stripe program.
+
+    Integer semantics throughout (the reference has no float): i8 activations and
+    weights, i32 accumulators and biases, ReLU outputs stored to i8 (wrapping, ir.cpp:39-48).
+    Layers: 7x7/2 stem conv + bias + ReLU, 3x3/2 max-pool (padding constraints),
+    bottleneck stages (1x1 -> 3x3 (stride on the 3x3, v1.5) -> 1x1, projection 1x1 on the
+    first block of each stage, residual add + ReLU), global 7x7 sum (no divide intrinsic;
+    the 1/49 folds into fc), fc matmul + bias.  Activations are locals of one top-level
+    network block (device-resident scratch); the program's buffers are the image, the
+    weights and the logits.  Returns (text, info) with per-conv shapes and useful MACs.
+    """
+    bufs_in, locals_, body, convs = [], [], [], []
+    X = Buf("X", "i8", (N, image, image, in_ch))
+    bufs_in.append(X)
+    lid = [0]
+
+    def new_conv(src, H, W, C, K, R, S, stride, pad, relu=True, residual=None):
+        l = lid[0]
+        lid[0] += 1
+        w = Buf(f"W{l}", "i8", (R, S, K, C), tag="untiled")
+        b = Buf(f"B{l}", "i32", (K,))
+        bufs_in.extend([w, b])
+        P = (H + 2 * pad - R) // stride + 1
+        Q = (W + 2 * pad - S) // stride + 1
+        dst = Buf(f"A{l}", "i8", (N, P, Q, K))
+        locals_.append(dst)
+        txt, _ = conv_layer(src, dst, w, b, N, H, W, C, K, R, S, stride, pad, relu, residual, ind=2,
+                            tname=f"T{l}")
+        body.append(txt)
+        macs = N * K * C * sum(1 for x in range(P) for i in range(R) if 0 <= stride * x + i - pad < H) * \
+            sum(1 for y in range(Q) for j in range(S) if 0 <= stride * y + j - pad < W)
+        convs.append(dict(layer=l, H=H, W=W, C=C, K=K, R=R, S=S, stride=stride, pad=pad, P=P, Q=Q, macs=macs))
+        return dst, P, Q
+
+    a, H, W = new_conv(X, image, image, in_ch, width, 7, 7, 2, 3)
+    # 3x3/2 max-pool with padding constraints into a zero-initialised local
+    P = (H + 2 - 3) // 2 + 1
+    pool = Buf("Pool", "i8", (N, P, P, width))
+    locals_.append(pool)
+    cons = [f"{_aff((2, 'x'), (1, 'i'), -1)} >= 0", f"{_aff((-2, 'x'), (-1, 'i'), H)} >= 0",
+            f"{_aff((2, 'y'), (1, 'j'), -1)} >= 0", f"{_aff((-2, 'y'), (-1, 'j'), W)} >= 0"]
+    body.append(_block([("n", N), ("x", P), ("y", P), ("c", width), ("i", 3), ("j", 3)], cons,
+                       [a.point("in", ["n", _aff((2, "x"), (1, "i"), -1), _aff((2, "y"), (1, "j"), -1), "c"]),
+                        pool.point("out", ["n", "x", "y", "c"], "max")],
+                       [f"$v = load({a.name})", f"{pool.name} = store($v)"], 2))
+    a, H, W, C = pool, P, P, width
+    for si, nblocks in enumerate(stages):
+        mid = width * (2 ** si)
+        out = mid * 4
+        for bi in range(nblocks):
+            stride = 2 if (bi == 0 and si > 0) else 1
+            if bi == 0:
+                sc, _, _ = new_conv(a, H, W, C, out, 1, 1, stride, 0, relu=False)
+            else:
+                sc = a
+            t1, H1, W1 = new_conv(a, H, W, C, mid, 1, 1, 1, 0)
+            t2, H2, W2 = new_conv(t1, H1, W1, mid, mid, 3, 3, stride, 1)
+            a, H, W = new_conv(t2, H2, W2, mid, out, 1, 1, 1, 0, relu=True, residual=sc)
+            C = out
+    # global sum over the final H x W (wraps into i8 like every activation store)
+    G = Buf("G", "i8", (N, C))
+    locals_.append(G)
+    body.append(_block([("n", N), ("x", H), ("y", W), ("c", C)], [],
+                       [a.point("in", ["n", "x", "y", "c"]), G.point("out", ["n", "c"], "add")],
+                       [f"$v = load({a.name})", f"{G.name} = store($v)"], 2))
+    Wfc = Buf("Wfc", "i8", (classes, C), tag="untiled")
+    Bfc = Buf("Bfc", "i32", (classes,))
+    bufs_in.extend([Wfc, Bfc])
+    logits = Buf("Logits", "i32", (N, classes))
+    Tfc = Buf("Tfc", "i32", (N, classes))
+    fc = _block([("n", N), ("o", classes), ("c", C)], [],
+                [G.point("in", ["n", "c"]), Wfc.point("in", ["o", "c"]), Tfc.point("out", ["n", "o"], "add")],
+                [f"$g = load({G.name})", f"$w = load({Wfc.name})", "$p = mul($g, $w)", f"{Tfc.name} = store($p)"], 3)
+    fce = _block([("n", N), ("o", classes)], [],
+                 [Tfc.point("in", ["n", "o"]), Bfc.point("in", ["o"]), logits.point("out", ["n", "o"], "assign")],
+                 [f"$t = load({Tfc.name})", f"$b = load({Bfc.name})", "$s = add($t, $b)",
+                  f"{logits.name} = store($s)"], 3)
+    body.append(_block([], [], [G.ref("in"), Wfc.ref("in"), Bfc.ref("in"), Tfc.ref("inout", agg="add"),
+                                logits.ref("out", agg="assign")], [fc, fce], 2))
+    net_refs = [x.ref("in") for x in bufs_in] + [logits.ref("out", agg="assign")]
+    net_refs += [l.ref("inout", agg="assign") for l in locals_]
+    net = _block([], [], net_refs, body, 1)
+    root_refs = [x.ref("in") for x in bufs_in] + [logits.ref("out", agg="assign")]
+    text = "\n".join([f"block []:1 ("] + [f"\t{r}" for r in root_refs] + [") {", "\t0:", f"\t{net}", "}", ""])
+    macs = sum(c["macs"] for c in convs) + N * classes * C
+    info = dict(convs=convs, macs=macs, flops=2 * macs, inputs=[x.name for x in bufs_in], output="Logits")
+    return text, info

@@ -1,0 +1,117 @@
+"""General im2col-TMA implicit-GEMM conv (kernels/conv_igemm.cu): strided, 1x1, streamed
+filters, any output-channel count, fused bias/ReLU epilogue to i8 -- bit-exact.
+
+Checkers: the CPU restatement (oracle/port) on small cases, which pins the exact
+PyTorch restatement (tests/intmodel.py) used at larger shapes.
+"""
+import numpy as np
+import pytest
+
+from harness import gpu_available
+from oracle import Port
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not gpu_available():
+        pytest.skip("no B200")
+
+
+def rand_inputs(prog, seed):
+    import paper_1903_06498_b200 as sb
+    rng = np.random.default_rng(seed)
+    store = {}
+    for name, d in prog.buffers.items():
+        if d.dir == sb.Dir.Out:
+            continue
+        bits = int(d.dtype)
+        lo, hi = -(1 << (bits - 1)), (1 << (bits - 1))
+        store[name] = sb.Buffer(d.dtype, rng.integers(lo, hi, d.elements, dtype=np.int64))
+    return store
+
+
+def run(text, seed=0):
+    import paper_1903_06498_b200 as sb
+    prog = sb.parse_program(text)
+    store = rand_inputs(prog, seed)
+    inputs = {n: b.data.copy() for n, b in store.items()}
+    sb.prepare_outputs(prog, store)
+    sb.execute(prog, store)
+    return prog, inputs, {n: b.data for n, b in store.items()}
+
+
+CONVS = [
+    # N, H, W, C, K, R, S, stride, pad
+    (2, 16, 16, 64, 64, 3, 3, 2, 1),      # strided 3x3 (ResNet v1.5 stage entry)
+    (2, 14, 14, 256, 256, 3, 3, 1, 1),    # filter too large for shared memory
+    (2, 8, 8, 128, 512, 1, 1, 1, 0),      # 1x1, K > 256
+    (2, 16, 16, 64, 256, 1, 1, 2, 0),     # strided 1x1 projection
+    (1, 7, 7, 512, 2048, 1, 1, 1, 0),     # stage-4 1x1
+    (3, 9, 11, 64, 320, 3, 3, 1, 1),      # ragged tiles, K not a multiple of 128
+    (1, 32, 32, 64, 64, 7, 7, 2, 3),      # 7x7/2 (stem shape with 64 channels)
+    (2, 15, 13, 128, 64, 3, 3, 2, 1),     # odd extents with stride 2
+]
+
+
+@pytest.mark.parametrize("shape", CONVS, ids=lambda s: "x".join(map(str, s)))
+def test_igemm_conv_exact(shape):
+    import torch
+    import paper_1903_06498_b200 as sb
+    from paper_1903_06498_b200 import workloads as W
+    from intmodel import conv_exact, wrap
+    N, H, Wd, C, K, R, S, st, pad = shape
+    text = W.conv2d(N, H, Wd, C, K, R, S, pad=pad, stride=st)
+    plan = sb.parse_program(text).describe_plan()
+    assert "conv_igemm_tc" in plan or "conv_i8_tc" in plan, plan
+    prog, inp, out = run(text, seed=sum(shape))
+    x = inp["I"].reshape(N, H, Wd, C)
+    w = inp["F"].reshape(R, S, K, C)
+    exp = wrap(32, conv_exact(x, w, st, pad, "cuda")).cpu().numpy().ravel()
+    np.testing.assert_array_equal(out["O"], exp)
+
+
+def test_igemm_pinned_against_port():
+    from paper_1903_06498_b200 import workloads as W
+    text = W.conv2d(1, 9, 7, 64, 192, 3, 3, pad=1, stride=2)
+    prog, inp, out = run(text, seed=5)
+    ref = Port.execute(text, {**inp, "O": np.zeros_like(out["O"])})
+    np.testing.assert_array_equal(out["O"], ref["O"])
+
+
+FUSED = [
+    # N, H, W, C, K, R, S, stride, pad, relu, residual
+    (2, 16, 16, 64, 64, 3, 3, 2, 1, True, False),
+    (2, 8, 8, 256, 512, 1, 1, 1, 0, True, False),
+    (2, 14, 14, 256, 256, 3, 3, 1, 1, False, False),
+    (2, 8, 8, 64, 256, 1, 1, 1, 0, True, True),   # residual: unfused epilogue (map kernel)
+]
+
+
+@pytest.mark.parametrize("case", FUSED, ids=lambda s: "x".join(map(str, s)))
+def test_igemm_fused_epilogue_i8(case):
+    import paper_1903_06498_b200 as sb
+    from paper_1903_06498_b200 import workloads as W
+    from intmodel import conv_layer_exact
+    import torch
+    N, H, Wd, C, K, R, S, st, pad, relu, res = case
+    text = W.conv_fused(N, H, Wd, C, K, R, S, st, pad, relu=relu, residual=res)
+    plan = sb.parse_program(text).describe_plan()
+    if not res:
+        assert "fused" in plan, plan
+    prog, inp, out = run(text, seed=sum(case[:9]))
+    P = (H + 2 * pad - R) // st + 1
+    Q = (Wd + 2 * pad - S) // st + 1
+    r = torch.as_tensor(inp["Res"].reshape(N, P, Q, K), device="cuda") if res else None
+    exp = conv_layer_exact(inp["I"].reshape(N, H, Wd, C), inp["F"].reshape(R, S, K, C), inp["Bias"], st, pad,
+                           relu, r, 8, "cuda").cpu().numpy().ravel()
+    np.testing.assert_array_equal(out["O"], exp)
+
+
+def test_fused_small_pinned_against_port():
+    from paper_1903_06498_b200 import workloads as W
+    text = W.conv_fused(1, 6, 6, 64, 128, 3, 3, 2, 1)
+    prog, inp, out = run(text, seed=9)
+    ref = Port.execute(text, {**inp, "O": np.zeros_like(out["O"])})
+    np.testing.assert_array_equal(out["O"], ref["O"])
