@@ -23,7 +23,7 @@ def peaks():
         return 6650.0, 1590.0
 
 
-def configs():
+def configs(want=None):
     from paper_1903_06498_b200 import workloads as W
     out = {}
     # C1: matmul 1024^3 (integer modes; the reference has no f32)
@@ -41,6 +41,13 @@ def configs():
                               bytes=128 * 112 * 112 * 64 * 4 + 128 * 56 * 56 * 64 * 4)
     out["c4b_global_sum"] = dict(text=W.global_sum(1024, 7, 7, 2048), flops=0.0,
                                  bytes=1024 * 49 * 2048 * 4 + 1024 * 2048 * 4)
+    # C5: ResNet-50 program; batch 1024 sharded 8 ways -> 128 images per GPU
+    if want and not any(w.startswith("c5") for w in want):
+        return out
+    b5 = int(os.environ.get("SB_C5_BATCH", "128"))
+    text, info = W.resnet50(b5)
+    out["c5_resnet50"] = dict(text=text, flops=float(info["flops"]), bytes=b5 * 224 * 224 * 3 + b5 * 1000 * 4,
+                              images=b5)
     return out
 
 
@@ -58,7 +65,7 @@ def main():
     stream = torch.cuda.Stream()
     ctx.set_stream(stream.cuda_stream)
     want = set(args.configs.split(",")) if args.configs else None
-    for name, cfg in configs().items():
+    for name, cfg in configs(want).items():
         if want and not any(name.startswith(w) for w in want):
             continue
         prog = sb.parse_program(cfg["text"])
@@ -90,6 +97,9 @@ def main():
                 "plan": [l.split(" mode")[0] for l in prog.describe_plan(True, not args.generic).splitlines()]}
         if cfg["flops"]:
             line["GOP/s"] = round(cfg["flops"] / ms / 1e6, 1)
+        if "images" in cfg:
+            line["images_per_s"] = round(cfg["images"] / ms * 1e3, 1)
+            line["plan"] = [p for p in line["plan"] if not p.startswith("(elided)") and not p.startswith("note")]
         print(json.dumps(line), flush=True)
 
 

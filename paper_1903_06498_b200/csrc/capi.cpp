@@ -9,6 +9,9 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <set>
 #include <map>
@@ -95,7 +98,9 @@ struct sb_context {
   std::uint64_t launches = 0;
   struct State {
     sb::GenericDesc* d_descs = nullptr;
-    std::vector<void*> scratch;  // by plan buffer id (scratch only)
+    void* arena = nullptr;       // one allocation for every live scratch buffer
+    std::size_t arena_bytes = 0;
+    std::vector<void*> scratch;  // by plan buffer id (scratch only; null when never touched)
   };
   std::map<std::uint64_t, State> states;  // by Compiled::id
   std::vector<std::pair<void*, std::size_t>> roots;  // host-path device buffers
@@ -103,7 +108,7 @@ struct sb_context {
 
   static void release(State& st) {
     cudaFree(st.d_descs);
-    for (void* p : st.scratch) cudaFree(p);
+    cudaFree(st.arena);
   }
   ~sb_context();
   void body_dtor() {
@@ -150,6 +155,37 @@ sb_program::~sb_program() {
 
 namespace {
 
+// Plan buffers a step reads or writes.
+std::vector<int> step_buffers(const sb::PStep& s) {
+  std::vector<int> out;
+  if (s.kind == sb::PStep::Fill) {
+    out.push_back(s.buf);
+    return out;
+  }
+  const sb::PLaunch& l = s.launch;
+  switch (l.kernel) {
+    case sb::KernelKind::ConvI8TC:
+    case sb::KernelKind::ConvIgemmTC:
+      out = {l.conv.a_buf, l.conv.b_buf, l.conv.c_buf};
+      if (l.conv.epi_vec) out.push_back(l.conv.vec_buf);
+      if (l.conv.epi_res) out.push_back(l.conv.res_buf);
+      if (l.conv.packed) {
+        out.push_back(l.conv.pack_a);
+        out.push_back(l.conv.pack_b);
+      }
+      break;
+    case sb::KernelKind::GemmI8TC:
+      out = {l.gemm.a_buf, l.gemm.b_buf, l.gemm.c_buf};
+      break;
+    case sb::KernelKind::Reduce:
+      out = {l.reduce.in_buf, l.reduce.out_buf};
+      break;
+    default:
+      for (const auto& a : l.acc) out.push_back(a.buf);
+  }
+  return out;
+}
+
 Compiled* get_plan(sb_program* p, const std::vector<bool>& fresh, bool tc) {
   std::string key(tc ? "T" : "G");
   for (bool f : fresh) key += f ? '1' : '0';
@@ -188,12 +224,50 @@ sb_context::State& ensure_state(sb_context* ctx, const Compiled* c) {
                           cudaMemcpyHostToDevice),
                "upload desc");
   }
-  st.scratch.assign(c->plan.bufs.size(), nullptr);
-  for (std::size_t b = 0; b < c->plan.bufs.size(); b++) {
-    const auto& pb = c->plan.bufs[b];
-    if (pb.root) continue;
-    cuda_check(cudaMalloc(&st.scratch[b], padded(pb.elements * kind_bytes(pb.kind))), "cudaMalloc(scratch)");
+  // Scratch (locals, spills) lives in one arena.  Offsets come from live intervals over
+  // the non-elided steps: buffers whose [first, last] step ranges are disjoint share
+  // bytes (greedy first-fit, largest first); locals a fused epilogue never materialises
+  // get nothing.
+  const auto& plan = c->plan;
+  const std::size_t nb = plan.bufs.size();
+  std::vector<int> first(nb, -1), last(nb, -1);
+  for (std::size_t i = 0; i < plan.steps.size(); i++) {
+    const auto& s = plan.steps[i];
+    if (s.elided) continue;
+    for (int b : step_buffers(s)) {
+      if (b < 0 || plan.bufs[b].root) continue;
+      if (first[b] < 0) first[b] = static_cast<int>(i);
+      last[b] = static_cast<int>(i);
+    }
   }
+  struct Slot {
+    int buf;
+    std::size_t off, bytes;
+  };
+  std::vector<int> order;
+  for (std::size_t b = 0; b < nb; b++)
+    if (first[b] >= 0) order.push_back(static_cast<int>(b));
+  auto bytes_of = [&](int b) { return (plan.bufs[b].elements * kind_bytes(plan.bufs[b].kind) + 255) / 256 * 256; };
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return bytes_of(a) > bytes_of(b); });
+  std::vector<Slot> placed;
+  std::size_t total = 0;
+  for (int b : order) {
+    std::vector<std::pair<std::size_t, std::size_t>> busy;
+    for (const auto& q : placed)
+      if (!(last[q.buf] < first[b] || last[b] < first[q.buf])) busy.emplace_back(q.off, q.off + q.bytes);
+    std::sort(busy.begin(), busy.end());
+    std::size_t off = 0, need = bytes_of(b);
+    for (const auto& [lo, hi] : busy) {
+      if (off + need <= lo) break;
+      off = std::max(off, hi);
+    }
+    placed.push_back({b, off, need});
+    total = std::max(total, off + need);
+  }
+  st.scratch.assign(nb, nullptr);
+  if (total) cuda_check(cudaMalloc(&st.arena, total), "cudaMalloc(scratch arena)");
+  for (const auto& q : placed) st.scratch[q.buf] = static_cast<char*>(st.arena) + q.off;
+  st.arena_bytes = total;
   return ctx->states.emplace(c->id, std::move(st)).first->second;
 }
 
@@ -202,14 +276,14 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
   auto& st = ensure_state(ctx, c);
   const auto& plan = c->plan;
   auto ptr_of = [&](int b) { return plan.bufs[b].root ? root_ptr[plan.bufs[b].root_index] : st.scratch[b]; };
-  for (std::size_t i = 0; i < plan.steps.size(); i++) {
+  auto step = [&](std::size_t i) {
     const auto& s = plan.steps[i];
-    if (s.elided) continue;
+    if (s.elided) return;
     if (s.kind == sb::PStep::Fill) {
       const auto& pb = plan.bufs[s.buf];
       cuda_check(sb::launch_fill(ptr_of(s.buf), pb.kind, pb.elements, s.value, ctx->stream), "fill");
       ctx->launches++;
-      continue;
+      return;
     }
     const sb::PLaunch& l = s.launch;
     if (l.kernel == sb::KernelKind::ConvI8TC || l.kernel == sb::KernelKind::ConvIgemmTC) {
@@ -225,18 +299,28 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
         a.vec = ptr_of(l.conv.vec_buf);
         a.vec_kind = plan.bufs[l.conv.vec_buf].kind;
       }
-      if (l.kernel == sb::KernelKind::ConvI8TC)
+      if (l.conv.epi_res) a.res = ptr_of(l.conv.res_buf);
+      if (l.kernel == sb::KernelKind::ConvI8TC) {
         cuda_check(sb::launch_conv_tc(l.conv, a, ctx->stream, ctx->num_sms), "conv_tc");
-      else
+      } else if (l.conv.packed) {
+        void* pa = ptr_of(l.conv.pack_a);
+        void* pb = ptr_of(l.conv.pack_b);
+        cuda_check(sb::launch_conv_pack(l.conv, a.a, a.b, pa, pb, ctx->stream), "conv_pack");
+        ctx->launches += 2;
+        a.a = pa;
+        a.b = pb;
+        cuda_check(sb::launch_conv_igemm(sb::packed_view(l.conv), a, ctx->stream, ctx->num_sms), "conv_igemm");
+      } else {
         cuda_check(sb::launch_conv_igemm(l.conv, a, ctx->stream, ctx->num_sms), "conv_igemm");
+      }
       ctx->launches++;
-      continue;
+      return;
     }
     if (l.kernel == sb::KernelKind::GemmI8TC) {
       sb::GemmArgs a{ptr_of(l.gemm.a_buf), ptr_of(l.gemm.b_buf), ptr_of(l.gemm.c_buf)};
       cuda_check(sb::launch_gemm_tc(l.gemm, a, ctx->stream, ctx->num_sms), "gemm_tc");
       ctx->launches++;
-      continue;
+      return;
     }
     if (l.kernel == sb::KernelKind::Reduce) {
       sb::ReduceArgs a;
@@ -266,7 +350,7 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
       a.pcount = r.pcount;
       cuda_check(sb::launch_reduce(a, ctx->stream), "reduce");
       ctx->launches++;
-      continue;
+      return;
     }
     int di = c->desc_of_step[i];
     sb::BufTable t;
@@ -286,7 +370,36 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
       cuda_check(sb::launch_generic(st.d_descs + di, l.pcount, t, ctx->d_err, static_cast<int>(i), ctx->stream),
                  "generic");
     ctx->launches++;
+  };
+  static const bool profile = std::getenv("SB_PROFILE_STEPS") != nullptr;
+  if (!profile) {
+    for (std::size_t i = 0; i < plan.steps.size(); i++) step(i);
+    return;
   }
+  // tracing aid: per-step device time (events on the context stream), printed to stderr
+  std::vector<cudaEvent_t> ev(plan.steps.size() + 1);
+  for (auto& e : ev) cudaEventCreate(&e);
+  for (std::size_t i = 0; i < plan.steps.size(); i++) {
+    cudaEventRecord(ev[i], ctx->stream);
+    step(i);
+  }
+  cudaEventRecord(ev.back(), ctx->stream);
+  cudaEventSynchronize(ev.back());
+  static const char* kinds[] = {"generic", "conv_i8_tc", "map", "reduce", "gemm_i8_tc", "conv_igemm_tc"};
+  for (std::size_t i = 0; i < plan.steps.size(); i++) {
+    const auto& s = plan.steps[i];
+    if (s.elided) continue;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+    if (s.kind == sb::PStep::Fill)
+      std::fprintf(stderr, "[sb step %3zu] %9.4f ms fill %s (%lld elems)\n", i, ms, plan.bufs[s.buf].name.c_str(),
+                   static_cast<long long>(plan.bufs[s.buf].elements));
+    else
+      std::fprintf(stderr, "[sb step %3zu] %9.4f ms %s %s points=%lld\n", i, ms,
+                   kinds[static_cast<int>(s.launch.kernel)], s.launch.path.c_str(),
+                   static_cast<long long>(s.launch.points));
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
 }
 
 void check_device_error(sb_context* ctx, const Compiled* c) {

@@ -52,6 +52,7 @@ struct ConvArgs {
   bool b_immutable = false;  // filter is a root `in` buffer no plan step writes
   const void* vec = nullptr;  // fused-epilogue per-channel vector buffer
   int vec_kind = 0;
+  const void* res = nullptr;  // fused-epilogue residual (i8, pixel-major)
 };
 // Host-side checks that the plan fits the kernel's tiling; empty string = ok.
 const char* conv_tc_unsupported(const ConvPlan& cp);
@@ -59,5 +60,8 @@ cudaError_t launch_conv_tc(const ConvPlan& cp, const ConvArgs& args, cudaStream_
 // General im2col-TMA implicit GEMM (kernels/conv_igemm.cu): strides, 1x1, streamed filters.
 const char* conv_igemm_unsupported(const ConvPlan& cp);
 cudaError_t launch_conv_igemm(const ConvPlan& cp, const ConvArgs& args, cudaStream_t s, int num_sms);
+// Packs a small-channel conv's taps x channels per output pixel (and its filter) for the
+// 1x1 im2col GEMM (ConvPlan::packed).
+cudaError_t launch_conv_pack(const ConvPlan& cp, const void* a, const void* b, void* pa, void* pb, cudaStream_t s);
 
 }  // namespace sb

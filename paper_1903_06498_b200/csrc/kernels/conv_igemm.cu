@@ -22,6 +22,8 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
+#include <climits>
 #include <cstdint>
 #include <cstring>
 #include <mutex>
@@ -35,6 +37,10 @@ namespace {
 constexpr int kThreads = 192;
 constexpr int BM = 128, BN = 128;
 constexpr int kRingBytes = 128 * 1024;  // A+B stage ring
+constexpr int kStgBytes = BM * BN * 4;    // output staging (i32 worst case)
+constexpr int kResBytes = BM * BN;        // residual tile (i8)
+constexpr int kVecBytes = 2048 * 4;       // per-channel epilogue vector
+constexpr int kMaxVecK = 2048;
 
 struct IgKParams {
   int M, N;           // GEMM rows (output pixels) and cols (output channels)
@@ -44,13 +50,15 @@ struct IgKParams {
   int S, cblocks, kblocks;
   int tiles_m, tiles_n;
   int bk, stages;     // channels per k-block (64 or 128), ring depth
+  int stg_off, res_off, vec_off, bar_off;  // dynamic smem layout (bytes from the 1 KB-aligned base)
+  int smem;
   int fresh, tma_out, out_kind;
   void* c;
   long long ldc;      // elements between consecutive output pixels
   std::uint32_t idesc, desc_hi;
   int pdl;
   // fused epilogue: out = wrap(max(acc + vec[k], lo))
-  int epi, epi_vec, epi_lo, vec_kind;
+  int epi, epi_vec, epi_lo, epi_res, vec_kind;
   const void* vec;
   long long vec_k;
   long long lo;
@@ -125,35 +133,25 @@ __device__ __forceinline__ void tmem_ld32(std::uint32_t taddr, std::uint32_t (&v
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// fused epilogue on the exact s32 accumulator: int64 arithmetic (the reference's temps),
-// wrapped to the output dtype by the store
-__device__ __forceinline__ std::uint32_t epi_value(const IgKParams& p, int k, std::uint32_t acc) {
-  long long v = static_cast<std::int32_t>(acc);
-  if (p.epi_vec) {
-    long long vi = static_cast<long long>(k) * p.vec_k;
-    v += p.vec_kind == kI8 ? static_cast<const std::int8_t*>(p.vec)[vi]
-         : p.vec_kind == kI16 ? static_cast<const std::int16_t*>(p.vec)[vi]
-                              : static_cast<const std::int32_t*>(p.vec)[vi];
-  }
-  if (p.epi_lo && v < p.lo) v = p.lo;
-  return static_cast<std::uint32_t>(v);
-}
-
 __global__ void __launch_bounds__(kThreads, 1)
     conv_igemm_i8_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
-                         const __grid_constant__ CUtensorMap cmap, const IgKParams p) {
+                         const __grid_constant__ CUtensorMap cmap, const __grid_constant__ CUtensorMap rmap,
+                         const IgKParams p) {
   extern __shared__ __align__(1024) std::uint8_t smem_raw[];
   std::uint8_t* base =
       reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t{1023});
   const std::uint32_t stage_a = BM * p.bk, stage_b = BN * p.bk;
   std::uint8_t* ring = base;                    // stages x (A | B)
-  std::uint8_t* stg = ring + kRingBytes;        // 64 KB output staging (4 x 16 KB column quarters)
-  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(stg + BM * BN * 4);
+  std::uint8_t* stg = base + p.stg_off;         // output staging: i32 4 x 16 KB quarters | i8 2 x 16 KB
+  std::uint8_t* rstg = base + p.res_off;        // residual tiles (i8, 2 x 16 KB)
+  std::int32_t* vec_s = reinterpret_cast<std::int32_t*>(base + p.vec_off);  // per-channel vector (<= 2048)
+  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(base + p.bar_off);
   std::uint64_t* full = bars;
   std::uint64_t* empty = bars + 16;
   std::uint64_t* tfull = bars + 32;
   std::uint64_t* tempty = bars + 34;
-  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 36);
+  std::uint64_t* rfull = bars + 36;  // [2]
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 40);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int tiles = p.tiles_m * p.tiles_n;
   const int stages = p.stages;
@@ -167,6 +165,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 128);
     }
+    mbar_init(&rfull[0], 1);
+    mbar_init(&rfull[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -242,17 +242,48 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
+    const int sw = row & 7;  // 128B swizzle phase of this staging row
     const bool leader = threadIdx.x == 64;
+    if (p.epi_vec) {
+      // per-output-channel vector (e.g. the bias) as int32 in smem, read with ld.shared.v4
+      if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+      for (int k = threadIdx.x - 64; k < p.N; k += 128) {
+        const long long vi = static_cast<long long>(k) * p.vec_k;
+        vec_s[k] = p.vec_kind == kI8 ? static_cast<const std::int8_t*>(p.vec)[vi]
+                   : p.vec_kind == kI16 ? static_cast<const std::int16_t*>(p.vec)[vi]
+                                        : static_cast<const std::int32_t*>(p.vec)[vi];
+      }
+    }
+    if (p.epi_res && leader && p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    const long long lo = p.epi_lo ? p.lo : LLONG_MIN;
+    // residual tile [128 pixels x 128 channels] i8 of tile t into buffer b
+    auto load_res = [&](int t, int b) {
+      const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * BN;
+      mbar_expect_tx(&rfull[b], BM * BN);
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
+              "r"(smem_u32(rstg + b * kResBytes)),
+          "l"(reinterpret_cast<std::uint64_t>(&rmap)), "r"(smem_u32(&rfull[b])), "r"(n0), "r"(m0)
+          : "memory");
+    };
+    if (p.epi_res && leader && static_cast<int>(blockIdx.x) < tiles) load_res(blockIdx.x, 0);
     int iter = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, iter++) {
       const int acc = iter & 1;
       const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * BN;
-      if (p.tma_out) {
-        if (leader) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (p.tma_out || p.epi_res) {
+        // i32 staging is single-buffered, i8 staging double-buffered
+        if (leader && p.tma_out == 1) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        if (leader && p.tma_out == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // staging and the older residual buffer are free
       }
+      if (p.epi_res && leader && t + static_cast<int>(gridDim.x) < tiles) load_res(t + gridDim.x, (iter + 1) & 1);
       mbar_wait(&tfull[acc], (iter >> 1) & 1);
       tc_fence_after();
+      if (p.epi_res) mbar_wait(&rfull[iter & 1], (iter >> 1) & 1);
+      std::uint8_t* rcur = rstg + (iter & 1) * kResBytes;
+      std::uint8_t* scur = p.tma_out == 2 ? stg + (iter & 1) * 16384 : stg;
       const int m = m0 + row;
       for (int h = 0; h < BN / 32; h++) {
         std::uint32_t v[32];
@@ -261,44 +292,67 @@ __global__ void __launch_bounds__(kThreads, 1)
                   v);
         const int kbase = n0 + h * 32;
         if (p.epi) {
+          // exact s32 accumulator + vector + residual in int64 (the reference's temps),
+          // clamped, wrapped by the store
+          int bv[32];
 #pragma unroll
-          for (int q = 0; q < 32; q++)
-            if (kbase + q < p.N) v[q] = epi_value(p, kbase + q, v[q]);
+          for (int q = 0; q < 8; q++) {
+            if (p.epi_vec)
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(bv[4 * q]), "=r"(bv[4 * q + 1]), "=r"(bv[4 * q + 2]), "=r"(bv[4 * q + 3])
+                           : "r"(smem_u32(vec_s + (kbase + 4 * q < p.N ? kbase + 4 * q : 0))));
+            else
+              bv[4 * q] = bv[4 * q + 1] = bv[4 * q + 2] = bv[4 * q + 3] = 0;
+          }
+          std::uint32_t rw[8];
+          if (p.epi_res) {
+            const std::uint32_t rrow = smem_u32(rcur + row * 128);
+#pragma unroll
+            for (int u = 0; u < 2; u++)
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(rw[4 * u]), "=r"(rw[4 * u + 1]), "=r"(rw[4 * u + 2]), "=r"(rw[4 * u + 3])
+                           : "r"(rrow + (((2 * h + u) ^ sw) << 4)));
+          }
+#pragma unroll
+          for (int q = 0; q < 32; q++) {
+            long long x = static_cast<long long>(static_cast<std::int32_t>(v[q])) + bv[q];
+            if (p.epi_res) x += static_cast<std::int8_t>(rw[q >> 2] >> (8 * (q & 3)));
+            v[q] = static_cast<std::uint32_t>(x < lo ? lo : x);
+          }
         }
-        if (p.tma_out) {
-          std::uint32_t rbase = smem_u32(stg + h * 16384 + row * 128);
+        if (p.tma_out == 1) {
+          const std::uint32_t rbase = smem_u32(stg + h * 16384 + row * 128);
 #pragma unroll
           for (int q = 0; q < 8; q++)
-            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rbase + ((q ^ (row & 7)) << 4)),
-                         "r"(v[4 * q]), "r"(v[4 * q + 1]), "r"(v[4 * q + 2]), "r"(v[4 * q + 3]));
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rbase + ((q ^ sw) << 4)), "r"(v[4 * q]),
+                         "r"(v[4 * q + 1]), "r"(v[4 * q + 2]), "r"(v[4 * q + 3]));
+        } else if (p.tma_out == 2) {
+          // i8: this row's 32 channels -> two swizzled 16-byte chunks of a 128-byte row
+          std::uint32_t w[8];
+#pragma unroll
+          for (int q = 0; q < 8; q++)
+            w[q] = (v[4 * q] & 0xFF) | ((v[4 * q + 1] & 0xFF) << 8) | ((v[4 * q + 2] & 0xFF) << 16) |
+                   (v[4 * q + 3] << 24);
+          const std::uint32_t rbase = smem_u32(scur + row * 128);
+#pragma unroll
+          for (int u = 0; u < 2; u++)
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rbase + (((2 * h + u) ^ sw) << 4)),
+                         "r"(w[4 * u]), "r"(w[4 * u + 1]), "r"(w[4 * u + 2]), "r"(w[4 * u + 3]));
         } else if (m < p.M) {
           const long long rowbase = static_cast<long long>(m) * p.ldc;
-          if (p.fresh && p.out_kind == kI8 && kbase + 32 <= p.N &&
-              (reinterpret_cast<std::uintptr_t>(p.c) + rowbase + kbase) % 16 == 0) {
-            // packed: 32 wrapped bytes as two 16-byte stores
-            std::uint32_t w[8];
-#pragma unroll
-            for (int q = 0; q < 8; q++)
-              w[q] = (v[4 * q] & 0xFF) | ((v[4 * q + 1] & 0xFF) << 8) | ((v[4 * q + 2] & 0xFF) << 16) |
-                     (v[4 * q + 3] << 24);
-            uint4* o = reinterpret_cast<uint4*>(static_cast<std::int8_t*>(p.c) + rowbase + kbase);
-            o[0] = make_uint4(w[0], w[1], w[2], w[3]);
-            o[1] = make_uint4(w[4], w[5], w[6], w[7]);
-          } else {
-            for (int q = 0; q < 32; q++) {
-              const int n = kbase + q;
-              if (n >= p.N) break;
-              const long long idx = rowbase + n;
-              if (p.out_kind == kI32) {
-                std::int32_t* o = static_cast<std::int32_t*>(p.c) + idx;
-                *o = static_cast<std::int32_t>(p.fresh ? v[q] : static_cast<std::uint32_t>(*o) + v[q]);
-              } else if (p.out_kind == kI16) {
-                std::int16_t* o = static_cast<std::int16_t*>(p.c) + idx;
-                *o = static_cast<std::int16_t>(p.fresh ? v[q] : static_cast<std::uint32_t>(*o) + v[q]);
-              } else {
-                std::int8_t* o = static_cast<std::int8_t*>(p.c) + idx;
-                *o = static_cast<std::int8_t>(p.fresh ? v[q] : static_cast<std::uint32_t>(*o) + v[q]);
-              }
+          for (int q = 0; q < 32; q++) {
+            const int n = kbase + q;
+            if (n >= p.N) break;
+            const long long idx = rowbase + n;
+            if (p.out_kind == kI32) {
+              std::int32_t* o = static_cast<std::int32_t*>(p.c) + idx;
+              *o = static_cast<std::int32_t>(p.fresh ? v[q] : static_cast<std::uint32_t>(*o) + v[q]);
+            } else if (p.out_kind == kI16) {
+              std::int16_t* o = static_cast<std::int16_t*>(p.c) + idx;
+              *o = static_cast<std::int16_t>(p.fresh ? v[q] : static_cast<std::uint32_t>(*o) + v[q]);
+            } else {
+              std::int8_t* o = static_cast<std::int8_t*>(p.c) + idx;
+              *o = static_cast<std::int8_t>(p.fresh ? v[q] : static_cast<std::uint32_t>(*o) + v[q]);
             }
           }
         }
@@ -309,12 +363,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (leader) {
-          for (int h = 0; h < BN / 32; h++)
-            if (n0 + h * 32 < p.N)
-              asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                               reinterpret_cast<std::uint64_t>(&cmap)),
-                           "r"(smem_u32(stg + h * 16384)), "r"(n0 + h * 32), "r"(m0)
-                           : "memory");
+          if (p.tma_out == 1) {
+            for (int h = 0; h < BN / 32; h++)
+              if (n0 + h * 32 < p.N)
+                asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                                 reinterpret_cast<std::uint64_t>(&cmap)),
+                             "r"(smem_u32(stg + h * 16384)), "r"(n0 + h * 32), "r"(m0)
+                             : "memory");
+          } else {
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                             reinterpret_cast<std::uint64_t>(&cmap)),
+                         "r"(smem_u32(scur)), "r"(n0), "r"(m0)
+                         : "memory");
+          }
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
       }
@@ -337,7 +398,7 @@ F driver_fn(const char* name) {
   return nullptr;
 }
 
-constexpr std::size_t kSmem = 1024 + kRingBytes + BM * BN * 4 + 512;
+constexpr int kSmemMax = 227 * 1024;
 
 struct Geometry {
   std::int64_t Hin, Win;       // input window extents (tensor map dims)
@@ -361,10 +422,10 @@ bool geometry(const ConvPlan& cp, Geometry* g) {
 
 struct Prepared {
   ConvPlan cp;
-  const void *a, *b, *vec;
+  const void *a, *b, *vec, *res;
   void* c;
   IgKParams kp;
-  CUtensorMap amap, bmap, cmap;
+  CUtensorMap amap, bmap, cmap, rmap;
 };
 
 std::mutex g_mu;
@@ -376,7 +437,8 @@ bool same(const ConvPlan& x, const ConvPlan& y) {
          x.u_lo == y.u_lo && x.u_hi == y.u_hi && x.v_lo == y.v_lo && x.v_hi == y.v_hi && x.b_i == y.b_i &&
          x.b_j == y.b_j && x.b_k == y.b_k && x.b0 == y.b0 && x.c_n == y.c_n && x.c_x == y.c_x && x.c_y == y.c_y &&
          x.c0 == y.c0 && x.c_dtype == y.c_dtype && x.fresh_output == y.fresh_output && x.epi == y.epi &&
-         x.epi_vec == y.epi_vec && x.epi_lo == y.epi_lo && x.vec_k == y.vec_k && x.vec_c == y.vec_c && x.lo == y.lo;
+         x.epi_vec == y.epi_vec && x.epi_lo == y.epi_lo && x.vec_k == y.vec_k && x.vec_c == y.vec_c && x.lo == y.lo &&
+         x.epi_res == y.epi_res && x.res_c0 == y.res_c0 && x.res_pix == y.res_pix;
 }
 
 int kind_of(DType d) { return d == DType::I8 ? kI8 : d == DType::I16 ? kI16 : kI32; }
@@ -387,6 +449,7 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
   out->b = args.b;
   out->c = args.c;
   out->vec = args.vec;
+  out->res = args.res;
   auto enc_tiled = driver_fn<PFN_cuTensorMapEncodeTiled_v12000>("cuTensorMapEncodeTiled");
   auto enc_im2col = driver_fn<PFN_cuTensorMapEncodeIm2col_v12000>("cuTensorMapEncodeIm2col");
   if (!enc_tiled || !enc_im2col) return cudaErrorNotSupported;
@@ -406,7 +469,6 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
   kp.bk = g.bk;
   kp.cblocks = static_cast<int>(cp.C / g.bk);
   kp.kblocks = static_cast<int>(cp.R * cp.S) * kp.cblocks;
-  kp.stages = static_cast<int>(kRingBytes / (2 * BM * g.bk));
   kp.tiles_m = (kp.M + BM - 1) / BM;
   kp.tiles_n = (kp.N + BN - 1) / BN;
   kp.fresh = cp.fresh_output ? 1 : 0;
@@ -417,6 +479,7 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
   kp.epi = cp.epi ? 1 : 0;
   kp.epi_vec = cp.epi_vec ? 1 : 0;
   kp.epi_lo = cp.epi_lo ? 1 : 0;
+  kp.epi_res = cp.epi_res ? 1 : 0;
   kp.lo = cp.lo;
   kp.vec_k = cp.vec_k;
   kp.vec_kind = args.vec_kind;
@@ -424,8 +487,28 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     const int vb = args.vec_kind == kI8 ? 1 : args.vec_kind == kI16 ? 2 : 4;
     kp.vec = static_cast<const char*>(args.vec) + cp.vec_c * vb;
   }
-  kp.tma_out = kp.fresh && kp.out_kind == kI32 && (kp.ldc * 4) % 16 == 0 &&
-               reinterpret_cast<std::uintptr_t>(kp.c) % 16 == 0;
+  {
+    const std::uintptr_t cbase = reinterpret_cast<std::uintptr_t>(kp.c);
+    if (kp.fresh && kp.out_kind == kI32 && (kp.ldc * 4) % 16 == 0 && cbase % 16 == 0) kp.tma_out = 1;
+    else if (kp.fresh && kp.out_kind == kI8 && kp.ldc % 16 == 0 && cbase % 16 == 0) kp.tma_out = 2;
+    else kp.tma_out = 0;
+  }
+  {
+    // dynamic smem: A/B ring (up to 128 KB) | output staging | residual tiles | vector | barriers
+    const int stg = kp.tma_out == 1 ? kStgBytes : kp.tma_out == 2 ? 2 * 16384 : 0;
+    const int res = kp.epi_res ? 2 * kResBytes : 0;
+    const int vec = kp.epi_vec ? kVecBytes : 0;
+    const int stage = 2 * BM * g.bk;
+    int ring = std::min(kRingBytes, (kSmemMax - 1024 - 512 - stg - res - vec) / stage * stage);
+    if (ring < 2 * stage) return cudaErrorNotSupported;
+    kp.stages = std::min(16, ring / stage);
+    ring = kp.stages * stage;
+    kp.stg_off = ring;
+    kp.res_off = ring + stg;
+    kp.vec_off = ring + stg + res;
+    kp.bar_off = ring + stg + res + vec;
+    kp.smem = 1024 + kp.bar_off + 512;
+  }
   // idesc: S32 accumulate, signed A/B, both K-major, N = 128, M = 128
   kp.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
   // descriptor high word: SBO = 8 rows x row bytes, version 1, swizzle 128B (2) / 64B (4)
@@ -460,7 +543,7 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   std::memset(&out->cmap, 0, sizeof(out->cmap));
-  if (kp.tma_out) {
+  if (kp.tma_out == 1) {
     cuuint64_t cdim[2] = {static_cast<cuuint64_t>(kp.N), static_cast<cuuint64_t>(kp.M)};
     cuuint64_t cstr[1] = {static_cast<cuuint64_t>(kp.ldc * 4)};
     cuuint32_t cbox[2] = {32, BM};
@@ -468,18 +551,107 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
+  } else if (kp.tma_out == 2) {
+    cuuint64_t cdim[2] = {static_cast<cuuint64_t>(kp.N), static_cast<cuuint64_t>(kp.M)};
+    cuuint64_t cstr[1] = {static_cast<cuuint64_t>(kp.ldc)};
+    cuuint32_t cbox[2] = {BN, BM};
+    if (enc_tiled(&out->cmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, kp.c, cdim, cstr, cbox, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  std::memset(&out->rmap, 0, sizeof(out->rmap));
+  if (kp.epi_res) {
+    const std::int8_t* rbase = static_cast<const std::int8_t*>(args.res) + cp.res_c0;
+    if (reinterpret_cast<std::uintptr_t>(rbase) % 16 || cp.res_pix % 16) return cudaErrorMisalignedAddress;
+    cuuint64_t rdim[2] = {static_cast<cuuint64_t>(kp.N), static_cast<cuuint64_t>(kp.M)};
+    cuuint64_t rstr[1] = {static_cast<cuuint64_t>(cp.res_pix)};
+    cuuint32_t rbox[2] = {BN, BM};
+    if (enc_tiled(&out->rmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<std::int8_t*>(rbase), rdim, rstr, rbox, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
   }
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(conv_igemm_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kSmem));
+    cudaError_t e = cudaFuncSetAttribute(conv_igemm_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   return cudaSuccess;
 }
 
+// One thread per 16 packed bytes of one output pixel: kk -> (i, j, c), c fastest.
+__global__ void __launch_bounds__(256) conv_pack_kernel(const std::int8_t* __restrict__ a, std::int8_t* __restrict__ pa,
+                                                        long long pixels, int H, int W, int C, int S, int rsc, int kp,
+                                                        int sx, int sy, long long a_n, long long a_x, long long a_y,
+                                                        long long a0, int u_lo, int u_hi, int v_lo, int v_hi) {
+  const int chunks = kp / 16;
+  const long long total = pixels * chunks;
+  for (long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; g < total;
+       g += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long m = g / chunks;
+    const int ch = static_cast<int>(g - m * chunks);
+    const long long n = m / (static_cast<long long>(H) * W);
+    const int rem = static_cast<int>(m - n * H * W);
+    const int x = rem / W, y = rem - x * W;
+    std::uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      std::uint32_t word = 0;
+#pragma unroll
+      for (int e = 0; e < 4; e++) {
+        const int kk = ch * 16 + q * 4 + e;
+        std::int8_t val = 0;
+        if (kk < rsc) {
+          const int c = kk % C, ij = kk / C;
+          const int i = ij / S, j = ij - i * S;
+          const int u = sx * x + i, v = sy * y + j;
+          if (u >= u_lo && u <= u_hi && v >= v_lo && v <= v_hi) val = a[a0 + a_n * n + a_x * u + a_y * v + c];
+        }
+        word |= static_cast<std::uint32_t>(static_cast<std::uint8_t>(val)) << (8 * e);
+      }
+      w[q] = word;
+    }
+    reinterpret_cast<uint4*>(pa)[g] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+__global__ void conv_pack_filter_kernel(const std::int8_t* __restrict__ b, std::int8_t* __restrict__ pb, int K, int C,
+                                        int S, int rsc, int kp, long long b_i, long long b_j, long long b_k,
+                                        long long b_c, long long b0) {
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < K * kp; g += gridDim.x * blockDim.x) {
+    const int k = g / kp, kk = g - k * kp;
+    std::int8_t val = 0;
+    if (kk < rsc) {
+      const int c = kk % C, ij = kk / C;
+      const int i = ij / S, j = ij - i * S;
+      val = b[b0 + b_i * i + b_j * j + b_k * k + b_c * c];
+    }
+    pb[g] = val;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_conv_pack(const ConvPlan& cp, const void* a, const void* b, void* pa, void* pb, cudaStream_t s) {
+  const long long pixels = cp.N * cp.H * cp.W;
+  const int kp = static_cast<int>(cp.pack_k), rsc = static_cast<int>(cp.R * cp.S * cp.C);
+  const long long work = pixels * (kp / 16);
+  const long long blocks = std::min<long long>((work + 255) / 256, 148 * 16);
+  conv_pack_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(
+      static_cast<const std::int8_t*>(a), static_cast<std::int8_t*>(pa), pixels, static_cast<int>(cp.H),
+      static_cast<int>(cp.W), static_cast<int>(cp.C), static_cast<int>(cp.S), rsc, kp, static_cast<int>(cp.sx),
+      static_cast<int>(cp.sy), cp.a_n, cp.a_x, cp.a_y, cp.a0, static_cast<int>(cp.u_lo), static_cast<int>(cp.u_hi),
+      static_cast<int>(cp.v_lo), static_cast<int>(cp.v_hi));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int fb = static_cast<int>(std::min<long long>((cp.K * kp + 255) / 256, 1024));
+  conv_pack_filter_kernel<<<fb, 256, 0, s>>>(static_cast<const std::int8_t*>(b), static_cast<std::int8_t*>(pb),
+                                             static_cast<int>(cp.K), static_cast<int>(cp.C), static_cast<int>(cp.S),
+                                             rsc, kp, cp.b_i, cp.b_j, cp.b_k, cp.b_c, cp.b0);
+  return cudaGetLastError();
+}
 
 const char* conv_igemm_unsupported(const ConvPlan& cp) {
   Geometry g;
@@ -495,6 +667,8 @@ const char* conv_igemm_unsupported(const ConvPlan& cp) {
   if (cp.c_y < cp.K || (cp.H > 1 && cp.c_x != cp.W * cp.c_y) || (cp.N > 1 && cp.c_n != cp.H * cp.W * cp.c_y))
     return "output not pixel-major";
   if (cp.R * cp.S * cp.C * 128 * 128 >= (1ll << 31)) return "reduction too long for exact s32 accumulation";
+  if (cp.epi_vec && cp.K > kMaxVecK) return "epilogue vector longer than 2048";
+  if (cp.epi_res && (cp.res_pix % 16 || cp.res_c0 % 16)) return "residual rows not 16-byte aligned";
   return nullptr;
 }
 
@@ -504,7 +678,8 @@ cudaError_t launch_conv_igemm(const ConvPlan& cp, const ConvArgs& args, cudaStre
     std::lock_guard<std::mutex> lock(g_mu);
     if (!g_prep) g_prep = new std::vector<Prepared>();
     for (auto& e : *g_prep)
-      if (e.a == args.a && e.b == args.b && e.c == args.c && e.vec == args.vec && same(e.cp, cp)) pr = &e;
+      if (e.a == args.a && e.b == args.b && e.c == args.c && e.vec == args.vec && e.res == args.res && same(e.cp, cp))
+        pr = &e;
     if (!pr) {
       if (g_prep->size() >= 512) g_prep->clear();
       Prepared fresh;
@@ -520,14 +695,14 @@ cudaError_t launch_conv_igemm(const ConvPlan& cp, const ConvArgs& args, cudaStre
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(tiles < num_sms ? tiles : num_sms));
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = kSmem;
+  cfg.dynamicSmemBytes = static_cast<unsigned>(kp.smem);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, conv_igemm_i8_kernel, pr->amap, pr->bmap, pr->cmap, kp);
+  return cudaLaunchKernelEx(&cfg, conv_igemm_i8_kernel, pr->amap, pr->bmap, pr->cmap, pr->rmap, kp);
 }
 
 }  // namespace sb

@@ -590,6 +590,7 @@ bool fill_params(const ConvPlan& cp, ConvKParams* kp) {
 const char* conv_tc_unsupported(const ConvPlan& cp) {
   ConvKParams kp;
   if (cp.sx != 1 || cp.sy != 1) return "strided";
+  if (cp.epi_res) return "residual epilogue";
   if (!fill_params(cp, &kp)) return "image row too wide for one 128-row tile";
   if (cp.C % 64 != 0) return "channels not a multiple of 64";
   if (cp.K % 32 != 0 || cp.K > 256) return "output channels not a multiple of 32 in [32, 256]";

@@ -472,15 +472,16 @@ bool fuse_conv_epilogue(Plan* plan, std::size_t s, const Program& prog, const Pl
   int pd = -1, kd = -1;
   for (int d = 0; d < 2; d++) (el.dims[d].range == K ? kd : pd) = d;
   if (pd < 0 || kd < 0 || el.dims[pd].range != NHW) return false;
-  // symbolic evaluation of the body: each temp is ACC, VEC (per-k vector), CONST or an op on them
+  // symbolic evaluation of the body: each temp is ACC, VEC (per-k vector), RES (per-element
+  // residual), CONST or an op on them
   struct Sym {
-    int kind = -1;  // 0 ACC, 1 VEC, 2 CONST, 3 ADD(a,b), 4 MAX(a,b)
+    int kind = -1;  // 0 ACC, 1 VEC, 2 CONST, 3 ADD(a,b), 4 MAX(a,b), 5 RES
     int a = -1, b = -1;
     std::int64_t c = 0;
   };
   std::vector<Sym> nodes;
   std::vector<int> temp(el.ntemps, -1);
-  int vec_acc = -1, out_acc = -1, out_node = -1;
+  int vec_acc = -1, res_acc = -1, out_acc = -1, out_node = -1;
   DInstr store_ins{};
   auto operand = [&](int x) -> int {
     if (x >= 0) return temp[x];
@@ -497,11 +498,19 @@ bool fuse_conv_epilogue(Plan* plan, std::size_t s, const Program& prog, const Pl
       if (a.buf == T) {
         if (!(a.addr.c == 0 && a.addr.at(pd) == K && a.addr.at(kd) == 1)) return false;
         s.kind = 0;
-      } else {
-        if (a.addr.at(pd) != 0 || el.acc_mode[ins.acc] != kAccRead) return false;
+      } else if (a.addr.at(pd) == 0) {
+        if (el.acc_mode[ins.acc] != kAccRead) return false;
         if (vec_acc >= 0 && !(el.acc[vec_acc].buf == a.buf && el.acc[vec_acc].addr == a.addr)) return false;
         vec_acc = ins.acc;
         s.kind = 1;
+      } else {
+        // residual: pixel-major i8 with contiguous channels
+        if (el.acc_mode[ins.acc] != kAccRead || res_acc >= 0 || a.addr.at(kd) != 1 || a.addr.at(pd) <= 0 ||
+            plan->bufs[a.buf].kind != kI8 || a.addr.c < 0 ||
+            a.addr.c + a.addr.at(pd) * (NHW - 1) + K - 1 >= plan->bufs[a.buf].elements)
+          return false;
+        res_acc = ins.acc;
+        s.kind = 5;
       }
     } else if (ins.op == kOpConst) {
       int o = operand(ins.a);
@@ -530,7 +539,7 @@ bool fuse_conv_epilogue(Plan* plan, std::size_t s, const Program& prog, const Pl
     temp[ins.dst] = static_cast<int>(nodes.size()) - 1;
   }
   if (out_acc < 0) return false;
-  // match out = MAX(x, CONST) | x ;  x = ADD(ACC, VEC) | ADD(VEC, ACC) | ACC
+  // match out = MAX(x, CONST) | x ;  x = a sum (int64, order-free) of ACC, optional VEC, optional RES
   ConvPlan e = c;
   int n = out_node;
   e.epi_lo = false;
@@ -542,20 +551,37 @@ bool fuse_conv_epilogue(Plan* plan, std::size_t s, const Program& prog, const Pl
     e.lo = nodes[b].c;
     n = a;
   }
-  e.epi_vec = false;
-  if (nodes[n].kind == 3) {
-    int a = nodes[n].a, b = nodes[n].b;
-    if (nodes[a].kind == 1) std::swap(a, b);
-    if (nodes[a].kind != 0 || nodes[b].kind != 1) return false;
-    e.epi_vec = true;
+  int n_acc = 0, n_vec = 0, n_res = 0;
+  {
+    std::vector<int> work = {n};
+    while (!work.empty()) {
+      int x = work.back();
+      work.pop_back();
+      switch (nodes[x].kind) {
+        case 3: work.push_back(nodes[x].a); work.push_back(nodes[x].b); break;
+        case 0: n_acc++; break;
+        case 1: n_vec++; break;
+        case 5: n_res++; break;
+        default: return false;
+      }
+    }
+  }
+  if (n_acc != 1 || n_vec > 1 || n_res > 1) return false;
+  e.epi_vec = n_vec == 1;
+  if (e.epi_vec) {
     const PAccess& va = el.acc[vec_acc];
     e.vec_buf = va.buf;
     e.vec_c = va.addr.c;
     e.vec_k = va.addr.at(kd);
     if (plan->bufs[va.buf].kind != kI32 && plan->bufs[va.buf].kind != kI16 && plan->bufs[va.buf].kind != kI8) return false;
     if (e.vec_c < 0 || e.vec_k < 0 || e.vec_c + e.vec_k * (K - 1) >= plan->bufs[va.buf].elements) return false;
-  } else if (nodes[n].kind != 0) {
-    return false;
+  }
+  e.epi_res = n_res == 1;
+  if (e.epi_res) {
+    const PAccess& ra = el.acc[res_acc];
+    e.res_buf = ra.buf;
+    e.res_c0 = ra.addr.c;
+    e.res_pix = ra.addr.at(pd);
   }
   // output O: address = o_pix * pix + k + o_c over the consumer's dims
   const PAccess& O = el.acc[out_acc];
@@ -580,7 +606,9 @@ bool fuse_conv_epilogue(Plan* plan, std::size_t s, const Program& prog, const Pl
   e.c0 = O.addr.c;
   e.fresh_output = true;  // the consumer overwrites (assign) or adds onto the fused identity 0
   e.overwrites = overwrite;
-  if (cl.kernel == KernelKind::ConvIgemmTC ? conv_igemm_unsupported(e) != nullptr : conv_tc_unsupported(e) != nullptr)
+  if (cl.kernel == KernelKind::ConvIgemmTC
+          ? conv_igemm_unsupported(e.packed ? packed_view(e) : e) != nullptr
+          : conv_tc_unsupported(e) != nullptr)
     return false;
   c = e;
   plan->steps[fill_step].elided = true;
@@ -588,6 +616,62 @@ bool fuse_conv_epilogue(Plan* plan, std::size_t s, const Program& prog, const Pl
   if (fresh_root && covers) cl.fused_fill_root = ob.root_index;
   plan->notes.push_back("launch " + cl.path + ": epilogue of " + el.path + " fused; local buffer " + plan->bufs[T].name +
                         " never materialised");
+  return true;
+}
+
+}  // namespace
+
+ConvPlan packed_view(const ConvPlan& c) {
+  ConvPlan v = c;
+  v.packed = false;
+  v.a_buf = c.pack_a;
+  v.b_buf = c.pack_b;
+  v.C = c.pack_k;
+  v.R = v.S = 1;
+  v.sx = v.sy = 1;
+  v.a_y = c.pack_k;
+  v.a_x = c.W * c.pack_k;
+  v.a_n = c.H * c.W * c.pack_k;
+  v.a0 = 0;
+  v.u_lo = 0;
+  v.u_hi = c.H - 1;
+  v.v_lo = 0;
+  v.v_hi = c.W - 1;
+  v.b_i = v.b_j = 0;
+  v.b_k = c.pack_k;
+  v.b_c = 1;
+  v.b0 = 0;
+  v.b_immutable = false;
+  return v;
+}
+
+namespace {
+
+// Small-channel convs (C not a multiple of 64, e.g. the 7x7x3 stem): pack, then 1x1 igemm.
+bool try_packed_conv(Plan* plan, ConvPlan* cp) {
+  const std::int64_t rsc = cp->R * cp->S * cp->C;
+  if (rsc > 1024 || cp->C % 64 == 0) return false;
+  const std::int64_t kp = (rsc + 63) / 64 * 64;
+  ConvPlan c = *cp;
+  c.packed = true;
+  c.pack_k = kp;
+  const std::int64_t pixels = c.N * c.H * c.W;
+  c.pack_a = static_cast<int>(plan->bufs.size());
+  c.pack_b = c.pack_a + 1;
+  if (conv_igemm_unsupported(packed_view(c))) return false;
+  PBuffer a;
+  a.name = "pack:" + plan->bufs[c.a_buf].name;
+  a.dtype = DType::I8;
+  a.kind = kI8;
+  a.elements = pixels * kp;
+  PBuffer b;
+  b.name = "pack:" + plan->bufs[c.b_buf].name;
+  b.dtype = DType::I8;
+  b.kind = kI8;
+  b.elements = c.K * kp;
+  plan->bufs.push_back(a);
+  plan->bufs.push_back(b);
+  *cp = c;
   return true;
 }
 
@@ -641,7 +725,8 @@ void elide_dead_fills(Plan* plan) {
       const PLaunch& l = ps.launch;
       bool conv = l.kernel == KernelKind::ConvI8TC || l.kernel == KernelKind::ConvIgemmTC;
       bool touches = conv && (l.conv.c_buf == B || l.conv.a_buf == B || l.conv.b_buf == B ||
-                              (l.conv.epi_vec && l.conv.vec_buf == B));
+                              (l.conv.packed && (l.conv.pack_a == B || l.conv.pack_b == B)) ||
+                              (l.conv.epi_vec && l.conv.vec_buf == B) || (l.conv.epi_res && l.conv.res_buf == B));
       for (const auto& a : l.acc) touches |= a.buf == B;
       if (!touches) continue;
       bool dead = false;
@@ -692,6 +777,15 @@ void match_kernels(Plan* plan, const Program& p, const PlanOptions& opt) {
           if (!fused) plan->steps[s].launch.kernel = KernelKind::ConvI8TC;
         }
         if (!fused) fresh_scratch_output(plan, s);
+        continue;
+      }
+      if (try_packed_conv(plan, &cp)) {
+        st.launch.kernel = KernelKind::ConvIgemmTC;
+        st.launch.conv = cp;
+        if (cp.fresh_output) st.launch.fused_fill_root = plan->bufs[cp.c_buf].root_index;
+        if (!fuse_conv_epilogue(plan, s, p, opt)) fresh_scratch_output(plan, s);
+        plan->notes.push_back("launch " + st.launch.path + ": small-channel conv packed to " +
+                              std::to_string(cp.pack_k) + " taps x channels per pixel");
         continue;
       }
       why = std::string(bad_tc) + "; " + bad_ig;

@@ -105,7 +105,20 @@ struct ConvPlan {
   bool epi = false, epi_vec = false, epi_lo = false;
   int vec_buf = -1;
   std::int64_t vec_c = 0, vec_k = 0, lo = 0;
+  // + res[pixel, k] (i8, pixel-major like the output): residual add (im2col kernel only)
+  bool epi_res = false;
+  int res_buf = -1;
+  std::int64_t res_c0 = 0, res_pix = 0;
+  // small-channel lowering (the 7x7x3 stem): taps x channels packed per output pixel into
+  // a scratch [pixels, pack_k] (zero where a constraint skips the tap), the filter into
+  // [K, pack_k]; the im2col kernel then runs the 1x1 conv packed_view() describes
+  bool packed = false;
+  int pack_a = -1, pack_b = -1;
+  std::int64_t pack_k = 0;
 };
+
+// The 1x1 conv over the packed operands of a `packed` conv (same output and epilogue).
+ConvPlan packed_view(const ConvPlan& c);
 
 struct PLaunch {
   std::string path;  // dot path of the leaf block ("0.1.0")

@@ -85,7 +85,8 @@ FUSED = [
     (2, 16, 16, 64, 64, 3, 3, 2, 1, True, False),
     (2, 8, 8, 256, 512, 1, 1, 1, 0, True, False),
     (2, 14, 14, 256, 256, 3, 3, 1, 1, False, False),
-    (2, 8, 8, 64, 256, 1, 1, 1, 0, True, True),   # residual: unfused epilogue (map kernel)
+    (2, 8, 8, 64, 256, 1, 1, 1, 0, True, True),   # residual add fused (TMA-loaded tile)
+    (3, 7, 9, 128, 192, 3, 3, 1, 1, True, True),  # residual with ragged M and N tiles
 ]
 
 
@@ -98,8 +99,7 @@ def test_igemm_fused_epilogue_i8(case):
     N, H, Wd, C, K, R, S, st, pad, relu, res = case
     text = W.conv_fused(N, H, Wd, C, K, R, S, st, pad, relu=relu, residual=res)
     plan = sb.parse_program(text).describe_plan()
-    if not res:
-        assert "fused" in plan, plan
+    assert "fused" in plan, plan
     prog, inp, out = run(text, seed=sum(case[:9]))
     P = (H + 2 * pad - R) // st + 1
     Q = (Wd + 2 * pad - S) // st + 1

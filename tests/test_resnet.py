@@ -69,7 +69,9 @@ def test_tiny_resnet_gpu_vs_reference():
     import paper_1903_06498_b200 as sb
     prog = sb.parse_program(text)
     bufs = [(n, int(d.dtype), d.elements, int(d.dir)) for n, d in prog.buffers.items()]
-    port = Port.execute(text, random_inputs(bufs, 1005))
+    store = random_inputs(bufs, 1005)
+    store["Logits"] = np.zeros(prog.buffers["Logits"].elements, dtype=np.int64)
+    port = Port.execute(text, store)
     np.testing.assert_array_equal(logits, port["Logits"])
 
 

@@ -1,0 +1,42 @@
+#!/usr/bin/env python
+"""Per-plan-step device times of one program (SB_PROFILE_STEPS tracing aid).
+
+    SB_PROFILE_STEPS=1 python tools/profile_steps.py c5 [batch]
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import torch
+    import paper_1903_06498_b200 as sb
+    from paper_1903_06498_b200 import workloads as W
+    which = sys.argv[1] if len(sys.argv) > 1 else "c5"
+    batch = int(sys.argv[2]) if len(sys.argv) > 2 else 128
+    if which == "c5":
+        text, info = W.resnet50(batch)
+    elif which == "c2":
+        text = W.conv2d(32, 56, 56, 64, 64)
+    else:
+        raise SystemExit("unknown program " + which)
+    prog = sb.parse_program(text)
+    ctx = sb.Context(0)
+    bufs, keep = {}, []
+    for bn, d in prog.buffers.items():
+        nbytes = d.elements * {8: 1, 16: 2, 32: 4}[d.dtype]
+        t = torch.randint(-128, 128, (nbytes,), dtype=torch.int8, device="cuda")
+        keep.append(t)
+        bufs[bn] = (t.data_ptr(), d.elements, sb.SB_BUF_PREPARE if int(d.dir) != 0 else 0)
+    run = ctx.bind_device(prog, bufs)
+    for _ in range(3):
+        print("---- run", flush=True)
+        sys.stderr.flush()
+        run()
+        ctx.sync()
+
+
+if __name__ == "__main__":
+    main()
