@@ -180,6 +180,9 @@ std::vector<int> step_buffers(const sb::PStep& s) {
     case sb::KernelKind::Reduce:
       out = {l.reduce.in_buf, l.reduce.out_buf};
       break;
+    case sb::KernelKind::Pool:
+      out = {l.pool.in_buf, l.pool.out_buf};
+      break;
     default:
       for (const auto& a : l.acc) out.push_back(a.buf);
   }
@@ -322,6 +325,11 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
       ctx->launches++;
       return;
     }
+    if (l.kernel == sb::KernelKind::Pool) {
+      cuda_check(sb::launch_pool(l.pool, ptr_of(l.pool.in_buf), ptr_of(l.pool.out_buf), ctx->stream), "pool");
+      ctx->launches++;
+      return;
+    }
     if (l.kernel == sb::KernelKind::Reduce) {
       sb::ReduceArgs a;
       std::memset(&a, 0, sizeof(a));
@@ -385,7 +393,7 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
   }
   cudaEventRecord(ev.back(), ctx->stream);
   cudaEventSynchronize(ev.back());
-  static const char* kinds[] = {"generic", "conv_i8_tc", "map", "reduce", "gemm_i8_tc", "conv_igemm_tc"};
+  static const char* kinds[] = {"generic", "conv_i8_tc", "map", "reduce", "gemm_i8_tc", "conv_igemm_tc", "pool"};
   for (std::size_t i = 0; i < plan.steps.size(); i++) {
     const auto& s = plan.steps[i];
     if (s.elided) continue;

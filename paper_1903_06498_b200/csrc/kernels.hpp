@@ -43,6 +43,10 @@ struct GemmArgs {
 const char* gemm_tc_unsupported(const GemmPlan& g);
 cudaError_t launch_gemm_tc(const GemmPlan& g, const GemmArgs& args, cudaStream_t s, int num_sms);
 
+// Windowed max/min over constraint-bounded taps, 16-byte channel vectors (kernels/pool.cu).
+const char* pool_unsupported(const PoolPlan& pp);
+cudaError_t launch_pool(const PoolPlan& pp, const void* in, void* out, cudaStream_t s);
+
 // tcgen05 implicit-GEMM convolution, i8 x i8 -> i32 accumulate (kernels/conv_tc.cu).
 struct ConvArgs {
   const void* a;  // input activations (i8)

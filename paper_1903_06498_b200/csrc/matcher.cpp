@@ -333,6 +333,121 @@ bool match_reduce(const Plan& plan, PLaunch& l, const Program& prog, const PlanO
 // lanes; every access is broadcast (coefficient 0), an aligned contiguous vector
 // (coefficient 1, everything else a multiple of kVec) or a per-lane gather.  Written
 // buffers must be aligned contiguous vectors so each thread owns whole vectors.
+// $v = load(I); O = store($v), O:max|min: output dims (n, x, y, c) and taps (i, j) with
+// u = sx*x + i, v = sy*y + j bounded by interval constraints (the stem max-pool,
+// support.cpp:126-155 with padding).
+bool match_pool(const Plan& plan, PLaunch& l) {
+  if (l.mode != kModeOwner || l.pdims.empty() || !l.priv.empty() || l.has_spill || !l.specials.empty() ||
+      l.code.size() != 2 || l.is_float)
+    return false;
+  const DInstr& ld = l.code[0];
+  const DInstr& st = l.code[1];
+  if (ld.op != kOpLoad || st.op != kOpStore || st.a != ld.dst || ld.acc == st.acc) return false;
+  if (st.agg != static_cast<std::int8_t>(Agg::Max) && st.agg != static_cast<std::int8_t>(Agg::Min)) return false;
+  if (l.acc_mode[ld.acc] != kAccRead || l.acc_mode[st.acc] != kAccOwned) return false;
+  const PAccess& I = l.acc[ld.acc];
+  const PAccess& O = l.acc[st.acc];
+  const PBuffer& ib = plan.bufs[I.buf];
+  const PBuffer& ob = plan.bufs[O.buf];
+  if (ib.kind != ob.kind || (ib.kind != kI8 && ib.kind != kI16 && ib.kind != kI32) ||
+      st.dtype != static_cast<std::int8_t>(ob.dtype))
+    return false;
+  const int nd = static_cast<int>(l.dims.size());
+  int cdim = -1;
+  std::vector<int> out, taps;
+  for (int d = 0; d < nd; d++) {
+    const bool ui = I.addr.uses(d), uo = O.addr.uses(d);
+    if (ui && uo) {
+      if (I.addr.at(d) == 1 && O.addr.at(d) == 1 && cdim < 0) cdim = d;
+      else out.push_back(d);
+    } else if (ui) {
+      taps.push_back(d);
+    } else {
+      return false;
+    }
+    if (I.addr.at(d) < 0 || O.addr.at(d) < 0) return false;
+  }
+  if (cdim < 0 || out.empty() || out.size() > 3 || taps.size() > 2) return false;
+  std::sort(out.begin(), out.end(), [&](int a, int b) { return I.addr.at(a) < I.addr.at(b); });
+  std::sort(taps.begin(), taps.end(), [&](int a, int b) { return I.addr.at(a) < I.addr.at(b); });
+  const int ydim = out[0], xdim = out.size() > 1 ? out[1] : -1, ndim = out.size() > 2 ? out[2] : -1;
+  auto stride_of = [&](int sp, int tp) -> std::int64_t {
+    if (sp < 0 || tp < 0) return 0;
+    std::int64_t a = I.addr.at(sp), t = I.addr.at(tp);
+    if (t <= 0 || a % t != 0 || a / t < 1 || a / t > 64) return 0;
+    return a / t;
+  };
+  int idim = -1, jdim = -1;
+  if (taps.size() == 2) {
+    jdim = taps[0];
+    idim = taps[1];
+    if (!stride_of(ydim, jdim) || !stride_of(xdim, idim)) return false;
+  } else if (taps.size() == 1) {
+    if (stride_of(ydim, taps[0])) jdim = taps[0];
+    else if (stride_of(xdim, taps[0])) idim = taps[0];
+    else return false;
+  }
+  auto range = [&](int d) -> std::int64_t { return d < 0 ? 1 : l.dims[d].range; };
+  PoolPlan pp;
+  pp.in_buf = I.buf;
+  pp.out_buf = O.buf;
+  pp.kind = ib.kind;
+  pp.agg = st.agg;
+  pp.N = range(ndim);
+  pp.H = range(xdim);
+  pp.W = range(ydim);
+  pp.C = range(cdim);
+  pp.R = range(idim);
+  pp.S = range(jdim);
+  pp.sx = idim >= 0 ? stride_of(xdim, idim) : 1;
+  pp.sy = jdim >= 0 ? stride_of(ydim, jdim) : 1;
+  pp.a_n = ndim >= 0 ? I.addr.at(ndim) : 0;
+  pp.a_x = idim >= 0 ? I.addr.at(idim) : (xdim >= 0 ? I.addr.at(xdim) : 0);
+  pp.a_y = jdim >= 0 ? I.addr.at(jdim) : I.addr.at(ydim);
+  pp.a0 = I.addr.c;
+  pp.o_n = ndim >= 0 ? O.addr.at(ndim) : 0;
+  pp.o_x = xdim >= 0 ? O.addr.at(xdim) : 0;
+  pp.o_y = O.addr.at(ydim);
+  pp.o0 = O.addr.c;
+  pp.u_lo = 0;
+  pp.u_hi = pp.sx * (pp.H - 1) + pp.R - 1;
+  pp.v_lo = 0;
+  pp.v_hi = pp.sy * (pp.W - 1) + pp.S - 1;
+  for (const auto& con : l.cons) {
+    int used = 0;
+    for (int d = 0; d < nd; d++) used += con.uses(d) ? 1 : 0;
+    std::int64_t cx = xdim < 0 ? 0 : con.at(xdim), ci = idim < 0 ? 0 : con.at(idim);
+    std::int64_t cy = con.at(ydim), cj = jdim < 0 ? 0 : con.at(jdim);
+    std::int64_t au = idim >= 0 ? ci : cx, av = jdim >= 0 ? cj : cy;
+    bool on_u = xdim >= 0 && cx != 0 && (au == 1 || au == -1) && cx == pp.sx * au && used == (idim >= 0 ? 2 : 1) &&
+                (idim < 0 || ci != 0);
+    bool on_v = cy != 0 && (av == 1 || av == -1) && cy == pp.sy * av && used == (jdim >= 0 ? 2 : 1) &&
+                (jdim < 0 || cj != 0);
+    if (on_u) {
+      if (au == 1) pp.u_lo = std::max(pp.u_lo, -con.c);
+      else pp.u_hi = std::min(pp.u_hi, con.c);
+    } else if (on_v) {
+      if (av == 1) pp.v_lo = std::max(pp.v_lo, -con.c);
+      else pp.v_hi = std::min(pp.v_hi, con.c);
+    } else {
+      return false;
+    }
+  }
+  // every address the kernel may touch lies inside the buffers
+  const std::int64_t ulo = std::max<std::int64_t>(pp.u_lo, 0), vlo = std::max<std::int64_t>(pp.v_lo, 0);
+  const std::int64_t uhi = std::min(pp.u_hi, pp.sx * (pp.H - 1) + pp.R - 1);
+  const std::int64_t vhi = std::min(pp.v_hi, pp.sy * (pp.W - 1) + pp.S - 1);
+  if (ulo > uhi || vlo > vhi) return false;
+  if (pp.a0 + pp.a_x * ulo + pp.a_y * vlo < 0 ||
+      pp.a0 + pp.a_n * (pp.N - 1) + pp.a_x * uhi + pp.a_y * vhi + pp.C - 1 >= ib.elements)
+    return false;
+  if (pp.o0 < 0 || pp.o0 + pp.o_n * (pp.N - 1) + pp.o_x * (pp.H - 1) + pp.o_y * (pp.W - 1) + pp.C - 1 >= ob.elements)
+    return false;
+  if (pool_unsupported(pp)) return false;
+  l.pool = pp;
+  return true;
+}
+
 bool match_map(PLaunch& l) {
   if (l.is_float || l.mode != kModeOwner || l.pdims.empty() || !l.specials.empty()) return false;
   if (l.ntemps > kVecMaxTemps || l.ncells > kVecMaxCells || l.priv.size() > static_cast<std::size_t>(kVecMaxCells))
@@ -797,6 +912,7 @@ void match_kernels(Plan* plan, const Program& p, const PlanOptions& opt) {
     if (!why.empty())
       plan->notes.push_back("launch " + st.launch.path + ": contraction kept on the generic kernel (" + why + ")");
     if (match_reduce(*plan, st.launch, p, opt, s)) st.launch.kernel = KernelKind::Reduce;
+    else if (match_pool(*plan, st.launch)) st.launch.kernel = KernelKind::Pool;
     else if (match_map(st.launch)) st.launch.kernel = KernelKind::Map;
   }
   elide_dead_fills(plan);

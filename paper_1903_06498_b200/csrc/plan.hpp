@@ -61,7 +61,19 @@ struct PSpecial {
 };
 
 // Specialised kernel families the matcher can route a launch to.
-enum class KernelKind { Generic, ConvI8TC, Map, Reduce, GemmI8TC, ConvIgemmTC };
+enum class KernelKind { Generic, ConvI8TC, Map, Reduce, GemmI8TC, ConvIgemmTC, Pool };
+
+// Windowed max/min (pooling) leaf: $v = load(I); O = store($v) with O:max|min, taps
+// bounded by interval constraints (kernels/pool.cu).
+struct PoolPlan {
+  int in_buf = -1, out_buf = -1;
+  int kind = 0;  // element kind (in == out)
+  int agg = 0;
+  std::int64_t N = 1, H = 1, W = 1, C = 1, R = 1, S = 1, sx = 1, sy = 1;
+  std::int64_t a_n = 0, a_x = 0, a_y = 0, a0 = 0;  // input: a0 + a_n*n + a_x*u + a_y*v + c, u = sx*x + i
+  std::int64_t u_lo = 0, u_hi = 0, v_lo = 0, v_hi = 0;
+  std::int64_t o_n = 0, o_x = 0, o_y = 0, o0 = 0;  // output: o0 + o_n*n + o_x*x + o_y*y + c
+};
 
 // tcgen05 GEMM (kernels/gemm_tc.cu): C[m,n] (+)= sum_k A[m,k] B[k,n], i8 operands.
 struct GemmPlan {
@@ -145,6 +157,7 @@ struct PLaunch {
   ConvPlan conv;
   ReducePlan reduce;
   GemmPlan gemm;
+  PoolPlan pool;
   int fused_fill_root = -1;  // root buffer whose prepare_outputs fill this launch performs itself
   // map kernel (vectorised owner mode): vdim = thread dim split into kVec-lane vectors
   int vdim = -1;

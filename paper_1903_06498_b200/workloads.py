@@ -412,3 +412,21 @@ def resnet50(N, image=224, width=64, stages=(3, 4, 6, 3), classes=1000, in_ch=3)
     macs = sum(c["macs"] for c in convs) + N * classes * C
     info = dict(convs=convs, macs=macs, flops=2 * macs, inputs=[x.name for x in bufs_in], output="Logits")
     return text, info
+
+
+def pool2d(N, H, W, C, R=3, S=3, stride=2, pad=1, agg="max", dtype="i8"):
+    """Windowed max/min with padding constraints (the ResNet stem pool shape)."""
+    P = (H + 2 * pad - R) // stride + 1
+    Q = (W + 2 * pad - S) // stride + 1
+    I = Buf("I", dtype, (N, H, W, C))
+    O = Buf("O", dtype, (N, P, Q, C))
+    cons = []
+    if pad:
+        cons = [f"{_aff((stride, 'x'), (1, 'i'), -pad)} >= 0", f"{_aff((-stride, 'x'), (-1, 'i'), H - 1 + pad)} >= 0",
+                f"{_aff((stride, 'y'), (1, 'j'), -pad)} >= 0", f"{_aff((-stride, 'y'), (-1, 'j'), W - 1 + pad)} >= 0"]
+    blk = _block([("n", N), ("x", P), ("y", Q), ("c", C), ("i", R), ("j", S)], cons,
+                 [I.point("in", ["n", _aff((stride, "x"), (1, "i"), -pad), _aff((stride, "y"), (1, "j"), -pad), "c"]),
+                  O.point("out", ["n", "x", "y", "c"], agg)],
+                 ["$v = load(I)", "O = store($v)"], 1)
+    return "\n".join(["block []:1 (", f"\t{I.ref('in')}", f"\t{O.ref('out', agg='assign')}", ") {", "\t0:",
+                      f"\t{blk}", "}", ""])
