@@ -306,13 +306,12 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
       if (l.kernel == sb::KernelKind::ConvI8TC) {
         cuda_check(sb::launch_conv_tc(l.conv, a, ctx->stream, ctx->num_sms), "conv_tc");
       } else if (l.conv.packed) {
-        void* pa = ptr_of(l.conv.pack_a);
+        // small-channel conv: filter packed to [K, pack_k]; A rows gathered inside the kernel
         void* pb = ptr_of(l.conv.pack_b);
-        cuda_check(sb::launch_conv_pack(l.conv, a.a, a.b, pa, pb, ctx->stream), "conv_pack");
-        ctx->launches += 2;
-        a.a = pa;
+        cuda_check(sb::launch_conv_pack_filter(l.conv, a.b, pb, ctx->stream), "conv_pack_filter");
+        ctx->launches++;
         a.b = pb;
-        cuda_check(sb::launch_conv_igemm(sb::packed_view(l.conv), a, ctx->stream, ctx->num_sms), "conv_igemm");
+        cuda_check(sb::launch_conv_igemm(l.conv, a, ctx->stream, ctx->num_sms), "conv_igemm");
       } else {
         cuda_check(sb::launch_conv_igemm(l.conv, a, ctx->stream, ctx->num_sms), "conv_igemm");
       }

@@ -67,5 +67,6 @@ cudaError_t launch_conv_igemm(const ConvPlan& cp, const ConvArgs& args, cudaStre
 // Packs a small-channel conv's taps x channels per output pixel (and its filter) for the
 // 1x1 im2col GEMM (ConvPlan::packed).
 cudaError_t launch_conv_pack(const ConvPlan& cp, const void* a, const void* b, void* pa, void* pb, cudaStream_t s);
+cudaError_t launch_conv_pack_filter(const ConvPlan& cp, const void* b, void* pb, cudaStream_t s);
 
 }  // namespace sb

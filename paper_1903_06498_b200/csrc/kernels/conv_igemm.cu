@@ -34,7 +34,8 @@
 namespace sb {
 namespace {
 
-constexpr int kThreads = 192;
+constexpr int kThreads = 192;        // producer, MMA, 4 epilogue warps
+constexpr int kThreadsGather = 448;  // + 8 warps gathering A tiles (small-channel convs), 2 per row
 constexpr int BM = 128, BN = 128;
 constexpr int kRingBytes = 128 * 1024;  // A+B stage ring
 constexpr int kStgBytes = BM * BN * 4;    // output staging (i32 worst case)
@@ -52,6 +53,11 @@ struct IgKParams {
   int bk, stages;     // channels per k-block (64 or 128), ring depth
   int stg_off, res_off, vec_off, bar_off;  // dynamic smem layout (bytes from the 1 KB-aligned base)
   int smem;
+  // gather mode (ConvPlan::packed): A rows built by warps 6-9 from the original input
+  int gather, tab_off, rsc, g_C, g_S, g_R, g_run;
+  long long g_an, g_ax, g_ay, g_a0;
+  int g_ulo, g_uhi, g_vlo, g_vhi;
+  const std::int8_t* g_in;
   int fresh, tma_out, out_kind;
   void* c;
   long long ldc;      // elements between consecutive output pixels
@@ -133,7 +139,7 @@ __device__ __forceinline__ void tmem_ld32(std::uint32_t taddr, std::uint32_t (&v
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreadsGather, 1)
     conv_igemm_i8_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
                          const __grid_constant__ CUtensorMap cmap, const __grid_constant__ CUtensorMap rmap,
                          const IgKParams p) {
@@ -158,7 +164,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; s++) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], p.gather ? 257 : 1);  // TMA transaction (+ 256 gathering threads)
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; a++) {
@@ -196,11 +202,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < p.kblocks; kb++) {
           const int r = tap / p.S, s = tap - r * p.S;
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], stage_a + stage_b);
           const std::uint32_t sa = smem_u32(ring + stage * (stage_a + stage_b));
-          tma_load_im2col(sa, &amap, &full[stage], cb * p.bk, w0, h0, img, static_cast<std::uint16_t>(s),
-                          static_cast<std::uint16_t>(r));
-          tma_load_4d(sa + stage_a, &bmap, &full[stage], cb * p.bk, n0, s, r);
+          if (p.gather) {
+            mbar_expect_tx(&full[stage], stage_b);
+            tma_load_4d(sa + stage_a, &bmap, &full[stage], kb * p.bk, n0, 0, 0);
+          } else {
+            mbar_expect_tx(&full[stage], stage_a + stage_b);
+            tma_load_im2col(sa, &amap, &full[stage], cb * p.bk, w0, h0, img, static_cast<std::uint16_t>(s),
+                            static_cast<std::uint16_t>(r));
+            tma_load_4d(sa + stage_a, &bmap, &full[stage], cb * p.bk, n0, s, r);
+          }
           if (++cb == p.cblocks) {
             cb = 0;
             tap++;
@@ -239,6 +250,107 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma_commit(&tfull[acc]);
       }
     }
+  } else if (warp >= 6) {
+    // gather producers: row r of every A stage = the packed (i, j, c) taps of pixel m0 + r,
+    // zero where a constraint skips the tap; written in the TMA swizzle layout
+    const int gt = threadIdx.x - 192;  // 0..255: row r = gt / 2, half = gt % 2 splits each row's work
+    const int r = gt >> 1, half = gt & 1;
+    std::int32_t* toff = reinterpret_cast<std::int32_t*>(base + p.tab_off);
+    std::int8_t* tdi = reinterpret_cast<std::int8_t*>(toff + p.kblocks * p.bk);
+    std::int8_t* tdj = tdi + p.kblocks * p.bk;
+    for (int kk = gt; kk < p.kblocks * p.bk; kk += 256) {
+      if (kk < p.rsc) {
+        const int c = kk % p.g_C, ij = kk / p.g_C, i = ij / p.g_S, j = ij - i * p.g_S;
+        toff[kk] = static_cast<std::int32_t>(p.g_ax * i + p.g_ay * j + c);
+        tdi[kk] = static_cast<std::int8_t>(i);
+        tdj[kk] = static_cast<std::int8_t>(j);
+      } else {
+        toff[kk] = 0;
+        tdi[kk] = -128;  // never valid
+        tdj[kk] = 0;
+      }
+    }
+    if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("bar.sync 2, 256;" ::: "memory");
+    const int PQ = p.P * p.Q;
+    const int sw = p.bk == 128 ? (r & 7) : ((r >> 1) & 3);
+    int stage = 0;
+    std::uint32_t phase = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int m = (t / p.tiles_n) * BM + r;
+      const bool live = m < p.M;
+      const int img = live ? m / PQ : 0, rem = m - img * PQ;
+      const int ox = rem / p.Q, oy = rem - ox * p.Q;
+      const int u0 = p.sx * ox, v0 = p.sy * oy;
+      const std::int8_t* pix = p.g_in + p.g_a0 + p.g_an * img + p.g_ax * u0 + p.g_ay * v0;
+      for (int kb = 0; kb < p.kblocks; kb++) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        std::uint8_t* rowp = ring + stage * (stage_a + stage_b) + r * p.bk;
+        if (p.g_run) {
+          // run layout: tap row i's S*C input bytes are contiguous (a_y == C); copy them with
+          // aligned word loads + funnel shifts, zeroing bytes whose column j is skipped
+          const int RUN = p.g_run;
+          const int jlo = max(0, p.g_vlo - v0), jhi = min(p.g_S - 1, p.g_vhi - v0);
+          const int d0 = jlo * p.g_C, dlen = (jhi - jlo + 1) * p.g_C;
+          for (int ri = half; ri < p.bk / RUN; ri += 2) {
+            const int i = kb * (p.bk / RUN) + ri;
+            const int u = u0 + i;
+            const bool ok = live && i < p.g_R && u >= p.g_ulo && u <= p.g_uhi && dlen > 0;
+            const long long src = static_cast<long long>(reinterpret_cast<std::uintptr_t>(pix)) + p.g_ax * i;
+            const long long first_w = (src + d0) >> 2, last_w = (src + d0 + dlen - 1) >> 2;
+            const long long A0 = src >> 2;
+            const int sh = static_cast<int>(src & 3) * 8;
+            // all loads of the run first (independent, in flight together), then the shifts;
+            // words e in [e_lo, e_hi] hold valid bytes (the others are never dereferenced)
+            const int e_lo = ok ? static_cast<int>(first_w - A0) : 1 << 20;
+            const int e_hi = ok ? min(static_cast<int>(last_w - A0), RUN / 4) : -1;
+            const std::uint32_t* wp = reinterpret_cast<const std::uint32_t*>(A0 << 2);
+            std::uint32_t wd[17];
+#pragma unroll
+            for (int e = 0; e < 17; e++) wd[e] = (e >= e_lo && e <= e_hi) ? __ldg(wp + e) : 0u;
+            auto below = [](int x) -> std::uint32_t { return x <= 0 ? 0u : x >= 4 ? ~0u : ((1u << (8 * x)) - 1u); };
+#pragma unroll
+            for (int ch = 0; ch < 4; ch++) {
+              if (ch >= RUN / 16) break;
+              std::uint32_t w[4];
+#pragma unroll
+              for (int e = 0; e < 4; e++) {
+                const int ow = ch * 4 + e;
+                const std::uint32_t v = __funnelshift_r(wd[ow], wd[ow + 1], sh);
+                const int lb = d0 - 4 * ow, hb = d0 + dlen - 4 * ow;
+                w[e] = v & below(hb) & ~below(lb);
+              }
+              const int q = (ri * RUN) / 16 + ch;
+              *reinterpret_cast<uint4*>(rowp + ((q ^ sw) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          }
+        } else
+        for (int q = half; q < p.bk / 16; q += 2) {
+          std::uint32_t w[4];
+#pragma unroll
+          for (int e4 = 0; e4 < 4; e4++) {
+            std::uint32_t word = 0;
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+              const int kk = kb * p.bk + q * 16 + e4 * 4 + e;
+              const int u = u0 + tdi[kk], v = v0 + tdj[kk];
+              std::int8_t val = 0;
+              if (live && tdi[kk] != -128 && u >= p.g_ulo && u <= p.g_uhi && v >= p.g_vlo && v <= p.g_vhi)
+                val = __ldg(pix + toff[kk]);
+              word |= static_cast<std::uint32_t>(static_cast<std::uint8_t>(val)) << (8 * e);
+            }
+            w[e4] = word;
+          }
+          *reinterpret_cast<uint4*>(rowp + ((q ^ sw) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tcgen05 reads
+        mbar_arrive(&full[stage]);
+        if (++stage == stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
   } else {
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
@@ -257,6 +369,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (p.epi_res && leader && p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("bar.sync 1, 128;" ::: "memory");
     const long long lo = p.epi_lo ? p.lo : LLONG_MIN;
+    const bool relu0 = p.epi_lo && p.lo == 0;
     // residual tile [128 pixels x 128 channels] i8 of tile t into buffer b
     auto load_res = [&](int t, int b) {
       const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * BN;
@@ -313,11 +426,43 @@ __global__ void __launch_bounds__(kThreads, 1)
                            : "=r"(rw[4 * u]), "=r"(rw[4 * u + 1]), "=r"(rw[4 * u + 2]), "=r"(rw[4 * u + 3])
                            : "r"(rrow + (((2 * h + u) ^ sw) << 4)));
           }
+          if (!p.epi_lo) {
+            // no clamp: only the wrapped low bits reach the store
 #pragma unroll
-          for (int q = 0; q < 32; q++) {
-            long long x = static_cast<long long>(static_cast<std::int32_t>(v[q])) + bv[q];
-            if (p.epi_res) x += static_cast<std::int8_t>(rw[q >> 2] >> (8 * (q & 3)));
-            v[q] = static_cast<std::uint32_t>(x < lo ? lo : x);
+            for (int q = 0; q < 32; q++) {
+              const std::uint32_t r = p.epi_res ? static_cast<std::uint32_t>(
+                                                      static_cast<std::int32_t>(static_cast<std::int8_t>(rw[q >> 2] >> (8 * (q & 3)))))
+                                                : 0u;
+              v[q] = v[q] + static_cast<std::uint32_t>(bv[q]) + r;
+            }
+          } else if (relu0) {
+            // exact x = acc + vec (+ res) as a 64-bit (hi:lo) carry chain; ReLU keeps lo iff hi >= 0
+#pragma unroll
+            for (int q = 0; q < 32; q++) {
+              const std::uint32_t r = p.epi_res ? static_cast<std::uint32_t>(
+                                                      static_cast<std::int32_t>(static_cast<std::int8_t>(rw[q >> 2] >> (8 * (q & 3)))))
+                                                : 0u;
+              std::uint32_t lo32;
+              std::int32_t hi32;
+              asm("{\n\t.reg .s32 sa, sb, sr;\n\t"
+                  "shr.s32 sa, %2, 31;\n\t"
+                  "shr.s32 sb, %3, 31;\n\t"
+                  "shr.s32 sr, %4, 31;\n\t"
+                  "add.cc.u32 %0, %2, %3;\n\t"
+                  "addc.cc.s32 %1, sa, sb;\n\t"
+                  "add.cc.u32 %0, %0, %4;\n\t"
+                  "addc.s32 %1, %1, sr;\n\t}"
+                  : "=r"(lo32), "=r"(hi32)
+                  : "r"(v[q]), "r"(bv[q]), "r"(r));
+              v[q] = hi32 < 0 ? 0u : lo32;
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 32; q++) {
+              long long x = static_cast<long long>(static_cast<std::int32_t>(v[q])) + bv[q];
+              if (p.epi_res) x += static_cast<std::int8_t>(rw[q >> 2] >> (8 * (q & 3)));
+              v[q] = static_cast<std::uint32_t>(x < lo ? lo : x);
+            }
           }
         }
         if (p.tma_out == 1) {
@@ -453,8 +598,9 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
   auto enc_tiled = driver_fn<PFN_cuTensorMapEncodeTiled_v12000>("cuTensorMapEncodeTiled");
   auto enc_im2col = driver_fn<PFN_cuTensorMapEncodeIm2col_v12000>("cuTensorMapEncodeIm2col");
   if (!enc_tiled || !enc_im2col) return cudaErrorNotSupported;
+  const ConvPlan gp = cp.packed ? packed_view(cp) : cp;  // GEMM geometry (B map, K blocks)
   Geometry g;
-  if (!geometry(cp, &g)) return cudaErrorNotSupported;
+  if (!geometry(gp, &g)) return cudaErrorNotSupported;
   IgKParams& kp = out->kp;
   std::memset(&kp, 0, sizeof(kp));
   kp.M = static_cast<int>(cp.N * cp.H * cp.W);
@@ -465,10 +611,27 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
   kp.sy = static_cast<int>(cp.sy);
   kp.lower_h = g.lower_h;
   kp.lower_w = g.lower_w;
-  kp.S = static_cast<int>(cp.S);
+  kp.S = static_cast<int>(gp.S);
   kp.bk = g.bk;
-  kp.cblocks = static_cast<int>(cp.C / g.bk);
-  kp.kblocks = static_cast<int>(cp.R * cp.S) * kp.cblocks;
+  kp.cblocks = static_cast<int>(gp.C / g.bk);
+  kp.kblocks = static_cast<int>(gp.R * gp.S) * kp.cblocks;
+  if (cp.packed) {
+    kp.gather = 1;
+    kp.rsc = static_cast<int>(cp.R * cp.S * cp.C);
+    kp.g_C = static_cast<int>(cp.C);
+    kp.g_S = static_cast<int>(cp.S);
+    kp.g_R = static_cast<int>(cp.R);
+    kp.g_an = cp.a_n;
+    kp.g_ax = cp.a_x;
+    kp.g_ay = cp.a_y;
+    kp.g_a0 = cp.a0;
+    kp.g_ulo = static_cast<int>(cp.u_lo);
+    kp.g_uhi = static_cast<int>(cp.u_hi);
+    kp.g_vlo = static_cast<int>(cp.v_lo);
+    kp.g_vhi = static_cast<int>(cp.v_hi);
+    kp.g_in = static_cast<const std::int8_t*>(args.a);
+    kp.g_run = static_cast<int>(cp.pack_run);
+  }
   kp.tiles_m = (kp.M + BM - 1) / BM;
   kp.tiles_n = (kp.N + BN - 1) / BN;
   kp.fresh = cp.fresh_output ? 1 : 0;
@@ -498,15 +661,17 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     const int stg = kp.tma_out == 1 ? kStgBytes : kp.tma_out == 2 ? 2 * 16384 : 0;
     const int res = kp.epi_res ? 2 * kResBytes : 0;
     const int vec = kp.epi_vec ? kVecBytes : 0;
+    const int tab = kp.gather ? (kp.kblocks * kp.bk * 6 + 15) / 16 * 16 : 0;
     const int stage = 2 * BM * g.bk;
-    int ring = std::min(kRingBytes, (kSmemMax - 1024 - 512 - stg - res - vec) / stage * stage);
+    int ring = std::min(kRingBytes, (kSmemMax - 1024 - 512 - stg - res - vec - tab) / stage * stage);
     if (ring < 2 * stage) return cudaErrorNotSupported;
     kp.stages = std::min(16, ring / stage);
     ring = kp.stages * stage;
     kp.stg_off = ring;
     kp.res_off = ring + stg;
     kp.vec_off = ring + stg + res;
-    kp.bar_off = ring + stg + res + vec;
+    kp.tab_off = ring + stg + res + vec;
+    kp.bar_off = kp.tab_off + tab;
     kp.smem = 1024 + kp.bar_off + 512;
   }
   // idesc: S32 accumulate, signed A/B, both K-major, N = 128, M = 128
@@ -515,6 +680,8 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
   kp.desc_hi = g.bk == 128 ? ((1024u >> 4) | (1u << 14) | (2u << 29)) : ((512u >> 4) | (1u << 14) | (4u << 29));
   const CUtensorMapSwizzle sw = g.bk == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
 
+  std::memset(&out->amap, 0, sizeof(out->amap));
+  if (!kp.gather) {
   // A: im2col over (c, v, u, n) from the window corner (u_lo, v_lo)
   const std::int8_t* abase = static_cast<const std::int8_t*>(args.a) + cp.a0 + cp.a_x * cp.u_lo + cp.a_y * cp.v_lo;
   if (reinterpret_cast<std::uintptr_t>(abase) % 16) return cudaErrorMisalignedAddress;
@@ -529,13 +696,14 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
                  upper, static_cast<cuuint32_t>(g.bk), BM, aes, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
-  // B: filter as (c, k, j, i), box (bk, 128, 1, 1)
-  const std::int8_t* bbase = static_cast<const std::int8_t*>(args.b) + cp.b0;
+  }
+  // B: filter as (c, k, j, i), box (bk, 128, 1, 1) (the packed [K, pack_k] filter in gather mode)
+  const std::int8_t* bbase = static_cast<const std::int8_t*>(args.b) + gp.b0;
   if (reinterpret_cast<std::uintptr_t>(bbase) % 16) return cudaErrorMisalignedAddress;
-  cuuint64_t bdim[4] = {static_cast<cuuint64_t>(cp.C), static_cast<cuuint64_t>(cp.K), static_cast<cuuint64_t>(cp.S),
-                        static_cast<cuuint64_t>(cp.R)};
-  cuuint64_t bstr[3] = {static_cast<cuuint64_t>(cp.b_k), static_cast<cuuint64_t>(cp.S > 1 ? cp.b_j : cp.b_k * cp.K),
-                        static_cast<cuuint64_t>(cp.R > 1 ? cp.b_i : cp.b_k * cp.K * cp.S)};
+  cuuint64_t bdim[4] = {static_cast<cuuint64_t>(gp.C), static_cast<cuuint64_t>(gp.K), static_cast<cuuint64_t>(gp.S),
+                        static_cast<cuuint64_t>(gp.R)};
+  cuuint64_t bstr[3] = {static_cast<cuuint64_t>(gp.b_k), static_cast<cuuint64_t>(gp.S > 1 ? gp.b_j : gp.b_k * gp.K),
+                        static_cast<cuuint64_t>(gp.R > 1 ? gp.b_i : gp.b_k * gp.K * gp.S)};
   cuuint32_t bbox[4] = {static_cast<cuuint32_t>(g.bk), BN, 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   if (enc_tiled(&out->bmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<std::int8_t*>(bbase), bdim, bstr, bbox, es,
@@ -617,15 +785,23 @@ __global__ void __launch_bounds__(256) conv_pack_kernel(const std::int8_t* __res
   }
 }
 
+// kk layout: dense (i, j, c) when run == 0, else i * run + (j * C + c) with zero padding
 __global__ void conv_pack_filter_kernel(const std::int8_t* __restrict__ b, std::int8_t* __restrict__ pb, int K, int C,
-                                        int S, int rsc, int kp, long long b_i, long long b_j, long long b_k,
+                                        int R, int S, int run, int kp, long long b_i, long long b_j, long long b_k,
                                         long long b_c, long long b0) {
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < K * kp; g += gridDim.x * blockDim.x) {
     const int k = g / kp, kk = g - k * kp;
+    int i, jc;
+    if (run) {
+      i = kk / run;
+      jc = kk - i * run;
+    } else {
+      i = kk / (S * C);
+      jc = kk - i * S * C;
+    }
     std::int8_t val = 0;
-    if (kk < rsc) {
-      const int c = kk % C, ij = kk / C;
-      const int i = ij / S, j = ij - i * S;
+    if (i < R && jc < S * C) {
+      const int c = jc % C, j = jc / C;
       val = b[b0 + b_i * i + b_j * j + b_k * k + b_c * c];
     }
     pb[g] = val;
@@ -633,6 +809,17 @@ __global__ void conv_pack_filter_kernel(const std::int8_t* __restrict__ b, std::
 }
 
 }  // namespace
+
+cudaError_t launch_conv_pack_filter(const ConvPlan& cp, const void* b, void* pb, cudaStream_t s) {
+  const int kp = static_cast<int>(cp.pack_k), rsc = static_cast<int>(cp.R * cp.S * cp.C);
+  const int fb = static_cast<int>(std::min<long long>((cp.K * kp + 255) / 256, 1024));
+  (void)rsc;
+  conv_pack_filter_kernel<<<fb, 256, 0, s>>>(static_cast<const std::int8_t*>(b), static_cast<std::int8_t*>(pb),
+                                             static_cast<int>(cp.K), static_cast<int>(cp.C), static_cast<int>(cp.R),
+                                             static_cast<int>(cp.S), static_cast<int>(cp.pack_run), kp, cp.b_i, cp.b_j,
+                                             cp.b_k, cp.b_c, cp.b0);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_conv_pack(const ConvPlan& cp, const void* a, const void* b, void* pa, void* pb, cudaStream_t s) {
   const long long pixels = cp.N * cp.H * cp.W;
@@ -648,12 +835,22 @@ cudaError_t launch_conv_pack(const ConvPlan& cp, const void* a, const void* b, v
   if (e != cudaSuccess) return e;
   const int fb = static_cast<int>(std::min<long long>((cp.K * kp + 255) / 256, 1024));
   conv_pack_filter_kernel<<<fb, 256, 0, s>>>(static_cast<const std::int8_t*>(b), static_cast<std::int8_t*>(pb),
-                                             static_cast<int>(cp.K), static_cast<int>(cp.C), static_cast<int>(cp.S),
-                                             rsc, kp, cp.b_i, cp.b_j, cp.b_k, cp.b_c, cp.b0);
+                                             static_cast<int>(cp.K), static_cast<int>(cp.C), static_cast<int>(cp.R),
+                                             static_cast<int>(cp.S), 0, kp, cp.b_i, cp.b_j, cp.b_k, cp.b_c, cp.b0);
   return cudaGetLastError();
 }
 
 const char* conv_igemm_unsupported(const ConvPlan& cp) {
+  if (cp.packed) {
+    // gather mode: the kernel builds A rows from the original input; the GEMM is packed_view
+    if (cp.pack_run && (cp.a_y != cp.C || cp.S * cp.C > cp.pack_run || (cp.pack_run != 16 && cp.pack_run != 32 &&
+                                                                          cp.pack_run != 64)))
+      return "run layout needs contiguous pixels";
+    if (cp.R > 127 || cp.S > 127 || cp.pack_k > 1024 || cp.pack_k % 64 ||
+        cp.a_x * (cp.R - 1) + cp.a_y * (cp.S - 1) + cp.C >= (1ll << 30))
+      return "gathered taps out of range";
+    return conv_igemm_unsupported(packed_view(cp));
+  }
   Geometry g;
   if (!geometry(cp, &g)) return "padding halo outside the im2col corner range";
   if (cp.C % 64 != 0) return "channels not a multiple of 64";
@@ -669,6 +866,7 @@ const char* conv_igemm_unsupported(const ConvPlan& cp) {
   if (cp.R * cp.S * cp.C * 128 * 128 >= (1ll << 31)) return "reduction too long for exact s32 accumulation";
   if (cp.epi_vec && cp.K > kMaxVecK) return "epilogue vector longer than 2048";
   if (cp.epi_res && (cp.res_pix % 16 || cp.res_c0 % 16)) return "residual rows not 16-byte aligned";
+
   return nullptr;
 }
 
@@ -694,7 +892,7 @@ cudaError_t launch_conv_igemm(const ConvPlan& cp, const ConvArgs& args, cudaStre
   const int tiles = kp.tiles_m * kp.tiles_n;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(tiles < num_sms ? tiles : num_sms));
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(kp.gather ? kThreadsGather : kThreads);
   cfg.dynamicSmemBytes = static_cast<unsigned>(kp.smem);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];

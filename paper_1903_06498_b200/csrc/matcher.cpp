@@ -722,7 +722,7 @@ bool fuse_conv_epilogue(Plan* plan, std::size_t s, const Program& prog, const Pl
   e.fresh_output = true;  // the consumer overwrites (assign) or adds onto the fused identity 0
   e.overwrites = overwrite;
   if (cl.kernel == KernelKind::ConvIgemmTC
-          ? conv_igemm_unsupported(e.packed ? packed_view(e) : e) != nullptr
+          ? conv_igemm_unsupported(e) != nullptr
           : conv_tc_unsupported(e) != nullptr)
     return false;
   c = e;
@@ -766,25 +766,23 @@ namespace {
 bool try_packed_conv(Plan* plan, ConvPlan* cp) {
   const std::int64_t rsc = cp->R * cp->S * cp->C;
   if (rsc > 1024 || cp->C % 64 == 0) return false;
-  const std::int64_t kp = (rsc + 63) / 64 * 64;
   ConvPlan c = *cp;
   c.packed = true;
+  // run layout when each tap row's S*C bytes are contiguous in the input (dense pixels)
+  const std::int64_t sc = c.S * c.C;
+  c.pack_run = (c.a_y == c.C && sc <= 64) ? (sc <= 16 ? 16 : sc <= 32 ? 32 : 64) : 0;
+  const std::int64_t kp = c.pack_run ? (c.R * c.pack_run + 63) / 64 * 64 : (rsc + 63) / 64 * 64;
   c.pack_k = kp;
   const std::int64_t pixels = c.N * c.H * c.W;
-  c.pack_a = static_cast<int>(plan->bufs.size());
-  c.pack_b = c.pack_a + 1;
-  if (conv_igemm_unsupported(packed_view(c))) return false;
-  PBuffer a;
-  a.name = "pack:" + plan->bufs[c.a_buf].name;
-  a.dtype = DType::I8;
-  a.kind = kI8;
-  a.elements = pixels * kp;
+  c.pack_a = -1;  // A rows are gathered in the kernel (no packed copy in HBM)
+  c.pack_b = static_cast<int>(plan->bufs.size());
+  if (conv_igemm_unsupported(c)) return false;
+  (void)pixels;
   PBuffer b;
   b.name = "pack:" + plan->bufs[c.b_buf].name;
   b.dtype = DType::I8;
   b.kind = kI8;
   b.elements = c.K * kp;
-  plan->bufs.push_back(a);
   plan->bufs.push_back(b);
   *cp = c;
   return true;

@@ -127,6 +127,7 @@ struct ConvPlan {
   bool packed = false;
   int pack_a = -1, pack_b = -1;
   std::int64_t pack_k = 0;
+  std::int64_t pack_run = 0;  // >0: kk = i * pack_run + (j * C + c) (contiguous S*C-byte runs per tap row)
 };
 
 // The 1x1 conv over the packed operands of a `packed` conv (same output and epilogue).

@@ -115,3 +115,34 @@ def test_fused_small_pinned_against_port():
     prog, inp, out = run(text, seed=9)
     ref = Port.execute(text, {**inp, "O": np.zeros_like(out["O"])})
     np.testing.assert_array_equal(out["O"], ref["O"])
+
+
+SMALL_C = [
+    # N, H, W, C, K, R, S, stride, pad  (gather mode: taps x channels packed per pixel in smem)
+    (2, 32, 32, 3, 64, 7, 7, 2, 3),       # ResNet stem shape
+    (1, 9, 13, 16, 96, 3, 3, 1, 1),
+    (2, 10, 10, 24, 128, 5, 5, 2, 2),
+    (1, 8, 8, 3, 200, 3, 3, 1, 0),        # no padding, K > 128
+]
+
+
+@pytest.mark.parametrize("shape", SMALL_C, ids=lambda s: "x".join(map(str, s)))
+def test_gather_conv_exact(shape):
+    import paper_1903_06498_b200 as sb
+    from paper_1903_06498_b200 import workloads as W
+    from intmodel import conv_exact, wrap
+    N, H, Wd, C, K, R, S, st, pad = shape
+    text = W.conv2d(N, H, Wd, C, K, R, S, pad=pad, stride=st)
+    plan = sb.parse_program(text).describe_plan()
+    assert "packed" in plan, plan
+    prog, inp, out = run(text, seed=sum(shape))
+    exp = wrap(32, conv_exact(inp["I"].reshape(N, H, Wd, C), inp["F"].reshape(R, S, K, C), st, pad, "cuda"))
+    np.testing.assert_array_equal(out["O"], exp.cpu().numpy().ravel())
+
+
+def test_gather_stem_fused_vs_port():
+    from paper_1903_06498_b200 import workloads as W
+    text = W.conv_fused(1, 12, 12, 3, 64, 7, 7, 2, 3)
+    prog, inp, out = run(text, seed=21)
+    ref = Port.execute(text, {**inp, "O": np.zeros_like(out["O"])})
+    np.testing.assert_array_equal(out["O"], ref["O"])
