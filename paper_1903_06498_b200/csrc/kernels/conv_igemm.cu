@@ -65,6 +65,7 @@ struct IgKParams {
   int pdl;
   // fused epilogue: out = wrap(max(acc + vec[k], lo))
   int epi, epi_vec, epi_lo, epi_res, vec_kind;
+  int fast_clamp;  // |acc| + 128 < 2^31: clamp decided by an int32 compare against lo - vec[k]
   const void* vec;
   long long vec_k;
   long long lo;
@@ -356,14 +357,23 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
     const int row = quarter * 32 + lane;
     const int sw = row & 7;  // 128B swizzle phase of this staging row
     const bool leader = threadIdx.x == 64;
-    if (p.epi_vec) {
-      // per-output-channel vector (e.g. the bias) as int32 in smem, read with ld.shared.v4
+    std::int32_t* thr_s = vec_s + kMaxVecK;
+    if (p.epi_vec || p.fast_clamp) {
+      // per-output-channel vector (e.g. the bias) as int32 in smem, read with ld.shared.v4; with
+      // fast_clamp also the threshold t[k] = clamp32(lo - vec[k]): acc + res + vec >= lo
+      // <=> acc + res >= t[k] exactly, because |acc + res| < 2^31 - 1
       if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
       for (int k = threadIdx.x - 64; k < p.N; k += 128) {
         const long long vi = static_cast<long long>(k) * p.vec_k;
-        vec_s[k] = p.vec_kind == kI8 ? static_cast<const std::int8_t*>(p.vec)[vi]
-                   : p.vec_kind == kI16 ? static_cast<const std::int16_t*>(p.vec)[vi]
-                                        : static_cast<const std::int32_t*>(p.vec)[vi];
+        const std::int32_t b = !p.epi_vec ? 0
+                               : p.vec_kind == kI8 ? static_cast<const std::int8_t*>(p.vec)[vi]
+                               : p.vec_kind == kI16 ? static_cast<const std::int16_t*>(p.vec)[vi]
+                                                    : static_cast<const std::int32_t*>(p.vec)[vi];
+        vec_s[k] = b;
+        if (p.fast_clamp) {
+          const long long t = p.lo - b;
+          thr_s[k] = static_cast<std::int32_t>(t < INT_MIN ? INT_MIN : t > INT_MAX ? INT_MAX : t);
+        }
       }
     }
     if (p.epi_res && leader && p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -410,7 +420,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
           int bv[32];
 #pragma unroll
           for (int q = 0; q < 8; q++) {
-            if (p.epi_vec)
+            if (p.epi_vec || p.fast_clamp)
               asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                            : "=r"(bv[4 * q]), "=r"(bv[4 * q + 1]), "=r"(bv[4 * q + 2]), "=r"(bv[4 * q + 3])
                            : "r"(smem_u32(vec_s + (kbase + 4 * q < p.N ? kbase + 4 * q : 0))));
@@ -434,6 +444,21 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
                                                       static_cast<std::int32_t>(static_cast<std::int8_t>(rw[q >> 2] >> (8 * (q & 3)))))
                                                 : 0u;
               v[q] = v[q] + static_cast<std::uint32_t>(bv[q]) + r;
+            }
+          } else if (p.fast_clamp) {
+            int tv[32];
+#pragma unroll
+            for (int q = 0; q < 8; q++)
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(tv[4 * q]), "=r"(tv[4 * q + 1]), "=r"(tv[4 * q + 2]), "=r"(tv[4 * q + 3])
+                           : "r"(smem_u32(thr_s + (kbase + 4 * q < p.N ? kbase + 4 * q : 0))));
+            const std::uint32_t lo32 = static_cast<std::uint32_t>(p.lo);
+#pragma unroll
+            for (int q = 0; q < 32; q++) {
+              const std::int32_t r = p.epi_res ? static_cast<std::int32_t>(static_cast<std::int8_t>(rw[q >> 2] >> (8 * (q & 3))))
+                                               : 0;
+              const std::int32_t ar = static_cast<std::int32_t>(v[q]) + r;
+              v[q] = ar >= tv[q] ? static_cast<std::uint32_t>(ar) + static_cast<std::uint32_t>(bv[q]) : lo32;
             }
           } else if (relu0) {
             // exact x = acc + vec (+ res) as a 64-bit (hi:lo) carry chain; ReLU keeps lo iff hi >= 0
@@ -643,6 +668,10 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
   kp.epi_vec = cp.epi_vec ? 1 : 0;
   kp.epi_lo = cp.epi_lo ? 1 : 0;
   kp.epi_res = cp.epi_res ? 1 : 0;
+  {
+    const long long taps = cp.packed ? cp.R * cp.S * cp.C : gp.R * gp.S * gp.C;
+    kp.fast_clamp = cp.epi_lo && cp.K <= kMaxVecK && taps * 128 * 128 + 128 < (1ll << 31) - 1 ? 1 : 0;
+  }
   kp.lo = cp.lo;
   kp.vec_k = cp.vec_k;
   kp.vec_kind = args.vec_kind;
@@ -660,7 +689,7 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     // dynamic smem: A/B ring (up to 128 KB) | output staging | residual tiles | vector | barriers
     const int stg = kp.tma_out == 1 ? kStgBytes : kp.tma_out == 2 ? 2 * 16384 : 0;
     const int res = kp.epi_res ? 2 * kResBytes : 0;
-    const int vec = kp.epi_vec ? kVecBytes : 0;
+    const int vec = kp.fast_clamp ? 2 * kVecBytes : kp.epi_vec ? kVecBytes : 0;
     const int tab = kp.gather ? (kp.kblocks * kp.bk * 6 + 15) / 16 * 16 : 0;
     const int stage = 2 * BM * g.bk;
     int ring = std::min(kRingBytes, (kSmemMax - 1024 - 512 - stg - res - vec - tab) / stage * stage);

@@ -584,9 +584,16 @@ bool fuse_conv_epilogue(Plan* plan, std::size_t s, const Program& prog, const Pl
   const std::int64_t K = c.K, HW = c.H * c.W, NHW = c.N * HW;
   if (!(c.c0 == 0 && c.c_y == K && (c.H == 1 || c.c_x == c.W * K) && (c.N == 1 || c.c_n == HW * K))) return false;
   if (el.dims.size() != 2) return false;
+  // channel dim: unit coefficient in the consumer's read of T (ranges alone are ambiguous
+  // when the pixel count equals K)
   int pd = -1, kd = -1;
-  for (int d = 0; d < 2; d++) (el.dims[d].range == K ? kd : pd) = d;
-  if (pd < 0 || kd < 0 || el.dims[pd].range != NHW) return false;
+  for (const auto& a : el.acc)
+    if (a.buf == T)
+      for (int d = 0; d < 2; d++)
+        if (a.addr.at(d) == 1) kd = d;
+  if (kd < 0) return false;
+  pd = 1 - kd;
+  if (el.dims[kd].range != K || el.dims[pd].range != NHW) return false;
   // symbolic evaluation of the body: each temp is ACC, VEC (per-k vector), RES (per-element
   // residual), CONST or an op on them
   struct Sym {

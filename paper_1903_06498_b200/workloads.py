@@ -47,7 +47,7 @@ def conv2d(N, H, W, C, K, R=3, S=3, in_dtype="i8", out_dtype="i32", pad=1, strid
 """.replace("\n\n", "\n")
 
 
-def conv_fused(N, H, W, C, K, R=3, S=3, stride=1, pad=1, relu=True, residual=False, out_dtype="i8"):
+def conv_fused(N, H, W, C, K, R=3, S=3, stride=1, pad=1, relu=True, residual=False, out_dtype="i8", lo=0):
     """One conv layer in the fused/localized form (conv_layer): O = wrap(max(conv + Bias (+ Res), 0))."""
     P = (H + 2 * pad - R) // stride + 1
     Q = (W + 2 * pad - S) // stride + 1
@@ -56,7 +56,7 @@ def conv_fused(N, H, W, C, K, R=3, S=3, stride=1, pad=1, relu=True, residual=Fal
     B = Buf("Bias", "i32", (K,))
     O = Buf("O", out_dtype, (N, P, Q, K))
     Rz = Buf("Res", "i8", (N, P, Q, K)) if residual else None
-    body, _ = conv_layer(I, O, F, B, N, H, W, C, K, R, S, stride, pad, relu, Rz, ind=1)
+    body, _ = conv_layer(I, O, F, B, N, H, W, C, K, R, S, stride, pad, relu, Rz, ind=1, lo=lo)
     refs = [I.ref("in"), F.ref("in"), B.ref("in")] + ([Rz.ref("in")] if Rz else []) + [O.ref("out", agg="assign")]
     return "\n".join(["block []:1 ("] + [f"\t{r}" for r in refs] + [") {", "\t0:", f"\t{body}", "}", ""])
 
@@ -283,7 +283,7 @@ def _block(idx, cons, refs, body, ind):
 
 
 def conv_layer(src, dst, w, b, N, H, W, C, K, R, S, stride, pad, relu=True, residual=None, ind=1,
-               acc_dtype="i32", tname="T"):
+               acc_dtype="i32", tname="T", lo=0):
     """One conv + bias (+ residual) (+ ReLU) as the fuse/localize passes leave it
     (test_passes.cpp:357-379): a wrapper block owning the local accumulator T,
     statement 0 the conv leaf into T (add), statement 1 the element-wise epilogue
@@ -312,7 +312,7 @@ def conv_layer(src, dst, w, b, N, H, W, C, K, R, S, stride, pad, relu=True, resi
         body += [f"$r = load({residual.name})", "$u = add($s, $r)"]
         v = "$u"
     if relu:
-        body += ["$z = constant(0)", f"$o = max({v}, $z)"]
+        body += [f"$z = constant({lo})", f"$o = max({v}, $z)"]
         v = "$o"
     epi_refs.append(dst.point("out", ["n", "x", "y", "k"], "assign"))
     body.append(f"{dst.name} = store({v})")

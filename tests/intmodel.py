@@ -27,7 +27,7 @@ def conv_exact(x_nhwc, w_rskc, stride, pad, device):
     return o.permute(0, 2, 3, 1).round().long()
 
 
-def conv_layer_exact(x, w, b, stride, pad, relu=True, residual=None, out_bits=8, device="cuda"):
+def conv_layer_exact(x, w, b, stride, pad, relu=True, residual=None, out_bits=8, device="cuda", lo=0):
     """conv_layer semantics: T = wrap32(conv); out = wrap_out(max(T + b (+ res), 0))."""
     import torch
     t = wrap(32, conv_exact(x, w, stride, pad, device))
@@ -35,7 +35,7 @@ def conv_layer_exact(x, w, b, stride, pad, relu=True, residual=None, out_bits=8,
     if residual is not None:
         s = s + residual.long()
     if relu:
-        s = torch.clamp(s, min=0)
+        s = torch.clamp(s, min=lo)
     return wrap(out_bits, s)
 
 

@@ -109,6 +109,27 @@ def test_igemm_fused_epilogue_i8(case):
     np.testing.assert_array_equal(out["O"], exp)
 
 
+@pytest.mark.parametrize("lo", [-5, 1000, -(1 << 33), (1 << 33)])
+def test_igemm_fused_clamp_constants(lo):
+    """max(x, lo) with lo away from 0 and outside the i32 range (int64 temps)."""
+    import paper_1903_06498_b200 as sb
+    from paper_1903_06498_b200 import workloads as W
+    from intmodel import conv_layer_exact
+    import torch
+    N, H, Wd, C, K = 2, 8, 8, 64, 128
+    for res in (False, True):
+        for od, bits in (("i8", 8), ("i32", 32)):
+            if res and od == "i32":
+                continue
+            text = W.conv_fused(N, H, Wd, C, K, 3, 3, 1, 1, relu=True, residual=res, out_dtype=od, lo=lo)
+            assert "fused" in sb.parse_program(text).describe_plan()
+            prog, inp, out = run(text, seed=lo & 0xFFFF)
+            r = torch.as_tensor(inp["Res"].reshape(N, H, Wd, K), device="cuda") if res else None
+            exp = conv_layer_exact(inp["I"].reshape(N, H, Wd, C), inp["F"].reshape(3, 3, K, C), inp["Bias"], 1, 1,
+                                   True, r, bits, "cuda", lo=lo).cpu().numpy().ravel()
+            np.testing.assert_array_equal(out["O"], exp, err_msg=f"lo={lo} res={res} out={od}")
+
+
 def test_fused_small_pinned_against_port():
     from paper_1903_06498_b200 import workloads as W
     text = W.conv_fused(1, 6, 6, 64, 128, 3, 3, 2, 1)
