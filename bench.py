@@ -15,6 +15,10 @@ e2e    : same metric through the public API (sb_execute) from pinned host
          buffers: H2D of I and F and D2H of O inside the timed region.
 --impl reference: the reference interpreter (oracle/_ref, stripe::execute) on
          the host cores over a bounded sample of the same workload.
+
+--config c5: BASELINE config 5 instead -- the ResNet-50-shaped Stripe program
+         (workloads.resnet50), 128 images per GPU (batch 1024 over 8 GPUs, sharded on
+         the batch index, no collective).  value = useful GFLOP/s of the whole network.
 """
 import argparse
 import ctypes
@@ -153,9 +157,66 @@ def cpu_reference(samples_rows=8, threads=None, steps=1, warmup=0):
     return gflops, threads, sample, times
 
 
+def cpu_reference_resnet(threads=None, steps=1, warmup=0):
+    """Reference interpreter on a bounded sample of config 5: concurrent executions (one per
+    host thread) of the full-width ResNet-50 program on one 32x32 image (1.4e8 useful MACs
+    after the stem), i.e. the same layer mix at 1/49 of the spatial work."""
+    import numpy as np
+
+    from oracle import Ref, random_inputs
+    from paper_1903_06498_b200 import workloads as Wk
+    threads = threads or os.cpu_count() or 1
+    text, info = Wk.resnet50(1, image=32)
+    L = Ref.lib()
+    prog = Ref.parse(text)
+    bufs = prog.buffers()
+    inputs = random_inputs(bufs, 1005)
+    times = []
+    for it in range(warmup + steps):
+        progs = (ctypes.c_void_p * threads)(*([prog.h] * threads))
+        stores = []
+        for t in range(threads):
+            s = L.sr_store_new()
+            for n, bits, el, d in bufs:
+                arr = inputs[n] if n in inputs else np.zeros(el, np.int64)
+                L.sr_store_set(s, n.encode(), bits, arr.ctypes.data, arr.size)
+            stores.append(s)
+        st = (ctypes.c_void_p * threads)(*stores)
+        t0 = time.perf_counter()
+        bad = L.sr_execute_many(progs, st, threads, threads)
+        dt = time.perf_counter() - t0
+        for s in stores:
+            L.sr_store_free(s)
+        if bad:
+            raise RuntimeError("reference execute failed")
+        if it >= warmup:
+            times.append(dt)
+    gflops = info["flops"] * threads / (sum(times) / len(times)) / 1e9
+    sample = (f"{threads} concurrent stripe::execute runs (one per host thread) of the config-5 ResNet-50 program "
+              f"at 32x32 image, batch 1 ({info['macs']} useful MACs each)")
+    return gflops, threads, sample, times
+
+
 def run_reference_arm(args):
     world, rank, _ = dist_setup()
     if rank != 0:
+        return
+    if args.config == "c5":
+        from oracle import Ref
+        if not Ref.available():
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libstripe_ref.so not built"}))
+            return
+        gflops, cores, sample, times = cpu_reference_resnet(steps=args.steps, warmup=min(args.warmup, 1))
+        print(json.dumps({
+            "metric": METRIC, "value": round(gflops, 4), "unit": "GFLOP/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1000 * sum(times) / len(times), 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "i8xi8->i32 (int64 carriers)", "data": "synthetic (random_inputs, seed 1005)",
+            "config": {"workload": "BASELINE config 5: ResNet-50 Stripe program", "sample": "32x32 image"},
+            "cpu_baseline": {"value": round(gflops, 4), "unit": "GFLOP/s", "cores": cores, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": round(gflops, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }))
         return
     from oracle import Ref
     if not Ref.available():
@@ -363,6 +424,151 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_ours_resnet(args):
+    """Config 5: ResNet-50 program, 128 images per GPU, weak scaling over batch shards."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1903_06498_b200 as sb
+    from paper_1903_06498_b200 import workloads as Wk
+
+    world, rank, local = dist_setup()
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+    per_gpu = args.batch_per_gpu
+    text, info = Wk.resnet50(per_gpu)
+    prog = sb.parse_program(text)
+    ctx = sb.Context(local)
+    ctx.set_stream(stream.cuda_stream)
+    flops_step = float(info["flops"])
+    nbytes = {n: d.elements * {8: 1, 16: 2, 32: 4}[d.dtype] for n, d in prog.buffers.items()}
+    in_names = [n for n, d in prog.buffers.items() if int(d.dir) == 0]
+    alg_bytes = sum(nbytes.values())
+    # two input/output sets: each step's activations (> 1 GB of scratch) flush L2 anyway
+    g = torch.Generator(device=dev).manual_seed(1005 + rank)
+    sets = []
+    for _ in range(2):
+        bufs, keep = {}, []
+        for n, d in prog.buffers.items():
+            t = torch.randint(-128, 128, (nbytes[n],), dtype=torch.int8, device=dev, generator=g)
+            keep.append(t)
+            bufs[n] = (t.data_ptr(), d.elements, sb.SB_BUF_PREPARE if int(d.dir) != 0 else 0)
+        sets.append((bufs, keep))
+    bound = [ctx.bind_device(prog, b) for b, _ in sets]
+
+    def step(i):
+        bound[i % 2]()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    with torch.cuda.stream(stream):
+        clk = ClockSampler(local).__enter__()
+        clk.wait_first_sample()
+        for i in range(args.warmup):
+            step(i)
+        t_settle = time.perf_counter()
+        settle = 0
+        while time.perf_counter() - t_settle < 1.0:
+            step(settle)
+            settle += 1
+            torch.cuda.synchronize(dev)
+        ctx.sync()
+        graph = sb.Graph(ctx, lambda: [step(i) for i in range(args.steps)])
+        graph.launch()
+        torch.cuda.synchronize(dev)
+        barrier()
+        torch.cuda.synchronize(dev)
+        launches0 = ctx.launch_count
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        graph.launch()
+        t_end.record(stream)
+        torch.cuda.synchronize(dev)
+        clk.__exit__(None, None, None)
+        ctx.sync()
+        barrier()
+        torch.cuda.synchronize(dev)
+        launches = ctx.launch_count - launches0
+        elapsed_ms = t_start.elapsed_time(t_end)
+    t = torch.tensor([elapsed_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(t.item())
+    ms_per_step = elapsed_ms / args.steps
+    value = flops_step * world * args.steps / (elapsed_ms / 1e3) / 1e9
+
+    # end to end through sb_execute from pinned host buffers (every program input copied in,
+    # the logits copied out, each step)
+    ctx.set_stream(None)
+    host, pins = {}, []
+    for n, d in prog.buffers.items():
+        p = ctypes.c_void_p()
+        sb._check(sb.lib().sb_host_alloc_pinned(nbytes[n], ctypes.byref(p)))
+        pins.append(p)
+        ct = {8: ctypes.c_int8, 16: ctypes.c_int16, 32: ctypes.c_int32}[d.dtype]
+        host[n] = np.ctypeslib.as_array((ct * d.elements).from_address(p.value))
+    rng = np.random.default_rng(11 + rank)
+    for n in in_names:
+        host[n][:] = rng.integers(-128, 128, host[n].size).astype(host[n].dtype)
+    outs = tuple(n for n in prog.buffers if n not in in_names)
+    for _ in range(2):
+        ctx.execute_native(prog, host, prepare=outs)
+    barrier()
+    e2e_steps = max(3, min(args.steps, 10))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        ctx.execute_native(prog, host, prepare=outs)
+    te = torch.tensor([time.perf_counter() - t0], device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e = {"value": round(flops_step * world * e2e_steps / float(te.item()) / 1e9, 3), "unit": "GFLOP/s",
+           "h2d_bytes_per_step": int(sum(nbytes[n] for n in in_names)),
+           "d2h_bytes_per_step": int(sum(nbytes[n] for n in outs)), "steps": e2e_steps,
+           "timer": "host wall clock around synchronous sb_execute calls"}
+    for p in pins:
+        sb.lib().sb_host_free_pinned(p)
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
+        try:
+            from oracle import Ref
+            if Ref.available():
+                gf, cores, sample, _ = cpu_reference_resnet(steps=1, warmup=0)
+                cpu = {"value": round(gf, 4), "unit": "GFLOP/s", "cores": cores, "kind": "reference",
+                       "sample": sample}
+        except Exception as e:
+            cpu = {"value": None, "unit": "GFLOP/s", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
+    if rank == 0:
+        hbm_peak, bf16_peak, peak_kind = peaks()
+        tops = flops_step / (ms_per_step / 1e3) / 1e12
+        i8_peak = 2 * bf16_peak
+        print(json.dumps({
+            "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "i8xi8->i32",
+            "data": "synthetic (uniform random int8 image, weights, i32 biases in HBM)",
+            "config": {"workload": f"BASELINE config 5: ResNet-50 Stripe program (53 convs, max-pool, residuals, "
+                                   f"global sum, fc), {per_gpu} images per GPU",
+                       "global_batch": per_gpu * world, "parallelism": f"batch-sharded x{world} (no collective)",
+                       "images_per_s": round(per_gpu * world / (ms_per_step / 1e3), 1),
+                       "l2": "activations > 1 GB per step (scratch arena) flush L2"},
+            "roofline": {"bound": "tensor", "achieved": round(tops, 2), "peak": round(i8_peak, 1), "unit": "TFLOP/s",
+                         "frac": round(tops / i8_peak, 4), "traffic": None,
+                         "peak_kind": f"dense int8 = 2 x {peak_kind} bf16 ({bf16_peak})",
+                         "note": "whole-network useful ops / step time (all 59 launches)"},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
+        }))
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -370,11 +576,15 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", default="c2", choices=["c2", "c5"])
+    ap.add_argument("--batch-per-gpu", type=int, default=128, help="config 5 images per GPU")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         run_reference_arm(args)
+    elif args.config == "c5":
+        run_ours_resnet(args)
     else:
         run_ours(args)
 
