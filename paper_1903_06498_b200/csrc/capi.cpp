@@ -176,6 +176,11 @@ std::vector<int> step_buffers(const sb::PStep& s) {
       break;
     case sb::KernelKind::GemmI8TC:
       out = {l.gemm.a_buf, l.gemm.b_buf, l.gemm.c_buf};
+      if (l.gemm.limbs_a) {
+        out.push_back(l.gemm.planes_a);
+        out.push_back(l.gemm.planes_b);
+        out.push_back(l.gemm.sums);
+      }
       break;
     case sb::KernelKind::Reduce:
       out = {l.reduce.in_buf, l.reduce.out_buf};
@@ -315,6 +320,22 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
       } else {
         cuda_check(sb::launch_conv_igemm(l.conv, a, ctx->stream, ctx->num_sms), "conv_igemm");
       }
+      ctx->launches++;
+      return;
+    }
+    if (l.kernel == sb::KernelKind::GemmI8TC && l.gemm.limbs_a) {
+      const sb::GemmPlan& g = l.gemm;
+      char* pa = static_cast<char*>(ptr_of(g.planes_a));
+      char* pb = static_cast<char*>(ptr_of(g.planes_b));
+      char* sums = static_cast<char*>(ptr_of(g.sums));
+      cuda_check(sb::launch_limb_split(g, ptr_of(g.a_buf), ptr_of(g.b_buf), pa, pb, ctx->stream), "limb_split");
+      ctx->launches += 2;
+      for (int t = 0; t <= sb::limb_smax(g); t++) {
+        sb::GemmArgs a{pa + sb::limb_a_off(g, t), pb + sb::limb_b_off(g, t), sums + 4ll * t * g.M * g.N};
+        cuda_check(sb::launch_gemm_tc(sb::limb_sum_plan(g, t), a, ctx->stream, ctx->num_sms), "gemm_tc(limb)");
+        ctx->launches++;
+      }
+      cuda_check(sb::launch_limb_combine(g, sums, ptr_of(g.c_buf), ctx->stream), "limb_combine");
       ctx->launches++;
       return;
     }

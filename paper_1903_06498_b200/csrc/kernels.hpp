@@ -41,6 +41,15 @@ struct GemmArgs {
   void* c;
 };
 const char* gemm_tc_unsupported(const GemmPlan& g);
+// byte-limb mode: split A/B into concatenated unsigned byte planes, and the final combine
+cudaError_t launch_limb_split(const GemmPlan& g, const void* a, const void* b, void* pa, void* pb, cudaStream_t s);
+cudaError_t launch_limb_combine(const GemmPlan& g, const void* sums, void* c, cudaStream_t s);
+// The u8 GEMM computing S_s inside a limb plan.
+GemmPlan limb_sum_plan(const GemmPlan& g, int s);
+long long limb_plane_bytes_a(const GemmPlan& g);
+long long limb_a_off(const GemmPlan& g, int s);
+long long limb_b_off(const GemmPlan& g, int s);
+long long limb_plane_bytes_b(const GemmPlan& g);
 cudaError_t launch_gemm_tc(const GemmPlan& g, const GemmArgs& args, cudaStream_t s, int num_sms);
 
 // Windowed max/min over constraint-bounded taps, 16-byte channel vectors (kernels/pool.cu).

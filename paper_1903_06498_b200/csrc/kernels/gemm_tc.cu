@@ -288,7 +288,7 @@ struct Prepared {
 
 bool same(const GemmPlan& x, const GemmPlan& y) {
   return std::memcmp(&x.M, &y.M, sizeof(long long) * 9) == 0 && x.b_kmajor == y.b_kmajor && x.fresh == y.fresh &&
-         x.c_dtype == y.c_dtype;
+         x.c_dtype == y.c_dtype && x.unsigned_ab == y.unsigned_ab;
 }
 
 std::mutex g_mu;
@@ -317,7 +317,8 @@ cudaError_t prepare(const GemmPlan& g, const GemmArgs& args, Prepared* out) {
   kp.tma_out = kp.fresh && kp.out_kind == kI32 && g.ldc % 4 == 0 &&
                reinterpret_cast<std::uintptr_t>(kp.c) % 16 == 0;
   // idesc: S32 accumulate, signed A/B, A K-major, B K- or MN-major, N = 128, M = 128
-  kp.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((kp.b_kmajor ? 0u : 1u) << 16) | ((128u >> 3) << 17) |
+  const std::uint32_t sgn = g.unsigned_ab ? 0u : 1u;  // atype/btype: 0 = U8, 1 = S8
+  kp.idesc = (2u << 4) | (sgn << 7) | (sgn << 10) | ((kp.b_kmajor ? 0u : 1u) << 16) | ((128u >> 3) << 17) |
              ((128u >> 4) << 24);
   cuuint32_t es[2] = {1, 1};
   const std::int8_t* a = static_cast<const std::int8_t*>(args.a) + g.a0;
@@ -370,12 +371,174 @@ cudaError_t prepare(const GemmPlan& g, const GemmArgs& args, Prepared* out) {
 }  // namespace
 
 const char* gemm_tc_unsupported(const GemmPlan& g) {
-  if (g.K * 128 * 128 >= (1ll << 31)) return "reduction too long for exact s32 accumulation";
+  if (g.limbs_a) {
+    if (g.K % 16 || (!g.b_kmajor && g.N % 16)) return "limb planes need 16-byte rows";
+    for (int s = 0; s <= limb_smax(g); s++)
+      if (const char* e = gemm_tc_unsupported(limb_sum_plan(g, s))) return e;
+    return nullptr;
+  }
+  const long long amax = g.unsigned_ab ? 255 * 255 : 128 * 128;
+  if (g.K * amax >= (1ll << 31)) return "reduction too long for exact s32 accumulation";
   if (g.lda % 16 || g.ldb % 16 || g.a0 % 16 || g.b0 % 16) return "operand rows not 16-byte aligned";
   if (g.M < 1 || g.N < 1 || g.K < 1) return "empty";
   if (g.lda < g.K || (g.b_kmajor ? g.ldb < g.K : g.ldb < g.N)) return "overlapping operand rows";
   return nullptr;
 }
+
+// ---- byte-limb mode ------------------------------------------------------------------------
+
+// Offsets (bytes) of sum s's concatenated A / B operands inside the plane buffers.
+long long limb_a_off(const GemmPlan& g, int s) {
+  long long o = 0;
+  for (int t = 0; t < s; t++) o += static_cast<long long>(limb_pairs(g, t)) * g.M * g.K;
+  return o;
+}
+long long limb_b_off(const GemmPlan& g, int s) {
+  long long o = 0;
+  for (int t = 0; t < s; t++) o += static_cast<long long>(limb_pairs(g, t)) * g.K * g.N;
+  return o;
+}
+
+namespace {
+
+__device__ __forceinline__ std::uint32_t elem_bits(const void* p, int kind, long long i) {
+  if (kind == kI8) return static_cast<std::uint32_t>(static_cast<const std::int8_t*>(p)[i]);
+  if (kind == kI16) return static_cast<std::uint32_t>(static_cast<const std::int16_t*>(p)[i]);
+  return static_cast<std::uint32_t>(static_cast<const std::int32_t*>(p)[i]);
+}
+
+struct SplitArgs {
+  const void* src;
+  std::uint8_t* dst;
+  int kind, limbs, smax, lb_other;  // lb_other: limbs of the other operand
+  long long rows, cols, ld, off;    // source matrix rows x cols (cols contiguous), element strides
+  long long pair_stride;            // bytes between pair segments inside one concatenated row/col
+  long long dst_ld;                 // bytes per destination row
+  int is_a, kcat_cols;              // A: pairs concatenate along cols (k); B: along rows or cols
+  long long sum_off[4];             // byte offset of each sum's operand
+  int pairs[4];
+};
+
+// Every source element's limb i goes to each sum s whose pair list contains it.
+__global__ void limb_split_kernel(SplitArgs a) {
+  const long long total = a.rows * a.cols;
+  for (long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; g < total;
+       g += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = g / a.cols, c = g - r * a.cols;
+    const std::uint32_t v = elem_bits(a.src, a.kind, a.off + r * a.ld + c);
+    for (int s = 0; s <= a.smax; s++) {
+      int p = 0;
+      for (int i = 0; i <= s; i++) {
+        const int j = s - i;
+        if (i >= (a.is_a ? a.limbs : a.lb_other) || j >= (a.is_a ? a.lb_other : a.limbs)) continue;
+        const int mine = a.is_a ? i : j;
+        const std::uint8_t byte = static_cast<std::uint8_t>(v >> (8 * mine));
+        // pair p occupies segment p along the concatenated axis
+        long long idx;
+        if (a.kcat_cols) idx = r * (a.pairs[s] * a.cols) + p * a.cols + c;  // [rows][pairs * cols]
+        else idx = (p * a.rows + r) * a.cols + c;                          // [pairs * rows][cols]
+        a.dst[a.sum_off[s] + idx] = byte;
+        p++;
+      }
+    }
+  }
+}
+
+__global__ void limb_combine_kernel(const std::int32_t* __restrict__ sums, void* c, int smax, long long M, long long N,
+                                    long long ldc, int out_kind, int fresh) {
+  const long long total = M * N;
+  for (long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; g < total;
+       g += static_cast<long long>(gridDim.x) * blockDim.x) {
+    std::uint32_t v = 0;
+    for (int s = 0; s <= smax; s++) v += static_cast<std::uint32_t>(sums[s * total + g]) << (8 * s);
+    const long long m = g / N, n = g - m * N, o = m * ldc + n;
+    if (out_kind == kI32) {
+      auto* p = static_cast<std::int32_t*>(c) + o;
+      *p = static_cast<std::int32_t>(fresh ? v : static_cast<std::uint32_t>(*p) + v);
+    } else if (out_kind == kI16) {
+      auto* p = static_cast<std::int16_t*>(c) + o;
+      *p = static_cast<std::int16_t>(fresh ? v : static_cast<std::uint32_t>(*p) + v);
+    } else {
+      auto* p = static_cast<std::int8_t*>(c) + o;
+      *p = static_cast<std::int8_t>(fresh ? v : static_cast<std::uint32_t>(*p) + v);
+    }
+  }
+}
+
+}  // namespace
+
+GemmPlan limb_sum_plan(const GemmPlan& g, int s) {
+  GemmPlan u = g;
+  u.limbs_a = u.limbs_b = 0;
+  u.unsigned_ab = true;
+  const int p = limb_pairs(g, s);
+  u.K = p * g.K;
+  u.lda = u.K;
+  u.a0 = 0;
+  u.ldb = g.b_kmajor ? u.K : g.N;
+  u.b0 = 0;
+  u.ldc = g.N;
+  u.c0 = 0;
+  u.c_dtype = DType::I32;
+  u.fresh = true;
+  return u;
+}
+
+cudaError_t launch_limb_split(const GemmPlan& g, const void* a, const void* b, void* pa, void* pb, cudaStream_t s) {
+  const int smax = limb_smax(g);
+  SplitArgs A{};
+  A.src = a;
+  A.dst = static_cast<std::uint8_t*>(pa);
+  A.kind = g.a_kind;
+  A.limbs = g.limbs_a;
+  A.lb_other = g.limbs_b;
+  A.smax = smax;
+  A.rows = g.M;
+  A.cols = g.K;
+  A.ld = g.lda;
+  A.off = g.a0;
+  A.is_a = 1;
+  A.kcat_cols = 1;
+  for (int t = 0; t <= smax; t++) {
+    A.sum_off[t] = limb_a_off(g, t);
+    A.pairs[t] = limb_pairs(g, t);
+  }
+  SplitArgs B = A;
+  B.src = b;
+  B.dst = static_cast<std::uint8_t*>(pb);
+  B.kind = g.b_kind;
+  B.limbs = g.limbs_b;
+  B.lb_other = g.limbs_a;
+  B.is_a = 0;
+  if (g.b_kmajor) {  // B[n][k]: pairs concatenate along k (columns)
+    B.rows = g.N;
+    B.cols = g.K;
+    B.kcat_cols = 1;
+  } else {  // B[k][n]: pairs stack along k (rows)
+    B.rows = g.K;
+    B.cols = g.N;
+    B.kcat_cols = 0;
+  }
+  B.ld = g.ldb;
+  B.off = g.b0;
+  for (int t = 0; t <= smax; t++) B.sum_off[t] = limb_b_off(g, t);
+  const int grid = 148 * 8;
+  limb_split_kernel<<<grid, 256, 0, s>>>(A);
+  limb_split_kernel<<<grid, 256, 0, s>>>(B);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_limb_combine(const GemmPlan& g, const void* sums, void* c, cudaStream_t s) {
+  const int ob = g.c_dtype == DType::I8 ? 1 : g.c_dtype == DType::I16 ? 2 : 4;
+  const int ok = g.c_dtype == DType::I8 ? kI8 : g.c_dtype == DType::I16 ? kI16 : kI32;
+  limb_combine_kernel<<<148 * 8, 256, 0, s>>>(static_cast<const std::int32_t*>(sums),
+                                              static_cast<char*>(c) + g.c0 * ob, limb_smax(g), g.M, g.N, g.ldc, ok,
+                                              g.fresh ? 1 : 0);
+  return cudaGetLastError();
+}
+
+long long limb_plane_bytes_a(const GemmPlan& g) { return limb_a_off(g, limb_smax(g) + 1); }
+long long limb_plane_bytes_b(const GemmPlan& g) { return limb_b_off(g, limb_smax(g) + 1); }
 
 cudaError_t launch_gemm_tc(const GemmPlan& g, const GemmArgs& args, cudaStream_t s, int num_sms) {
   Prepared* pr = nullptr;

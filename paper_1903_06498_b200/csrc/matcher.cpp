@@ -488,7 +488,9 @@ bool match_gemm(const Plan& plan, PLaunch& l, const Program& prog, const PlanOpt
   const PAccess* A = &l.acc[la.acc];
   const PAccess* B = &l.acc[lb.acc];
   const PAccess& C = l.acc[st.acc];
-  if (A->buf == C.buf || B->buf == C.buf || plan.bufs[A->buf].kind != kI8 || plan.bufs[B->buf].kind != kI8) return false;
+  auto intk = [](int k) { return k == kI8 || k == kI16 || k == kI32; };
+  if (A->buf == C.buf || B->buf == C.buf || !intk(plan.bufs[A->buf].kind) || !intk(plan.bufs[B->buf].kind))
+    return false;
   DType cdt = static_cast<DType>(st.dtype);
   if (cdt == DType::F32 || plan.bufs[C.buf].dtype != cdt) return false;
   if (l.dims.size() != 3) return false;
@@ -530,6 +532,18 @@ bool match_gemm(const Plan& plan, PLaunch& l, const Program& prog, const PlanOpt
   g.a_buf = A->buf;
   g.b_buf = B->buf;
   g.c_buf = C.buf;
+  {
+    const int ka = plan.bufs[A->buf].kind, kb = plan.bufs[B->buf].kind;
+    if (ka != kI8 || kb != kI8) {
+      // exact modulo 2^(8 * bytes(C)) on u8 tensor cores: each operand, sign-extended to the
+      // output width, is sum_i limb_i 256^i with unsigned byte limbs (narrower inputs included)
+      const int ob = cdt == DType::I8 ? 1 : cdt == DType::I16 ? 2 : 4;
+      g.limbs_a = ob;
+      g.limbs_b = ob;
+      g.a_kind = ka;
+      g.b_kind = kb;
+    }
+  }
   if (g.lda <= 0 || g.ldb <= 0 || g.ldc < g.N || g.a0 < 0 || g.b0 < 0 || g.c0 < 0) return false;
   if (g.a0 + g.lda * (g.M - 1) + g.K - 1 >= plan.bufs[A->buf].elements) return false;
   long long bmax = g.b_kmajor ? g.b0 + g.ldb * (g.N - 1) + g.K - 1 : g.b0 + g.ldb * (g.K - 1) + g.N - 1;
@@ -772,7 +786,8 @@ namespace {
 // Small-channel convs (C not a multiple of 64, e.g. the 7x7x3 stem): pack, then 1x1 igemm.
 bool try_packed_conv(Plan* plan, ConvPlan* cp) {
   const std::int64_t rsc = cp->R * cp->S * cp->C;
-  if (rsc > 1024 || cp->C % 64 == 0) return false;
+  // 1x1 contractions with few channels are plain GEMMs (gemm_tc takes ragged K directly)
+  if (rsc > 1024 || cp->C % 64 == 0 || cp->R * cp->S == 1) return false;
   ConvPlan c = *cp;
   c.packed = true;
   // run layout when each tap row's S*C bytes are contiguous in the input (dense pixels)
@@ -896,6 +911,18 @@ void match_kernels(Plan* plan, const Program& p, const PlanOptions& opt) {
           fused = fuse_conv_epilogue(plan, s, p, opt);
           if (!fused) plan->steps[s].launch.kernel = KernelKind::ConvI8TC;
         }
+        if (!fused && cp.R * cp.S == 1 && cp.H == 1 && cp.N == 1) {
+          // a plain matmul with nothing to fuse: the tiled GEMM kernel
+          PLaunch trial = plan->steps[s].launch;
+          trial.fused_fill_root = -1;
+          if (match_gemm(*plan, trial, p, opt, s)) {
+            trial.kernel = KernelKind::GemmI8TC;
+            if (!trial.gemm.limbs_a) {
+              plan->steps[s].launch = trial;
+              continue;
+            }
+          }
+        }
         if (!fused) fresh_scratch_output(plan, s);
         continue;
       }
@@ -912,6 +939,23 @@ void match_kernels(Plan* plan, const Program& p, const PlanOptions& opt) {
     }
     if (match_gemm(*plan, st.launch, p, opt, s)) {
       st.launch.kernel = KernelKind::GemmI8TC;
+      GemmPlan& g = st.launch.gemm;
+      if (g.limbs_a) {
+        auto scratch = [&](const std::string& name, std::int8_t kind, long long elems) {
+          PBuffer b;
+          b.name = name;
+          b.dtype = kind == kI8 ? DType::I8 : DType::I32;
+          b.kind = kind;
+          b.elements = elems;
+          plan->bufs.push_back(b);
+          return static_cast<int>(plan->bufs.size()) - 1;
+        };
+        g.planes_a = scratch("limbs:" + plan->bufs[g.a_buf].name, kI8, limb_plane_bytes_a(g));
+        g.planes_b = scratch("limbs:" + plan->bufs[g.b_buf].name, kI8, limb_plane_bytes_b(g));
+        g.sums = scratch("limbsums:" + plan->bufs[g.c_buf].name, kI32, (limb_smax(g) + 1) * g.M * g.N);
+        plan->notes.push_back("launch " + st.launch.path + ": matmul exact modulo 2^" + std::to_string(g.limbs_a * 8) +
+                              " as " + std::to_string(limb_smax(g) + 1) + " u8 tensor-core GEMMs over byte limbs");
+      }
       continue;
     }
     if (!why.empty())

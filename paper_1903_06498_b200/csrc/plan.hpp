@@ -12,6 +12,7 @@
 // slices of a zero-filled scratch buffer (interp.cpp:239-247, 442-447).
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -81,7 +82,26 @@ struct GemmPlan {
   bool b_kmajor = false, fresh = false;
   DType c_dtype = DType::I32;
   int a_buf = -1, b_buf = -1, c_buf = -1;
+  bool unsigned_ab = false;  // u8 x u8 operands (byte limbs)
+  // byte-limb mode (i16/i32 operands, exact modulo 2^(8*bytes(C))): A = sum_i a_i 256^i with
+  // unsigned byte planes; S_s = sum_{i+j=s} a_i b_j runs as ONE u8 GEMM per s over operands
+  // concatenated along k (planes_a / planes_b), C (+)= sum_s S_s << 8s wrapped at the store
+  int limbs_a = 0, limbs_b = 0, a_kind = 0, b_kind = 0;
+  int planes_a = -1, planes_b = -1, sums = -1;  // scratch buffers
 };
+
+// Number of (i, j) limb pairs with i + j = s.
+inline int limb_pairs(const GemmPlan& g, int s) {
+  int n = 0;
+  for (int i = 0; i < g.limbs_a; i++)
+    if (s - i >= 0 && s - i < g.limbs_b) n++;
+  return n;
+}
+// Output bytes that matter (sums s = 0 .. limb_smax).
+inline int limb_smax(const GemmPlan& g) {
+  const int ob = g.c_dtype == DType::I8 ? 1 : g.c_dtype == DType::I16 ? 2 : 4;
+  return std::min(ob, g.limbs_a + g.limbs_b - 1) - 1;
+}
 
 // Streaming reduce/copy ($v = load(I); O = store($v)): kernels/reduce.cu.
 struct ReducePlan {

@@ -65,3 +65,48 @@ def test_matmul_config1_shape_exact():
     B = rng.integers(-128, 128, size=(1024, 1024)).astype(np.int64)
     got = run_device(W.matmul(1024, 1024, 1024, "i8", "i32"), {"A": (8, A.ravel()), "B": (8, B.ravel())})
     np.testing.assert_array_equal(got["C"].reshape(1024, 1024), A @ B)
+
+
+# ---- byte-limb mode: i16 / i32 operands, exact modulo 2^bits(C) on u8 tensor cores ----------
+
+LIMB = [
+    # M, N, K, in dtype, out dtype, B transposed
+    (64, 48, 32, "i32", "i32", False),
+    (130, 96, 80, "i16", "i32", False),
+    (128, 64, 48, "i32", "i16", True),
+    (96, 112, 64, "i16", "i8", True),
+    (33, 16, 16, "i32", "i32", True),
+]
+
+
+@pytest.mark.parametrize("case", LIMB, ids=lambda c: "x".join(map(str, c)))
+def test_limb_gemm_vs_reference(case):
+    M, N, K, dt, od, bt = case
+    text = (W.matmul_bt if bt else W.matmul)(M, N, K, in_dtype=dt, out_dtype=od)
+    check(text, seed=M + N + K)
+    check(text, seed=M + N + K + 1, provide_out=True)
+
+
+def test_limb_gemm_config1_i32_exact():
+    """Config 1 in the reference's exact integer mode: 1024^3 i32 x i32 -> i32 (mod 2^32)."""
+    import torch
+    import paper_1903_06498_b200 as sb
+    text = W.matmul(1024, 1024, 1024, in_dtype="i32", out_dtype="i32")
+    p = sb.parse_program(text)
+    assert "byte limbs" in p.describe_plan(True)
+    rng = np.random.default_rng(1001)
+    a = rng.integers(-2**31, 2**31, 1024 * 1024, dtype=np.int64)
+    b = rng.integers(-2**31, 2**31, 1024 * 1024, dtype=np.int64)
+    store = {"A": sb.Buffer(32, a.copy()), "B": sb.Buffer(32, b.copy())}
+    sb.prepare_outputs(p, store)
+    sb.execute(p, store)
+    # exact reference: 16-bit halves on the GPU in float64 (every partial sum < 2^53)
+    A = torch.as_tensor(a.reshape(1024, 1024) & 0xFFFFFFFF, device="cuda")
+    B = torch.as_tensor(b.reshape(1024, 1024) & 0xFFFFFFFF, device="cuda")
+    al, ah = (A & 0xFFFF).double(), (A >> 16).double()
+    bl, bh = (B & 0xFFFF).double(), (B >> 16).double()
+    ll = (al @ bl).long()
+    mid = ((al @ bh) + (ah @ bl)).long()
+    c = (ll + (mid << 16)) & 0xFFFFFFFF
+    c = torch.where(c >= 2**31, c - 2**32, c).cpu().numpy().ravel()
+    np.testing.assert_array_equal(store["C"].data, c)
