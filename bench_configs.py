@@ -28,10 +28,11 @@ def configs(want=None):
     out = {}
     # C1: matmul 1024^3 (integer modes; the reference has no f32)
     M = N = Kd = 1024
-    for dt, od in (("i8", "i32"), ("i32", "i32")):
+    for dt, od in (("i8", "i32"), ("i32", "i32"), ("f32", "f32")):
         out[f"c1_matmul_{dt}"] = dict(text=W.matmul(M, N, Kd, in_dtype=dt, out_dtype=od),
                                       flops=2.0 * M * N * Kd,
                                       bytes=(M * Kd + Kd * N) * (1 if dt == "i8" else 4) + M * N * 4)
+    # (f32 inputs: torch.randint bytes reinterpreted as floats; finite values are not needed for timing)
     out["c2_conv"] = dict(text=W.conv2d(32, 56, 56, 64, 64), flops=2.0 * W.conv_useful_macs(32, 56, 56, 64, 64),
                           bytes=32 * 56 * 56 * 64 + 9 * 64 * 64 + 32 * 56 * 56 * 64 * 4)
     out["c3_conv_bias_relu"] = dict(text=W.conv_bias_relu(128, 56, 56, 64, 64),
@@ -71,7 +72,7 @@ def main():
         prog = sb.parse_program(cfg["text"])
         bufs, keep = {}, []
         for bn, d in prog.buffers.items():
-            nbytes = d.elements * {8: 1, 16: 2, 32: 4}[d.dtype]
+            nbytes = d.elements * {8: 1, 16: 2, 32: 4, 0x20F: 4}[d.dtype]
             t = torch.randint(-128, 128, (nbytes,), dtype=torch.int8, device="cuda")
             keep.append(t)
             bufs[bn] = (t.data_ptr(), d.elements, sb.SB_BUF_PREPARE if int(d.dir) != 0 else 0)

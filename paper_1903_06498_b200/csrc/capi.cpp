@@ -174,6 +174,7 @@ std::vector<int> step_buffers(const sb::PStep& s) {
         out.push_back(l.conv.pack_b);
       }
       break;
+    case sb::KernelKind::GemmF32:
     case sb::KernelKind::GemmI8TC:
       out = {l.gemm.a_buf, l.gemm.b_buf, l.gemm.c_buf};
       if (l.gemm.limbs_a) {
@@ -323,6 +324,13 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
       ctx->launches++;
       return;
     }
+    if (l.kernel == sb::KernelKind::GemmF32) {
+      cuda_check(sb::launch_gemm_f32(l.gemm, ptr_of(l.gemm.a_buf), ptr_of(l.gemm.b_buf), ptr_of(l.gemm.c_buf),
+                                     ctx->stream),
+                 "gemm_f32");
+      ctx->launches++;
+      return;
+    }
     if (l.kernel == sb::KernelKind::GemmI8TC && l.gemm.limbs_a) {
       const sb::GemmPlan& g = l.gemm;
       char* pa = static_cast<char*>(ptr_of(g.planes_a));
@@ -413,7 +421,7 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
   }
   cudaEventRecord(ev.back(), ctx->stream);
   cudaEventSynchronize(ev.back());
-  static const char* kinds[] = {"generic", "conv_i8_tc", "map", "reduce", "gemm_i8_tc", "conv_igemm_tc", "pool"};
+  static const char* kinds[] = {"generic", "conv_i8_tc", "map", "reduce", "gemm_i8_tc", "conv_igemm_tc", "pool", "gemm_f32"};
   for (std::size_t i = 0; i < plan.steps.size(); i++) {
     const auto& s = plan.steps[i];
     if (s.elided) continue;

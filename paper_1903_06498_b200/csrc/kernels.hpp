@@ -41,6 +41,8 @@ struct GemmArgs {
   void* c;
 };
 const char* gemm_tc_unsupported(const GemmPlan& g);
+// fp32 mode: exact-order SIMT GEMM, bitwise equal to the F32 oracle (kernels/gemm_f32.cu)
+cudaError_t launch_gemm_f32(const GemmPlan& g, const void* a, const void* b, void* c, cudaStream_t s);
 // byte-limb mode: split A/B into concatenated unsigned byte planes, and the final combine
 cudaError_t launch_limb_split(const GemmPlan& g, const void* a, const void* b, void* pa, void* pb, cudaStream_t s);
 cudaError_t launch_limb_combine(const GemmPlan& g, const void* sums, void* c, cudaStream_t s);

@@ -489,10 +489,13 @@ bool match_gemm(const Plan& plan, PLaunch& l, const Program& prog, const PlanOpt
   const PAccess* B = &l.acc[lb.acc];
   const PAccess& C = l.acc[st.acc];
   auto intk = [](int k) { return k == kI8 || k == kI16 || k == kI32; };
-  if (A->buf == C.buf || B->buf == C.buf || !intk(plan.bufs[A->buf].kind) || !intk(plan.bufs[B->buf].kind))
+  const bool f32 = l.is_float;
+  if (A->buf == C.buf || B->buf == C.buf) return false;
+  if (f32 ? (plan.bufs[A->buf].kind != kF32 || plan.bufs[B->buf].kind != kF32 || plan.bufs[C.buf].kind != kF32)
+          : (!intk(plan.bufs[A->buf].kind) || !intk(plan.bufs[B->buf].kind)))
     return false;
   DType cdt = static_cast<DType>(st.dtype);
-  if (cdt == DType::F32 || plan.bufs[C.buf].dtype != cdt) return false;
+  if ((cdt == DType::F32) != f32 || plan.bufs[C.buf].dtype != cdt) return false;
   if (l.dims.size() != 3) return false;
   auto roles = [&](const PAccess* a, const PAccess* b, int* m, int* n, int* k) {
     *m = *n = *k = -1;
@@ -532,7 +535,8 @@ bool match_gemm(const Plan& plan, PLaunch& l, const Program& prog, const PlanOpt
   g.a_buf = A->buf;
   g.b_buf = B->buf;
   g.c_buf = C.buf;
-  {
+  g.f32 = f32;
+  if (!f32) {
     const int ka = plan.bufs[A->buf].kind, kb = plan.bufs[B->buf].kind;
     if (ka != kI8 || kb != kI8) {
       // exact modulo 2^(8 * bytes(C)) on u8 tensor cores: each operand, sign-extended to the
@@ -549,7 +553,7 @@ bool match_gemm(const Plan& plan, PLaunch& l, const Program& prog, const PlanOpt
   long long bmax = g.b_kmajor ? g.b0 + g.ldb * (g.N - 1) + g.K - 1 : g.b0 + g.ldb * (g.K - 1) + g.N - 1;
   if (bmax >= plan.bufs[B->buf].elements) return false;
   if (g.c0 + g.ldc * (g.M - 1) + g.N - 1 >= plan.bufs[C.buf].elements) return false;
-  if (gemm_tc_unsupported(g)) return false;
+  if (!f32 && gemm_tc_unsupported(g)) return false;
   const PBuffer& cb = plan.bufs[C.buf];
   std::vector<int> pd = {m, n};
   if (cb.root && cb.root_index < static_cast<int>(opt.fresh_outputs.size()) && opt.fresh_outputs[cb.root_index] &&
@@ -938,7 +942,7 @@ void match_kernels(Plan* plan, const Program& p, const PlanOptions& opt) {
       why = std::string(bad_tc) + "; " + bad_ig;
     }
     if (match_gemm(*plan, st.launch, p, opt, s)) {
-      st.launch.kernel = KernelKind::GemmI8TC;
+      st.launch.kernel = st.launch.gemm.f32 ? KernelKind::GemmF32 : KernelKind::GemmI8TC;
       GemmPlan& g = st.launch.gemm;
       if (g.limbs_a) {
         auto scratch = [&](const std::string& name, std::int8_t kind, long long elems) {

@@ -62,7 +62,7 @@ struct PSpecial {
 };
 
 // Specialised kernel families the matcher can route a launch to.
-enum class KernelKind { Generic, ConvI8TC, Map, Reduce, GemmI8TC, ConvIgemmTC, Pool };
+enum class KernelKind { Generic, ConvI8TC, Map, Reduce, GemmI8TC, ConvIgemmTC, Pool, GemmF32 };
 
 // Windowed max/min (pooling) leaf: $v = load(I); O = store($v) with O:max|min, taps
 // bounded by interval constraints (kernels/pool.cu).
@@ -83,6 +83,7 @@ struct GemmPlan {
   DType c_dtype = DType::I32;
   int a_buf = -1, b_buf = -1, c_buf = -1;
   bool unsigned_ab = false;  // u8 x u8 operands (byte limbs)
+  bool f32 = false;          // fp32 numeric mode (kernels/gemm_f32.cu)
   // byte-limb mode (i16/i32 operands, exact modulo 2^(8*bytes(C))): A = sum_i a_i 256^i with
   // unsigned byte planes; S_s = sum_{i+j=s} a_i b_j runs as ONE u8 GEMM per s over operands
   // concatenated along k (planes_a / planes_b), C (+)= sum_s S_s << 8s wrapped at the store

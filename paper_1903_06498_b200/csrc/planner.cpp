@@ -756,7 +756,7 @@ Plan build_plan(const Program& p, const PlanOptions& opt) {
 std::string Plan::describe() const {
   std::ostringstream os;
   static const char* modes[] = {"owner", "atomic", "serial"};
-  static const char* kinds[] = {"generic", "conv_i8_tc", "map", "reduce", "gemm_i8_tc", "conv_igemm_tc", "pool"};
+  static const char* kinds[] = {"generic", "conv_i8_tc", "map", "reduce", "gemm_i8_tc", "conv_igemm_tc", "pool", "gemm_f32"};
   for (const auto& s : steps) {
     if (s.elided) os << "(elided) ";
     if (s.kind == PStep::Fill) {

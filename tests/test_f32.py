@@ -149,3 +149,59 @@ def test_f32_conv_vs_torch():
     w = torch.from_numpy(store["F"].data.reshape(3, 3, K, C)).permute(2, 3, 0, 1).double()
     o = torch.nn.functional.conv2d(x, w, padding=1).permute(0, 2, 3, 1).float().numpy().ravel()
     np.testing.assert_allclose(store["O"].data, o, rtol=1e-4, atol=1e-4)
+
+
+# ---- fp32 matmul (config 1 "fp32 matmul contraction") on the exact-order SIMT GEMM ----------
+
+GEMMS = [(64, 48, 32, False), (130, 96, 80, False), (200, 72, 333, True), (1, 1, 1, False)]
+
+
+def test_f32_gemm_planned():
+    import paper_1903_06498_b200 as sb
+    from paper_1903_06498_b200 import workloads as W
+    p = sb.parse_program(W.matmul(128, 128, 128, in_dtype="f32", out_dtype="f32"))
+    assert "kernel=gemm_f32" in p.describe_plan(True)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", GEMMS, ids=lambda c: "x".join(map(str, c)))
+def test_f32_gemm_bitwise_vs_oracle(case):
+    """Owner mode, k folded in order with rounded mul then add: bitwise equal to the oracle."""
+    if not gpu_available():
+        pytest.skip("no B200")
+    from paper_1903_06498_b200 import workloads as W
+    M, N, K, bt = case
+    text = (W.matmul_bt if bt else W.matmul)(M, N, K, in_dtype="f32", out_dtype="f32")
+    for accumulate in (False, True):
+        import paper_1903_06498_b200 as sb
+        prog = sb.parse_program(text)
+        store = random_f32_inputs(prog, M + K)
+        if accumulate:
+            store["C"] = sb.Buffer(prog.buffers["C"].dtype,
+                                   np.random.default_rng(1).standard_normal(M * N).astype(np.float32))
+        sb.prepare_outputs(prog, store)
+        ref = Port.execute(text, {n: b.data.copy() for n, b in store.items()}, f32=True)
+        sb.execute(prog, store)
+        np.testing.assert_array_equal(store["C"].data.view(np.uint32),
+                                      np.asarray(ref["C"], np.float32).view(np.uint32))
+
+
+@pytest.mark.gpu
+def test_f32_gemm_config1_vs_torch():
+    """1024^3 fp32: stated bound |c - exact| <= 1e-5 * sum_k |a||b| (sequential fp32 fold)."""
+    if not gpu_available():
+        pytest.skip("no B200")
+    import torch
+    import paper_1903_06498_b200 as sb
+    from paper_1903_06498_b200 import workloads as W
+    text = W.matmul(1024, 1024, 1024, in_dtype="f32", out_dtype="f32")
+    prog = sb.parse_program(text)
+    store = random_f32_inputs(prog, 1001)
+    sb.prepare_outputs(prog, store)
+    a = torch.as_tensor(store["A"].data.reshape(1024, 1024), device="cuda").double()
+    b = torch.as_tensor(store["B"].data.reshape(1024, 1024), device="cuda").double()
+    sb.execute(prog, store)
+    exact = (a @ b).cpu().numpy().ravel()
+    scale = (a.abs() @ b.abs()).cpu().numpy().ravel()
+    err = np.abs(store["C"].data.astype(np.float64) - exact)
+    assert np.all(err <= 1e-5 * scale), float((err / scale).max())
