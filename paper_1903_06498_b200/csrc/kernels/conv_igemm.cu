@@ -55,6 +55,7 @@ struct IgKParams {
   int smem;
   // gather mode (ConvPlan::packed): A rows built by warps 6-9 from the original input
   int gather, tab_off, rsc, g_C, g_S, g_R, g_run;
+  int epi_warps;  // 4 or 8 (two warps per TMEM lane quarter, each taking half the columns)
   long long g_an, g_ax, g_ay, g_a0;
   int g_ulo, g_uhi, g_vlo, g_vhi;
   const std::int8_t* g_in;
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
     }
     for (int a = 0; a < 2; a++) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], 32 * p.epi_warps);
     }
     mbar_init(&rfull[0], 1);
     mbar_init(&rfull[1], 1);
@@ -251,10 +252,10 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
         umma_commit(&tfull[acc]);
       }
     }
-  } else if (warp >= 6) {
+  } else if (warp >= 2 + p.epi_warps) {
     // gather producers: row r of every A stage = the packed (i, j, c) taps of pixel m0 + r,
     // zero where a constraint skips the tap; written in the TMA swizzle layout
-    const int gt = threadIdx.x - 192;  // 0..255: row r = gt / 2, half = gt % 2 splits each row's work
+    const int gt = threadIdx.x - 64 - 32 * p.epi_warps;  // 0..255: row r = gt / 2, half = gt % 2
     const int r = gt >> 1, half = gt & 1;
     std::int32_t* toff = reinterpret_cast<std::int32_t*>(base + p.tab_off);
     std::int8_t* tdi = reinterpret_cast<std::int8_t*>(toff + p.kblocks * p.bk);
@@ -353,8 +354,11 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       }
     }
   } else {
-    const int quarter = warp & 3;
+    const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31 (warp % 4 rule)
     const int row = quarter * 32 + lane;
+    const int ethreads = 32 * p.epi_warps;
+    const int hgroups = p.epi_warps / 4, hgroup = (warp - 2) / 4;  // column halves when 8 warps
+    const int h_lo = hgroup * (BN / 32) / hgroups, h_hi = (hgroup + 1) * (BN / 32) / hgroups;
     const int sw = row & 7;  // 128B swizzle phase of this staging row
     const bool leader = threadIdx.x == 64;
     std::int32_t* thr_s = vec_s + kMaxVecK;
@@ -363,7 +367,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       // fast_clamp also the threshold t[k] = clamp32(lo - vec[k]): acc + res + vec >= lo
       // <=> acc + res >= t[k] exactly, because |acc + res| < 2^31 - 1
       if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
-      for (int k = threadIdx.x - 64; k < p.N; k += 128) {
+      for (int k = threadIdx.x - 64; k < p.N; k += ethreads) {
         const long long vi = static_cast<long long>(k) * p.vec_k;
         const std::int32_t b = !p.epi_vec ? 0
                                : p.vec_kind == kI8 ? static_cast<const std::int8_t*>(p.vec)[vi]
@@ -377,7 +381,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       }
     }
     if (p.epi_res && leader && p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
-    asm volatile("bar.sync 1, 128;" ::: "memory");
+    asm volatile("bar.sync 1, %0;" ::"r"(ethreads) : "memory");
     const long long lo = p.epi_lo ? p.lo : LLONG_MIN;
     const bool relu0 = p.epi_lo && p.lo == 0;
     // residual tile [128 pixels x 128 channels] i8 of tile t into buffer b
@@ -399,7 +403,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
         // i32 staging is single-buffered, i8 staging double-buffered
         if (leader && p.tma_out == 1) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         if (leader && p.tma_out == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // staging and the older residual buffer are free
+        asm volatile("bar.sync 1, %0;" ::"r"(ethreads) : "memory");  // staging and the older residual buffer are free
       }
       if (p.epi_res && leader && t + static_cast<int>(gridDim.x) < tiles) load_res(t + gridDim.x, (iter + 1) & 1);
       mbar_wait(&tfull[acc], (iter >> 1) & 1);
@@ -408,7 +412,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       std::uint8_t* rcur = rstg + (iter & 1) * kResBytes;
       std::uint8_t* scur = p.tma_out == 2 ? stg + (iter & 1) * 16384 : stg;
       const int m = m0 + row;
-      for (int h = 0; h < BN / 32; h++) {
+      for (int h = h_lo; h < h_hi; h++) {
         std::uint32_t v[32];
         tmem_ld32(tmem_base + (static_cast<std::uint32_t>(quarter * 32) << 16) +
                       static_cast<std::uint32_t>(acc * BN + h * 32),
@@ -531,7 +535,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       mbar_arrive(&tempty[acc]);
       if (p.tma_out) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"r"(ethreads) : "memory");
         if (leader) {
           if (p.tma_out == 1) {
             for (int h = 0; h < BN / 32; h++)
@@ -640,6 +644,7 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
   kp.bk = g.bk;
   kp.cblocks = static_cast<int>(gp.C / g.bk);
   kp.kblocks = static_cast<int>(gp.R * gp.S) * kp.cblocks;
+  kp.epi_warps = cp.packed ? 4 : 8;
   if (cp.packed) {
     kp.gather = 1;
     kp.rsc = static_cast<int>(cp.R * cp.S * cp.C);
@@ -921,7 +926,7 @@ cudaError_t launch_conv_igemm(const ConvPlan& cp, const ConvArgs& args, cudaStre
   const int tiles = kp.tiles_m * kp.tiles_n;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(tiles < num_sms ? tiles : num_sms));
-  cfg.blockDim = dim3(kp.gather ? kThreadsGather : kThreads);
+  cfg.blockDim = dim3(64 + 32 * kp.epi_warps + (kp.gather ? 256 : 0));
   cfg.dynamicSmemBytes = static_cast<unsigned>(kp.smem);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
