@@ -1,0 +1,76 @@
+// oracle/dropin/dropin_test.cpp — TEST INFRASTRUCTURE: the drop-in check from the
+// reference's side.  Built against the UNMODIFIED reference sources (parser, interpreter,
+// tests/support.h random_inputs) and include/stripe_b200_binding.hpp; for each program
+// file given it runs stripe::execute (the reference) and stripe::b200::execute (the B200
+// executor through the C ABI) on the same random inputs and compares every buffer.
+//
+//   dropin_test [--seed S] prog1.stripe [prog2.stripe ...]
+// Prints one line per program ("OK <name>" / "DIFF <name> ..." / "ERR <name> code code");
+// exit status = number of mismatches.  Error parity: when the reference throws ExecError,
+// the binding must throw the same code.
+#include <cstdio>
+#include <cstdlib>
+#include <fstream>
+#include <sstream>
+#include <string>
+
+#include "stripe/interp.h"
+#include "stripe/text.h"
+#include "stripe_b200_binding.hpp"
+#include "support.h"
+
+int main(int argc, char** argv) {
+  std::uint64_t seed = 1001;
+  int bad = 0;
+  for (int i = 1; i < argc; i++) {
+    std::string arg = argv[i];
+    if (arg == "--seed" && i + 1 < argc) {
+      seed = std::strtoull(argv[++i], nullptr, 10);
+      continue;
+    }
+    std::ifstream f(arg);
+    std::stringstream ss;
+    ss << f.rdbuf();
+    stripe::Program prog;
+    try {
+      prog = stripe::parse_program(ss.str());
+    } catch (const std::exception& e) {
+      std::printf("SKIP %s parse: %s\n", arg.c_str(), e.what());
+      continue;
+    }
+    stripe::testing::Rng rng(seed);
+    stripe::BufferStore ref = stripe::testing::random_inputs(prog, &rng);
+    stripe::BufferStore dev = ref;
+    std::string ref_err, dev_err;
+    try {
+      stripe::execute(prog, &ref);
+    } catch (const stripe::ExecError& e) {
+      ref_err = e.code;
+    }
+    try {
+      stripe::b200::execute(prog, &dev);
+    } catch (const stripe::ExecError& e) {
+      dev_err = e.code;
+    }
+    if (!ref_err.empty() || !dev_err.empty()) {
+      const bool same = ref_err == dev_err;
+      std::printf("%s %s error ref=%s b200=%s\n", same ? "OK" : "ERR", arg.c_str(), ref_err.c_str(),
+                  dev_err.c_str());
+      bad += same ? 0 : 1;
+      continue;
+    }
+    std::string diff;
+    for (const auto& [name, buf] : ref) {
+      const auto it = dev.find(name);
+      if (it == dev.end() || it->second.data != buf.data) {
+        std::size_t first = 0;
+        if (it != dev.end())
+          while (first < buf.data.size() && buf.data[first] == it->second.data[first]) first++;
+        diff += " " + name + "@" + std::to_string(first);
+      }
+    }
+    std::printf("%s %s%s\n", diff.empty() ? "OK" : "DIFF", arg.c_str(), diff.c_str());
+    bad += diff.empty() ? 0 : 1;
+  }
+  return bad;
+}

@@ -63,6 +63,7 @@ struct ConvKParams {
   std::uint32_t idesc;
   int base_offset_mode;   // experimental: encode (addr >> 7) & 7 into the descriptor base offset
   int st_out;             // tma_out staging drained with coalesced LSU stores instead of TMA stores
+  int vec4;               // direct path: 16-byte aligned i32 rows (c0, strides multiples of 4)
   int cluster;            // CTAs per thread-block cluster (filter multicast)
   int debug_nofilt;       // timing experiments only
   int pdl;                // launched with programmatic stream serialization
@@ -481,7 +482,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                         static_cast<std::uint32_t>(acc * p.K + k0),
                     v);
           if (!valid) continue;
-          if (p.out_kind == kI32) {
+          if (p.out_kind == kI32 && p.fresh && p.vec4) {
+            // 16-byte stores straight from registers (no staging round trip through smem)
+            uint4* o4 = reinterpret_cast<uint4*>(static_cast<std::int32_t*>(out) + obase + k0);
+#pragma unroll
+            for (int q = 0; q < 8; q++)
+              o4[q] = make_uint4(epilogue(k0 + 4 * q, v[4 * q]), epilogue(k0 + 4 * q + 1, v[4 * q + 1]),
+                                 epilogue(k0 + 4 * q + 2, v[4 * q + 2]), epilogue(k0 + 4 * q + 3, v[4 * q + 3]));
+          } else if (p.out_kind == kI32) {
             std::int32_t* o = static_cast<std::int32_t*>(out) + obase + k0;
 #pragma unroll
             for (int q = 0; q < 32; q++)
@@ -637,6 +645,8 @@ cudaError_t prepare_conv(const ConvPlan& cp, const ConvArgs& args, Prepared* out
   if (const char* e = std::getenv("SB_CONV_BASEOFF")) kp.base_offset_mode = e[0] == '1';
   if (const char* e = std::getenv("SB_CONV_ST_OUT")) kp.st_out = e[0] == '1';
   kp.debug_nofilt = std::getenv("SB_CONV_DEBUG_NOFILT") != nullptr;
+  kp.vec4 = cp.c0 % 4 == 0 && cp.c_y % 4 == 0 && cp.c_x % 4 == 0 && cp.c_n % 4 == 0 &&
+            reinterpret_cast<std::uintptr_t>(args.c) % 16 == 0;
   if (std::getenv("SB_CONV_NO_TMA_OUT")) {
     kp.tma_out = 0;
     kp.staging_bytes = 0;
