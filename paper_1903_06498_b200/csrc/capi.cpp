@@ -77,6 +77,9 @@ struct Compiled {
   std::vector<sb::GenericDesc> descs;
   std::vector<std::vector<int>> bufmaps;
   std::vector<int> desc_of_step;
+  sb::LaneSchedule lanes;
+  std::vector<long long> arena_off, arena_bytes;  // scratch buffer -> arena range (-1: none)
+  std::size_t arena_total = 0;
 };
 
 }  // namespace
@@ -103,6 +106,11 @@ struct sb_context {
     std::vector<void*> scratch;  // by plan buffer id (scratch only; null when never touched)
   };
   std::map<std::uint64_t, State> states;  // by Compiled::id
+  cudaStream_t lane_streams[8] = {};       // statement-DAG lanes 1..7 (lane 0 = stream)
+  std::vector<cudaEvent_t> step_events;    // per plan step (reused across runs)
+  cudaEvent_t fork_event = nullptr, join_events[8] = {};
+  cudaStream_t aux_streams[4] = {};        // intra-step forks (byte-limb sums)
+  cudaEvent_t aux_fork = nullptr, aux_join[4] = {};
   std::vector<std::pair<void*, std::size_t>> roots;  // host-path device buffers
   std::vector<std::pair<void*, std::size_t>> pinned;  // host-path staging
 
@@ -118,6 +126,17 @@ struct sb_context {
     for (auto& r : pinned) cudaFreeHost(r.first);
     cudaFree(d_err);
     cudaFreeHost(h_err);
+    for (auto& s : lane_streams)
+      if (s) cudaStreamDestroy(s);
+    for (auto& e : step_events) cudaEventDestroy(e);
+    for (auto& s : aux_streams)
+      if (s) cudaStreamDestroy(s);
+    if (aux_fork) cudaEventDestroy(aux_fork);
+    for (auto& e : aux_join)
+      if (e) cudaEventDestroy(e);
+    if (fork_event) cudaEventDestroy(fork_event);
+    for (auto& e : join_events)
+      if (e) cudaEventDestroy(e);
     if (own) cudaStreamDestroy(own);
   }
 };
@@ -195,48 +214,11 @@ std::vector<int> step_buffers(const sb::PStep& s) {
   return out;
 }
 
-Compiled* get_plan(sb_program* p, const std::vector<bool>& fresh, bool tc) {
-  std::string key(tc ? "T" : "G");
-  for (bool f : fresh) key += f ? '1' : '0';
-  std::lock_guard<std::mutex> lock(p->mu);
-  auto it = p->plans.find(key);
-  if (it != p->plans.end()) return it->second.get();
-  auto c = std::make_unique<Compiled>();
-  c->id = g_next_plan_id++;
-  sb::PlanOptions opt;
-  opt.enable_tc = tc;
-  opt.fresh_outputs = fresh;
-  c->plan = sb::build_plan(p->prog, opt);
-  for (const auto& s : c->plan.steps) {
-    if (s.kind == sb::PStep::Launch &&
-        (s.launch.kernel == sb::KernelKind::Generic || s.launch.kernel == sb::KernelKind::Map)) {
-      c->desc_of_step.push_back(static_cast<int>(c->descs.size()));
-      c->descs.emplace_back();
-      c->bufmaps.emplace_back();
-      sb::to_desc(s.launch, &c->descs.back(), &c->bufmaps.back());
-    } else {
-      c->desc_of_step.push_back(-1);
-    }
-  }
-  Compiled* raw = c.get();
-  p->plans[key] = std::move(c);
-  return raw;
-}
-
-sb_context::State& ensure_state(sb_context* ctx, const Compiled* c) {
-  auto it = ctx->states.find(c->id);
-  if (it != ctx->states.end()) return it->second;
-  sb_context::State st;
-  if (!c->descs.empty()) {
-    cuda_check(cudaMalloc(&st.d_descs, sizeof(sb::GenericDesc) * c->descs.size()), "cudaMalloc(desc)");
-    cuda_check(cudaMemcpy(st.d_descs, c->descs.data(), sizeof(sb::GenericDesc) * c->descs.size(),
-                          cudaMemcpyHostToDevice),
-               "upload desc");
-  }
-  // Scratch (locals, spills) lives in one arena.  Offsets come from live intervals over
-  // the non-elided steps: buffers whose [first, last] step ranges are disjoint share
-  // bytes (greedy first-fit, largest first); locals a fused epilogue never materialises
-  // get nothing.
+// Scratch (locals, spills) lives in one arena.  Offsets come from live intervals over
+// the non-elided steps: buffers whose [first, last] step ranges are disjoint share bytes
+// (greedy first-fit, largest first); locals a fused epilogue never materialises get
+// nothing.  Shared bytes are dependencies for the lane scheduler (alias()).
+void layout_arena(Compiled* c) {
   const auto& plan = c->plan;
   const std::size_t nb = plan.bufs.size();
   std::vector<int> first(nb, -1), last(nb, -1);
@@ -273,10 +255,74 @@ sb_context::State& ensure_state(sb_context* ctx, const Compiled* c) {
     placed.push_back({b, off, need});
     total = std::max(total, off + need);
   }
+  c->arena_off.assign(nb, -1);
+  c->arena_bytes.assign(nb, 0);
+  for (const auto& q : placed) {
+    c->arena_off[q.buf] = static_cast<long long>(q.off);
+    c->arena_bytes[q.buf] = static_cast<long long>(q.bytes);
+  }
+  c->arena_total = total;
+}
+
+Compiled* get_plan(sb_program* p, const std::vector<bool>& fresh, bool tc) {
+  std::string key(tc ? "T" : "G");
+  for (bool f : fresh) key += f ? '1' : '0';
+  std::lock_guard<std::mutex> lock(p->mu);
+  auto it = p->plans.find(key);
+  if (it != p->plans.end()) return it->second.get();
+  auto c = std::make_unique<Compiled>();
+  c->id = g_next_plan_id++;
+  sb::PlanOptions opt;
+  opt.enable_tc = tc;
+  opt.fresh_outputs = fresh;
+  c->plan = sb::build_plan(p->prog, opt);
+  for (const auto& s : c->plan.steps) {
+    if (s.kind == sb::PStep::Launch &&
+        (s.launch.kernel == sb::KernelKind::Generic || s.launch.kernel == sb::KernelKind::Map)) {
+      c->desc_of_step.push_back(static_cast<int>(c->descs.size()));
+      c->descs.emplace_back();
+      c->bufmaps.emplace_back();
+      sb::to_desc(s.launch, &c->descs.back(), &c->bufmaps.back());
+    } else {
+      c->desc_of_step.push_back(-1);
+    }
+  }
+  {
+    static const int max_lanes = [] {
+      const char* e = std::getenv("SB_LANES");
+      int v = e ? std::atoi(e) : 4;
+      return v < 1 ? 1 : v > 8 ? 8 : v;
+    }();
+    layout_arena(c.get());
+    const Compiled* cc = c.get();
+    auto alias = [cc](int a, int b) {
+      if (a < 0 || b < 0 || cc->arena_off[a] < 0 || cc->arena_off[b] < 0) return false;
+      return cc->arena_off[a] < cc->arena_off[b] + cc->arena_bytes[b] &&
+             cc->arena_off[b] < cc->arena_off[a] + cc->arena_bytes[a];
+    };
+    c->lanes = sb::schedule_lanes(c->plan, max_lanes, alias);
+  }
+  Compiled* raw = c.get();
+  p->plans[key] = std::move(c);
+  return raw;
+}
+
+sb_context::State& ensure_state(sb_context* ctx, const Compiled* c) {
+  auto it = ctx->states.find(c->id);
+  if (it != ctx->states.end()) return it->second;
+  sb_context::State st;
+  if (!c->descs.empty()) {
+    cuda_check(cudaMalloc(&st.d_descs, sizeof(sb::GenericDesc) * c->descs.size()), "cudaMalloc(desc)");
+    cuda_check(cudaMemcpy(st.d_descs, c->descs.data(), sizeof(sb::GenericDesc) * c->descs.size(),
+                          cudaMemcpyHostToDevice),
+               "upload desc");
+  }
+  const std::size_t nb = c->plan.bufs.size();
   st.scratch.assign(nb, nullptr);
-  if (total) cuda_check(cudaMalloc(&st.arena, total), "cudaMalloc(scratch arena)");
-  for (const auto& q : placed) st.scratch[q.buf] = static_cast<char*>(st.arena) + q.off;
-  st.arena_bytes = total;
+  if (c->arena_total) cuda_check(cudaMalloc(&st.arena, c->arena_total), "cudaMalloc(scratch arena)");
+  for (std::size_t b = 0; b < nb; b++)
+    if (c->arena_off[b] >= 0) st.scratch[b] = static_cast<char*>(st.arena) + c->arena_off[b];
+  st.arena_bytes = c->arena_total;
   return ctx->states.emplace(c->id, std::move(st)).first->second;
 }
 
@@ -338,11 +384,27 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
       char* sums = static_cast<char*>(ptr_of(g.sums));
       cuda_check(sb::launch_limb_split(g, ptr_of(g.a_buf), ptr_of(g.b_buf), pa, pb, ctx->stream), "limb_split");
       ctx->launches += 2;
-      for (int t = 0; t <= sb::limb_smax(g); t++) {
+      // the sums are independent GEMMs: run them side by side (each alone fills only
+      // ceil(M/128) * ceil(N/128) CTAs), joined before the combine
+      auto ev = [](cudaEvent_t* e) {
+        if (!*e) cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+        return *e;
+      };
+      const int ns = sb::limb_smax(g) + 1;
+      cuda_check(cudaEventRecord(ev(&ctx->aux_fork), ctx->stream), "limb fork");
+      for (int t = 0; t < ns; t++) {
+        cudaStream_t s = ctx->stream;
+        if (t > 0) {
+          if (!ctx->aux_streams[t]) cuda_check(cudaStreamCreateWithFlags(&ctx->aux_streams[t], cudaStreamNonBlocking), "aux");
+          s = ctx->aux_streams[t];
+          cuda_check(cudaStreamWaitEvent(s, ctx->aux_fork, 0), "limb fork wait");
+        }
         sb::GemmArgs a{pa + sb::limb_a_off(g, t), pb + sb::limb_b_off(g, t), sums + 4ll * t * g.M * g.N};
-        cuda_check(sb::launch_gemm_tc(sb::limb_sum_plan(g, t), a, ctx->stream, ctx->num_sms), "gemm_tc(limb)");
+        cuda_check(sb::launch_gemm_tc(sb::limb_sum_plan(g, t), a, s, ctx->num_sms), "gemm_tc(limb)");
         ctx->launches++;
+        if (t > 0) cuda_check(cudaEventRecord(ev(&ctx->aux_join[t]), s), "limb join");
       }
+      for (int t = 1; t < ns; t++) cuda_check(cudaStreamWaitEvent(ctx->stream, ctx->aux_join[t], 0), "limb join wait");
       cuda_check(sb::launch_limb_combine(g, sums, ptr_of(g.c_buf), ctx->stream), "limb_combine");
       ctx->launches++;
       return;
@@ -408,6 +470,35 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
     ctx->launches++;
   };
   static const bool profile = std::getenv("SB_PROFILE_STEPS") != nullptr;
+  const sb::LaneSchedule& ls = c->lanes;
+  if (!profile && ls.nlanes > 1) {
+    // independent steps on parallel lanes (events only where a step depends across lanes)
+    const cudaStream_t main = ctx->stream;
+    auto ev = [](cudaEvent_t* e) {
+      if (!*e) cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+      return *e;
+    };
+    if (ctx->step_events.size() < plan.steps.size()) ctx->step_events.resize(plan.steps.size(), nullptr);
+    cuda_check(cudaEventRecord(ev(&ctx->fork_event), main), "fork");
+    for (int L = 1; L < ls.nlanes; L++) {
+      if (!ctx->lane_streams[L]) cuda_check(cudaStreamCreateWithFlags(&ctx->lane_streams[L], cudaStreamNonBlocking), "lane");
+      cuda_check(cudaStreamWaitEvent(ctx->lane_streams[L], ctx->fork_event, 0), "fork wait");
+    }
+    for (std::size_t i = 0; i < plan.steps.size(); i++) {
+      if (plan.steps[i].elided) continue;
+      const cudaStream_t s = ls.lane[i] == 0 ? main : ctx->lane_streams[ls.lane[i]];
+      for (int w : ls.waits[i]) cuda_check(cudaStreamWaitEvent(s, ctx->step_events[w], 0), "dep wait");
+      ctx->stream = s;
+      step(i);
+      ctx->stream = main;
+      if (ls.signal[i]) cuda_check(cudaEventRecord(ev(&ctx->step_events[i]), s), "dep record");
+    }
+    for (int L = 1; L < ls.nlanes; L++) {
+      cuda_check(cudaEventRecord(ev(&ctx->join_events[L]), ctx->lane_streams[L]), "join");
+      cuda_check(cudaStreamWaitEvent(main, ctx->join_events[L], 0), "join wait");
+    }
+    return;
+  }
   if (!profile) {
     for (std::size_t i = 0; i < plan.steps.size(); i++) step(i);
     return;

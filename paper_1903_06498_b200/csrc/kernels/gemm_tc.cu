@@ -419,25 +419,34 @@ struct SplitArgs {
   int pairs[4];
 };
 
-// Every source element's limb i goes to each sum s whose pair list contains it.
+// Every source element's limb i goes to each sum s whose pair list contains it.  One thread
+// per 4 consecutive columns: limb i of the 4 elements is one 32-bit word, stored once per
+// (s, pair) segment it belongs to (cols % 4 == 0, 16-byte aligned plane rows).
 __global__ void limb_split_kernel(SplitArgs a) {
-  const long long total = a.rows * a.cols;
+  const long long cq = a.cols / 4;
+  const long long total = a.rows * cq;
   for (long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; g < total;
        g += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long r = g / a.cols, c = g - r * a.cols;
-    const std::uint32_t v = elem_bits(a.src, a.kind, a.off + r * a.ld + c);
+    const long long r = g / cq, c = (g - r * cq) * 4;
+    std::uint32_t v[4];
+#pragma unroll
+    for (int e = 0; e < 4; e++) v[e] = elem_bits(a.src, a.kind, a.off + r * a.ld + c + e);
+    std::uint32_t limb[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      const unsigned sel = static_cast<unsigned>(i | ((4 + i) << 4));  // [x.byte i, y.byte i]
+      limb[i] = __byte_perm(__byte_perm(v[0], v[1], sel), __byte_perm(v[2], v[3], sel), 0x5410);
+    }
     for (int s = 0; s <= a.smax; s++) {
       int p = 0;
       for (int i = 0; i <= s; i++) {
         const int j = s - i;
         if (i >= (a.is_a ? a.limbs : a.lb_other) || j >= (a.is_a ? a.lb_other : a.limbs)) continue;
         const int mine = a.is_a ? i : j;
-        const std::uint8_t byte = static_cast<std::uint8_t>(v >> (8 * mine));
-        // pair p occupies segment p along the concatenated axis
         long long idx;
         if (a.kcat_cols) idx = r * (a.pairs[s] * a.cols) + p * a.cols + c;  // [rows][pairs * cols]
         else idx = (p * a.rows + r) * a.cols + c;                          // [pairs * rows][cols]
-        a.dst[a.sum_off[s] + idx] = byte;
+        *reinterpret_cast<std::uint32_t*>(a.dst + a.sum_off[s] + idx) = limb[mine];
         p++;
       }
     }

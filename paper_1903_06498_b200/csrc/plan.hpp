@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -151,6 +152,16 @@ struct ConvPlan {
   std::int64_t pack_run = 0;  // >0: kk = i * pack_run + (j * C + c) (contiguous S*C-byte runs per tap row)
 };
 
+// Statement-DAG concurrency (schedule.cpp): independent steps on up to N streams.
+struct PStep;
+struct Plan;
+struct LaneSchedule {
+  int nlanes = 1;
+  std::vector<int> lane;                // per step
+  std::vector<std::vector<int>> waits;  // per step: steps on other lanes to wait for
+  std::vector<char> signal;             // per step: record an event after it
+};
+
 // The 1x1 conv over the packed operands of a `packed` conv (same output and epilogue).
 ConvPlan packed_view(const ConvPlan& c);
 
@@ -213,5 +224,10 @@ Plan build_plan(const Program& p, const PlanOptions& opt);
 // Fills a device descriptor for a generic launch.
 // bufmap receives the plan buffer id of every launch-local buffer slot.
 void to_desc(const PLaunch& l, GenericDesc* d, std::vector<int>* bufmap);
+
+// Plan buffers a step reads / writes (aggregating stores count as both).
+void step_access(const PStep& s, std::vector<int>* reads, std::vector<int>* writes);
+// `alias(a, b)`: distinct plan buffers that share device memory (scratch arena reuse).
+LaneSchedule schedule_lanes(const Plan& plan, int max_lanes, const std::function<bool(int, int)>& alias);
 
 }  // namespace sb
