@@ -625,6 +625,13 @@ int sb_program_describe_plan(sb_program* p, int fresh_outputs, int disable_tc, c
     for (std::size_t r = 0; r < fresh.size(); r++) fresh[r] = fresh_outputs && p->prog.buffers[r].dir != sb::Dir::In;
     Compiled* c = get_plan(p, fresh, !disable_tc);
     std::string s = c->plan.describe();
+    if (c->lanes.nlanes > 1) {
+      s += "lanes " + std::to_string(c->lanes.nlanes) + ":";
+      for (std::size_t i = 0; i < c->plan.steps.size(); i++)
+        if (!c->plan.steps[i].elided) s += " " + std::to_string(c->lanes.lane[i]);
+      s += "\n";
+    }
+    s += "arena " + std::to_string(c->arena_total) + " bytes\n";
     if (len) *len = s.size();
     if (buf && cap) {
       std::size_t n = std::min(s.size(), cap - 1);
