@@ -33,6 +33,9 @@ def configs(want=None):
                                       flops=2.0 * M * N * Kd,
                                       bytes=(M * Kd + Kd * N) * (1 if dt == "i8" else 4) + M * N * 4)
     # (f32 inputs: torch.randint bytes reinterpreted as floats; finite values are not needed for timing)
+    out["c1_matmul_f32_tf32x3"] = dict(text=W.matmul(M, N, Kd, in_dtype="f32", out_dtype="f32"),
+                                       flops=2.0 * M * N * Kd, bytes=(M * Kd + Kd * N) * 4 + M * N * 4,
+                                       opts=dict(fp32_mode=1))
     out["c2_conv"] = dict(text=W.conv2d(32, 56, 56, 64, 64), flops=2.0 * W.conv_useful_macs(32, 56, 56, 64, 64),
                           bytes=32 * 56 * 56 * 64 + 9 * 64 * 64 + 32 * 56 * 56 * 64 * 4)
     out["c3_conv_bias_relu"] = dict(text=W.conv_bias_relu(128, 56, 56, 64, 64),
@@ -76,7 +79,7 @@ def main():
             t = torch.randint(-128, 128, (nbytes,), dtype=torch.int8, device="cuda")
             keep.append(t)
             bufs[bn] = (t.data_ptr(), d.elements, sb.SB_BUF_PREPARE if int(d.dir) != 0 else 0)
-        opts = sb.ExecOptions(disable_tensor_cores=args.generic)
+        opts = sb.ExecOptions(disable_tensor_cores=args.generic, **cfg.get("opts", {}))
         run = ctx.bind_device(prog, bufs, opts)
         with torch.cuda.stream(stream):
             run()
@@ -95,7 +98,8 @@ def main():
         line = {"config": name, "ms_per_step": round(ms, 5),
                 "launches_per_step": (ctx.launch_count - launches0) // (2 * args.steps),
                 "GB/s": round(cfg["bytes"] / ms / 1e6, 1), "hbm_frac": round(cfg["bytes"] / ms / 1e6 / hbm, 4),
-                "plan": [l.split(" mode")[0] for l in prog.describe_plan(True, not args.generic).splitlines()]}
+                "plan": [l.split(" mode")[0] for l in
+                         prog.describe_plan(True, not args.generic, cfg.get("opts", {}).get("fp32_mode", 0)).splitlines()]}
         if cfg["flops"]:
             line["GOP/s"] = round(cfg["flops"] / ms / 1e6, 1)
         if "images" in cfg:

@@ -81,12 +81,15 @@ typedef struct sb_device_buffer {
   int64_t count;
 } sb_device_buffer;
 
+enum { SB_FP32_EXACT = 0, SB_FP32_TF32X3 = 1 };
+
 typedef struct sb_exec_options {
   int32_t order;     /* IterOrder: 0 Lex, 1 Reversed, 2 Shuffled — accepted, result is order-free */
   int32_t observer;  /* nonzero = caller wants an ExecObserver: rejected (SB_ERR_UNSUPPORTED) */
   uint64_t seed;     /* Shuffled seed (ignored) */
   int32_t disable_tensor_cores; /* force the generic kernel family (testing) */
-  int32_t reserved;
+  int32_t fp32_mode; /* SB_FP32_EXACT (0): fp32 matmuls bitwise equal to the CPU F32 policy;
+                        SB_FP32_TF32X3 (1): 3xTF32 tensor cores, |err| <= 1e-5 * sum|a||b| */
 } sb_exec_options;
 
 typedef struct sb_context sb_context;
@@ -104,7 +107,8 @@ int sb_program_buffer_count(const sb_program* p);
 int sb_program_buffer_info(const sb_program* p, int i, const char** name, int* dtype,
                            int64_t* elements, int* dir);
 int sb_program_output_identity(const sb_program* p, const char* name, int64_t* value);
-/* Human-readable launch plan (which kernel family / execution mode per block). */
+/* Human-readable launch plan (which kernel family / execution mode per block).
+ * `disable_tensor_cores` bit 0: generic kernels only; bit 1: plan for SB_FP32_TF32X3. */
 int sb_program_describe_plan(sb_program* p, int fresh_outputs, int disable_tensor_cores, char* buf,
                              size_t cap, size_t* len);
 

@@ -61,7 +61,7 @@ class DeviceBuffer(ctypes.Structure):
 
 class _Opts(ctypes.Structure):
     _fields_ = [("order", ctypes.c_int32), ("observer", ctypes.c_int32), ("seed", ctypes.c_uint64),
-                ("disable_tensor_cores", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("disable_tensor_cores", ctypes.c_int32), ("fp32_mode", ctypes.c_int32)]
 
 
 _lib = None
@@ -177,13 +177,12 @@ class Program:
         _check(lib().sb_program_output_identity(self._h, name.encode(), ctypes.byref(v)))
         return v.value
 
-    def describe_plan(self, fresh_outputs: bool = False, tensor_cores: bool = True) -> str:
+    def describe_plan(self, fresh_outputs: bool = False, tensor_cores: bool = True, fp32_mode: int = 0) -> str:
         n = ctypes.c_size_t()
-        _check(lib().sb_program_describe_plan(self._h, int(fresh_outputs), int(not tensor_cores), None, 0,
-                                              ctypes.byref(n)))
+        flags = int(not tensor_cores) | (2 if fp32_mode == 1 else 0)
+        _check(lib().sb_program_describe_plan(self._h, int(fresh_outputs), flags, None, 0, ctypes.byref(n)))
         buf = ctypes.create_string_buffer(n.value + 1)
-        _check(lib().sb_program_describe_plan(self._h, int(fresh_outputs), int(not tensor_cores), buf,
-                                              len(buf), ctypes.byref(n)))
+        _check(lib().sb_program_describe_plan(self._h, int(fresh_outputs), flags, buf, len(buf), ctypes.byref(n)))
         return buf.value.decode()
 
 
@@ -225,10 +224,11 @@ class ExecOptions:
     seed: int = 0
     observer: Optional[object] = None
     disable_tensor_cores: bool = False
+    fp32_mode: int = 0  # 0 exact (bitwise = CPU F32 policy), 1 3xTF32 tensor cores (stated bound)
 
     def _c(self) -> _Opts:
         return _Opts(int(self.order), 1 if self.observer is not None else 0, self.seed,
-                     int(self.disable_tensor_cores), 0)
+                     int(self.disable_tensor_cores), int(self.fp32_mode))
 
 
 def prepare_outputs(program: Program, store: BufferStore) -> None:

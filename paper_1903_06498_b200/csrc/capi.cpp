@@ -195,12 +195,7 @@ std::vector<int> step_buffers(const sb::PStep& s) {
       break;
     case sb::KernelKind::GemmF32:
     case sb::KernelKind::GemmI8TC:
-      out = {l.gemm.a_buf, l.gemm.b_buf, l.gemm.c_buf};
-      if (l.gemm.limbs_a) {
-        out.push_back(l.gemm.planes_a);
-        out.push_back(l.gemm.planes_b);
-        out.push_back(l.gemm.sums);
-      }
+      out = {l.gemm.a_buf, l.gemm.b_buf, l.gemm.c_buf, l.gemm.planes_a, l.gemm.planes_b, l.gemm.sums};
       break;
     case sb::KernelKind::Reduce:
       out = {l.reduce.in_buf, l.reduce.out_buf};
@@ -264,8 +259,9 @@ void layout_arena(Compiled* c) {
   c->arena_total = total;
 }
 
-Compiled* get_plan(sb_program* p, const std::vector<bool>& fresh, bool tc) {
+Compiled* get_plan(sb_program* p, const std::vector<bool>& fresh, bool tc, int fp32_mode = 0) {
   std::string key(tc ? "T" : "G");
+  key += fp32_mode == 1 ? 'x' : 'e';
   for (bool f : fresh) key += f ? '1' : '0';
   std::lock_guard<std::mutex> lock(p->mu);
   auto it = p->plans.find(key);
@@ -275,6 +271,7 @@ Compiled* get_plan(sb_program* p, const std::vector<bool>& fresh, bool tc) {
   sb::PlanOptions opt;
   opt.enable_tc = tc;
   opt.fresh_outputs = fresh;
+  opt.fp32_tc = fp32_mode == 1;
   c->plan = sb::build_plan(p->prog, opt);
   for (const auto& s : c->plan.steps) {
     if (s.kind == sb::PStep::Launch &&
@@ -367,6 +364,35 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
       } else {
         cuda_check(sb::launch_conv_igemm(l.conv, a, ctx->stream, ctx->num_sms), "conv_igemm");
       }
+      ctx->launches++;
+      return;
+    }
+    if (l.kernel == sb::KernelKind::GemmF32 && l.gemm.tf32x3) {
+      const sb::GemmPlan& g = l.gemm;
+      void* pa = ptr_of(g.planes_a);
+      void* pb = ptr_of(g.planes_b);
+      char* sums = static_cast<char*>(ptr_of(g.sums));
+      cuda_check(sb::launch_tf32_split(g, ptr_of(g.a_buf), ptr_of(g.b_buf), pa, pb, ctx->stream), "tf32_split");
+      ctx->launches++;
+      auto ev = [](cudaEvent_t* e) {
+        if (!*e) cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+        return *e;
+      };
+      cuda_check(cudaEventRecord(ev(&ctx->aux_fork), ctx->stream), "tf32 fork");
+      for (int t = 0; t < 3; t++) {
+        cudaStream_t s = ctx->stream;
+        if (t > 0) {
+          if (!ctx->aux_streams[t]) cuda_check(cudaStreamCreateWithFlags(&ctx->aux_streams[t], cudaStreamNonBlocking), "aux");
+          s = ctx->aux_streams[t];
+          cuda_check(cudaStreamWaitEvent(s, ctx->aux_fork, 0), "tf32 fork wait");
+        }
+        sb::GemmArgs a{pa, pb, sums + 4ll * t * g.M * g.N};
+        cuda_check(sb::launch_gemm_tc(sb::tf32_sum_plan(g, t), a, s, ctx->num_sms), "gemm_tc(tf32x3)");
+        ctx->launches++;
+        if (t > 0) cuda_check(cudaEventRecord(ev(&ctx->aux_join[t]), s), "tf32 join");
+      }
+      for (int t = 1; t < 3; t++) cuda_check(cudaStreamWaitEvent(ctx->stream, ctx->aux_join[t], 0), "tf32 join wait");
+      cuda_check(sb::launch_tf32_combine(g, sums, ptr_of(g.c_buf), ctx->stream), "tf32_combine");
       ctx->launches++;
       return;
     }
@@ -623,7 +649,7 @@ int sb_program_describe_plan(sb_program* p, int fresh_outputs, int disable_tc, c
   return guarded([&] {
     std::vector<bool> fresh(p->prog.buffers.size(), false);
     for (std::size_t r = 0; r < fresh.size(); r++) fresh[r] = fresh_outputs && p->prog.buffers[r].dir != sb::Dir::In;
-    Compiled* c = get_plan(p, fresh, !disable_tc);
+    Compiled* c = get_plan(p, fresh, !(disable_tc & 1), (disable_tc & 2) ? 1 : 0);
     std::string s = c->plan.describe();
     if (c->lanes.nlanes > 1) {
       s += "lanes " + std::to_string(c->lanes.nlanes) + ":";
@@ -730,7 +756,8 @@ int sb_execute_device(sb_context* ctx, sb_program* p, const sb_device_buffer* bu
                                              std::to_string(prog.buffers[r].elements));
       ptrs[r] = bufs[slot[r]].dptr;
     }
-    Compiled* c = get_plan(p, fresh_flags(prog, slot, flags), !(opts && opts->disable_tensor_cores));
+    Compiled* c = get_plan(p, fresh_flags(prog, slot, flags), !(opts && opts->disable_tensor_cores),
+                           opts ? opts->fp32_mode : 0);
     for (std::size_t r = 0; r < prog.buffers.size(); r++) {
       if ((flags[slot[r]] & SB_BUF_PREPARE) && prog.buffers[r].dir != sb::Dir::In) {
         const auto& b = prog.buffers[r];
@@ -770,7 +797,8 @@ int sb_execute(sb_context* ctx, sb_program* p, sb_host_buffer* bufs, int n, cons
                                              std::to_string(bufs[slot[r]].count) + " elements, expected " +
                                              std::to_string(prog.buffers[r].elements));
     }
-    Compiled* c = get_plan(p, fresh_flags(prog, slot, flags), !(opts && opts->disable_tensor_cores));
+    Compiled* c = get_plan(p, fresh_flags(prog, slot, flags), !(opts && opts->disable_tensor_cores),
+                           opts ? opts->fp32_mode : 0);
     const std::size_t nr = prog.buffers.size();
     if (ctx->roots.size() < nr) ctx->roots.resize(nr, {nullptr, 0});
     if (ctx->pinned.size() < nr) ctx->pinned.resize(nr, {nullptr, 0});

@@ -49,6 +49,10 @@ cudaError_t launch_limb_combine(const GemmPlan& g, const void* sums, void* c, cu
 // The u8 GEMM computing S_s inside a limb plan.
 GemmPlan limb_sum_plan(const GemmPlan& g, int s);
 long long limb_plane_bytes_a(const GemmPlan& g);
+// 3xTF32 mode for fp32 matmuls (opt-in, stated bound): split + one kind::tf32 GEMM
+GemmPlan tf32_sum_plan(const GemmPlan& g, int t);
+cudaError_t launch_tf32_combine(const GemmPlan& g, const void* sums, void* c, cudaStream_t s);
+cudaError_t launch_tf32_split(const GemmPlan& g, const void* a, const void* b, void* pa, void* pb, cudaStream_t s);
 long long limb_a_off(const GemmPlan& g, int s);
 long long limb_b_off(const GemmPlan& g, int s);
 long long limb_plane_bytes_b(const GemmPlan& g);

@@ -40,6 +40,8 @@ struct GemmKParams {
   long long ldc;  // elements
   std::uint32_t idesc;
   int pdl, b_early;
+  int tf32;  // kind::tf32 (fp32 accumulators, f32 output)
+  int bk_el;  // k-block width in elements (128 bytes)
 };
 
 __device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
@@ -82,6 +84,16 @@ __device__ __forceinline__ void umma_i8(std::uint32_t d, std::uint32_t a_lo, std
       "mov.b64 db, {%3, %4};\n\t"
       "setp.ne.b32 p, %6, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], da, db, %5, p;\n\t}" ::"r"(d),
+      "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_tf32(std::uint32_t d, std::uint32_t a_lo, std::uint32_t a_hi, std::uint32_t b_lo,
+                                          std::uint32_t b_hi, std::uint32_t idesc, std::uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 da, db;\n\t"
+      "mov.b64 da, {%1, %2};\n\t"
+      "mov.b64 db, {%3, %4};\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], da, db, %5, p;\n\t}" ::"r"(d),
       "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc));
 }
 __device__ __forceinline__ void umma_commit(std::uint64_t* bar) {
@@ -158,9 +170,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < p.kblocks; kb++) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], kStageA + kStageB);
-          tma_load_2d(smem_u32(sa + stage * kStageA), &amap, &full[stage], kb * BK, m0);
-          if (p.b_kmajor) tma_load_2d(smem_u32(sbm + stage * kStageB), &bmap, &full[stage], kb * BK, n0);
-          else tma_load_2d(smem_u32(sbm + stage * kStageB), &bmap, &full[stage], n0, kb * BK);
+          tma_load_2d(smem_u32(sa + stage * kStageA), &amap, &full[stage], kb * p.bk_el, m0);
+          if (p.b_kmajor) tma_load_2d(smem_u32(sbm + stage * kStageB), &bmap, &full[stage], kb * p.bk_el, n0);
+          else tma_load_2d(smem_u32(sbm + stage * kStageB), &bmap, &full[stage], n0, kb * p.bk_el);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -187,7 +199,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             // A: +32 bytes along the 128-byte K row; B: K-major +32 bytes, N-major +32 rows (4 KB)
             std::uint32_t b_lo = p.b_kmajor ? (((bsm + ks * 32) >> 4) | (1u << 16))
                                             : (((bsm + ks * 32 * 128) >> 4) | ((static_cast<std::uint32_t>(BK * 128) >> 4) << 16));
-            umma_i8(d, a0 + ks * 2, kHiSW128, b_lo, kHiSW128, p.idesc, (kb | ks) != 0);
+            if (p.tf32) umma_tf32(d, a0 + ks * 2, kHiSW128, b_lo, kHiSW128, p.idesc, (kb | ks) != 0);
+            else umma_i8(d, a0 + ks * 2, kHiSW128, b_lo, kHiSW128, p.idesc, (kb | ks) != 0);
           }
           umma_commit(&empty[stage]);
           if (++stage == kStages) {
@@ -227,7 +240,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             int n = n0 + h * 32 + q;
             if (n >= p.N) break;
             long long idx = static_cast<long long>(m0 + row) * p.ldc + n;
-            if (p.out_kind == kI32) {
+            if (p.tf32) {
+              float* o = static_cast<float*>(p.c) + idx;
+              *o = p.fresh ? __uint_as_float(v[q]) : *o + __uint_as_float(v[q]);
+            } else if (p.out_kind == kI32) {
               std::int32_t* o = static_cast<std::int32_t*>(p.c) + idx;
               *o = static_cast<std::int32_t>(p.fresh ? v[q] : static_cast<std::uint32_t>(*o) + v[q]);
             } else if (p.out_kind == kI16) {
@@ -288,7 +304,7 @@ struct Prepared {
 
 bool same(const GemmPlan& x, const GemmPlan& y) {
   return std::memcmp(&x.M, &y.M, sizeof(long long) * 9) == 0 && x.b_kmajor == y.b_kmajor && x.fresh == y.fresh &&
-         x.c_dtype == y.c_dtype && x.unsigned_ab == y.unsigned_ab;
+         x.c_dtype == y.c_dtype && x.unsigned_ab == y.unsigned_ab && x.tf32x3 == y.tf32x3;
 }
 
 std::mutex g_mu;
@@ -306,12 +322,16 @@ cudaError_t prepare(const GemmPlan& g, const GemmArgs& args, Prepared* out) {
   kp.M = static_cast<int>(g.M);
   kp.N = static_cast<int>(g.N);
   kp.K = static_cast<int>(g.K);
+  const int es_ab = g.tf32x3 ? 4 : 1;  // operand element bytes; a k-block is always 128 bytes
+  const int bk_el = BK / es_ab;
+  kp.tf32 = g.tf32x3 ? 1 : 0;
+  kp.bk_el = bk_el;
   kp.tiles_m = static_cast<int>((g.M + BM - 1) / BM);
   kp.tiles_n = static_cast<int>((g.N + BN - 1) / BN);
-  kp.kblocks = static_cast<int>((g.K + BK - 1) / BK);
+  kp.kblocks = static_cast<int>((g.K + bk_el - 1) / bk_el);
   kp.b_kmajor = g.b_kmajor ? 1 : 0;
   kp.fresh = g.fresh ? 1 : 0;
-  kp.out_kind = g.c_dtype == DType::I8 ? kI8 : g.c_dtype == DType::I16 ? kI16 : kI32;
+  kp.out_kind = g.c_dtype == DType::I8 ? kI8 : g.c_dtype == DType::I16 ? kI16 : kI32;  // F32: 32-bit
   kp.ldc = g.ldc;
   kp.c = static_cast<char*>(args.c) + g.c0 * (kp.out_kind == kI8 ? 1 : kp.out_kind == kI16 ? 2 : 4);
   kp.tma_out = kp.fresh && kp.out_kind == kI32 && g.ldc % 4 == 0 &&
@@ -320,23 +340,26 @@ cudaError_t prepare(const GemmPlan& g, const GemmArgs& args, Prepared* out) {
   const std::uint32_t sgn = g.unsigned_ab ? 0u : 1u;  // atype/btype: 0 = U8, 1 = S8
   kp.idesc = (2u << 4) | (sgn << 7) | (sgn << 10) | ((kp.b_kmajor ? 0u : 1u) << 16) | ((128u >> 3) << 17) |
              ((128u >> 4) << 24);
+  if (g.tf32x3)  // D = F32 (1), A = B = TF32 (2), both K-major
+    kp.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+  const CUtensorMapDataType ttype = g.tf32x3 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT8;
   cuuint32_t es[2] = {1, 1};
-  const std::int8_t* a = static_cast<const std::int8_t*>(args.a) + g.a0;
-  const std::int8_t* b = static_cast<const std::int8_t*>(args.b) + g.b0;
+  const std::int8_t* a = static_cast<const std::int8_t*>(args.a) + g.a0 * es_ab;
+  const std::int8_t* b = static_cast<const std::int8_t*>(args.b) + g.b0 * es_ab;
   if (reinterpret_cast<std::uintptr_t>(a) % 16 || reinterpret_cast<std::uintptr_t>(b) % 16) return cudaErrorMisalignedAddress;
   cuuint64_t adim[2] = {static_cast<cuuint64_t>(g.K), static_cast<cuuint64_t>(g.M)};
-  cuuint64_t astr[1] = {static_cast<cuuint64_t>(g.lda)};
-  cuuint32_t abox[2] = {BK, BM};
-  if (encode(&out->amap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<std::int8_t*>(a), adim, astr, abox, es,
+  cuuint64_t astr[1] = {static_cast<cuuint64_t>(g.lda * es_ab)};
+  cuuint32_t abox[2] = {static_cast<cuuint32_t>(bk_el), BM};
+  if (encode(&out->amap, ttype, 2, const_cast<std::int8_t*>(a), adim, astr, abox, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
-  cuuint64_t bdim[2], bstr[1] = {static_cast<cuuint64_t>(g.ldb)};
+  cuuint64_t bdim[2], bstr[1] = {static_cast<cuuint64_t>(g.ldb * es_ab)};
   cuuint32_t bbox[2];
   if (g.b_kmajor) {
     bdim[0] = static_cast<cuuint64_t>(g.K);
     bdim[1] = static_cast<cuuint64_t>(g.N);
-    bbox[0] = BK;
+    bbox[0] = static_cast<cuuint32_t>(bk_el);
     bbox[1] = BN;
   } else {
     bdim[0] = static_cast<cuuint64_t>(g.N);
@@ -344,7 +367,7 @@ cudaError_t prepare(const GemmPlan& g, const GemmArgs& args, Prepared* out) {
     bbox[0] = BN;
     bbox[1] = BK;
   }
-  if (encode(&out->bmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<std::int8_t*>(b), bdim, bstr, bbox, es,
+  if (encode(&out->bmap, ttype, 2, const_cast<std::int8_t*>(b), bdim, bstr, bbox, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
@@ -547,6 +570,110 @@ cudaError_t launch_limb_combine(const GemmPlan& g, const void* sums, void* c, cu
 }
 
 long long limb_plane_bytes_a(const GemmPlan& g) { return limb_a_off(g, limb_smax(g) + 1); }
+
+// ---- 3xTF32 mode -----------------------------------------------------------------------
+// a = hi(a) + lo(a) with hi = tf32(a), lo = tf32(a - hi); A*B ~= hi*hi + hi*lo + lo*hi as
+// ONE kind::tf32 GEMM over k concatenated three times: A' = [a_hi | a_hi | a_lo] (M x 3K),
+// B'^T = [b_hi | b_lo | b_hi] (N x 3K, K-major).  fp32 accumulation in TMEM.
+
+namespace {
+
+__device__ __forceinline__ float tf32_rn(float x) {
+  std::uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__global__ void tf32_split_a_kernel(const float* __restrict__ a, float* pa, long long M, long long K, long long lda) {
+  const long long ta = M * K;
+  for (long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; g < ta;
+       g += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long m = g / K, k = g - m * K;
+    const float x = a[m * lda + k];
+    const float hi = tf32_rn(x), lo = tf32_rn(x - hi);
+    float* row = pa + m * 3 * K;
+    row[k] = hi;
+    row[K + k] = hi;
+    row[2 * K + k] = lo;
+  }
+}
+
+// B'^T[n][seg * K + k] from B[k][n] (N-major) through a 32 x 32 smem tile: coalesced reads
+// along n and coalesced writes along k.  K-major sources (b_k == 1) need no transpose.
+__global__ void tf32_split_b_kernel(const float* __restrict__ b, float* pb, long long N, long long K, long long b_k,
+                                    long long b_n) {
+  __shared__ float tile[32][33];
+  const long long tiles_n = (N + 31) / 32, tiles_k = (K + 31) / 32;
+  for (long long t = blockIdx.x; t < tiles_n * tiles_k; t += gridDim.x) {
+    const long long n0 = (t % tiles_n) * 32, k0 = (t / tiles_n) * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+      const long long k = k0 + r, n = n0 + threadIdx.x;
+      tile[r][threadIdx.x] = (k < K && n < N) ? b[k * b_k + n * b_n] : 0.0f;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+      const long long n = n0 + r, k = k0 + threadIdx.x;
+      if (n < N && k < K) {
+        const float x = tile[threadIdx.x][r];
+        const float hi = tf32_rn(x), lo = tf32_rn(x - hi);
+        float* row = pb + n * 3 * K;
+        row[k] = hi;
+        row[K + k] = lo;
+        row[2 * K + k] = hi;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+// Product t (0: hi*hi, 1: hi*lo, 2: lo*hi) as its own GEMM over segment t of the planes,
+// written to sums[t]; the three run side by side and tf32_combine adds them.
+GemmPlan tf32_sum_plan(const GemmPlan& g, int t) {
+  GemmPlan u = g;
+  u.tf32x3 = true;
+  u.f32 = false;
+  u.lda = 3 * g.K;
+  u.a0 = t * g.K;
+  u.b_kmajor = true;
+  u.ldb = 3 * g.K;
+  u.b0 = t * g.K;
+  u.ldc = g.N;
+  u.c0 = 0;
+  u.fresh = true;
+  u.c_dtype = DType::I32;  // 32-bit output path (fp32 bits)
+  return u;
+}
+
+namespace {
+__global__ void tf32_combine_kernel(const float* __restrict__ sums, float* c, long long M, long long N, long long ldc,
+                                    int fresh) {
+  const long long total = M * N;
+  for (long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; g < total;
+       g += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long m = g / N, n = g - m * N;
+    const float v = sums[g] + (sums[total + g] + sums[2 * total + g]);
+    float* o = c + m * ldc + n;
+    *o = fresh ? v : *o + v;
+  }
+}
+}  // namespace
+
+cudaError_t launch_tf32_combine(const GemmPlan& g, const void* sums, void* c, cudaStream_t s) {
+  tf32_combine_kernel<<<148 * 8, 256, 0, s>>>(static_cast<const float*>(sums), static_cast<float*>(c) + g.c0, g.M,
+                                              g.N, g.ldc, g.fresh ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tf32_split(const GemmPlan& g, const void* a, const void* b, void* pa, void* pb, cudaStream_t s) {
+  const float* af = static_cast<const float*>(a) + g.a0;
+  const float* bf = static_cast<const float*>(b) + g.b0;
+  const long long b_k = g.b_kmajor ? 1 : g.ldb, b_n = g.b_kmajor ? g.ldb : 1;
+  tf32_split_a_kernel<<<148 * 8, 256, 0, s>>>(af, static_cast<float*>(pa), g.M, g.K, g.lda);
+  tf32_split_b_kernel<<<148 * 8, dim3(32, 8), 0, s>>>(bf, static_cast<float*>(pb), g.N, g.K, b_k, b_n);
+  return cudaGetLastError();
+}
 long long limb_plane_bytes_b(const GemmPlan& g) { return limb_b_off(g, limb_smax(g) + 1); }
 
 cudaError_t launch_gemm_tc(const GemmPlan& g, const GemmArgs& args, cudaStream_t s, int num_sms) {

@@ -944,6 +944,26 @@ void match_kernels(Plan* plan, const Program& p, const PlanOptions& opt) {
     if (match_gemm(*plan, st.launch, p, opt, s)) {
       st.launch.kernel = st.launch.gemm.f32 ? KernelKind::GemmF32 : KernelKind::GemmI8TC;
       GemmPlan& g = st.launch.gemm;
+      if (g.f32 && opt.fp32_tc) {
+        GemmPlan t = g;
+        t.tf32x3 = true;
+        if (!gemm_tc_unsupported(tf32_sum_plan(t, 0)) && !gemm_tc_unsupported(tf32_sum_plan(t, 2))) {
+          g.tf32x3 = true;
+          auto scratch = [&](const std::string& name, long long elems) {
+            PBuffer b;
+            b.name = name;
+            b.dtype = DType::F32;
+            b.kind = kF32;
+            b.elements = elems;
+            plan->bufs.push_back(b);
+            return static_cast<int>(plan->bufs.size()) - 1;
+          };
+          g.planes_a = scratch("tf32x3:" + plan->bufs[g.a_buf].name, g.M * 3 * g.K);
+          g.planes_b = scratch("tf32x3:" + plan->bufs[g.b_buf].name, g.N * 3 * g.K);
+          g.sums = scratch("tf32x3sums:" + plan->bufs[g.c_buf].name, 3 * g.M * g.N);
+          plan->notes.push_back("launch " + st.launch.path + ": fp32 matmul as one 3xTF32 tensor-core GEMM (k x 3)");
+        }
+      }
       if (g.limbs_a) {
         auto scratch = [&](const std::string& name, std::int8_t kind, long long elems) {
           PBuffer b;

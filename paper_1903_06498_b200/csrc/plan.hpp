@@ -85,6 +85,7 @@ struct GemmPlan {
   int a_buf = -1, b_buf = -1, c_buf = -1;
   bool unsigned_ab = false;  // u8 x u8 operands (byte limbs)
   bool f32 = false;          // fp32 numeric mode (kernels/gemm_f32.cu)
+  bool tf32x3 = false;       // fp32 via 3xTF32 on tensor cores (PlanOptions::fp32_tc)
   // byte-limb mode (i16/i32 operands, exact modulo 2^(8*bytes(C))): A = sum_i a_i 256^i with
   // unsigned byte planes; S_s = sum_{i+j=s} a_i b_j runs as ONE u8 GEMM per s over operands
   // concatenated along k (planes_a / planes_b), C (+)= sum_s S_s << 8s wrapped at the store
@@ -217,6 +218,7 @@ struct PlanOptions {
   bool enable_tc = true;           // route matched contractions to tcgen05 kernels
   std::vector<bool> fresh_outputs; // per root buffer: contents are prepare_outputs' identity
   std::int64_t max_unroll = 1 << 16;
+  bool fp32_tc = false;            // fp32 matmuls as 3xTF32 tensor-core GEMMs (stated bound)
 };
 
 Plan build_plan(const Program& p, const PlanOptions& opt);

@@ -205,3 +205,34 @@ def test_f32_gemm_config1_vs_torch():
     scale = (a.abs() @ b.abs()).cpu().numpy().ravel()
     err = np.abs(store["C"].data.astype(np.float64) - exact)
     assert np.all(err <= 1e-5 * scale), float((err / scale).max())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape", [(1024, 1024, 1024, False), (256, 384, 512, True), (130, 96, 80, False)],
+                         ids=lambda c: "x".join(map(str, c)))
+def test_f32_gemm_tf32x3_stated_bound(shape):
+    """Opt-in SB_FP32_TF32X3: one kind::tf32 GEMM over [hi|hi|lo] x [hi;lo;hi];
+    stated bound |c - exact| <= 1e-5 * sum_k |a||b| (fresh and accumulating outputs)."""
+    if not gpu_available():
+        pytest.skip("no B200")
+    import torch
+    import paper_1903_06498_b200 as sb
+    from paper_1903_06498_b200 import workloads as W
+    M, N, K, bt = shape
+    text = (W.matmul_bt if bt else W.matmul)(M, N, K, in_dtype="f32", out_dtype="f32")
+    prog = sb.parse_program(text)
+    assert "3xTF32" in prog.describe_plan(True, fp32_mode=1)
+    for accumulate in (False, True):
+        store = random_f32_inputs(prog, 7 + M)
+        c0 = np.random.default_rng(2).standard_normal(M * N).astype(np.float32) if accumulate else None
+        if accumulate:
+            store["C"] = sb.Buffer(prog.buffers["C"].dtype, c0.copy())
+        sb.prepare_outputs(prog, store)
+        a = torch.as_tensor(store["A"].data.reshape(M, K), device="cuda").double()
+        bm = store["B"].data.reshape(N, K).T if bt else store["B"].data.reshape(K, N)
+        b = torch.as_tensor(np.ascontiguousarray(bm), device="cuda").double()
+        sb.execute(prog, store, sb.ExecOptions(fp32_mode=1))
+        exact = (a @ b).cpu().numpy().ravel() + (c0.astype(np.float64) if accumulate else 0)
+        scale = (a.abs() @ b.abs()).cpu().numpy().ravel() + (np.abs(c0) if accumulate else 0)
+        err = np.abs(store["C"].data.astype(np.float64) - exact)
+        assert np.all(err <= 1e-5 * scale + 1e-30), float((err / (scale + 1e-30)).max())
