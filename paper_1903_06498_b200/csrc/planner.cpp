@@ -595,7 +595,74 @@ class Lowerer {
   // in every access and constraint are one index of range r_d * r_{d+1} (a tiled index
   // after tile_rewrite, tile.cpp:100-235, becomes untiled again).  Adjacency keeps the
   // lexicographic order, so execution semantics are unchanged.
-  static void coalesce(PLaunch& l) {
+  // A launch whose result does not depend on the order of its points: no buffer is both
+  // read and written, and every written buffer either aggregates with one integer
+  // commutative-associative op (add/mul/max/min wrap modulo 2^n) or is written at most once
+  // per address (injective over all dims).  Its dims may be merged in any order.
+  bool order_free(const PLaunch& l) const {
+    if (!l.specials.empty() || !l.priv.empty() || l.has_spill) return false;
+    std::set<int> loaded;
+    std::map<int, std::set<int>> aggs;
+    for (const auto& ins : l.code) {
+      if (ins.op == kOpLoad) loaded.insert(l.acc[ins.acc].buf);
+      if (ins.op == kOpStore) aggs[l.acc[ins.acc].buf].insert(ins.agg);
+    }
+    for (const auto& a : l.acc)
+      if (plan_->bufs[a.buf].dtype == DType::F32) return false;
+    std::vector<int> all;
+    for (std::size_t d = 0; d < l.dims.size(); d++) all.push_back(static_cast<int>(d));
+    for (auto& [b, s] : aggs) {
+      if (loaded.count(b)) return false;
+      bool comm = s.size() == 1 && !s.count(static_cast<int>(Agg::Assign));
+      if (comm) continue;
+      int nst = 0;
+      const FAff* addr = nullptr;
+      for (const auto& ins : l.code)
+        if (ins.op == kOpStore && l.acc[ins.acc].buf == b) {
+          nst++;
+          addr = &l.acc[ins.acc].addr;
+        }
+      if (nst != 1 || !injective(*addr, all, l.dims)) return false;
+    }
+    return true;
+  }
+
+  void coalesce(PLaunch& l) const {
+    coalesce_adjacent(l);
+    if (!order_free(l)) return;
+    // any two dims d (outer) and e (inner) with k_d = k_e * r_e everywhere are one index
+    // (e.g. the outer and inner halves of a tile_rewrite-tiled index that other indexes
+    // separate in the nest); order-free launches may iterate them merged
+    bool changed = true;
+    while (changed) {
+      changed = false;
+      for (std::size_t d = 0; d < l.dims.size() && !changed; d++)
+        for (std::size_t e = 0; e < l.dims.size() && !changed; e++) {
+          if (d == e) continue;
+          const std::int64_t re = l.dims[e].range;
+          auto ok = [&](const FAff& f) { return f.at(d) == f.at(e) * re; };
+          bool all = true;
+          bool used = false;
+          for (const auto& a : l.acc) {
+            all &= ok(a.addr);
+            used |= a.addr.uses(e);
+          }
+          for (const auto& c : l.cons) all &= ok(c);
+          if (!all || !used) continue;
+          for (auto& a : l.acc)
+            if (d < a.addr.k.size()) a.addr.k.erase(a.addr.k.begin() + static_cast<long>(d));
+          for (auto& c : l.cons)
+            if (d < c.k.size()) c.k.erase(c.k.begin() + static_cast<long>(d));
+          l.dims[e].name = l.dims[d].name + "*" + l.dims[e].name;
+          l.dims[e].range *= l.dims[d].range;
+          l.dims.erase(l.dims.begin() + static_cast<long>(d));
+          changed = true;
+        }
+    }
+    coalesce_adjacent(l);
+  }
+
+  static void coalesce_adjacent(PLaunch& l) {
     bool changed = true;
     while (changed) {
       changed = false;
