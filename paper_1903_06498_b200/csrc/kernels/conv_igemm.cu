@@ -235,6 +235,9 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
         mbar_wait(&tempty[acc], ((iter >> 1) & 1) ^ 1);
         tc_fence_after();
         const std::uint32_t d = tmem_base + static_cast<std::uint32_t>(acc * BN);
+        // a last n-tile with <= 64 valid output channels runs N = 64 instructions (48 vs 64 cycles)
+        const int nrem = p.N - (t % p.tiles_n) * BN;
+        const std::uint32_t idesc = nrem <= 64 ? ((p.idesc & ~(0x3Fu << 17)) | ((64u >> 3) << 17)) : p.idesc;
         for (int kb = 0; kb < p.kblocks; kb++) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -242,7 +245,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
           const std::uint32_t a_lo = (sa >> 4) | (1u << 16);
           const std::uint32_t b_lo = ((sa + stage_a) >> 4) | (1u << 16);
           for (int ks = 0; ks < ksteps; ks++)  // +32 bytes along the K-major rows
-            umma_i8(d, a_lo + ks * 2, p.desc_hi, b_lo + ks * 2, p.desc_hi, p.idesc, (kb | ks) != 0);
+            umma_i8(d, a_lo + ks * 2, p.desc_hi, b_lo + ks * 2, p.desc_hi, idesc, (kb | ks) != 0);
           umma_commit(&empty[stage]);
           if (++stage == stages) {
             stage = 0;
@@ -413,6 +416,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       std::uint8_t* scur = p.tma_out == 2 ? stg + (iter & 1) * 16384 : stg;
       const int m = m0 + row;
       for (int h = h_lo; h < h_hi; h++) {
+        if (n0 + h * 32 >= p.N) break;  // columns past N: nothing to store (warp-uniform)
         std::uint32_t v[32];
         tmem_ld32(tmem_base + (static_cast<std::uint32_t>(quarter * 32) << 16) +
                       static_cast<std::uint32_t>(acc * BN + h * 32),

@@ -5,7 +5,8 @@
 // placed on up to `max_lanes` CUDA streams (lanes) by a list scheduler over estimated step
 // times.  A step waits only for the latest conflicting step on each other lane (events);
 // same-lane order needs nothing.  Under CUDA-graph capture the lanes become parallel graph
-// branches.  Programs whose steps form a chain keep one lane (no events at all).
+// branches.  Programs whose steps form a chain keep one lane (no events at all), and so do
+// steps that saturate the GPU alone.
 #include <algorithm>
 #include <cmath>
 #include <functional>
@@ -131,11 +132,18 @@ LaneSchedule schedule_lanes(const Plan& plan, int max_lanes, const std::function
         ready = std::max(ready, finish[i]);
       }
     }
-    // earliest start over lanes; prefer the lane that holds the latest dependency
+    // earliest start over lanes; prefer the lane that holds the latest dependency.  A step
+    // long enough to fill the GPU on its own (est. >= 8 us) gains nothing from a second lane
+    // and would lose programmatic-dependent-launch chaining: it stays on its dependency's lane.
     int best = -1;
     double best_start = 0.0;
     const int last_dep = deps.empty() ? -1 : deps.back();
-    for (int L = 0; L < static_cast<int>(lane_free.size()); L++) {
+    const bool saturating = step_cost(plan, plan.steps[j]) >= 8.0;
+    if (saturating) {
+      best = last_dep >= 0 ? ls.lane[last_dep] : 0;
+      best_start = std::max(lane_free[best], ready);
+    }
+    for (int L = 0; L < static_cast<int>(lane_free.size()) && !saturating; L++) {
       if (L >= used + 1) break;  // open at most one new lane at a time
       const double start = std::max(lane_free[L], ready);
       const bool pref = last_dep >= 0 && ls.lane[last_dep] == L;
