@@ -107,6 +107,14 @@ int sb_program_buffer_count(const sb_program* p);
 int sb_program_buffer_info(const sb_program* p, int i, const char** name, int* dtype,
                            int64_t* elements, int* dir);
 int sb_program_output_identity(const sb_program* p, const char* name, int64_t* value);
+/* Aggregation of a root output (0 assign, 1 add, 2 max, 3 min, 4 mul) as prepare_outputs
+ * resolves it (interp.cpp:620-632). */
+int sb_program_output_aggregation(const sb_program* p, const char* name, int* agg);
+/* Split-aggregation sharding: a copy of `p` whose ranged index `index` in the
+ * block at dot path `block_path` ("" = root, "0", "0.1", ...) runs over [lo, hi) only.
+ * Shards' outputs combine with the output's aggregation (all-reduce sum/max/min/prod). */
+int sb_program_restrict_index(const sb_program* p, const char* block_path, const char* index, int64_t lo,
+                              int64_t hi, sb_program** out);
 /* Human-readable launch plan (which kernel family / execution mode per block).
  * `disable_tensor_cores` bit 0: generic kernels only; bit 1: plan for SB_FP32_TF32X3. */
 int sb_program_describe_plan(sb_program* p, int fresh_outputs, int disable_tensor_cores, char* buf,

@@ -42,6 +42,7 @@ EXPORTED = [
     "sb_last_error", "sb_status_name", "sb_abi_version",
     "sb_program_parse", "sb_program_free", "sb_program_print", "sb_program_buffer_count",
     "sb_program_buffer_info", "sb_program_output_identity", "sb_program_describe_plan",
+    "sb_program_output_aggregation", "sb_program_restrict_index",
     "sb_context_create", "sb_context_destroy", "sb_context_set_stream", "sb_context_stream",
     "sb_context_sync", "sb_context_launch_count", "sb_device_alloc", "sb_device_free",
     "sb_host_alloc_pinned", "sb_host_free_pinned", "sb_execute", "sb_execute_device",
@@ -85,6 +86,8 @@ def lib() -> ctypes.CDLL:
         L.sb_program_buffer_info.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(i32),
                                              ctypes.POINTER(i64), ctypes.POINTER(i32)]
         L.sb_program_output_identity.argtypes = [vp, ctypes.c_char_p, ctypes.POINTER(i64)]
+        L.sb_program_output_aggregation.argtypes = [vp, ctypes.c_char_p, ctypes.POINTER(i32)]
+        L.sb_program_restrict_index.argtypes = [vp, ctypes.c_char_p, ctypes.c_char_p, i64, i64, ctypes.POINTER(vp)]
         L.sb_program_describe_plan.argtypes = [vp, i32, i32, ctypes.c_char_p, ctypes.c_size_t,
                                                ctypes.POINTER(ctypes.c_size_t)]
         L.sb_context_create.argtypes = [i32, ctypes.POINTER(vp)]
@@ -176,6 +179,21 @@ class Program:
         v = ctypes.c_int64()
         _check(lib().sb_program_output_identity(self._h, name.encode(), ctypes.byref(v)))
         return v.value
+
+    def output_aggregation(self, name: str) -> int:
+        """0 assign, 1 add, 2 max, 3 min, 4 mul (interp.cpp:620-632)."""
+        v = ctypes.c_int()
+        _check(lib().sb_program_output_aggregation(self._h, name.encode(), ctypes.byref(v)))
+        return v.value
+
+    def restrict_index(self, block_path: str, index: str, lo: int, hi: int) -> "Program":
+        """Split-aggregation shard: ranged `index` of the block at `block_path` over [lo, hi)."""
+        h = ctypes.c_void_p()
+        _check(lib().sb_program_restrict_index(self._h, block_path.encode(), index.encode(), lo, hi, ctypes.byref(h)))
+        return Program(h.value)
+
+    def text(self) -> str:
+        return print_program(self)
 
     def describe_plan(self, fresh_outputs: bool = False, tensor_cores: bool = True, fp32_mode: int = 0) -> str:
         n = ctypes.c_size_t()

@@ -644,6 +644,19 @@ int sb_program_output_identity(const sb_program* p, const char* name, int64_t* v
   return guarded([&] { *value = sb::output_identity(p->prog, name); });
 }
 
+int sb_program_output_aggregation(const sb_program* p, const char* name, int* agg) {
+  return guarded([&] { *agg = static_cast<int>(sb::output_aggregation(p->prog, name)); });
+}
+
+int sb_program_restrict_index(const sb_program* p, const char* block_path, const char* index, int64_t lo, int64_t hi,
+                              sb_program** out) {
+  return guarded([&] {
+    auto q = std::make_unique<sb_program>();
+    q->prog = sb::restrict_index(p->prog, block_path ? block_path : "", index, lo, hi);
+    *out = q.release();
+  });
+}
+
 int sb_program_describe_plan(sb_program* p, int fresh_outputs, int disable_tc, char* buf, size_t cap,
                              size_t* len) {
   return guarded([&] {

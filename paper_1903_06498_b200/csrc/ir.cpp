@@ -244,6 +244,70 @@ std::string print_program(const Program& p) {
   return os.str();
 }
 
+Agg output_aggregation(const Program& p, const std::string& name) {
+  const Refinement* root_ref = p.root.find_ref(name);
+  if (!root_ref) throw Error("MissingBuffer", "no root refinement '" + name + "'");
+  Agg agg = root_ref->has_agg ? root_ref->agg : Agg::Assign;
+  std::vector<const Block*> stack = {&p.root};
+  while (!stack.empty()) {
+    const Block* b = stack.back();
+    stack.pop_back();
+    const Refinement* r = b->find_ref(name);
+    if (b != &p.root && (r == nullptr || !r->has_agg)) continue;
+    if (r && r->has_agg) agg = r->agg;
+    for (const auto& s : b->stmts)
+      if (s.kind == StmtKind::Block) stack.push_back(s.block.get());
+  }
+  return agg;
+}
+
+namespace {
+
+// idx -> idx + lo in every affine that sees `idx` (the block's own constraints and
+// refinement offsets, and the subtree below it until a block redeclares the name).
+void shift_index(Block* b, const std::string& idx, std::int64_t lo, bool own) {
+  auto fix = [&](Affine& a) {
+    const std::int64_t k = a.coeff(idx);
+    if (k) a.constant += k * lo;
+  };
+  if (!own) {
+    for (auto& i : b->indexes) {
+      if (i.is_alias) fix(i.alias);  // aliases read the parent scope
+      if (i.name == idx) return;     // shadowed below this point
+    }
+  }
+  for (auto& c : b->constraints) fix(c);
+  for (auto& r : b->refs)
+    for (auto& o : r.offsets) fix(o);
+  for (auto& s : b->stmts)
+    if (s.kind == StmtKind::Block) shift_index(s.block.get(), idx, lo, false);
+}
+
+}  // namespace
+
+Program restrict_index(const Program& p, const std::string& path, const std::string& idx, std::int64_t lo,
+                       std::int64_t hi) {
+  Program q = p;
+  Block* b = &q.root;
+  std::stringstream ss(path);
+  std::string part;
+  while (!path.empty() && std::getline(ss, part, '.')) {
+    const std::size_t k = static_cast<std::size_t>(std::stoll(part));
+    if (k >= b->stmts.size() || b->stmts[k].kind != StmtKind::Block)
+      throw Error("Unsupported", "no block at path '" + path + "'");
+    b = b->stmts[k].block.get();
+  }
+  Index* target = nullptr;
+  for (auto& i : b->indexes)
+    if (i.name == idx && !i.is_alias) target = &i;
+  if (!target) throw Error("UnboundIndex", "block '" + path + "' has no ranged index '" + idx + "'");
+  if (lo < 0 || hi > target->range || lo >= hi) throw Error("Unsupported", "bad index range");
+  target->range = hi - lo;
+  shift_index(b, idx, lo, true);
+  if (b->has_annotation) b->annotation = b->range_product();
+  return q;
+}
+
 std::int64_t output_identity(const Program& p, const std::string& name) {
   const Refinement* root_ref = p.root.find_ref(name);
   if (!root_ref) throw Error("MissingBuffer", "no root refinement '" + name + "'");

@@ -181,5 +181,12 @@ void rebind_buffers(Program* p);
 // prepare_outputs' fill value for root buffer `name` (interp.cpp:617-642):
 // the identity of the deepest aggregation writing it.
 std::int64_t output_identity(const Program& p, const std::string& name);
+// The aggregation prepare_outputs keys on (deepest re-declaration, interp.cpp:620-632).
+Agg output_aggregation(const Program& p, const std::string& name);
+// Split-aggregation sharding: the program with ranged index `idx` of the block at dot path
+// `path` restricted to [lo, hi) (idx -> idx + lo below it).  Partial results of the shards
+// combine with the output's aggregation (add: sum, max, min, mul: product).
+Program restrict_index(const Program& p, const std::string& path, const std::string& idx, std::int64_t lo,
+                       std::int64_t hi);
 
 }  // namespace sb

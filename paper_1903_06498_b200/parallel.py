@@ -1,0 +1,47 @@
+"""Multi-GPU sharding of Stripe programs, one process per GPU.
+
+* Partitioned indexes (batch n, output channels, rows m): each rank runs the program over
+  its contiguous slice (workloads.shard_range); outputs are disjoint, no collective.
+* Split aggregation (optional demo: split-K of a matmul, a huge global sum): each rank runs
+  `shard_aggregation(...)` — the program with the aggregation index restricted to its slice
+  (sb_program_restrict_index) — into FRESH outputs (prepare_outputs' identity), and
+  `allreduce_outputs` combines the partials with the output's aggregation: add -> SUM,
+  max -> MAX, min -> MIN, mul -> PRODUCT (NCCL over NVLink on B200; gloo on CPU).  Integer
+  outputs wrap modulo 2^bits exactly like the reference's store (the wrapping sum of wrapped
+  partials is the wrapped total), so the split is bit-exact.
+"""
+from typing import Dict
+
+import numpy as np
+
+from . import Dir, Program
+from .workloads import shard_range
+
+AGG_OPS = {1: "SUM", 2: "MAX", 3: "MIN", 4: "PRODUCT"}
+
+
+def shard_aggregation(program: Program, block_path: str, index: str, extent: int, world: int, rank: int) -> Program:
+    lo, hi = shard_range(extent, world, rank)
+    return program.restrict_index(block_path, index, lo, hi)
+
+
+def _wrap(x: np.ndarray, bits: int) -> np.ndarray:
+    m = 1 << bits
+    return ((x + (m >> 1)) % m) - (m >> 1)
+
+
+def allreduce_outputs(program: Program, outputs: Dict[str, object], group=None) -> None:
+    """outputs: name -> torch tensor (int64 carriers on CPU/gloo, or native-width on GPU/NCCL),
+    reduced in place across `group` with each output's aggregation."""
+    import torch
+    import torch.distributed as dist
+    for name, t in outputs.items():
+        decl = program.buffers[name]
+        if decl.dir == Dir.In:
+            continue
+        agg = program.output_aggregation(name)
+        if agg not in AGG_OPS:
+            raise ValueError(f"output '{name}' is assigned, not aggregated: it cannot be split")
+        dist.all_reduce(t, op=getattr(dist.ReduceOp, AGG_OPS[agg]), group=group)
+        if t.dtype == torch.int64 and int(decl.dtype) in (8, 16, 32):
+            t.copy_(torch.from_numpy(_wrap(t.cpu().numpy(), int(decl.dtype))).to(t.device))

@@ -65,3 +65,98 @@ def test_shard_range_partitions():
             spans = [W.shard_range(total, world, r) for r in range(world)]
             assert spans[0][0] == 0 and spans[-1][1] == total
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+
+
+# ---- split aggregation (SURVEY §8(e) optional demo): shards + all-reduce -----------------
+
+def _split_worker(rank, world, port, out):
+    import torch
+
+    import paper_1903_06498_b200 as sb
+    from oracle import Port, Rng, wrap
+    from paper_1903_06498_b200.parallel import allreduce_outputs, shard_aggregation
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cases = {
+        # split-K of an i32 matmul (add -> SUM, wrap mod 2^32)
+        "matmul": (W.matmul(12, 10, 37, in_dtype="i32", out_dtype="i32"), "0", "k", 37),
+        # a global sum split over rows (add)
+        "gsum": (W.global_sum(3, 7, 5, 16), "0", "x", 7),
+        # max-pool taps split across ranks (max -> MAX)
+        "pool": (W.maxpool2x2(2, 6, 8, 16), "0", "i", 2),
+    }
+    ok = {}
+    for name, (text, path, idx, extent) in cases.items():
+        prog = sb.parse_program(text)
+        rng = Rng(500 + len(name))
+        inputs = {}
+        for n, d in prog.buffers.items():
+            if d.dir == sb.Dir.Out:
+                continue
+            inputs[n] = wrap(int(d.dtype), rng.bulk(d.elements))
+        shard = shard_aggregation(prog, path, idx, extent, world, rank)
+        store = dict(inputs)
+        for n, d in prog.buffers.items():
+            if d.dir != sb.Dir.In:
+                store[n] = np.full(d.elements, prog.output_identity(n), np.int64)  # fresh on every rank
+        part = Port.execute(sb.print_program(shard), store)
+        outs = {n: torch.from_numpy(part[n].copy()) for n, d in prog.buffers.items() if d.dir != sb.Dir.In}
+        allreduce_outputs(prog, outs)
+        full_store = dict(inputs)
+        for n, d in prog.buffers.items():
+            if d.dir != sb.Dir.In:
+                full_store[n] = np.full(d.elements, prog.output_identity(n), np.int64)
+        full = Port.execute(text, full_store)
+        ok[name] = all(np.array_equal(outs[n].numpy(), full[n]) for n in outs)
+    if rank == 0:
+        out.update(ok)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_split_aggregation_gloo_world2():
+    from oracle import Port
+    if not Port.available():
+        pytest.skip("oracle/_port not built")
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_split_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    assert dict(out) == {"matmul": True, "gsum": True, "pool": True}, dict(out)
+
+
+def test_restrict_index_rejects_assign_outputs():
+    import torch  # noqa: F401
+    import paper_1903_06498_b200 as sb
+    from paper_1903_06498_b200.parallel import AGG_OPS
+    prog = sb.parse_program(W.matmul(4, 4, 4))
+    assert AGG_OPS[prog.output_aggregation("C")] == "SUM"
+    with pytest.raises(sb.ExecError):
+        prog.restrict_index("0", "q", 0, 1)
+
+
+@pytest.mark.gpu
+def test_split_k_shards_on_device():
+    """The shard programs of a split-K i8 matmul run on the B200 kernels (16-aligned k slices
+    stay on the tcgen05 GEMM) and their wrapped sum equals the full product."""
+    from harness import gpu_available
+    if not gpu_available():
+        pytest.skip("no B200")
+    import paper_1903_06498_b200 as sb
+    from oracle import Rng, wrap
+    from paper_1903_06498_b200.parallel import shard_aggregation
+    text = W.matmul(256, 128, 512, in_dtype="i8", out_dtype="i32")
+    prog = sb.parse_program(text)
+    rng = Rng(77)
+    A = wrap(8, rng.bulk(256 * 512))
+    B = wrap(8, rng.bulk(512 * 128))
+    total = np.zeros(256 * 128, np.int64)
+    for r in range(4):
+        shard = shard_aggregation(prog, "0", "k", 512, 4, r)
+        assert "gemm_i8_tc" in shard.describe_plan(True)
+        st = {"A": sb.Buffer(8, A.copy()), "B": sb.Buffer(8, B.copy())}
+        sb.prepare_outputs(shard, st)
+        sb.execute(shard, st)
+        total += st["C"].data
+    full = (A.reshape(256, 512) @ B.reshape(512, 128)).ravel()
+    np.testing.assert_array_equal(wrap(32, total.astype(np.uint64)), wrap(32, full.astype(np.uint64)))
