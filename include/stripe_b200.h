@@ -110,6 +110,10 @@ int sb_program_output_identity(const sb_program* p, const char* name, int64_t* v
 /* Aggregation of a root output (0 assign, 1 add, 2 max, 3 min, 4 mul) as prepare_outputs
  * resolves it (interp.cpp:620-632). */
 int sb_program_output_aggregation(const sb_program* p, const char* name, int* agg);
+/* Constraint-satisfying points of the block at `block_path` (its own ranged indexes and
+ * constraints), the reference's count_valid_points (tile.cpp:338-370) evaluated on the
+ * device in closed form per innermost row. */
+int sb_count_valid_points(sb_context* ctx, const sb_program* p, const char* block_path, int64_t* count);
 /* Split-aggregation sharding: a copy of `p` whose ranged index `index` in the
  * block at dot path `block_path` ("" = root, "0", "0.1", ...) runs over [lo, hi) only.
  * Shards' outputs combine with the output's aggregation (all-reduce sum/max/min/prod). */

@@ -132,6 +132,7 @@ class Ref:
             L.sr_gen_oracle.argtypes = [_cp, _i64, _i64, _i64, _i64, _i32, _vp]
             L.sr_tile_rewrite.argtypes = [_vp, _cp, _cp, _cp, _sz, _cp, _sz]
             L.sr_pipeline.argtypes = [_vp, _cp, _cp, _sz, _cp, _sz]
+            L.sr_useful_ops.argtypes = [_vp, _cp, ctypes.POINTER(_i64), _cp, _sz]
             cls._lib = L
         return cls._lib
 
@@ -200,6 +201,16 @@ class Ref:
         buf = ctypes.create_string_buffer(n + 1)
         cls.lib().sr_tile_rewrite(p.h, path.encode(), tiles.encode(), buf, n + 1, err, len(err))
         return buf.value.decode()
+
+    @classmethod
+    def useful_ops(cls, text: str, path: str) -> int:
+        """count_valid_points of the block at `path` via tile_cost (tile.cpp:404-411)."""
+        p = cls.parse(text)
+        err = ctypes.create_string_buffer(4096)
+        v = _i64()
+        if cls.lib().sr_useful_ops(p.h, path.encode(), ctypes.byref(v), err, len(err)):
+            raise OracleError(err.value.decode())
+        return v.value
 
     @classmethod
     def pipeline(cls, text: str, hwcfg: str) -> str:

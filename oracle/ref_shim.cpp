@@ -250,6 +250,17 @@ int sr_tile_rewrite(void* p, const char* path, const char* tiles, char* buf, std
   return put(out, buf, cap);
 }
 
+// useful_ops of tile_cost (tile.cpp:404-411) = count_valid_points(block) (tile.cpp:338-370).
+int sr_useful_ops(void* p, const char* path, std::int64_t* out, char* err, std::size_t ecap) {
+  return guarded(err, ecap, [&] {
+    const Program& prog = *static_cast<Program*>(p);
+    const Block* blk = block_at_path(&prog.root, path);
+    if (!blk) throw std::runtime_error("bad block path");
+    TileShape ts;
+    *out = tile_cost(*blk, ts, CacheModel{8, std::int64_t{1} << 40}, std::int64_t{1} << 40).useful_ops;
+  });
+}
+
 // apply_pipeline (passes.cpp:905-1023) with a .hwcfg text.
 int sr_pipeline(void* p, const char* hwcfg, char* buf, std::size_t cap, char* err,
                 std::size_t ecap) {

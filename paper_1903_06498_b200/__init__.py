@@ -42,7 +42,7 @@ EXPORTED = [
     "sb_last_error", "sb_status_name", "sb_abi_version",
     "sb_program_parse", "sb_program_free", "sb_program_print", "sb_program_buffer_count",
     "sb_program_buffer_info", "sb_program_output_identity", "sb_program_describe_plan",
-    "sb_program_output_aggregation", "sb_program_restrict_index",
+    "sb_program_output_aggregation", "sb_program_restrict_index", "sb_count_valid_points",
     "sb_context_create", "sb_context_destroy", "sb_context_set_stream", "sb_context_stream",
     "sb_context_sync", "sb_context_launch_count", "sb_device_alloc", "sb_device_free",
     "sb_host_alloc_pinned", "sb_host_free_pinned", "sb_execute", "sb_execute_device",
@@ -88,6 +88,7 @@ def lib() -> ctypes.CDLL:
         L.sb_program_output_identity.argtypes = [vp, ctypes.c_char_p, ctypes.POINTER(i64)]
         L.sb_program_output_aggregation.argtypes = [vp, ctypes.c_char_p, ctypes.POINTER(i32)]
         L.sb_program_restrict_index.argtypes = [vp, ctypes.c_char_p, ctypes.c_char_p, i64, i64, ctypes.POINTER(vp)]
+        L.sb_count_valid_points.argtypes = [vp, vp, ctypes.c_char_p, ctypes.POINTER(i64)]
         L.sb_program_describe_plan.argtypes = [vp, i32, i32, ctypes.c_char_p, ctypes.c_size_t,
                                                ctypes.POINTER(ctypes.c_size_t)]
         L.sb_context_create.argtypes = [i32, ctypes.POINTER(vp)]
@@ -194,6 +195,13 @@ class Program:
 
     def text(self) -> str:
         return print_program(self)
+
+    def count_valid_points(self, block_path: str = "0", ctx: "Context" = None) -> int:
+        """tile.cpp:338-370 on the device (closed form per innermost row)."""
+        v = ctypes.c_int64()
+        _check(lib().sb_count_valid_points((ctx or default_context(0)).handle, self._h, block_path.encode(),
+                                           ctypes.byref(v)))
+        return v.value
 
     def describe_plan(self, fresh_outputs: bool = False, tensor_cores: bool = True, fp32_mode: int = 0) -> str:
         n = ctypes.c_size_t()

@@ -17,6 +17,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -646,6 +647,57 @@ int sb_program_output_identity(const sb_program* p, const char* name, int64_t* v
 
 int sb_program_output_aggregation(const sb_program* p, const char* name, int* agg) {
   return guarded([&] { *agg = static_cast<int>(sb::output_aggregation(p->prog, name)); });
+}
+
+int sb_count_valid_points(sb_context* ctx, const sb_program* p, const char* block_path, int64_t* count) {
+  return guarded([&] {
+    cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const sb::Block* b = &p->prog.root;
+    std::string path = block_path ? block_path : "";
+    std::stringstream ss(path);
+    std::string part;
+    while (!path.empty() && std::getline(ss, part, '.')) {
+      const std::size_t k = static_cast<std::size_t>(std::stoll(part));
+      if (k >= b->stmts.size() || b->stmts[k].kind != sb::StmtKind::Block)
+        throw sb::Error("Unsupported", "no block at path '" + path + "'");
+      b = b->stmts[k].block.get();
+    }
+    // the reference's definition: the block's own ranged indexes, its own constraints
+    std::vector<long long> ranges;
+    std::vector<std::string> names;
+    for (const auto& idx : b->indexes) {
+      if (idx.is_alias) throw sb::Error("InvalidTile", "count_valid_points requires alias-free blocks");
+      names.push_back(idx.name);
+      ranges.push_back(idx.range);
+    }
+    std::int64_t total = 1;
+    for (auto r : ranges) total *= r;
+    if (ranges.empty()) {
+      ranges.push_back(1);
+      names.push_back("");
+    }
+    const int nd = static_cast<int>(ranges.size()), nc = static_cast<int>(b->constraints.size());
+    std::vector<long long> cc(nc), ck(static_cast<std::size_t>(nc) * nd, 0);
+    for (int c = 0; c < nc; c++) {
+      cc[c] = b->constraints[c].constant;
+      for (const auto& [name, k] : b->constraints[c].terms) {
+        auto it = std::find(names.begin(), names.end(), name);
+        if (it == names.end()) throw sb::Error("UnboundIndex", "unbound index '" + name + "'");
+        ck[static_cast<std::size_t>(c) * nd + (it - names.begin())] = k;
+      }
+    }
+    if (total == 0) {
+      *count = 0;
+      return;
+    }
+    void* scratch = nullptr;
+    cuda_check(cudaMalloc(&scratch, sb::count_points_scratch_bytes()), "cudaMalloc(count)");
+    unsigned long long h = 0;
+    cudaError_t e = sb::launch_count_points(nd, ranges.data(), nc, cc.data(), ck.data(), scratch, &h, ctx->stream);
+    cudaFree(scratch);
+    cuda_check(e, "count_points");
+    *count = static_cast<std::int64_t>(h);
+  });
 }
 
 int sb_program_restrict_index(const sb_program* p, const char* block_path, const char* index, int64_t lo, int64_t hi,

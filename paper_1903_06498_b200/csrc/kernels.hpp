@@ -58,6 +58,11 @@ long long limb_b_off(const GemmPlan& g, int s);
 long long limb_plane_bytes_b(const GemmPlan& g);
 cudaError_t launch_gemm_tc(const GemmPlan& g, const GemmArgs& args, cudaStream_t s, int num_sms);
 
+// Constraint-satisfying points of one block (kernels/count.cu); cons_k is [nc][nd].
+cudaError_t launch_count_points(int nd, const long long* ranges, int nc, const long long* cons_c,
+                                const long long* cons_k, void* scratch, unsigned long long* h_out, cudaStream_t s);
+std::size_t count_points_scratch_bytes();
+
 // Windowed max/min over constraint-bounded taps, 16-byte channel vectors (kernels/pool.cu).
 const char* pool_unsupported(const PoolPlan& pp);
 cudaError_t launch_pool(const PoolPlan& pp, const void* in, void* out, cudaStream_t s);
