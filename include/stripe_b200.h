@@ -148,6 +148,13 @@ int sb_execute_device(sb_context* ctx, sb_program* p, const sb_device_buffer* bu
                       const sb_exec_options* opts);
 
 /* ---- CUDA graphs (launch overhead off the critical path) ---- */
+/* Asynchronous sb_execute: native-width carriers in pinned host memory (sb_host_alloc_pinned),
+ * H2D + kernels + D2H enqueued on the context stream and the call returns; results and
+ * device errors are available after sb_context_sync.  Two contexts ping-ponging steps
+ * overlap one step's device-to-host copy with the next step's host-to-device copy. */
+int sb_execute_async(sb_context* ctx, sb_program* p, sb_host_buffer* bufs, int n,
+                     const sb_exec_options* opts);
+
 typedef struct sb_graph sb_graph;
 /* Starts capturing everything this thread enqueues on the context stream
  * (sb_execute_device calls; plans must have run once outside capture). */

@@ -45,7 +45,7 @@ EXPORTED = [
     "sb_program_output_aggregation", "sb_program_restrict_index", "sb_count_valid_points",
     "sb_context_create", "sb_context_destroy", "sb_context_set_stream", "sb_context_stream",
     "sb_context_sync", "sb_context_launch_count", "sb_device_alloc", "sb_device_free",
-    "sb_host_alloc_pinned", "sb_host_free_pinned", "sb_execute", "sb_execute_device",
+    "sb_host_alloc_pinned", "sb_host_free_pinned", "sb_execute", "sb_execute_device", "sb_execute_async",
     "sb_graph_begin", "sb_graph_end", "sb_graph_launch", "sb_graph_free",
 ]
 
@@ -106,6 +106,7 @@ def lib() -> ctypes.CDLL:
         L.sb_host_free_pinned.argtypes = [vp]
         L.sb_execute.argtypes = [vp, vp, ctypes.POINTER(HostBuffer), i32, ctypes.POINTER(_Opts)]
         L.sb_execute_device.argtypes = [vp, vp, ctypes.POINTER(DeviceBuffer), i32, ctypes.POINTER(_Opts)]
+        L.sb_execute_async.argtypes = [vp, vp, ctypes.POINTER(HostBuffer), i32, ctypes.POINTER(_Opts)]
         L.sb_graph_begin.argtypes = [vp]
         L.sb_graph_end.argtypes = [vp, ctypes.POINTER(vp)]
         L.sb_graph_launch.argtypes = [vp, vp]
@@ -327,6 +328,18 @@ class Context:
                                  a.ctypes.data, a.size))
         arr = (HostBuffer * len(hb))(*hb)
         _check(lib().sb_execute(self._h, program.handle, arr, len(hb), ctypes.byref(opts._c())))
+
+    def execute_native_async(self, program: Program, arrays: Dict[str, np.ndarray], prepare=(),
+                             opts: Optional[ExecOptions] = None) -> None:
+        """sb_execute_async: arrays must live in pinned host memory; results after sync()."""
+        opts = opts or ExecOptions()
+        hb = []
+        for name, a in arrays.items():
+            assert a.flags["C_CONTIGUOUS"]
+            hb.append(HostBuffer(name.encode(), SB_CARRIER_NATIVE, SB_BUF_PREPARE if name in prepare else 0,
+                                 a.ctypes.data, a.size))
+        arr = (HostBuffer * len(hb))(*hb)
+        _check(lib().sb_execute_async(self._h, program.handle, arr, len(hb), ctypes.byref(opts._c())))
 
     def execute_device(self, program: Program, buffers: Dict[str, tuple], opts: Optional[ExecOptions] = None) -> None:
         """buffers: name -> (device_ptr, count, flags).  Asynchronous on the context stream."""

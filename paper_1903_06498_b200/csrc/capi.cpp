@@ -841,8 +841,15 @@ int sb_execute_device(sb_context* ctx, sb_program* p, const sb_device_buffer* bu
   });
 }
 
-int sb_execute(sb_context* ctx, sb_program* p, sb_host_buffer* bufs, int n, const sb_exec_options* opts) {
+}  // extern "C"
+
+namespace {
+int execute_host(sb_context* ctx, sb_program* p, sb_host_buffer* bufs, int n, const sb_exec_options* opts, bool async) {
   return guarded([&] {
+    if (async)
+      for (int i = 0; i < n; i++)
+        if (bufs[i].carrier != SB_CARRIER_NATIVE)
+          throw sb::Error("Unsupported", "sb_execute_async needs native-width carriers (pinned host memory)");
     check_opts(opts);
     cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
     const auto& prog = p->prog;
@@ -926,6 +933,7 @@ int sb_execute(sb_context* ctx, sb_program* p, sb_host_buffer* bufs, int n, cons
       cuda_check(cudaMemcpyAsync(dst, ptrs[r], b.elements * kind_bytes(kind), cudaMemcpyDeviceToHost, ctx->stream),
                  "D2H");
     }
+    if (async) return;  // errors surface at sb_context_sync
     ctx->h_err->code = 1;
     check_device_error(ctx, c);
     for (std::size_t r = 0; r < nr; r++) {
@@ -945,6 +953,17 @@ int sb_execute(sb_context* ctx, sb_program* p, sb_host_buffer* bufs, int n, cons
       }
     }
   });
+}
+}  // namespace
+
+extern "C" {
+
+int sb_execute(sb_context* ctx, sb_program* p, sb_host_buffer* bufs, int n, const sb_exec_options* opts) {
+  return execute_host(ctx, p, bufs, n, opts, false);
+}
+
+int sb_execute_async(sb_context* ctx, sb_program* p, sb_host_buffer* bufs, int n, const sb_exec_options* opts) {
+  return execute_host(ctx, p, bufs, n, opts, true);
 }
 
 }  // extern "C"

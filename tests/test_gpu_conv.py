@@ -145,3 +145,40 @@ def test_fused_epilogue_int64_semantics_near_overflow():
     exp = expected(text, inp)
     got = run_device(text, inp)
     np.testing.assert_array_equal(got["O"], exp["O"])
+
+
+def test_async_two_context_pingpong_matches_sync():
+    """sb_execute_async on two contexts (the bench's e2e pattern) gives the sync results."""
+    import ctypes
+
+    import paper_1903_06498_b200 as sb
+    from paper_1903_06498_b200 import workloads as W
+    text = W.conv2d(4, 10, 10, 64, 64)
+    prog = sb.parse_program(text)
+    ctxs = [sb.Context(0), sb.Context(0)]
+    pins = []
+
+    def pinned(n, ct):
+        p = ctypes.c_void_p()
+        sb._check(sb.lib().sb_host_alloc_pinned(n * ctypes.sizeof(ct), ctypes.byref(p)))
+        pins.append(p)
+        return np.ctypeslib.as_array((ct * n).from_address(p.value))
+
+    rng = np.random.default_rng(5)
+    steps = []
+    for i in range(4):
+        I = pinned(4 * 10 * 10 * 64, ctypes.c_int8)
+        F = pinned(9 * 64 * 64, ctypes.c_int8)
+        O = pinned(4 * 10 * 10 * 64, ctypes.c_int32)
+        I[:] = rng.integers(-128, 128, I.size, dtype=np.int8)
+        F[:] = rng.integers(-128, 128, F.size, dtype=np.int8)
+        steps.append((I, F, O))
+        ctxs[i % 2].execute_native_async(prog, {"I": I, "F": F, "O": O}, prepare=("O",))
+    for c in ctxs:
+        c.sync()
+    for I, F, O in steps:
+        ref = np.empty_like(O)
+        sb.default_context(0).execute_native(prog, {"I": I.copy(), "F": F.copy(), "O": ref}, prepare=("O",))
+        np.testing.assert_array_equal(O, ref)
+    for p in pins:
+        sb.lib().sb_host_free_pinned(p)
