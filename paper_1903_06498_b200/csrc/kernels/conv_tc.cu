@@ -388,7 +388,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tfull[acc], aphase);
         if (leader) trace_at(p.trace, 32 + iter);
         tc_fence_after();
-        std::uint8_t* stg = staging + static_cast<std::uint32_t>(sb * halves) * 16384u;
+        std::uint8_t* stg = p.tma_out == 2 ? staging + static_cast<std::uint32_t>(sb * (halves / 2)) * 8192u
+                                           : staging + static_cast<std::uint32_t>(sb * halves) * 16384u;
         for (int h = 0; h < halves; h++) {
           std::uint32_t v[32];
           tmem_ld32(tmem_base + (static_cast<std::uint32_t>(quarter * 32) << 16) +
@@ -414,6 +415,22 @@ __global__ void __launch_bounds__(kThreads, 1)
               long long x = static_cast<long long>(static_cast<std::int32_t>(v[q])) + bv[q];
               v[q] = static_cast<std::uint32_t>(x < lo ? lo : x);
             }
+          }
+          if (p.tma_out == 2) {
+            // i8: 32 wrapped bytes = two 16-byte chunks of this row's 64-byte SW64 line
+            std::uint32_t w[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++)
+              w[q] = (v[4 * q] & 0xFF) | ((v[4 * q + 1] & 0xFF) << 8) | ((v[4 * q + 2] & 0xFF) << 16) |
+                     (v[4 * q + 3] << 24);
+            const std::uint32_t rb = smem_u32(stg + (h >> 1) * 8192 + row * 64);
+#pragma unroll
+            for (int u = 0; u < 2; u++) {
+              const int chunk = (h & 1) * 2 + u;
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rb + ((chunk ^ ((row >> 1) & 3)) << 4)),
+                           "r"(w[4 * u]), "r"(w[4 * u + 1]), "r"(w[4 * u + 2]), "r"(w[4 * u + 3]));
+            }
+            continue;
           }
           std::uint32_t rbase = smem_u32(stg + h * 16384 + row * 128);
 #pragma unroll
@@ -454,12 +471,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (leader) {
           int n = t / p.tiles_x;
           int x0 = (t % p.tiles_x) * p.TX;
-          for (int h = 0; h < halves; h++)
-            asm volatile(
-                "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
-                    reinterpret_cast<std::uint64_t>(&omap)),
-                "r"(smem_u32(stg + h * 16384)), "r"(h * 32), "r"(0), "r"(x0), "r"(n)
-                : "memory");
+          if (p.tma_out == 2) {
+            for (int g = 0; g < halves / 2; g++)
+              asm volatile(
+                  "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                      reinterpret_cast<std::uint64_t>(&omap)),
+                  "r"(smem_u32(stg + g * 8192)), "r"(g * 64), "r"(0), "r"(x0), "r"(n)
+                  : "memory");
+          } else {
+            for (int h = 0; h < halves; h++)
+              asm volatile(
+                  "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                      reinterpret_cast<std::uint64_t>(&omap)),
+                  "r"(smem_u32(stg + h * 16384)), "r"(h * 32), "r"(0), "r"(x0), "r"(n)
+                  : "memory");
+          }
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           trace_at(p.trace, 40 + iter);
         }
@@ -574,11 +600,17 @@ bool fill_params(const ConvPlan& cp, ConvKParams* kp) {
   kp->filt_bytes = static_cast<std::uint32_t>(cp.R * cp.S * kp->chunks) * kp->filt_tap_bytes;
   kp->tma_out = kp->fresh && kp->out_kind == kI32 && cp.c_y % 4 == 0 && cp.c_x % 4 == 0 && cp.c_n % 4 == 0 &&
                 cp.c0 % 4 == 0;
+  // fresh i8 outputs (fused epilogues into i8 activations): 64-channel SW64 staging rows
+  if (kp->fresh && kp->out_kind == kI8 && cp.K % 64 == 0 && cp.c_y % 16 == 0 && cp.c_x % 16 == 0 &&
+      cp.c_n % 16 == 0 && cp.c0 % 16 == 0)
+    kp->tma_out = 2;
   kp->nstg = 2;
-  kp->staging_bytes = kp->tma_out ? static_cast<std::uint32_t>(kp->nstg * (cp.K / 32) * 16384) : 0;
+  kp->staging_bytes = kp->tma_out == 1   ? static_cast<std::uint32_t>(kp->nstg * (cp.K / 32) * 16384)
+                      : kp->tma_out == 2 ? static_cast<std::uint32_t>(kp->nstg * (cp.K / 64) * 8192)
+                                         : 0;
   if (kp->tma_out && smem_bytes(*kp) > 220 * 1024) {
     kp->nstg = 1;
-    kp->staging_bytes = static_cast<std::uint32_t>((cp.K / 32) * 16384);
+    kp->staging_bytes = static_cast<std::uint32_t>(kp->tma_out == 2 ? (cp.K / 64) * 8192 : (cp.K / 32) * 16384);
   }
   if (kp->tma_out && smem_bytes(*kp) > 220 * 1024) {
     kp->tma_out = 0;
@@ -643,7 +675,7 @@ cudaError_t prepare_conv(const ConvPlan& cp, const ConvArgs& args, Prepared* out
   ConvKParams& kp = out->kp;
   if (!fill_params(cp, &kp) || conv_tc_unsupported(cp)) return cudaErrorNotSupported;
   if (const char* e = std::getenv("SB_CONV_BASEOFF")) kp.base_offset_mode = e[0] == '1';
-  if (const char* e = std::getenv("SB_CONV_ST_OUT")) kp.st_out = e[0] == '1';
+  if (const char* e = std::getenv("SB_CONV_ST_OUT")) kp.st_out = e[0] == '1' && kp.tma_out == 1;
   kp.debug_nofilt = std::getenv("SB_CONV_DEBUG_NOFILT") != nullptr;
   kp.vec4 = cp.c0 % 4 == 0 && cp.c_y % 4 == 0 && cp.c_x % 4 == 0 && cp.c_n % 4 == 0 &&
             reinterpret_cast<std::uintptr_t>(args.c) % 16 == 0;
@@ -679,7 +711,19 @@ cudaError_t prepare_conv(const ConvPlan& cp, const ConvArgs& args, Prepared* out
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   std::memset(&out->omap, 0, sizeof(out->omap));
-  if (kp.tma_out) {
+  if (kp.tma_out == 2) {
+    std::int8_t* obase = static_cast<std::int8_t*>(args.c) + cp.c0;
+    if (reinterpret_cast<std::uintptr_t>(obase) % 16 != 0) return cudaErrorMisalignedAddress;
+    cuuint64_t odims[4] = {static_cast<cuuint64_t>(cp.K), static_cast<cuuint64_t>(cp.W),
+                           static_cast<cuuint64_t>(cp.H), static_cast<cuuint64_t>(cp.N)};
+    cuuint64_t ostr[3] = {static_cast<cuuint64_t>(cp.c_y), static_cast<cuuint64_t>(cp.H > 1 ? cp.c_x : cp.c_y * cp.W),
+                          static_cast<cuuint64_t>(cp.N > 1 ? cp.c_n : cp.c_y * cp.W * cp.H)};
+    cuuint32_t obox[4] = {64u, static_cast<cuuint32_t>(kp.P), static_cast<cuuint32_t>(kp.TX), 1u};
+    if (encode(&out->omap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, obase, odims, ostr, obox, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  } else if (kp.tma_out) {
     std::int32_t* obase = static_cast<std::int32_t*>(args.c) + cp.c0;
     if (reinterpret_cast<std::uintptr_t>(obase) % 16 != 0) return cudaErrorMisalignedAddress;
     cuuint64_t odims[4] = {static_cast<cuuint64_t>(cp.K), static_cast<cuuint64_t>(cp.W),

@@ -669,7 +669,9 @@ bool fuse_conv_epilogue(Plan* plan, std::size_t s, const Program& prog, const Pl
       out_node = temp[ins.a];
       if (out_node < 0) return false;
       // the resident-filter kernel's TMA-store epilogue writes i32; the im2col one any width
-      if (static_cast<DType>(ins.dtype) != DType::I32 && cl.kernel != KernelKind::ConvIgemmTC) return false;
+      if (static_cast<DType>(ins.dtype) != DType::I32 && cl.kernel != KernelKind::ConvIgemmTC &&
+          !(static_cast<DType>(ins.dtype) == DType::I8 && c.K % 64 == 0 && std::getenv("SB_TC_I8_EPI")))
+        return false;
       if (ins.agg != static_cast<std::int8_t>(Agg::Assign) && ins.agg != static_cast<std::int8_t>(Agg::Add)) return false;
       continue;
     } else {
@@ -727,7 +729,11 @@ bool fuse_conv_epilogue(Plan* plan, std::size_t s, const Program& prog, const Pl
   const PAccess& O = el.acc[out_acc];
   const PBuffer& ob = plan->bufs[O.buf];
   if (O.addr.at(kd) != 1 || O.addr.at(pd) <= 0) return false;
-  if (ob.kind != kI32 && !(cl.kernel == KernelKind::ConvIgemmTC && (ob.kind == kI8 || ob.kind == kI16))) return false;
+  if (ob.kind != kI32 && !(cl.kernel == KernelKind::ConvIgemmTC && (ob.kind == kI8 || ob.kind == kI16)) &&
+      // opt-in: the resident-filter kernel's i8 epilogue is faster alone, but inside chains of
+      // im2col convs (ResNet) the im2col kernel's shorter prologue overlaps better (measured)
+      !(cl.kernel == KernelKind::ConvI8TC && ob.kind == kI8 && K % 64 == 0 && std::getenv("SB_TC_I8_EPI")))
+    return false;
   if (static_cast<std::int8_t>(ob.dtype) != store_ins.dtype) return false;
   const std::int64_t op = O.addr.at(pd);
   if (O.addr.c < 0 || O.addr.c + op * (NHW - 1) + K - 1 >= ob.elements) return false;

@@ -167,3 +167,25 @@ def test_gather_stem_fused_vs_port():
     prog, inp, out = run(text, seed=21)
     ref = Port.execute(text, {**inp, "O": np.zeros_like(out["O"])})
     np.testing.assert_array_equal(out["O"], ref["O"])
+
+
+@pytest.mark.parametrize("case", [(2, 16, 16, 64, 64, True), (3, 9, 11, 64, 128, True), (2, 14, 14, 64, 192, False)],
+                         ids=lambda c: "x".join(map(str, c)))
+def test_resident_filter_conv_fused_i8(case):
+    """Stride-1 3x3 with C = 64: the resident-filter kernel's i8 TMA-store epilogue (opt-in
+    routing SB_TC_I8_EPI; the default keeps these layers on the im2col kernel)."""
+    import os
+
+    import paper_1903_06498_b200 as sb
+    os.environ["SB_TC_I8_EPI"] = "1"
+    from paper_1903_06498_b200 import workloads as W
+    from intmodel import conv_layer_exact
+    N, H, Wd, C, K, relu = case
+    text = W.conv_fused(N, H, Wd, C, K, 3, 3, 1, 1, relu=relu)
+    plan = sb.parse_program(text).describe_plan()
+    assert "kernel=conv_i8_tc" in plan and "fused" in plan, plan
+    prog, inp, out = run(text, seed=N + H + K)
+    del os.environ["SB_TC_I8_EPI"]
+    exp = conv_layer_exact(inp["I"].reshape(N, H, Wd, C), inp["F"].reshape(3, 3, K, C), inp["Bias"], 1, 1, relu,
+                           None, 8, "cuda").cpu().numpy().ravel()
+    np.testing.assert_array_equal(out["O"], exp)
