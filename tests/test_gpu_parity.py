@@ -115,3 +115,39 @@ def test_live_tilings():
             got = run_device(text, st)
             for n in exp:
                 np.testing.assert_array_equal(got[n], exp[n][1], err_msg=f"{kind} {tiles}")
+
+
+def test_concurrent_host_threads_distinct_contexts():
+    """SPEC.md:263 / SURVEY §8(b) threading: execute is reentrant; one context per host
+    thread, the same parsed program shared (plans built under the program's lock)."""
+    import threading
+
+    import paper_1903_06498_b200 as sb
+    from paper_1903_06498_b200 import workloads as W
+    text = W.conv2d(2, 12, 12, 64, 64)
+    prog = sb.parse_program(text)
+    rng = np.random.default_rng(3)
+    I = rng.integers(-128, 128, 2 * 12 * 12 * 64).astype(np.int64)
+    F = rng.integers(-128, 128, 9 * 64 * 64).astype(np.int64)
+    ref = {"I": sb.Buffer(8, I.copy()), "F": sb.Buffer(8, F.copy())}
+    sb.prepare_outputs(prog, ref)
+    sb.execute(prog, ref)
+    errors, results = [], []
+
+    def worker():
+        try:
+            ctx = sb.Context(0)
+            for _ in range(5):
+                st = {"I": sb.Buffer(8, I.copy()), "F": sb.Buffer(8, F.copy())}
+                sb.prepare_outputs(prog, st)
+                ctx.execute(prog, st)
+                results.append(np.array_equal(st["O"].data, ref["O"].data))
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    threads = [threading.Thread(target=worker) for _ in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors and len(results) == 20 and all(results)
