@@ -111,6 +111,15 @@ struct sb_context {
   std::vector<cudaEvent_t> step_events;    // per plan step (reused across runs)
   cudaEvent_t fork_event = nullptr, join_events[8] = {};
   cudaStream_t aux_streams[4] = {};        // intra-step forks (byte-limb sums)
+  // Launches that may still be running on `stream` since the last serialization point
+  // (programmatic dependent launches that did not wait): byte ranges read / written.
+  struct Span {
+    std::uintptr_t lo, hi;
+  };
+  struct InFlight {
+    std::vector<Span> rd, wr;
+  };
+  std::vector<InFlight> window;
   cudaEvent_t aux_fork = nullptr, aux_join[4] = {};
   std::vector<std::pair<void*, std::size_t>> roots;  // host-path device buffers
   std::vector<std::pair<void*, std::size_t>> pinned;  // host-path staging
@@ -329,9 +338,53 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
   auto& st = ensure_state(ctx, c);
   const auto& plan = c->plan;
   auto ptr_of = [&](int b) { return plan.bufs[b].root ? root_ptr[plan.bufs[b].root_index] : st.scratch[b]; };
+  const bool single_lane = c->lanes.nlanes <= 1;
+  // Dependency-aware PDL: a tensor-core launch that touches nothing an in-flight launch writes
+  // (and writes nothing one reads) need not wait for its predecessor at all, so consecutive
+  // independent executes overlap completely (the previous grid's tail wave is filled).
+  auto pdl_mode = [&](std::size_t i) -> int {
+    // opt-in (SB_PDL_FREE=1): measured no gain on the configs (the first-tile filter fetch,
+    // not the tail wave, dominates the gap between kernels), so the default keeps every
+    // tensor-core launch waiting on its predecessor
+    static const bool allow_free = std::getenv("SB_PDL_FREE") != nullptr;
+    if (!single_lane || !allow_free) {
+      ctx->window.clear();
+      return sb::kPdlWait;
+    }
+    std::vector<int> rd, wr;
+    sb::step_access(plan.steps[i], &rd, &wr);
+    sb_context::InFlight me;
+    auto span = [&](int b) {
+      const auto lo = reinterpret_cast<std::uintptr_t>(ptr_of(b));
+      return sb_context::Span{lo, lo + static_cast<std::uintptr_t>(plan.bufs[b].elements * kind_bytes(plan.bufs[b].kind))};
+    };
+    for (int b : rd) me.rd.push_back(span(b));
+    for (int b : wr) me.wr.push_back(span(b));
+    auto ov = [](const std::vector<sb_context::Span>& x, const std::vector<sb_context::Span>& y) {
+      for (const auto& a : x)
+        for (const auto& b : y)
+          if (a.lo < b.hi && b.lo < a.hi) return true;
+      return false;
+    };
+    bool any = false;
+    for (const auto& w : ctx->window) any |= ov(w.wr, me.rd) || ov(w.wr, me.wr) || ov(w.rd, me.wr);
+    if (!any && ctx->window.size() < 64) {
+      ctx->window.push_back(std::move(me));
+      return sb::kPdlFree;
+    }
+    const bool one = ctx->window.size() == 1;  // only the immediately preceding launch may still run
+    ctx->window.clear();
+    ctx->window.push_back(std::move(me));
+    return one ? sb::kPdlWait : sb::kPdlOff;
+  };
   auto step = [&](std::size_t i) {
     const auto& s = plan.steps[i];
     if (s.elided) return;
+    const bool tc_single = s.kind == sb::PStep::Launch &&
+                           ((s.launch.kernel == sb::KernelKind::ConvI8TC) ||
+                            (s.launch.kernel == sb::KernelKind::ConvIgemmTC && !s.launch.conv.packed) ||
+                            (s.launch.kernel == sb::KernelKind::GemmI8TC && !s.launch.gemm.limbs_a));
+    if (!tc_single) ctx->window.clear();  // plain stream-ordered launches serialize everything
     if (s.kind == sb::PStep::Fill) {
       const auto& pb = plan.bufs[s.buf];
       cuda_check(sb::launch_fill(ptr_of(s.buf), pb.kind, pb.elements, s.value, ctx->stream), "fill");
@@ -353,6 +406,7 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
         a.vec_kind = plan.bufs[l.conv.vec_buf].kind;
       }
       if (l.conv.epi_res) a.res = ptr_of(l.conv.res_buf);
+      if (tc_single) a.pdl_mode = pdl_mode(i);
       if (l.kernel == sb::KernelKind::ConvI8TC) {
         cuda_check(sb::launch_conv_tc(l.conv, a, ctx->stream, ctx->num_sms), "conv_tc");
       } else if (l.conv.packed) {
@@ -438,6 +492,7 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
     }
     if (l.kernel == sb::KernelKind::GemmI8TC) {
       sb::GemmArgs a{ptr_of(l.gemm.a_buf), ptr_of(l.gemm.b_buf), ptr_of(l.gemm.c_buf)};
+      a.pdl_mode = pdl_mode(i);
       cuda_check(sb::launch_gemm_tc(l.gemm, a, ctx->stream, ctx->num_sms), "gemm_tc");
       ctx->launches++;
       return;
@@ -763,7 +818,10 @@ int sb_context_create(int device, sb_context** out) {
 void sb_context_destroy(sb_context* ctx) { delete ctx; }
 
 int sb_context_set_stream(sb_context* ctx, void* s) {
-  return guarded([&] { ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own; });
+  return guarded([&] {
+    ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own;
+    ctx->window.clear();
+  });
 }
 
 void* sb_context_stream(sb_context* ctx) { return ctx->stream; }
@@ -771,6 +829,7 @@ void* sb_context_stream(sb_context* ctx) { return ctx->stream; }
 int sb_context_sync(sb_context* ctx) {
   return guarded([&] {
     cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    ctx->window.clear();
     ctx->h_err->code = 1;
     check_device_error(ctx, nullptr);
   });
@@ -846,6 +905,7 @@ int sb_execute_device(sb_context* ctx, sb_program* p, const sb_device_buffer* bu
 namespace {
 int execute_host(sb_context* ctx, sb_program* p, sb_host_buffer* bufs, int n, const sb_exec_options* opts, bool async) {
   return guarded([&] {
+    ctx->window.clear();  // host copies serialize the stream
     if (async)
       for (int i = 0; i < n; i++)
         if (bufs[i].carrier != SB_CARRIER_NATIVE)
@@ -989,12 +1049,14 @@ int sb_graph_begin(sb_context* ctx) {
   return guarded([&] {
     cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
     g_capture_mark = ctx->launches;
+    ctx->window.clear();
     cuda_check(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
   });
 }
 
 int sb_graph_end(sb_context* ctx, sb_graph** out) {
   return guarded([&] {
+    ctx->window.clear();
     auto g = std::make_unique<sb_graph>();
     cuda_check(cudaStreamEndCapture(ctx->stream, &g->graph), "cudaStreamEndCapture");
     cuda_check(cudaGraphInstantiate(&g->exec, g->graph, 0), "cudaGraphInstantiate");

@@ -35,10 +35,16 @@ int reduce_vec_lanes(int in_kind);
 cudaError_t launch_reduce(const ReduceArgs& a, cudaStream_t s);
 
 // tcgen05 GEMM (kernels/gemm_tc.cu).
+// Programmatic dependent launch per call (capi.cpp decides from buffer overlap with the
+// launches that may still run): 0 plain stream order, 1 PDL + griddepcontrol.wait,
+// 2 PDL without waiting (independent of every in-flight launch).
+enum : int { kPdlOff = 0, kPdlWait = 1, kPdlFree = 2 };
+
 struct GemmArgs {
   const void* a;
   const void* b;
   void* c;
+  int pdl_mode = kPdlWait;
 };
 const char* gemm_tc_unsupported(const GemmPlan& g);
 // fp32 mode: exact-order SIMT GEMM, bitwise equal to the F32 oracle (kernels/gemm_f32.cu)
@@ -77,6 +83,7 @@ struct ConvArgs {
   const void* vec = nullptr;  // fused-epilogue per-channel vector buffer
   int vec_kind = 0;
   const void* res = nullptr;  // fused-epilogue residual (i8, pixel-major)
+  int pdl_mode = kPdlWait;
 };
 // Host-side checks that the plan fits the kernel's tiling; empty string = ok.
 const char* conv_tc_unsupported(const ConvPlan& cp);

@@ -56,6 +56,7 @@ struct IgKParams {
   // gather mode (ConvPlan::packed): A rows built by warps 6-9 from the original input
   int gather, tab_off, rsc, g_C, g_S, g_R, g_run;
   int epi_warps;  // 4 or 8 (two warps per TMEM lane quarter, each taking half the columns)
+  int pdl_wait;   // griddepcontrol.wait before touching buffers (else independent of in-flight work)
   long long g_an, g_ax, g_ay, g_a0;
   int g_ulo, g_uhi, g_vlo, g_vhi;
   const std::int8_t* g_in;
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+      if (p.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
       const int PQ = p.P * p.Q;
       int stage = 0;
       std::uint32_t phase = 0;
@@ -275,7 +276,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
         tdj[kk] = 0;
       }
     }
-    if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (p.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("bar.sync 2, 256;" ::: "memory");
     const int PQ = p.P * p.Q;
     const int sw = p.bk == 128 ? (r & 7) : ((r >> 1) & 3);
@@ -369,7 +370,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       // per-output-channel vector (e.g. the bias) as int32 in smem, read with ld.shared.v4; with
       // fast_clamp also the threshold t[k] = clamp32(lo - vec[k]): acc + res + vec >= lo
       // <=> acc + res >= t[k] exactly, because |acc + res| < 2^31 - 1
-      if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+      if (p.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
       for (int k = threadIdx.x - 64; k < p.N; k += ethreads) {
         const long long vi = static_cast<long long>(k) * p.vec_k;
         const std::int32_t b = !p.epi_vec ? 0
@@ -383,7 +384,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
         }
       }
     }
-    if (p.epi_res && leader && p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (p.epi_res && leader && p.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("bar.sync 1, %0;" ::"r"(ethreads) : "memory");
     const long long lo = p.epi_lo ? p.lo : LLONG_MIN;
     const bool relu0 = p.epi_lo && p.lo == 0;
@@ -926,7 +927,8 @@ cudaError_t launch_conv_igemm(const ConvPlan& cp, const ConvArgs& args, cudaStre
     }
   }
   IgKParams kp = pr->kp;
-  kp.pdl = 1;
+  kp.pdl = args.pdl_mode != kPdlOff ? 1 : 0;
+  kp.pdl_wait = args.pdl_mode == kPdlWait ? 1 : 0;
   const int tiles = kp.tiles_m * kp.tiles_n;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(tiles < num_sms ? tiles : num_sms));
@@ -937,7 +939,7 @@ cudaError_t launch_conv_igemm(const ConvPlan& cp, const ConvArgs& args, cudaStre
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = kp.pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, conv_igemm_i8_kernel, pr->amap, pr->bmap, pr->cmap, pr->rmap, kp);
 }
 

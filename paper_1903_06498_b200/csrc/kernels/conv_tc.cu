@@ -64,6 +64,7 @@ struct ConvKParams {
   int base_offset_mode;   // experimental: encode (addr >> 7) & 7 into the descriptor base offset
   int st_out;             // tma_out staging drained with coalesced LSU stores instead of TMA stores
   int vec4;               // direct path: 16-byte aligned i32 rows (c0, strides multiples of 4)
+  int pdl_wait;           // griddepcontrol.wait before touching buffers (else independent)
   int cluster;            // CTAs per thread-block cluster (filter multicast)
   int debug_nofilt;       // timing experiments only
   int pdl;                // launched with programmatic stream serialization
@@ -258,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
       };
       bool filter_issued = false;
-      if (p.pdl) {
+      if (p.pdl_wait) {
         // Programmatic dependent launch: this prologue overlapped the previous kernel's tail.
         // An immutable filter (a root `in` buffer nothing in the plan writes) may be fetched
         // before the dependency resolves; the activations only after it.
@@ -791,7 +792,8 @@ cudaError_t launch_conv_tc(const ConvPlan& cp, const ConvArgs& args, cudaStream_
     const char* e = std::getenv("SB_CONV_PDL");
     return e ? e[0] == '1' : true;
   }();
-  kp.pdl = pdl ? 1 : 0;
+  kp.pdl = pdl && args.pdl_mode != kPdlOff ? 1 : 0;
+  kp.pdl_wait = kp.pdl && args.pdl_mode == kPdlWait ? 1 : 0;
   kp.filter_early = args.b_immutable ? 1 : 0;
   kp.epi = cp.epi ? 1 : 0;
   kp.epi_vec = cp.epi_vec ? 1 : 0;
@@ -809,7 +811,7 @@ cudaError_t launch_conv_tc(const ConvPlan& cp, const ConvArgs& args, cudaStream_
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 2 : 1;
+  cfg.numAttrs = kp.pdl ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, conv_i8_tc_kernel, pr->amap, pr->fmap, pr->omap, args.c, kp);
 }
 

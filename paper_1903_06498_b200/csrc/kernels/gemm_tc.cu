@@ -42,6 +42,7 @@ struct GemmKParams {
   int pdl, b_early;
   int tf32;  // kind::tf32 (fp32 accumulators, f32 output)
   int bk_el;  // k-block width in elements (128 bytes)
+  int pdl_wait;
 };
 
 __device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
@@ -162,7 +163,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+      if (p.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
       int stage = 0;
       std::uint32_t phase = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
@@ -693,7 +694,8 @@ cudaError_t launch_gemm_tc(const GemmPlan& g, const GemmArgs& args, cudaStream_t
     }
   }
   GemmKParams kp = pr->kp;
-  kp.pdl = 1;
+  kp.pdl = args.pdl_mode != kPdlOff ? 1 : 0;
+  kp.pdl_wait = args.pdl_mode == kPdlWait ? 1 : 0;
   int tiles = kp.tiles_m * kp.tiles_n;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(tiles < num_sms ? tiles : num_sms));
@@ -704,7 +706,7 @@ cudaError_t launch_gemm_tc(const GemmPlan& g, const GemmArgs& args, cudaStream_t
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = kp.pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, gemm_i8_tc_kernel, pr->amap, pr->bmap, pr->cmap, kp);
 }
 
