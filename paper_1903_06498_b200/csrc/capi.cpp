@@ -409,6 +409,17 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
       if (tc_single) a.pdl_mode = pdl_mode(i);
       if (l.kernel == sb::KernelKind::ConvI8TC) {
         cuda_check(sb::launch_conv_tc(l.conv, a, ctx->stream, ctx->num_sms), "conv_tc");
+      } else if (l.conv.packed && l.conv.fold_x) {
+        // phase-folded small-channel conv: fold the input and the filter, then the stride-1
+        // im2col conv over the folded copy (packed_view)
+        void* fa = ptr_of(l.conv.pack_a);
+        void* pb = ptr_of(l.conv.pack_b);
+        cuda_check(sb::launch_conv_fold(l.conv, a.a, fa, ctx->stream), "conv_fold");
+        cuda_check(sb::launch_conv_pack_filter(l.conv, a.b, pb, ctx->stream), "conv_pack_filter");
+        ctx->launches += 2;
+        a.a = fa;
+        a.b = pb;
+        cuda_check(sb::launch_conv_igemm(sb::packed_view(l.conv), a, ctx->stream, ctx->num_sms), "conv_igemm");
       } else if (l.conv.packed) {
         // small-channel conv: filter packed to [K, pack_k]; A rows gathered inside the kernel
         void* pb = ptr_of(l.conv.pack_b);

@@ -95,5 +95,7 @@ cudaError_t launch_conv_igemm(const ConvPlan& cp, const ConvArgs& args, cudaStre
 // 1x1 im2col GEMM (ConvPlan::packed).
 cudaError_t launch_conv_pack(const ConvPlan& cp, const void* a, const void* b, void* pa, void* pb, cudaStream_t s);
 cudaError_t launch_conv_pack_filter(const ConvPlan& cp, const void* b, void* pb, cudaStream_t s);
+// Phase-folds the input of a folded small-channel conv (ConvPlan::fold_x) into f.
+cudaError_t launch_conv_fold(const ConvPlan& cp, const void* a, void* f, cudaStream_t s);
 
 }  // namespace sb

@@ -68,6 +68,10 @@ struct IgKParams {
   // fused epilogue: out = wrap(max(acc + vec[k], lo))
   int epi, epi_vec, epi_lo, epi_res, vec_kind;
   int fast_clamp;  // |acc| + 128 < 2^31: clamp decided by an int32 compare against lo - vec[k]
+  // i8 TMA-store epilogue in int32 arithmetic: out = wrap8(max(acc + res + vec[k], lo)); exact when
+  // there is no clamp (wrapped low bits) or every |vec[k]| <= bias_bound (no int32 overflow)
+  int fast8;
+  long long bias_bound;
   const void* vec;
   long long vec_k;
   long long lo;
@@ -176,6 +180,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
     }
     mbar_init(&rfull[0], 1);
     mbar_init(&rfull[1], 1);
+    *reinterpret_cast<int*>(bars + 41) = 0;  // some |vec[k]| > bias_bound
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -290,47 +295,63 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       const int u0 = p.sx * ox, v0 = p.sy * oy;
       const std::int8_t* pix = p.g_in + p.g_a0 + p.g_an * img + p.g_ax * u0 + p.g_ay * v0;
       for (int kb = 0; kb < p.kblocks; kb++) {
-        mbar_wait(&empty[stage], phase ^ 1);
         std::uint8_t* rowp = ring + stage * (stage_a + stage_b) + r * p.bk;
         if (p.g_run) {
           // run layout: tap row i's S*C input bytes are contiguous (a_y == C); copy them with
-          // aligned word loads + funnel shifts, zeroing bytes whose column j is skipped
+          // aligned word loads + funnel shifts, zeroing bytes whose column j is skipped.
+          // Both of this thread's runs issue their loads before the stage wait, so one L2
+          // round trip per k-block overlaps the ring back-pressure.
           const int RUN = p.g_run;
           const int jlo = max(0, p.g_vlo - v0), jhi = min(p.g_S - 1, p.g_vhi - v0);
           const int d0 = jlo * p.g_C, dlen = (jhi - jlo + 1) * p.g_C;
-          for (int ri = half; ri < p.bk / RUN; ri += 2) {
-            const int i = kb * (p.bk / RUN) + ri;
-            const int u = u0 + i;
-            const bool ok = live && i < p.g_R && u >= p.g_ulo && u <= p.g_uhi && dlen > 0;
-            const long long src = static_cast<long long>(reinterpret_cast<std::uintptr_t>(pix)) + p.g_ax * i;
-            const long long first_w = (src + d0) >> 2, last_w = (src + d0 + dlen - 1) >> 2;
-            const long long A0 = src >> 2;
-            const int sh = static_cast<int>(src & 3) * 8;
-            // all loads of the run first (independent, in flight together), then the shifts;
-            // words e in [e_lo, e_hi] hold valid bytes (the others are never dereferenced)
-            const int e_lo = ok ? static_cast<int>(first_w - A0) : 1 << 20;
-            const int e_hi = ok ? min(static_cast<int>(last_w - A0), RUN / 4) : -1;
-            const std::uint32_t* wp = reinterpret_cast<const std::uint32_t*>(A0 << 2);
-            std::uint32_t wd[17];
+          const int nruns = p.bk / RUN;
+          for (int rb = half; rb < nruns; rb += 4) {
+            std::uint32_t wd[2][17];
+            int sh[2];
 #pragma unroll
-            for (int e = 0; e < 17; e++) wd[e] = (e >= e_lo && e <= e_hi) ? __ldg(wp + e) : 0u;
+            for (int z = 0; z < 2; z++) {
+              const int ri = rb + 2 * z;
+              const int i = kb * nruns + ri;
+              const int u = u0 + i;
+              const bool ok = ri < nruns && live && i < p.g_R && u >= p.g_ulo && u <= p.g_uhi && dlen > 0;
+              const long long src = static_cast<long long>(reinterpret_cast<std::uintptr_t>(pix)) + p.g_ax * i;
+              const long long first_w = (src + d0) >> 2, last_w = (src + d0 + dlen - 1) >> 2;
+              const long long A0 = src >> 2;
+              sh[z] = static_cast<int>(src & 3) * 8;
+              // words e in [e_lo, e_hi] hold valid bytes (the others are never dereferenced)
+              const int e_lo = ok ? static_cast<int>(first_w - A0) : 1 << 20;
+              const int e_hi = ok ? min(static_cast<int>(last_w - A0), RUN / 4) : -1;
+              const std::uint32_t* wp = reinterpret_cast<const std::uint32_t*>(A0 << 2);
+#pragma unroll
+              for (int e = 0; e < 17; e++) wd[z][e] = (e >= e_lo && e <= e_hi) ? __ldg(wp + e) : 0u;
+            }
+            if (rb == half) mbar_wait(&empty[stage], phase ^ 1);  // stage free before the first store
             auto below = [](int x) -> std::uint32_t { return x <= 0 ? 0u : x >= 4 ? ~0u : ((1u << (8 * x)) - 1u); };
 #pragma unroll
-            for (int ch = 0; ch < 4; ch++) {
-              if (ch >= RUN / 16) break;
-              std::uint32_t w[4];
+            for (int z = 0; z < 2; z++) {
+              const int ri = rb + 2 * z;
+              if (ri >= nruns) break;
 #pragma unroll
-              for (int e = 0; e < 4; e++) {
-                const int ow = ch * 4 + e;
-                const std::uint32_t v = __funnelshift_r(wd[ow], wd[ow + 1], sh);
-                const int lb = d0 - 4 * ow, hb = d0 + dlen - 4 * ow;
-                w[e] = v & below(hb) & ~below(lb);
+              for (int ch = 0; ch < 4; ch++) {
+                if (ch >= RUN / 16) break;
+                std::uint32_t w[4];
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                  const int ow = ch * 4 + e;
+                  const std::uint32_t v = __funnelshift_r(wd[z][ow], wd[z][ow + 1], sh[z]);
+                  const int lb = d0 - 4 * ow, hb = d0 + dlen - 4 * ow;
+                  w[e] = v & below(hb) & ~below(lb);
+                }
+                const int q = (ri * RUN) / 16 + ch;
+                *reinterpret_cast<uint4*>(rowp + ((q ^ sw) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
               }
-              const int q = (ri * RUN) / 16 + ch;
-              *reinterpret_cast<uint4*>(rowp + ((q ^ sw) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
             }
           }
-        } else
+          if (half >= nruns) mbar_wait(&empty[stage], phase ^ 1);
+        } else {
+          mbar_wait(&empty[stage], phase ^ 1);
+        }
+        if (!p.g_run)
         for (int q = half; q < p.bk / 16; q += 2) {
           std::uint32_t w[4];
 #pragma unroll
@@ -378,14 +399,19 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
                                : p.vec_kind == kI16 ? static_cast<const std::int16_t*>(p.vec)[vi]
                                                     : static_cast<const std::int32_t*>(p.vec)[vi];
         vec_s[k] = b;
+        if (p.fast8 && p.epi_lo && (b > p.bias_bound || b < -p.bias_bound)) atomicOr(reinterpret_cast<int*>(bars + 41), 1);
         if (p.fast_clamp) {
           const long long t = p.lo - b;
           thr_s[k] = static_cast<std::int32_t>(t < INT_MIN ? INT_MIN : t > INT_MAX ? INT_MAX : t);
         }
       }
     }
+    if (p.epi_vec)  // zero tail: chunk loads past N need no bounds select
+      for (int k = p.N + threadIdx.x - 64; k < (p.N + BN - 1) / BN * BN && k < kMaxVecK; k += ethreads) vec_s[k] = 0;
     if (p.epi_res && leader && p.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("bar.sync 1, %0;" ::"r"(ethreads) : "memory");
+    const bool fast8 = p.fast8 && !(p.epi_lo && *reinterpret_cast<volatile int*>(bars + 41));
+    const std::int32_t lo8 = p.epi_lo ? static_cast<std::int32_t>(p.lo) : INT_MIN;
     const long long lo = p.epi_lo ? p.lo : LLONG_MIN;
     const bool relu0 = p.epi_lo && p.lo == 0;
     // residual tile [128 pixels x 128 channels] i8 of tile t into buffer b
@@ -416,13 +442,59 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       std::uint8_t* rcur = rstg + (iter & 1) * kResBytes;
       std::uint8_t* scur = p.tma_out == 2 ? stg + (iter & 1) * 16384 : stg;
       const int m = m0 + row;
-      for (int h = h_lo; h < h_hi; h++) {
-        if (n0 + h * 32 >= p.N) break;  // columns past N: nothing to store (warp-uniform)
+      // this warp's 32-column chunks: the valid chunks of the tile split between the column groups
+      const int nch = min(BN, p.N - n0 + 31) / 32;
+      const int c_lo = hgroups == 1 ? 0 : hgroup * nch / hgroups, c_hi = hgroups == 1 ? nch : (hgroup + 1) * nch / hgroups;
+      (void)h_lo;
+      (void)h_hi;
+      for (int h = c_lo; h < c_hi; h++) {
         std::uint32_t v[32];
         tmem_ld32(tmem_base + (static_cast<std::uint32_t>(quarter * 32) << 16) +
                       static_cast<std::uint32_t>(acc * BN + h * 32),
                   v);
         const int kbase = n0 + h * 32;
+        if (fast8) {
+          // out = wrap8(max(acc + res + vec, lo)) in int32 (exact: see IgKParams::fast8)
+          std::int32_t bv[32];
+#pragma unroll
+          for (int q = 0; q < 8; q++) {
+            if (p.epi_vec)
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(bv[4 * q]), "=r"(bv[4 * q + 1]), "=r"(bv[4 * q + 2]), "=r"(bv[4 * q + 3])
+                           : "r"(smem_u32(vec_s + kbase + 4 * q)));
+            else
+              bv[4 * q] = bv[4 * q + 1] = bv[4 * q + 2] = bv[4 * q + 3] = 0;
+          }
+          std::uint32_t w[8];
+          if (p.epi_res) {
+            std::uint32_t rw[8];
+            const std::uint32_t rrow = smem_u32(rcur + row * 128);
+#pragma unroll
+            for (int u = 0; u < 2; u++)
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(rw[4 * u]), "=r"(rw[4 * u + 1]), "=r"(rw[4 * u + 2]), "=r"(rw[4 * u + 3])
+                           : "r"(rrow + (((2 * h + u) ^ sw) << 4)));
+#pragma unroll
+            for (int q = 0; q < 32; q++) {
+              const std::int32_t r = static_cast<std::int32_t>(rw[q >> 2] << (24 - 8 * (q & 3))) >> 24;
+              v[q] = static_cast<std::uint32_t>(max(static_cast<std::int32_t>(v[q]) + r + bv[q], lo8));
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 32; q++)
+              v[q] = static_cast<std::uint32_t>(max(static_cast<std::int32_t>(v[q]) + bv[q], lo8));
+          }
+#pragma unroll
+          for (int q = 0; q < 8; q++)
+            w[q] = __byte_perm(__byte_perm(v[4 * q], v[4 * q + 1], 0x0040), __byte_perm(v[4 * q + 2], v[4 * q + 3], 0x0040),
+                               0x5410);
+          const std::uint32_t rbase = smem_u32(scur + row * 128);
+#pragma unroll
+          for (int u = 0; u < 2; u++)
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rbase + (((2 * h + u) ^ sw) << 4)),
+                         "r"(w[4 * u]), "r"(w[4 * u + 1]), "r"(w[4 * u + 2]), "r"(w[4 * u + 3]));
+          continue;
+        }
         if (p.epi) {
           // exact s32 accumulator + vector + residual in int64 (the reference's temps),
           // clamped, wrapped by the store
@@ -696,6 +768,13 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     else kp.tma_out = 0;
   }
   {
+    const long long taps = cp.packed ? cp.R * cp.S * cp.C : gp.R * gp.S * gp.C;
+    const long long T = taps * 128 * 128 + 128;  // bound on |acc + res|
+    const bool lo_ok = !cp.epi_lo || (cp.lo >= INT_MIN && cp.lo <= INT_MAX && T < INT_MAX);
+    kp.fast8 = kp.tma_out == 2 && cp.K <= kMaxVecK && lo_ok ? 1 : 0;
+    kp.bias_bound = T < INT_MAX ? INT_MAX - T : 0;
+  }
+  {
     // dynamic smem: A/B ring (up to 128 KB) | output staging | residual tiles | vector | barriers
     const int stg = kp.tma_out == 1 ? kStgBytes : kp.tma_out == 2 ? 2 * 16384 : 0;
     const int res = kp.epi_res ? 2 * kResBytes : 0;
@@ -728,8 +807,8 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
                         static_cast<cuuint64_t>(cp.N)};
   cuuint64_t astr[3] = {static_cast<cuuint64_t>(cp.a_y), static_cast<cuuint64_t>(cp.a_x),
                         static_cast<cuuint64_t>(cp.a_n)};
-  int lower[2] = {g.lower_h, g.lower_w};  // {H, W}
-  int upper[2] = {g.upper_h, g.upper_w};
+  int lower[2] = {g.lower_w, g.lower_h};  // innermost first: {W, H}
+  int upper[2] = {g.upper_w, g.upper_h};
   cuuint32_t aes[4] = {1, static_cast<cuuint32_t>(cp.sy), static_cast<cuuint32_t>(cp.sx), 1};
   if (enc_im2col(&out->amap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<std::int8_t*>(abase), adim, astr, lower,
                  upper, static_cast<cuuint32_t>(g.bk), BM, aes, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
@@ -847,9 +926,81 @@ __global__ void conv_pack_filter_kernel(const std::int8_t* __restrict__ b, std::
   }
 }
 
+// Phase fold: F[n, U, V, kf] = I[n, fx*U + di, fy*V + dj, c] for kf = (di*fy + dj)*C + c
+// (zero outside the constraint window and for kf >= fx*fy*C).  One thread per folded pixel
+// and 4-byte word; the window test is per byte.
+__global__ void __launch_bounds__(256) conv_fold_kernel(const std::int8_t* __restrict__ a, std::uint32_t* __restrict__ f,
+                                                        long long words, int FU, int FV, int FW, int fx, int fy, int C,
+                                                        long long a_n, long long a_x, long long a_y, long long a0,
+                                                        int u_lo, int u_hi, int v_lo, int v_hi) {
+  const int fyc = fy * C, fxyc = fx * fyc;
+  for (long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; g < words;
+       g += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long pix = g / FW;
+    const int w = static_cast<int>(g - pix * FW);
+    const long long nu = pix / FV;
+    const int V = static_cast<int>(pix - nu * FV);
+    const long long n = nu / FU;
+    const int U = static_cast<int>(nu - n * FU);
+    std::uint32_t word = 0;
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      const int kf = 4 * w + e;
+      if (kf < fxyc) {
+        const int di = kf / fyc, r = kf - di * fyc, dj = r / C, c = r - dj * C;
+        const int u = fx * U + di, v = fy * V + dj;
+        if (u >= u_lo && u <= u_hi && v >= v_lo && v <= v_hi)
+          word |= static_cast<std::uint32_t>(static_cast<std::uint8_t>(__ldg(a + a0 + a_n * n + a_x * u + a_y * v + c)))
+                  << (8 * e);
+      }
+    }
+    f[g] = word;
+  }
+}
+
+// Folded filter: G[a, k, q], q = b*fold_c + kf -> F[fx*a + di, fy*b + dj, k, c] (zero when the
+// tap is past R/S or kf is padding)
+__global__ void conv_fold_filter_kernel(const std::int8_t* __restrict__ b, std::int8_t* __restrict__ pb, int K, int C,
+                                        int R, int S, int fx, int fy, int fc, int cv, int fr, long long b_i,
+                                        long long b_j, long long b_k, long long b_c, long long b0) {
+  const int total = fr * K * cv, fyc = fy * C;
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
+    const int q = g % cv, ak = g / cv, k = ak % K, ta = ak / K;
+    const int tb = q / fc, kf = q - tb * fc;
+    std::int8_t val = 0;
+    if (kf < fx * fyc) {
+      const int di = kf / fyc, r = kf - di * fyc, dj = r / C, c = r - dj * C;
+      const int i = fx * ta + di, j = fy * tb + dj;
+      if (i < R && j < S) val = b[b0 + b_i * i + b_j * j + b_k * k + b_c * c];
+    }
+    pb[g] = val;
+  }
+}
+
 }  // namespace
 
+cudaError_t launch_conv_fold(const ConvPlan& cp, const void* a, void* f, cudaStream_t s) {
+  const int FW = static_cast<int>(cp.fold_c / 4);
+  const long long words = cp.N * cp.fold_u * cp.fold_v * FW;
+  const long long blocks = std::min<long long>((words + 255) / 256, 148 * 16);
+  conv_fold_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(
+      static_cast<const std::int8_t*>(a), static_cast<std::uint32_t*>(f), words, static_cast<int>(cp.fold_u),
+      static_cast<int>(cp.fold_v), FW, static_cast<int>(cp.fold_x), static_cast<int>(cp.fold_y),
+      static_cast<int>(cp.C), cp.a_n, cp.a_x, cp.a_y, cp.a0, static_cast<int>(cp.u_lo), static_cast<int>(cp.u_hi),
+      static_cast<int>(cp.v_lo), static_cast<int>(cp.v_hi));
+  return cudaGetLastError();
+}
+
 cudaError_t launch_conv_pack_filter(const ConvPlan& cp, const void* b, void* pb, cudaStream_t s) {
+  if (cp.fold_x) {
+    const int total = static_cast<int>(cp.fold_r * cp.K * cp.fold_cv);
+    conv_fold_filter_kernel<<<std::min(1024, (total + 255) / 256), 256, 0, s>>>(
+        static_cast<const std::int8_t*>(b), static_cast<std::int8_t*>(pb), static_cast<int>(cp.K),
+        static_cast<int>(cp.C), static_cast<int>(cp.R), static_cast<int>(cp.S), static_cast<int>(cp.fold_x),
+        static_cast<int>(cp.fold_y), static_cast<int>(cp.fold_c), static_cast<int>(cp.fold_cv),
+        static_cast<int>(cp.fold_r), cp.b_i, cp.b_j, cp.b_k, cp.b_c, cp.b0);
+    return cudaGetLastError();
+  }
   const int kp = static_cast<int>(cp.pack_k), rsc = static_cast<int>(cp.R * cp.S * cp.C);
   const int fb = static_cast<int>(std::min<long long>((cp.K * kp + 255) / 256, 1024));
   (void)rsc;
@@ -880,6 +1031,14 @@ cudaError_t launch_conv_pack(const ConvPlan& cp, const void* a, const void* b, v
 }
 
 const char* conv_igemm_unsupported(const ConvPlan& cp) {
+  if (cp.packed && cp.fold_x) {
+    if (cp.fold_x != cp.sx || cp.fold_y != cp.sy || cp.fold_c % 16 || cp.fold_cv % 64 ||
+        cp.fold_x * cp.fold_y * cp.C > cp.fold_c || cp.fold_s * cp.fold_c > cp.fold_cv ||
+        cp.fold_u < cp.H + cp.fold_r - 1 || (cp.fold_v - cp.W + 1) * cp.fold_c < cp.fold_cv)
+      return "inconsistent phase fold";
+    if (cp.N * cp.fold_u * cp.fold_v >= (1ll << 31)) return "folded input too large";
+    return conv_igemm_unsupported(packed_view(cp));
+  }
   if (cp.packed) {
     // gather mode: the kernel builds A rows from the original input; the GEMM is packed_view
     if (cp.pack_run && (cp.a_y != cp.C || cp.S * cp.C > cp.pack_run || (cp.pack_run != 16 && cp.pack_run != 32 &&

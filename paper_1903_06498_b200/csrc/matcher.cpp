@@ -772,6 +772,30 @@ ConvPlan packed_view(const ConvPlan& c) {
   v.packed = false;
   v.a_buf = c.pack_a;
   v.b_buf = c.pack_b;
+  if (c.fold_x) {
+    // out[x, y] = sum_{a, q} Fold[x + a, y, q] * G[a, k, q] where "pixel" (U, y) of the view is
+    // the fold_cv bytes starting at folded pixel (U, y): rows overlap (pixel stride fold_c)
+    v.C = c.fold_cv;
+    v.R = c.fold_r;
+    v.S = 1;
+    v.sx = v.sy = 1;
+    v.a_y = c.fold_c;
+    v.a_x = c.fold_v * c.fold_c;
+    v.a_n = c.fold_u * c.fold_v * c.fold_c;
+    v.a0 = 0;
+    v.u_lo = 0;
+    v.u_hi = c.fold_u - 1;
+    v.v_lo = 0;
+    v.v_hi = c.W - 1;
+    v.b_i = c.K * c.fold_cv;
+    v.b_j = 0;
+    v.b_k = c.fold_cv;
+    v.b_c = 1;
+    v.b0 = 0;
+    v.b_immutable = false;
+    v.fold_x = v.fold_y = 0;
+    return v;
+  }
   v.C = c.pack_k;
   v.R = v.S = 1;
   v.sx = v.sy = 1;
@@ -798,6 +822,40 @@ bool try_packed_conv(Plan* plan, ConvPlan* cp) {
   const std::int64_t rsc = cp->R * cp->S * cp->C;
   // 1x1 contractions with few channels are plain GEMMs (gemm_tc takes ragged K directly)
   if (rsc > 1024 || cp->C % 64 == 0 || cp->R * cp->S == 1) return false;
+  // Preferred: phase fold (a stride-1 conv over a folded copy of the input, A tiles by TMA
+  // im2col); the in-kernel gather below is the fallback.
+  if (!std::getenv("SB_NO_FOLD")) {
+    ConvPlan c = *cp;
+    c.packed = true;
+    c.fold_x = c.sx;
+    c.fold_y = c.sy;
+    c.fold_c = (c.sx * c.sy * c.C + 15) / 16 * 16;
+    c.fold_r = (c.R + c.sx - 1) / c.sx;
+    c.fold_s = (c.S + c.sy - 1) / c.sy;
+    c.fold_cv = (c.fold_s * c.fold_c + 63) / 64 * 64;
+    c.fold_u = c.H + c.fold_r - 1;
+    c.fold_v = c.W + (c.fold_cv + c.fold_c - 1) / c.fold_c - 1;
+    c.pack_k = c.fold_r * c.fold_cv;
+    c.pack_a = static_cast<int>(plan->bufs.size());
+    c.pack_b = c.pack_a + 1;
+    const std::int64_t folded = c.N * c.fold_u * c.fold_v * c.fold_c;
+    if (c.pack_k <= 1024 && folded < (1ll << 34) && !conv_igemm_unsupported(c)) {
+      PBuffer f;
+      f.name = "fold:" + plan->bufs[c.a_buf].name;
+      f.dtype = DType::I8;
+      f.kind = kI8;
+      f.elements = folded;
+      plan->bufs.push_back(f);
+      PBuffer b;
+      b.name = "pack:" + plan->bufs[c.b_buf].name;
+      b.dtype = DType::I8;
+      b.kind = kI8;
+      b.elements = c.K * c.pack_k;
+      plan->bufs.push_back(b);
+      *cp = c;
+      return true;
+    }
+  }
   ConvPlan c = *cp;
   c.packed = true;
   // run layout when each tap row's S*C bytes are contiguous in the input (dense pixels)
@@ -941,8 +999,14 @@ void match_kernels(Plan* plan, const Program& p, const PlanOptions& opt) {
         st.launch.conv = cp;
         if (cp.fresh_output) st.launch.fused_fill_root = plan->bufs[cp.c_buf].root_index;
         if (!fuse_conv_epilogue(plan, s, p, opt)) fresh_scratch_output(plan, s);
-        plan->notes.push_back("launch " + st.launch.path + ": small-channel conv packed to " +
-                              std::to_string(cp.pack_k) + " taps x channels per pixel");
+        if (cp.fold_x)
+          plan->notes.push_back("launch " + st.launch.path + ": small-channel conv phase-folded (" +
+                                std::to_string(cp.fold_x) + "x" + std::to_string(cp.fold_y) + ", " +
+                                std::to_string(cp.fold_c) + " bytes per folded pixel), packed to " +
+                                std::to_string(cp.fold_r) + " tap rows x " + std::to_string(cp.fold_cv));
+        else
+          plan->notes.push_back("launch " + st.launch.path + ": small-channel conv packed to " +
+                                std::to_string(cp.pack_k) + " taps x channels per pixel (gathered)");
         continue;
       }
       why = std::string(bad_tc) + "; " + bad_ig;

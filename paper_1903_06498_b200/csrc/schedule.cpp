@@ -39,7 +39,10 @@ void step_access(const PStep& s, std::vector<int>* reads, std::vector<int>* writ
       if (l.conv.epi_res) R(l.conv.res_buf);
       if (!l.conv.fresh_output) R(l.conv.c_buf);
       W(l.conv.c_buf);
-      if (l.conv.packed) W(l.conv.pack_b);
+      if (l.conv.packed) {
+        W(l.conv.pack_a);
+        W(l.conv.pack_b);
+      }
       return;
     case KernelKind::GemmI8TC:
     case KernelKind::GemmF32:

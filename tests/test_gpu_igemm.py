@@ -52,6 +52,8 @@ CONVS = [
     (3, 9, 11, 64, 320, 3, 3, 1, 1),      # ragged tiles, K not a multiple of 128
     (1, 32, 32, 64, 64, 7, 7, 2, 3),      # 7x7/2 (stem shape with 64 channels)
     (2, 15, 13, 128, 64, 3, 3, 2, 1),     # odd extents with stride 2
+    (2, 16, 15, 64, 64, 3, 3, 2, 1),      # im2col corners differ in H and W (upper -2 vs -1)
+    (1, 6, 17, 64, 128, 1, 3, 2, 0),      # 1x3 filter, no padding, wide rows
 ]
 
 
@@ -139,16 +141,27 @@ def test_fused_small_pinned_against_port():
 
 
 SMALL_C = [
-    # N, H, W, C, K, R, S, stride, pad  (gather mode: taps x channels packed per pixel in smem)
+    # N, H, W, C, K, R, S, stride, pad  (phase fold, or gather mode: taps x channels per pixel in smem)
     (2, 32, 32, 3, 64, 7, 7, 2, 3),       # ResNet stem shape
     (1, 9, 13, 16, 96, 3, 3, 1, 1),
     (2, 10, 10, 24, 128, 5, 5, 2, 2),
     (1, 8, 8, 3, 200, 3, 3, 1, 0),        # no padding, K > 128
+    (2, 13, 18, 3, 64, 7, 7, 2, 3),       # odd/even extents under the 2x2 fold
+    (1, 11, 9, 5, 32, 3, 5, 3, 1),        # stride 3 fold (45 bytes per folded pixel)
 ]
 
 
+@pytest.fixture(params=["fold", "gather"])
+def small_c_mode(request, monkeypatch):
+    if request.param == "gather":
+        monkeypatch.setenv("SB_NO_FOLD", "1")
+    else:
+        monkeypatch.delenv("SB_NO_FOLD", raising=False)
+    return request.param
+
+
 @pytest.mark.parametrize("shape", SMALL_C, ids=lambda s: "x".join(map(str, s)))
-def test_gather_conv_exact(shape):
+def test_gather_conv_exact(shape, small_c_mode):
     import paper_1903_06498_b200 as sb
     from paper_1903_06498_b200 import workloads as W
     from intmodel import conv_exact, wrap
@@ -156,12 +169,16 @@ def test_gather_conv_exact(shape):
     text = W.conv2d(N, H, Wd, C, K, R, S, pad=pad, stride=st)
     plan = sb.parse_program(text).describe_plan()
     assert "packed" in plan, plan
+    if small_c_mode == "fold":
+        assert "phase-folded" in plan, plan
+    elif "phase-folded" in plan:
+        pytest.fail(plan)
     prog, inp, out = run(text, seed=sum(shape))
     exp = wrap(32, conv_exact(inp["I"].reshape(N, H, Wd, C), inp["F"].reshape(R, S, K, C), st, pad, "cuda"))
     np.testing.assert_array_equal(out["O"], exp.cpu().numpy().ravel())
 
 
-def test_gather_stem_fused_vs_port():
+def test_gather_stem_fused_vs_port(small_c_mode):
     from paper_1903_06498_b200 import workloads as W
     text = W.conv_fused(1, 12, 12, 3, 64, 7, 7, 2, 3)
     prog, inp, out = run(text, seed=21)

@@ -18,6 +18,8 @@ def main():
     batch = int(sys.argv[2]) if len(sys.argv) > 2 else 128
     if which == "c5":
         text, info = W.resnet50(batch)
+    elif which == "stem":
+        text = W.conv_fused(batch, 224, 224, 3, 64, 7, 7, 2, 3)
     elif which == "c2":
         text = W.conv2d(32, 56, 56, 64, 64)
     else:
