@@ -26,6 +26,7 @@
 #include <climits>
 #include <cstdint>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -56,6 +57,7 @@ struct IgKParams {
   // gather mode (ConvPlan::packed): A rows built by warps 6-9 from the original input
   int gather, tab_off, rsc, g_C, g_S, g_R, g_run;
   int epi_warps;  // 4 or 8 (two warps per TMEM lane quarter, each taking half the columns)
+  int epi_split;  // 8 epilogue warps as two independent groups of 4 taking alternate tiles
   int pdl_wait;   // griddepcontrol.wait before touching buffers (else independent of in-flight work)
   long long g_an, g_ax, g_ay, g_a0;
   int g_ulo, g_uhi, g_vlo, g_vhi;
@@ -171,12 +173,12 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; s++) {
-      mbar_init(&full[s], p.gather ? 257 : 1);  // TMA transaction (+ 256 gathering threads)
+      mbar_init(&full[s], p.gather ? 257 : 2);  // A and B transactions (B + 256 gathering threads)
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; a++) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 32 * p.epi_warps);
+      mbar_init(&tempty[a], p.epi_split ? 128 : 32 * p.epi_warps);
     }
     mbar_init(&rfull[0], 1);
     mbar_init(&rfull[1], 1);
@@ -194,11 +196,19 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
   const std::uint32_t tmem_base = *tmem_slot;
   if (p.pdl && threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
-  if (warp == 0) {
+  // TMA producers.  One thread issues a tensor load only every ~260 cycles whatever the box
+  // size (measured, scratch/tma_lat.cu), so im2col mode splits the issue over four warps:
+  // A and B loads on separate threads, alternate k-blocks on two chains.  Gather mode has
+  // one producer (B only; the A rows are built by the gather warps).
+  const int pw0 = 2 + p.epi_warps + (p.gather ? 8 : 0);  // extra producer warps pw0 .. pw0 + 2
+  const int pidx = warp == 0 ? 0 : (!p.gather && warp >= pw0) ? warp - pw0 + 1 : -1;
+  if (pidx >= 0) {
     if (lane == 0) {
       if (p.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
+      const bool do_a = !p.gather && (pidx & 1) == 0, do_b = p.gather || (pidx & 1) == 1;
+      const int nchains = p.gather ? 1 : 2, chain = p.gather ? 0 : pidx >> 1;
       const int PQ = p.P * p.Q;
-      int stage = 0;
+      int stage = 0, kit = 0;
       std::uint32_t phase = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
         // n-tiles of one m-tile are adjacent in t: the A strip stays hot in L2
@@ -206,23 +216,28 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
         const int img = m0 / PQ, rem = m0 - img * PQ;
         const int ox = rem / p.Q, oy = rem - ox * p.Q;
         const int h0 = p.lower_h + ox * p.sx, w0 = p.lower_w + oy * p.sy;
-        int cb = 0, tap = 0;
-        for (int kb = 0; kb < p.kblocks; kb++) {
-          const int r = tap / p.S, s = tap - r * p.S;
-          mbar_wait(&empty[stage], phase ^ 1);
-          const std::uint32_t sa = smem_u32(ring + stage * (stage_a + stage_b));
-          if (p.gather) {
-            mbar_expect_tx(&full[stage], stage_b);
-            tma_load_4d(sa + stage_a, &bmap, &full[stage], kb * p.bk, n0, 0, 0);
-          } else {
-            mbar_expect_tx(&full[stage], stage_a + stage_b);
-            tma_load_im2col(sa, &amap, &full[stage], cb * p.bk, w0, h0, img, static_cast<std::uint16_t>(s),
-                            static_cast<std::uint16_t>(r));
-            tma_load_4d(sa + stage_a, &bmap, &full[stage], cb * p.bk, n0, s, r);
+        int cb = 0, r = 0, s = 0;
+        for (int kb = 0; kb < p.kblocks; kb++, kit++) {
+          if (kit % nchains == chain) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            const std::uint32_t sa = smem_u32(ring + stage * (stage_a + stage_b));
+            if (do_a) {
+              mbar_expect_tx(&full[stage], stage_a);
+              tma_load_im2col(sa, &amap, &full[stage], cb * p.bk, w0, h0, img, static_cast<std::uint16_t>(s),
+                              static_cast<std::uint16_t>(r));
+            }
+            if (do_b) {
+              mbar_expect_tx(&full[stage], stage_b);
+              if (p.gather) tma_load_4d(sa + stage_a, &bmap, &full[stage], kb * p.bk, n0, 0, 0);
+              else tma_load_4d(sa + stage_a, &bmap, &full[stage], cb * p.bk, n0, s, r);
+            }
           }
           if (++cb == p.cblocks) {
             cb = 0;
-            tap++;
+            if (++s == p.S) {
+              s = 0;
+              r++;
+            }
           }
           if (++stage == stages) {
             stage = 0;
@@ -261,7 +276,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
         umma_commit(&tfull[acc]);
       }
     }
-  } else if (warp >= 2 + p.epi_warps) {
+  } else if (p.gather && warp >= 2 + p.epi_warps) {
     // gather producers: row r of every A stage = the packed (i, j, c) taps of pixel m0 + r,
     // zero where a constraint skips the tap; written in the TMA swizzle layout
     const int gt = threadIdx.x - 64 - 32 * p.epi_warps;  // 0..255: row r = gt / 2, half = gt % 2
@@ -385,7 +400,13 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
     const int hgroups = p.epi_warps / 4, hgroup = (warp - 2) / 4;  // column halves when 8 warps
     const int h_lo = hgroup * (BN / 32) / hgroups, h_hi = (hgroup + 1) * (BN / 32) / hgroups;
     const int sw = row & 7;  // 128B swizzle phase of this staging row
-    const bool leader = threadIdx.x == 64;
+    // split: group g = hgroup owns TMEM accumulator g, staging/residual buffer g and tiles
+    // blockIdx.x + g*grid, + 2*grid, ... (its own barrier and store leader), so the two
+    // groups' per-tile chains (TMEM wait, math, barrier, TMA store) overlap
+    const bool split = p.epi_split != 0;
+    const int gthreads = split ? 128 : ethreads;
+    const int gbar = split && hgroup ? 3 : 1;
+    const bool leader = threadIdx.x == 64 + (split ? 128 * hgroup : 0);
     std::int32_t* thr_s = vec_s + kMaxVecK;
     if (p.epi_vec || p.fast_clamp) {
       // per-output-channel vector (e.g. the bias) as int32 in smem, read with ld.shared.v4; with
@@ -424,27 +445,32 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
           "l"(reinterpret_cast<std::uint64_t>(&rmap)), "r"(smem_u32(&rfull[b])), "r"(n0), "r"(m0)
           : "memory");
     };
-    if (p.epi_res && leader && static_cast<int>(blockIdx.x) < tiles) load_res(blockIdx.x, 0);
-    int iter = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, iter++) {
+    const int g0 = split ? hgroup : 0, tstep = split ? 2 * static_cast<int>(gridDim.x) : static_cast<int>(gridDim.x);
+    if (p.epi_res && leader && static_cast<int>(blockIdx.x) + g0 * static_cast<int>(gridDim.x) < tiles)
+      load_res(blockIdx.x + g0 * gridDim.x, g0);
+    int iter = g0;
+    for (int t = blockIdx.x + g0 * gridDim.x; t < tiles; t += tstep, iter += split ? 2 : 1) {
       const int acc = iter & 1;
       const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * BN;
       if (p.tma_out || p.epi_res) {
-        // i32 staging is single-buffered, i8 staging double-buffered
-        if (leader && p.tma_out == 1) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        if (leader && p.tma_out == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-        asm volatile("bar.sync 1, %0;" ::"r"(ethreads) : "memory");  // staging and the older residual buffer are free
+        // i32 staging is single-buffered, i8 staging double-buffered (one buffer per group when split)
+        if (leader && (p.tma_out == 1 || (split && p.tma_out == 2)))
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        if (leader && !split && p.tma_out == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        asm volatile("bar.sync %0, %1;" ::"r"(gbar), "r"(gthreads) : "memory");  // staging and the older residual buffer are free
       }
-      if (p.epi_res && leader && t + static_cast<int>(gridDim.x) < tiles) load_res(t + gridDim.x, (iter + 1) & 1);
+      if (!split && p.epi_res && leader && t + static_cast<int>(gridDim.x) < tiles) load_res(t + gridDim.x, (iter + 1) & 1);
       mbar_wait(&tfull[acc], (iter >> 1) & 1);
       tc_fence_after();
       if (p.epi_res) mbar_wait(&rfull[iter & 1], (iter >> 1) & 1);
       std::uint8_t* rcur = rstg + (iter & 1) * kResBytes;
       std::uint8_t* scur = p.tma_out == 2 ? stg + (iter & 1) * 16384 : stg;
       const int m = m0 + row;
-      // this warp's 32-column chunks: the valid chunks of the tile split between the column groups
+      // this warp's 32-column chunks: all valid chunks (split), else the valid chunks of the
+      // tile divided between the two column groups
       const int nch = min(BN, p.N - n0 + 31) / 32;
-      const int c_lo = hgroups == 1 ? 0 : hgroup * nch / hgroups, c_hi = hgroups == 1 ? nch : (hgroup + 1) * nch / hgroups;
+      const int c_lo = split || hgroups == 1 ? 0 : (hgroup * nch) >> 1;
+      const int c_hi = split || hgroups == 1 ? nch : ((hgroup + 1) * nch) >> 1;
       (void)h_lo;
       (void)h_hi;
       for (int h = c_lo; h < c_hi; h++) {
@@ -610,9 +636,13 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
-      if (p.tma_out) {
+      if (p.tma_out || split) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("bar.sync 1, %0;" ::"r"(ethreads) : "memory");
+        asm volatile("bar.sync %0, %1;" ::"r"(gbar), "r"(gthreads) : "memory");
+        // split: the group's residual buffer is free again -> prefetch its next tile's
+        if (split && p.epi_res && leader && t + tstep < tiles) load_res(t + tstep, g0);
+      }
+      if (p.tma_out) {
         if (leader) {
           if (p.tma_out == 1) {
             for (int h = 0; h < BN / 32; h++)
@@ -772,6 +802,7 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     const long long T = taps * 128 * 128 + 128;  // bound on |acc + res|
     const bool lo_ok = !cp.epi_lo || (cp.lo >= INT_MIN && cp.lo <= INT_MAX && T < INT_MAX);
     kp.fast8 = kp.tma_out == 2 && cp.K <= kMaxVecK && lo_ok ? 1 : 0;
+    kp.epi_split = kp.epi_warps == 8 && kp.tma_out != 1 && !std::getenv("SB_IG_NOSPLIT") ? 1 : 0;
     kp.bias_bound = T < INT_MAX ? INT_MAX - T : 0;
   }
   {
@@ -1091,7 +1122,7 @@ cudaError_t launch_conv_igemm(const ConvPlan& cp, const ConvArgs& args, cudaStre
   const int tiles = kp.tiles_m * kp.tiles_n;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(tiles < num_sms ? tiles : num_sms));
-  cfg.blockDim = dim3(64 + 32 * kp.epi_warps + (kp.gather ? 256 : 0));
+  cfg.blockDim = dim3(64 + 32 * kp.epi_warps + (kp.gather ? 256 : 96));
   cfg.dynamicSmemBytes = static_cast<unsigned>(kp.smem);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
