@@ -58,6 +58,8 @@ struct IgKParams {
   int gather, tab_off, rsc, g_C, g_S, g_R, g_run;
   int epi_warps;  // 4 or 8 (two warps per TMEM lane quarter, each taking half the columns)
   int epi_split;  // 8 epilogue warps as two independent groups of 4 taking alternate tiles
+  int b_res, bres_off;
+  int kpb;  // k-blocks per ring stage (one barrier handshake per stage: ~200 cycles each, measured)  // whole filter resident in smem (one n-tile, small reduction): the ring holds A only
   int pdl_wait;   // griddepcontrol.wait before touching buffers (else independent of in-flight work)
   long long g_an, g_ax, g_ay, g_a0;
   int g_ulo, g_uhi, g_vlo, g_vhi;
@@ -156,7 +158,9 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
   std::uint8_t* base =
       reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t{1023});
   const std::uint32_t stage_a = BM * p.bk, stage_b = BN * p.bk;
-  std::uint8_t* ring = base;                    // stages x (A | B)
+  std::uint8_t* ring = base;                    // stages x (A | B), or stages x A with the filter resident
+  const std::uint32_t sstride = p.kpb * (stage_a + (p.b_res ? 0u : stage_b));
+  std::uint8_t* bres = base + p.bres_off;       // resident filter: kblocks x stage_b
   std::uint8_t* stg = base + p.stg_off;         // output staging: i32 4 x 16 KB quarters | i8 2 x 16 KB
   std::uint8_t* rstg = base + p.res_off;        // residual tiles (i8, 2 x 16 KB)
   std::int32_t* vec_s = reinterpret_cast<std::int32_t*>(base + p.vec_off);  // per-channel vector (<= 2048)
@@ -166,6 +170,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
   std::uint64_t* tfull = bars + 32;
   std::uint64_t* tempty = bars + 34;
   std::uint64_t* rfull = bars + 36;  // [2]
+  std::uint64_t* bfull = bars + 38;  // resident filter landed
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 40);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int tiles = p.tiles_m * p.tiles_n;
@@ -173,7 +178,8 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; s++) {
-      mbar_init(&full[s], p.gather ? 257 : 2);  // A and B transactions (B + 256 gathering threads)
+      // A and B transactions (B + 256 gathering threads); no B arrival with the filter resident
+      mbar_init(&full[s], (p.gather ? 256 : 1) + (p.b_res ? 0 : 1));
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; a++) {
@@ -182,6 +188,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
     }
     mbar_init(&rfull[0], 1);
     mbar_init(&rfull[1], 1);
+    mbar_init(bfull, 1);
     *reinterpret_cast<int*>(bars + 41) = 0;  // some |vec[k]| > bias_bound
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -208,6 +215,25 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       const bool do_a = !p.gather && (pidx & 1) == 0, do_b = p.gather || (pidx & 1) == 1;
       const int nchains = p.gather ? 1 : 2, chain = p.gather ? 0 : pidx >> 1;
       const int PQ = p.P * p.Q;
+      if (do_b && p.b_res) {
+        // the whole filter once (tiles_n == 1), then this producer is done
+        if (chain == 0) {
+          mbar_expect_tx(bfull, p.kblocks * stage_b);
+          int cb = 0, r = 0, s = 0;
+          for (int kb = 0; kb < p.kblocks; kb++) {
+            const std::uint32_t dst = smem_u32(bres + kb * stage_b);
+            if (p.gather) tma_load_4d(dst, &bmap, bfull, kb * p.bk, 0, 0, 0);
+            else tma_load_4d(dst, &bmap, bfull, cb * p.bk, 0, s, r);
+            if (++cb == p.cblocks) {
+              cb = 0;
+              if (++s == p.S) {
+                s = 0;
+                r++;
+              }
+            }
+          }
+        }
+      } else {
       int stage = 0, kit = 0;
       std::uint32_t phase = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
@@ -217,26 +243,30 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
         const int ox = rem / p.Q, oy = rem - ox * p.Q;
         const int h0 = p.lower_h + ox * p.sx, w0 = p.lower_w + oy * p.sy;
         int cb = 0, r = 0, s = 0;
-        for (int kb = 0; kb < p.kblocks; kb++, kit++) {
-          if (kit % nchains == chain) {
+        for (int kb0 = 0; kb0 < p.kblocks; kb0 += p.kpb, kit++) {
+          const bool mine = kit % nchains == chain;
+          if (mine) {
             mbar_wait(&empty[stage], phase ^ 1);
-            const std::uint32_t sa = smem_u32(ring + stage * (stage_a + stage_b));
-            if (do_a) {
-              mbar_expect_tx(&full[stage], stage_a);
-              tma_load_im2col(sa, &amap, &full[stage], cb * p.bk, w0, h0, img, static_cast<std::uint16_t>(s),
-                              static_cast<std::uint16_t>(r));
-            }
-            if (do_b) {
-              mbar_expect_tx(&full[stage], stage_b);
-              if (p.gather) tma_load_4d(sa + stage_a, &bmap, &full[stage], kb * p.bk, n0, 0, 0);
-              else tma_load_4d(sa + stage_a, &bmap, &full[stage], cb * p.bk, n0, s, r);
-            }
+            if (do_a) mbar_expect_tx(&full[stage], p.kpb * stage_a);
+            if (do_b && !p.b_res) mbar_expect_tx(&full[stage], p.kpb * stage_b);
           }
-          if (++cb == p.cblocks) {
-            cb = 0;
-            if (++s == p.S) {
-              s = 0;
-              r++;
+          const std::uint32_t sa = smem_u32(ring + stage * sstride);
+          for (int j = 0; j < p.kpb; j++) {
+            const int kb = kb0 + j;
+            if (mine && do_a)
+              tma_load_im2col(sa + j * stage_a, &amap, &full[stage], cb * p.bk, w0, h0, img,
+                              static_cast<std::uint16_t>(s), static_cast<std::uint16_t>(r));
+            if (mine && do_b && !p.b_res) {
+              const std::uint32_t sb = sa + p.kpb * stage_a + j * stage_b;
+              if (p.gather) tma_load_4d(sb, &bmap, &full[stage], kb * p.bk, n0, 0, 0);
+              else tma_load_4d(sb, &bmap, &full[stage], cb * p.bk, n0, s, r);
+            }
+            if (++cb == p.cblocks) {
+              cb = 0;
+              if (++s == p.S) {
+                s = 0;
+                r++;
+              }
             }
           }
           if (++stage == stages) {
@@ -245,12 +275,17 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
           }
         }
       }
+      }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       int stage = 0, iter = 0;
       std::uint32_t phase = 0;
       const int ksteps = p.bk / 32;
+      if (p.b_res) {
+        mbar_wait(bfull, 0);
+        tc_fence_after();
+      }
       for (int t = blockIdx.x; t < tiles; t += gridDim.x, iter++) {
         const int acc = iter & 1;
         mbar_wait(&tempty[acc], ((iter >> 1) & 1) ^ 1);
@@ -259,14 +294,18 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
         // a last n-tile with <= 64 valid output channels runs N = 64 instructions (48 vs 64 cycles)
         const int nrem = p.N - (t % p.tiles_n) * BN;
         const std::uint32_t idesc = nrem <= 64 ? ((p.idesc & ~(0x3Fu << 17)) | ((64u >> 3) << 17)) : p.idesc;
-        for (int kb = 0; kb < p.kblocks; kb++) {
+        for (int kb0 = 0; kb0 < p.kblocks; kb0 += p.kpb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const std::uint32_t sa = smem_u32(ring + stage * (stage_a + stage_b));
-          const std::uint32_t a_lo = (sa >> 4) | (1u << 16);
-          const std::uint32_t b_lo = ((sa + stage_a) >> 4) | (1u << 16);
-          for (int ks = 0; ks < ksteps; ks++)  // +32 bytes along the K-major rows
-            umma_i8(d, a_lo + ks * 2, p.desc_hi, b_lo + ks * 2, p.desc_hi, idesc, (kb | ks) != 0);
+          const std::uint32_t sa = smem_u32(ring + stage * sstride);
+          for (int j = 0; j < p.kpb; j++) {
+            const int kb = kb0 + j;
+            const std::uint32_t a_lo = ((sa + j * stage_a) >> 4) | (1u << 16);
+            const std::uint32_t b_lo =
+                ((p.b_res ? smem_u32(bres + kb * stage_b) : sa + p.kpb * stage_a + j * stage_b) >> 4) | (1u << 16);
+            for (int ks = 0; ks < ksteps; ks++)  // +32 bytes along the K-major rows
+              umma_i8(d, a_lo + ks * 2, p.desc_hi, b_lo + ks * 2, p.desc_hi, idesc, (kb | ks) != 0);
+          }
           umma_commit(&empty[stage]);
           if (++stage == stages) {
             stage = 0;
@@ -310,7 +349,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       const int u0 = p.sx * ox, v0 = p.sy * oy;
       const std::int8_t* pix = p.g_in + p.g_a0 + p.g_an * img + p.g_ax * u0 + p.g_ay * v0;
       for (int kb = 0; kb < p.kblocks; kb++) {
-        std::uint8_t* rowp = ring + stage * (stage_a + stage_b) + r * p.bk;
+        std::uint8_t* rowp = ring + stage * sstride + r * p.bk;
         if (p.g_run) {
           // run layout: tap row i's S*C input bytes are contiguous (a_y == C); copy them with
           // aligned word loads + funnel shifts, zeroing bytes whose column j is skipped.
@@ -811,11 +850,27 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     const int res = kp.epi_res ? 2 * kResBytes : 0;
     const int vec = kp.fast_clamp ? 2 * kVecBytes : kp.epi_vec ? kVecBytes : 0;
     const int tab = kp.gather ? (kp.kblocks * kp.bk * 6 + 15) / 16 * 16 : 0;
-    const int stage = 2 * BM * g.bk;
-    int ring = std::min(kRingBytes, (kSmemMax - 1024 - 512 - stg - res - vec - tab) / stage * stage);
+    // the filter stays resident when there is one n-tile and it is small (<= 64 KB)
+    const int bres = kp.tiles_n == 1 && kp.kblocks * BN * g.bk <= 64 * 1024 && !std::getenv("SB_IG_NOBRES")
+                         ? kp.kblocks * BN * g.bk : 0;
+    kp.b_res = bres ? 1 : 0;
+    const int kstage = (bres ? 1 : 2) * BM * g.bk;  // one k-block's A (+ B)
+    const int avail = std::min(kRingBytes, kSmemMax - 1024 - 512 - stg - res - vec - tab - bres);
+    // k-blocks per stage: up to 4 while three stages still fit (gather mode: 1)
+    kp.kpb = 1;
+    if (!kp.gather && !std::getenv("SB_IG_KPB1"))
+      for (int c : {4, 2})
+        if (kp.kblocks % c == 0 && 3 * c * kstage <= avail) {
+          kp.kpb = c;
+          break;
+        }
+    const int stage = kp.kpb * kstage;
+    int ring = avail / stage * stage;
     if (ring < 2 * stage) return cudaErrorNotSupported;
     kp.stages = std::min(16, ring / stage);
     ring = kp.stages * stage;
+    kp.bres_off = ring;
+    ring += bres;
     kp.stg_off = ring;
     kp.res_off = ring + stg;
     kp.vec_off = ring + stg + res;
@@ -957,35 +1012,84 @@ __global__ void conv_pack_filter_kernel(const std::int8_t* __restrict__ b, std::
   }
 }
 
-// Phase fold: F[n, U, V, kf] = I[n, fx*U + di, fy*V + dj, c] for kf = (di*fy + dj)*C + c
-// (zero outside the constraint window and for kf >= fx*fy*C).  One thread per folded pixel
-// and 4-byte word; the window test is per byte.
-__global__ void __launch_bounds__(256) conv_fold_kernel(const std::int8_t* __restrict__ a, std::uint32_t* __restrict__ f,
-                                                        long long words, int FU, int FV, int FW, int fx, int fy, int C,
-                                                        long long a_n, long long a_x, long long a_y, long long a0,
-                                                        int u_lo, int u_hi, int v_lo, int v_hi) {
-  const int fyc = fy * C, fxyc = fx * fyc;
+// Folded rows T[n, U, y, q], q = b*fold_c + kf < fold_cv: the folded pixel F[n, U, y + b] of
+// kf = (di*fy + dj)*C + c, i.e. I[n, fx*U + di, fy*(y + b) + dj, c] (zero outside the
+// constraint window and on padding bytes).  Specialised: one thread per row, everything
+// unrolled (the ResNet stem is FX = FY = 2, C = 3, four 16-byte folded pixels per row).
+template <int FX, int FY, int CC, int NB>
+__global__ void __launch_bounds__(256) conv_fold_rows_fixed(const std::int8_t* __restrict__ a, uint4* __restrict__ T,
+                                                            int rows, int FU, int Q, long long a_n, long long a_x,
+                                                            long long a_y, long long a0, int u_lo, int u_hi, int v_lo,
+                                                            int v_hi) {
+  constexpr int FC = (FX * FY * CC + 15) / 16 * 16, CV = NB * FC;
+  for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < rows; row += gridDim.x * blockDim.x) {
+    const int nu = row / Q, y = row - nu * Q;
+    const int n = nu / FU, U = nu - n * FU;
+    std::uint32_t w[CV / 4];
+#pragma unroll
+    for (int i = 0; i < CV / 4; i++) w[i] = 0;
+#pragma unroll
+    for (int di = 0; di < FX; di++) {
+      const int u = FX * U + di;
+      const bool uok = u >= u_lo && u <= u_hi;
+      const std::int8_t* rp = a + a0 + a_n * n + a_x * u;
+#pragma unroll
+      for (int b = 0; b < NB; b++)
+#pragma unroll
+        for (int dj = 0; dj < FY; dj++) {
+          const int v = FY * (y + b) + dj;
+          if (uok && v >= v_lo && v <= v_hi) {
+#pragma unroll
+            for (int c = 0; c < CC; c++) {
+              const int q = b * FC + (di * FY + dj) * CC + c;
+              w[q / 4] |= static_cast<std::uint32_t>(static_cast<std::uint8_t>(__ldg(rp + a_y * v + c))) << (8 * (q % 4));
+            }
+          }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < CV / 16; i++)
+      T[static_cast<long long>(row) * (CV / 16) + i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+  }
+}
+
+// Any fold: one thread per 4 bytes of a row, per-byte (du, dv, c) from a shared table.
+__global__ void __launch_bounds__(256) conv_fold_rows(const std::int8_t* __restrict__ a, std::uint32_t* __restrict__ T,
+                                                      long long words, int FU, int Q, int CVW, int fx, int fy, int C,
+                                                      int fc, long long a_n, long long a_x, long long a_y, long long a0,
+                                                      int u_lo, int u_hi, int v_lo, int v_hi) {
+  __shared__ int tab[1024];  // du | c << 8 | dv << 16, or -1
+  const int cv = 4 * CVW, fyc = fy * C;
+  for (int q = threadIdx.x; q < cv; q += blockDim.x) {
+    const int b = q / fc, kf = q - b * fc;
+    int e = -1;
+    if (kf < fx * fyc) {
+      const int di = kf / fyc, r = kf - di * fyc, dj = r / C, c = r - dj * C;
+      e = di | (c << 8) | ((fy * b + dj) << 16);
+    }
+    tab[q] = e;
+  }
+  __syncthreads();
   for (long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; g < words;
        g += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long pix = g / FW;
-    const int w = static_cast<int>(g - pix * FW);
-    const long long nu = pix / FV;
-    const int V = static_cast<int>(pix - nu * FV);
+    const long long row = g / CVW;
+    const int wi = static_cast<int>(g - row * CVW);
+    const long long nu = row / Q;
+    const int y = static_cast<int>(row - nu * Q);
     const long long n = nu / FU;
     const int U = static_cast<int>(nu - n * FU);
     std::uint32_t word = 0;
 #pragma unroll
     for (int e = 0; e < 4; e++) {
-      const int kf = 4 * w + e;
-      if (kf < fxyc) {
-        const int di = kf / fyc, r = kf - di * fyc, dj = r / C, c = r - dj * C;
-        const int u = fx * U + di, v = fy * V + dj;
+      const int t = tab[4 * wi + e];
+      if (t >= 0) {
+        const int u = fx * U + (t & 0xFF), v = fy * y + (t >> 16), c = (t >> 8) & 0xFF;
         if (u >= u_lo && u <= u_hi && v >= v_lo && v <= v_hi)
           word |= static_cast<std::uint32_t>(static_cast<std::uint8_t>(__ldg(a + a0 + a_n * n + a_x * u + a_y * v + c)))
                   << (8 * e);
       }
     }
-    f[g] = word;
+    T[g] = word;
   }
 }
 
@@ -1011,14 +1115,29 @@ __global__ void conv_fold_filter_kernel(const std::int8_t* __restrict__ b, std::
 }  // namespace
 
 cudaError_t launch_conv_fold(const ConvPlan& cp, const void* a, void* f, cudaStream_t s) {
-  const int FW = static_cast<int>(cp.fold_c / 4);
-  const long long words = cp.N * cp.fold_u * cp.fold_v * FW;
-  const long long blocks = std::min<long long>((words + 255) / 256, 148 * 16);
-  conv_fold_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(
-      static_cast<const std::int8_t*>(a), static_cast<std::uint32_t*>(f), words, static_cast<int>(cp.fold_u),
-      static_cast<int>(cp.fold_v), FW, static_cast<int>(cp.fold_x), static_cast<int>(cp.fold_y),
-      static_cast<int>(cp.C), cp.a_n, cp.a_x, cp.a_y, cp.a0, static_cast<int>(cp.u_lo), static_cast<int>(cp.u_hi),
-      static_cast<int>(cp.v_lo), static_cast<int>(cp.v_hi));
+  const long long rows = cp.N * cp.fold_u * cp.W;
+  const auto* in = static_cast<const std::int8_t*>(a);
+  const int lo_u = static_cast<int>(cp.u_lo), hi_u = static_cast<int>(cp.u_hi);
+  const int lo_v = static_cast<int>(cp.v_lo), hi_v = static_cast<int>(cp.v_hi);
+  const int blocks_rows = static_cast<int>(std::min<long long>((rows + 255) / 256, 148 * 32));
+  const int nb = cp.fold_cv % cp.fold_c == 0 ? static_cast<int>(cp.fold_cv / cp.fold_c) : 0;
+  if (cp.fold_x == 2 && cp.fold_y == 2 && cp.C == 3 && nb == 4 && cp.fold_c == 16) {
+    conv_fold_rows_fixed<2, 2, 3, 4><<<blocks_rows, 256, 0, s>>>(in, static_cast<uint4*>(f), static_cast<int>(rows),
+                                                                 static_cast<int>(cp.fold_u), static_cast<int>(cp.W),
+                                                                 cp.a_n, cp.a_x, cp.a_y, cp.a0, lo_u, hi_u, lo_v, hi_v);
+  } else if (cp.fold_x == 1 && cp.fold_y == 1 && cp.C == 3 && nb == 4 && cp.fold_c == 16) {
+    conv_fold_rows_fixed<1, 1, 3, 4><<<blocks_rows, 256, 0, s>>>(in, static_cast<uint4*>(f), static_cast<int>(rows),
+                                                                 static_cast<int>(cp.fold_u), static_cast<int>(cp.W),
+                                                                 cp.a_n, cp.a_x, cp.a_y, cp.a0, lo_u, hi_u, lo_v, hi_v);
+  } else {
+    const int CVW = static_cast<int>(cp.fold_cv / 4);
+    const long long words = rows * CVW;
+    const long long blocks = std::min<long long>((words + 255) / 256, 148 * 32);
+    conv_fold_rows<<<static_cast<int>(blocks), 256, 0, s>>>(
+        in, static_cast<std::uint32_t*>(f), words, static_cast<int>(cp.fold_u), static_cast<int>(cp.W), CVW,
+        static_cast<int>(cp.fold_x), static_cast<int>(cp.fold_y), static_cast<int>(cp.C), static_cast<int>(cp.fold_c),
+        cp.a_n, cp.a_x, cp.a_y, cp.a0, lo_u, hi_u, lo_v, hi_v);
+  }
   return cudaGetLastError();
 }
 
@@ -1067,7 +1186,8 @@ const char* conv_igemm_unsupported(const ConvPlan& cp) {
         cp.fold_x * cp.fold_y * cp.C > cp.fold_c || cp.fold_s * cp.fold_c > cp.fold_cv ||
         cp.fold_u < cp.H + cp.fold_r - 1 || (cp.fold_v - cp.W + 1) * cp.fold_c < cp.fold_cv)
       return "inconsistent phase fold";
-    if (cp.N * cp.fold_u * cp.fold_v >= (1ll << 31)) return "folded input too large";
+    if (cp.N * cp.fold_u * cp.W >= (1ll << 31) || cp.fold_cv > 1024 || cp.fold_r > 127 || cp.C > 255)
+      return "folded input too large";
     return conv_igemm_unsupported(packed_view(cp));
   }
   if (cp.packed) {
