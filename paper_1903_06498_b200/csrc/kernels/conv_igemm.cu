@@ -59,6 +59,7 @@ struct IgKParams {
   int epi_warps;  // 4 or 8 (two warps per TMEM lane quarter, each taking half the columns)
   int epi_split;  // 8 epilogue warps as two independent groups of 4 taking alternate tiles
   int b_res, bres_off;
+  int bn_box;  // filter rows per TMA box / smem tile: 64 when N <= 64, else BN
   int kpb;  // k-blocks per ring stage (one barrier handshake per stage: ~200 cycles each, measured)  // whole filter resident in smem (one n-tile, small reduction): the ring holds A only
   int pdl_wait;   // griddepcontrol.wait before touching buffers (else independent of in-flight work)
   long long g_an, g_ax, g_ay, g_a0;
@@ -157,7 +158,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
   extern __shared__ __align__(1024) std::uint8_t smem_raw[];
   std::uint8_t* base =
       reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t{1023});
-  const std::uint32_t stage_a = BM * p.bk, stage_b = BN * p.bk;
+  const std::uint32_t stage_a = BM * p.bk, stage_b = p.bn_box * p.bk;
   std::uint8_t* ring = base;                    // stages x (A | B), or stages x A with the filter resident
   const std::uint32_t sstride = p.kpb * (stage_a + (p.b_res ? 0u : stage_b));
   std::uint8_t* bres = base + p.bres_off;       // resident filter: kblocks x stage_b
@@ -851,15 +852,16 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     const int vec = kp.fast_clamp ? 2 * kVecBytes : kp.epi_vec ? kVecBytes : 0;
     const int tab = kp.gather ? (kp.kblocks * kp.bk * 6 + 15) / 16 * 16 : 0;
     // the filter stays resident when there is one n-tile and it is small (<= 64 KB)
-    const int bres = kp.tiles_n == 1 && kp.kblocks * BN * g.bk <= 64 * 1024 && !std::getenv("SB_IG_NOBRES")
-                         ? kp.kblocks * BN * g.bk : 0;
+    kp.bn_box = kp.N <= 64 ? 64 : BN;
+    const int bres = kp.tiles_n == 1 && kp.kblocks * kp.bn_box * g.bk <= 96 * 1024 && !std::getenv("SB_IG_NOBRES")
+                         ? kp.kblocks * kp.bn_box * g.bk : 0;
     kp.b_res = bres ? 1 : 0;
-    const int kstage = (bres ? 1 : 2) * BM * g.bk;  // one k-block's A (+ B)
+    const int kstage = (BM + (bres ? 0 : kp.bn_box)) * g.bk;  // one k-block's A (+ B)
     const int avail = std::min(kRingBytes, kSmemMax - 1024 - 512 - stg - res - vec - tab - bres);
     // k-blocks per stage: up to 4 while three stages still fit (gather mode: 1)
     kp.kpb = 1;
     if (!kp.gather && !std::getenv("SB_IG_KPB1"))
-      for (int c : {4, 2})
+      for (int c : {4, 3, 2})
         if (kp.kblocks % c == 0 && 3 * c * kstage <= avail) {
           kp.kpb = c;
           break;
@@ -908,7 +910,7 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
                         static_cast<cuuint64_t>(gp.R)};
   cuuint64_t bstr[3] = {static_cast<cuuint64_t>(gp.b_k), static_cast<cuuint64_t>(gp.S > 1 ? gp.b_j : gp.b_k * gp.K),
                         static_cast<cuuint64_t>(gp.R > 1 ? gp.b_i : gp.b_k * gp.K * gp.S)};
-  cuuint32_t bbox[4] = {static_cast<cuuint32_t>(g.bk), BN, 1, 1};
+  cuuint32_t bbox[4] = {static_cast<cuuint32_t>(g.bk), static_cast<cuuint32_t>(kp.bn_box), 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   if (enc_tiled(&out->bmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<std::int8_t*>(bbase), bdim, bstr, bbox, es,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
