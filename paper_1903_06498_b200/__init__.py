@@ -26,7 +26,8 @@ from typing import Dict, Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libstripe_b200.so")
+# SB_LIBRARY: development override (e.g. the `make trace` build); default the in-tree library
+LIB_PATH = os.environ.get("SB_LIBRARY") or os.path.join(_HERE, "libstripe_b200.so")
 
 SB_I8, SB_I16, SB_I32, SB_F32 = 8, 16, 32, 0x20F
 SB_CARRIER_I64, SB_CARRIER_NATIVE = 0, 1

@@ -32,6 +32,26 @@
 
 #include "../kernels.hpp"
 
+// Development aid (make trace): per-tile timestamps of CTA 0 printed after each launch.
+#ifdef SB_TILE_TRACE
+#include <cstdio>
+#define TILE_STAMP(slot, i) \
+  do {                                                                            \
+    if (p.trace && blockIdx.x == 0 && (i) < 128) p.trace[(slot)*128 + (i)] = clock64(); \
+  } while (0)
+#define STAGE_STAMP(iter, st, k)                                                                      \
+  do {                                                                                                \
+    if (p.trace && blockIdx.x == 0 && (iter) < 32 && (st) < 4) p.trace[640 + ((iter)*4 + (st)) * 3 + (k)] = clock64(); \
+  } while (0)
+#else
+#define STAGE_STAMP(iter, st, k) \
+  do {                           \
+  } while (0)
+#define TILE_STAMP(slot, i) \
+  do {                      \
+  } while (0)
+#endif
+
 namespace sb {
 namespace {
 
@@ -70,6 +90,7 @@ struct IgKParams {
   long long ldc;      // elements between consecutive output pixels
   std::uint32_t idesc, desc_hi;
   int pdl;
+  long long* trace;  // SB_TILE_TRACE builds only: per-tile clock64 stamps of CTA 0
   // fused epilogue: out = wrap(max(acc + vec[k], lo))
   int epi, epi_vec, epi_lo, epi_res, vec_kind;
   int fast_clamp;  // |acc| + 128 < 2^31: clamp decided by an int32 compare against lo - vec[k]
@@ -131,6 +152,11 @@ __device__ __forceinline__ void umma_i8(std::uint32_t d, std::uint32_t a_lo, std
       "setp.ne.b32 p, %6, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], da, db, %5, p;\n\t}" ::"r"(d),
       "r"(a_lo), "r"(a_hi), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ bool elect_one() {
+  std::uint32_t is;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(is));
+  return is != 0;
 }
 __device__ __forceinline__ void umma_commit(std::uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
@@ -194,8 +220,10 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
+    // all 512 columns (one CTA per SM): the allocation is then column 0, so the MMA issuer
+    // addresses accumulators with compile-time-uniform values
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(256));
+                 "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -248,6 +276,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
           const bool mine = kit % nchains == chain;
           if (mine) {
             mbar_wait(&empty[stage], phase ^ 1);
+            if (pidx == 0 && kb0 == 0) TILE_STAMP(0, (t - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x));
             if (do_a) mbar_expect_tx(&full[stage], p.kpb * stage_a);
             if (do_b && !p.b_res) mbar_expect_tx(&full[stage], p.kpb * stage_b);
           }
@@ -279,42 +308,52 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      int stage = 0, iter = 0;
-      std::uint32_t phase = 0;
-      const int ksteps = p.bk / 32;
-      if (p.b_res) {
-        mbar_wait(bfull, 0);
+    // the whole warp runs the loop (converged, so the descriptors stay in uniform registers);
+    // one elected lane issues the MMAs and commits
+    const bool issuer = elect_one();
+    int stage = 0, iter = 0;
+    std::uint32_t phase = 0;
+    const int ksteps = p.bk / 32;
+    if (p.b_res) {
+      mbar_wait(bfull, 0);
+      tc_fence_after();
+    }
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, iter++) {
+      const int acc = iter & 1;
+      mbar_wait(&tempty[acc], ((iter >> 1) & 1) ^ 1);
+      tc_fence_after();
+      if (issuer) TILE_STAMP(1, iter);
+      const std::uint32_t d = static_cast<std::uint32_t>(acc * BN);  // TMEM column (allocation at 0)
+      // a last n-tile with <= 64 valid output channels runs N = 64 instructions (48 vs 64 cycles)
+      const int nrem = p.N - (t % p.tiles_n) * BN;
+      const std::uint32_t idesc = nrem <= 64 ? ((p.idesc & ~(0x3Fu << 17)) | ((64u >> 3) << 17)) : p.idesc;
+      for (int kb0 = 0; kb0 < p.kblocks; kb0 += p.kpb) {
+        if (issuer) STAGE_STAMP(iter, kb0 / p.kpb, 0);
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
-      }
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x, iter++) {
-        const int acc = iter & 1;
-        mbar_wait(&tempty[acc], ((iter >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const std::uint32_t d = tmem_base + static_cast<std::uint32_t>(acc * BN);
-        // a last n-tile with <= 64 valid output channels runs N = 64 instructions (48 vs 64 cycles)
-        const int nrem = p.N - (t % p.tiles_n) * BN;
-        const std::uint32_t idesc = nrem <= 64 ? ((p.idesc & ~(0x3Fu << 17)) | ((64u >> 3) << 17)) : p.idesc;
-        for (int kb0 = 0; kb0 < p.kblocks; kb0 += p.kpb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const std::uint32_t sa = smem_u32(ring + stage * sstride);
-          for (int j = 0; j < p.kpb; j++) {
-            const int kb = kb0 + j;
-            const std::uint32_t a_lo = ((sa + j * stage_a) >> 4) | (1u << 16);
-            const std::uint32_t b_lo =
-                ((p.b_res ? smem_u32(bres + kb * stage_b) : sa + p.kpb * stage_a + j * stage_b) >> 4) | (1u << 16);
-            for (int ks = 0; ks < ksteps; ks++)  // +32 bytes along the K-major rows
+        if (issuer) STAGE_STAMP(iter, kb0 / p.kpb, 1);
+        const std::uint32_t sa = smem_u32(ring + stage * sstride);
+        for (int j = 0; j < p.kpb; j++) {
+          const int kb = kb0 + j;
+          const std::uint32_t a_lo = ((sa + j * stage_a) >> 4) | (1u << 16);
+          const std::uint32_t b_lo =
+              ((p.b_res ? smem_u32(bres + kb * stage_b) : sa + p.kpb * stage_a + j * stage_b) >> 4) | (1u << 16);
+#pragma unroll
+          for (int ks = 0; ks < 4; ks++)  // +32 bytes along the K-major rows
+            if (ks < ksteps && issuer)
               umma_i8(d, a_lo + ks * 2, p.desc_hi, b_lo + ks * 2, p.desc_hi, idesc, (kb | ks) != 0);
-          }
-          umma_commit(&empty[stage]);
-          if (++stage == stages) {
-            stage = 0;
-            phase ^= 1;
-          }
         }
-        umma_commit(&tfull[acc]);
+        if (issuer) STAGE_STAMP(iter, kb0 / p.kpb, 2);
+        if (issuer) umma_commit(&empty[stage]);
+        __syncwarp();
+        if (++stage == stages) {
+          stage = 0;
+          phase ^= 1;
+        }
       }
+      if (issuer) umma_commit(&tfull[acc]);
+      __syncwarp();
+      if (issuer) TILE_STAMP(2, iter);
     }
   } else if (p.gather && warp >= 2 + p.epi_warps) {
     // gather producers: row r of every A stage = the packed (i, j, c) taps of pixel m0 + r,
@@ -502,6 +541,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       if (!split && p.epi_res && leader && t + static_cast<int>(gridDim.x) < tiles) load_res(t + gridDim.x, (iter + 1) & 1);
       mbar_wait(&tfull[acc], (iter >> 1) & 1);
       tc_fence_after();
+      if (leader) TILE_STAMP(3, iter);
       if (p.epi_res) mbar_wait(&rfull[iter & 1], (iter >> 1) & 1);
       std::uint8_t* rcur = rstg + (iter & 1) * kResBytes;
       std::uint8_t* scur = p.tma_out == 2 ? stg + (iter & 1) * 16384 : stg;
@@ -698,6 +738,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
                          : "memory");
           }
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          TILE_STAMP(4, iter);
         }
       }
     }
@@ -706,7 +747,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(256));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
   }
 }
 
@@ -1252,7 +1293,30 @@ cudaError_t launch_conv_igemm(const ConvPlan& cp, const ConvArgs& args, cudaStre
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = kp.pdl ? 1 : 0;
+#ifdef SB_TILE_TRACE
+  static long long* tr = nullptr;
+  if (!tr) cudaMalloc(&tr, (640 + 32 * 4 * 3) * 8);
+  cudaMemsetAsync(tr, 0, (640 + 32 * 4 * 3) * 8, s);
+  kp.trace = tr;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, conv_igemm_i8_kernel, pr->amap, pr->bmap, pr->cmap, pr->rmap, kp);
+  long long h[640 + 32 * 4 * 3];
+  cudaStreamSynchronize(s);
+  cudaMemcpy(h, tr, sizeof(h), cudaMemcpyDeviceToHost);
+  std::fprintf(stderr, "igemm M=%d N=%d kblocks=%d kpb=%d stages=%d b_res=%d split=%d tiles=%d\n", kp.M, kp.N, kp.kblocks,
+               kp.kpb, kp.stages, kp.b_res, kp.epi_split, tiles);
+  for (int i = 0; i < 128; i++)
+    if (h[128 + i])
+      std::fprintf(stderr, "tile %3d prod %8lld mma0 %8lld mma1 %8lld epi0 %8lld epi1 %8lld\n", i, h[i] ? h[i] - h[128] : -1,
+                   h[128 + i] - h[128], h[256 + i] - h[128], h[384 + i] - h[128], h[512 + i] - h[128]);
+  for (int i = 0; i < 32; i++)
+    for (int st = 0; st < 4; st++) {
+      const long long* q = h + 640 + (i * 4 + st) * 3;
+      if (q[0]) std::fprintf(stderr, "  tile %2d stage %d: wait %6lld..%6lld  mma issue %5lld\n", i, st, q[0] - h[128], q[1] - h[128], q[2] - q[1]);
+    }
+  return e;
+#else
   return cudaLaunchKernelEx(&cfg, conv_igemm_i8_kernel, pr->amap, pr->bmap, pr->cmap, pr->rmap, kp);
+#endif
 }
 
 }  // namespace sb

@@ -20,6 +20,10 @@ def main():
         text, info = W.resnet50(batch)
     elif which == "stem":
         text = W.conv_fused(batch, 224, 224, 3, 64, 7, 7, 2, 3)
+    elif which == "l3x3":
+        text = W.conv_fused(batch, 56, 56, 64, 64, 3, 3, 1, 1)
+    elif which == "l1x1":
+        text = W.conv_fused(batch, 56, 56, 64, 64, 1, 1, 1, 0)
     elif which == "c2":
         text = W.conv2d(32, 56, 56, 64, 64)
     else:
