@@ -239,14 +239,15 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
   const int pw0 = 2 + p.epi_warps + (p.gather ? 8 : 0);  // extra producer warps pw0 .. pw0 + 2
   const int pidx = warp == 0 ? 0 : (!p.gather && warp >= pw0) ? warp - pw0 + 1 : -1;
   if (pidx >= 0) {
-    if (lane == 0) {
+    {  // converged warp; one elected lane issues (uniform-register operands, see the MMA warp)
+      const bool issuer = elect_one();
       if (p.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
       const bool do_a = !p.gather && (pidx & 1) == 0, do_b = p.gather || (pidx & 1) == 1;
       const int nchains = p.gather ? 1 : 2, chain = p.gather ? 0 : pidx >> 1;
       const int PQ = p.P * p.Q;
       if (do_b && p.b_res) {
         // the whole filter once (tiles_n == 1), then this producer is done
-        if (chain == 0) {
+        if (chain == 0 && issuer) {
           mbar_expect_tx(bfull, p.kblocks * stage_b);
           int cb = 0, r = 0, s = 0;
           for (int kb = 0; kb < p.kblocks; kb++) {
@@ -276,17 +277,18 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
           const bool mine = kit % nchains == chain;
           if (mine) {
             mbar_wait(&empty[stage], phase ^ 1);
-            if (pidx == 0 && kb0 == 0) TILE_STAMP(0, (t - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x));
-            if (do_a) mbar_expect_tx(&full[stage], p.kpb * stage_a);
-            if (do_b && !p.b_res) mbar_expect_tx(&full[stage], p.kpb * stage_b);
+            if (issuer && pidx == 0 && kb0 == 0)
+              TILE_STAMP(0, (t - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x));
+            if (issuer && do_a) mbar_expect_tx(&full[stage], p.kpb * stage_a);
+            if (issuer && do_b && !p.b_res) mbar_expect_tx(&full[stage], p.kpb * stage_b);
           }
           const std::uint32_t sa = smem_u32(ring + stage * sstride);
           for (int j = 0; j < p.kpb; j++) {
             const int kb = kb0 + j;
-            if (mine && do_a)
+            if (issuer && mine && do_a)
               tma_load_im2col(sa + j * stage_a, &amap, &full[stage], cb * p.bk, w0, h0, img,
                               static_cast<std::uint16_t>(s), static_cast<std::uint16_t>(r));
-            if (mine && do_b && !p.b_res) {
+            if (issuer && mine && do_b && !p.b_res) {
               const std::uint32_t sb = sa + p.kpb * stage_a + j * stage_b;
               if (p.gather) tma_load_4d(sb, &bmap, &full[stage], kb * p.bk, n0, 0, 0);
               else tma_load_4d(sb, &bmap, &full[stage], cb * p.bk, n0, s, r);
@@ -299,6 +301,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
               }
             }
           }
+          __syncwarp();
           if (++stage == stages) {
             stage = 0;
             phase ^= 1;
