@@ -55,12 +55,10 @@
 namespace sb {
 namespace {
 
-constexpr int kThreads = 192;        // producer, MMA, 4 epilogue warps
 constexpr int kThreadsGather = 448;  // + 8 warps gathering A tiles (small-channel convs), 2 per row
 constexpr int BM = 128, BN = 128;
 constexpr int kRingBytes = 128 * 1024;  // A+B stage ring
 constexpr int kStgBytes = BM * BN * 4;    // output staging (i32 worst case)
-constexpr int kResBytes = BM * BN;        // residual tile (i8)
 constexpr int kVecBytes = 2048 * 4;       // per-channel epilogue vector
 constexpr int kMaxVecK = 2048;
 
@@ -79,7 +77,8 @@ struct IgKParams {
   int epi_warps;  // 4 or 8 (two warps per TMEM lane quarter, each taking half the columns)
   int epi_split;  // 8 epilogue warps as two independent groups of 4 taking alternate tiles
   int b_res, bres_off;
-  int bn_box;  // filter rows per TMA box / smem tile: 64 when N <= 64, else BN
+  int bn;      // tile width in output channels: 128 or 256 (N = 256 MMAs, 512 TMEM columns)
+  int bn_box;  // filter rows per TMA box / smem tile: 64 when N <= 64, else bn
   int kpb;  // k-blocks per ring stage (one barrier handshake per stage: ~200 cycles each, measured)  // whole filter resident in smem (one n-tile, small reduction): the ring holds A only
   int pdl_wait;   // griddepcontrol.wait before touching buffers (else independent of in-flight work)
   long long g_an, g_ax, g_ay, g_a0;
@@ -268,7 +267,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       std::uint32_t phase = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
         // n-tiles of one m-tile are adjacent in t: the A strip stays hot in L2
-        const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * BN;
+        const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * p.bn;
         const int img = m0 / PQ, rem = m0 - img * PQ;
         const int ox = rem / p.Q, oy = rem - ox * p.Q;
         const int h0 = p.lower_h + ox * p.sx, w0 = p.lower_w + oy * p.sy;
@@ -326,10 +325,11 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       mbar_wait(&tempty[acc], ((iter >> 1) & 1) ^ 1);
       tc_fence_after();
       if (issuer) TILE_STAMP(1, iter);
-      const std::uint32_t d = static_cast<std::uint32_t>(acc * BN);  // TMEM column (allocation at 0)
-      // a last n-tile with <= 64 valid output channels runs N = 64 instructions (48 vs 64 cycles)
-      const int nrem = p.N - (t % p.tiles_n) * BN;
-      const std::uint32_t idesc = nrem <= 64 ? ((p.idesc & ~(0x3Fu << 17)) | ((64u >> 3) << 17)) : p.idesc;
+      const std::uint32_t d = static_cast<std::uint32_t>(acc * p.bn);  // TMEM column (allocation at 0)
+      // a last n-tile with few valid output channels runs narrower instructions
+      const int nrem = p.N - (t % p.tiles_n) * p.bn;
+      const std::uint32_t ninst = nrem <= 64 ? 64u : nrem <= 128 ? 128u : static_cast<std::uint32_t>(p.bn);
+      const std::uint32_t idesc = (p.idesc & ~(0x3Fu << 17)) | ((ninst >> 3) << 17);
       for (int kb0 = 0; kb0 < p.kblocks; kb0 += p.kpb) {
         if (issuer) STAGE_STAMP(iter, kb0 / p.kpb, 0);
         mbar_wait(&full[stage], phase);
@@ -480,7 +480,6 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
     const int row = quarter * 32 + lane;
     const int ethreads = 32 * p.epi_warps;
     const int hgroups = p.epi_warps / 4, hgroup = (warp - 2) / 4;  // column halves when 8 warps
-    const int h_lo = hgroup * (BN / 32) / hgroups, h_hi = (hgroup + 1) * (BN / 32) / hgroups;
     const int sw = row & 7;  // 128B swizzle phase of this staging row
     // split: group g = hgroup owns TMEM accumulator g, staging/residual buffer g and tiles
     // blockIdx.x + g*grid, + 2*grid, ... (its own barrier and store leader), so the two
@@ -510,22 +509,25 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       }
     }
     if (p.epi_vec)  // zero tail: chunk loads past N need no bounds select
-      for (int k = p.N + threadIdx.x - 64; k < (p.N + BN - 1) / BN * BN && k < kMaxVecK; k += ethreads) vec_s[k] = 0;
+      for (int k = p.N + threadIdx.x - 64; k < (p.N + p.bn - 1) / p.bn * p.bn && k < kMaxVecK; k += ethreads) vec_s[k] = 0;
     if (p.epi_res && leader && p.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("bar.sync 1, %0;" ::"r"(ethreads) : "memory");
     const bool fast8 = p.fast8 && !(p.epi_lo && *reinterpret_cast<volatile int*>(bars + 41));
     const std::int32_t lo8 = p.epi_lo ? static_cast<std::int32_t>(p.lo) : INT_MIN;
     const long long lo = p.epi_lo ? p.lo : LLONG_MIN;
     const bool relu0 = p.epi_lo && p.lo == 0;
-    // residual tile [128 pixels x 128 channels] i8 of tile t into buffer b
+    // residual tile [128 pixels x bn channels] i8 of tile t into buffer b, as 128-channel halves
+    const int res_buf = BM * p.bn, stg_buf = p.bn / 128 * 16384;
     auto load_res = [&](int t, int b) {
-      const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * BN;
-      mbar_expect_tx(&rfull[b], BM * BN);
-      asm volatile(
-          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
-              "r"(smem_u32(rstg + b * kResBytes)),
-          "l"(reinterpret_cast<std::uint64_t>(&rmap)), "r"(smem_u32(&rfull[b])), "r"(n0), "r"(m0)
-          : "memory");
+      const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * p.bn;
+      const int halves = min(p.bn, p.N - n0 + 127) / 128;
+      mbar_expect_tx(&rfull[b], BM * 128 * halves);
+      for (int hh = 0; hh < halves; hh++)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
+                "r"(smem_u32(rstg + b * res_buf + hh * 16384)),
+            "l"(reinterpret_cast<std::uint64_t>(&rmap)), "r"(smem_u32(&rfull[b])), "r"(n0 + hh * 128), "r"(m0)
+            : "memory");
     };
     const int g0 = split ? hgroup : 0, tstep = split ? 2 * static_cast<int>(gridDim.x) : static_cast<int>(gridDim.x);
     if (p.epi_res && leader && static_cast<int>(blockIdx.x) + g0 * static_cast<int>(gridDim.x) < tiles)
@@ -533,7 +535,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
     int iter = g0;
     for (int t = blockIdx.x + g0 * gridDim.x; t < tiles; t += tstep, iter += split ? 2 : 1) {
       const int acc = iter & 1;
-      const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * BN;
+      const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * p.bn;
       if (p.tma_out || p.epi_res) {
         // i32 staging is single-buffered, i8 staging double-buffered (one buffer per group when split)
         if (leader && (p.tma_out == 1 || (split && p.tma_out == 2)))
@@ -546,24 +548,23 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       tc_fence_after();
       if (leader) TILE_STAMP(3, iter);
       if (p.epi_res) mbar_wait(&rfull[iter & 1], (iter >> 1) & 1);
-      std::uint8_t* rcur = rstg + (iter & 1) * kResBytes;
-      std::uint8_t* scur = p.tma_out == 2 ? stg + (iter & 1) * 16384 : stg;
+      std::uint8_t* rcur = rstg + (iter & 1) * res_buf;
+      std::uint8_t* scur = p.tma_out == 2 ? stg + (iter & 1) * stg_buf : stg;
       const int m = m0 + row;
       // this warp's 32-column chunks: all valid chunks (split), else the valid chunks of the
       // tile divided between the two column groups
-      const int nch = min(BN, p.N - n0 + 31) / 32;
+      const int nch = min(p.bn, p.N - n0 + 31) / 32;
       const int c_lo = split || hgroups == 1 ? 0 : (hgroup * nch) >> 1;
       const int c_hi = split || hgroups == 1 ? nch : ((hgroup + 1) * nch) >> 1;
-      (void)h_lo;
-      (void)h_hi;
       for (int h = c_lo; h < c_hi; h++) {
         std::uint32_t v[32];
         tmem_ld32(tmem_base + (static_cast<std::uint32_t>(quarter * 32) << 16) +
-                      static_cast<std::uint32_t>(acc * BN + h * 32),
+                      static_cast<std::uint32_t>(acc * p.bn + h * 32),
                   v);
         const int kbase = n0 + h * 32;
         if (fast8) {
           // out = wrap8(max(acc + res + vec, lo)) in int32 (exact: see IgKParams::fast8)
+
           std::int32_t bv[32];
 #pragma unroll
           for (int q = 0; q < 8; q++) {
@@ -577,15 +578,16 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
           std::uint32_t w[8];
           if (p.epi_res) {
             std::uint32_t rw[8];
-            const std::uint32_t rrow = smem_u32(rcur + row * 128);
+            const std::uint32_t rrow = smem_u32(rcur + (h >> 2) * 16384 + row * 128);
 #pragma unroll
             for (int u = 0; u < 2; u++)
               asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                            : "=r"(rw[4 * u]), "=r"(rw[4 * u + 1]), "=r"(rw[4 * u + 2]), "=r"(rw[4 * u + 3])
-                           : "r"(rrow + (((2 * h + u) ^ sw) << 4)));
+                           : "r"(rrow + (((2 * (h & 3) + u) ^ sw) << 4)));
 #pragma unroll
             for (int q = 0; q < 32; q++) {
-              const std::int32_t r = static_cast<std::int32_t>(rw[q >> 2] << (24 - 8 * (q & 3))) >> 24;
+              std::int32_t r;  // sign-extended residual byte (prmt sign-replicate selector)
+              asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(rw[q >> 2]), "r"(0x8880u + 0x1111u * (q & 3)));
               v[q] = static_cast<std::uint32_t>(max(static_cast<std::int32_t>(v[q]) + r + bv[q], lo8));
             }
           } else {
@@ -597,10 +599,10 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
           for (int q = 0; q < 8; q++)
             w[q] = __byte_perm(__byte_perm(v[4 * q], v[4 * q + 1], 0x0040), __byte_perm(v[4 * q + 2], v[4 * q + 3], 0x0040),
                                0x5410);
-          const std::uint32_t rbase = smem_u32(scur + row * 128);
+          const std::uint32_t rbase = smem_u32(scur + (h >> 2) * 16384 + row * 128);
 #pragma unroll
           for (int u = 0; u < 2; u++)
-            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rbase + (((2 * h + u) ^ sw) << 4)),
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rbase + (((2 * (h & 3) + u) ^ sw) << 4)),
                          "r"(w[4 * u]), "r"(w[4 * u + 1]), "r"(w[4 * u + 2]), "r"(w[4 * u + 3]));
           continue;
         }
@@ -619,12 +621,12 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
           }
           std::uint32_t rw[8];
           if (p.epi_res) {
-            const std::uint32_t rrow = smem_u32(rcur + row * 128);
+            const std::uint32_t rrow = smem_u32(rcur + (h >> 2) * 16384 + row * 128);
 #pragma unroll
             for (int u = 0; u < 2; u++)
               asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                            : "=r"(rw[4 * u]), "=r"(rw[4 * u + 1]), "=r"(rw[4 * u + 2]), "=r"(rw[4 * u + 3])
-                           : "r"(rrow + (((2 * h + u) ^ sw) << 4)));
+                           : "r"(rrow + (((2 * (h & 3) + u) ^ sw) << 4)));
           }
           if (!p.epi_lo) {
             // no clamp: only the wrapped low bits reach the store
@@ -693,10 +695,10 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
           for (int q = 0; q < 8; q++)
             w[q] = (v[4 * q] & 0xFF) | ((v[4 * q + 1] & 0xFF) << 8) | ((v[4 * q + 2] & 0xFF) << 16) |
                    (v[4 * q + 3] << 24);
-          const std::uint32_t rbase = smem_u32(scur + row * 128);
+          const std::uint32_t rbase = smem_u32(scur + (h >> 2) * 16384 + row * 128);
 #pragma unroll
           for (int u = 0; u < 2; u++)
-            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rbase + (((2 * h + u) ^ sw) << 4)),
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rbase + (((2 * (h & 3) + u) ^ sw) << 4)),
                          "r"(w[4 * u]), "r"(w[4 * u + 1]), "r"(w[4 * u + 2]), "r"(w[4 * u + 3]));
         } else if (m < p.M) {
           const long long rowbase = static_cast<long long>(m) * p.ldc;
@@ -735,10 +737,11 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
                              "r"(smem_u32(stg + h * 16384)), "r"(n0 + h * 32), "r"(m0)
                              : "memory");
           } else {
-            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                             reinterpret_cast<std::uint64_t>(&cmap)),
-                         "r"(smem_u32(scur)), "r"(n0), "r"(m0)
-                         : "memory");
+            for (int hh = 0; hh < p.bn / 128 && n0 + hh * 128 < p.N; hh++)
+              asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                               reinterpret_cast<std::uint64_t>(&cmap)),
+                           "r"(smem_u32(scur + hh * 16384)), "r"(n0 + hh * 128), "r"(m0)
+                           : "memory");
           }
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           TILE_STAMP(4, iter);
@@ -854,7 +857,8 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     kp.g_run = static_cast<int>(cp.pack_run);
   }
   kp.tiles_m = (kp.M + BM - 1) / BM;
-  kp.tiles_n = (kp.N + BN - 1) / BN;
+  kp.bn = 128;
+  kp.tiles_n = (kp.N + BN - 1) / BN;  // final value from layout() below
   kp.fresh = cp.fresh_output ? 1 : 0;
   kp.out_kind = kind_of(cp.c_dtype);
   kp.ldc = cp.c_y;
@@ -889,14 +893,17 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     kp.epi_split = kp.epi_warps == 8 && kp.tma_out != 1 && !std::getenv("SB_IG_NOSPLIT") ? 1 : 0;
     kp.bias_bound = T < INT_MAX ? INT_MAX - T : 0;
   }
-  {
-    // dynamic smem: A/B ring (up to 128 KB) | output staging | residual tiles | vector | barriers
-    const int stg = kp.tma_out == 1 ? kStgBytes : kp.tma_out == 2 ? 2 * 16384 : 0;
-    const int res = kp.epi_res ? 2 * kResBytes : 0;
+  // dynamic smem: A/B ring (up to 128 KB) | resident filter | output staging | residual tiles |
+  // vector | gather table | barriers, for tile width bn (false: does not fit)
+  auto layout = [&](int bn) -> bool {
+    kp.bn = bn;
+    kp.tiles_n = (kp.N + bn - 1) / bn;
+    const int stg = kp.tma_out == 1 ? kStgBytes : kp.tma_out == 2 ? 2 * (bn / 128) * 16384 : 0;
+    const int res = kp.epi_res ? 2 * BM * bn : 0;
     const int vec = kp.fast_clamp ? 2 * kVecBytes : kp.epi_vec ? kVecBytes : 0;
     const int tab = kp.gather ? (kp.kblocks * kp.bk * 6 + 15) / 16 * 16 : 0;
-    // the filter stays resident when there is one n-tile and it is small (<= 64 KB)
-    kp.bn_box = kp.N <= 64 ? 64 : BN;
+    // the filter stays resident when there is one n-tile and it is small (<= 96 KB)
+    kp.bn_box = kp.N <= 64 ? 64 : bn;
     const int bres = kp.tiles_n == 1 && kp.kblocks * kp.bn_box * g.bk <= 96 * 1024 && !std::getenv("SB_IG_NOBRES")
                          ? kp.kblocks * kp.bn_box * g.bk : 0;
     kp.b_res = bres ? 1 : 0;
@@ -911,8 +918,8 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
           break;
         }
     const int stage = kp.kpb * kstage;
+    if (avail < 2 * stage) return false;
     int ring = avail / stage * stage;
-    if (ring < 2 * stage) return cudaErrorNotSupported;
     kp.stages = std::min(16, ring / stage);
     ring = kp.stages * stage;
     kp.bres_off = ring;
@@ -923,7 +930,11 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     kp.tab_off = ring + stg + res + vec;
     kp.bar_off = kp.tab_off + tab;
     kp.smem = 1024 + kp.bar_off + 512;
-  }
+    return true;
+  };
+  // 256-wide tiles (N = 256 MMAs: half the instructions and A re-reads) for wide outputs
+  const bool wide = kp.epi_split && kp.N >= 256 && cp.K <= kMaxVecK && !std::getenv("SB_IG_BN128");
+  if (!(wide && layout(256)) && !layout(128)) return cudaErrorNotSupported;
   // idesc: S32 accumulate, signed A/B, both K-major, N = 128, M = 128
   kp.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
   // descriptor high word: SBO = 8 rows x row bytes, version 1, swizzle 128B (2) / 64B (4)
