@@ -79,6 +79,9 @@ struct IgKParams {
   int b_res, bres_off;
   int bn;      // tile width in output channels: 128 or 256 (N = 256 MMAs, 512 TMEM columns)
   int bn_box;  // filter rows per TMA box / smem tile: 64 when N <= 64, else bn
+  // residual added by the tensor core: res tile (pixels x channels, SW128) x identity (128 x 128,
+  // resident) accumulated into the tile after its k-blocks; loaded by a fifth producer warp
+  int res_mma, ident_off;
   int kpb;  // k-blocks per ring stage (one barrier handshake per stage: ~200 cycles each, measured)  // whole filter resident in smem (one n-tile, small reduction): the ring holds A only
   int pdl_wait;   // griddepcontrol.wait before touching buffers (else independent of in-flight work)
   long long g_an, g_ax, g_ay, g_a0;
@@ -198,6 +201,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
   std::uint64_t* rfull = bars + 36;  // [2]
   std::uint64_t* bfull = bars + 38;  // resident filter landed
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 40);
+  std::uint64_t* rempty = bars + 44;  // [2] residual buffer consumed by the MMAs (res_mma)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int tiles = p.tiles_m * p.tiles_n;
   const int stages = p.stages;
@@ -214,6 +218,8 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
     }
     mbar_init(&rfull[0], 1);
     mbar_init(&rfull[1], 1);
+    mbar_init(&rempty[0], 1);
+    mbar_init(&rempty[1], 1);
     mbar_init(bfull, 1);
     *reinterpret_cast<int*>(bars + 41) = 0;  // some |vec[k]| > bias_bound
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -224,6 +230,17 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (p.res_mma) {
+    // identity B operand, K-major 128 x 128 with the 128B swizzle: row n has its 1 at byte n
+    uint4* id = reinterpret_cast<uint4*>(base + p.ident_off);
+    for (int u = threadIdx.x; u < 1024; u += blockDim.x) {
+      const int n = u >> 3, unit = (u & 7) ^ (n & 7);  // logical 16-byte unit of this physical slot
+      std::uint32_t w[4] = {0, 0, 0, 0};
+      if (unit == (n >> 4)) w[(n & 15) >> 2] = 1u << (8 * (n & 3));
+      id[u] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
@@ -244,7 +261,27 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       const bool do_a = !p.gather && (pidx & 1) == 0, do_b = p.gather || (pidx & 1) == 1;
       const int nchains = p.gather ? 1 : 2, chain = p.gather ? 0 : pidx >> 1;
       const int PQ = p.P * p.Q;
-      if (do_b && p.b_res) {
+      if (pidx == 4) {
+        // residual tiles for the tensor-core add, double-buffered by tile parity
+        const int res_buf = BM * p.bn;
+        int it = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x, it++) {
+          const int b = it & 1;
+          mbar_wait(&rempty[b], ((it >> 1) & 1) ^ 1);
+          const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * p.bn;
+          const int halves = min(p.bn, p.N - n0 + 127) / 128;
+          if (issuer) {
+            mbar_expect_tx(&rfull[b], BM * 128 * halves);
+            for (int hh = 0; hh < halves; hh++)
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+                  "[%2];" ::"r"(smem_u32(base + p.res_off + b * res_buf + hh * 16384)),
+                  "l"(reinterpret_cast<std::uint64_t>(&rmap)), "r"(smem_u32(&rfull[b])), "r"(n0 + hh * 128), "r"(m0)
+                  : "memory");
+          }
+          __syncwarp();
+        }
+      } else if (do_b && p.b_res) {
         // the whole filter once (tiles_n == 1), then this producer is done
         if (chain == 0 && issuer) {
           mbar_expect_tx(bfull, p.kblocks * stage_b);
@@ -353,6 +390,23 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
           stage = 0;
           phase ^= 1;
         }
+      }
+      if (p.res_mma) {
+        // + residual: D[:, 128 hh + n] += R[:, 128 hh + k] * I[n, k], four K = 32 steps per half
+        mbar_wait(&rfull[acc], (iter >> 1) & 1);
+        tc_fence_after();
+        const int halves = min(p.bn, nrem + 127) / 128;
+        const std::uint32_t hi128 = (1024u >> 4) | (1u << 14) | (2u << 29);
+        const std::uint32_t id128 = (p.idesc & ~(0x3Fu << 17)) | ((128u >> 3) << 17);
+        const std::uint32_t ra = smem_u32(base + p.res_off + acc * BM * p.bn), ib = smem_u32(base + p.ident_off);
+        for (int hh = 0; hh < halves; hh++)
+#pragma unroll
+          for (int ks = 0; ks < 4; ks++)
+            if (issuer)
+              umma_i8(d + 128 * hh, (((ra + hh * 16384) >> 4) | (1u << 16)) + ks * 2, hi128, ((ib >> 4) | (1u << 16)) + ks * 2,
+                      hi128, id128, 1);
+        if (issuer) umma_commit(&rempty[acc]);
+        __syncwarp();
       }
       if (issuer) umma_commit(&tfull[acc]);
       __syncwarp();
@@ -510,7 +564,8 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
     }
     if (p.epi_vec)  // zero tail: chunk loads past N need no bounds select
       for (int k = p.N + threadIdx.x - 64; k < (p.N + p.bn - 1) / p.bn * p.bn && k < kMaxVecK; k += ethreads) vec_s[k] = 0;
-    if (p.epi_res && leader && p.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
+    const bool eres = p.epi_res && !p.res_mma;  // residual read by the epilogue (else added by the MMAs)
+    if (eres && leader && p.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("bar.sync 1, %0;" ::"r"(ethreads) : "memory");
     const bool fast8 = p.fast8 && !(p.epi_lo && *reinterpret_cast<volatile int*>(bars + 41));
     const std::int32_t lo8 = p.epi_lo ? static_cast<std::int32_t>(p.lo) : INT_MIN;
@@ -530,24 +585,24 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
             : "memory");
     };
     const int g0 = split ? hgroup : 0, tstep = split ? 2 * static_cast<int>(gridDim.x) : static_cast<int>(gridDim.x);
-    if (p.epi_res && leader && static_cast<int>(blockIdx.x) + g0 * static_cast<int>(gridDim.x) < tiles)
+    if (eres && leader && static_cast<int>(blockIdx.x) + g0 * static_cast<int>(gridDim.x) < tiles)
       load_res(blockIdx.x + g0 * gridDim.x, g0);
     int iter = g0;
     for (int t = blockIdx.x + g0 * gridDim.x; t < tiles; t += tstep, iter += split ? 2 : 1) {
       const int acc = iter & 1;
       const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * p.bn;
-      if (p.tma_out || p.epi_res) {
+      if (p.tma_out || eres) {
         // i32 staging is single-buffered, i8 staging double-buffered (one buffer per group when split)
         if (leader && (p.tma_out == 1 || (split && p.tma_out == 2)))
           asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         if (leader && !split && p.tma_out == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         asm volatile("bar.sync %0, %1;" ::"r"(gbar), "r"(gthreads) : "memory");  // staging and the older residual buffer are free
       }
-      if (!split && p.epi_res && leader && t + static_cast<int>(gridDim.x) < tiles) load_res(t + gridDim.x, (iter + 1) & 1);
+      if (!split && eres && leader && t + static_cast<int>(gridDim.x) < tiles) load_res(t + gridDim.x, (iter + 1) & 1);
       mbar_wait(&tfull[acc], (iter >> 1) & 1);
       tc_fence_after();
       if (leader) TILE_STAMP(3, iter);
-      if (p.epi_res) mbar_wait(&rfull[iter & 1], (iter >> 1) & 1);
+      if (eres) mbar_wait(&rfull[iter & 1], (iter >> 1) & 1);
       std::uint8_t* rcur = rstg + (iter & 1) * res_buf;
       std::uint8_t* scur = p.tma_out == 2 ? stg + (iter & 1) * stg_buf : stg;
       const int m = m0 + row;
@@ -576,7 +631,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
               bv[4 * q] = bv[4 * q + 1] = bv[4 * q + 2] = bv[4 * q + 3] = 0;
           }
           std::uint32_t w[8];
-          if (p.epi_res) {
+          if (eres) {
             std::uint32_t rw[8];
             const std::uint32_t rrow = smem_u32(rcur + (h >> 2) * 16384 + row * 128);
 #pragma unroll
@@ -620,7 +675,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
               bv[4 * q] = bv[4 * q + 1] = bv[4 * q + 2] = bv[4 * q + 3] = 0;
           }
           std::uint32_t rw[8];
-          if (p.epi_res) {
+          if (eres) {
             const std::uint32_t rrow = smem_u32(rcur + (h >> 2) * 16384 + row * 128);
 #pragma unroll
             for (int u = 0; u < 2; u++)
@@ -632,7 +687,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
             // no clamp: only the wrapped low bits reach the store
 #pragma unroll
             for (int q = 0; q < 32; q++) {
-              const std::uint32_t r = p.epi_res ? static_cast<std::uint32_t>(
+              const std::uint32_t r = eres ? static_cast<std::uint32_t>(
                                                       static_cast<std::int32_t>(static_cast<std::int8_t>(rw[q >> 2] >> (8 * (q & 3)))))
                                                 : 0u;
               v[q] = v[q] + static_cast<std::uint32_t>(bv[q]) + r;
@@ -647,7 +702,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
             const std::uint32_t lo32 = static_cast<std::uint32_t>(p.lo);
 #pragma unroll
             for (int q = 0; q < 32; q++) {
-              const std::int32_t r = p.epi_res ? static_cast<std::int32_t>(static_cast<std::int8_t>(rw[q >> 2] >> (8 * (q & 3))))
+              const std::int32_t r = eres ? static_cast<std::int32_t>(static_cast<std::int8_t>(rw[q >> 2] >> (8 * (q & 3))))
                                                : 0;
               const std::int32_t ar = static_cast<std::int32_t>(v[q]) + r;
               v[q] = ar >= tv[q] ? static_cast<std::uint32_t>(ar) + static_cast<std::uint32_t>(bv[q]) : lo32;
@@ -656,7 +711,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
             // exact x = acc + vec (+ res) as a 64-bit (hi:lo) carry chain; ReLU keeps lo iff hi >= 0
 #pragma unroll
             for (int q = 0; q < 32; q++) {
-              const std::uint32_t r = p.epi_res ? static_cast<std::uint32_t>(
+              const std::uint32_t r = eres ? static_cast<std::uint32_t>(
                                                       static_cast<std::int32_t>(static_cast<std::int8_t>(rw[q >> 2] >> (8 * (q & 3)))))
                                                 : 0u;
               std::uint32_t lo32;
@@ -677,7 +732,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
 #pragma unroll
             for (int q = 0; q < 32; q++) {
               long long x = static_cast<long long>(static_cast<std::int32_t>(v[q])) + bv[q];
-              if (p.epi_res) x += static_cast<std::int8_t>(rw[q >> 2] >> (8 * (q & 3)));
+              if (eres) x += static_cast<std::int8_t>(rw[q >> 2] >> (8 * (q & 3)));
               v[q] = static_cast<std::uint32_t>(x < lo ? lo : x);
             }
           }
@@ -725,7 +780,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("bar.sync %0, %1;" ::"r"(gbar), "r"(gthreads) : "memory");
         // split: the group's residual buffer is free again -> prefetch its next tile's
-        if (split && p.epi_res && leader && t + tstep < tiles) load_res(t + tstep, g0);
+        if (split && eres && leader && t + tstep < tiles) load_res(t + tstep, g0);
       }
       if (p.tma_out) {
         if (leader) {
@@ -902,13 +957,14 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     const int res = kp.epi_res ? 2 * BM * bn : 0;
     const int vec = kp.fast_clamp ? 2 * kVecBytes : kp.epi_vec ? kVecBytes : 0;
     const int tab = kp.gather ? (kp.kblocks * kp.bk * 6 + 15) / 16 * 16 : 0;
+    const int ident = kp.res_mma ? 16384 : 0;
     // the filter stays resident when there is one n-tile and it is small (<= 96 KB)
     kp.bn_box = kp.N <= 64 ? 64 : bn;
     const int bres = kp.tiles_n == 1 && kp.kblocks * kp.bn_box * g.bk <= 96 * 1024 && !std::getenv("SB_IG_NOBRES")
                          ? kp.kblocks * kp.bn_box * g.bk : 0;
     kp.b_res = bres ? 1 : 0;
     const int kstage = (BM + (bres ? 0 : kp.bn_box)) * g.bk;  // one k-block's A (+ B)
-    const int avail = std::min(kRingBytes, kSmemMax - 1024 - 512 - stg - res - vec - tab - bres);
+    const int avail = std::min(kRingBytes, kSmemMax - 1024 - 512 - stg - res - vec - tab - bres - ident);
     // k-blocks per stage: up to 4 while three stages still fit (gather mode: 1)
     kp.kpb = 1;
     if (!kp.gather && !std::getenv("SB_IG_KPB1"))
@@ -926,12 +982,15 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     ring += bres;
     kp.stg_off = ring;
     kp.res_off = ring + stg;
+    kp.ident_off = ring + stg + res;
+    ring += ident;
     kp.vec_off = ring + stg + res;
     kp.tab_off = ring + stg + res + vec;
     kp.bar_off = kp.tab_off + tab;
     kp.smem = 1024 + kp.bar_off + 512;
     return true;
   };
+  kp.res_mma = kp.epi_res && !kp.gather && kp.epi_split && !std::getenv("SB_IG_RESEPI") ? 1 : 0;
   // 256-wide tiles (N = 256 MMAs: half the instructions and A re-reads) for wide outputs
   const bool wide = kp.epi_split && kp.N >= 256 && cp.K <= kMaxVecK && !std::getenv("SB_IG_BN128");
   if (!(wide && layout(256)) && !layout(128)) return cudaErrorNotSupported;
@@ -1299,7 +1358,7 @@ cudaError_t launch_conv_igemm(const ConvPlan& cp, const ConvArgs& args, cudaStre
   const int tiles = kp.tiles_m * kp.tiles_n;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(tiles < num_sms ? tiles : num_sms));
-  cfg.blockDim = dim3(64 + 32 * kp.epi_warps + (kp.gather ? 256 : 96));
+  cfg.blockDim = dim3(64 + 32 * kp.epi_warps + (kp.gather ? 256 : 96 + (kp.res_mma ? 32 : 0)));
   cfg.dynamicSmemBytes = static_cast<unsigned>(kp.smem);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
