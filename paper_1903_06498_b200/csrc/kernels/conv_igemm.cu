@@ -93,6 +93,7 @@ struct IgKParams {
   std::uint32_t idesc, desc_hi;
   int pdl;
   long long* trace;  // SB_TILE_TRACE builds only: per-tile clock64 stamps of CTA 0
+  int exp;           // SB_TILE_TRACE builds only: SB_IG_EXP knock-out bits (experiments)
   // fused epilogue: out = wrap(max(acc + vec[k], lo))
   int epi, epi_vec, epi_lo, epi_res, vec_kind;
   int fast_clamp;  // |acc| + 128 < 2^31: clamp decided by an int32 compare against lo - vec[k]
@@ -177,6 +178,18 @@ __device__ __forceinline__ void tmem_ld32(std::uint32_t taddr, std::uint32_t (&v
         "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// One ring stage's MMAs, fully unrolled (compile-time KPB k-blocks x KS 32-byte k-steps):
+// descriptors advance by constants, so the issue is a straight run of uniform adds + UTCIMMA.
+template <int KPB, int KS>
+__device__ __forceinline__ void issue_stage(std::uint32_t d, std::uint32_t a0, std::uint32_t a_step, std::uint32_t b0,
+                                            std::uint32_t b_step, std::uint32_t hi, std::uint32_t idesc, bool first) {
+#pragma unroll
+  for (int j = 0; j < KPB; j++)
+#pragma unroll
+    for (int ks = 0; ks < KS; ks++)
+      umma_i8(d, a0 + j * a_step + ks * 2, hi, b0 + j * b_step + ks * 2, hi, idesc, (first && j == 0 && ks == 0) ? 0u : 1u);
 }
 
 __global__ void __launch_bounds__(kThreadsGather, 1)
@@ -315,13 +328,21 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
             mbar_wait(&empty[stage], phase ^ 1);
             if (issuer && pidx == 0 && kb0 == 0)
               TILE_STAMP(0, (t - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x));
+#ifdef SB_TILE_TRACE
+            if (issuer && do_a && (p.exp & 1)) mbar_arrive(&full[stage]);
+            else
+#endif
             if (issuer && do_a) mbar_expect_tx(&full[stage], p.kpb * stage_a);
             if (issuer && do_b && !p.b_res) mbar_expect_tx(&full[stage], p.kpb * stage_b);
           }
           const std::uint32_t sa = smem_u32(ring + stage * sstride);
           for (int j = 0; j < p.kpb; j++) {
             const int kb = kb0 + j;
-            if (issuer && mine && do_a)
+            if (issuer && mine && do_a
+#ifdef SB_TILE_TRACE
+                && !(p.exp & 1)
+#endif
+            )
               tma_load_im2col(sa + j * stage_a, &amap, &full[stage], cb * p.bk, w0, h0, img,
                               static_cast<std::uint16_t>(s), static_cast<std::uint16_t>(r));
             if (issuer && mine && do_b && !p.b_res) {
@@ -373,15 +394,24 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
         tc_fence_after();
         if (issuer) STAGE_STAMP(iter, kb0 / p.kpb, 1);
         const std::uint32_t sa = smem_u32(ring + stage * sstride);
-        for (int j = 0; j < p.kpb; j++) {
-          const int kb = kb0 + j;
-          const std::uint32_t a_lo = ((sa + j * stage_a) >> 4) | (1u << 16);
-          const std::uint32_t b_lo =
-              ((p.b_res ? smem_u32(bres + kb * stage_b) : sa + p.kpb * stage_a + j * stage_b) >> 4) | (1u << 16);
-#pragma unroll
-          for (int ks = 0; ks < 4; ks++)  // +32 bytes along the K-major rows
-            if (ks < ksteps && issuer)
-              umma_i8(d, a_lo + ks * 2, p.desc_hi, b_lo + ks * 2, p.desc_hi, idesc, (kb | ks) != 0);
+        const std::uint32_t a0 = (sa >> 4) | (1u << 16);
+        const std::uint32_t b0 = ((p.b_res ? smem_u32(bres + kb0 * stage_b) : sa + p.kpb * stage_a) >> 4) | (1u << 16);
+        const std::uint32_t as = stage_a >> 4, bs = stage_b >> 4, hi = p.desc_hi;
+        const bool first = kb0 == 0;
+#ifdef SB_TILE_TRACE
+        if (!(p.exp & 2))
+#endif
+        if (issuer) {
+          switch (p.kpb * 8 + ksteps) {
+            case 1 * 8 + 2: issue_stage<1, 2>(d, a0, as, b0, bs, hi, idesc, first); break;
+            case 1 * 8 + 4: issue_stage<1, 4>(d, a0, as, b0, bs, hi, idesc, first); break;
+            case 2 * 8 + 2: issue_stage<2, 2>(d, a0, as, b0, bs, hi, idesc, first); break;
+            case 2 * 8 + 4: issue_stage<2, 4>(d, a0, as, b0, bs, hi, idesc, first); break;
+            case 3 * 8 + 2: issue_stage<3, 2>(d, a0, as, b0, bs, hi, idesc, first); break;
+            case 3 * 8 + 4: issue_stage<3, 4>(d, a0, as, b0, bs, hi, idesc, first); break;
+            case 4 * 8 + 2: issue_stage<4, 2>(d, a0, as, b0, bs, hi, idesc, first); break;
+            default: issue_stage<4, 4>(d, a0, as, b0, bs, hi, idesc, first); break;
+          }
         }
         if (issuer) STAGE_STAMP(iter, kb0 / p.kpb, 2);
         if (issuer) umma_commit(&empty[stage]);
@@ -591,6 +621,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
     for (int t = blockIdx.x + g0 * gridDim.x; t < tiles; t += tstep, iter += split ? 2 : 1) {
       const int acc = iter & 1;
       const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * p.bn;
+      if (leader) TILE_STAMP(8, iter);
       if (p.tma_out || eres) {
         // i32 staging is single-buffered, i8 staging double-buffered (one buffer per group when split)
         if (leader && (p.tma_out == 1 || (split && p.tma_out == 2)))
@@ -613,6 +644,11 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       const int c_hi = split || hgroups == 1 ? nch : ((hgroup + 1) * nch) >> 1;
       for (int h = c_lo; h < c_hi; h++) {
         std::uint32_t v[32];
+#ifdef SB_TILE_TRACE
+        if (p.exp & 4) {
+          for (int q = 0; q < 32; q++) v[q] = 0;
+        } else
+#endif
         tmem_ld32(tmem_base + (static_cast<std::uint32_t>(quarter * 32) << 16) +
                       static_cast<std::uint32_t>(acc * p.bn + h * 32),
                   v);
@@ -774,6 +810,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
           }
         }
       }
+      if (leader) TILE_STAMP(9, iter);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
       if (p.tma_out || split) {
@@ -1368,19 +1405,21 @@ cudaError_t launch_conv_igemm(const ConvPlan& cp, const ConvArgs& args, cudaStre
   cfg.numAttrs = kp.pdl ? 1 : 0;
 #ifdef SB_TILE_TRACE
   static long long* tr = nullptr;
-  if (!tr) cudaMalloc(&tr, (640 + 32 * 4 * 3) * 8);
-  cudaMemsetAsync(tr, 0, (640 + 32 * 4 * 3) * 8, s);
+  if (!tr) cudaMalloc(&tr, (640 + 32 * 4 * 3 + 256) * 8);
+  cudaMemsetAsync(tr, 0, (640 + 32 * 4 * 3 + 256) * 8, s);
   kp.trace = tr;
+  kp.exp = std::getenv("SB_IG_EXP") ? std::atoi(std::getenv("SB_IG_EXP")) : 0;
   cudaError_t e = cudaLaunchKernelEx(&cfg, conv_igemm_i8_kernel, pr->amap, pr->bmap, pr->cmap, pr->rmap, kp);
-  long long h[640 + 32 * 4 * 3];
+  long long h[640 + 32 * 4 * 3 + 256];
   cudaStreamSynchronize(s);
   cudaMemcpy(h, tr, sizeof(h), cudaMemcpyDeviceToHost);
   std::fprintf(stderr, "igemm M=%d N=%d kblocks=%d kpb=%d stages=%d b_res=%d split=%d tiles=%d\n", kp.M, kp.N, kp.kblocks,
                kp.kpb, kp.stages, kp.b_res, kp.epi_split, tiles);
   for (int i = 0; i < 128; i++)
     if (h[128 + i])
-      std::fprintf(stderr, "tile %3d prod %8lld mma0 %8lld mma1 %8lld epi0 %8lld epi1 %8lld\n", i, h[i] ? h[i] - h[128] : -1,
-                   h[128 + i] - h[128], h[256 + i] - h[128], h[384 + i] - h[128], h[512 + i] - h[128]);
+      std::fprintf(stderr, "tile %3d prod %8lld mma0 %8lld mma1 %8lld | etop %8lld epi0 %8lld math %8lld epi1 %8lld\n", i,
+                   h[i] ? h[i] - h[128] : -1, h[128 + i] - h[128], h[256 + i] - h[128], h[1024 + i] - h[128],
+                   h[384 + i] - h[128], h[1152 + i] - h[128], h[512 + i] - h[128]);
   for (int i = 0; i < 32; i++)
     for (int st = 0; st < 4; st++) {
       const long long* q = h + 640 + (i * 4 + st) * 3;
