@@ -1165,70 +1165,65 @@ __global__ void conv_pack_filter_kernel(const std::int8_t* __restrict__ b, std::
   }
 }
 
-// Folded rows T[n, U, y, q], q = b*fold_c + kf < fold_cv: the folded pixel F[n, U, y + b] of
-// kf = (di*fy + dj)*C + c, i.e. I[n, fx*U + di, fy*(y + b) + dj, c] (zero outside the
-// constraint window and on padding bytes).  Specialised: one thread per row, everything
-// unrolled (the ResNet stem is FX = FY = 2, C = 3, four 16-byte folded pixels per row).
-template <int FX, int FY, int CC, int NB>
-__global__ void __launch_bounds__(256) conv_fold_rows_fixed(const std::int8_t* __restrict__ a, uint4* __restrict__ T,
-                                                            int rows, int FU, int Q, long long a_n, long long a_x,
-                                                            long long a_y, long long a0, int u_lo, int u_hi, int v_lo,
-                                                            int v_hi) {
-  constexpr int FC = (FX * FY * CC + 15) / 16 * 16, CV = NB * FC;
-  for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < rows; row += gridDim.x * blockDim.x) {
-    const int nu = row / Q, y = row - nu * Q;
+// Folded pixels F[n, U, V, kf], kf = (di*fy + dj)*C + c: I[n, fx*U + di, fy*V + dj, c] (zero
+// outside the constraint window and on the padding bytes up to fold_c).  Specialised: one
+// thread per folded pixel, unrolled (the ResNet stem is FX = FY = 2, C = 3: 12 of 16 bytes).
+template <int FX, int FY, int CC>
+__global__ void __launch_bounds__(256) conv_fold_fixed(const std::int8_t* __restrict__ a, uint4* __restrict__ F, int pixels,
+                                                       int FU, int FV, long long a_n, long long a_x, long long a_y,
+                                                       long long a0, int u_lo, int u_hi, int v_lo, int v_hi) {
+  constexpr int FC = (FX * FY * CC + 15) / 16 * 16;
+  for (int pix = blockIdx.x * blockDim.x + threadIdx.x; pix < pixels; pix += gridDim.x * blockDim.x) {
+    const int nu = pix / FV, V = pix - nu * FV;
     const int n = nu / FU, U = nu - n * FU;
-    std::uint32_t w[CV / 4];
+    std::uint32_t w[FC / 4];
 #pragma unroll
-    for (int i = 0; i < CV / 4; i++) w[i] = 0;
+    for (int i = 0; i < FC / 4; i++) w[i] = 0;
 #pragma unroll
     for (int di = 0; di < FX; di++) {
       const int u = FX * U + di;
       const bool uok = u >= u_lo && u <= u_hi;
       const std::int8_t* rp = a + a0 + a_n * n + a_x * u;
 #pragma unroll
-      for (int b = 0; b < NB; b++)
+      for (int dj = 0; dj < FY; dj++) {
+        const int v = FY * V + dj;
+        if (uok && v >= v_lo && v <= v_hi) {
 #pragma unroll
-        for (int dj = 0; dj < FY; dj++) {
-          const int v = FY * (y + b) + dj;
-          if (uok && v >= v_lo && v <= v_hi) {
-#pragma unroll
-            for (int c = 0; c < CC; c++) {
-              const int q = b * FC + (di * FY + dj) * CC + c;
-              w[q / 4] |= static_cast<std::uint32_t>(static_cast<std::uint8_t>(__ldg(rp + a_y * v + c))) << (8 * (q % 4));
-            }
+          for (int c = 0; c < CC; c++) {
+            const int q = (di * FY + dj) * CC + c;
+            w[q / 4] |= static_cast<std::uint32_t>(static_cast<std::uint8_t>(__ldg(rp + a_y * v + c))) << (8 * (q % 4));
           }
         }
+      }
     }
 #pragma unroll
-    for (int i = 0; i < CV / 16; i++)
-      T[static_cast<long long>(row) * (CV / 16) + i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+    for (int i = 0; i < FC / 16; i++)
+      F[static_cast<long long>(pix) * (FC / 16) + i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
   }
 }
 
-// Any fold: one thread per 4 bytes of a row, per-byte (du, dv, c) from a shared table.
-__global__ void __launch_bounds__(256) conv_fold_rows(const std::int8_t* __restrict__ a, std::uint32_t* __restrict__ T,
-                                                      long long words, int FU, int Q, int CVW, int fx, int fy, int C,
-                                                      int fc, long long a_n, long long a_x, long long a_y, long long a0,
-                                                      int u_lo, int u_hi, int v_lo, int v_hi) {
-  __shared__ int tab[1024];  // du | c << 8 | dv << 16, or -1
-  const int cv = 4 * CVW, fyc = fy * C;
-  for (int q = threadIdx.x; q < cv; q += blockDim.x) {
-    const int b = q / fc, kf = q - b * fc;
+// Any fold: one thread per 4 bytes of a folded pixel, per-byte (di, dj, c) from a shared table.
+__global__ void __launch_bounds__(256) conv_fold_any(const std::int8_t* __restrict__ a, std::uint32_t* __restrict__ F,
+                                                     long long words, int FU, int FV, int FCW, int fx, int fy, int C,
+                                                     long long a_n, long long a_x, long long a_y, long long a0, int u_lo,
+                                                     int u_hi, int v_lo, int v_hi) {
+  __shared__ int tab[1024];  // di | c << 8 | dj << 16, or -1
+  const int fc = 4 * FCW, fyc = fy * C;
+  for (int q = threadIdx.x; q < fc; q += blockDim.x) {
     int e = -1;
-    if (kf < fx * fyc) {
-      const int di = kf / fyc, r = kf - di * fyc, dj = r / C, c = r - dj * C;
-      e = di | (c << 8) | ((fy * b + dj) << 16);
+    if (q < fx * fyc) {
+      const int di = q / fyc, r = q - di * fyc, dj = r / C, c = r - dj * C;
+      e = di | (c << 8) | (dj << 16);
     }
     tab[q] = e;
   }
   __syncthreads();
   for (long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; g < words;
        g += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long row = g / CVW;
-    const int wi = static_cast<int>(g - row * CVW);
-    const long long nu = row / Q;
-    const int y = static_cast<int>(row - nu * Q);
+    const long long pix = g / FCW;
+    const int wi = static_cast<int>(g - pix * FCW);
+    const long long nu = pix / FV;
+    const int V = static_cast<int>(pix - nu * FV);
     const long long n = nu / FU;
     const int U = static_cast<int>(nu - n * FU);
     std::uint32_t word = 0;
@@ -1236,13 +1231,13 @@ __global__ void __launch_bounds__(256) conv_fold_rows(const std::int8_t* __restr
     for (int e = 0; e < 4; e++) {
       const int t = tab[4 * wi + e];
       if (t >= 0) {
-        const int u = fx * U + (t & 0xFF), v = fy * y + (t >> 16), c = (t >> 8) & 0xFF;
+        const int u = fx * U + (t & 0xFF), v = fy * V + (t >> 16), c = (t >> 8) & 0xFF;
         if (u >= u_lo && u <= u_hi && v >= v_lo && v <= v_hi)
           word |= static_cast<std::uint32_t>(static_cast<std::uint8_t>(__ldg(a + a0 + a_n * n + a_x * u + a_y * v + c)))
                   << (8 * e);
       }
     }
-    T[g] = word;
+    F[g] = word;
   }
 }
 
@@ -1268,28 +1263,27 @@ __global__ void conv_fold_filter_kernel(const std::int8_t* __restrict__ b, std::
 }  // namespace
 
 cudaError_t launch_conv_fold(const ConvPlan& cp, const void* a, void* f, cudaStream_t s) {
-  const long long rows = cp.N * cp.fold_u * cp.W;
+  const long long pixels = cp.N * cp.fold_u * cp.fold_v;
   const auto* in = static_cast<const std::int8_t*>(a);
   const int lo_u = static_cast<int>(cp.u_lo), hi_u = static_cast<int>(cp.u_hi);
   const int lo_v = static_cast<int>(cp.v_lo), hi_v = static_cast<int>(cp.v_hi);
-  const int blocks_rows = static_cast<int>(std::min<long long>((rows + 255) / 256, 148 * 32));
-  const int nb = cp.fold_cv % cp.fold_c == 0 ? static_cast<int>(cp.fold_cv / cp.fold_c) : 0;
-  if (cp.fold_x == 2 && cp.fold_y == 2 && cp.C == 3 && nb == 4 && cp.fold_c == 16) {
-    conv_fold_rows_fixed<2, 2, 3, 4><<<blocks_rows, 256, 0, s>>>(in, static_cast<uint4*>(f), static_cast<int>(rows),
-                                                                 static_cast<int>(cp.fold_u), static_cast<int>(cp.W),
-                                                                 cp.a_n, cp.a_x, cp.a_y, cp.a0, lo_u, hi_u, lo_v, hi_v);
-  } else if (cp.fold_x == 1 && cp.fold_y == 1 && cp.C == 3 && nb == 4 && cp.fold_c == 16) {
-    conv_fold_rows_fixed<1, 1, 3, 4><<<blocks_rows, 256, 0, s>>>(in, static_cast<uint4*>(f), static_cast<int>(rows),
-                                                                 static_cast<int>(cp.fold_u), static_cast<int>(cp.W),
-                                                                 cp.a_n, cp.a_x, cp.a_y, cp.a0, lo_u, hi_u, lo_v, hi_v);
+  const int blocks = static_cast<int>(std::min<long long>((pixels + 255) / 256, 148 * 32));
+  if (cp.fold_x == 2 && cp.fold_y == 2 && cp.C == 3 && cp.fold_c == 16) {
+    conv_fold_fixed<2, 2, 3><<<blocks, 256, 0, s>>>(in, static_cast<uint4*>(f), static_cast<int>(pixels),
+                                                    static_cast<int>(cp.fold_u), static_cast<int>(cp.fold_v), cp.a_n,
+                                                    cp.a_x, cp.a_y, cp.a0, lo_u, hi_u, lo_v, hi_v);
+  } else if (cp.fold_x == 1 && cp.fold_y == 1 && cp.C == 3 && cp.fold_c == 16) {
+    conv_fold_fixed<1, 1, 3><<<blocks, 256, 0, s>>>(in, static_cast<uint4*>(f), static_cast<int>(pixels),
+                                                    static_cast<int>(cp.fold_u), static_cast<int>(cp.fold_v), cp.a_n,
+                                                    cp.a_x, cp.a_y, cp.a0, lo_u, hi_u, lo_v, hi_v);
   } else {
-    const int CVW = static_cast<int>(cp.fold_cv / 4);
-    const long long words = rows * CVW;
-    const long long blocks = std::min<long long>((words + 255) / 256, 148 * 32);
-    conv_fold_rows<<<static_cast<int>(blocks), 256, 0, s>>>(
-        in, static_cast<std::uint32_t*>(f), words, static_cast<int>(cp.fold_u), static_cast<int>(cp.W), CVW,
-        static_cast<int>(cp.fold_x), static_cast<int>(cp.fold_y), static_cast<int>(cp.C), static_cast<int>(cp.fold_c),
-        cp.a_n, cp.a_x, cp.a_y, cp.a0, lo_u, hi_u, lo_v, hi_v);
+    const int FCW = static_cast<int>(cp.fold_c / 4);
+    const long long words = pixels * FCW;
+    const long long wblocks = std::min<long long>((words + 255) / 256, 148 * 32);
+    conv_fold_any<<<static_cast<int>(wblocks), 256, 0, s>>>(
+        in, static_cast<std::uint32_t*>(f), words, static_cast<int>(cp.fold_u), static_cast<int>(cp.fold_v), FCW,
+        static_cast<int>(cp.fold_x), static_cast<int>(cp.fold_y), static_cast<int>(cp.C), cp.a_n, cp.a_x, cp.a_y, cp.a0,
+        lo_u, hi_u, lo_v, hi_v);
   }
   return cudaGetLastError();
 }
@@ -1339,7 +1333,7 @@ const char* conv_igemm_unsupported(const ConvPlan& cp) {
         cp.fold_x * cp.fold_y * cp.C > cp.fold_c || cp.fold_s * cp.fold_c > cp.fold_cv ||
         cp.fold_u < cp.H + cp.fold_r - 1 || (cp.fold_v - cp.W + 1) * cp.fold_c < cp.fold_cv)
       return "inconsistent phase fold";
-    if (cp.N * cp.fold_u * cp.W >= (1ll << 31) || cp.fold_cv > 1024 || cp.fold_r > 127 || cp.C > 255)
+    if (cp.N * cp.fold_u * cp.fold_v >= (1ll << 31) || cp.fold_c > 1024 || cp.fold_r > 127 || cp.C > 255)
       return "folded input too large";
     return conv_igemm_unsupported(packed_view(cp));
   }

@@ -773,15 +773,16 @@ ConvPlan packed_view(const ConvPlan& c) {
   v.a_buf = c.pack_a;
   v.b_buf = c.pack_b;
   if (c.fold_x) {
-    // out[x, y] = sum_{a, q} T[x + a, y, q] * G[a, k, q]: "pixel" (U, y) of the view is the
-    // fold_cv-byte row T[n, U, y] = folded pixels (U, y .. y + fold_cv / fold_c - 1)
+    // out[x, y] = sum_{a, q} F[x + a, y + q / fold_c, q % fold_c] * G[a, k, q]: "pixel" (U, y)
+    // of the view is the fold_cv bytes starting at folded pixel (U, y), so consecutive view
+    // pixels overlap (pixel stride fold_c < fold_cv; TMA im2col reads them as rows)
     v.C = c.fold_cv;
     v.R = c.fold_r;
     v.S = 1;
     v.sx = v.sy = 1;
-    v.a_y = c.fold_cv;
-    v.a_x = c.W * c.fold_cv;
-    v.a_n = c.fold_u * c.W * c.fold_cv;
+    v.a_y = c.fold_c;
+    v.a_x = c.fold_v * c.fold_c;
+    v.a_n = c.fold_u * c.fold_v * c.fold_c;
     v.a0 = 0;
     v.u_lo = 0;
     v.u_hi = c.fold_u - 1;
@@ -838,7 +839,7 @@ bool try_packed_conv(Plan* plan, ConvPlan* cp) {
     c.pack_k = c.fold_r * c.fold_cv;
     c.pack_a = static_cast<int>(plan->bufs.size());
     c.pack_b = c.pack_a + 1;
-    const std::int64_t folded = c.N * c.fold_u * c.W * c.fold_cv;
+    const std::int64_t folded = c.N * c.fold_u * c.fold_v * c.fold_c;
     if (c.pack_k <= 1024 && folded < (1ll << 34) && !conv_igemm_unsupported(c)) {
       PBuffer f;
       f.name = "fold:" + plan->bufs[c.a_buf].name;

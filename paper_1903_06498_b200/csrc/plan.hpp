@@ -151,11 +151,11 @@ struct ConvPlan {
   int pack_a = -1, pack_b = -1;
   std::int64_t pack_k = 0;
   std::int64_t pack_run = 0;  // >0: kk = i * pack_run + (j * C + c) (contiguous S*C-byte runs per tap row)
-  // phase fold (fold_x/fold_y > 0, pack_a = the folded rows): the strided small-channel conv
+  // phase fold (fold_x/fold_y > 0, pack_a = the folded input): the strided small-channel conv
   // becomes a stride-1 valid conv over folded pixels F[n, U, V, (di, dj, c)] =
-  // I[n, sx*U + di, sy*V + dj, c] (zero outside the constraint window; fold_c bytes each),
-  // materialised as rows T[n, U, y] = F[n, U, y .. y + fold_cv / fold_c - 1] of fold_cv bytes:
-  // fold_r tap rows of one fold_cv-byte "pixel" each (see packed_view())
+  // I[n, sx*U + di, sy*V + dj, c] (zero outside the constraint window; fold_c bytes each,
+  // fold_u x fold_v of them per image): fold_r tap rows of one fold_cv-byte "pixel" each,
+  // the fold_cv / fold_c folded pixels from (U, y) on (see packed_view())
   std::int64_t fold_x = 0, fold_y = 0, fold_c = 0, fold_r = 0, fold_s = 0, fold_cv = 0, fold_u = 0, fold_v = 0;
 };
 
