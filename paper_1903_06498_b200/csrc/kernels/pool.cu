@@ -20,6 +20,8 @@ struct PoolArgs {
   long long a_n, a_x, a_y, a0;  // bytes
   long long o_n, o_x, o_y, o0;  // bytes
   int u_lo, u_hi, v_lo, v_hi;
+  int fresh;           // start from init (the elided fill) instead of reading the output
+  std::uint32_t init;  // fill value replicated over the 4-byte lane word
 };
 
 template <int KIND, bool MAX>
@@ -30,20 +32,21 @@ __device__ __forceinline__ std::uint32_t fold(std::uint32_t a, std::uint32_t b) 
   return static_cast<std::uint32_t>(MAX ? (x < y ? y : x) : (y < x ? y : x));
 }
 
-template <int KIND, bool MAX>
+template <int KIND, bool MAX, typename IDX>
 __global__ void __launch_bounds__(256) pool_kernel(const std::uint8_t* __restrict__ in, std::uint8_t* __restrict__ out,
                                                    const PoolArgs p) {
-  const long long total = p.N * p.H * p.W * p.CV;
-  for (long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; g < total;
-       g += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long cv = g % p.CV;
-    long long pix = g / p.CV;
-    const int y = static_cast<int>(pix % p.W);
-    pix /= p.W;
-    const int x = static_cast<int>(pix % p.H);
-    const long long n = pix / p.H;
+  // IDX = int when the index space fits (32-bit division is several times cheaper)
+  const IDX total = static_cast<IDX>(p.N * p.H * p.W * p.CV);
+  const IDX CV = static_cast<IDX>(p.CV), W = static_cast<IDX>(p.W), H = static_cast<IDX>(p.H);
+  for (IDX g = blockIdx.x * static_cast<IDX>(blockDim.x) + threadIdx.x; g < total;
+       g += static_cast<IDX>(gridDim.x) * blockDim.x) {
+    const IDX pix0 = g / CV, cv = g - pix0 * CV;
+    const IDX pix1 = pix0 / W;
+    const int y = static_cast<int>(pix0 - pix1 * W);
+    const IDX n = pix1 / H;
+    const int x = static_cast<int>(pix1 - n * H);
     uint4* o = reinterpret_cast<uint4*>(out + p.o0 + p.o_n * n + p.o_x * x + p.o_y * y + cv * 16);
-    uint4 acc = *o;
+    uint4 acc = p.fresh ? make_uint4(p.init, p.init, p.init, p.init) : *o;
     const std::uint8_t* ib = in + p.a0 + p.a_n * n + cv * 16;
     const int u0 = p.sx * x, v0 = p.sy * y;
     for (int i = 0; i < p.R; i++) {
@@ -102,16 +105,26 @@ cudaError_t launch_pool(const PoolPlan& pp, const void* in, void* out, cudaStrea
   a.u_hi = static_cast<int>(pp.u_hi);
   a.v_lo = static_cast<int>(pp.v_lo);
   a.v_hi = static_cast<int>(pp.v_hi);
+  a.fresh = pp.fresh ? 1 : 0;
+  {
+    const std::uint32_t v = static_cast<std::uint32_t>(pp.fill_value);
+    a.init = es == 1 ? (v & 0xFFu) * 0x01010101u : es == 2 ? (v & 0xFFFFu) * 0x00010001u : v;
+  }
   const long long total = a.N * a.H * a.W * a.CV;
   const int grid = static_cast<int>(std::max<long long>(1, std::min<long long>((total + 255) / 256, 148 * 16)));
   const auto* i = static_cast<const std::uint8_t*>(in);
   auto* o = static_cast<std::uint8_t*>(out);
   const bool mx = pp.agg == static_cast<int>(Agg::Max);
+  const bool small = total < (1ll << 31) - 148ll * 16 * 256;
+#define SB_POOL(K, M)                                                                      \
+  (small ? pool_kernel<K, M, int><<<grid, 256, 0, s>>>(i, o, a)                           \
+         : pool_kernel<K, M, long long><<<grid, 256, 0, s>>>(i, o, a))
   switch (pp.kind) {
-    case kI8: mx ? pool_kernel<kI8, true><<<grid, 256, 0, s>>>(i, o, a) : pool_kernel<kI8, false><<<grid, 256, 0, s>>>(i, o, a); break;
-    case kI16: mx ? pool_kernel<kI16, true><<<grid, 256, 0, s>>>(i, o, a) : pool_kernel<kI16, false><<<grid, 256, 0, s>>>(i, o, a); break;
-    default: mx ? pool_kernel<kI32, true><<<grid, 256, 0, s>>>(i, o, a) : pool_kernel<kI32, false><<<grid, 256, 0, s>>>(i, o, a); break;
+    case kI8: mx ? SB_POOL(kI8, true) : SB_POOL(kI8, false); break;
+    case kI16: mx ? SB_POOL(kI16, true) : SB_POOL(kI16, false); break;
+    default: mx ? SB_POOL(kI32, true) : SB_POOL(kI32, false); break;
   }
+#undef SB_POOL
   return cudaGetLastError();
 }
 

@@ -956,6 +956,34 @@ void elide_dead_fills(Plan* plan) {
   }
 }
 
+// A pool whose output is a local touched only by an earlier fill: the pool writes every
+// element exactly once, so it can start from the fill value and the fill goes.
+void fresh_pool_output(Plan* plan, std::size_t s) {
+  PoolPlan& pp = plan->steps[s].launch.pool;
+  const PBuffer& ob = plan->bufs[pp.out_buf];
+  if (ob.root || pp.out_buf == pp.in_buf) return;
+  const bool covers = pp.o0 == 0 && pp.o_y == pp.C && (pp.H == 1 || pp.o_x == pp.W * pp.C) &&
+                      (pp.N == 1 || pp.o_n == pp.H * pp.W * pp.C) && pp.N * pp.H * pp.W * pp.C == ob.elements;
+  if (!covers) return;
+  int fill = -1;
+  for (std::size_t k = 0; k < s; k++) {
+    const PStep& ps = plan->steps[k];
+    if (ps.elided) continue;
+    if (ps.kind == PStep::Fill) {
+      if (ps.buf == pp.out_buf) fill = static_cast<int>(k);
+      continue;
+    }
+    std::vector<int> rd, wr;
+    step_access(ps, &rd, &wr);
+    for (int b : rd) if (b == pp.out_buf) return;
+    for (int b : wr) if (b == pp.out_buf) return;
+  }
+  if (fill < 0) return;
+  pp.fresh = true;
+  pp.fill_value = plan->steps[fill].value;
+  plan->steps[fill].elided = true;
+}
+
 }  // namespace
 
 void match_kernels(Plan* plan, const Program& p, const PlanOptions& opt) {
@@ -1056,7 +1084,10 @@ void match_kernels(Plan* plan, const Program& p, const PlanOptions& opt) {
     if (!why.empty())
       plan->notes.push_back("launch " + st.launch.path + ": contraction kept on the generic kernel (" + why + ")");
     if (match_reduce(*plan, st.launch, p, opt, s)) st.launch.kernel = KernelKind::Reduce;
-    else if (match_pool(*plan, st.launch)) st.launch.kernel = KernelKind::Pool;
+    else if (match_pool(*plan, st.launch)) {
+      st.launch.kernel = KernelKind::Pool;
+      fresh_pool_output(plan, s);
+    }
     else if (match_map(st.launch)) st.launch.kernel = KernelKind::Map;
   }
   elide_dead_fills(plan);

@@ -75,6 +75,10 @@ struct PoolPlan {
   std::int64_t a_n = 0, a_x = 0, a_y = 0, a0 = 0;  // input: a0 + a_n*n + a_x*u + a_y*v + c, u = sx*x + i
   std::int64_t u_lo = 0, u_hi = 0, v_lo = 0, v_hi = 0;
   std::int64_t o_n = 0, o_x = 0, o_y = 0, o0 = 0;  // output: o0 + o_n*n + o_x*x + o_y*y + c
+  // the output's only earlier touch is a fill (elided): start every element from fill_value
+  // instead of reading it back
+  bool fresh = false;
+  std::int64_t fill_value = 0;
 };
 
 // tcgen05 GEMM (kernels/gemm_tc.cu): C[m,n] (+)= sum_k A[m,k] B[k,n], i8 operands.

@@ -61,7 +61,7 @@ void step_access(const PStep& s, std::vector<int>* reads, std::vector<int>* writ
       return;
     case KernelKind::Pool:
       R(l.pool.in_buf);
-      R(l.pool.out_buf);
+      if (!l.pool.fresh) R(l.pool.out_buf);
       W(l.pool.out_buf);
       return;
     default:
