@@ -32,6 +32,27 @@ __device__ __forceinline__ std::uint32_t fold(std::uint32_t a, std::uint32_t b) 
   return static_cast<std::uint32_t>(MAX ? (x < y ? y : x) : (y < x ? y : x));
 }
 
+// i8 lanes as two sign-extended s16x2 halves (even bytes | odd bytes): packed max/min of bytes
+// has no instruction, max.s16x2 does -- two prmt + two max per 4-byte word instead of the
+// ~13-instruction byte emulation
+__device__ __forceinline__ std::uint32_t sx_even(std::uint32_t w) {
+  std::uint32_t r;
+  asm("prmt.b32 %0, %1, 0, 0xA280;" : "=r"(r) : "r"(w));
+  return r;
+}
+__device__ __forceinline__ std::uint32_t sx_odd(std::uint32_t w) {
+  std::uint32_t r;
+  asm("prmt.b32 %0, %1, 0, 0xB391;" : "=r"(r) : "r"(w));
+  return r;
+}
+template <bool MAX>
+__device__ __forceinline__ std::uint32_t mm16x2(std::uint32_t a, std::uint32_t b) {
+  std::uint32_t r;
+  if (MAX) asm("max.s16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  else asm("min.s16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+
 template <int KIND, bool MAX, typename IDX>
 __global__ void __launch_bounds__(256) pool_kernel(const std::uint8_t* __restrict__ in, std::uint8_t* __restrict__ out,
                                                    const PoolArgs p) {
@@ -47,20 +68,61 @@ __global__ void __launch_bounds__(256) pool_kernel(const std::uint8_t* __restric
     const int x = static_cast<int>(pix1 - n * H);
     uint4* o = reinterpret_cast<uint4*>(out + p.o0 + p.o_n * n + p.o_x * x + p.o_y * y + cv * 16);
     uint4 acc = p.fresh ? make_uint4(p.init, p.init, p.init, p.init) : *o;
+    std::uint32_t ev[4], od[4];  // i8: the accumulator as s16x2 halves
+    if (KIND == kI8) {
+      const std::uint32_t a4[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        ev[q] = sx_even(a4[q]);
+        od[q] = sx_odd(a4[q]);
+      }
+    }
     const std::uint8_t* ib = in + p.a0 + p.a_n * n + cv * 16;
     const int u0 = p.sx * x, v0 = p.sy * y;
-    for (int i = 0; i < p.R; i++) {
-      const int u = u0 + i;
-      if (u < p.u_lo || u > p.u_hi) continue;
-      for (int j = 0; j < p.S; j++) {
-        const int v = v0 + j;
-        if (v < p.v_lo || v > p.v_hi) continue;
-        const uint4 t = __ldg(reinterpret_cast<const uint4*>(ib + p.a_x * u + p.a_y * v));
+    auto fold_tap = [&](const uint4 t) {
+      if (KIND == kI8) {
+        const std::uint32_t t4[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          ev[q] = mm16x2<MAX>(ev[q], sx_even(t4[q]));
+          od[q] = mm16x2<MAX>(od[q], sx_odd(t4[q]));
+        }
+      } else {
         acc.x = fold<KIND, MAX>(acc.x, t.x);
         acc.y = fold<KIND, MAX>(acc.y, t.y);
         acc.z = fold<KIND, MAX>(acc.z, t.z);
         acc.w = fold<KIND, MAX>(acc.w, t.w);
       }
+    };
+    if (p.R == 3 && p.S == 3) {
+      // the common 3x3 window: all nine loads in flight before the folds (memory-level parallelism)
+      uint4 t[9];
+      bool ok[9];
+#pragma unroll
+      for (int k = 0; k < 9; k++) {
+        const int u = u0 + k / 3, v = v0 + k % 3;
+        ok[k] = u >= p.u_lo && u <= p.u_hi && v >= p.v_lo && v <= p.v_hi;
+        t[k] = ok[k] ? __ldg(reinterpret_cast<const uint4*>(ib + p.a_x * u + p.a_y * v)) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int k = 0; k < 9; k++)
+        if (ok[k]) fold_tap(t[k]);
+    } else {
+      for (int i = 0; i < p.R; i++) {
+        const int u = u0 + i;
+        if (u < p.u_lo || u > p.u_hi) continue;
+        for (int j = 0; j < p.S; j++) {
+          const int v = v0 + j;
+          if (v < p.v_lo || v > p.v_hi) continue;
+          fold_tap(__ldg(reinterpret_cast<const uint4*>(ib + p.a_x * u + p.a_y * v)));
+        }
+      }
+    }
+    if (KIND == kI8) {
+      std::uint32_t r[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) r[q] = __byte_perm(ev[q], od[q], 0x6240);
+      acc = make_uint4(r[0], r[1], r[2], r[3]);
     }
     *o = acc;
   }
