@@ -142,6 +142,11 @@ __device__ __forceinline__ void umma_i8(std::uint32_t tmem_d, std::uint32_t a_lo
 constexpr std::uint32_t kDescHi = (512u >> 4) | (1u << 14) | (4u << 29);
 constexpr std::uint32_t kDescLoLbo = 1u << 16;
 
+__device__ __forceinline__ bool elect_one() {
+  std::uint32_t is;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(is));
+  return is != 0;
+}
 __device__ __forceinline__ void umma_commit(std::uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -292,8 +297,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (!filter_issued) load_filter();
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer (one thread) ----------------
+    {
+      // ---------------- MMA issuer: the converged warp, one elected lane issues ----------------
+      // (uniform control flow keeps the descriptors in uniform registers; no per-MMA waterfall)
+      const bool issuer = elect_one();
       int stage = 0;
       std::uint32_t phase = 0;
       int iter = 0;
@@ -304,17 +311,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         int acc = iter & 1;
         std::uint32_t aphase = (iter >> 1) & 1;
         mbar_wait(&tempty[acc], aphase ^ 1);
-        trace_at(p.trace, 8 + iter);
+        if (issuer) trace_at(p.trace, 8 + iter);
         tc_fence_after();
         std::uint32_t dcol = tmem_base + static_cast<std::uint32_t>(acc * p.K);
         for (int cc = 0; cc < p.chunks; cc++) {
           mbar_wait(&full[stage], phase);
-          trace_at(p.trace, 16 + iter);
+          if (issuer) trace_at(p.trace, 16 + iter);
           tc_fence_after();
           const std::uint32_t sbase = smem_u32(strips + stage * p.strip_bytes);
           const std::uint32_t bbase = fsm_addr + static_cast<std::uint32_t>(cc) * p.filt_tap_bytes;
           const std::uint32_t btap = static_cast<std::uint32_t>(p.chunks) * p.filt_tap_bytes;
-          if (p.R == 3 && p.S == 3 && !p.base_offset_mode) {
+          if (!issuer) {
+          } else if (p.R == 3 && p.S == 3 && !p.base_offset_mode) {
             const std::uint32_t a_lo0 = (sbase >> 4) | kDescLoLbo;
             const std::uint32_t b_lo0 = (bbase >> 4) | kDescLoLbo;
             const std::uint32_t prow = static_cast<std::uint32_t>(p.P) * 4;  // (P * 64) >> 4
@@ -337,14 +345,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                           kDescHi, p.idesc, (cc | i | j | s) != 0);
                 }
           }
-          umma_commit(&empty[stage]);  // smem slot free once these MMAs retire
+          if (issuer) umma_commit(&empty[stage]);  // smem slot free once these MMAs retire
+          __syncwarp();
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
-        trace_at(p.trace, 24 + iter);
+        if (issuer) umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        __syncwarp();
+        if (issuer) trace_at(p.trace, 24 + iter);
       }
     }
   } else {
