@@ -42,7 +42,7 @@
 namespace sb {
 namespace {
 
-constexpr int kThreads = 192;  // 6 warps
+constexpr int kThreads = 320;  // producer, MMA, 8 epilogue warps (two groups of 4)
 constexpr int kStages = 4;
 constexpr int kTileM = 128;
 constexpr int kMaxTrace = 160;
@@ -357,8 +357,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (issuer) trace_at(p.trace, 24 + iter);
       }
     }
-  } else {
-    // ---------------- epilogue: warps 2..5 ----------------
+  } else if (warp < 6 || (p.tma_out && p.nstg == 2 && !p.st_out)) {
+    // ---------------- epilogue: warps 2..5, or 2..9 as two groups ----------------
+    // With two staging buffers the eight warps form two independent groups of four (one
+    // per TMEM lane quarter each): group g owns accumulator g, staging buffer g, its own
+    // named barrier and store leader, and tiles blockIdx.x + g*grid, + 2*grid, ... -- the two
+    // groups' per-tile chains (TMEM drain, staging, barrier, TMA store) overlap.
+    const bool split = p.tma_out && p.nstg == 2 && !p.st_out;
+    const int eg = split ? (warp - 2) >> 2 : 0;
+    const int gbar = eg ? 3 : 1;
+    const int ethreads = split ? 256 : 128;
     const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31
     const int row = quarter * 32 + lane;
     const int xl = row / p.P;
@@ -366,13 +374,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     int iter = 0;
     if (p.epi_vec) {
       // per-output-channel vector of the fused epilogue (e.g. the bias), as int32 in smem
-      for (int k = threadIdx.x - 64; k < p.K; k += 128) {
+      for (int k = threadIdx.x - 64; k < p.K; k += ethreads) {
         long long a = p.vec_c + p.vec_k * k;
         vec_s[k] = p.vec_kind == kI8 ? static_cast<const std::int8_t*>(p.vec)[a]
                    : p.vec_kind == kI16 ? static_cast<const std::int16_t*>(p.vec)[a]
                                         : static_cast<const std::int32_t*>(p.vec)[a];
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"r"(ethreads) : "memory");
     }
     // fused epilogue on the exact s32 accumulator, int64 arithmetic, wrap at the i32 store
     auto epilogue = [&](int k, std::uint32_t acc_bits) -> std::uint32_t {
@@ -385,17 +393,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (p.tma_out) {
       // TMEM -> registers -> 128B-swizzled staging (row = TMEM lane, conflict-free) ->
       // TMA tensor stores of full lines; rows outside the image are clipped by the map.
-      const bool leader = threadIdx.x == 64;
+      const bool leader = threadIdx.x == 64 + 128 * eg;
       const int halves = p.K / 32;
-      for (int t = blockIdx.x; t < p.tiles; t += gridDim.x, iter++) {
+      const int tstep = (split ? 2 : 1) * static_cast<int>(gridDim.x);
+      iter = eg;
+      for (int t = blockIdx.x + eg * gridDim.x; t < p.tiles; t += tstep, iter += split ? 2 : 1) {
         int acc = iter & 1;
         std::uint32_t aphase = (iter >> 1) & 1;
-        int sb = p.nstg == 2 ? (iter & 1) : 0;
+        int sb = p.nstg == 2 ? (iter & 1) : 0;  // split: iter & 1 == eg, the group's own buffer
         if (leader) {
-          if (p.nstg == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          if (p.nstg == 2 && !split) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
           else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // staging buffer sb is free again
+        asm volatile("bar.sync %0, 128;" ::"r"(gbar) : "memory");  // staging buffer sb is free again
         mbar_wait(&tfull[acc], aphase);
         if (leader) trace_at(p.trace, 32 + iter);
         tc_fence_after();
@@ -478,7 +488,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           continue;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync %0, 128;" ::"r"(gbar) : "memory");
         if (leader) {
           int n = t / p.tiles_x;
           int x0 = (t % p.tiles_x) * p.TX;
