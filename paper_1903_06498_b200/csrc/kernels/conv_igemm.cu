@@ -57,7 +57,7 @@ namespace {
 
 constexpr int kThreadsGather = 448;  // + 8 warps gathering A tiles (small-channel convs), 2 per row
 constexpr int BM = 128, BN = 128;
-constexpr int kRingBytes = 128 * 1024;  // A+B stage ring
+constexpr int kRingBytes = 192 * 1024;  // A+B stage ring (cap)
 constexpr int kStgBytes = BM * BN * 4;    // output staging (i32 worst case)
 constexpr int kVecBytes = 2048 * 4;       // per-channel epilogue vector
 constexpr int kMaxVecK = 2048;

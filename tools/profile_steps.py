@@ -22,6 +22,10 @@ def main():
         text = W.conv_fused(batch, 224, 224, 3, 64, 7, 7, 2, 3)
     elif which == "l3x3":
         text = W.conv_fused(batch, 56, 56, 64, 64, 3, 3, 1, 1)
+    elif which == "s3_3x3":
+        text = W.conv_fused(batch, 14, 14, 256, 256, 3, 3, 1, 1)
+    elif which == "s3_1x1":
+        text = W.conv_fused(batch, 14, 14, 256, 1024, 1, 1, 1, 0, residual=True)
     elif which == "l1x1r":
         text = W.conv_fused(batch, 56, 56, 64, 256, 1, 1, 1, 0, residual=True)
     elif which == "l1x1":
