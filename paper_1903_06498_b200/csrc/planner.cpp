@@ -843,6 +843,13 @@ std::string Plan::describe() const {
     os << "] cons=" << l.cons.size() << " acc=" << l.acc.size() << " code=" << l.code.size()
        << " points=" << l.points;
     if (l.is_float) os << " f32";
+    if (l.kernel == KernelKind::ConvI8TC || l.kernel == KernelKind::ConvIgemmTC) {
+      const ConvPlan& c = l.conv;
+      if (c.epi)
+        os << " epilogue=" << (c.epi_vec ? "vec" : "") << (c.epi_res ? "+res" : "") << (c.epi_lo ? "+clamp" : "");
+      if (c.fresh_output) os << " fresh";
+    }
+    if (l.kernel == KernelKind::Pool && l.pool.fresh) os << " fresh";
     if (!l.why.empty()) os << " why=\"" << l.why << "\"";
     os << "\n";
   }

@@ -38,6 +38,13 @@ def test_resnet_structure():
     assert abs(info["macs"] / 2 - 4.09e9) / 4.09e9 < 0.05  # 3.95e9 useful MAC/img (+fc)
     plan = sb.parse_program(text).describe_plan()
     assert plan.count("kernel=conv_igemm_tc") + plan.count("kernel=conv_i8_tc") >= 40, plan
+    # the 7x7/2 stem on 3 channels runs phase-folded (2x2 fold, 16-byte folded pixels) on the
+    # im2col tensor-core kernel; the max-pool absorbs its output's zero fill
+    assert "small-channel conv phase-folded (2x2, 16 bytes per folded pixel)" in plan, plan
+    assert "kernel=pool" in plan and "(elided) fill alloc:0:Pool" in plan, plan
+    # bias + residual + ReLU fuse into the producing conv (the residual add runs on the
+    # tensor core inside the kernel): one per bottleneck block
+    assert plan.count("epilogue=vec+res+clamp") == 16, plan
 
 
 def golden(name):
