@@ -78,6 +78,7 @@ struct IgKParams {
   int epi_split;  // 8 epilogue warps as two independent groups of 4 taking alternate tiles
   int b_res, bres_off;
   int bn;      // tile width in output channels: 128 or 256 (N = 256 MMAs, 512 TMEM columns)
+  int mt;      // 128-row M sub-tiles per tile (1 or 2): one stage feeds mt x the MMAs
   int bn_box;  // filter rows per TMA box / smem tile: 64 when N <= 64, else bn
   // residual added by the tensor core: res tile (pixels x channels, SW128) x identity (128 x 128,
   // resident) accumulated into the tile after its k-blocks; loaded by a fifth producer warp
@@ -199,7 +200,8 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
   extern __shared__ __align__(1024) std::uint8_t smem_raw[];
   std::uint8_t* base =
       reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t{1023});
-  const std::uint32_t stage_a = BM * p.bk, stage_b = p.bn_box * p.bk;
+  const int TM = BM * p.mt;  // tile rows (output pixels)
+  const std::uint32_t stage_a = TM * p.bk, stage_b = p.bn_box * p.bk;
   std::uint8_t* ring = base;                    // stages x (A | B), or stages x A with the filter resident
   const std::uint32_t sstride = p.kpb * (stage_a + (p.b_res ? 0u : stage_b));
   std::uint8_t* bres = base + p.bres_off;       // resident filter: kblocks x stage_b
@@ -276,21 +278,23 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       const int PQ = p.P * p.Q;
       if (pidx == 4) {
         // residual tiles for the tensor-core add, double-buffered by tile parity
-        const int res_buf = BM * p.bn;
+        const int res_buf = TM * p.bn, hcount = (p.bn + 127) / 128;
         int it = 0;
         for (int t = blockIdx.x; t < tiles; t += gridDim.x, it++) {
           const int b = it & 1;
           mbar_wait(&rempty[b], ((it >> 1) & 1) ^ 1);
-          const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * p.bn;
+          const int m0 = (t / p.tiles_n) * TM, n0 = (t % p.tiles_n) * p.bn;
           const int halves = min(p.bn, p.N - n0 + 127) / 128;
           if (issuer) {
-            mbar_expect_tx(&rfull[b], BM * 128 * halves);
-            for (int hh = 0; hh < halves; hh++)
-              asm volatile(
-                  "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
-                  "[%2];" ::"r"(smem_u32(base + p.res_off + b * res_buf + hh * 16384)),
-                  "l"(reinterpret_cast<std::uint64_t>(&rmap)), "r"(smem_u32(&rfull[b])), "r"(n0 + hh * 128), "r"(m0)
-                  : "memory");
+            mbar_expect_tx(&rfull[b], p.mt * BM * 128 * halves);
+            for (int sub = 0; sub < p.mt; sub++)
+              for (int hh = 0; hh < halves; hh++)
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+                    "[%2];" ::"r"(smem_u32(base + p.res_off + b * res_buf + (sub * hcount + hh) * 16384)),
+                    "l"(reinterpret_cast<std::uint64_t>(&rmap)), "r"(smem_u32(&rfull[b])), "r"(n0 + hh * 128),
+                    "r"(m0 + sub * BM)
+                    : "memory");
           }
           __syncwarp();
         }
@@ -317,7 +321,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       std::uint32_t phase = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
         // n-tiles of one m-tile are adjacent in t: the A strip stays hot in L2
-        const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * p.bn;
+        const int m0 = (t / p.tiles_n) * TM, n0 = (t % p.tiles_n) * p.bn;
         const int img = m0 / PQ, rem = m0 - img * PQ;
         const int ox = rem / p.Q, oy = rem - ox * p.Q;
         const int h0 = p.lower_h + ox * p.sx, w0 = p.lower_w + oy * p.sy;
@@ -383,7 +387,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       mbar_wait(&tempty[acc], ((iter >> 1) & 1) ^ 1);
       tc_fence_after();
       if (issuer) TILE_STAMP(1, iter);
-      const std::uint32_t d = static_cast<std::uint32_t>(acc * p.bn);  // TMEM column (allocation at 0)
+      const std::uint32_t d = static_cast<std::uint32_t>(acc * p.mt * p.bn);  // TMEM column (allocation at 0)
       // a last n-tile with few valid output channels runs narrower instructions
       const int nrem = p.N - (t % p.tiles_n) * p.bn;
       const std::uint32_t ninst = nrem <= 64 ? 64u : nrem <= 128 ? 128u : static_cast<std::uint32_t>(p.bn);
@@ -402,15 +406,19 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
         if (!(p.exp & 2))
 #endif
         if (issuer) {
-          switch (p.kpb * 8 + ksteps) {
-            case 1 * 8 + 2: issue_stage<1, 2>(d, a0, as, b0, bs, hi, idesc, first); break;
-            case 1 * 8 + 4: issue_stage<1, 4>(d, a0, as, b0, bs, hi, idesc, first); break;
-            case 2 * 8 + 2: issue_stage<2, 2>(d, a0, as, b0, bs, hi, idesc, first); break;
-            case 2 * 8 + 4: issue_stage<2, 4>(d, a0, as, b0, bs, hi, idesc, first); break;
-            case 3 * 8 + 2: issue_stage<3, 2>(d, a0, as, b0, bs, hi, idesc, first); break;
-            case 3 * 8 + 4: issue_stage<3, 4>(d, a0, as, b0, bs, hi, idesc, first); break;
-            case 4 * 8 + 2: issue_stage<4, 2>(d, a0, as, b0, bs, hi, idesc, first); break;
-            default: issue_stage<4, 4>(d, a0, as, b0, bs, hi, idesc, first); break;
+          // sub-tile sub: rows 128 sub .. of every k-block's A, accumulator columns + sub * bn
+          for (int sub = 0; sub < p.mt; sub++) {
+            const std::uint32_t ds = d + sub * p.bn, as0 = a0 + sub * ((BM * p.bk) >> 4);
+            switch (p.kpb * 8 + ksteps) {
+              case 1 * 8 + 2: issue_stage<1, 2>(ds, as0, as, b0, bs, hi, idesc, first); break;
+              case 1 * 8 + 4: issue_stage<1, 4>(ds, as0, as, b0, bs, hi, idesc, first); break;
+              case 2 * 8 + 2: issue_stage<2, 2>(ds, as0, as, b0, bs, hi, idesc, first); break;
+              case 2 * 8 + 4: issue_stage<2, 4>(ds, as0, as, b0, bs, hi, idesc, first); break;
+              case 3 * 8 + 2: issue_stage<3, 2>(ds, as0, as, b0, bs, hi, idesc, first); break;
+              case 3 * 8 + 4: issue_stage<3, 4>(ds, as0, as, b0, bs, hi, idesc, first); break;
+              case 4 * 8 + 2: issue_stage<4, 2>(ds, as0, as, b0, bs, hi, idesc, first); break;
+              default: issue_stage<4, 4>(ds, as0, as, b0, bs, hi, idesc, first); break;
+            }
           }
         }
         if (issuer) STAGE_STAMP(iter, kb0 / p.kpb, 2);
@@ -428,13 +436,15 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
         const int halves = min(p.bn, nrem + 127) / 128;
         const std::uint32_t hi128 = (1024u >> 4) | (1u << 14) | (2u << 29);
         const std::uint32_t id128 = (p.idesc & ~(0x3Fu << 17)) | ((128u >> 3) << 17);
-        const std::uint32_t ra = smem_u32(base + p.res_off + acc * BM * p.bn), ib = smem_u32(base + p.ident_off);
-        for (int hh = 0; hh < halves; hh++)
+        const std::uint32_t ra = smem_u32(base + p.res_off + acc * TM * p.bn), ib = smem_u32(base + p.ident_off);
+        const int hcount = (p.bn + 127) / 128;
+        for (int sub = 0; sub < p.mt; sub++)
+          for (int hh = 0; hh < halves; hh++)
 #pragma unroll
-          for (int ks = 0; ks < 4; ks++)
-            if (issuer)
-              umma_i8(d + 128 * hh, (((ra + hh * 16384) >> 4) | (1u << 16)) + ks * 2, hi128, ((ib >> 4) | (1u << 16)) + ks * 2,
-                      hi128, id128, 1);
+            for (int ks = 0; ks < 4; ks++)
+              if (issuer)
+                umma_i8(d + sub * p.bn + 128 * hh, (((ra + (sub * hcount + hh) * 16384) >> 4) | (1u << 16)) + ks * 2,
+                        hi128, ((ib >> 4) | (1u << 16)) + ks * 2, hi128, id128, 1);
         if (issuer) umma_commit(&rempty[acc]);
         __syncwarp();
       }
@@ -602,8 +612,9 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
     const long long lo = p.epi_lo ? p.lo : LLONG_MIN;
     const bool relu0 = p.epi_lo && p.lo == 0;
     // residual tile [128 pixels x bn channels] i8 of tile t into buffer b, as 128-channel halves
-    const int res_buf = BM * p.bn, stg_buf = p.bn / 128 * 16384;
-    auto load_res = [&](int t, int b) {
+    const int hcnt = (p.bn + 127) / 128;  // 16 KB staging boxes per 128-row sub-tile
+    const int res_buf = TM * p.bn, stg_buf = p.mt * hcnt * 16384;
+    auto load_res = [&](int t, int b) {  // (epilogue-read residual: mt == 1 only)
       const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * p.bn;
       const int halves = min(p.bn, p.N - n0 + 127) / 128;
       mbar_expect_tx(&rfull[b], BM * 128 * halves);
@@ -620,7 +631,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
     int iter = g0;
     for (int t = blockIdx.x + g0 * gridDim.x; t < tiles; t += tstep, iter += split ? 2 : 1) {
       const int acc = iter & 1;
-      const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * p.bn;
+      const int m0 = (t / p.tiles_n) * TM, n0 = (t % p.tiles_n) * p.bn;
       if (leader) TILE_STAMP(8, iter);
       if (p.tma_out || eres) {
         // i32 staging is single-buffered, i8 staging double-buffered (one buffer per group when split)
@@ -642,7 +653,9 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       const int nch = min(p.bn, p.N - n0 + 31) / 32;
       const int c_lo = split || hgroups == 1 ? 0 : (hgroup * nch) >> 1;
       const int c_hi = split || hgroups == 1 ? nch : ((hgroup + 1) * nch) >> 1;
+      for (int sub = 0; sub < p.mt; sub++)
       for (int h = c_lo; h < c_hi; h++) {
+        const int msub = m + sub * BM;
         std::uint32_t v[32];
 #ifdef SB_TILE_TRACE
         if (p.exp & 4) {
@@ -650,7 +663,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
         } else
 #endif
         tmem_ld32(tmem_base + (static_cast<std::uint32_t>(quarter * 32) << 16) +
-                      static_cast<std::uint32_t>(acc * p.bn + h * 32),
+                      static_cast<std::uint32_t>(acc * p.mt * p.bn + sub * p.bn + h * 32),
                   v);
         const int kbase = n0 + h * 32;
         if (fast8) {
@@ -669,7 +682,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
           std::uint32_t w[8];
           if (eres) {
             std::uint32_t rw[8];
-            const std::uint32_t rrow = smem_u32(rcur + (h >> 2) * 16384 + row * 128);
+            const std::uint32_t rrow = smem_u32(rcur + (sub * hcnt + (h >> 2)) * 16384 + row * 128);
 #pragma unroll
             for (int u = 0; u < 2; u++)
               asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
@@ -690,7 +703,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
           for (int q = 0; q < 8; q++)
             w[q] = __byte_perm(__byte_perm(v[4 * q], v[4 * q + 1], 0x0040), __byte_perm(v[4 * q + 2], v[4 * q + 3], 0x0040),
                                0x5410);
-          const std::uint32_t rbase = smem_u32(scur + (h >> 2) * 16384 + row * 128);
+          const std::uint32_t rbase = smem_u32(scur + (sub * hcnt + (h >> 2)) * 16384 + row * 128);
 #pragma unroll
           for (int u = 0; u < 2; u++)
             asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rbase + (((2 * (h & 3) + u) ^ sw) << 4)),
@@ -712,7 +725,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
           }
           std::uint32_t rw[8];
           if (eres) {
-            const std::uint32_t rrow = smem_u32(rcur + (h >> 2) * 16384 + row * 128);
+            const std::uint32_t rrow = smem_u32(rcur + (sub * hcnt + (h >> 2)) * 16384 + row * 128);
 #pragma unroll
             for (int u = 0; u < 2; u++)
               asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
@@ -786,13 +799,13 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
           for (int q = 0; q < 8; q++)
             w[q] = (v[4 * q] & 0xFF) | ((v[4 * q + 1] & 0xFF) << 8) | ((v[4 * q + 2] & 0xFF) << 16) |
                    (v[4 * q + 3] << 24);
-          const std::uint32_t rbase = smem_u32(scur + (h >> 2) * 16384 + row * 128);
+          const std::uint32_t rbase = smem_u32(scur + (sub * hcnt + (h >> 2)) * 16384 + row * 128);
 #pragma unroll
           for (int u = 0; u < 2; u++)
             asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rbase + (((2 * (h & 3) + u) ^ sw) << 4)),
                          "r"(w[4 * u]), "r"(w[4 * u + 1]), "r"(w[4 * u + 2]), "r"(w[4 * u + 3]));
-        } else if (m < p.M) {
-          const long long rowbase = static_cast<long long>(m) * p.ldc;
+        } else if (msub < p.M) {
+          const long long rowbase = static_cast<long long>(msub) * p.ldc;
           for (int q = 0; q < 32; q++) {
             const int n = kbase + q;
             if (n >= p.N) break;
@@ -829,11 +842,12 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
                              "r"(smem_u32(stg + h * 16384)), "r"(n0 + h * 32), "r"(m0)
                              : "memory");
           } else {
-            for (int hh = 0; hh < p.bn / 128 && n0 + hh * 128 < p.N; hh++)
-              asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                               reinterpret_cast<std::uint64_t>(&cmap)),
-                           "r"(smem_u32(scur + hh * 16384)), "r"(n0 + hh * 128), "r"(m0)
-                           : "memory");
+            for (int sub = 0; sub < p.mt; sub++)
+              for (int hh = 0; hh < p.bn / 128 && n0 + hh * 128 < p.N; hh++)
+                asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                                 reinterpret_cast<std::uint64_t>(&cmap)),
+                             "r"(smem_u32(scur + (sub * hcnt + hh) * 16384)), "r"(n0 + hh * 128), "r"(m0 + sub * BM)
+                             : "memory");
           }
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           TILE_STAMP(4, iter);
@@ -948,7 +962,8 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     kp.g_in = static_cast<const std::int8_t*>(args.a);
     kp.g_run = static_cast<int>(cp.pack_run);
   }
-  kp.tiles_m = (kp.M + BM - 1) / BM;
+  kp.mt = 1;
+  kp.tiles_m = (kp.M + BM - 1) / BM;  // final value from layout() below
   kp.bn = 128;
   kp.tiles_n = (kp.N + BN - 1) / BN;  // final value from layout() below
   kp.fresh = cp.fresh_output ? 1 : 0;
@@ -987,11 +1002,13 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
   }
   // dynamic smem: A/B ring (up to 128 KB) | resident filter | output staging | residual tiles |
   // vector | gather table | barriers, for tile width bn (false: does not fit)
-  auto layout = [&](int bn) -> bool {
+  auto layout = [&](int bn, int mt) -> bool {
     kp.bn = bn;
+    kp.mt = mt;
     kp.tiles_n = (kp.N + bn - 1) / bn;
-    const int stg = kp.tma_out == 1 ? kStgBytes : kp.tma_out == 2 ? 2 * (bn / 128) * 16384 : 0;
-    const int res = kp.epi_res ? 2 * BM * bn : 0;
+    kp.tiles_m = (kp.M + BM * mt - 1) / (BM * mt);
+    const int stg = kp.tma_out == 1 ? kStgBytes : kp.tma_out == 2 ? 2 * mt * (bn / 128) * 16384 : 0;
+    const int res = kp.epi_res ? 2 * BM * mt * bn : 0;
     const int vec = kp.fast_clamp ? 2 * kVecBytes : kp.epi_vec ? kVecBytes : 0;
     const int tab = kp.gather ? (kp.kblocks * kp.bk * 6 + 15) / 16 * 16 : 0;
     const int ident = kp.res_mma ? 16384 : 0;
@@ -1000,7 +1017,7 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     const int bres = kp.tiles_n == 1 && kp.kblocks * kp.bn_box * g.bk <= 96 * 1024 && !std::getenv("SB_IG_NOBRES")
                          ? kp.kblocks * kp.bn_box * g.bk : 0;
     kp.b_res = bres ? 1 : 0;
-    const int kstage = (BM + (bres ? 0 : kp.bn_box)) * g.bk;  // one k-block's A (+ B)
+    const int kstage = (BM * mt + (bres ? 0 : kp.bn_box)) * g.bk;  // one k-block's A (+ B)
     const int avail = std::min(kRingBytes, kSmemMax - 1024 - 512 - stg - res - vec - tab - bres - ident);
     // k-blocks per stage: up to 4 while three stages still fit (gather mode: 1)
     kp.kpb = 1;
@@ -1030,7 +1047,11 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
   kp.res_mma = kp.epi_res && !kp.gather && kp.epi_split && !std::getenv("SB_IG_RESEPI") ? 1 : 0;
   // 256-wide tiles (N = 256 MMAs: half the instructions and A re-reads) for wide outputs
   const bool wide = kp.epi_split && kp.N >= 256 && cp.K <= kMaxVecK && !std::getenv("SB_IG_BN128");
-  if (!(wide && layout(256)) && !layout(128)) return cudaErrorNotSupported;
+  // two 128-row sub-tiles per tile (one stage handshake and one filter tile feed twice the
+  // MMAs) for narrow outputs with enough tiles left for every SM
+  const bool tall = kp.epi_split && kp.tma_out != 1 && kp.N <= 128 && !(kp.epi_res && !kp.res_mma) &&
+                    (kp.M + 2 * BM - 1) / (2 * BM) >= 2 * 148 && !std::getenv("SB_IG_MT1");
+  if (!(wide && layout(256, 1)) && !(tall && layout(128, 2)) && !layout(128, 1)) return cudaErrorNotSupported;
   // idesc: S32 accumulate, signed A/B, both K-major, N = 128, M = 128
   kp.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
   // descriptor high word: SBO = 8 rows x row bytes, version 1, swizzle 128B (2) / 64B (4)
@@ -1050,7 +1071,8 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
   int upper[2] = {g.upper_w, g.upper_h};
   cuuint32_t aes[4] = {1, static_cast<cuuint32_t>(cp.sy), static_cast<cuuint32_t>(cp.sx), 1};
   if (enc_im2col(&out->amap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<std::int8_t*>(abase), adim, astr, lower,
-                 upper, static_cast<cuuint32_t>(g.bk), BM, aes, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                 upper, static_cast<cuuint32_t>(g.bk), static_cast<cuuint32_t>(BM * kp.mt), aes,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   }

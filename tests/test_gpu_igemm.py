@@ -89,6 +89,10 @@ FUSED = [
     (2, 14, 14, 256, 256, 3, 3, 1, 1, False, False),
     (2, 8, 8, 64, 256, 1, 1, 1, 0, True, True),   # residual add fused (TMA-loaded tile)
     (3, 7, 9, 128, 192, 3, 3, 1, 1, True, True),  # residual with ragged M and N tiles
+    (2, 14, 14, 256, 512, 1, 1, 1, 0, True, True),  # 256-wide tiles + tensor-core residual
+    # large M with N <= 128: two 128-row sub-tiles per tile (M = 2 x 128 rows, one stage handshake)
+    (32, 56, 56, 64, 64, 3, 3, 1, 1, True, False),
+    (27, 56, 56, 64, 128, 1, 1, 1, 0, True, True),  # + residual per sub-tile, ragged last tile
 ]
 
 
