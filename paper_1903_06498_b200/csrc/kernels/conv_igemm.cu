@@ -1023,7 +1023,7 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     kp.kpb = 1;
     if (!kp.gather && !std::getenv("SB_IG_KPB1"))
       for (int c : {4, 3, 2})
-        if (kp.kblocks % c == 0 && 3 * c * kstage <= avail) {
+        if (kp.kblocks % c == 0 && (std::getenv("SB_IG_KPB3") ? 3 : 2) * c * kstage <= avail) {
           kp.kpb = c;
           break;
         }
