@@ -102,6 +102,7 @@ struct IgKParams {
   // there is no clamp (wrapped low bits) or every |vec[k]| <= bias_bound (no int32 overflow)
   int fast8;
   long long bias_bound;
+  int thr_always;  // fast8 with a clamp bound outside int32: always the threshold form
   const void* vec;
   long long vec_k;
   long long lo;
@@ -607,7 +608,11 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
     const bool eres = p.epi_res && !p.res_mma;  // residual read by the epilogue (else added by the MMAs)
     if (eres && leader && p.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("bar.sync 1, %0;" ::"r"(ethreads) : "memory");
-    const bool fast8 = p.fast8 && !(p.epi_lo && *reinterpret_cast<volatile int*>(bars + 41));
+    // fast8 clamp: max(acc + res + vec, lo) in int32 when no |vec[k]| can overflow it, else the
+    // exact threshold form acc + res >= clamp32(lo - vec[k]) (both keep the wrapped low byte)
+    const bool fast8 = p.fast8 != 0;
+    const bool thr8 = p.epi_lo && (p.thr_always || *reinterpret_cast<volatile int*>(bars + 41));
+    const std::uint32_t lo32u = static_cast<std::uint32_t>(p.lo);
     const std::int32_t lo8 = p.epi_lo ? static_cast<std::int32_t>(p.lo) : INT_MIN;
     const long long lo = p.epi_lo ? p.lo : LLONG_MIN;
     const bool relu0 = p.epi_lo && p.lo == 0;
@@ -692,8 +697,19 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
             for (int q = 0; q < 32; q++) {
               std::int32_t r;  // sign-extended residual byte (prmt sign-replicate selector)
               asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(rw[q >> 2]), "r"(0x8880u + 0x1111u * (q & 3)));
-              v[q] = static_cast<std::uint32_t>(max(static_cast<std::int32_t>(v[q]) + r + bv[q], lo8));
+              v[q] = static_cast<std::uint32_t>(static_cast<std::int32_t>(v[q]) + r);
             }
+          }
+          if (thr8) {
+            std::int32_t tv[32];
+#pragma unroll
+            for (int q = 0; q < 8; q++)
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(tv[4 * q]), "=r"(tv[4 * q + 1]), "=r"(tv[4 * q + 2]), "=r"(tv[4 * q + 3])
+                           : "r"(smem_u32(thr_s + kbase + 4 * q)));
+#pragma unroll
+            for (int q = 0; q < 32; q++)
+              v[q] = static_cast<std::int32_t>(v[q]) >= tv[q] ? v[q] + static_cast<std::uint32_t>(bv[q]) : lo32u;
           } else {
 #pragma unroll
             for (int q = 0; q < 32; q++)
@@ -996,7 +1012,10 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     const long long taps = cp.packed ? cp.R * cp.S * cp.C : gp.R * gp.S * gp.C;
     const long long T = taps * 128 * 128 + 128;  // bound on |acc + res|
     const bool lo_ok = !cp.epi_lo || (cp.lo >= INT_MIN && cp.lo <= INT_MAX && T < INT_MAX);
-    kp.fast8 = kp.tma_out == 2 && cp.K <= kMaxVecK && lo_ok ? 1 : 0;
+    // i8 epilogue in int32: no clamp (wrapped low bits), or a clamp decided exactly by max()
+    // (small biases, lo in int32) or by the per-channel threshold (needs the fast_clamp bound)
+    kp.fast8 = kp.tma_out == 2 && cp.K <= kMaxVecK && (!cp.epi_lo || kp.fast_clamp) ? 1 : 0;
+    kp.thr_always = cp.epi_lo && !lo_ok ? 1 : 0;
     kp.epi_split = kp.epi_warps == 8 && kp.tma_out != 1 && !std::getenv("SB_IG_NOSPLIT") ? 1 : 0;
     kp.bias_bound = T < INT_MAX ? INT_MAX - T : 0;
   }

@@ -24,6 +24,8 @@ def main():
         text = W.conv_fused(batch, 56, 56, 64, 64, 3, 3, 1, 1)
     elif which == "s3_3x3":
         text = W.conv_fused(batch, 14, 14, 256, 256, 3, 3, 1, 1)
+    elif which == "s3_1024":
+        text = W.conv_fused(batch, 14, 14, 1024, 256, 1, 1, 1, 0)
     elif which == "s3_1x1":
         text = W.conv_fused(batch, 14, 14, 256, 1024, 1, 1, 1, 0, residual=True)
     elif which == "l1x1r":
