@@ -376,12 +376,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       // per-output-channel vector of the fused epilogue (e.g. the bias), as int32 in smem
       for (int k = threadIdx.x - 64; k < p.K; k += ethreads) {
         long long a = p.vec_c + p.vec_k * k;
-        vec_s[k] = p.vec_kind == kI8 ? static_cast<const std::int8_t*>(p.vec)[a]
-                   : p.vec_kind == kI16 ? static_cast<const std::int16_t*>(p.vec)[a]
-                                        : static_cast<const std::int32_t*>(p.vec)[a];
+        const int b = p.vec_kind == kI8 ? static_cast<const std::int8_t*>(p.vec)[a]
+                      : p.vec_kind == kI16 ? static_cast<const std::int16_t*>(p.vec)[a]
+                                           : static_cast<const std::int32_t*>(p.vec)[a];
+        vec_s[k] = b;
+        // threshold t[k] = clamp32(lo - b): since |acc| < 2^31 - 1 (planner bound),
+        // acc + b >= lo  <=>  acc >= t[k], so the clamp is one int32 compare per element
+        const long long t = p.lo - b;
+        vec_s[p.K + k] = static_cast<int>(t < INT_MIN ? INT_MIN : t > INT_MAX ? INT_MAX : t);
       }
       asm volatile("bar.sync 1, %0;" ::"r"(ethreads) : "memory");
     }
+    // clamp threshold when there is no vector: clamp32(lo)
+    const int lo_t = static_cast<int>(p.lo < INT_MIN ? INT_MIN : p.lo > INT_MAX ? INT_MAX : p.lo);
     // fused epilogue on the exact s32 accumulator, int64 arithmetic, wrap at the i32 store
     auto epilogue = [&](int k, std::uint32_t acc_bits) -> std::uint32_t {
       if (!p.epi) return acc_bits;
@@ -430,11 +437,27 @@ __global__ void __launch_bounds__(kThreads, 1)
               else
                 bv[4 * q] = bv[4 * q + 1] = bv[4 * q + 2] = bv[4 * q + 3] = 0;
             }
-            const long long lo = p.epi_lo ? p.lo : LLONG_MIN;
+            // wrap(max(acc + vec, lo)) in int32: the store keeps the low 32 (or 8) bits of the
+            // exact sum, and the clamp decision is acc >= t[k] (t filled with the vector)
+            if (p.epi_lo) {
+              int tv[32];
+              const std::uint32_t taddr = smem_u32(vec_s + p.K + h * 32);
 #pragma unroll
-            for (int q = 0; q < 32; q++) {
-              long long x = static_cast<long long>(static_cast<std::int32_t>(v[q])) + bv[q];
-              v[q] = static_cast<std::uint32_t>(x < lo ? lo : x);
+              for (int q = 0; q < 8; q++) {
+                if (p.epi_vec)
+                  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                               : "=r"(tv[4 * q]), "=r"(tv[4 * q + 1]), "=r"(tv[4 * q + 2]), "=r"(tv[4 * q + 3])
+                               : "r"(taddr + q * 16));
+                else
+                  tv[4 * q] = tv[4 * q + 1] = tv[4 * q + 2] = tv[4 * q + 3] = lo_t;
+              }
+              const std::uint32_t lo32 = static_cast<std::uint32_t>(p.lo);
+#pragma unroll
+              for (int q = 0; q < 32; q++)
+                v[q] = static_cast<std::int32_t>(v[q]) >= tv[q] ? v[q] + static_cast<std::uint32_t>(bv[q]) : lo32;
+            } else {
+#pragma unroll
+              for (int q = 0; q < 32; q++) v[q] += static_cast<std::uint32_t>(bv[q]);
             }
           }
           if (p.tma_out == 2) {
