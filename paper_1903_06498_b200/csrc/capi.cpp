@@ -342,12 +342,14 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
   // Dependency-aware PDL: a tensor-core launch that touches nothing an in-flight launch writes
   // (and writes nothing one reads) need not wait for its predecessor at all, so consecutive
   // independent executes overlap completely (the previous grid's tail wave is filled).
-  auto pdl_mode = [&](std::size_t i) -> int {
-    // opt-in (SB_PDL_FREE=1): measured no gain on the configs (the first-tile filter fetch,
-    // not the tail wave, dominates the gap between kernels), so the default keeps every
-    // tensor-core launch waiting on its predecessor
+  auto pdl_mode = [&](std::size_t i, bool load_early_ok) -> int {
+    // Free is opt-in (SB_PDL_FREE=1): measured no gain on the configs. LoadEarly (default
+    // for the resident-filter conv): when only the immediately preceding launch may still run
+    // and it writes nothing this launch reads, the loads and MMAs start at once and only the
+    // stores wait for the predecessor (WAW / WAR ordering kept).
     static const bool allow_free = std::getenv("SB_PDL_FREE") != nullptr;
-    if (!single_lane || !allow_free) {
+    static const bool load_early = std::getenv("SB_PDL_NO_EARLY") == nullptr;
+    if (!single_lane) {
       ctx->window.clear();
       return sb::kPdlWait;
     }
@@ -366,16 +368,20 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
           if (a.lo < b.hi && b.lo < a.hi) return true;
       return false;
     };
-    bool any = false;
-    for (const auto& w : ctx->window) any |= ov(w.wr, me.rd) || ov(w.wr, me.wr) || ov(w.rd, me.wr);
-    if (!any && ctx->window.size() < 64) {
+    bool raw = false, any = false;
+    for (const auto& w : ctx->window) {
+      raw |= ov(w.wr, me.rd);
+      any |= ov(w.wr, me.rd) || ov(w.wr, me.wr) || ov(w.rd, me.wr);
+    }
+    if (allow_free && !any && ctx->window.size() < 64) {
       ctx->window.push_back(std::move(me));
       return sb::kPdlFree;
     }
-    const bool one = ctx->window.size() == 1;  // only the immediately preceding launch may still run
+    const std::size_t inflight = ctx->window.size();  // 0/1: only the preceding launch may still run
     ctx->window.clear();
     ctx->window.push_back(std::move(me));
-    return one ? sb::kPdlWait : sb::kPdlOff;
+    if (inflight <= 1 && !raw && load_early && load_early_ok) return sb::kPdlLoadEarly;
+    return inflight <= 1 ? sb::kPdlWait : sb::kPdlOff;
   };
   auto step = [&](std::size_t i) {
     const auto& s = plan.steps[i];
@@ -406,7 +412,7 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
         a.vec_kind = plan.bufs[l.conv.vec_buf].kind;
       }
       if (l.conv.epi_res) a.res = ptr_of(l.conv.res_buf);
-      if (tc_single) a.pdl_mode = pdl_mode(i);
+      if (tc_single) a.pdl_mode = pdl_mode(i, l.kernel == sb::KernelKind::ConvI8TC);
       if (l.kernel == sb::KernelKind::ConvI8TC) {
         cuda_check(sb::launch_conv_tc(l.conv, a, ctx->stream, ctx->num_sms), "conv_tc");
       } else if (l.conv.packed && l.conv.fold_x) {
@@ -503,7 +509,7 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
     }
     if (l.kernel == sb::KernelKind::GemmI8TC) {
       sb::GemmArgs a{ptr_of(l.gemm.a_buf), ptr_of(l.gemm.b_buf), ptr_of(l.gemm.c_buf)};
-      a.pdl_mode = pdl_mode(i);
+      a.pdl_mode = pdl_mode(i, false);
       cuda_check(sb::launch_gemm_tc(l.gemm, a, ctx->stream, ctx->num_sms), "gemm_tc");
       ctx->launches++;
       return;

@@ -37,8 +37,10 @@ cudaError_t launch_reduce(const ReduceArgs& a, cudaStream_t s);
 // tcgen05 GEMM (kernels/gemm_tc.cu).
 // Programmatic dependent launch per call (capi.cpp decides from buffer overlap with the
 // launches that may still run): 0 plain stream order, 1 PDL + griddepcontrol.wait,
-// 2 PDL without waiting (independent of every in-flight launch).
-enum : int { kPdlOff = 0, kPdlWait = 1, kPdlFree = 2 };
+// 2 PDL without waiting (independent of every in-flight launch), 3 PDL whose loads may start
+// at once (nothing in flight writes what it reads) but whose stores wait (resident-filter conv
+// only; other kernels treat it as 1).
+enum : int { kPdlOff = 0, kPdlWait = 1, kPdlFree = 2, kPdlLoadEarly = 3 };
 
 struct GemmArgs {
   const void* a;

@@ -65,6 +65,7 @@ struct ConvKParams {
   int st_out;             // tma_out staging drained with coalesced LSU stores instead of TMA stores
   int vec4;               // direct path: 16-byte aligned i32 rows (c0, strides multiples of 4)
   int pdl_wait;           // griddepcontrol.wait before touching buffers (else independent)
+  int store_wait;         // loads start at once; the epilogue waits for the predecessor before storing
   int cluster;            // CTAs per thread-block cluster (filter multicast)
   int debug_nofilt;       // timing experiments only
   int pdl;                // launched with programmatic stream serialization
@@ -369,6 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ethreads = split ? 256 : 128;
     const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31
     const int row = quarter * 32 + lane;
+    if (p.store_wait) asm volatile("griddepcontrol.wait;" ::: "memory");  // WAW/WAR with the predecessor
     const int xl = row / p.P;
     const int y = row % p.P;
     int iter = 0;
@@ -837,6 +839,7 @@ cudaError_t launch_conv_tc(const ConvPlan& cp, const ConvArgs& args, cudaStream_
   }();
   kp.pdl = pdl && args.pdl_mode != kPdlOff ? 1 : 0;
   kp.pdl_wait = kp.pdl && args.pdl_mode == kPdlWait ? 1 : 0;
+  kp.store_wait = kp.pdl && args.pdl_mode == kPdlLoadEarly ? 1 : 0;
   kp.filter_early = args.b_immutable ? 1 : 0;
   kp.epi = cp.epi ? 1 : 0;
   kp.epi_vec = cp.epi_vec ? 1 : 0;
