@@ -9,7 +9,9 @@
 // identity that this launch covers exactly once, the initial read is skipped.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <limits>
 
 #include "../kernels.hpp"
 
@@ -116,8 +118,106 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceArgs a) {
   }
 }
 
+// Few outputs, long reductions (the ResNet global sum: 16K vectors x 49 rows): a block is 32
+// output vectors x kSplit row phases; each thread folds rows r = phase (mod kSplit) into
+// an identity-started accumulator, then the kSplit partials are folded in shared memory.
+// add (wrapping), max, min and mul fold in any order to the same wrapped result, so this
+// equals the reference's lexicographic sequence of wrapping stores.
+constexpr int kSplit = 8;
+
+template <int AGG, typename TO>
+__device__ __forceinline__ std::int64_t agg_identity() {
+  if constexpr (AGG == 1) return 0;
+  if constexpr (AGG == 2) return static_cast<std::int64_t>(std::numeric_limits<TO>::min());
+  if constexpr (AGG == 3) return static_cast<std::int64_t>(std::numeric_limits<TO>::max());
+  return 1;
+}
+
+template <int AGG, typename TI, typename TO>
+__global__ void __launch_bounds__(256) reduce_split_kernel(const ReduceArgs a) {
+  constexpr int V = Vec16<TI>::N;
+  extern __shared__ std::int64_t roff[];  // [rcount] offsets, then [256][V] partials
+  for (int r = threadIdx.x; r < a.rcount; r += blockDim.x) {
+    std::int64_t rest = r, off = 0;
+    for (int i = a.nr - 1; i >= 0; i--) {
+      off += (rest % a.rrange[i]) * a.rstep[i];
+      rest /= a.rrange[i];
+    }
+    roff[r] = off;
+  }
+  std::int64_t* part = roff + ((a.rcount + 1) & ~1);
+  __syncthreads();
+  const TI* in = static_cast<const TI*>(a.in);
+  TO* out = static_cast<TO*>(a.out);
+  const std::int64_t nvec = a.prange[0] / V;
+  const std::int64_t total = a.pcount / V;
+  const int vi = threadIdx.x & 31, phase = threadIdx.x >> 5;
+  for (std::int64_t base = static_cast<std::int64_t>(blockIdx.x) * 32; base < total;
+       base += static_cast<std::int64_t>(gridDim.x) * 32) {
+    const std::int64_t lin = base + vi;
+    const bool live = lin < total;
+    std::int64_t ib = 0, ob = 0;
+    if (live) {
+      std::int64_t rest = lin;
+      const std::int64_t c0 = (rest % nvec) * V;
+      rest /= nvec;
+      ib = a.in_c + c0;
+      ob = a.out_c + c0;
+      for (int i = 1; i < a.np; i++) {
+        const std::int64_t c = rest % a.prange[i];
+        rest /= a.prange[i];
+        ib += c * a.pin[i];
+        ob += c * a.pout[i];
+      }
+    }
+    std::int64_t acc[V];
+#pragma unroll
+    for (int l = 0; l < V; l++) acc[l] = agg_identity<AGG, TO>();
+    if (live)
+      for (int r = phase; r < a.rcount; r += kSplit) {
+        TI x[V];
+        load16<TI>(in + ib + roff[r], x);
+#pragma unroll
+        for (int l = 0; l < V; l++) acc[l] = agg<AGG, TO>(acc[l], x[l]);
+      }
+#pragma unroll
+    for (int l = 0; l < V; l++) part[threadIdx.x * V + l] = acc[l];
+    __syncthreads();
+    if (phase == 0 && live) {
+#pragma unroll
+      for (int l = 0; l < V; l++) acc[l] = a.fresh ? a.identity : static_cast<std::int64_t>(out[ob + l]);
+      for (int q = 0; q < kSplit; q++)
+#pragma unroll
+        for (int l = 0; l < V; l++) acc[l] = agg<AGG, TO>(acc[l], part[(q * 32 + vi) * V + l]);
+      constexpr int per16 = 16 / sizeof(TO);
+#pragma unroll
+      for (int q = 0; q < V / per16; q++) {
+        int4 w;
+        TO* st = reinterpret_cast<TO*>(&w);
+#pragma unroll
+        for (int l = 0; l < per16; l++) st[l] = static_cast<TO>(acc[q * per16 + l]);
+        *reinterpret_cast<int4*>(out + ob + q * per16) = w;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 template <int AGG, typename TI>
 cudaError_t dispatch_out(const ReduceArgs& a, int grid, std::size_t smem, cudaStream_t s) {
+  const int V = Vec16<TI>::N;
+  const std::int64_t vecs = a.pcount / V;
+  // split the rows when the outputs alone cannot fill the GPU (assign stays sequential)
+  if (AGG != 0 && a.rcount >= 2 * kSplit && a.rcount <= 1024 && vecs < 148ll * 256 * 2) {
+    const int sgrid = static_cast<int>(std::min<std::int64_t>((vecs + 31) / 32, 148 * 8));
+    const std::size_t ssmem = ((a.rcount + 1) & ~1) * sizeof(std::int64_t) + 256 * V * sizeof(std::int64_t);
+    switch (a.out_kind) {
+      case kI8: reduce_split_kernel<AGG, TI, std::int8_t><<<sgrid, 256, ssmem, s>>>(a); break;
+      case kI16: reduce_split_kernel<AGG, TI, std::int16_t><<<sgrid, 256, ssmem, s>>>(a); break;
+      default: reduce_split_kernel<AGG, TI, std::int32_t><<<sgrid, 256, ssmem, s>>>(a); break;
+    }
+    return cudaGetLastError();
+  }
   switch (a.out_kind) {
     case kI8: reduce_kernel<AGG, TI, std::int8_t><<<grid, 256, smem, s>>>(a); break;
     case kI16: reduce_kernel<AGG, TI, std::int16_t><<<grid, 256, smem, s>>>(a); break;

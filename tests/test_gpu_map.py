@@ -60,6 +60,30 @@ def test_reduce_all_aggregations(agg):
     check(W.global_sum(4, 3, 5, 256).replace("O[n, c]:add", f"O[n, c]:{agg}"), expect_kernel="reduce")
 
 
+@pytest.mark.parametrize("dt", ["i8", "i16", "i32"])
+@pytest.mark.parametrize("agg", ["add", "max", "min", "mul"])
+@pytest.mark.parametrize("prefill", [False, True])
+def test_reduce_row_split(dt, agg, prefill):
+    """Few outputs x many rows (the ResNet global sum shape): rows folded in 8 phases and
+    combined in shared memory (order-free for add/max/min/mul); with a prefilled output the
+    partials fold onto its old values."""
+    import paper_1903_06498_b200 as sb
+    text = W.global_sum(4, 5, 7, 256, in_dtype=dt, out_dtype=dt).replace("O[n, c]:add", f"O[n, c]:{agg}")
+    p = sb.parse_program(text)
+    assert "kernel=reduce" in p.describe_plan(True)
+    bufs = [(n, d.dtype, d.elements, int(d.dir)) for n, d in p.buffers.items()]
+    inp = {n: (p.buffers[n].dtype, a) for n, a in random_inputs(bufs, 17).items()}
+    if prefill:  # an existing output: the reduction accumulates onto it
+        o = random_inputs([("O", p.buffers["O"].dtype, p.buffers["O"].elements, 0)], 23)["O"]
+        inp["O"] = (p.buffers["O"].dtype, o)
+    store = {n: a for n, (b, a) in inp.items()}
+    if "O" not in store:
+        store["O"] = np.full(p.buffers["O"].elements, p.output_identity("O"), np.int64)
+    exp = Port.execute(text, {n: a.copy() for n, a in store.items()})
+    got = run_device(text, inp)
+    np.testing.assert_array_equal(got["O"], exp["O"])
+
+
 def _eltwise(N, C, body, out_agg="assign", dt="i32", extra_cons=""):
     return f"""block []:1 (
 	in A[0, 0] {dt}({N}, {C}):({C}, 1)
