@@ -77,6 +77,7 @@ struct IgKParams {
   int epi_warps;  // 4 or 8 (two warps per TMEM lane quarter, each taking half the columns)
   int epi_split;  // 8 epilogue warps as two independent groups of 4 taking alternate tiles
   int b_res, bres_off;
+  int b_early;  // resident filter immutable: loaded before griddepcontrol.wait
   int bn;      // tile width in output channels: 128 or 256 (N = 256 MMAs, 512 TMEM columns)
   int mt;      // 128-row M sub-tiles per tile (1 or 2): one stage feeds mt x the MMAs
   int bn_box;  // filter rows per TMA box / smem tile: 64 when N <= 64, else bn
@@ -273,8 +274,10 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
   if (pidx >= 0) {
     {  // converged warp; one elected lane issues (uniform-register operands, see the MMA warp)
       const bool issuer = elect_one();
-      if (p.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
-      const bool do_a = !p.gather && (pidx & 1) == 0, do_b = p.gather || (pidx & 1) == 1;
+      const bool do_a = !p.gather && (pidx & 1) == 0 && pidx != 4, do_b = p.gather || (pidx & 1) == 1;
+      // an immutable resident filter (a root `in` buffer no plan step writes) is fetched while
+      // the predecessor still runs; everything else waits for it
+      if (p.pdl_wait && !(p.b_early && do_b && p.b_res)) asm volatile("griddepcontrol.wait;" ::: "memory");
       const int nchains = p.gather ? 1 : 2, chain = p.gather ? 0 : pidx >> 1;
       const int PQ = p.P * p.Q;
       if (pidx == 4) {
@@ -1427,6 +1430,7 @@ cudaError_t launch_conv_igemm(const ConvPlan& cp, const ConvArgs& args, cudaStre
   IgKParams kp = pr->kp;
   kp.pdl = args.pdl_mode != kPdlOff ? 1 : 0;
   kp.pdl_wait = args.pdl_mode == kPdlWait ? 1 : 0;
+  kp.b_early = args.b_immutable ? 1 : 0;
   const int tiles = kp.tiles_m * kp.tiles_n;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(tiles < num_sms ? tiles : num_sms));
