@@ -26,6 +26,10 @@ def main():
         text = W.conv_fused(batch, 14, 14, 256, 256, 3, 3, 1, 1)
     elif which == "s3_1024":
         text = W.conv_fused(batch, 14, 14, 1024, 256, 1, 1, 1, 0)
+    elif which == "s4_3x3":
+        text = W.conv_fused(batch, 7, 7, 512, 512, 3, 3, 1, 1)
+    elif which == "s4_1x1":
+        text = W.conv_fused(batch, 7, 7, 512, 2048, 1, 1, 1, 0, residual=True)
     elif which == "s3_1x1":
         text = W.conv_fused(batch, 14, 14, 256, 1024, 1, 1, 1, 0, residual=True)
     elif which == "l1x1r":
