@@ -1212,10 +1212,12 @@ __global__ void conv_pack_filter_kernel(const std::int8_t* __restrict__ b, std::
 // Folded pixels F[n, U, V, kf], kf = (di*fy + dj)*C + c: I[n, fx*U + di, fy*V + dj, c] (zero
 // outside the constraint window and on the padding bytes up to fold_c).  Specialised: one
 // thread per folded pixel, unrolled (the ResNet stem is FX = FY = 2, C = 3: 12 of 16 bytes).
-template <int FX, int FY, int CC>
+// ROWS (fold_c == 16): the folded pixel (n, U, V) is scattered into the materialised rows
+// T[n, U, y, b] = F[n, U, y + b] for b < NB, 0 <= y < Q (every row slot written once).
+template <int FX, int FY, int CC, bool ROWS>
 __global__ void __launch_bounds__(256) conv_fold_fixed(const std::int8_t* __restrict__ a, uint4* __restrict__ F, int pixels,
                                                        int FU, int FV, long long a_n, long long a_x, long long a_y,
-                                                       long long a0, int u_lo, int u_hi, int v_lo, int v_hi) {
+                                                       long long a0, int u_lo, int u_hi, int v_lo, int v_hi, int Q, int NB) {
   constexpr int FC = (FX * FY * CC + 15) / 16 * 16;
   for (int pix = blockIdx.x * blockDim.x + threadIdx.x; pix < pixels; pix += gridDim.x * blockDim.x) {
     const int nu = pix / FV, V = pix - nu * FV;
@@ -1240,9 +1242,85 @@ __global__ void __launch_bounds__(256) conv_fold_fixed(const std::int8_t* __rest
         }
       }
     }
+    if (ROWS) {
+      const uint4 val = make_uint4(w[0], w[1], w[2], w[3]);
+      for (int b = 0; b < NB; b++) {
+        const int y = V - b;
+        if (y >= 0 && y < Q) F[(static_cast<long long>(nu) * Q + y) * NB + b] = val;
+      }
+    } else {
 #pragma unroll
-    for (int i = 0; i < FC / 16; i++)
-      F[static_cast<long long>(pix) * (FC / 16) + i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+      for (int i = 0; i < FC / 16; i++)
+        F[static_cast<long long>(pix) * (FC / 16) + i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+    }
+  }
+}
+
+// Rows layout, one block per folded row (n, U): the row's FV folded pixels are built in shared
+// memory (one thread each), then the Q x NB 16-byte row slots are written contiguously
+// (coalesced 16-byte stores; the scatter form above writes them 64 bytes apart).
+template <int FX, int FY, int CC>
+__global__ void __launch_bounds__(256) conv_fold_rows_block(const std::int8_t* __restrict__ a, uint4* __restrict__ T,
+                                                            int rows, int FU, int FV, long long a_n, long long a_x,
+                                                            long long a_y, long long a0, int u_lo, int u_hi, int v_lo,
+                                                            int v_hi, int Q, int NB) {
+  extern __shared__ uint4 fp[];  // [FV]
+  for (int nu = blockIdx.x; nu < rows; nu += gridDim.x) {
+    const int n = nu / FU, U = nu - n * FU;
+    for (int V = threadIdx.x; V < FV; V += blockDim.x) {
+      std::uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int di = 0; di < FX; di++) {
+        const int u = FX * U + di;
+        const bool uok = u >= u_lo && u <= u_hi;
+        const std::int8_t* rp = a + a0 + a_n * n + a_x * u;
+#pragma unroll
+        for (int dj = 0; dj < FY; dj++) {
+          const int v = FY * V + dj;
+          if (uok && v >= v_lo && v <= v_hi) {
+#pragma unroll
+            for (int c = 0; c < CC; c++) {
+              const int q = (di * FY + dj) * CC + c;
+              w[q / 4] |= static_cast<std::uint32_t>(static_cast<std::uint8_t>(__ldg(rp + a_y * v + c))) << (8 * (q % 4));
+            }
+          }
+        }
+      }
+      fp[V] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    __syncthreads();
+    uint4* dst = T + static_cast<long long>(nu) * Q * NB;
+    for (int i = threadIdx.x; i < Q * NB; i += blockDim.x) {
+      const int y = i / NB, b = i - y * NB;
+      dst[i] = fp[y + b];
+    }
+    __syncthreads();
+  }
+}
+
+// Rows layout for any fold with 16-byte folded pixels (fx*fy*C <= 16): one thread per pixel.
+__global__ void __launch_bounds__(256) conv_fold_rows_any(const std::int8_t* __restrict__ a, uint4* __restrict__ T,
+                                                          int pixels, int FU, int FV, int fx, int fy, int C,
+                                                          long long a_n, long long a_x, long long a_y, long long a0,
+                                                          int u_lo, int u_hi, int v_lo, int v_hi, int Q, int NB) {
+  for (int pix = blockIdx.x * blockDim.x + threadIdx.x; pix < pixels; pix += gridDim.x * blockDim.x) {
+    const int nu = pix / FV, V = pix - nu * FV;
+    const int n = nu / FU, U = nu - n * FU;
+    std::uint32_t w[4] = {0, 0, 0, 0};
+    int q = 0;
+    for (int di = 0; di < fx; di++)
+      for (int dj = 0; dj < fy; dj++)
+        for (int c = 0; c < C; c++, q++) {
+          const int u = fx * U + di, v = fy * V + dj;
+          if (u >= u_lo && u <= u_hi && v >= v_lo && v <= v_hi)
+            w[q >> 2] |= static_cast<std::uint32_t>(static_cast<std::uint8_t>(__ldg(a + a0 + a_n * n + a_x * u + a_y * v + c)))
+                         << (8 * (q & 3));
+        }
+    const uint4 val = make_uint4(w[0], w[1], w[2], w[3]);
+    for (int b = 0; b < NB; b++) {
+      const int y = V - b;
+      if (y >= 0 && y < Q) T[(static_cast<long long>(nu) * Q + y) * NB + b] = val;
+    }
   }
 }
 
@@ -1312,14 +1390,30 @@ cudaError_t launch_conv_fold(const ConvPlan& cp, const void* a, void* f, cudaStr
   const int lo_u = static_cast<int>(cp.u_lo), hi_u = static_cast<int>(cp.u_hi);
   const int lo_v = static_cast<int>(cp.v_lo), hi_v = static_cast<int>(cp.v_hi);
   const int blocks = static_cast<int>(std::min<long long>((pixels + 255) / 256, 148 * 32));
-  if (cp.fold_x == 2 && cp.fold_y == 2 && cp.C == 3 && cp.fold_c == 16) {
-    conv_fold_fixed<2, 2, 3><<<blocks, 256, 0, s>>>(in, static_cast<uint4*>(f), static_cast<int>(pixels),
-                                                    static_cast<int>(cp.fold_u), static_cast<int>(cp.fold_v), cp.a_n,
-                                                    cp.a_x, cp.a_y, cp.a0, lo_u, hi_u, lo_v, hi_v);
-  } else if (cp.fold_x == 1 && cp.fold_y == 1 && cp.C == 3 && cp.fold_c == 16) {
-    conv_fold_fixed<1, 1, 3><<<blocks, 256, 0, s>>>(in, static_cast<uint4*>(f), static_cast<int>(pixels),
-                                                    static_cast<int>(cp.fold_u), static_cast<int>(cp.fold_v), cp.a_n,
-                                                    cp.a_x, cp.a_y, cp.a0, lo_u, hi_u, lo_v, hi_v);
+  const int Q = static_cast<int>(cp.W), NB = static_cast<int>(cp.fold_cv / 16);
+  auto fixed = [&](auto kern) {
+    kern<<<blocks, 256, 0, s>>>(in, static_cast<uint4*>(f), static_cast<int>(pixels), static_cast<int>(cp.fold_u),
+                                static_cast<int>(cp.fold_v), cp.a_n, cp.a_x, cp.a_y, cp.a0, lo_u, hi_u, lo_v, hi_v, Q, NB);
+  };
+  const bool stem = cp.fold_x == 2 && cp.fold_y == 2 && cp.C == 3 && cp.fold_c == 16;
+  const bool c3s1 = cp.fold_x == 1 && cp.fold_y == 1 && cp.C == 3 && cp.fold_c == 16;
+  if (stem && cp.fold_rows) {
+    const int rows = static_cast<int>(cp.N * cp.fold_u);
+    conv_fold_rows_block<2, 2, 3><<<std::min(rows, 148 * 16), 128, static_cast<int>(cp.fold_v) * 16, s>>>(
+        in, static_cast<uint4*>(f), rows, static_cast<int>(cp.fold_u), static_cast<int>(cp.fold_v), cp.a_n, cp.a_x,
+        cp.a_y, cp.a0, lo_u, hi_u, lo_v, hi_v, Q, NB);
+  } else if (stem) {
+    fixed(conv_fold_fixed<2, 2, 3, false>);
+  } else if (c3s1 && cp.fold_rows) {
+    fixed(conv_fold_fixed<1, 1, 3, true>);
+  } else if (c3s1) {
+    fixed(conv_fold_fixed<1, 1, 3, false>);
+  } else if (cp.fold_rows) {
+    conv_fold_rows_any<<<blocks, 256, 0, s>>>(in, static_cast<uint4*>(f), static_cast<int>(pixels),
+                                              static_cast<int>(cp.fold_u), static_cast<int>(cp.fold_v),
+                                              static_cast<int>(cp.fold_x), static_cast<int>(cp.fold_y),
+                                              static_cast<int>(cp.C), cp.a_n, cp.a_x, cp.a_y, cp.a0, lo_u, hi_u, lo_v,
+                                              hi_v, Q, NB);
   } else {
     const int FCW = static_cast<int>(cp.fold_c / 4);
     const long long words = pixels * FCW;

@@ -780,9 +780,9 @@ ConvPlan packed_view(const ConvPlan& c) {
     v.R = c.fold_r;
     v.S = 1;
     v.sx = v.sy = 1;
-    v.a_y = c.fold_c;
-    v.a_x = c.fold_v * c.fold_c;
-    v.a_n = c.fold_u * c.fold_v * c.fold_c;
+    v.a_y = c.fold_rows ? c.fold_cv : c.fold_c;
+    v.a_x = c.fold_rows ? c.W * c.fold_cv : c.fold_v * c.fold_c;
+    v.a_n = c.fold_u * v.a_x;
     v.a0 = 0;
     v.u_lo = 0;
     v.u_hi = c.fold_u - 1;
@@ -839,7 +839,9 @@ bool try_packed_conv(Plan* plan, ConvPlan* cp) {
     c.pack_k = c.fold_r * c.fold_cv;
     c.pack_a = static_cast<int>(plan->bufs.size());
     c.pack_b = c.pack_a + 1;
-    const std::int64_t folded = c.N * c.fold_u * c.fold_v * c.fold_c;
+    // materialised rows when a folded pixel is one 16-byte unit and a row a whole number of them
+    c.fold_rows = c.fold_c == 16 && c.fold_cv % 16 == 0 && !std::getenv("SB_FOLD_OVERLAP");
+    const std::int64_t folded = c.fold_rows ? c.N * c.fold_u * c.W * c.fold_cv : c.N * c.fold_u * c.fold_v * c.fold_c;
     if (c.pack_k <= 1024 && folded < (1ll << 34) && !conv_igemm_unsupported(c)) {
       PBuffer f;
       f.name = "fold:" + plan->bufs[c.a_buf].name;

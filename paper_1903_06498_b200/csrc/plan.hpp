@@ -161,6 +161,10 @@ struct ConvPlan {
   // fold_u x fold_v of them per image): fold_r tap rows of one fold_cv-byte "pixel" each,
   // the fold_cv / fold_c folded pixels from (U, y) on (see packed_view())
   std::int64_t fold_x = 0, fold_y = 0, fold_c = 0, fold_r = 0, fold_s = 0, fold_cv = 0, fold_u = 0, fold_v = 0;
+  // fold_rows: the folded input is materialised as rows T[n, U, y] = F[n, U, y .. y + fold_cv /
+  // fold_c - 1] (fold_cv bytes, 64-byte aligned TMA rows; ~2x the im2col rate of the
+  // overlapping-stride view) instead of the folded pixels themselves
+  bool fold_rows = false;
 };
 
 // Statement-DAG concurrency (schedule.cpp): independent steps on up to N streams.
