@@ -93,6 +93,8 @@ FUSED = [
     # large M with N <= 128: two 128-row sub-tiles per tile (M = 2 x 128 rows, one stage handshake)
     (32, 56, 56, 64, 64, 3, 3, 1, 1, True, False),
     (27, 56, 56, 64, 128, 1, 1, 1, 0, True, True),  # + residual per sub-tile, ragged last tile
+    (2, 14, 14, 64, 320, 1, 1, 1, 0, True, True),   # 256-wide tiles, last n-tile 64 wide + residual
+    (4, 14, 14, 256, 256, 3, 3, 1, 1, True, False),  # streamed 3x3 filter, 18 k-blocks
 ]
 
 
@@ -152,6 +154,7 @@ SMALL_C = [
     (1, 8, 8, 3, 200, 3, 3, 1, 0),        # no padding, K > 128
     (2, 13, 18, 3, 64, 7, 7, 2, 3),       # odd/even extents under the 2x2 fold
     (1, 11, 9, 5, 32, 3, 5, 3, 1),        # stride 3 fold (45 bytes per folded pixel)
+    (3, 15, 17, 3, 64, 7, 7, 2, 3),       # odd extents, materialised fold rows
 ]
 
 
