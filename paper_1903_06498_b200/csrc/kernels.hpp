@@ -93,9 +93,8 @@ cudaError_t launch_conv_tc(const ConvPlan& cp, const ConvArgs& args, cudaStream_
 // General im2col-TMA implicit GEMM (kernels/conv_igemm.cu): strides, 1x1, streamed filters.
 const char* conv_igemm_unsupported(const ConvPlan& cp);
 cudaError_t launch_conv_igemm(const ConvPlan& cp, const ConvArgs& args, cudaStream_t s, int num_sms);
-// Packs a small-channel conv's taps x channels per output pixel (and its filter) for the
-// 1x1 im2col GEMM (ConvPlan::packed).
-cudaError_t launch_conv_pack(const ConvPlan& cp, const void* a, const void* b, void* pa, void* pb, cudaStream_t s);
+// Packs a small-channel conv's filter for gather mode ([K, pack_k] rows) or the phase fold
+// ([fold_r][K][fold_cv]) (ConvPlan::packed).
 cudaError_t launch_conv_pack_filter(const ConvPlan& cp, const void* b, void* pb, cudaStream_t s);
 // Phase-folds the input of a folded small-channel conv (ConvPlan::fold_x) into f.
 cudaError_t launch_conv_fold(const ConvPlan& cp, const void* a, void* f, cudaStream_t s);

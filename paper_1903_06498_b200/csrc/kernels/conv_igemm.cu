@@ -1150,42 +1150,6 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
   return cudaSuccess;
 }
 
-// One thread per 16 packed bytes of one output pixel: kk -> (i, j, c), c fastest.
-__global__ void __launch_bounds__(256) conv_pack_kernel(const std::int8_t* __restrict__ a, std::int8_t* __restrict__ pa,
-                                                        long long pixels, int H, int W, int C, int S, int rsc, int kp,
-                                                        int sx, int sy, long long a_n, long long a_x, long long a_y,
-                                                        long long a0, int u_lo, int u_hi, int v_lo, int v_hi) {
-  const int chunks = kp / 16;
-  const long long total = pixels * chunks;
-  for (long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; g < total;
-       g += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long m = g / chunks;
-    const int ch = static_cast<int>(g - m * chunks);
-    const long long n = m / (static_cast<long long>(H) * W);
-    const int rem = static_cast<int>(m - n * H * W);
-    const int x = rem / W, y = rem - x * W;
-    std::uint32_t w[4];
-#pragma unroll
-    for (int q = 0; q < 4; q++) {
-      std::uint32_t word = 0;
-#pragma unroll
-      for (int e = 0; e < 4; e++) {
-        const int kk = ch * 16 + q * 4 + e;
-        std::int8_t val = 0;
-        if (kk < rsc) {
-          const int c = kk % C, ij = kk / C;
-          const int i = ij / S, j = ij - i * S;
-          const int u = sx * x + i, v = sy * y + j;
-          if (u >= u_lo && u <= u_hi && v >= v_lo && v <= v_hi) val = a[a0 + a_n * n + a_x * u + a_y * v + c];
-        }
-        word |= static_cast<std::uint32_t>(static_cast<std::uint8_t>(val)) << (8 * e);
-      }
-      w[q] = word;
-    }
-    reinterpret_cast<uint4*>(pa)[g] = make_uint4(w[0], w[1], w[2], w[3]);
-  }
-}
-
 // kk layout: dense (i, j, c) when run == 0, else i * run + (j * C + c) with zero padding
 __global__ void conv_pack_filter_kernel(const std::int8_t* __restrict__ b, std::int8_t* __restrict__ pb, int K, int C,
                                         int R, int S, int run, int kp, long long b_i, long long b_j, long long b_k,
@@ -1443,25 +1407,6 @@ cudaError_t launch_conv_pack_filter(const ConvPlan& cp, const void* b, void* pb,
                                              static_cast<int>(cp.K), static_cast<int>(cp.C), static_cast<int>(cp.R),
                                              static_cast<int>(cp.S), static_cast<int>(cp.pack_run), kp, cp.b_i, cp.b_j,
                                              cp.b_k, cp.b_c, cp.b0);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_conv_pack(const ConvPlan& cp, const void* a, const void* b, void* pa, void* pb, cudaStream_t s) {
-  const long long pixels = cp.N * cp.H * cp.W;
-  const int kp = static_cast<int>(cp.pack_k), rsc = static_cast<int>(cp.R * cp.S * cp.C);
-  const long long work = pixels * (kp / 16);
-  const long long blocks = std::min<long long>((work + 255) / 256, 148 * 16);
-  conv_pack_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(
-      static_cast<const std::int8_t*>(a), static_cast<std::int8_t*>(pa), pixels, static_cast<int>(cp.H),
-      static_cast<int>(cp.W), static_cast<int>(cp.C), static_cast<int>(cp.S), rsc, kp, static_cast<int>(cp.sx),
-      static_cast<int>(cp.sy), cp.a_n, cp.a_x, cp.a_y, cp.a0, static_cast<int>(cp.u_lo), static_cast<int>(cp.u_hi),
-      static_cast<int>(cp.v_lo), static_cast<int>(cp.v_hi));
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  const int fb = static_cast<int>(std::min<long long>((cp.K * kp + 255) / 256, 1024));
-  conv_pack_filter_kernel<<<fb, 256, 0, s>>>(static_cast<const std::int8_t*>(b), static_cast<std::int8_t*>(pb),
-                                             static_cast<int>(cp.K), static_cast<int>(cp.C), static_cast<int>(cp.R),
-                                             static_cast<int>(cp.S), 0, kp, cp.b_i, cp.b_j, cp.b_k, cp.b_c, cp.b0);
   return cudaGetLastError();
 }
 
