@@ -119,6 +119,13 @@ int sb_count_valid_points(sb_context* ctx, const sb_program* p, const char* bloc
  * Shards' outputs combine with the output's aggregation (all-reduce sum/max/min/prod). */
 int sb_program_restrict_index(const sb_program* p, const char* block_path, const char* index, int64_t lo,
                               int64_t hi, sb_program** out);
+/* SB_OK when splitting ranged `index` of the block at `block_path` across shards and
+ * combining the shards' outputs with each output's aggregation is exact; otherwise
+ * SB_ERR_UNSUPPORTED with the reason (an assigned output, a store whose aggregation differs
+ * from the output's, a read of an output or a write to an outer local inside the block, or
+ * an output written outside it).  The reference has no split (tile.cpp:668-685 refuses
+ * aggregation indexes in `partition`); this states the condition under which one is exact. */
+int sb_program_check_split(const sb_program* p, const char* block_path, const char* index);
 /* Human-readable launch plan (which kernel family / execution mode per block).
  * `disable_tensor_cores` bit 0: generic kernels only; bit 1: plan for SB_FP32_TF32X3. */
 int sb_program_describe_plan(sb_program* p, int fresh_outputs, int disable_tensor_cores, char* buf,

@@ -34,12 +34,24 @@ inline void check(int rc) {
   throw ExecError(colon == std::string::npos ? sb_status_name(rc) : msg.substr(0, colon), msg);
 }
 
-// One device context per process (device 0 unless selected before first use).
+// One device context per host thread (and device): concurrent execute calls on disjoint
+// stores run on their own streams, staging and device buffers -- "execute is reentrant; a
+// single invocation owns its BufferStore exclusively".  Each context is
+// destroyed when its thread exits.
 inline sb_context* context(int device = 0) {
-  static std::once_flag once;
-  static sb_context* ctx = nullptr;
-  std::call_once(once, [&] { check(sb_context_create(device, &ctx)); });
-  return ctx;
+  struct Holder {
+    std::map<int, sb_context*> ctx;
+    ~Holder() {
+      for (auto& [d, c] : ctx) sb_context_destroy(c);
+    }
+  };
+  thread_local Holder h;
+  auto it = h.ctx.find(device);
+  if (it != h.ctx.end()) return it->second;
+  sb_context* c = nullptr;
+  check(sb_context_create(device, &c));
+  h.ctx.emplace(device, c);
+  return c;
 }
 
 // Parsed programs cached by canonical text (plans and device state live with them).

@@ -4,7 +4,10 @@
 // file given it runs stripe::execute (the reference) and stripe::b200::execute (the B200
 // executor through the C ABI) on the same random inputs and compares every buffer.
 //
-//   dropin_test [--seed S] prog1.stripe [prog2.stripe ...]
+//   dropin_test [--seed S] [--threads T] prog1.stripe [prog2.stripe ...]
+// With --threads T (> 1) every program is additionally run by T concurrent host threads,
+// each through stripe::b200::execute on its own copy of the store (disjoint stores, the
+// reference's reentrancy contract SPEC.md:263), every copy compared with the reference.
 // Prints one line per program ("OK <name>" / "DIFF <name> ..." / "ERR <name> code code");
 // exit status = number of mismatches.  Error parity: when the reference throws ExecError,
 // the binding must throw the same code.
@@ -13,19 +16,35 @@
 #include <fstream>
 #include <sstream>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "stripe/interp.h"
 #include "stripe/text.h"
 #include "stripe_b200_binding.hpp"
 #include "support.h"
 
+static bool same_store(const stripe::BufferStore& a, const stripe::BufferStore& b) {
+  if (a.size() != b.size()) return false;
+  for (const auto& [name, buf] : b) {
+    const auto it = a.find(name);
+    if (it == a.end() || it->second.data != buf.data) return false;
+  }
+  return true;
+}
+
 int main(int argc, char** argv) {
   std::uint64_t seed = 1001;
+  int threads = 1;
   int bad = 0;
   for (int i = 1; i < argc; i++) {
     std::string arg = argv[i];
     if (arg == "--seed" && i + 1 < argc) {
       seed = std::strtoull(argv[++i], nullptr, 10);
+      continue;
+    }
+    if (arg == "--threads" && i + 1 < argc) {
+      threads = std::atoi(argv[++i]);
       continue;
     }
     std::ifstream f(arg);
@@ -71,6 +90,31 @@ int main(int argc, char** argv) {
     }
     std::printf("%s %s%s\n", diff.empty() ? "OK" : "DIFF", arg.c_str(), diff.c_str());
     bad += diff.empty() ? 0 : 1;
+    if (threads > 1) {
+      // T host threads, disjoint stores, all at once through the binding
+      stripe::testing::Rng rng2(seed);
+      const stripe::BufferStore inputs = stripe::testing::random_inputs(prog, &rng2);
+      std::vector<stripe::BufferStore> stores(threads, inputs);
+      std::vector<std::string> errs(threads);
+      std::vector<std::thread> pool;
+      for (int t = 0; t < threads; t++)
+        pool.emplace_back([&, t] {
+          try {
+            for (int rep = 0; rep < 3; rep++) {
+              stores[t] = inputs;
+              stripe::b200::execute(prog, &stores[t]);
+            }
+          } catch (const stripe::ExecError& e) {
+            errs[t] = e.code;
+          }
+        });
+      for (auto& th : pool) th.join();
+      int tbad = 0;
+      for (int t = 0; t < threads; t++)
+        if (!errs[t].empty() || !same_store(stores[t], ref)) tbad++;
+      std::printf("%s %s threads=%d mismatching=%d\n", tbad ? "DIFF" : "OK", arg.c_str(), threads, tbad);
+      bad += tbad ? 1 : 0;
+    }
   }
   return bad;
 }

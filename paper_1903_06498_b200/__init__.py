@@ -43,7 +43,7 @@ EXPORTED = [
     "sb_last_error", "sb_status_name", "sb_abi_version",
     "sb_program_parse", "sb_program_free", "sb_program_print", "sb_program_buffer_count",
     "sb_program_buffer_info", "sb_program_output_identity", "sb_program_describe_plan",
-    "sb_program_output_aggregation", "sb_program_restrict_index", "sb_count_valid_points",
+    "sb_program_output_aggregation", "sb_program_restrict_index", "sb_program_check_split", "sb_count_valid_points",
     "sb_context_create", "sb_context_destroy", "sb_context_set_stream", "sb_context_stream",
     "sb_context_sync", "sb_context_launch_count", "sb_device_alloc", "sb_device_free",
     "sb_host_alloc_pinned", "sb_host_free_pinned", "sb_execute", "sb_execute_device", "sb_execute_async",
@@ -89,6 +89,7 @@ def lib() -> ctypes.CDLL:
         L.sb_program_output_identity.argtypes = [vp, ctypes.c_char_p, ctypes.POINTER(i64)]
         L.sb_program_output_aggregation.argtypes = [vp, ctypes.c_char_p, ctypes.POINTER(i32)]
         L.sb_program_restrict_index.argtypes = [vp, ctypes.c_char_p, ctypes.c_char_p, i64, i64, ctypes.POINTER(vp)]
+        L.sb_program_check_split.argtypes = [vp, ctypes.c_char_p, ctypes.c_char_p]
         L.sb_count_valid_points.argtypes = [vp, vp, ctypes.c_char_p, ctypes.POINTER(i64)]
         L.sb_program_describe_plan.argtypes = [vp, i32, i32, ctypes.c_char_p, ctypes.c_size_t,
                                                ctypes.POINTER(ctypes.c_size_t)]
@@ -194,6 +195,11 @@ class Program:
         h = ctypes.c_void_p()
         _check(lib().sb_program_restrict_index(self._h, block_path.encode(), index.encode(), lo, hi, ctypes.byref(h)))
         return Program(h.value)
+
+    def check_split(self, block_path: str, index: str) -> None:
+        """Raises ExecError('Unsupported') unless shards of `index` combine exactly
+        (sb_program_check_split)."""
+        _check(lib().sb_program_check_split(self._h, block_path.encode(), index.encode()))
 
     def text(self) -> str:
         return print_program(self)

@@ -93,6 +93,11 @@ struct sb_program {
 };
 
 struct sb_context {
+  // One execute at a time per context: the staging buffers, root buffers, plan states and
+  // the PDL window below are mutated by every execute ("execute is reentrant",
+  // concurrent callers on one context serialize here; callers wanting
+  // concurrency use one context per thread, as stripe::b200::execute does).
+  std::recursive_mutex mu;
   int device = 0;
   int num_sms = 148;
   cudaStream_t own = nullptr;
@@ -172,6 +177,7 @@ sb_program::~sb_program() {
   std::lock_guard<std::mutex> lock(g_registry_mu);
   for (auto& [key, c] : plans) {
     for (sb_context* ctx : g_contexts) {
+      std::lock_guard<std::recursive_mutex> cl(ctx->mu);
       auto it = ctx->states.find(c->id);
       if (it == ctx->states.end()) continue;
       cudaSetDevice(ctx->device);
@@ -339,16 +345,43 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
   const auto& plan = c->plan;
   auto ptr_of = [&](int b) { return plan.bufs[b].root ? root_ptr[plan.bufs[b].root_index] : st.scratch[b]; };
   const bool single_lane = c->lanes.nlanes <= 1;
+  auto span_of = [&](int b) {
+    const auto lo = reinterpret_cast<std::uintptr_t>(ptr_of(b));
+    return sb_context::Span{lo, lo + static_cast<std::uintptr_t>(plan.bufs[b].elements * kind_bytes(plan.bufs[b].kind))};
+  };
+  // writes of launches of earlier executes that may still run on this stream
+  std::vector<sb_context::Span> carried_wr;
+  for (const auto& w : ctx->window) carried_wr.insert(carried_wr.end(), w.wr.begin(), w.wr.end());
   // Dependency-aware PDL: a tensor-core launch that touches nothing an in-flight launch writes
   // (and writes nothing one reads) need not wait for its predecessor at all, so consecutive
   // independent executes overlap completely (the previous grid's tail wave is filled).
-  auto pdl_mode = [&](std::size_t i, bool load_early_ok) -> int {
+  // The kernels release their dependents only after their own griddepcontrol.wait has
+  // returned (then their predecessor has completed), so after a waiting launch only that
+  // launch may still run when the next one starts; the window holds it.  Free launches (no
+  // wait) release at entry and accumulate in the window.
+  // `early_b` (in/out): the launch wants to fetch plan buffer `early_b_buf` before its wait;
+  // cleared when any launch that may still run writes bytes of it (e.g. the previous
+  // execute's kernel producing this program's filter).
+  auto pdl_mode = [&](std::size_t i, bool load_early_ok, int early_b_buf = -1, bool* early_b = nullptr) -> int {
     // Free is opt-in (SB_PDL_FREE=1): measured no gain on the configs. LoadEarly (default
     // for the resident-filter conv): when only the immediately preceding launch may still run
     // and it writes nothing this launch reads, the loads and MMAs start at once and only the
     // stores wait for the predecessor (WAW / WAR ordering kept).
     static const bool allow_free = std::getenv("SB_PDL_FREE") != nullptr;
     static const bool load_early = std::getenv("SB_PDL_NO_EARLY") == nullptr;
+    auto ov = [](const std::vector<sb_context::Span>& x, const std::vector<sb_context::Span>& y) {
+      for (const auto& a : x)
+        for (const auto& b : y)
+          if (a.lo < b.hi && b.lo < a.hi) return true;
+      return false;
+    };
+    if (early_b && *early_b && early_b_buf >= 0) {
+      // b_immutable: no step of this plan writes it; only earlier executes on this stream can
+      const std::vector<sb_context::Span> bs{span_of(early_b_buf)};
+      if (ov(carried_wr, bs)) *early_b = false;
+      for (const auto& w : ctx->window)
+        if (ov(w.wr, bs)) *early_b = false;
+    }
     if (!single_lane) {
       ctx->window.clear();
       return sb::kPdlWait;
@@ -356,18 +389,8 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
     std::vector<int> rd, wr;
     sb::step_access(plan.steps[i], &rd, &wr);
     sb_context::InFlight me;
-    auto span = [&](int b) {
-      const auto lo = reinterpret_cast<std::uintptr_t>(ptr_of(b));
-      return sb_context::Span{lo, lo + static_cast<std::uintptr_t>(plan.bufs[b].elements * kind_bytes(plan.bufs[b].kind))};
-    };
-    for (int b : rd) me.rd.push_back(span(b));
-    for (int b : wr) me.wr.push_back(span(b));
-    auto ov = [](const std::vector<sb_context::Span>& x, const std::vector<sb_context::Span>& y) {
-      for (const auto& a : x)
-        for (const auto& b : y)
-          if (a.lo < b.hi && b.lo < a.hi) return true;
-      return false;
-    };
+    for (int b : rd) me.rd.push_back(span_of(b));
+    for (int b : wr) me.wr.push_back(span_of(b));
     bool raw = false, any = false;
     for (const auto& w : ctx->window) {
       raw |= ov(w.wr, me.rd);
@@ -406,13 +429,14 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
       a.a_elems = plan.bufs[l.conv.a_buf].elements;
       a.b_elems = plan.bufs[l.conv.b_buf].elements;
       a.c_elems = plan.bufs[l.conv.c_buf].elements;
-      a.b_immutable = l.conv.b_immutable;
+      bool b_early = l.conv.b_immutable;
       if (l.conv.epi_vec) {
         a.vec = ptr_of(l.conv.vec_buf);
         a.vec_kind = plan.bufs[l.conv.vec_buf].kind;
       }
       if (l.conv.epi_res) a.res = ptr_of(l.conv.res_buf);
-      if (tc_single) a.pdl_mode = pdl_mode(i, l.kernel == sb::KernelKind::ConvI8TC);
+      if (tc_single) a.pdl_mode = pdl_mode(i, l.kernel == sb::KernelKind::ConvI8TC, l.conv.b_buf, &b_early);
+      a.b_immutable = b_early;
       if (l.kernel == sb::KernelKind::ConvI8TC) {
         cuda_check(sb::launch_conv_tc(l.conv, a, ctx->stream, ctx->num_sms), "conv_tc");
       } else if (l.conv.packed && l.conv.fold_x) {
@@ -596,6 +620,18 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
       cuda_check(cudaEventRecord(ev(&ctx->join_events[L]), ctx->lane_streams[L]), "join");
       cuda_check(cudaStreamWaitEvent(main, ctx->join_events[L], 0), "join wait");
     }
+    // conservatively, any of this execute's launches may still run when the next one starts:
+    // its reads and writes form one in-flight entry for the next execute's PDL decisions
+    sb_context::InFlight all;
+    for (std::size_t i = 0; i < plan.steps.size(); i++) {
+      if (plan.steps[i].elided) continue;
+      std::vector<int> rd, wr;
+      sb::step_access(plan.steps[i], &rd, &wr);
+      for (int b : rd) all.rd.push_back(span_of(b));
+      for (int b : wr) all.wr.push_back(span_of(b));
+    }
+    ctx->window.clear();
+    ctx->window.push_back(std::move(all));
     return;
   }
   if (!profile) {
@@ -723,6 +759,7 @@ int sb_program_output_aggregation(const sb_program* p, const char* name, int* ag
 
 int sb_count_valid_points(sb_context* ctx, const sb_program* p, const char* block_path, int64_t* count) {
   return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lock(ctx->mu);
     cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
     const sb::Block* b = &p->prog.root;
     std::string path = block_path ? block_path : "";
@@ -781,6 +818,10 @@ int sb_program_restrict_index(const sb_program* p, const char* block_path, const
   });
 }
 
+int sb_program_check_split(const sb_program* p, const char* block_path, const char* index) {
+  return guarded([&] { sb::check_split(p->prog, block_path ? block_path : "", index ? index : ""); });
+}
+
 int sb_program_describe_plan(sb_program* p, int fresh_outputs, int disable_tc, char* buf, size_t cap,
                              size_t* len) {
   return guarded([&] {
@@ -836,6 +877,7 @@ void sb_context_destroy(sb_context* ctx) { delete ctx; }
 
 int sb_context_set_stream(sb_context* ctx, void* s) {
   return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lock(ctx->mu);
     ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own;
     ctx->window.clear();
   });
@@ -845,6 +887,7 @@ void* sb_context_stream(sb_context* ctx) { return ctx->stream; }
 
 int sb_context_sync(sb_context* ctx) {
   return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lock(ctx->mu);
     cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
     ctx->window.clear();
     ctx->h_err->code = 1;
@@ -852,7 +895,10 @@ int sb_context_sync(sb_context* ctx) {
   });
 }
 
-uint64_t sb_context_launch_count(sb_context* ctx) { return ctx->launches; }
+uint64_t sb_context_launch_count(sb_context* ctx) {
+  std::lock_guard<std::recursive_mutex> lock(ctx->mu);
+  return ctx->launches;
+}
 
 int sb_device_alloc(sb_context* ctx, int64_t bytes, void** dptr) {
   return guarded([&] {
@@ -877,6 +923,7 @@ int sb_host_free_pinned(void* ptr) { return guarded([&] { cuda_check(cudaFreeHos
 int sb_execute_device(sb_context* ctx, sb_program* p, const sb_device_buffer* bufs, int n,
                       const sb_exec_options* opts) {
   return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lock(ctx->mu);
     check_opts(opts);
     cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
     const auto& prog = p->prog;
@@ -910,6 +957,7 @@ int sb_execute_device(sb_context* ctx, sb_program* p, const sb_device_buffer* bu
                                      ctx->stream),
                      "prepare_outputs");
           ctx->launches++;
+          ctx->window.clear();  // a plain stream-ordered launch: everything before it has completed
         }
       }
     }
@@ -922,6 +970,7 @@ int sb_execute_device(sb_context* ctx, sb_program* p, const sb_device_buffer* bu
 namespace {
 int execute_host(sb_context* ctx, sb_program* p, sb_host_buffer* bufs, int n, const sb_exec_options* opts, bool async) {
   return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lock(ctx->mu);
     ctx->window.clear();  // host copies serialize the stream
     if (async)
       for (int i = 0; i < n; i++)
@@ -1064,6 +1113,7 @@ extern "C" {
 
 int sb_graph_begin(sb_context* ctx) {
   return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lock(ctx->mu);
     cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
     g_capture_mark = ctx->launches;
     ctx->window.clear();
@@ -1073,6 +1123,7 @@ int sb_graph_begin(sb_context* ctx) {
 
 int sb_graph_end(sb_context* ctx, sb_graph** out) {
   return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lock(ctx->mu);
     ctx->window.clear();
     auto g = std::make_unique<sb_graph>();
     cuda_check(cudaStreamEndCapture(ctx->stream, &g->graph), "cudaStreamEndCapture");
@@ -1085,6 +1136,7 @@ int sb_graph_end(sb_context* ctx, sb_graph** out) {
 
 int sb_graph_launch(sb_context* ctx, sb_graph* g) {
   return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lock(ctx->mu);
     cuda_check(cudaGraphLaunch(g->exec, ctx->stream), "cudaGraphLaunch");
     ctx->launches += g->kernels;
   });

@@ -271,10 +271,13 @@ void shift_index(Block* b, const std::string& idx, std::int64_t lo, bool own) {
     if (k) a.constant += k * lo;
   };
   if (!own) {
-    for (auto& i : b->indexes) {
-      if (i.is_alias) fix(i.alias);  // aliases read the parent scope
-      if (i.name == idx) return;     // shadowed below this point
-    }
+    // every alias reads the parent scope (interp.cpp:210), whatever its position among the
+    // block's indexes -- tile_rewrite emits `[x:3, ..., xo = 3*x]` with the child's ranged x
+    // declared before the alias that reads the parent's x (testdata/fig6b.stripe)
+    for (auto& i : b->indexes)
+      if (i.is_alias) fix(i.alias);
+    for (const auto& i : b->indexes)
+      if (i.name == idx) return;  // shadowed below this point
   }
   for (auto& c : b->constraints) fix(c);
   for (auto& r : b->refs)
@@ -306,6 +309,108 @@ Program restrict_index(const Program& p, const std::string& path, const std::str
   shift_index(b, idx, lo, true);
   if (b->has_annotation) b->annotation = b->range_product();
   return q;
+}
+
+namespace {
+
+// Binding of a refinement name in some scope: a root buffer, or a local allocation
+// (declared in the block `owner`, interp.cpp:234-247).
+struct Bound {
+  int root = -1;                 // root buffer index, else local
+  const Block* owner = nullptr;  // declaring block of a local
+  bool local_inside = false;     // local declared at or below the split block
+};
+
+
+struct SplitCheck {
+  const Program& p;
+  const Block* split;
+  std::string why;
+
+  void fail(const std::string& w) {
+    if (why.empty()) why = w;
+  }
+
+  void walk(const Block& b, const std::map<std::string, Bound>& parent, bool inside) {
+    inside = inside || &b == split;
+    std::map<std::string, Bound> env;
+    for (const auto& r : b.refs) {
+      Bound x;
+      if (&b == &p.root) {
+        x.root = p.buffer_index(r.name);
+      } else {
+        auto it = parent.find(r.name);
+        if (it != parent.end()) {
+          x = it->second;
+        } else {
+          x.owner = &b;
+          x.local_inside = inside;
+        }
+      }
+      env[r.name] = x;
+    }
+    auto agg_of = [&](const std::string& name) {
+      const Refinement* r = b.find_ref(name);
+      return r && r->has_agg ? r->agg : Agg::Assign;
+    };
+    auto on_write = [&](const std::string& name) {
+      auto it = env.find(name);
+      if (it == env.end()) return;
+      const Bound& x = it->second;
+      const bool out = x.root >= 0 && p.buffers[x.root].dir != Dir::In;
+      if (!inside) {
+        if (out) fail("a statement outside the split block writes output '" + name + "' (it would run on every shard)");
+        return;
+      }
+      if (x.root >= 0) {
+        const Agg a = output_aggregation(p, p.buffers[x.root].name);
+        if (a == Agg::Assign)
+          fail("output '" + p.buffers[x.root].name + "' is assigned, not aggregated: it cannot be split");
+        else if (agg_of(name) != a)
+          fail("a store into '" + name + "' aggregates differently from the output's combine");
+      } else if (!x.local_inside) {
+        fail("local '" + name + "' declared outside the split block would carry partial results");
+      }
+    };
+    auto on_read = [&](const std::string& name) {
+      if (!inside) return;
+      auto it = env.find(name);
+      if (it != env.end() && it->second.root >= 0 && p.buffers[it->second.root].dir != Dir::In)
+        fail("the split block reads output '" + name + "' (a partial value on each shard)");
+    };
+    for (const auto& st : b.stmts) {
+      switch (st.kind) {
+        case StmtKind::Load: on_read(st.from); break;
+        case StmtKind::Store: on_write(st.into); break;
+        case StmtKind::Special:
+          if (!st.refs.empty()) on_write(st.refs[0]);
+          for (std::size_t k = 1; k < st.refs.size(); k++) on_read(st.refs[k]);
+          break;
+        case StmtKind::Block: walk(*st.block, env, inside); break;
+        default: break;
+      }
+    }
+  }
+};
+
+}  // namespace
+
+void check_split(const Program& p, const std::string& path, const std::string& idx) {
+  const Block* b = &p.root;
+  std::stringstream ss(path);
+  std::string part;
+  while (!path.empty() && std::getline(ss, part, '.')) {
+    const std::size_t k = static_cast<std::size_t>(std::stoll(part));
+    if (k >= b->stmts.size() || b->stmts[k].kind != StmtKind::Block)
+      throw Error("Unsupported", "no block at path '" + path + "'");
+    b = b->stmts[k].block.get();
+  }
+  bool ranged = false;
+  for (const auto& i : b->indexes) ranged |= i.name == idx && !i.is_alias;
+  if (!ranged) throw Error("UnboundIndex", "block '" + path + "' has no ranged index '" + idx + "'");
+  SplitCheck c{p, b, {}};
+  c.walk(p.root, {}, false);
+  if (!c.why.empty()) throw Error("Unsupported", "index '" + idx + "' cannot be split across shards: " + c.why);
 }
 
 std::int64_t output_identity(const Program& p, const std::string& name) {

@@ -188,5 +188,11 @@ Agg output_aggregation(const Program& p, const std::string& name);
 // combine with the output's aggregation (add: sum, max, min, mul: product).
 Program restrict_index(const Program& p, const std::string& path, const std::string& idx, std::int64_t lo,
                        std::int64_t hi);
+// Throws Error("Unsupported") unless the shards of ranged index `idx` of the block at `path`
+// combine exactly with each output's aggregation: every write inside the block's subtree
+// goes to a root output whose aggregation (add/max/min/mul) the store uses, or to a local
+// declared at or below the block; nothing inside reads an output; nothing outside writes
+// one (it would run on every shard).
+void check_split(const Program& p, const std::string& path, const std::string& idx);
 
 }  // namespace sb

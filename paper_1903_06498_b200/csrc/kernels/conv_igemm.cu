@@ -263,7 +263,9 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
   __syncthreads();
   tc_fence_after();
   const std::uint32_t tmem_base = *tmem_slot;
-  if (p.pdl && threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // Dependents are released only after a griddepcontrol.wait of this grid returned (the
+  // predecessor has completed): at most this launch and its successor overlap.
+  if (p.pdl && !p.pdl_wait && threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // TMA producers.  One thread issues a tensor load only every ~260 cycles whatever the box
   // size (measured, scratch/tma_lat.cu), so im2col mode splits the issue over four warps:
@@ -277,7 +279,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       const bool do_a = !p.gather && (pidx & 1) == 0 && pidx != 4, do_b = p.gather || (pidx & 1) == 1;
       // an immutable resident filter (a root `in` buffer no plan step writes) is fetched while
       // the predecessor still runs; everything else waits for it
-      if (p.pdl_wait && !(p.b_early && do_b && p.b_res)) asm volatile("griddepcontrol.wait;" ::: "memory");
+      if (p.pdl_wait && !(p.b_early && do_b && p.b_res)) asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory");
       const int nchains = p.gather ? 1 : 2, chain = p.gather ? 0 : pidx >> 1;
       const int PQ = p.P * p.Q;
       if (pidx == 4) {
@@ -476,7 +478,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
         tdj[kk] = 0;
       }
     }
-    if (p.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (p.pdl_wait) asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("bar.sync 2, 256;" ::: "memory");
     const int PQ = p.P * p.Q;
     const int sw = p.bk == 128 ? (r & 7) : ((r >> 1) & 3);
@@ -591,7 +593,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       // per-output-channel vector (e.g. the bias) as int32 in smem, read with ld.shared.v4; with
       // fast_clamp also the threshold t[k] = clamp32(lo - vec[k]): acc + res + vec >= lo
       // <=> acc + res >= t[k] exactly, because |acc + res| < 2^31 - 1
-      if (p.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
+      if (p.pdl_wait) asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory");
       for (int k = threadIdx.x - 64; k < p.N; k += ethreads) {
         const long long vi = static_cast<long long>(k) * p.vec_k;
         const std::int32_t b = !p.epi_vec ? 0
@@ -609,7 +611,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
     if (p.epi_vec)  // zero tail: chunk loads past N need no bounds select
       for (int k = p.N + threadIdx.x - 64; k < (p.N + p.bn - 1) / p.bn * p.bn && k < kMaxVecK; k += ethreads) vec_s[k] = 0;
     const bool eres = p.epi_res && !p.res_mma;  // residual read by the epilogue (else added by the MMAs)
-    if (eres && leader && p.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (eres && leader && p.pdl_wait) asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("bar.sync 1, %0;" ::"r"(ethreads) : "memory");
     // fast8 clamp: max(acc + res + vec, lo) in int32 when no |vec[k]| can overflow it, else the
     // exact threshold form acc + res >= clamp32(lo - vec[k]) (both keep the wrapped low byte)

@@ -223,7 +223,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const std::uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) trace_at(p.trace, 49);
   // the next kernel in the stream may start its prologue as soon as SMs free up
-  if (p.pdl && threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // Dependents are released only after this grid's own griddepcontrol.wait returned (then
+  // the predecessor has completed), so at most this launch and its successor overlap: the
+  // executor's in-flight window holds one launch.  Non-waiting (free) launches release at once.
+  if (p.pdl && !p.pdl_wait && !p.store_wait && threadIdx.x == 0)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0) {
     if (lane == 0) {
@@ -273,7 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           load_filter();
           filter_issued = true;
         }
-        asm volatile("griddepcontrol.wait;" ::: "memory");
+        asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory");
       }
       int stage = 0;
       std::uint32_t phase = 0;
@@ -370,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ethreads = split ? 256 : 128;
     const int quarter = warp & 3;  // TMEM lanes 32*quarter .. +31
     const int row = quarter * 32 + lane;
-    if (p.store_wait) asm volatile("griddepcontrol.wait;" ::: "memory");  // WAW/WAR with the predecessor
+    if (p.store_wait) asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory");  // WAW/WAR with the predecessor
     const int xl = row / p.P;
     const int y = row % p.P;
     int iter = 0;

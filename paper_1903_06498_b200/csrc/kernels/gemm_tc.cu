@@ -159,11 +159,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const std::uint32_t tmem_base = *tmem_slot;
-  if (p.pdl && threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // dependents are released after this grid's wait (see conv_tc.cu)
+  if (p.pdl && !p.pdl_wait && threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0) {
     if (lane == 0) {
-      if (p.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
+      if (p.pdl_wait) asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory");
       int stage = 0;
       std::uint32_t phase = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {

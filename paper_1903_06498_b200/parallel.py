@@ -21,6 +21,7 @@ AGG_OPS = {1: "SUM", 2: "MAX", 3: "MIN", 4: "PRODUCT"}
 
 
 def shard_aggregation(program: Program, block_path: str, index: str, extent: int, world: int, rank: int) -> Program:
+    program.check_split(block_path, index)  # exact only when every path is a linear combine
     lo, hi = shard_range(extent, world, rank)
     return program.restrict_index(block_path, index, lo, hi)
 
@@ -32,7 +33,8 @@ def _wrap(x: np.ndarray, bits: int) -> np.ndarray:
 
 def allreduce_outputs(program: Program, outputs: Dict[str, object], group=None) -> None:
     """outputs: name -> torch tensor (int64 carriers on CPU/gloo, or native-width on GPU/NCCL),
-    reduced in place across `group` with each output's aggregation."""
+    reduced in place across `group` with each output's aggregation.  The shards must come
+    from shard_aggregation (whose check_split proves the combine exact)."""
     import torch
     import torch.distributed as dist
     for name, t in outputs.items():

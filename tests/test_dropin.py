@@ -37,3 +37,29 @@ def test_reference_side_dropin(tmp_path):
     bad = [l for l in lines if not l.startswith(("OK", "SKIP"))]
     assert r.returncode == 0 and not bad, "\n".join(bad[:20]) + r.stderr[-2000:]
     assert sum(l.startswith("OK") for l in lines) >= len(files) - 2
+
+
+@pytest.mark.gpu
+def test_reference_side_dropin_concurrent_threads(tmp_path):
+    """8 host threads call stripe::b200::execute at once on disjoint stores (SPEC.md:263:
+    execute is reentrant); every thread's store must equal stripe::execute's."""
+    if not gpu_available():
+        pytest.skip("no B200")
+    if not os.path.exists(BIN):
+        pytest.skip("oracle/_ref/dropin_test not built (needs /root/reference at build time)")
+    from paper_1903_06498_b200 import workloads as W
+    progs = {"c2_small": W.conv2d(2, 12, 12, 64, 64), "igemm_s2": W.conv2d(1, 9, 9, 64, 128, pad=1, stride=2),
+             "fused": W.conv_fused(1, 8, 8, 64, 64), "pool": W.pool2d(2, 9, 9, 16),
+             "limb": W.matmul(64, 48, 32, in_dtype="i32", out_dtype="i32")}
+    for c in corpus():
+        if c.name in ("fx_matmul64", "fx_conv_relu", "fx_gather", "rnd_prog_03", "tile_conv_x3y4"):
+            progs[c.name] = c.text
+    files = []
+    for name, text in progs.items():
+        p = tmp_path / f"{name}.stripe"
+        p.write_text(text)
+        files.append(str(p))
+    r = subprocess.run([BIN, "--seed", "77", "--threads", "8"] + files, capture_output=True, text=True, timeout=600)
+    lines = [l for l in r.stdout.splitlines() if "threads=" in l]
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert len(lines) >= len(files) - 1 and all(l.startswith("OK") for l in lines), r.stdout

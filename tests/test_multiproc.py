@@ -160,3 +160,49 @@ def test_split_k_shards_on_device():
         total += st["C"].data
     full = (A.reshape(256, 512) @ B.reshape(512, 128)).ravel()
     np.testing.assert_array_equal(wrap(32, total.astype(np.uint64)), wrap(32, full.astype(np.uint64)))
+
+
+def test_check_split_accepts_linear_and_rejects_nonlinear():
+    """a split is exact only when every path from the index to an output is a
+    combine with the output's own aggregation (sb_program_check_split)."""
+    import paper_1903_06498_b200 as sb
+    ok = [(W.matmul(12, 10, 37), "0", "k"), (W.global_sum(3, 7, 5, 16), "0", "x"),
+          (W.maxpool2x2(2, 6, 8, 16), "0", "i"), (W.conv2d(2, 6, 6, 8, 4, in_dtype="i32"), "0", "c")]
+    for text, path, idx in ok:
+        sb.parse_program(text).check_split(path, idx)
+    # conv -> local T (declared above the leaf) -> bias + relu -> O:assign: relu(partial) != partial
+    fused = sb.parse_program(W.conv_fused(1, 6, 6, 64, 64))
+    with pytest.raises(sb.ExecError) as e:
+        fused.check_split("0.0", "c")
+    assert e.value.code == "Unsupported"
+    # the epilogue block's own index writes an assigned output
+    with pytest.raises(sb.ExecError):
+        fused.check_split("0.1", "k")
+    # unknown index
+    with pytest.raises(sb.ExecError) as e:
+        fused.check_split("0.0", "zz")
+    assert e.value.code == "UnboundIndex"
+
+
+def test_restrict_index_shifts_tile_aliases_fig6b():
+    """restrict_index on the outer tile index of a tile_rewrite output shifts the
+    child's `xo = 3*x` alias even though the child's own ranged x is declared before it.
+    Shards of x (a partition index here) run one after the other over the same store must
+    equal the full program (reference fixture testdata/fig6b.stripe)."""
+    import paper_1903_06498_b200 as sb
+    from harness import corpus
+    from oracle import Ref
+    if not Ref.available():
+        pytest.skip("oracle/_ref not built")
+    case = next(c for c in corpus() if c.name == "fx_fig6b")
+    prog = sb.parse_program(case.text)
+    # the unmodified reference runs both the full program and the shards
+    full = Ref.execute(Ref.parse(case.text), dict(case.inputs))
+    for cuts in ((0, 2, 4), (0, 1, 3, 4)):
+        store = dict(case.inputs)
+        for lo, hi in zip(cuts, cuts[1:]):
+            shard = prog.restrict_index("0", "x", lo, hi)
+            store = Ref.execute(Ref.parse(sb.print_program(shard)), store)
+        for n in full:
+            assert np.array_equal(store[n][1], full[n][1]), (cuts, n)
+    assert not np.array_equal(full["O"][1], case.inputs["O"][1])
