@@ -1,24 +1,30 @@
 #!/usr/bin/env python
 """Benchmark of the B200 Stripe block executor (BASELINE.json contract).
 
-Workload (N=1): BASELINE config 2 — a 3x3 conv2d NHWC 56x56x64->64, batch 32,
-with padding constraints, as ONE Stripe block (paper_1903_06498_b200.workloads.conv2d),
-i8 x i8 -> i32 (the reference's integer semantics; bit-exact vs its interpreter).
-A step = prepare_outputs + execute of that program over one batch (the identity
-fill of the output is fused into the conv epilogue).  Multi-GPU: weak scaling,
-each rank runs its own batch-32 shard (the batch index partitions with no
-data-path collective).
+Default workload (N=1): BASELINE config 5 -- the ResNet-50-shaped Stripe program
+(paper_1903_06498_b200.workloads.resnet50: 53 convs, max-pool, residuals, global sum, fc) at
+its named global batch of 1024 images, i8 x i8 -> i32 with i8 activations (the reference's
+integer semantics; bit-exact vs its interpreter).  With N GPUs the batch index is sharded
+1024/N images per rank (strong scaling, no data-path collective).
 
-value  : useful GFLOP/s (2 x constraint-satisfying MAC points, tile.cpp:338-370),
-         inputs resident in HBM, max-over-ranks device time.
-e2e    : same metric through the public API (sb_execute) from pinned host
-         buffers: H2D of I and F and D2H of O inside the timed region.
---impl reference: the reference interpreter (oracle/_ref, stripe::execute) on
-         the host cores over a bounded sample of the same workload.
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5|c2|c3|c4a|c4b|c1|c1_i32]
+    python bench.py --impl reference ...   (the reference interpreter on the host cores)
 
---config c5: BASELINE config 5 instead -- the ResNet-50-shaped Stripe program
-         (workloads.resnet50), 128 images per GPU (batch 1024 over 8 GPUs, sharded on
-         the batch index, no collective).  value = useful GFLOP/s of the whole network.
+--gpus N starts N ranks itself (torch.distributed.run, NCCL only for the barrier and the
+max-over-ranks time) unless it already runs under a launcher (WORLD_SIZE set).
+
+A step = prepare_outputs + execute of the config's program over one batch.
+value  : useful GFLOP/s (2 x constraint-satisfying MAC points, tile.cpp:338-370) or, for the
+         memory-bound configs C4a/C4b, algorithmic GB/s; inputs resident in HBM, K steps
+         replayed as one CUDA graph, CUDA events on the launching stream, max over ranks.
+e2e    : the same metric through the public API from HOST buffers, host<->device copies
+         inside the timed region: `value` = sb_execute_async with native-width pinned buffers
+         (two contexts ping-ponging), `dropin` = sb_execute with int64 carriers (the
+         stripe::b200::execute boundary, synchronous, int64<->native conversion included).
+roofline: the dominant kernel family, from a per-step CUDA-event pass (sb_context_set_profile)
+         after the timed region; `network` = whole step against the same peak.
+cpu_baseline: the unmodified reference interpreter (oracle/_ref) on 1 and P host threads over
+         a bounded sample of the same workload (rank 0, N=1 only).
 """
 import argparse
 import ctypes
@@ -34,17 +40,29 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "Stripe-kernel GFLOP/s & GB/s vs B200 roofline at 1/2/4/8 GPU; x vs CPU ref"
-N_IMG, H, W, C, K = 32, 56, 56, 64, 64
 L2_BYTES = 126 * 1024 * 1024
+ISZ = {8: 1, 16: 2, 32: 4, 0x20F: 4}
 
 
+# ------------------------------------------------------------------------------------------
 def peaks():
+    """HBM and dense tensor peaks: MEASURED_PEAKS.json (driver) + profiles/r02_peaks.json
+    (int8 / tf32 dense measured on this pool's B200 by tools/measure_peaks.py)."""
+    out = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "kind": "fallback (B200_PROFILING.md)"}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
+        out.update(hbm_gbs=float(p["hbm_gbs"]), bf16_tflops=float(p["bf16_tflops"]), kind="measured")
     except Exception:
-        return 6650.0, 1590.0, "fallback"
+        pass
+    out["int8_tops"], out["int8_kind"] = 2 * out["bf16_tflops"], "derived: 2 x bf16"
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_peaks.json")) as f:
+            q = json.load(f)
+        out["int8_tops"], out["int8_kind"] = float(q["int8_tops"]), f"measured ({q['int8_how']})"
+    except Exception:
+        pass
+    return out
 
 
 class ClockSampler:
@@ -107,132 +125,176 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def dist_setup():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
+def dist_env():
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
 
 
 # ------------------------------------------------------------------------------------------
-def cpu_reference(samples_rows=8, threads=None, steps=1, warmup=0):
-    """Reference interpreter (unmodified stripe::execute from oracle/_ref) on host cores.
-    One step = `threads` concurrent executions (one per host thread, execute is reentrant,
-    SPEC.md:263) of a row-band sample of config 2: 1 image x `samples_rows` output rows."""
+# Config specs.  Everything a rank needs: its program text, useful work, algorithmic bytes,
+# which roofline bounds it, and the CPU-reference sample.
+def spec(cfg, world, rank, args):
+    from paper_1903_06498_b200 import workloads as Wk
+    s = {"cfg": cfg, "scaling": "weak"}
+    if cfg == "c5":
+        total = args.batch or 1024
+        lo, hi = Wk.shard_range(total, world, rank)
+        n = hi - lo
+        text, info = Wk.resnet50(n)
+        conv_flops = 2.0 * sum(c["macs"] for c in info["convs"])
+        s.update(text=text, flops=float(info["flops"]), unit="GFLOP/s", bound="tensor", scaling="strong",
+                 global_batch=total, images=n, dominant=("conv_igemm_tc", "conv_i8_tc", "gemm_i8_tc"),
+                 dominant_flops=float(info["flops"]), conv_flops=conv_flops, nsets=2,
+                 workload=f"BASELINE config 5: ResNet-50 Stripe program (53 convs, max-pool, residuals, global sum, fc), "
+                          f"global batch {total} sharded on n ({n} images on this rank)",
+                 cpu=dict(text=Wk.resnet50(1, image=32)[0], work=float(Wk.resnet50(1, image=32)[1]["flops"]),
+                          what="ResNet-50 program at 32x32, batch 1 per thread (same layer mix, 1/49 of the "
+                               "spatial work): rate EXTRAPOLATED to the 224x224 config", seed=1005))
+    elif cfg == "c2":
+        n = args.batch or 32
+        text = Wk.conv2d(n, 56, 56, 64, 64)
+        s.update(text=text, flops=2.0 * Wk.conv_useful_macs(n, 56, 56, 64, 64), unit="GFLOP/s", bound="hbm",
+                 global_batch=n * world, images=n, dominant=("conv_i8_tc",),
+                 workload=f"BASELINE config 2: conv2d 3x3 NHWC 56x56x64->64, batch {n} per GPU, padding "
+                          f"constraints, one Stripe block (i8 x i8 -> i32)",
+                 cpu=dict(text=Wk.conv2d(1, 56, 56, 64, 64), work=2.0 * Wk.conv_useful_macs(1, 56, 56, 64, 64),
+                          what="one image of config 2 per thread (a batch shard)", seed=1001))
+    elif cfg == "c3":
+        n = args.batch or 128
+        s.update(text=Wk.conv_bias_relu(n, 56, 56, 64, 64), flops=2.0 * Wk.conv_useful_macs(n, 56, 56, 64, 64),
+                 unit="GFLOP/s", bound="hbm", global_batch=n * world, images=n, dominant=("conv_i8_tc",),
+                 workload=f"BASELINE config 3: fused conv3x3+bias+ReLU (tile/fuse/localize form), 56x56x64->64, "
+                          f"batch {n} per GPU",
+                 cpu=dict(text=Wk.conv_bias_relu(1, 56, 56, 64, 64),
+                          work=2.0 * Wk.conv_useful_macs(1, 56, 56, 64, 64),
+                          what="one image of config 3 per thread (a batch shard)", seed=1003))
+    elif cfg == "c4a":
+        n = args.batch or 128
+        s.update(text=Wk.maxpool2x2(n, 112, 112, 64), flops=0.0, unit="GB/s", bound="hbm", global_batch=n * world,
+                 images=n, dominant=("reduce", "pool"),
+                 workload=f"BASELINE config 4a: 2x2 max-pool 112x112x64 i32, batch {n} per GPU",
+                 cpu=dict(text=Wk.maxpool2x2(8, 112, 112, 64), work=8 * (112 * 112 * 64 + 56 * 56 * 64) * 4.0,
+                          what="8 images of config 4a per thread (a batch shard)", seed=1004))
+    elif cfg == "c4b":
+        n = args.batch or 1024
+        s.update(text=Wk.global_sum(n, 7, 7, 2048), flops=0.0, unit="GB/s", bound="hbm", global_batch=n * world,
+                 images=n, dominant=("reduce",),
+                 workload=f"BASELINE config 4b: global sum 7x7x2048 i32, batch {n} per GPU",
+                 cpu=dict(text=Wk.global_sum(64, 7, 7, 2048), work=64 * (49 * 2048 + 2048) * 4.0,
+                          what="64 images of config 4b per thread (a batch shard)", seed=1004))
+    elif cfg in ("c1", "c1_i32"):
+        dt = "i8" if cfg == "c1" else "i32"
+        M = 1024
+        lo, hi = Wk.shard_range(M, world, rank)
+        m = hi - lo
+        s.update(text=Wk.matmul(m, 1024, 1024, in_dtype=dt, out_dtype="i32"), flops=2.0 * m * 1024 * 1024,
+                 unit="GFLOP/s", bound="tensor", scaling="strong", global_batch=M, images=m,
+                 dominant=("gemm_i8_tc",),
+                 workload=f"BASELINE config 1: matmul C[i,j] += A[i,k]*B[k,j] 1024^3 ({dt} x {dt} -> i32, exact), "
+                          f"rows sharded ({m} on this rank)",
+                 cpu=dict(text=Wk.matmul(64, 1024, 1024, in_dtype=dt, out_dtype="i32"), work=2.0 * 64 * 1024 * 1024,
+                          what="64 rows of config 1 per thread (a row shard; 16 threads = the whole matmul)",
+                          seed=1001))
+    else:
+        raise SystemExit(f"unknown config {cfg}")
+    return s
+
+
+def alg_bytes_of(prog):
+    """Algorithmic bytes: every root buffer once at native width (inputs read, outputs written)."""
+    return sum(d.elements * ISZ[d.dtype] for d in prog.buffers.values())
+
+
+# ------------------------------------------------------------------------------------------
+def cpu_reference(sp, threads_list, steps=1):
+    """The unmodified reference interpreter (oracle/_ref: stripe::execute) on host threads.
+    Returns [{threads, rate, seconds}] -- each thread runs its own Program/BufferStore on one
+    unit of the config's work (a batch or row shard), all threads at once."""
     import numpy as np
 
     from oracle import Ref, random_inputs
-    from paper_1903_06498_b200 import workloads as Wk
-    threads = threads or os.cpu_count() or 1
-    text = Wk.conv2d(1, samples_rows, W, C, K)
-    macs = Wk.conv_useful_macs(1, samples_rows, W, C, K)
     L = Ref.lib()
-    prog = Ref.parse(text)
+    c = sp["cpu"]
+    prog = Ref.parse(c["text"])
     bufs = prog.buffers()
-    inputs = random_inputs(bufs, 1001)
-    times = []
-    for it in range(warmup + steps):
-        progs = (ctypes.c_void_p * threads)(*([prog.h] * threads))
-        stores = []
-        for t in range(threads):
-            s = L.sr_store_new()
-            for n, bits, el, d in bufs:
-                arr = inputs[n] if n in inputs else np.zeros(el, np.int64)
-                L.sr_store_set(s, n.encode(), bits, arr.ctypes.data, arr.size)
-            stores.append(s)
-        st = (ctypes.c_void_p * threads)(*stores)
-        t0 = time.perf_counter()
-        bad = L.sr_execute_many(progs, st, threads, threads)
-        dt = time.perf_counter() - t0
-        for s in stores:
-            L.sr_store_free(s)
-        if bad:
-            raise RuntimeError("reference execute failed")
-        if it >= warmup:
+    inputs = random_inputs(bufs, c["seed"])
+    res = []
+    for threads in threads_list:
+        times = []
+        for _ in range(steps):
+            progs = (ctypes.c_void_p * threads)(*([prog.h] * threads))
+            stores = []
+            for t in range(threads):
+                s = L.sr_store_new()
+                for n, bits, el, d in bufs:
+                    arr = inputs[n] if n in inputs else np.zeros(el, np.int64)
+                    L.sr_store_set(s, n.encode(), bits, arr.ctypes.data, arr.size)
+                stores.append(s)
+            st = (ctypes.c_void_p * threads)(*stores)
+            t0 = time.perf_counter()
+            bad = L.sr_execute_many(progs, st, threads, threads)
+            dt = time.perf_counter() - t0
+            for s in stores:
+                L.sr_store_free(s)
+            if bad:
+                raise RuntimeError("reference execute failed")
             times.append(dt)
-    gflops = 2.0 * macs * threads / (sum(times) / len(times)) / 1e9
-    sample = (f"{threads} concurrent stripe::execute runs (one per host thread) of config 2 restricted to "
-              f"1 image x {samples_rows} output rows ({macs} useful MACs each), reference built -O2 from "
-              f"/root/reference/proj/src")
-    return gflops, threads, sample, times
+        sec = statistics.mean(times)
+        res.append({"threads": threads, "rate": c["work"] * threads / sec / 1e9, "seconds": round(sec, 3)})
+    return res
 
 
-def cpu_reference_resnet(threads=None, steps=1, warmup=0):
-    """Reference interpreter on a bounded sample of config 5: concurrent executions (one per
-    host thread) of the full-width ResNet-50 program on one 32x32 image (1.4e8 useful MACs
-    after the stem), i.e. the same layer mix at 1/49 of the spatial work."""
-    import numpy as np
+def host_cpu():
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return model, os.cpu_count() or 1
 
-    from oracle import Ref, random_inputs
-    from paper_1903_06498_b200 import workloads as Wk
-    threads = threads or os.cpu_count() or 1
-    text, info = Wk.resnet50(1, image=32)
-    L = Ref.lib()
-    prog = Ref.parse(text)
-    bufs = prog.buffers()
-    inputs = random_inputs(bufs, 1005)
-    times = []
-    for it in range(warmup + steps):
-        progs = (ctypes.c_void_p * threads)(*([prog.h] * threads))
-        stores = []
-        for t in range(threads):
-            s = L.sr_store_new()
-            for n, bits, el, d in bufs:
-                arr = inputs[n] if n in inputs else np.zeros(el, np.int64)
-                L.sr_store_set(s, n.encode(), bits, arr.ctypes.data, arr.size)
-            stores.append(s)
-        st = (ctypes.c_void_p * threads)(*stores)
-        t0 = time.perf_counter()
-        bad = L.sr_execute_many(progs, st, threads, threads)
-        dt = time.perf_counter() - t0
-        for s in stores:
-            L.sr_store_free(s)
-        if bad:
-            raise RuntimeError("reference execute failed")
-        if it >= warmup:
-            times.append(dt)
-    gflops = info["flops"] * threads / (sum(times) / len(times)) / 1e9
-    sample = (f"{threads} concurrent stripe::execute runs (one per host thread) of the config-5 ResNet-50 program "
-              f"at 32x32 image, batch 1 ({info['macs']} useful MACs each)")
-    return gflops, threads, sample, times
+
+def cpu_baseline_obj(sp, steps=1):
+    from oracle import Ref
+    if not Ref.available():
+        return None
+    model, ncpu = host_cpu()
+    r = cpu_reference(sp, [1, ncpu], steps)
+    one, many = r[0], r[-1]
+    return {"value": round(many["rate"], 4), "unit": sp["unit"], "cores": ncpu, "kind": "reference",
+            "sample": f"{sp['cpu']['what']}; unmodified stripe::execute from oracle/_ref (-O2), one "
+                      f"Program/BufferStore per thread; {ncpu} threads {many['seconds']} s",
+            "one_thread": round(one["rate"], 5), "one_thread_seconds": one["seconds"],
+            "threads": ncpu, "cpu_model": model}
 
 
 def run_reference_arm(args):
-    world, rank, _ = dist_setup()
+    world, rank, _ = dist_env()
     if rank != 0:
-        return
-    if args.config == "c5":
-        from oracle import Ref
-        if not Ref.available():
-            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libstripe_ref.so not built"}))
-            return
-        gflops, cores, sample, times = cpu_reference_resnet(steps=args.steps, warmup=min(args.warmup, 1))
-        print(json.dumps({
-            "metric": METRIC, "value": round(gflops, 4), "unit": "GFLOP/s", "impl": "reference",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(1000 * sum(times) / len(times), 3), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "i8xi8->i32 (int64 carriers)", "data": "synthetic (random_inputs, seed 1005)",
-            "config": {"workload": "BASELINE config 5: ResNet-50 Stripe program", "sample": "32x32 image"},
-            "cpu_baseline": {"value": round(gflops, 4), "unit": "GFLOP/s", "cores": cores, "kind": "reference",
-                             "sample": sample},
-            "e2e": {"value": round(gflops, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        }))
         return
     from oracle import Ref
     if not Ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libstripe_ref.so not built"}))
         return
-    gflops, cores, sample, times = cpu_reference(samples_rows=8, steps=args.steps, warmup=args.warmup)
+    sp = spec(args.config, 1, 0, args)
+    model, ncpu = host_cpu()
+    t0 = time.perf_counter()
+    r = cpu_reference(sp, [ncpu], steps=args.steps if args.steps <= 3 else 3)[0]
+    wall = time.perf_counter() - t0
+    v = round(r["rate"], 4)
     print(json.dumps({
-        "metric": METRIC, "value": round(gflops, 4), "unit": "GFLOP/s", "impl": "reference", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1000 * sum(times) / len(times), 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "i8xi8->i32 (int64 carriers)",
-        "data": "synthetic (splitmix64 random_inputs, seed 1001)",
-        "config": {"workload": "BASELINE config 2: conv2d 3x3 NHWC 56x56x64->64 batch 32, padding constraints",
-                   "sample": "row band"},
-        "cpu_baseline": {"value": round(gflops, 4), "unit": "GFLOP/s", "cores": cores, "kind": "reference",
-                         "sample": sample},
-        "e2e": {"value": round(gflops, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "metric": METRIC, "value": v, "unit": sp["unit"], "impl": "reference", "n_gpus": args.gpus,
+        "steps": min(args.steps, 3), "warmup": 0, "ms_per_step": round(1000 * r["seconds"], 3),
+        "higher_is_better": True, "scaling": sp["scaling"], "vs_baseline": None,
+        "dtype": "int64 carriers (i8/i32 program dtypes)", "data": f"synthetic (splitmix64 random_inputs, seed "
+                                                                  f"{sp['cpu']['seed']})",
+        "config": {"workload": sp["workload"], "sample": sp["cpu"]["what"]},
+        "cpu_baseline": {"value": v, "unit": sp["unit"], "cores": ncpu, "kind": "reference",
+                         "sample": f"{sp['cpu']['what']}; {ncpu} host threads, one stripe::execute each",
+                         "cpu_model": model, "wall_s": round(wall, 2)},
+        "e2e": {"value": v, "unit": sp["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
 
@@ -243,40 +305,35 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_1903_06498_b200 as sb
-    from paper_1903_06498_b200 import workloads as Wk
 
-    world, rank, local = dist_setup()
+    world, rank, local = dist_env()
     if world > 1:
         dist.init_process_group("nccl", init_method="env://")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(device=dev)
-
-    text = Wk.conv2d(N_IMG, H, W, C, K)
-    prog = sb.parse_program(text)
-    plan = prog.describe_plan(fresh_outputs=True)
-    assert "conv_i8_tc" in plan, plan
+    sp = spec(args.config, world, rank, args)
+    prog = sb.parse_program(sp["text"])
     ctx = sb.Context(local)
     ctx.set_stream(stream.cuda_stream)
-
-    macs = Wk.conv_useful_macs(N_IMG, H, W, C, K)
-    flops_step = 2.0 * macs
-    in_bytes = N_IMG * H * W * C + 3 * 3 * K * C
-    out_bytes = N_IMG * H * W * K * 4
-    alg_bytes = in_bytes + out_bytes
-
-    # rotate through enough input/output sets that the working set exceeds L2
-    nsets = max(4, int(3 * L2_BYTES // alg_bytes) + 1)
-    g = torch.Generator(device=dev).manual_seed(1001 + rank)
+    pk = peaks()
+    alg_bytes = alg_bytes_of(prog)
+    in_names = [n for n, d in prog.buffers.items() if int(d.dir) == 0]
+    out_names = [n for n in prog.buffers if n not in in_names]
+    nbytes = {n: d.elements * ISZ[d.dtype] for n, d in prog.buffers.items()}
+    # rotate through enough input/output sets that the working set exceeds L2 (C5: each step's
+    # > 1 GB of activations flushes L2 anyway)
+    nsets = sp.get("nsets") or max(2, int(3 * L2_BYTES // max(alg_bytes, 1)) + 1)
+    g = torch.Generator(device=dev).manual_seed(1000 + rank)
     sets = []
     for _ in range(nsets):
-        I = torch.randint(-128, 128, (N_IMG, H, W, C), dtype=torch.int8, device=dev, generator=g)
-        F = torch.randint(-128, 128, (3, 3, K, C), dtype=torch.int8, device=dev, generator=g)
-        O = torch.empty((N_IMG, H, W, K), dtype=torch.int32, device=dev)
-        sets.append({"I": (I.data_ptr(), I.numel(), 0), "F": (F.data_ptr(), F.numel(), 0),
-                     "O": (O.data_ptr(), O.numel(), sb.SB_BUF_PREPARE), "_keep": (I, F, O)})
-
-    bound = [ctx.bind_device(prog, {k: v for k, v in s.items() if not k.startswith("_")}) for s in sets]
+        bufs, keep = {}, []
+        for n, d in prog.buffers.items():
+            t = torch.randint(-128, 128, (nbytes[n],), dtype=torch.int8, device=dev, generator=g)
+            keep.append(t)
+            bufs[n] = (t.data_ptr(), d.elements, sb.SB_BUF_PREPARE if int(d.dir) != 0 else 0)
+        sets.append((bufs, keep))
+    bound = [ctx.bind_device(prog, b) for b, _ in sets]
 
     def step(i):
         bound[i % nsets]()
@@ -291,34 +348,22 @@ def run_ours(args):
         for i in range(args.warmup):
             step(i)
         # keep the GPU busy ~1 s before the timed region so the sampled clocks reflect load
-        settle = 0
-        t_settle = time.perf_counter()
+        settle, t_settle = 0, time.perf_counter()
         while time.perf_counter() - t_settle < 1.0:
-            for _ in range(20):
+            for _ in range(max(1, 2000 // max(1, int(sp["flops"] / 1e9) + 1))):
                 step(args.warmup + settle)
                 settle += 1
             torch.cuda.synchronize(dev)
         ctx.sync()
-        barrier()
-        torch.cuda.synchronize(dev)
-        # eager (one host call per step) timing, for reference only
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for i in range(args.steps):
-            step(args.warmup + i)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        eager_ms = e0.elapsed_time(e1) / args.steps
-        # the timed region: exactly K steps, captured once as a CUDA graph (sb_graph_*) so
-        # host launch latency is off the device timeline
+        # the timed region: exactly K steps captured once as a CUDA graph (sb_graph_*) so host
+        # launch latency is off the device timeline
         graph = sb.Graph(ctx, lambda: [step(args.warmup + i) for i in range(args.steps)])
         graph.launch()  # warm the graph itself (untimed)
         torch.cuda.synchronize(dev)
         barrier()
         torch.cuda.synchronize(dev)
         launches0 = ctx.launch_count
-        t_start = torch.cuda.Event(enable_timing=True)
-        t_end = torch.cuda.Event(enable_timing=True)
+        t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t_start.record(stream)
         graph.launch()
         t_end.record(stream)
@@ -329,196 +374,139 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
         launches = ctx.launch_count - launches0
         elapsed_ms = t_start.elapsed_time(t_end)
-        kernel_ms = [elapsed_ms / args.steps]  # one conv launch per step, back to back
+
+        # isolated launches: one step at a time, synchronized on both sides (no overlap with a
+        # neighbouring step), median of 10
+        iso = []
+        for i in range(10):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize(dev)
+            a.record(stream)
+            step(i)
+            b.record(stream)
+            torch.cuda.synchronize(dev)
+            iso.append(a.elapsed_time(b))
+        iso_ms = statistics.median(iso)
+        # per-step device times (serial, CUDA events around every launch) for the roofline
+        ctx.set_profile(True)
+        prof = []
+        for i in range(3):
+            step(i)
+            ctx.sync()
+            prof.append(ctx.read_profile())
+        ctx.set_profile(False)
 
     t = torch.tensor([elapsed_ms], device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     elapsed_ms = float(t.item())
     ms_per_step = elapsed_ms / args.steps
-    value = flops_step * world * args.steps / (elapsed_ms / 1e3) / 1e9
+    work = sp["flops"] if sp["unit"] == "GFLOP/s" else float(alg_bytes)
+    value = work * world * args.steps / (elapsed_ms / 1e3) / 1e9 if sp["scaling"] == "weak" else \
+        sum_over_ranks(dist, world, dev, work) * args.steps / (elapsed_ms / 1e3) / 1e9
 
-    # ---- end-to-end through the public API (host buffers, H2D + D2H inside the region) ----
-    # sb_execute_async on two contexts ping-ponging steps: step i's device-to-host copy of O
-    # overlaps step i+1's host-to-device copy of I and F (the two copy directions run
-    # concurrently over PCIe); every step still copies its inputs in and its result out.
-    ctx.set_stream(None)
-    e2e_steps = max(4, min(args.steps, 20))
-    ctxs = [ctx, sb.Context(local)]
-    pins = []
+    # ---- roofline of the dominant kernel family (median over the profiled executes) ----
+    fam = {}
+    for rec in prof:
+        per = {}
+        for (_, ms, kern, _, _) in rec:
+            per[kern] = per.get(kern, 0.0) + ms
+        for k, v in per.items():
+            fam.setdefault(k, []).append(v)
+    fam_ms = {k: statistics.median(v) for k, v in fam.items()}
+    prof_total = sum(fam_ms.values())
+    dom = [k for k in sp["dominant"] if k in fam_ms]
+    dom_ms = sum(fam_ms[k] for k in dom)
+    dom_launches = sum(1 for (_, _, kern, _, _) in prof[-1] if kern in dom)
+    if sp["bound"] == "tensor":
+        dflops = sp.get("dominant_flops", sp["flops"])
+        ach = dflops / (dom_ms / 1e3) / 1e12 if dom_ms else None
+        roof = {"bound": "tensor", "achieved": round(ach, 2) if ach else None, "peak": round(pk["int8_tops"], 1),
+                "unit": "TFLOP/s", "frac": round(ach / pk["int8_tops"], 4) if ach else None,
+                "traffic": None, "peak_kind": pk["int8_kind"], "kernel": "+".join(dom),
+                "kernel_ms_per_step": round(dom_ms, 5), "launches_per_step": dom_launches,
+                "algorithmic_ops_per_step": dflops,
+                "network": {"achieved": round(work / (ms_per_step / 1e3) / 1e12, 2),
+                            "frac": round(work / (ms_per_step / 1e3) / 1e12 / pk["int8_tops"], 4),
+                            "note": "whole step (all launches, lanes overlapped, graph replay) / int8 peak"}}
+    else:
+        # HBM-bound: algorithmic bytes of the step / the dominant kernel's time.  The step of
+        # C2/C3/C4 is ONE launch, so the graph-timed step is that kernel's launch duration.
+        kms = ms_per_step if dom_launches == 1 and len(prof[-1]) == 1 else dom_ms
+        ach = alg_bytes / (kms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": round(ach / pk["hbm_gbs"], 4), "traffic": traffic_of(sp["cfg"]), "peak_kind": pk["kind"],
+                "kernel": "+".join(dom), "kernel_ms": round(kms, 5), "algorithmic_bytes_per_launch": alg_bytes,
+                "isolated": {"kernel_ms": round(iso_ms, 5),
+                             "frac": round(alg_bytes / (iso_ms / 1e3) / 1e9 / pk["hbm_gbs"], 4),
+                             "note": "one step alone, synchronized before and after (no PDL overlap)"}}
+        if sp["flops"]:
+            roof["tensor"] = {"achieved_tops": round(sp["flops"] / (kms / 1e3) / 1e12, 2),
+                              "int8_peak_tops": round(pk["int8_tops"], 1), "peak_kind": pk["int8_kind"],
+                              "frac": round(sp["flops"] / (kms / 1e3) / 1e12 / pk["int8_tops"], 4)}
+    breakdown = {k: {"ms": round(v, 5), "share": round(v / prof_total, 4)} for k, v in
+                 sorted(fam_ms.items(), key=lambda kv: -kv[1])} if prof_total else {}
 
-    def pinned(n, ct):
-        p = ctypes.c_void_p()  # pinned host memory from the library's own allocator
-        sb._check(sb.lib().sb_host_alloc_pinned(n * ctypes.sizeof(ct), ctypes.byref(p)))
-        pins.append(p)
-        return np.ctypeslib.as_array((ct * n).from_address(p.value))
-
-    hI = pinned(N_IMG * H * W * C, ctypes.c_int8)
-    hF = pinned(3 * 3 * K * C, ctypes.c_int8)
-    hO = [pinned(N_IMG * H * W * K, ctypes.c_int32) for _ in ctxs]
-    rng = np.random.default_rng(7 + rank)
-    hI[:] = rng.integers(-128, 128, hI.size, dtype=np.int8)
-    hF[:] = rng.integers(-128, 128, hF.size, dtype=np.int8)
-    for i in range(4):
-        ctxs[i % 2].execute_native_async(prog, {"I": hI, "F": hF, "O": hO[i % 2]}, prepare=("O",))
-    for c_ in ctxs:
-        c_.sync()
-    barrier()
-    t0 = time.perf_counter()
-    for i in range(e2e_steps):
-        ctxs[i % 2].execute_native_async(prog, {"I": hI, "F": hF, "O": hO[i % 2]}, prepare=("O",))
-    for c_ in ctxs:
-        c_.sync()
-    e2e_s = time.perf_counter() - t0
-    te = torch.tensor([e2e_s], device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e = {"value": round(flops_step * world * e2e_steps / float(te.item()) / 1e9, 3), "unit": "GFLOP/s",
-           "h2d_bytes_per_step": int(hI.nbytes + hF.nbytes), "d2h_bytes_per_step": int(hO[0].nbytes),
-           "steps": e2e_steps,
-           "timer": "host wall clock from the first sb_execute_async to the last context sync (2 contexts)"}
-    for p in pins:
-        sb.lib().sb_host_free_pinned(p)
-
-    hbm_peak, bf16_peak, peak_kind = peaks()
-    avg_kernel_ms = statistics.mean(kernel_ms)
-    achieved_gbs = alg_bytes / (avg_kernel_ms / 1e3) / 1e9
-    tensor_tops = flops_step / (avg_kernel_ms / 1e3) / 1e12
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "conv_tc_traffic.json")) as f:
-            traffic = json.load(f).get("bytes_per_launch")
-    except Exception:
-        pass
+    # ---- end to end through the public API (host buffers, copies inside the timed region) ----
+    e2e = e2e_native(args, sb, np, torch, dist, world, ctx, prog, nbytes, in_names, out_names, work, sp['unit'],
+                     dev, local)
+    dropin = e2e_dropin(args, sb, np, torch, dist, world, ctx, prog, in_names, out_names, work, sp['unit'], dev)
+    e2e["dropin"] = dropin
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         try:
-            from oracle import Ref
-            if Ref.available():
-                gf, cores, sample, _ = cpu_reference(samples_rows=8, steps=1, warmup=0)
-                cpu = {"value": round(gf, 4), "unit": "GFLOP/s", "cores": cores, "kind": "reference",
-                       "sample": sample}
+            cpu = cpu_baseline_obj(sp)
         except Exception as e:  # reported, never silently substituted
-            cpu = {"value": None, "unit": "GFLOP/s", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
+            cpu = {"value": None, "unit": sp["unit"], "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
 
     if rank == 0:
-        clocks = clk.summary()
+        cfgj = {"workload": sp["workload"], "global_batch": sp["global_batch"],
+                "parallelism": f"batch-sharded x{world} (no collective)" if sp["cfg"] not in ("c1", "c1_i32")
+                else f"row-sharded x{world} (no collective)",
+                "l2": f"{nsets} rotating input/output sets ({nsets * alg_bytes / 2**20:.0f} MiB)"
+                      + (" + >1 GB activation arena per step" if sp["cfg"] == "c5" else "")}
+        if sp["cfg"] == "c5":
+            cfgj["images_per_s"] = round(sp["global_batch"] / (ms_per_step / 1e3), 1)
         line = {
-            "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "value": round(value, 3), "unit": sp["unit"], "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "i8xi8->i32",
-            "data": "synthetic (uniform random int8 inputs in HBM)",
-            "config": {"workload": "BASELINE config 2: conv2d 3x3 NHWC 56x56x64->64, batch 32 per GPU, "
-                                   "padding constraints, one Stripe block",
-                       "global_batch": N_IMG * world, "parallelism": f"batch-sharded x{world} (no collective)",
-                       "l2": f"{nsets} rotating input/output sets ({nsets * alg_bytes / 2**20:.0f} MiB > L2)"},
-            "roofline": {"bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
-                         "frac": round(achieved_gbs / hbm_peak, 4), "traffic": traffic,
-                         "peak_kind": peak_kind, "algorithmic_bytes_per_launch": alg_bytes,
-                         "kernel_ms": round(avg_kernel_ms, 5),
-                         "tensor": {"achieved_tops": round(tensor_tops, 2),
-                                    "int8_peak_tops_derived": round(2 * bf16_peak, 1),
-                                    "frac": round(tensor_tops / (2 * bf16_peak), 4)}},
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": int(launches),
-            "eager_ms_per_step": round(eager_ms, 5),
-            "clock_settle_steps": settle,
-            "clocks": clocks,
+            "scaling": sp["scaling"], "vs_baseline": None, "dtype": "i8xi8->i32" if sp["flops"] else "i32",
+            "data": "synthetic (uniform random bytes in HBM; i8 images/weights, i32 biases)",
+            "config": cfgj, "roofline": roof, "kernel_breakdown": breakdown, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(launches), "launches_per_step": int(launches) // args.steps,
+            "clocks": clk.summary(),
         }
-        print(json.dumps(line))
+        print(json.dumps(line), flush=True)
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
 
 
-def run_ours_resnet(args):
-    """Config 5: ResNet-50 program, 128 images per GPU, weak scaling over batch shards."""
-    import numpy as np
+def sum_over_ranks(dist, world, dev, work):
     import torch
-    import torch.distributed as dist
-
-    import paper_1903_06498_b200 as sb
-    from paper_1903_06498_b200 import workloads as Wk
-
-    world, rank, local = dist_setup()
+    t = torch.tensor([work], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.init_process_group("nccl", init_method="env://")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    stream = torch.cuda.Stream(device=dev)
-    per_gpu = args.batch_per_gpu
-    text, info = Wk.resnet50(per_gpu)
-    prog = sb.parse_program(text)
-    ctx = sb.Context(local)
-    ctx.set_stream(stream.cuda_stream)
-    flops_step = float(info["flops"])
-    nbytes = {n: d.elements * {8: 1, 16: 2, 32: 4}[d.dtype] for n, d in prog.buffers.items()}
-    in_names = [n for n, d in prog.buffers.items() if int(d.dir) == 0]
-    alg_bytes = sum(nbytes.values())
-    # two input/output sets: each step's activations (> 1 GB of scratch) flush L2 anyway
-    g = torch.Generator(device=dev).manual_seed(1005 + rank)
-    sets = []
-    for _ in range(2):
-        bufs, keep = {}, []
-        for n, d in prog.buffers.items():
-            t = torch.randint(-128, 128, (nbytes[n],), dtype=torch.int8, device=dev, generator=g)
-            keep.append(t)
-            bufs[n] = (t.data_ptr(), d.elements, sb.SB_BUF_PREPARE if int(d.dir) != 0 else 0)
-        sets.append((bufs, keep))
-    bound = [ctx.bind_device(prog, b) for b, _ in sets]
+        dist.all_reduce(t)
+    return float(t.item())
 
-    def step(i):
-        bound[i % 2]()
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
+def traffic_of(cfg):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the committed ncu
+    capture (profiles/r02_traffic.json, written by tools/ncu_traffic.py), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as f:
+            return json.load(f)[cfg]["dram_bytes_per_launch"]
+    except Exception:
+        return None
 
-    with torch.cuda.stream(stream):
-        clk = ClockSampler(local).__enter__()
-        clk.wait_first_sample()
-        for i in range(args.warmup):
-            step(i)
-        t_settle = time.perf_counter()
-        settle = 0
-        while time.perf_counter() - t_settle < 1.0:
-            step(settle)
-            settle += 1
-            torch.cuda.synchronize(dev)
-        ctx.sync()
-        graph = sb.Graph(ctx, lambda: [step(i) for i in range(args.steps)])
-        graph.launch()
-        torch.cuda.synchronize(dev)
-        barrier()
-        torch.cuda.synchronize(dev)
-        launches0 = ctx.launch_count
-        t_start = torch.cuda.Event(enable_timing=True)
-        t_end = torch.cuda.Event(enable_timing=True)
-        t_start.record(stream)
-        graph.launch()
-        t_end.record(stream)
-        torch.cuda.synchronize(dev)
-        clk.__exit__(None, None, None)
-        ctx.sync()
-        barrier()
-        torch.cuda.synchronize(dev)
-        launches = ctx.launch_count - launches0
-        elapsed_ms = t_start.elapsed_time(t_end)
-    t = torch.tensor([elapsed_ms], device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    elapsed_ms = float(t.item())
-    ms_per_step = elapsed_ms / args.steps
-    value = flops_step * world * args.steps / (elapsed_ms / 1e3) / 1e9
 
-    # end to end through the public API from pinned host buffers (every program input copied
-    # in, the logits copied out, each step): sb_execute_async on two contexts ping-ponging
-    # steps, so step i+1's host-to-device copies overlap step i's compute
+def e2e_native(args, sb, np, torch, dist, world, ctx, prog, nbytes, in_names, out_names, work, unit, dev, local):
+    """sb_execute_async on two contexts ping-ponging steps: every step copies its inputs in
+    from pinned host memory and its outputs out; step i's D2H overlaps step i+1's H2D."""
     ctx.set_stream(None)
     ctxs = [ctx, sb.Context(local)]
-    pins = []
-    hosts = []
+    pins, hosts = [], []
     for _ in ctxs:
         host = {}
         for n, d in prog.buffers.items():
@@ -528,83 +516,125 @@ def run_ours_resnet(args):
             ct = {8: ctypes.c_int8, 16: ctypes.c_int16, 32: ctypes.c_int32}[d.dtype]
             host[n] = np.ctypeslib.as_array((ct * d.elements).from_address(p.value))
         hosts.append(host)
-    rng = np.random.default_rng(11 + rank)
+    rng = np.random.default_rng(11)
     for n in in_names:
         vals = rng.integers(-128, 128, hosts[0][n].size).astype(hosts[0][n].dtype)
         for h in hosts:
             h[n][:] = vals
-    outs = tuple(n for n in prog.buffers if n not in in_names)
+    outs = tuple(out_names)
     for i in range(2):
         ctxs[i % 2].execute_native_async(prog, hosts[i % 2], prepare=outs)
     for c_ in ctxs:
         c_.sync()
-    barrier()
-    e2e_steps = max(4, min(args.steps, 10))
+    if world > 1:
+        dist.barrier()
+    steps = max(4, min(args.steps, 10))
     t0 = time.perf_counter()
-    for i in range(e2e_steps):
+    for i in range(steps):
         ctxs[i % 2].execute_native_async(prog, hosts[i % 2], prepare=outs)
     for c_ in ctxs:
         c_.sync()
     te = torch.tensor([time.perf_counter() - t0], device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e = {"value": round(flops_step * world * e2e_steps / float(te.item()) / 1e9, 3), "unit": "GFLOP/s",
-           "h2d_bytes_per_step": int(sum(nbytes[n] for n in in_names)),
-           "d2h_bytes_per_step": int(sum(nbytes[n] for n in outs)), "steps": e2e_steps,
-           "timer": "host wall clock from the first sb_execute_async to the last context sync (2 contexts)"}
+    tot = sum_over_ranks(dist, world, dev, work)
     for p in pins:
         sb.lib().sb_host_free_pinned(p)
+    return {"value": round(tot * steps / float(te.item()) / 1e9, 3), "unit": unit, "h2d_bytes_per_step": int(sum(nbytes[n] for n in in_names)),
+            "d2h_bytes_per_step": int(sum(nbytes[n] for n in out_names)), "steps": steps,
+            "api": "sb_execute_async, native-width pinned host buffers",
+            "timer": "host wall clock from the first sb_execute_async to the last context sync (2 contexts)"}
 
-    cpu = None
-    if rank == 0 and not args.no_cpu_baseline and world == 1:
-        try:
-            from oracle import Ref
-            if Ref.available():
-                gf, cores, sample, _ = cpu_reference_resnet(steps=1, warmup=0)
-                cpu = {"value": round(gf, 4), "unit": "GFLOP/s", "cores": cores, "kind": "reference",
-                       "sample": sample}
-        except Exception as e:
-            cpu = {"value": None, "unit": "GFLOP/s", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
+
+def e2e_dropin(args, sb, np, torch, dist, world, ctx, prog, in_names, out_names, work, unit, dev):
+    """The stripe::b200::execute boundary: sb_execute with int64 carriers (interp.h:14-17), one
+    synchronous call per step -- int64 -> native conversion, H2D, execute, D2H, native -> int64."""
+    rng = np.random.default_rng(12)
+    store = {}
+    for n in in_names:
+        store[n] = sb.Buffer(prog.buffers[n].dtype, rng.integers(-128, 128, prog.buffers[n].elements,
+                                                                   dtype=np.int64))
+    c2 = sb.Context(ctx.device)
+    st = dict(store)
+    sb.prepare_outputs(prog, st)
+    c2.execute(prog, st)  # warm (plan, device buffers, pinned staging)
+    if world > 1:
+        dist.barrier()
+    steps = 2 if work > 1e12 else max(3, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        st = dict(store)
+        sb.prepare_outputs(prog, st)
+        c2.execute(prog, st)
+    te = torch.tensor([time.perf_counter() - t0], device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    tot = sum_over_ranks(dist, world, dev, work)
+    return {"value": round(tot * steps / float(te.item()) / 1e9, 3), "unit": unit,
+            "h2d_bytes_per_step": int(sum(prog.buffers[n].elements * 8 for n in in_names)),
+            "d2h_bytes_per_step": int(sum(prog.buffers[n].elements * 8 for n in out_names)), "steps": steps,
+            "api": "sb_execute with int64 carriers (the stripe::b200::execute drop-in boundary), synchronous",
+            "note": "bytes counted at the int64 carrier width the caller hands over"}
+
+
+def dry_run(args):
+    """What run_ours does across ranks, without a GPU: gloo process group, each rank's shard of
+    the config, the barrier and the max-over-ranks reduction of a (fake) device time."""
+    import torch
+    import torch.distributed as dist
+    world, rank, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo", init_method="env://")
+    sp = spec(args.config, world, rank, args)
+    t = torch.tensor([1.0 + rank])
+    imgs = torch.tensor([float(sp["images"])])
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(imgs)
     if rank == 0:
-        hbm_peak, bf16_peak, peak_kind = peaks()
-        tops = flops_step / (ms_per_step / 1e3) / 1e12
-        i8_peak = 2 * bf16_peak
-        print(json.dumps({
-            "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "i8xi8->i32",
-            "data": "synthetic (uniform random int8 image, weights, i32 biases in HBM)",
-            "config": {"workload": f"BASELINE config 5: ResNet-50 Stripe program (53 convs, max-pool, residuals, "
-                                   f"global sum, fc), {per_gpu} images per GPU",
-                       "global_batch": per_gpu * world, "parallelism": f"batch-sharded x{world} (no collective)",
-                       "images_per_s": round(per_gpu * world / (ms_per_step / 1e3), 1),
-                       "l2": "activations > 1 GB per step (scratch arena) flush L2"},
-            "roofline": {"bound": "tensor", "achieved": round(tops, 2), "peak": round(i8_peak, 1), "unit": "TFLOP/s",
-                         "frac": round(tops / i8_peak, 4), "traffic": None,
-                         "peak_kind": f"dense int8 = 2 x {peak_kind} bf16 ({bf16_peak})",
-                         "note": "whole-network useful ops / step time (all 59 launches)"},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
-        }))
+        print(json.dumps({"dry_run": True, "n_gpus": world, "max_elapsed": float(t.item()),
+                          "images_total": int(imgs.item()), "global_batch": sp["global_batch"],
+                          "scaling": sp["scaling"], "pid": os.getpid()}), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------------------------------
+def launch_ranks(args):
+    """`--gpus N` outside a launcher: start N ranks with torch.distributed.run (127.0.0.1)."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", default="c2", choices=["c2", "c5"])
-    ap.add_argument("--batch-per-gpu", type=int, default=128, help="config 5 images per GPU")
+    ap.add_argument("--config", default="c5", choices=["c5", "c2", "c3", "c4a", "c4b", "c1", "c1_i32"])
+    ap.add_argument("--batch", type=int, default=0, help="override the config's batch (C5: global batch)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher check on CPU: gloo ranks report their shard and the max-over-ranks time")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(launch_ranks(args))
+    if args.dry_run:
+        dry_run(args)
+    elif args.impl == "reference":
         run_reference_arm(args)
-    elif args.config == "c5":
-        run_ours_resnet(args)
     else:
         run_ours(args)
 

@@ -140,6 +140,11 @@ void* sb_context_stream(sb_context* ctx);
 /* Waits for the stream and reports any device-side error (OutOfBoundsAccess ...). */
 int sb_context_sync(sb_context* ctx);
 /* Number of kernels this library launched on the context so far. */
+/* Per-step device timing (development and bench aid): while enabled, every execute runs its
+ * steps serially on the context stream bracketed by CUDA events and appends one line per
+ * step, "step ms kernel path points", read (and cleared) by sb_context_profile_read. */
+int sb_context_set_profile(sb_context* ctx, int enable);
+int sb_context_profile_read(sb_context* ctx, char* buf, size_t cap, size_t* len);
 uint64_t sb_context_launch_count(sb_context* ctx);
 int sb_device_alloc(sb_context* ctx, int64_t bytes, void** dptr);
 int sb_device_free(sb_context* ctx, void* dptr);

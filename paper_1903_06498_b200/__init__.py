@@ -45,7 +45,7 @@ EXPORTED = [
     "sb_program_buffer_info", "sb_program_output_identity", "sb_program_describe_plan",
     "sb_program_output_aggregation", "sb_program_restrict_index", "sb_program_check_split", "sb_count_valid_points",
     "sb_context_create", "sb_context_destroy", "sb_context_set_stream", "sb_context_stream",
-    "sb_context_sync", "sb_context_launch_count", "sb_device_alloc", "sb_device_free",
+    "sb_context_sync", "sb_context_launch_count", "sb_context_set_profile", "sb_context_profile_read", "sb_device_alloc", "sb_device_free",
     "sb_host_alloc_pinned", "sb_host_free_pinned", "sb_execute", "sb_execute_device", "sb_execute_async",
     "sb_graph_begin", "sb_graph_end", "sb_graph_launch", "sb_graph_free",
 ]
@@ -102,6 +102,8 @@ def lib() -> ctypes.CDLL:
         L.sb_context_sync.argtypes = [vp]
         L.sb_context_launch_count.argtypes = [vp]
         L.sb_context_launch_count.restype = ctypes.c_uint64
+        L.sb_context_set_profile.argtypes = [vp, i32]
+        L.sb_context_profile_read.argtypes = [vp, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
         L.sb_device_alloc.argtypes = [vp, i64, ctypes.POINTER(vp)]
         L.sb_device_free.argtypes = [vp, vp]
         L.sb_host_alloc_pinned.argtypes = [i64, ctypes.POINTER(vp)]
@@ -301,6 +303,21 @@ class Context:
 
     def sync(self) -> None:
         _check(lib().sb_context_sync(self._h))
+
+    def set_profile(self, enable: bool) -> None:
+        _check(lib().sb_context_set_profile(self._h, int(enable)))
+
+    def read_profile(self):
+        """[(step, ms, kernel, path, points)] of the executes since the last read."""
+        n = ctypes.c_size_t()
+        _check(lib().sb_context_profile_read(self._h, None, 0, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value + 1)
+        _check(lib().sb_context_profile_read(self._h, buf, len(buf), ctypes.byref(n)))
+        out = []
+        for line in buf.value.decode().splitlines():
+            f = line.split()
+            out.append((int(f[0]), float(f[1]), f[2], f[3], int(f[4])))
+        return out
 
     @property
     def launch_count(self) -> int:

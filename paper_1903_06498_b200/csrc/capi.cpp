@@ -128,6 +128,8 @@ struct sb_context {
   cudaEvent_t aux_fork = nullptr, aux_join[4] = {};
   std::vector<std::pair<void*, std::size_t>> roots;  // host-path device buffers
   std::vector<std::pair<void*, std::size_t>> pinned;  // host-path staging
+  bool profile = false;      // per-step device times (sb_context_set_profile)
+  std::string profile_text;  // "step ms kernel path points" lines since the last read
 
   static void release(State& st) {
     cudaFree(st.d_descs);
@@ -592,7 +594,8 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
                  "generic");
     ctx->launches++;
   };
-  static const bool profile = std::getenv("SB_PROFILE_STEPS") != nullptr;
+  static const bool profile_env = std::getenv("SB_PROFILE_STEPS") != nullptr;
+  const bool profile = profile_env || ctx->profile;
   const sb::LaneSchedule& ls = c->lanes;
   if (!profile && ls.nlanes > 1) {
     // independent steps on parallel lanes (events only where a step depends across lanes)
@@ -653,13 +656,15 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
     if (s.elided) continue;
     float ms = 0;
     cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+    char line[512];
     if (s.kind == sb::PStep::Fill)
-      std::fprintf(stderr, "[sb step %3zu] %9.4f ms fill %s (%lld elems)\n", i, ms, plan.bufs[s.buf].name.c_str(),
-                   static_cast<long long>(plan.bufs[s.buf].elements));
+      std::snprintf(line, sizeof(line), "%zu %.6f fill %s %lld\n", i, ms, plan.bufs[s.buf].name.c_str(),
+                    static_cast<long long>(plan.bufs[s.buf].elements));
     else
-      std::fprintf(stderr, "[sb step %3zu] %9.4f ms %s %s points=%lld\n", i, ms,
-                   kinds[static_cast<int>(s.launch.kernel)], s.launch.path.c_str(),
-                   static_cast<long long>(s.launch.points));
+      std::snprintf(line, sizeof(line), "%zu %.6f %s %s %lld\n", i, ms, kinds[static_cast<int>(s.launch.kernel)],
+                    s.launch.path.c_str(), static_cast<long long>(s.launch.points));
+    if (ctx->profile) ctx->profile_text += line;
+    if (profile_env) std::fprintf(stderr, "[sb step] %s", line);
   }
   for (auto& e : ev) cudaEventDestroy(e);
 }
@@ -892,6 +897,27 @@ int sb_context_sync(sb_context* ctx) {
     ctx->window.clear();
     ctx->h_err->code = 1;
     check_device_error(ctx, nullptr);
+  });
+}
+
+int sb_context_set_profile(sb_context* ctx, int enable) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lock(ctx->mu);
+    ctx->profile = enable != 0;
+    ctx->profile_text.clear();
+  });
+}
+
+int sb_context_profile_read(sb_context* ctx, char* buf, size_t cap, size_t* len) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lock(ctx->mu);
+    if (len) *len = ctx->profile_text.size();
+    if (buf && cap) {
+      std::size_t n = std::min(ctx->profile_text.size(), cap - 1);
+      std::memcpy(buf, ctx->profile_text.data(), n);
+      buf[n] = 0;
+      ctx->profile_text.clear();
+    }
   });
 }
 

@@ -1,0 +1,23 @@
+#!/bin/bash
+# Round-2 profiling capture (run on the GPU box via gpurun; writes into gpurun_out/).
+#   1. dense int8 / tf32 peaks (tools/measure_peaks.py -> gpurun_out/r02_peaks.json)
+#   2. per config: the plain run, then the ncu metric list of the same command for every
+#      launch of the steps after the first (DRAM read/write, L2 write, tensor pipe, duration)
+#      -> gpurun_out/ncu_<cfg>.csv (tools/ncu_traffic.py summarises them)
+set -u
+mkdir -p gpurun_out
+M="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_op_write.sum,gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__throughput.avg.pct_of_peak_sustained_elapsed"
+CFGS=${CFGS:-"c2 c3 c4a c4b c1 c1_i32 c5"}
+for cfg in $CFGS; do
+  extra=""
+  skip=4; cnt=8
+  case $cfg in
+    c5) extra="--batch 128"; skip=70; cnt=80;;
+    c1_i32) skip=12; cnt=12;;
+  esac
+  CMD="python tools/run_config.py --config $cfg --steps 4 $extra"
+  $CMD > gpurun_out/plain_$cfg.log 2>&1 && \
+    ncu --metrics $M --clock-control none -s $skip -c $cnt --csv --log-file gpurun_out/ncu_$cfg.csv $CMD \
+      > gpurun_out/ncu_$cfg.log 2>&1
+  echo "$cfg rc=$?"
+done

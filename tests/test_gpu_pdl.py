@@ -41,24 +41,31 @@ def _t(torch, shape, dtype, gen):
 
 
 def test_three_step_chain_step3_reads_step1():
+    """step 1: fused conv (im2col kernel) writes X1 (i8); step 2: an independent resident-filter
+    conv; step 3: a resident-filter conv reading X1 -- launched load-early (its window holds
+    only step 2), so it must not start before step 1 has completed."""
     torch = _dev()
     import paper_1903_06498_b200 as sb
     from paper_1903_06498_b200 import workloads as W
     N, H, C = 8, 56, 64
-    prog = sb.parse_program(W.conv_fused(N, H, H, C, C))
-    assert "conv_i8_tc" in prog.describe_plan(True)
+    p1 = sb.parse_program(W.conv_fused(N, H, H, C, C))
+    p2 = sb.parse_program(W.conv2d(N, H, H, C, C))
+    assert "conv_i8_tc" in p2.describe_plan(True)
     g = torch.Generator(device="cuda").manual_seed(5)
     for trial in range(3):
         X0, Y0 = _t(torch, (N, H, H, C), torch.int8, g), _t(torch, (N, H, H, C), torch.int8, g)
         F, Bias = _t(torch, (3, 3, C, C), torch.int8, g), _t(torch, (C,), torch.int32, g)
         outs = {}
         for mode in (True, False):
-            X1, Y1, X2 = (torch.empty((N, H, H, C), dtype=torch.int8, device="cuda") for _ in range(3))
+            X1 = torch.empty((N, H, H, C), dtype=torch.int8, device="cuda")
+            Y1, X2 = (torch.empty((N, H, H, C), dtype=torch.int32, device="cuda") for _ in range(2))
+            s1 = {"I": (X0.data_ptr(), X0.numel(), 0), "F": (F.data_ptr(), F.numel(), 0),
+                  "Bias": (Bias.data_ptr(), Bias.numel(), 0), "O": (X1.data_ptr(), X1.numel(), sb.SB_BUF_PREPARE)}
 
-            def bufs(i, o):
+            def conv(i, o):
                 return {"I": (i.data_ptr(), i.numel(), 0), "F": (F.data_ptr(), F.numel(), 0),
-                        "Bias": (Bias.data_ptr(), Bias.numel(), 0), "O": (o.data_ptr(), o.numel(), sb.SB_BUF_PREPARE)}
-            _run_chain(torch, [(prog, bufs(X0, X1)), (prog, bufs(Y0, Y1)), (prog, bufs(X1, X2))], sync_each=mode)
+                        "O": (o.data_ptr(), o.numel(), sb.SB_BUF_PREPARE)}
+            _run_chain(torch, [(p1, s1), (p2, conv(Y0, Y1)), (p2, conv(X1, X2))], sync_each=mode)
             outs[mode] = (X1.cpu().numpy(), Y1.cpu().numpy(), X2.cpu().numpy())
         for a, b in zip(outs[True], outs[False]):
             assert np.array_equal(a, b), f"trial {trial}: back-to-back executes differ from synced ones"
