@@ -76,6 +76,15 @@ std::int8_t storage_kind(DType d) {
   return kI32;
 }
 
+// Is refinement `name` an operand of a gather/scatter special of block `b`?
+bool special_operand(const Block& b, const std::string& name) {
+  for (const auto& s : b.stmts)
+    if (s.kind == StmtKind::Special)
+      for (const auto& r : s.refs)
+        if (r == name) return true;
+  return false;
+}
+
 bool is_leaf(const Block& b) {
   for (const auto& s : b.stmts)
     if (s.kind == StmtKind::Block) return false;
@@ -216,15 +225,16 @@ class Lowerer {
       } else if (is_root) {
         v.buf = p_.buffer_index(r.name);
         v.base = flat;
-      } else if (leaf) {
+      } else if (leaf && !special_operand(b, r.name)) {
         // Per-point allocation used only by this block's own statements: every
         // access is at the alloc base (element 0), so it is one register cell,
         // zeroed per point (interp.cpp:442-447).
         v.priv = npriv++;
         priv.emplace_back(r.has_agg ? r.agg : Agg::Assign, r.dtype);
       } else {
-        // Per-iteration allocation visible to child blocks: a scratch slice per
-        // point of this block (and its ancestors), zero-filled before use.
+        // Per-iteration allocation visible to child blocks (or walked whole by a
+        // gather/scatter special, interp.cpp:540-600): a scratch slice per point of this
+        // block (and its ancestors), zero-filled before use.
         std::int64_t ext = r.extent();
         std::int64_t pts = point_count();
         v.buf = new_scratch("alloc:" + path + ":" + r.name, r.dtype, storage_kind(r.dtype), pts * ext);

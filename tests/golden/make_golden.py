@@ -50,7 +50,96 @@ def save(name, text, store, note=""):
     return err
 
 
+SCATTER = """block []:1 (
+	in SRC[0, 0] {dt}(12, 4):(4, 1)
+	in IDX[0, 0] i32(12, 4):(4, 1)
+	out DST[0, 0]:assign {dt}(8, 4):(4, 1)
+) {{
+	0:
+	block []:1 (
+		in SRC[0, 0] {dt}(12, 4):(4, 1)
+		in IDX[0, 0] i32(12, 4):(4, 1)
+		out DST[0, 0]:{agg} {dt}(8, 4):(4, 1)
+	) {{
+		0: special scatter(DST, SRC, IDX)
+	}}
+}}
+"""
+
+LOCAL_GATHER = """block []:1 (
+	in SRC[0, 0] i32(8, 4):(4, 1)
+	in IDX[0, 0] i32(6, 4):(4, 1)
+	out DST[0, 0]:assign i32(6, 4):(4, 1)
+) {
+	0:
+	block [i:6]:6 (
+		in SRC[0, 0] i32(8, 4):(4, 1)
+		in IDX[i, 0] i32(1, 4):(4, 1)
+		inout T[0, 0]:assign i32(1, 4):(4, 1)
+		out DST[i, 0]:assign i32(1, 4):(4, 1)
+	) {
+		0: special gather(T, SRC, IDX)
+		1: $t = load(T)
+		2: DST = store($t)
+	}
+}
+"""
+
+LOCAL_SCATTER = """block []:1 (
+	in A[0, 0] i32(6, 4):(4, 1)
+	in IDX[0, 0] i32(6, 4):(4, 1)
+	out DST[0, 0]:assign i32(8, 4):(4, 1)
+) {
+	0:
+	block [i:6]:6 (
+		in A[i, 0] i32(1, 4):(4, 1)
+		in IDX[i, 0] i32(1, 4):(4, 1)
+		inout T[0, 0]:assign i32(1, 4):(4, 1)
+		out DST[0, 0]:add i32(8, 4):(4, 1)
+	) {
+		0: $a = load(A)
+		1: $b = mul($a, 3)
+		2: T = store($b)
+		3: special scatter(DST, T, IDX)
+	}
+}
+"""
+
+
+def special_cases():
+    """gather/scatter specials the reference runs (interp.cpp:540-600): scatter with add /
+    assign (last writer in lexicographic order) / max aggregation, with index collisions, an
+    i8 scatter-add that wraps (ir.cpp:79-97), an out-of-range index (OutOfBoundsAccess), and
+    specials whose operand is a block-local allocation (interp.cpp:433-447)."""
+    from oracle import Rng, wrap
+    rng = Rng(4242)
+    idx = (rng.bulk(48) % np.uint64(8)).astype(np.int64)  # 12 x 4 indexes into 8 rows: collisions
+    for agg, dt, bits in [("add", "i32", 32), ("assign", "i32", 32), ("max", "i32", 32), ("add", "i8", 8),
+                          ("min", "i16", 16)]:
+        text = SCATTER.format(dt=dt, agg=agg)
+        src = wrap(bits, rng.bulk(48))
+        dst = wrap(bits, rng.bulk(32))
+        save(f"kat_scatter_{agg}_{dt}", text, {"SRC": (bits, src), "IDX": (32, idx), "DST": (bits, dst)},
+             f"scatter {agg} {dt} with index collisions (interp.cpp:578-590)")
+    bad = idx.copy()
+    bad[13] = 8
+    save("kat_scatter_oob", SCATTER.format(dt="i32", agg="add"),
+         {"SRC": (32, wrap(32, rng.bulk(48))), "IDX": (32, bad), "DST": (32, np.zeros(32, np.int64))},
+         "scatter index outside [0, 8) -> OutOfBoundsAccess (interp.cpp:578-582)")
+    save("kat_gather_local", LOCAL_GATHER, {"SRC": (32, 100 + np.arange(32, dtype=np.int64)),
+                                            "IDX": (32, (rng.bulk(24) % np.uint64(8)).astype(np.int64)),
+                                            "DST": (32, wrap(32, rng.bulk(24)))},
+         "gather into a per-point local allocation")
+    save("kat_scatter_local", LOCAL_SCATTER, {"A": (32, wrap(32, rng.bulk(24))),
+                                              "IDX": (32, (rng.bulk(24) % np.uint64(8)).astype(np.int64)),
+                                              "DST": (32, wrap(32, rng.bulk(32)))},
+         "scatter-add from a per-point local allocation")
+
+
 def main():
+    if "--only-specials" in sys.argv:
+        special_cases()
+        return
     for f in glob.glob(os.path.join(HERE, "*.npz")):
         os.remove(f)
     n = 0
@@ -110,6 +199,7 @@ def main():
     cr = open(os.path.join(TESTDATA, "conv_relu.stripe")).read()
     fused = Ref.pipeline(cr, CONV_RELU_HWCFG)
     save("pipe_conv_relu_fused", fused, Ref.random_inputs(Ref.parse(fused), 32), "test_passes.cpp:357-379")
+    special_cases()
     print("wrote", len(glob.glob(os.path.join(HERE, "*.npz"))), "cases")
 
 
