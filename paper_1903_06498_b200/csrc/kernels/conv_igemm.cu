@@ -1452,8 +1452,9 @@ const char* conv_igemm_unsupported(const ConvPlan& cp) {
 }
 
 cudaError_t launch_conv_igemm(const ConvPlan& cp, const ConvArgs& args, cudaStream_t s, int num_sms) {
-  Prepared* pr = nullptr;
+  Prepared prep;  // copied under the lock: another thread's push_back may move the cache
   {
+    Prepared* pr = nullptr;
     std::lock_guard<std::mutex> lock(g_mu);
     if (!g_prep) g_prep = new std::vector<Prepared>();
     for (auto& e : *g_prep)
@@ -1467,8 +1468,9 @@ cudaError_t launch_conv_igemm(const ConvPlan& cp, const ConvArgs& args, cudaStre
       g_prep->push_back(fresh);
       pr = &g_prep->back();
     }
+    prep = *pr;
   }
-  IgKParams kp = pr->kp;
+  IgKParams kp = prep.kp;
   kp.pdl = args.pdl_mode != kPdlOff ? 1 : 0;
   kp.pdl_wait = args.pdl_mode == kPdlWait ? 1 : 0;
   kp.b_early = args.b_immutable ? 1 : 0;
@@ -1489,7 +1491,7 @@ cudaError_t launch_conv_igemm(const ConvPlan& cp, const ConvArgs& args, cudaStre
   cudaMemsetAsync(tr, 0, (640 + 32 * 4 * 3 + 256) * 8, s);
   kp.trace = tr;
   kp.exp = std::getenv("SB_IG_EXP") ? std::atoi(std::getenv("SB_IG_EXP")) : 0;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, conv_igemm_i8_kernel, pr->amap, pr->bmap, pr->cmap, pr->rmap, kp);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, conv_igemm_i8_kernel, prep.amap, prep.bmap, prep.cmap, prep.rmap, kp);
   long long h[640 + 32 * 4 * 3 + 256];
   cudaStreamSynchronize(s);
   cudaMemcpy(h, tr, sizeof(h), cudaMemcpyDeviceToHost);
@@ -1507,7 +1509,7 @@ cudaError_t launch_conv_igemm(const ConvPlan& cp, const ConvArgs& args, cudaStre
     }
   return e;
 #else
-  return cudaLaunchKernelEx(&cfg, conv_igemm_i8_kernel, pr->amap, pr->bmap, pr->cmap, pr->rmap, kp);
+  return cudaLaunchKernelEx(&cfg, conv_igemm_i8_kernel, prep.amap, prep.bmap, prep.cmap, prep.rmap, kp);
 #endif
 }
 

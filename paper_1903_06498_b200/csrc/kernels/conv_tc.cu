@@ -800,8 +800,9 @@ cudaError_t prepare_conv(const ConvPlan& cp, const ConvArgs& args, Prepared* out
 
 cudaError_t launch_conv_tc(const ConvPlan& cp, const ConvArgs& args, cudaStream_t s, int num_sms) {
   static const bool tracing = std::getenv("SB_CONV_TRACE") != nullptr;
-  Prepared* pr = nullptr;
+  Prepared prep;  // copied under the lock: another thread's push_back may move the cache
   {
+    Prepared* pr = nullptr;
     std::lock_guard<std::mutex> lock(g_prep_mu);
     if (!g_prep) g_prep = new std::vector<Prepared>();
     for (auto& e : *g_prep)
@@ -814,8 +815,9 @@ cudaError_t launch_conv_tc(const ConvPlan& cp, const ConvArgs& args, cudaStream_
       g_prep->push_back(fresh);
       pr = &g_prep->back();
     }
+    prep = *pr;
   }
-  ConvKParams kp = pr->kp;
+  ConvKParams kp = prep.kp;
   kp.trace = nullptr;
   if (tracing) {
     if (!g_trace) cudaMalloc(&g_trace, kMaxTrace * 64 * sizeof(unsigned long long));
@@ -862,7 +864,7 @@ cudaError_t launch_conv_tc(const ConvPlan& cp, const ConvArgs& args, cudaStream_
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = kp.pdl ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, conv_i8_tc_kernel, pr->amap, pr->fmap, pr->omap, args.c, kp);
+  return cudaLaunchKernelEx(&cfg, conv_i8_tc_kernel, prep.amap, prep.fmap, prep.omap, args.c, kp);
 }
 
 }  // namespace sb

@@ -679,8 +679,9 @@ cudaError_t launch_tf32_split(const GemmPlan& g, const void* a, const void* b, v
 long long limb_plane_bytes_b(const GemmPlan& g) { return limb_b_off(g, limb_smax(g) + 1); }
 
 cudaError_t launch_gemm_tc(const GemmPlan& g, const GemmArgs& args, cudaStream_t s, int num_sms) {
-  Prepared* pr = nullptr;
+  Prepared prep;  // copied under the lock: another thread's push_back may move the cache
   {
+    Prepared* pr = nullptr;
     std::lock_guard<std::mutex> lock(g_mu);
     if (!g_prep) g_prep = new std::vector<Prepared>();
     for (auto& e : *g_prep)
@@ -693,8 +694,9 @@ cudaError_t launch_gemm_tc(const GemmPlan& g, const GemmArgs& args, cudaStream_t
       g_prep->push_back(fresh);
       pr = &g_prep->back();
     }
+    prep = *pr;
   }
-  GemmKParams kp = pr->kp;
+  GemmKParams kp = prep.kp;
   kp.pdl = args.pdl_mode != kPdlOff ? 1 : 0;
   kp.pdl_wait = args.pdl_mode == kPdlWait ? 1 : 0;
   int tiles = kp.tiles_m * kp.tiles_n;
@@ -708,7 +710,7 @@ cudaError_t launch_gemm_tc(const GemmPlan& g, const GemmArgs& args, cudaStream_t
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = kp.pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, gemm_i8_tc_kernel, pr->amap, pr->bmap, pr->cmap, kp);
+  return cudaLaunchKernelEx(&cfg, gemm_i8_tc_kernel, prep.amap, prep.bmap, prep.cmap, kp);
 }
 
 }  // namespace sb

@@ -356,7 +356,8 @@ def resnet50(N, image=224, width=64, stages=(3, 4, 6, 3), classes=1000, in_ch=3)
         body.append(txt)
         macs = N * K * C * sum(1 for x in range(P) for i in range(R) if 0 <= stride * x + i - pad < H) * \
             sum(1 for y in range(Q) for j in range(S) if 0 <= stride * y + j - pad < W)
-        convs.append(dict(layer=l, H=H, W=W, C=C, K=K, R=R, S=S, stride=stride, pad=pad, P=P, Q=Q, macs=macs))
+        convs.append(dict(layer=l, H=H, W=W, C=C, K=K, R=R, S=S, stride=stride, pad=pad, P=P, Q=Q, macs=macs,
+                          residual=residual is not None))
         return dst, P, Q
 
     a, H, W = new_conv(X, image, image, in_ch, width, 7, 7, 2, 3)

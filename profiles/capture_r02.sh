@@ -8,16 +8,18 @@ set -u
 mkdir -p gpurun_out
 M="gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_op_write.sum,gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__throughput.avg.pct_of_peak_sustained_elapsed"
 CFGS=${CFGS:-"c2 c3 c4a c4b c1 c1_i32 c5"}
+# this library's kernels only (the runner's torch init kernels are not profiled or counted)
+K="conv|gemm|reduce|pool|map_block|generic|fill_kernel|limb|tf32"
 for cfg in $CFGS; do
   extra=""
-  skip=4; cnt=8
+  skip=2; cnt=4
   case $cfg in
-    c5) extra="--batch 128"; skip=70; cnt=80;;
-    c1_i32) skip=12; cnt=12;;
+    c5) extra="--batch 128"; skip=59; cnt=59;;
+    c1_i32) skip=7; cnt=14;;
   esac
   CMD="python tools/run_config.py --config $cfg --steps 4 $extra"
   $CMD > gpurun_out/plain_$cfg.log 2>&1 && \
-    ncu --metrics $M --clock-control none -s $skip -c $cnt --csv --log-file gpurun_out/ncu_$cfg.csv $CMD \
+    ncu --metrics $M --clock-control none -k "regex:$K" -s $skip -c $cnt --csv --log-file gpurun_out/ncu_$cfg.csv $CMD \
       > gpurun_out/ncu_$cfg.log 2>&1
   echo "$cfg rc=$?"
 done
