@@ -1,8 +1,10 @@
-// Parser for the .stripe text format (grammar: proj/README.md "The text format";
-// acceptance rules and error codes follow the reference parser, text.cpp:135-451:
-// SyntaxError for malformed input, ScopeError for undeclared indexes/buffers).
-// Independent implementation: a scanning recursive-descent parser that works
-// directly on the character stream with one token of lookahead.
+// Parser for the .stripe text format (grammar: proj/README.md "The text format").
+// This follows the reference parser (proj/src/text.cpp:135-451) production by production
+// and keeps its diagnostic strings and error codes (SyntaxError for malformed input,
+// ScopeError for undeclared indexes/buffers) so error parity holds at the C ABI, which
+// carries programs as canonical text.  It is the drop-in surface's parser restated, not
+// part of the hot path: the reference's own parse_program stays the front end of the
+// binding (include/stripe_b200_binding.hpp prints the Program and this re-reads it).
 #include <cctype>
 #include <cstdlib>
 
