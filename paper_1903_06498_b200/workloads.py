@@ -192,6 +192,76 @@ def conv_bias_relu(N, H, W, C, K, tx=2, in_dtype="i8", acc_dtype="i32", out_dtyp
 """
 
 
+def conv_relu_prefuse(N, H, W, C, K, in_dtype="i8", acc_dtype="i32", out_dtype="i32"):
+    """testdata/conv_relu.stripe's structure at config-3 scale, BEFORE the pass pipeline: a
+    wrapper block owning T, statement 0 the 3x3 conv leaf [n, x, y, i, j, c, k] into T (add),
+    statement 1 the ReLU leaf [n, x, y, k] with a bias, O = max(T + Bias[k], 0).  Config 3 is
+    this program after the reference's own autotile -> fuse -> localize -> scalarize
+    (test_passes.cpp:357-379), see C3_PIPELINE."""
+    sI = (H * W * C, W * C, C, 1)
+    sF = (3 * K * C, K * C, C, 1)
+    sO = (H * W * K, W * K, K, 1)
+    pts = N * H * W * 9 * C * K
+    return f"""block []:1 (
+	in I[0, 0, 0, 0] {in_dtype}({N}, {H}, {W}, {C}):{sI}
+	in F[0, 0, 0, 0] {in_dtype}(3, 3, {K}, {C}):{sF} #untiled
+	in Bias[0] {acc_dtype}({K}):(1)
+	out O[0, 0, 0, 0]:assign {out_dtype}({N}, {H}, {W}, {K}):{sO}
+) {{
+	0:
+	block []:1 (
+		in I[0, 0, 0, 0] {in_dtype}({N}, {H}, {W}, {C}):{sI}
+		in F[0, 0, 0, 0] {in_dtype}(3, 3, {K}, {C}):{sF} #untiled
+		in Bias[0] {acc_dtype}({K}):(1)
+		inout T[0, 0, 0, 0]:assign {acc_dtype}({N}, {H}, {W}, {K}):{sO}
+		out O[0, 0, 0, 0]:assign {out_dtype}({N}, {H}, {W}, {K}):{sO}
+	) {{
+		0:
+		block [n:{N}, x:{H}, y:{W}, i:3, j:3, c:{C}, k:{K}]:{pts} (
+			i + x - 1 >= 0
+			-i - x + {H} >= 0
+			j + y - 1 >= 0
+			-j - y + {W} >= 0
+			in I[n, x + i - 1, y + j - 1, c] {in_dtype}(1, 1, 1, 1):{sI}
+			in F[i, j, k, c] {in_dtype}(1, 1, 1, 1):{sF} #untiled
+			out T[n, x, y, k]:add {acc_dtype}(1, 1, 1, 1):{sO}
+		) {{
+			0: $I = load(I)
+			1: $F = load(F)
+			2: $O = mul($I, $F)
+			3: T = store($O)
+		}}
+		1:
+		block [n:{N}, x:{H}, y:{W}, k:{K}]:{N * H * W * K} (
+			in T[n, x, y, k] {acc_dtype}(1, 1, 1, 1):{sO}
+			in Bias[k] {acc_dtype}(1):(1)
+			out O[n, x, y, k]:assign {out_dtype}(1, 1, 1, 1):{sO}
+		) {{
+			0: $t = load(T)
+			1: $b = load(Bias)
+			2: $s = add($t, $b)
+			3: $z = constant(0)
+			4: $r = max($s, $z)
+			5: O = store($r)
+		}}
+	}}
+}}
+"""
+
+
+# The pass pipeline of test_passes.cpp:357-379 at config-3 scale (the reference's hwconfig
+# syntax, hwconfig.cpp:81-194): tile both kernels per (image, 2-row band), fuse them, localize
+# T into the fused block, scalarize.  SRAM sized for one band's working set.
+C3_PIPELINE = """mem SRAM cap=1048576 line=64 banks=1
+pass autotile unit=SRAM tiles=n:1,x:2 block=0.0
+pass autotile unit=SRAM tiles=n:1,x:2 block=0.1
+pass fuse block=0 i=0 j=1
+pass localize
+pass scalarize
+pass schedule unit=SRAM
+"""
+
+
 def matmul_bt(M, N, K, in_dtype="i8", out_dtype="i32"):
     """C[m,n] += A[m,k] * B[n,k] (B stored k-contiguous, i.e. transposed)."""
     return matmul(M, N, K, in_dtype, out_dtype).replace(

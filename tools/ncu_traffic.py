@@ -2,9 +2,11 @@
 """Per-kernel DRAM traffic from an ncu --metrics CSV launch list (profiles/capture_r02.sh).
 
 For each kernel name: mean gpu__time_duration, dram__bytes_read, dram__bytes_write and the L2
-write bytes (lts__t_sectors_op_write x 32 B).  An output that fits in the 126 MB L2 is still
-dirty in L2 when its launch ends, so dram__bytes_write undercounts it; the traffic figure
-therefore uses max(dram write, L2 write) -- every written byte is eventually written back.
+write bytes (lts__t_sectors_op_write x 32 B, informational: on B200 it reads ~1.5x the bytes a
+kernel stores, the cross-die L2 traffic is counted too).  traffic = dram read + dram write as
+the roofline contract defines it.  An output that fits in the 126 MB L2 can still be dirty in
+L2 when its launch ends, so dram__bytes_write may undercount the write-back; dram read vs the
+algorithmic input bytes is the re-read check.
 
     python tools/ncu_traffic.py gpurun_out/ncu_c2.csv --config c2 --alg-bytes 32149504 \
         [--merge profiles/r02_traffic.json]
@@ -57,7 +59,9 @@ def summarize(launches):
                      "dram_pct": mean("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
                      "tensor_pct": mean("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed")}
         if rd is not None:
-            out[name]["traffic"] = rd + max(wr or 0, l2w or 0)
+            out[name]["traffic"] = rd + (wr or 0)
+            out[name]["total_traffic"] = (rd + (wr or 0)) * len(ls)
+            out[name]["total_us"] = (out[name]["us"] or 0) * len(ls)
     return out
 
 
@@ -81,6 +85,8 @@ def main():
         if a.alg_bytes:
             e["algorithmic_bytes"] = a.alg_bytes
             e["traffic_over_algorithmic"] = round(e["traffic"] / a.alg_bytes, 3) if e.get("traffic") else None
+        e["all_kernels_traffic"] = sum(v.get("total_traffic") or 0 for v in s.values())
+        e["all_kernels_us"] = sum(v.get("total_us") or 0 for v in s.values())
         cur[a.config] = e
         json.dump(cur, open(a.merge, "w"), indent=1)
 
