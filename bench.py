@@ -161,10 +161,14 @@ def spec(cfg, world, rank, args):
                           what="one image of config 2 per thread (a batch shard)", seed=1001))
     elif cfg == "c3":
         n = args.batch or 128
-        s.update(text=Wk.conv_bias_relu(n, 56, 56, 64, 64), flops=2.0 * Wk.conv_useful_macs(n, 56, 56, 64, 64),
+        # the program the reference's own passes produce (tests/golden/make_pipeline_programs.py)
+        piped = os.path.join(ROOT, "configs", f"c3_pipeline_b{n}.stripe")
+        text = open(piped).read() if os.path.exists(piped) else Wk.conv_bias_relu(n, 56, 56, 64, 64)
+        s.update(text=text, flops=2.0 * Wk.conv_useful_macs(n, 56, 56, 64, 64),
                  unit="GFLOP/s", bound="hbm", global_batch=n * world, images=n, dominant=("conv_i8_tc",),
-                 workload=f"BASELINE config 3: fused conv3x3+bias+ReLU (tile/fuse/localize form), 56x56x64->64, "
-                          f"batch {n} per GPU",
+                 workload=f"BASELINE config 3: fused conv3x3+bias+ReLU produced by the reference's "
+                          f"tile_rewrite/fuse/localize/scalarize passes ({os.path.basename(piped) if os.path.exists(piped) else 'hand-built equivalent'}), "
+                          f"56x56x64->64, batch {n} per GPU",
                  cpu=dict(text=Wk.conv_bias_relu(1, 56, 56, 64, 64),
                           work=2.0 * Wk.conv_useful_macs(1, 56, 56, 64, 64),
                           what="one image of config 3 per thread (a batch shard)", seed=1003))
