@@ -371,3 +371,16 @@ class Port:
         if rc:
             raise OracleError(err)
         return out
+
+
+def reference_execute(text: str, store: Dict[str, np.ndarray]) -> Dict[str, np.ndarray]:
+    """The parity checker the GPU tests use: the UNMODIFIED reference (its own parser and
+    interpreter, oracle/_ref) when it was built, so the checker shares no code with the
+    product; the port restatement (which shares the product's parser) only as a fallback.
+    store: name -> int64 carriers; returns name -> int64 arrays after execute()."""
+    if Ref.available():
+        p = Ref.parse(text)
+        bits = {b[0]: b[1] for b in p.buffers()}
+        out = Ref.execute(p, {n: (bits.get(n, 32), np.ascontiguousarray(a, dtype=np.int64)) for n, a in store.items()})
+        return {n: v[1] for n, v in out.items()}
+    return Port.execute(text, store)

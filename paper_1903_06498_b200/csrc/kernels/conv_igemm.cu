@@ -81,6 +81,7 @@ struct IgKParams {
   int bn;      // tile width in output channels: 128 or 256 (N = 256 MMAs, 512 TMEM columns)
   int mt;      // 128-row M sub-tiles per tile (1 or 2): one stage feeds mt x the MMAs
   int bn_box;  // filter rows per TMA box / smem tile: 64 when N <= 64, else bn
+  int stg4;    // split i8 epilogue with two staging buffers per group (when smem allows)
   // residual added by the tensor core: res tile (pixels x channels, SW128) x identity (128 x 128,
   // resident) accumulated into the tile after its k-blocks; loaded by a fifth producer warp
   int res_mma, ident_off;
@@ -170,6 +171,29 @@ __device__ __forceinline__ void umma_commit(std::uint64_t* bar) {
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// tcgen05.ld without the wait: the registers are valid only after tmem_wait_ld(v), whose
+// "+r" operands keep every use of v behind the wait.
+__device__ __forceinline__ void tmem_ld32_async(std::uint32_t taddr, std::uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld(std::uint32_t (&v)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+                 "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15]),
+                 "+r"(v[16]), "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]), "+r"(v[22]), "+r"(v[23]),
+                 "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]), "+r"(v[29]), "+r"(v[30]), "+r"(v[31])
+               :
+               : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld32(std::uint32_t taddr, std::uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
@@ -645,9 +669,10 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       if (leader) TILE_STAMP(8, iter);
       if (p.tma_out || eres) {
         // i32 staging is single-buffered, i8 staging double-buffered (one buffer per group when split)
-        if (leader && (p.tma_out == 1 || (split && p.tma_out == 2)))
+        if (leader && (p.tma_out == 1 || (split && p.tma_out == 2 && !p.stg4)))
           asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        if (leader && !split && p.tma_out == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        if (leader && ((!split && p.tma_out == 2) || p.stg4))
+          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         asm volatile("bar.sync %0, %1;" ::"r"(gbar), "r"(gthreads) : "memory");  // staging and the older residual buffer are free
       }
       if (!split && eres && leader && t + static_cast<int>(gridDim.x) < tiles) load_res(t + gridDim.x, (iter + 1) & 1);
@@ -656,7 +681,9 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       if (leader) TILE_STAMP(3, iter);
       if (eres) mbar_wait(&rfull[iter & 1], (iter >> 1) & 1);
       std::uint8_t* rcur = rstg + (iter & 1) * res_buf;
-      std::uint8_t* scur = p.tma_out == 2 ? stg + (iter & 1) * stg_buf : stg;
+      // i8 staging: buffer iter & 1 (one per group when split), or iter & 3 with stg4 (a group
+      // alternates between its two buffers: tile t's TMA store drains while t + 2 is staged)
+      std::uint8_t* scur = p.tma_out == 2 ? stg + (iter & (p.stg4 ? 3 : 1)) * stg_buf : stg;
       const int m = m0 + row;
       // this warp's 32-column chunks: all valid chunks (split), else the valid chunks of the
       // tile divided between the two column groups
@@ -672,9 +699,13 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
           for (int q = 0; q < 32; q++) v[q] = 0;
         } else
 #endif
-        tmem_ld32(tmem_base + (static_cast<std::uint32_t>(quarter * 32) << 16) +
-                      static_cast<std::uint32_t>(acc * p.mt * p.bn + sub * p.bn + h * 32),
-                  v);
+        {
+          const std::uint32_t ta = tmem_base + (static_cast<std::uint32_t>(quarter * 32) << 16) +
+                                   static_cast<std::uint32_t>(acc * p.mt * p.bn + sub * p.bn + h * 32);
+          // fast8: the TMEM load is waited for only after the bias loads below were issued
+          if (fast8) tmem_ld32_async(ta, v);
+          else tmem_ld32(ta, v);
+        }
         const int kbase = n0 + h * 32;
         if (fast8) {
           // out = wrap8(max(acc + res + vec, lo)) in int32 (exact: see IgKParams::fast8)
@@ -690,6 +721,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
               bv[4 * q] = bv[4 * q + 1] = bv[4 * q + 2] = bv[4 * q + 3] = 0;
           }
           std::uint32_t w[8];
+          tmem_wait_ld(v);
           if (eres) {
             std::uint32_t rw[8];
             const std::uint32_t rrow = smem_u32(rcur + (sub * hcnt + (h >> 2)) * 16384 + row * 128);
@@ -1031,7 +1063,7 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     kp.mt = mt;
     kp.tiles_n = (kp.N + bn - 1) / bn;
     kp.tiles_m = (kp.M + BM * mt - 1) / (BM * mt);
-    const int stg = kp.tma_out == 1 ? kStgBytes : kp.tma_out == 2 ? 2 * mt * (bn / 128) * 16384 : 0;
+    const int stg = kp.tma_out == 1 ? kStgBytes : kp.tma_out == 2 ? (kp.stg4 ? 4 : 2) * mt * (bn / 128) * 16384 : 0;
     const int res = kp.epi_res ? 2 * BM * mt * bn : 0;
     const int vec = kp.fast_clamp ? 2 * kVecBytes : kp.epi_vec ? kVecBytes : 0;
     const int tab = kp.gather ? (kp.kblocks * kp.bk * 6 + 15) / 16 * 16 : 0;
@@ -1075,7 +1107,17 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
   // MMAs) for narrow outputs with enough tiles left for every SM
   const bool tall = kp.epi_split && kp.tma_out != 1 && kp.N <= 128 && !(kp.epi_res && !kp.res_mma) &&
                     (kp.M + 2 * BM - 1) / (2 * BM) >= 2 * 148 && !std::getenv("SB_IG_MT1");
-  if (!(wide && layout(256, 1)) && !(tall && layout(128, 2)) && !layout(128, 1)) return cudaErrorNotSupported;
+  // split i8 epilogue: two staging buffers per group when the ring keeps >= 3 stages
+  const bool stg4_ok = kp.epi_split && kp.tma_out == 2 && !std::getenv("SB_IG_STG2");
+  auto shape = [&](int bn, int mt) {
+    if (stg4_ok) {
+      kp.stg4 = 1;
+      if (layout(bn, mt) && kp.stages >= 3) return true;
+    }
+    kp.stg4 = 0;
+    return layout(bn, mt);
+  };
+  if (!(wide && shape(256, 1)) && !(tall && shape(128, 2)) && !shape(128, 1)) return cudaErrorNotSupported;
   // idesc: S32 accumulate, signed A/B, both K-major, N = 128, M = 128
   kp.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
   // descriptor high word: SBO = 8 rows x row bytes, version 1, swizzle 128B (2) / 64B (4)

@@ -23,3 +23,12 @@ for cfg in $CFGS; do
       > gpurun_out/ncu_$cfg.log 2>&1
   echo "$cfg rc=$?"
 done
+# kernel families no BASELINE config isolates: the element-wise map kernel (config 3's epilogue
+# unfused) and the windowed pool kernel (the ResNet stem max-pool)
+for prog in ${PROGS:-"map pool"}; do
+  CMD="python tools/run_config.py --program $prog --steps 4"
+  $CMD > gpurun_out/plain_$prog.log 2>&1 && \
+    ncu --metrics $M --clock-control none -k "regex:$K" -s 2 -c 2 --csv --log-file gpurun_out/ncu_$prog.csv $CMD \
+      > gpurun_out/ncu_$prog.log 2>&1
+  echo "$prog rc=$?"
+done

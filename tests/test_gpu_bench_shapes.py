@@ -25,11 +25,12 @@ def _need_gpu():
 
 
 def _ctx():
+    """A context on its own (non-blocking) stream: every execute below is preceded by
+    torch.cuda.synchronize() so the inputs torch wrote on its stream are complete."""
     import torch
     import paper_1903_06498_b200 as sb
-    ctx = sb.Context(0)
-    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
-    return ctx
+    torch.cuda.synchronize()
+    return sb.Context(0)
 
 
 def _wrap(bits, x):
@@ -84,6 +85,7 @@ def test_c4a_maxpool_full_shape():
     # accumulate into existing contents (no prepare): max(old, window)
     O2 = torch.randint(-2**31, 2**31 - 1, O.shape, dtype=torch.int64, device="cuda", generator=g).to(torch.int32)
     old = O2.clone()
+    torch.cuda.synchronize()
     ctx.execute_device(prog, {"I": (I.data_ptr(), I.numel(), 0), "O": (O2.data_ptr(), O2.numel(), 0)})
     ctx.sync()
     assert torch.equal(O2, torch.maximum(old, exp))

@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 from harness import gpu_available, run_device
-from oracle import Port, Ref, random_inputs
+from oracle import Port, Ref, random_inputs, reference_execute
 from paper_1903_06498_b200 import workloads as W
 
 pytestmark = pytest.mark.gpu
@@ -39,7 +39,7 @@ def expected(text, inputs):
         r = Ref.parse(text)
         out = Ref.execute(r, {n: (p.buffers[n].dtype, a) for n, a in store.items()})
         return {n: v[1] for n, v in out.items()}
-    return Port.execute(text, store)
+    return reference_execute(text, store)
 
 
 SHAPES = [
@@ -108,15 +108,14 @@ def test_conv_tc_full_config2_exact():
     I = torch.randint(-128, 128, (N, H, Wd, C), dtype=torch.int8, device="cuda", generator=g)
     F = torch.randint(-128, 128, (3, 3, K, C), dtype=torch.int8, device="cuda", generator=g)
     O = torch.full((N, H, Wd, K), 12345, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()  # the context's own stream does not wait for torch's
     ctx = sb.default_context(0)
-    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
     ctx.execute_device(prog, {"I": (I.data_ptr(), I.numel(), 0), "F": (F.data_ptr(), F.numel(), 0),
                               "O": (O.data_ptr(), O.numel(), sb.SB_BUF_PREPARE)})
     ctx.sync()
     ref = torch.nn.functional.conv2d(I.permute(0, 3, 1, 2).double(), F.permute(2, 3, 0, 1).double(), padding=1)
     ref = ref.permute(0, 2, 3, 1).to(torch.int64)
     assert torch.equal(O.to(torch.int64), ref)
-    ctx.set_stream(None)
 
 
 @pytest.mark.parametrize("shape", [(2, 8, 8, 64, 64), (1, 6, 20, 128, 32), (3, 4, 9, 64, 96)],

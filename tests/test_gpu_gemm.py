@@ -3,7 +3,7 @@ import numpy as np
 import pytest
 
 from harness import gpu_available, run_device
-from oracle import Port, Ref, random_inputs
+from oracle import Port, Ref, random_inputs, reference_execute
 from paper_1903_06498_b200 import workloads as W
 
 pytestmark = pytest.mark.gpu
@@ -33,7 +33,7 @@ def check(text, seed=3, provide_out=False):
     if Ref.available():
         exp = {n: v[1] for n, v in Ref.execute(Ref.parse(text), {n: (p.buffers[n].dtype, a) for n, a in store.items()}).items()}
     else:
-        exp = Port.execute(text, store)
+        exp = reference_execute(text, store)
     got = run_device(text, inp)
     np.testing.assert_array_equal(got["C"], exp["C"])
 

@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 from harness import gpu_available
-from oracle import Port
+from oracle import Port, reference_execute
 
 pytestmark = pytest.mark.gpu
 
@@ -78,7 +78,7 @@ def test_igemm_pinned_against_port():
     from paper_1903_06498_b200 import workloads as W
     text = W.conv2d(1, 9, 7, 64, 192, 3, 3, pad=1, stride=2)
     prog, inp, out = run(text, seed=5)
-    ref = Port.execute(text, {**inp, "O": np.zeros_like(out["O"])})
+    ref = reference_execute(text, {**inp, "O": np.zeros_like(out["O"])})
     np.testing.assert_array_equal(out["O"], ref["O"])
 
 
@@ -142,7 +142,7 @@ def test_fused_small_pinned_against_port():
     from paper_1903_06498_b200 import workloads as W
     text = W.conv_fused(1, 6, 6, 64, 128, 3, 3, 2, 1)
     prog, inp, out = run(text, seed=9)
-    ref = Port.execute(text, {**inp, "O": np.zeros_like(out["O"])})
+    ref = reference_execute(text, {**inp, "O": np.zeros_like(out["O"])})
     np.testing.assert_array_equal(out["O"], ref["O"])
 
 
@@ -189,7 +189,7 @@ def test_gather_stem_fused_vs_port(small_c_mode):
     from paper_1903_06498_b200 import workloads as W
     text = W.conv_fused(1, 12, 12, 3, 64, 7, 7, 2, 3)
     prog, inp, out = run(text, seed=21)
-    ref = Port.execute(text, {**inp, "O": np.zeros_like(out["O"])})
+    ref = reference_execute(text, {**inp, "O": np.zeros_like(out["O"])})
     np.testing.assert_array_equal(out["O"], ref["O"])
 
 

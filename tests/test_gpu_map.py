@@ -3,7 +3,7 @@ import numpy as np
 import pytest
 
 from harness import gpu_available, run_device
-from oracle import Port, Ref, random_inputs
+from oracle import Port, Ref, random_inputs, reference_execute
 from paper_1903_06498_b200 import workloads as W
 
 pytestmark = pytest.mark.gpu
@@ -31,7 +31,7 @@ def check(text, seed=1, expect_kernel="map"):
     if Ref.available():
         exp = {n: v[1] for n, v in Ref.execute(Ref.parse(text), {n: (p.buffers[n].dtype, a) for n, a in store.items()}).items()}
     else:
-        exp = Port.execute(text, store)
+        exp = reference_execute(text, store)
     got = run_device(text, inp)
     for n in exp:
         np.testing.assert_array_equal(got[n], exp[n], err_msg=n)
@@ -79,7 +79,7 @@ def test_reduce_row_split(dt, agg, prefill):
     store = {n: a for n, (b, a) in inp.items()}
     if "O" not in store:
         store["O"] = np.full(p.buffers["O"].elements, p.output_identity("O"), np.int64)
-    exp = Port.execute(text, {n: a.copy() for n, a in store.items()})
+    exp = reference_execute(text, {n: a.copy() for n, a in store.items()})
     got = run_device(text, inp)
     np.testing.assert_array_equal(got["O"], exp["O"])
 

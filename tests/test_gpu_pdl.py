@@ -22,6 +22,7 @@ def _dev():
 
 def _run_chain(torch, steps, sync_each):
     import paper_1903_06498_b200 as sb
+    torch.cuda.synchronize()  # inputs written on torch's stream are complete
     ctx = sb.Context(0)
     stream = torch.cuda.Stream()
     ctx.set_stream(stream.cuda_stream)

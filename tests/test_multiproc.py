@@ -23,7 +23,7 @@ def _free_port():
 def _worker(rank, world, port, out):
     import torch
 
-    from oracle import Port, Rng, wrap
+    from oracle import Port, Rng, wrap, reference_execute
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     N, H, Wd, C, K = 4, 5, 6, 8, 4
@@ -32,14 +32,14 @@ def _worker(rank, world, port, out):
     F = wrap(8, rng.bulk(9 * K * C))
     lo, hi = W.shard_range(N, world, rank)
     text = W.conv2d(hi - lo, H, Wd, C, K)
-    o = Port.execute(text, {"I": I[lo:hi].ravel(), "F": F, "O": np.zeros((hi - lo) * H * Wd * K, np.int64)})["O"]
+    o = reference_execute(text, {"I": I[lo:hi].ravel(), "F": F, "O": np.zeros((hi - lo) * H * Wd * K, np.int64)})["O"]
     objs = [None] * world
     dist.all_gather_object(objs, o)
     gathered = [torch.from_numpy(x.astype(np.float64)) for x in objs]
     elapsed = torch.tensor([1.0 + rank])  # bench.py: device time reduced with MAX over ranks
     dist.all_reduce(elapsed, op=dist.ReduceOp.MAX)
     if rank == 0:
-        full = Port.execute(W.conv2d(N, H, Wd, C, K), {"I": I.ravel(), "F": F,
+        full = reference_execute(W.conv2d(N, H, Wd, C, K), {"I": I.ravel(), "F": F,
                                                        "O": np.zeros(N * H * Wd * K, np.int64)})["O"]
         out["ok"] = bool(np.array_equal(torch.cat(gathered).numpy().astype(np.int64), full))
         out["max"] = float(elapsed.item())
@@ -49,7 +49,7 @@ def _worker(rank, world, port, out):
 
 @pytest.mark.timeout(300)
 def test_batch_sharding_gloo_world2():
-    from oracle import Port
+    from oracle import Port, reference_execute
     if not Port.available():
         pytest.skip("oracle/_port not built")
     mgr = mp.Manager()
@@ -73,7 +73,7 @@ def _split_worker(rank, world, port, out):
     import torch
 
     import paper_1903_06498_b200 as sb
-    from oracle import Port, Rng, wrap
+    from oracle import Port, Rng, wrap, reference_execute
     from paper_1903_06498_b200.parallel import allreduce_outputs, shard_aggregation
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -99,14 +99,14 @@ def _split_worker(rank, world, port, out):
         for n, d in prog.buffers.items():
             if d.dir != sb.Dir.In:
                 store[n] = np.full(d.elements, prog.output_identity(n), np.int64)  # fresh on every rank
-        part = Port.execute(sb.print_program(shard), store)
+        part = reference_execute(sb.print_program(shard), store)
         outs = {n: torch.from_numpy(part[n].copy()) for n, d in prog.buffers.items() if d.dir != sb.Dir.In}
         allreduce_outputs(prog, outs)
         full_store = dict(inputs)
         for n, d in prog.buffers.items():
             if d.dir != sb.Dir.In:
                 full_store[n] = np.full(d.elements, prog.output_identity(n), np.int64)
-        full = Port.execute(text, full_store)
+        full = reference_execute(text, full_store)
         ok[name] = all(np.array_equal(outs[n].numpy(), full[n]) for n in outs)
     if rank == 0:
         out.update(ok)
@@ -116,7 +116,7 @@ def _split_worker(rank, world, port, out):
 
 @pytest.mark.timeout(300)
 def test_split_aggregation_gloo_world2():
-    from oracle import Port
+    from oracle import Port, reference_execute
     if not Port.available():
         pytest.skip("oracle/_port not built")
     mgr = mp.Manager()
@@ -143,7 +143,7 @@ def test_split_k_shards_on_device():
     if not gpu_available():
         pytest.skip("no B200")
     import paper_1903_06498_b200 as sb
-    from oracle import Rng, wrap
+    from oracle import Rng, wrap, reference_execute
     from paper_1903_06498_b200.parallel import shard_aggregation
     text = W.matmul(256, 128, 512, in_dtype="i8", out_dtype="i32")
     prog = sb.parse_program(text)
@@ -191,7 +191,7 @@ def test_restrict_index_shifts_tile_aliases_fig6b():
     equal the full program (reference fixture testdata/fig6b.stripe)."""
     import paper_1903_06498_b200 as sb
     from harness import corpus
-    from oracle import Ref
+    from oracle import Ref, reference_execute
     if not Ref.available():
         pytest.skip("oracle/_ref not built")
     case = next(c for c in corpus() if c.name == "fx_fig6b")

@@ -35,7 +35,7 @@ def test_c3_pipeline_program_plans_fused():
 
 def test_c3_pipeline_regenerates_identically():
     """The committed text is what the reference's passes produce (small case here)."""
-    from oracle import Ref
+    from oracle import Ref, reference_execute
     if not Ref.available():
         pytest.skip("oracle/_ref not built")
     import sys
@@ -67,7 +67,7 @@ def _bank_worker(rank, world, port, out):
     import torch
 
     import paper_1903_06498_b200 as sb
-    from oracle import Port, Ref
+    from oracle import Port, Ref, reference_execute
     from paper_1903_06498_b200 import workloads as W
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -79,7 +79,7 @@ def _bank_worker(rank, world, port, out):
     o = base["O"].copy()
     for bank in range(rank, 4, world):  # this rank's banks: disjoint slices of O
         shard = sb.print_program(prog.restrict_index("0", "n", bank, bank + 1))
-        part = Port.execute(shard, dict(base))["O"]
+        part = reference_execute(shard, dict(base))["O"]
         changed = part != base["O"]
         o[changed] = part[changed]
     t = torch.from_numpy(o - base["O"])
@@ -93,7 +93,7 @@ def _bank_worker(rank, world, port, out):
 
 @pytest.mark.timeout(300)
 def test_partition_banks_as_shards_gloo_world2():
-    from oracle import Port, Ref
+    from oracle import Port, Ref, reference_execute
     if not (Port.available() and Ref.available()):
         pytest.skip("oracles not built")
     mgr = mp.Manager()
@@ -126,6 +126,7 @@ def test_c3_pipeline_b128_on_device_exact():
     F = torch.randint(-128, 128, (3, 3, K, C), dtype=torch.int8, device="cuda", generator=g)
     B = torch.randint(-2**31, 2**31 - 1, (K,), dtype=torch.int64, device="cuda", generator=g).to(torch.int32)
     O = torch.full((N, H, H, K), 3, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()  # the context's own stream does not wait for torch's
     ctx = sb.Context(0)
     ctx.execute_device(prog, {"I": (I.data_ptr(), I.numel(), 0), "F": (F.data_ptr(), F.numel(), 0),
                               "Bias": (B.data_ptr(), B.numel(), 0), "O": (O.data_ptr(), O.numel(), sb.SB_BUF_PREPARE)})
@@ -139,7 +140,7 @@ def test_c3_pipeline_b128_on_device_exact():
 def test_c3_pipeline_b2_vs_reference():
     _dev()
     from harness import run_device
-    from oracle import Ref
+    from oracle import Ref, reference_execute
     text = _text("c3_pipeline_b2.stripe")
     r = Ref.parse(text)
     store = Ref.random_inputs(r, 32)
@@ -162,6 +163,7 @@ def test_c2_partition_banks_on_device():
     ctx = sb.Context(0)
 
     def run(p, O, flags):
+        torch.cuda.synchronize()  # the context's own stream does not wait for torch's
         ctx.execute_device(p, {"I": (I.data_ptr(), I.numel(), 0), "F": (F.data_ptr(), F.numel(), 0),
                                "O": (O.data_ptr(), O.numel(), flags)})
         ctx.sync()

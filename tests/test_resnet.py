@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 from harness import GOLDEN, gpu_available
-from oracle import Port, Ref, random_inputs
+from oracle import Port, Ref, random_inputs, reference_execute
 
 TINY = dict(image=32, width=8, stages=(1, 1, 1, 1), classes=10)
 
@@ -78,7 +78,7 @@ def test_tiny_resnet_gpu_vs_reference():
     bufs = [(n, int(d.dtype), d.elements, int(d.dir)) for n, d in prog.buffers.items()]
     store = random_inputs(bufs, 1005)
     store["Logits"] = np.zeros(prog.buffers["Logits"].elements, dtype=np.int64)
-    port = Port.execute(text, store)
+    port = reference_execute(text, store)
     np.testing.assert_array_equal(logits, port["Logits"])
 
 

@@ -34,6 +34,10 @@ def main():
         text = W.conv_fused(batch, 14, 14, 256, 1024, 1, 1, 1, 0, residual=True)
     elif which == "l1x1r":
         text = W.conv_fused(batch, 56, 56, 64, 256, 1, 1, 1, 0, residual=True)
+    elif which == "l1x1p":
+        text = W.conv_fused(batch, 56, 56, 64, 256, 1, 1, 1, 0, relu=False)
+    elif which == "pool":
+        text = W.pool2d(batch, 112, 112, 64)
     elif which == "l1x1":
         text = W.conv_fused(batch, 56, 56, 64, 64, 1, 1, 1, 0)
     elif which == "c2":
