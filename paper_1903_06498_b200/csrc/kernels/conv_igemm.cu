@@ -34,6 +34,7 @@
 
 // Development aid (make trace): per-tile timestamps of CTA 0 printed after each launch.
 #ifdef SB_TILE_TRACE
+#define EPI_EXP p.exp
 #include <cstdio>
 #define TILE_STAMP(slot, i) \
   do {                                                                            \
@@ -44,6 +45,7 @@
     if (p.trace && blockIdx.x == 0 && (iter) < 32 && (st) < 4) p.trace[640 + ((iter)*4 + (st)) * 3 + (k)] = clock64(); \
   } while (0)
 #else
+#define EPI_EXP 0
 #define STAGE_STAMP(iter, st, k) \
   do {                           \
   } while (0)
@@ -105,6 +107,7 @@ struct IgKParams {
   int fast8;
   long long bias_bound;
   int thr_always;  // fast8 with a clamp bound outside int32: always the threshold form
+  int epi_pipe;    // fast8 epilogue with the next chunk's TMEM load in flight
   const void* vec;
   long long vec_k;
   long long lo;
@@ -207,6 +210,23 @@ __device__ __forceinline__ void tmem_ld32(std::uint32_t taddr, std::uint32_t (&v
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// 16-column TMEM loads (32 lanes x 16 columns): the i8 epilogue ping-pongs two of these
+__device__ __forceinline__ void tmem_ld16_async(std::uint32_t taddr, std::uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld16(std::uint32_t (&v)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+                 "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15])
+               :
+               : "memory");
+}
+
 // One ring stage's MMAs, fully unrolled (compile-time KPB k-blocks x KS 32-byte k-steps):
 // descriptors advance by constants, so the issue is a straight run of uniform adds + UTCIMMA.
 template <int KPB, int KS>
@@ -217,6 +237,97 @@ __device__ __forceinline__ void issue_stage(std::uint32_t d, std::uint32_t a0, s
 #pragma unroll
     for (int ks = 0; ks < KS; ks++)
       umma_i8(d, a0 + j * a_step + ks * 2, hi, b0 + j * b_step + ks * 2, hi, idesc, (first && j == 0 && ks == 0) ? 0u : 1u);
+}
+
+// i8 TMA-store epilogue of one tile, software-pipelined: chunk c+1's TMEM load is in flight
+// while chunk c is transformed and staged (tcgen05.wait::ld waits for every outstanding load,
+// so the next load is issued right after the wait that makes chunk c valid).  Chunks run over
+// (sub-tile, 32-column chunk) pairs; out = wrap8(max(acc + res + vec, lo)) or, with THR, the
+// exact threshold form acc + res >= t[k] ? acc + res + vec : lo (see IgKParams::fast8).
+// vaddr / taddr: this tile's vector / threshold in smem; raddr / saddr: this thread's row of
+// the residual / staging buffer (16 KB boxes of 128 rows x 128 bytes, 128B swizzle).
+__device__ __forceinline__ std::uint32_t lds32(std::uint32_t a) {
+  std::uint32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint4 lds128(std::uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+// one 16-column half chunk (columns 32 h + 16 hf ..): transform v and stage its 16 bytes
+template <bool THR, bool RES>
+__device__ __forceinline__ void epi8_half(const std::uint32_t (&v)[16], int sub, int h, int hf, std::uint32_t vaddr,
+                                          std::uint32_t taddr, std::uint32_t raddr, std::uint32_t saddr, int hcnt,
+                                          int sw, std::uint32_t lo32u, std::int32_t lo8) {
+  const std::uint32_t box = (sub * hcnt + (h >> 2)) * 16384;
+  const std::uint32_t unit = (((2 * (h & 3) + hf) ^ sw) << 4);
+  uint4 r4 = make_uint4(0, 0, 0, 0);
+  if (RES) r4 = lds128(raddr + box + unit);
+  const std::uint32_t rq[4] = {r4.x, r4.y, r4.z, r4.w};
+  std::uint32_t w[4];
+#pragma unroll
+  for (int q4 = 0; q4 < 4; q4++) {
+    const int col = h * 32 + hf * 16 + 4 * q4;
+    const uint4 b4 = lds128(vaddr + col * 4);
+    const std::uint32_t bq[4] = {b4.x, b4.y, b4.z, b4.w};
+    uint4 t4 = make_uint4(0, 0, 0, 0);
+    if (THR) t4 = lds128(taddr + col * 4);
+    const std::uint32_t tq[4] = {t4.x, t4.y, t4.z, t4.w};
+    std::uint32_t o[4];
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      std::int32_t x = static_cast<std::int32_t>(v[4 * q4 + e]);
+      if (RES) {
+        std::int32_t r;  // sign-extended residual byte (prmt sign-replicate selector)
+        asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(rq[q4]), "r"(0x8880u + 0x1111u * e));
+        x += r;
+      }
+      if (THR) o[e] = x >= static_cast<std::int32_t>(tq[e]) ? static_cast<std::uint32_t>(x) + bq[e] : lo32u;
+      else o[e] = static_cast<std::uint32_t>(max(x + static_cast<std::int32_t>(bq[e]), lo8));
+    }
+    w[q4] = __byte_perm(__byte_perm(o[0], o[1], 0x0040), __byte_perm(o[2], o[3], 0x0040), 0x5410);
+  }
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(saddr + box + unit), "r"(w[0]), "r"(w[1]), "r"(w[2]),
+               "r"(w[3]));
+}
+
+// i8 TMA-store epilogue of one tile, software-pipelined over two 16-column register buffers:
+// half k+1's TMEM load is in flight while half k is transformed and staged (tcgen05.wait::ld
+// waits for every outstanding load, so the next load is issued right after the wait that made
+// half k valid; two named buffers, no register copies).  Halves run over (sub-tile, 32-column
+// chunk, half); out = wrap8(max(acc + res + vec, lo)) or, with THR, the exact threshold form
+// acc + res >= t[k] ? acc + res + vec : lo (see IgKParams::fast8).  vaddr / taddr: this tile's
+// vector / threshold in smem; raddr / saddr: this thread's row of the residual / staging
+// buffer (16 KB boxes of 128 rows x 128 bytes, 128B swizzle).
+template <bool THR, bool RES>
+__device__ __forceinline__ void epi8_pipelined(std::uint32_t tbase, int bn, int mt, int c_lo, int per,
+                                               std::uint32_t vaddr, std::uint32_t taddr, std::uint32_t raddr,
+                                               std::uint32_t saddr, int hcnt, int sw, std::uint32_t lo32u,
+                                               std::int32_t lo8, int exp) {
+  const int total = mt * per, c_end = c_lo + per;
+  if (total <= 0) return;
+  std::uint32_t va[16], vb[16];
+  // chunk (sub, h): half 0 in va, half 1 in vb; the next chunk's column advanced incrementally
+  tmem_ld16_async(tbase + c_lo * 32, va);
+  int sub = 0, h = c_lo;
+  for (int c = 0; c < total; c++) {
+    int nsub = sub, nh = h + 1;
+    if (nh == c_end) {
+      nh = c_lo;
+      nsub++;
+    }
+    const std::uint32_t col = tbase + sub * bn + h * 32;
+    tmem_wait_ld16(va);
+    tmem_ld16_async(col + 16, vb);
+    epi8_half<THR, RES>(va, sub, h, 0, vaddr, taddr, raddr, saddr, hcnt, sw, lo32u, lo8);
+    tmem_wait_ld16(vb);
+    if (c + 1 < total) tmem_ld16_async(tbase + nsub * bn + nh * 32, va);
+    epi8_half<THR, RES>(vb, sub, h, 1, vaddr, taddr, raddr, saddr, hcnt, sw, lo32u, lo8);
+    sub = nsub;
+    h = nh;
+  }
 }
 
 __global__ void __launch_bounds__(kThreadsGather, 1)
@@ -690,6 +801,17 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       const int nch = min(p.bn, p.N - n0 + 31) / 32;
       const int c_lo = split || hgroups == 1 ? 0 : (hgroup * nch) >> 1;
       const int c_hi = split || hgroups == 1 ? nch : ((hgroup + 1) * nch) >> 1;
+      if (fast8 && p.epi_pipe) {
+        const std::uint32_t tbase = tmem_base + (static_cast<std::uint32_t>(quarter * 32) << 16) +
+                                    static_cast<std::uint32_t>(acc * p.mt * p.bn);
+        const std::uint32_t vaddr = smem_u32(vec_s + n0), taddr = smem_u32(thr_s + n0);
+        const std::uint32_t raddr = smem_u32(rcur) + row * 128, saddr = smem_u32(scur) + row * 128;
+        const int per = c_hi - c_lo;
+        if (thr8 && eres) epi8_pipelined<true, true>(tbase, p.bn, p.mt, c_lo, per, vaddr, taddr, raddr, saddr, hcnt, sw, lo32u, lo8, EPI_EXP);
+        else if (thr8) epi8_pipelined<true, false>(tbase, p.bn, p.mt, c_lo, per, vaddr, taddr, raddr, saddr, hcnt, sw, lo32u, lo8, EPI_EXP);
+        else if (eres) epi8_pipelined<false, true>(tbase, p.bn, p.mt, c_lo, per, vaddr, taddr, raddr, saddr, hcnt, sw, lo32u, lo8, EPI_EXP);
+        else epi8_pipelined<false, false>(tbase, p.bn, p.mt, c_lo, per, vaddr, taddr, raddr, saddr, hcnt, sw, lo32u, lo8, EPI_EXP);
+      } else
       for (int sub = 0; sub < p.mt; sub++)
       for (int h = c_lo; h < c_hi; h++) {
         const int msub = m + sub * BM;
@@ -1053,6 +1175,7 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     // (small biases, lo in int32) or by the per-channel threshold (needs the fast_clamp bound)
     kp.fast8 = kp.tma_out == 2 && cp.K <= kMaxVecK && (!cp.epi_lo || kp.fast_clamp) ? 1 : 0;
     kp.thr_always = cp.epi_lo && !lo_ok ? 1 : 0;
+    kp.epi_pipe = kp.fast8;
     kp.epi_split = kp.epi_warps == 8 && kp.tma_out != 1 && !std::getenv("SB_IG_NOSPLIT") ? 1 : 0;
     kp.bias_bound = T < INT_MAX ? INT_MAX - T : 0;
   }
@@ -1516,6 +1639,7 @@ cudaError_t launch_conv_igemm(const ConvPlan& cp, const ConvArgs& args, cudaStre
   kp.pdl = args.pdl_mode != kPdlOff ? 1 : 0;
   kp.pdl_wait = args.pdl_mode == kPdlWait ? 1 : 0;
   kp.b_early = args.b_immutable ? 1 : 0;
+  if (kp.fast8 && std::getenv("SB_IG_NOPIPE")) kp.epi_pipe = 0;  // A/B switch, read per launch
   const int tiles = kp.tiles_m * kp.tiles_n;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(tiles < num_sms ? tiles : num_sms));

@@ -10,14 +10,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def main():
-    import torch
-    import paper_1903_06498_b200 as sb
+def program_text(which, batch):
     from paper_1903_06498_b200 import workloads as W
-    which = sys.argv[1] if len(sys.argv) > 1 else "c5"
-    batch = int(sys.argv[2]) if len(sys.argv) > 2 else 128
     if which == "c5":
-        text, info = W.resnet50(batch)
+        text, _ = W.resnet50(batch)
     elif which == "stem":
         text = W.conv_fused(batch, 224, 224, 3, 64, 7, 7, 2, 3)
     elif which == "l3x3":
@@ -44,6 +40,16 @@ def main():
         text = W.conv2d(32, 56, 56, 64, 64)
     else:
         raise SystemExit("unknown program " + which)
+    return text
+
+
+def main():
+    import torch
+    import paper_1903_06498_b200 as sb
+    from paper_1903_06498_b200 import workloads as W
+    which = sys.argv[1] if len(sys.argv) > 1 else "c5"
+    batch = int(sys.argv[2]) if len(sys.argv) > 2 else 128
+    text = program_text(which, batch)
     prog = sb.parse_program(text)
     ctx = sb.Context(0)
     bufs, keep = {}, []
