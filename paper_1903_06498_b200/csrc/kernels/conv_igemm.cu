@@ -108,6 +108,14 @@ struct IgKParams {
   long long bias_bound;
   int thr_always;  // fast8 with a clamp bound outside int32: always the threshold form
   int epi_pipe;    // fast8 epilogue with the next chunk's TMEM load in flight
+  // band mode (ConvPlan::fold_band): tile t = output rows (img, band*(t % band_rpi) ..) x 128
+  // columns; A = one bulk copy of band_bytes from the compact folded rows (band_rowb bytes
+  // each, band_img per image) into a ring stage of band_stage bytes, read with overlapping-row
+  // descriptors (a_hi); the band's rows stacked along N (vector index k % vec_mod)
+  int band, band_rpi, band_bytes, band_stage, vec_mod;
+  long long band_rowb, band_img;
+  const std::int8_t* band_src;
+  std::uint32_t a_hi;
   const void* vec;
   long long vec_k;
   long long lo;
@@ -260,9 +268,11 @@ __device__ __forceinline__ uint4 lds128(std::uint32_t a) {
 template <bool THR, bool RES>
 __device__ __forceinline__ void epi8_half(const std::uint32_t (&v)[16], int sub, int h, int hf, std::uint32_t vaddr,
                                           std::uint32_t taddr, std::uint32_t raddr, std::uint32_t saddr, int hcnt,
-                                          int sw, std::uint32_t lo32u, std::int32_t lo8) {
-  const std::uint32_t box = (sub * hcnt + (h >> 2)) * 16384;
-  const std::uint32_t unit = (((2 * (h & 3) + hf) ^ sw) << 4);
+                                          int hsh, int sw, std::uint32_t lo32u, std::int32_t lo8) {
+  // 16 KB staging box and swizzled 16-byte unit of this half: 128-byte rows hold 1 << hsh
+  // 32-column chunks (hsh = 2; band mode with 64 channels: hsh = 1, one band row per box)
+  const std::uint32_t box = (sub * hcnt + (h >> hsh)) * 16384;
+  const std::uint32_t unit = (((2 * (h & ((1 << hsh) - 1)) + hf) ^ sw) << 4);
   uint4 r4 = make_uint4(0, 0, 0, 0);
   if (RES) r4 = lds128(raddr + box + unit);
   const std::uint32_t rq[4] = {r4.x, r4.y, r4.z, r4.w};
@@ -304,7 +314,7 @@ __device__ __forceinline__ void epi8_half(const std::uint32_t (&v)[16], int sub,
 template <bool THR, bool RES>
 __device__ __forceinline__ void epi8_pipelined(std::uint32_t tbase, int bn, int mt, int c_lo, int per,
                                                std::uint32_t vaddr, std::uint32_t taddr, std::uint32_t raddr,
-                                               std::uint32_t saddr, int hcnt, int sw, std::uint32_t lo32u,
+                                               std::uint32_t saddr, int hcnt, int hsh, int sw, std::uint32_t lo32u,
                                                std::int32_t lo8, int exp) {
   const int total = mt * per, c_end = c_lo + per;
   if (total <= 0) return;
@@ -321,13 +331,26 @@ __device__ __forceinline__ void epi8_pipelined(std::uint32_t tbase, int bn, int 
     const std::uint32_t col = tbase + sub * bn + h * 32;
     tmem_wait_ld16(va);
     tmem_ld16_async(col + 16, vb);
-    epi8_half<THR, RES>(va, sub, h, 0, vaddr, taddr, raddr, saddr, hcnt, sw, lo32u, lo8);
+    epi8_half<THR, RES>(va, sub, h, 0, vaddr, taddr, raddr, saddr, hcnt, hsh, sw, lo32u, lo8);
     tmem_wait_ld16(vb);
     if (c + 1 < total) tmem_ld16_async(tbase + nsub * bn + nh * 32, va);
-    epi8_half<THR, RES>(vb, sub, h, 1, vaddr, taddr, raddr, saddr, hcnt, sw, lo32u, lo8);
+    epi8_half<THR, RES>(vb, sub, h, 1, vaddr, taddr, raddr, saddr, hcnt, hsh, sw, lo32u, lo8);
     sub = nsub;
     h = nh;
   }
+}
+
+// band mode: KB k-blocks (folded rows) x KS k-steps; A rows overlap (a_hi: no swizzle), B is
+// the resident banded filter (b_hi: its TMA swizzle)
+template <int KB, int KS>
+__device__ __forceinline__ void issue_band(std::uint32_t d, std::uint32_t a0, std::uint32_t a_step, std::uint32_t a_hi,
+                                           std::uint32_t b0, std::uint32_t b_step, std::uint32_t b_hi,
+                                           std::uint32_t idesc) {
+#pragma unroll
+  for (int j = 0; j < KB; j++)
+#pragma unroll
+    for (int ks = 0; ks < KS; ks++)
+      umma_i8(d, a0 + j * a_step + ks * 2, a_hi, b0 + j * b_step + ks * 2, b_hi, idesc, (j == 0 && ks == 0) ? 0u : 1u);
 }
 
 __global__ void __launch_bounds__(kThreadsGather, 1)
@@ -340,7 +363,8 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
   const int TM = BM * p.mt;  // tile rows (output pixels)
   const std::uint32_t stage_a = TM * p.bk, stage_b = p.bn_box * p.bk;
   std::uint8_t* ring = base;                    // stages x (A | B), or stages x A with the filter resident
-  const std::uint32_t sstride = p.kpb * (stage_a + (p.b_res ? 0u : stage_b));
+  const std::uint32_t sstride = p.band ? static_cast<std::uint32_t>(p.band_stage)
+                                        : p.kpb * (stage_a + (p.b_res ? 0u : stage_b));
   std::uint8_t* bres = base + p.bres_off;       // resident filter: kblocks x stage_b
   std::uint8_t* stg = base + p.stg_off;         // output staging: i32 4 x 16 KB quarters | i8 2 x 16 KB
   std::uint8_t* rstg = base + p.res_off;        // residual tiles (i8, 2 x 16 KB)
@@ -457,6 +481,30 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
             }
           }
         }
+      } else if (p.band) {
+        // one bulk copy per tile: the band's folded rows (plus the junk rows' tail)
+        if (pidx == 0) {
+          int stage = 0;
+          std::uint32_t phase = 0;
+          for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            if (issuer) {
+              const int img = t / p.band_rpi, u = (t - img * p.band_rpi) * p.band;
+              const std::int8_t* src = p.band_src + img * p.band_img + u * p.band_rowb;
+              mbar_expect_tx(&full[stage], static_cast<std::uint32_t>(p.band_bytes));
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                      smem_u32(ring + stage * sstride)),
+                  "l"(reinterpret_cast<std::uint64_t>(src)), "r"(p.band_bytes), "r"(smem_u32(&full[stage]))
+                  : "memory");
+            }
+            __syncwarp();
+            if (++stage == stages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
       } else {
       int stage = 0, kit = 0;
       std::uint32_t phase = 0;
@@ -546,7 +594,25 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
 #ifdef SB_TILE_TRACE
         if (!(p.exp & 2))
 #endif
-        if (issuer) {
+#ifdef SB_TILE_TRACE
+        if (issuer && p.band && blockIdx.x == 0 && iter == 0 && p.trace && (p.exp & 16)) {
+          // debug: the first band stage as the MMA sees it (2 KB) and its descriptor fields
+          const long long* src = reinterpret_cast<const long long*>(ring + stage * sstride);
+          for (int i = 0; i < 256; i++) p.trace[1280 + i] = src[i];
+          p.trace[1536] = sa;
+          p.trace[1537] = static_cast<long long>(stage);
+        }
+#endif
+        if (issuer && p.band) {
+          const std::uint32_t rs = static_cast<std::uint32_t>(p.band_rowb >> 4);
+          // A descriptor low word: start | 16-byte stride between core matrices along K (a_hi)
+          const std::uint32_t ab = (sa >> 4) | (1u << 16);
+          if (p.kblocks == 5 && ksteps == 2) issue_band<5, 2>(d, ab, rs, p.a_hi, b0, bs, hi, idesc);
+          else
+            for (int j = 0; j < p.kblocks; j++)
+              for (int ks = 0; ks < ksteps; ks++)
+                umma_i8(d, ab + j * rs + ks * 2, p.a_hi, b0 + j * bs + ks * 2, hi, idesc, (j | ks) ? 1u : 0u);
+        } else if (issuer) {
           // sub-tile sub: rows 128 sub .. of every k-block's A, accumulator columns + sub * bn
           for (int sub = 0; sub < p.mt; sub++) {
             const std::uint32_t ds = d + sub * p.bn, as0 = a0 + sub * ((BM * p.bk) >> 4);
@@ -730,7 +796,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       // <=> acc + res >= t[k] exactly, because |acc + res| < 2^31 - 1
       if (p.pdl_wait) asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory");
       for (int k = threadIdx.x - 64; k < p.N; k += ethreads) {
-        const long long vi = static_cast<long long>(k) * p.vec_k;
+        const long long vi = static_cast<long long>(p.vec_mod ? k % p.vec_mod : k) * p.vec_k;
         const std::int32_t b = !p.epi_vec ? 0
                                : p.vec_kind == kI8 ? static_cast<const std::int8_t*>(p.vec)[vi]
                                : p.vec_kind == kI16 ? static_cast<const std::int16_t*>(p.vec)[vi]
@@ -758,7 +824,10 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
     const bool relu0 = p.epi_lo && p.lo == 0;
     // residual tile [128 pixels x bn channels] i8 of tile t into buffer b, as 128-channel halves
     const int hcnt = (p.bn + 127) / 128;  // 16 KB staging boxes per 128-row sub-tile
-    const int res_buf = TM * p.bn, stg_buf = p.mt * hcnt * 16384;
+    // band mode with 64 channels: one box per band row (the TMA store pads 64-byte inner rows
+    // to the 128-byte swizzle span), two 32-column chunks per 128-byte row
+    const int shsh = p.band && p.vec_mod == 64 ? 1 : 2, sbox = shsh == 1 ? p.band : hcnt;
+    const int res_buf = TM * p.bn, stg_buf = p.mt * sbox * 16384;
     auto load_res = [&](int t, int b) {  // (epilogue-read residual: mt == 1 only)
       const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * p.bn;
       const int halves = min(p.bn, p.N - n0 + 127) / 128;
@@ -807,10 +876,10 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
         const std::uint32_t vaddr = smem_u32(vec_s + n0), taddr = smem_u32(thr_s + n0);
         const std::uint32_t raddr = smem_u32(rcur) + row * 128, saddr = smem_u32(scur) + row * 128;
         const int per = c_hi - c_lo;
-        if (thr8 && eres) epi8_pipelined<true, true>(tbase, p.bn, p.mt, c_lo, per, vaddr, taddr, raddr, saddr, hcnt, sw, lo32u, lo8, EPI_EXP);
-        else if (thr8) epi8_pipelined<true, false>(tbase, p.bn, p.mt, c_lo, per, vaddr, taddr, raddr, saddr, hcnt, sw, lo32u, lo8, EPI_EXP);
-        else if (eres) epi8_pipelined<false, true>(tbase, p.bn, p.mt, c_lo, per, vaddr, taddr, raddr, saddr, hcnt, sw, lo32u, lo8, EPI_EXP);
-        else epi8_pipelined<false, false>(tbase, p.bn, p.mt, c_lo, per, vaddr, taddr, raddr, saddr, hcnt, sw, lo32u, lo8, EPI_EXP);
+        if (thr8 && eres) epi8_pipelined<true, true>(tbase, p.bn, p.mt, c_lo, per, vaddr, taddr, raddr, saddr, sbox, shsh, sw, lo32u, lo8, EPI_EXP);
+        else if (thr8) epi8_pipelined<true, false>(tbase, p.bn, p.mt, c_lo, per, vaddr, taddr, raddr, saddr, sbox, shsh, sw, lo32u, lo8, EPI_EXP);
+        else if (eres) epi8_pipelined<false, true>(tbase, p.bn, p.mt, c_lo, per, vaddr, taddr, raddr, saddr, sbox, shsh, sw, lo32u, lo8, EPI_EXP);
+        else epi8_pipelined<false, false>(tbase, p.bn, p.mt, c_lo, per, vaddr, taddr, raddr, saddr, sbox, shsh, sw, lo32u, lo8, EPI_EXP);
       } else
       for (int sub = 0; sub < p.mt; sub++)
       for (int h = c_lo; h < c_hi; h++) {
@@ -974,10 +1043,10 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
           for (int q = 0; q < 8; q++)
             w[q] = (v[4 * q] & 0xFF) | ((v[4 * q + 1] & 0xFF) << 8) | ((v[4 * q + 2] & 0xFF) << 16) |
                    (v[4 * q + 3] << 24);
-          const std::uint32_t rbase = smem_u32(scur + (sub * hcnt + (h >> 2)) * 16384 + row * 128);
+          const std::uint32_t rbase = smem_u32(scur + (sub * sbox + (h >> shsh)) * 16384 + row * 128);
 #pragma unroll
           for (int u = 0; u < 2; u++)
-            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rbase + (((2 * (h & 3) + u) ^ sw) << 4)),
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rbase + (((2 * (h & ((1 << shsh) - 1)) + u) ^ sw) << 4)),
                          "r"(w[4 * u]), "r"(w[4 * u + 1]), "r"(w[4 * u + 2]), "r"(w[4 * u + 3]));
         } else if (msub < p.M) {
           const long long rowbase = static_cast<long long>(msub) * p.ldc;
@@ -998,6 +1067,16 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
           }
         }
       }
+#ifdef SB_TILE_TRACE
+      if (p.band && (p.exp & 32)) {
+        // debug: staging row = (row, 100 + row) per band row p, same swizzle as the epilogue
+        for (int c = 0; c < 8; c++) {
+          const std::uint32_t val = (c < 4 ? row : 100 + row) & 0xFF;
+          const std::uint32_t v4 = val * 0x01010101u;
+          asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(smem_u32(scur) + row * 128 + ((c ^ sw) << 4)), "r"(v4));
+        }
+      }
+#endif
       if (leader) TILE_STAMP(9, iter);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
@@ -1016,6 +1095,14 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
                                  reinterpret_cast<std::uint64_t>(&cmap)),
                              "r"(smem_u32(stg + h * 16384)), "r"(n0 + h * 32), "r"(m0)
                              : "memory");
+          } else if (p.band) {
+            // (k, row of the band, pixel, band index): pixels past the row width are clipped
+            // one 16 KB box per band row
+            for (int hh = 0; hh < p.band; hh++)
+              asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                               reinterpret_cast<std::uint64_t>(&cmap)),
+                           "r"(smem_u32(scur + hh * 16384)), "r"(0), "r"(hh), "r"(0), "r"(t)
+                           : "memory");
           } else {
             for (int sub = 0; sub < p.mt; sub++)
               for (int hh = 0; hh < p.bn / 128 && n0 + hh * 128 < p.N; hh++)
@@ -1120,6 +1207,29 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
   kp.cblocks = static_cast<int>(gp.C / g.bk);
   kp.kblocks = static_cast<int>(gp.R * gp.S) * kp.cblocks;
   kp.epi_warps = cp.packed ? 4 : 8;
+  if (cp.fold_band) {
+    // band view (packed_view of a band-folded conv): cp.H x cp.W output rows/cols, cp.K =
+    // band x the output channels, cp.a_x / cp.a_n = folded row / image bytes
+    const int band = static_cast<int>(cp.fold_band);
+    kp.band = band;
+    kp.band_rowb = cp.a_x;
+    kp.band_img = cp.a_n;
+    kp.band_rpi = static_cast<int>(cp.H / band);
+    // the band's kblocks folded rows; the last row up to pixel 127 + (C / a_y - 1) (junk rows
+    // of the tile read past the row: finite, discarded by the clipped store)
+    kp.band_bytes = static_cast<int>((kp.kblocks - 1) * cp.a_x + (BM + cp.C / cp.a_y - 1) * cp.a_y);
+    kp.band_bytes = (kp.band_bytes + 15) / 16 * 16;
+    // whole KB stages keep every later region (filter SW64, staging SW128) 1024-byte aligned
+    kp.band_stage = (kp.band_bytes + 1023) / 1024 * 1024;
+    kp.band_src = static_cast<const std::int8_t*>(args.a);
+    kp.vec_mod = static_cast<int>(cp.K / band);
+    kp.M = static_cast<int>(cp.N * kp.band_rpi * BM);
+    // K-major, no swizzle: core matrices of 8 rows x 16 bytes (rows 16 bytes apart), LBO (low
+    // word, 16 bytes) between core matrices along K, SBO (high word, 128 bytes) between 8-row
+    // groups along M -- measured on B200 by tools/microbench/desc_probe.cu -- so row m, byte q
+    // of the operand is at start + 16 m + q: overlapping 64-byte windows
+    kp.a_hi = (128u >> 4) | (1u << 14);
+  }
   if (cp.packed) {
     kp.gather = 1;
     kp.rsc = static_cast<int>(cp.R * cp.S * cp.C);
@@ -1186,7 +1296,8 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     kp.mt = mt;
     kp.tiles_n = (kp.N + bn - 1) / bn;
     kp.tiles_m = (kp.M + BM * mt - 1) / (BM * mt);
-    const int stg = kp.tma_out == 1 ? kStgBytes : kp.tma_out == 2 ? (kp.stg4 ? 4 : 2) * mt * (bn / 128) * 16384 : 0;
+    const int sboxes = kp.band && kp.vec_mod == 64 ? kp.band : bn / 128;  // 16 KB staging boxes per sub-tile
+    const int stg = kp.tma_out == 1 ? kStgBytes : kp.tma_out == 2 ? (kp.stg4 ? 4 : 2) * mt * sboxes * 16384 : 0;
     const int res = kp.epi_res ? 2 * BM * mt * bn : 0;
     const int vec = kp.fast_clamp ? 2 * kVecBytes : kp.epi_vec ? kVecBytes : 0;
     const int tab = kp.gather ? (kp.kblocks * kp.bk * 6 + 15) / 16 * 16 : 0;
@@ -1200,13 +1311,14 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     const int avail = std::min(kRingBytes, kSmemMax - 1024 - 512 - stg - res - vec - tab - bres - ident);
     // k-blocks per stage: up to 4 while three stages still fit (gather mode: 1)
     kp.kpb = 1;
-    if (!kp.gather && !std::getenv("SB_IG_KPB1"))
+    if (kp.band) kp.kpb = kp.kblocks;  // one bulk copy per tile feeds every k-block
+    else if (!kp.gather && !std::getenv("SB_IG_KPB1"))
       for (int c : {4, 3, 2})
         if (kp.kblocks % c == 0 && (std::getenv("SB_IG_KPB3") ? 3 : 2) * c * kstage <= avail) {
           kp.kpb = c;
           break;
         }
-    const int stage = kp.kpb * kstage;
+    const int stage = kp.band ? kp.band_stage : kp.kpb * kstage;
     if (avail < 2 * stage) return false;
     int ring = avail / stage * stage;
     kp.stages = std::min(16, ring / stage);
@@ -1228,7 +1340,7 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
   const bool wide = kp.epi_split && kp.N >= 256 && cp.K <= kMaxVecK && !std::getenv("SB_IG_BN128");
   // two 128-row sub-tiles per tile (one stage handshake and one filter tile feed twice the
   // MMAs) for narrow outputs with enough tiles left for every SM
-  const bool tall = kp.epi_split && kp.tma_out != 1 && kp.N <= 128 && !(kp.epi_res && !kp.res_mma) &&
+  const bool tall = !kp.band && kp.epi_split && kp.tma_out != 1 && kp.N <= 128 && !(kp.epi_res && !kp.res_mma) &&
                     (kp.M + 2 * BM - 1) / (2 * BM) >= 2 * 148 && !std::getenv("SB_IG_MT1");
   // split i8 epilogue: two staging buffers per group when the ring keeps >= 3 stages
   const bool stg4_ok = kp.epi_split && kp.tma_out == 2 && !std::getenv("SB_IG_STG2");
@@ -1248,7 +1360,9 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
   const CUtensorMapSwizzle sw = g.bk == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
 
   std::memset(&out->amap, 0, sizeof(out->amap));
-  if (!kp.gather) {
+  if (kp.band && (kp.tma_out != 2 || !kp.b_res || kp.bn != kp.N || kp.mt != 1)) return cudaErrorNotSupported;
+  if (kp.band && reinterpret_cast<std::uintptr_t>(args.a) % 16) return cudaErrorMisalignedAddress;
+  if (!kp.gather && !kp.band) {
   // A: im2col over (c, v, u, n) from the window corner (u_lo, v_lo)
   const std::int8_t* abase = static_cast<const std::int8_t*>(args.a) + cp.a0 + cp.a_x * cp.u_lo + cp.a_y * cp.v_lo;
   if (reinterpret_cast<std::uintptr_t>(abase) % 16) return cudaErrorMisalignedAddress;
@@ -1284,6 +1398,18 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     cuuint64_t cstr[1] = {static_cast<cuuint64_t>(kp.ldc * 4)};
     cuuint32_t cbox[2] = {32, BM};
     if (enc_tiled(&out->cmap, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, kp.c, cdim, cstr, cbox, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  } else if (kp.tma_out == 2 && kp.band) {
+    // (k, band row p, pixel y, band index nu): element (n, band * u + p, y, k) of the NHWC output
+    const long long ko = cp.K / kp.band;
+    cuuint64_t cdim[4] = {static_cast<cuuint64_t>(ko), static_cast<cuuint64_t>(kp.band), static_cast<cuuint64_t>(cp.W),
+                          static_cast<cuuint64_t>(cp.N * kp.band_rpi)};
+    cuuint64_t cstr[3] = {static_cast<cuuint64_t>(cp.c_x), static_cast<cuuint64_t>(cp.c_y),
+                          static_cast<cuuint64_t>(kp.band * cp.c_x)};
+    cuuint32_t cbox[4] = {static_cast<cuuint32_t>(ko), 1, BM, 1};
+    if (enc_tiled(&out->cmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, kp.c, cdim, cstr, cbox, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
@@ -1495,16 +1621,18 @@ __global__ void __launch_bounds__(256) conv_fold_any(const std::int8_t* __restri
 }
 
 // Folded filter: G[a, k, q], q = b*fold_c + kf -> F[fx*a + di, fy*b + dj, k, c] (zero when the
-// tap is past R/S or kf is padding)
+// tap is past R/S or kf is padding).  Banded (band > 1, ConvPlan::fold_band): rows r of
+// [fr + band - 1][band * K][cv], block (r, p) = G[r - p] (zero outside 0 <= r - p < fr).
 __global__ void conv_fold_filter_kernel(const std::int8_t* __restrict__ b, std::int8_t* __restrict__ pb, int K, int C,
-                                        int R, int S, int fx, int fy, int fc, int cv, int fr, long long b_i,
+                                        int R, int S, int fx, int fy, int fc, int cv, int fr, int band, long long b_i,
                                         long long b_j, long long b_k, long long b_c, long long b0) {
-  const int total = fr * K * cv, fyc = fy * C;
+  const int rows = band * K, total = (fr + band - 1) * rows * cv, fyc = fy * C;
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
-    const int q = g % cv, ak = g / cv, k = ak % K, ta = ak / K;
+    const int q = g % cv, rk = g / cv, row = rk % rows, r = rk / rows;
+    const int pband = row / K, k = row - pband * K, ta = r - pband;
     const int tb = q / fc, kf = q - tb * fc;
     std::int8_t val = 0;
-    if (kf < fx * fyc) {
+    if (ta >= 0 && ta < fr && kf < fx * fyc) {
       const int di = kf / fyc, r = kf - di * fyc, dj = r / C, c = r - dj * C;
       const int i = fx * ta + di, j = fy * tb + dj;
       if (i < R && j < S) val = b[b0 + b_i * i + b_j * j + b_k * k + b_c * c];
@@ -1559,12 +1687,13 @@ cudaError_t launch_conv_fold(const ConvPlan& cp, const void* a, void* f, cudaStr
 
 cudaError_t launch_conv_pack_filter(const ConvPlan& cp, const void* b, void* pb, cudaStream_t s) {
   if (cp.fold_x) {
-    const int total = static_cast<int>(cp.fold_r * cp.K * cp.fold_cv);
+    const int band = cp.fold_band ? static_cast<int>(cp.fold_band) : 1;
+    const int total = static_cast<int>((cp.fold_r + band - 1) * band * cp.K * cp.fold_cv);
     conv_fold_filter_kernel<<<std::min(1024, (total + 255) / 256), 256, 0, s>>>(
         static_cast<const std::int8_t*>(b), static_cast<std::int8_t*>(pb), static_cast<int>(cp.K),
         static_cast<int>(cp.C), static_cast<int>(cp.R), static_cast<int>(cp.S), static_cast<int>(cp.fold_x),
         static_cast<int>(cp.fold_y), static_cast<int>(cp.fold_c), static_cast<int>(cp.fold_cv),
-        static_cast<int>(cp.fold_r), cp.b_i, cp.b_j, cp.b_k, cp.b_c, cp.b0);
+        static_cast<int>(cp.fold_r), band, cp.b_i, cp.b_j, cp.b_k, cp.b_c, cp.b0);
     return cudaGetLastError();
   }
   const int kp = static_cast<int>(cp.pack_k), rsc = static_cast<int>(cp.R * cp.S * cp.C);
@@ -1596,6 +1725,19 @@ const char* conv_igemm_unsupported(const ConvPlan& cp) {
         cp.a_x * (cp.R - 1) + cp.a_y * (cp.S - 1) + cp.C >= (1ll << 30))
       return "gathered taps out of range";
     return conv_igemm_unsupported(packed_view(cp));
+  }
+  if (cp.fold_band) {
+    // band view (see prepare()): one 128-pixel tile per output row, stacked rows along N
+    if (cp.W > BM || cp.H % cp.fold_band || cp.fold_band != 2 || (cp.K != 128 && cp.K != 256) || cp.C != 64 ||
+        cp.a_y != 16 || cp.a_x % 16 ||
+        cp.R * cp.S * 64 * cp.K > 96 * 1024)
+      return "band geometry";
+    if (cp.c_dtype != DType::I8 || !cp.fresh_output || cp.epi_res || cp.c_y != cp.K / cp.fold_band ||
+        cp.c_x != cp.W * cp.c_y || cp.c_x % 16 || cp.c0 % 16)
+      return "band output not a fresh dense NHWC i8 activation";
+    if (cp.N * (cp.H / cp.fold_band) >= (1ll << 31) || cp.a_n >= (1ll << 40)) return "extent too large";
+    if (cp.epi_vec && cp.K > kMaxVecK) return "epilogue vector longer than 2048";
+    return nullptr;
   }
   Geometry g;
   if (!geometry(cp, &g)) return "padding halo outside the im2col corner range";
@@ -1653,16 +1795,25 @@ cudaError_t launch_conv_igemm(const ConvPlan& cp, const ConvArgs& args, cudaStre
   cfg.numAttrs = kp.pdl ? 1 : 0;
 #ifdef SB_TILE_TRACE
   static long long* tr = nullptr;
-  if (!tr) cudaMalloc(&tr, (640 + 32 * 4 * 3 + 256) * 8);
-  cudaMemsetAsync(tr, 0, (640 + 32 * 4 * 3 + 256) * 8, s);
+  if (!tr) cudaMalloc(&tr, (640 + 32 * 4 * 3 + 256 + 512) * 8);
+  cudaMemsetAsync(tr, 0, (640 + 32 * 4 * 3 + 256 + 512) * 8, s);
   kp.trace = tr;
   kp.exp = std::getenv("SB_IG_EXP") ? std::atoi(std::getenv("SB_IG_EXP")) : 0;
   cudaError_t e = cudaLaunchKernelEx(&cfg, conv_igemm_i8_kernel, prep.amap, prep.bmap, prep.cmap, prep.rmap, kp);
-  long long h[640 + 32 * 4 * 3 + 256];
+  long long h[640 + 32 * 4 * 3 + 256 + 512];
   cudaStreamSynchronize(s);
   cudaMemcpy(h, tr, sizeof(h), cudaMemcpyDeviceToHost);
   std::fprintf(stderr, "igemm M=%d N=%d kblocks=%d kpb=%d stages=%d b_res=%d split=%d tiles=%d\n", kp.M, kp.N, kp.kblocks,
                kp.kpb, kp.stages, kp.b_res, kp.epi_split, tiles);
+  if (kp.band && (kp.exp & 16)) {
+    const unsigned char* b = reinterpret_cast<const unsigned char*>(h + 1280);
+    std::fprintf(stderr, "band stage smem 0x%llx stage %lld rowb %lld bytes %d\n", h[1536], h[1537], kp.band_rowb, kp.band_bytes);
+    for (int r = 0; r < 128; r++) {
+      std::fprintf(stderr, "  %5d:", r * 16);
+      for (int q = 0; q < 16; q++) std::fprintf(stderr, " %3d", static_cast<signed char>(b[r * 16 + q]));
+      std::fprintf(stderr, "\n");
+    }
+  }
   for (int i = 0; i < 128; i++)
     if (h[128 + i])
       std::fprintf(stderr, "tile %3d prod %8lld mma0 %8lld mma1 %8lld | etop %8lld epi0 %8lld math %8lld epi1 %8lld\n", i,

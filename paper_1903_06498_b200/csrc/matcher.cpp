@@ -772,6 +772,31 @@ ConvPlan packed_view(const ConvPlan& c) {
   v.packed = false;
   v.a_buf = c.pack_a;
   v.b_buf = c.pack_b;
+  if (c.fold_x && c.fold_band) {
+    // band view: the GEMM geometry of the banded filter [fold_r + band - 1][band * K][fold_cv]
+    // over compact folded rows (prepare() in conv_igemm.cu reads the band fields)
+    v.C = c.fold_cv;
+    v.R = c.fold_r + c.fold_band - 1;
+    v.S = 1;
+    v.K = c.fold_band * c.K;
+    v.sx = v.sy = 1;
+    v.a_y = c.fold_c;
+    v.a_x = c.fold_v * c.fold_c;
+    v.a_n = c.fold_u * v.a_x;
+    v.a0 = 0;
+    v.u_lo = 0;
+    v.u_hi = c.fold_u - 1;
+    v.v_lo = 0;
+    v.v_hi = c.fold_v - 1;
+    v.b_i = v.K * c.fold_cv;
+    v.b_j = 0;
+    v.b_k = c.fold_cv;
+    v.b_c = 1;
+    v.b0 = 0;
+    v.b_immutable = false;
+    v.fold_x = v.fold_y = 0;
+    return v;
+  }
   if (c.fold_x) {
     // out[x, y] = sum_{a, q} F[x + a, y + q / fold_c, q % fold_c] * G[a, k, q]: "pixel" (U, y)
     // of the view is the fold_cv bytes starting at folded pixel (U, y), so consecutive view
@@ -818,6 +843,28 @@ ConvPlan packed_view(const ConvPlan& c) {
 
 namespace {
 
+// Band tiles for a phase-folded conv (ConvPlan::fold_band), decided once the output and the
+// fused epilogue are known: one output row fits one 128-row tile, two rows stack to N <= 256,
+// and the output is a fresh dense NHWC i8 activation (4-D clipped TMA store).  The fold buffer
+// becomes the compact folded pixels (+ a tail for the junk rows' reads), the packed filter the
+// banded [fold_r + 1][2K][fold_cv].
+void choose_band(Plan* plan, ConvPlan* cp) {
+  const ConvPlan& c = *cp;
+  if (!c.packed || !c.fold_x || std::getenv("SB_NO_BAND")) return;
+  const bool ok = c.fold_c == 16 && c.fold_cv == 64 && c.W <= 128 && c.H % 2 == 0 && (c.K == 64 || c.K == 128) &&
+                  c.c_dtype == DType::I8 && c.fresh_output && !c.epi_res && c.c_y == c.K && c.c_x == c.W * c.K &&
+                  (c.N == 1 || c.c_n == c.H * c.c_x) && c.c0 % 16 == 0;
+  if (!ok) return;
+  ConvPlan b = c;
+  b.fold_band = 2;
+  b.fold_rows = false;
+  b.pack_k = (b.fold_r + b.fold_band - 1) * b.fold_cv * b.fold_band;
+  if (conv_igemm_unsupported(b)) return;
+  *cp = b;
+  plan->bufs[b.pack_a].elements = b.N * b.fold_u * b.fold_v * b.fold_c + 128 * 16 + 64;
+  plan->bufs[b.pack_b].elements = b.K * b.pack_k;
+}
+
 // Small-channel convs (C not a multiple of 64, e.g. the 7x7x3 stem): pack, then 1x1 igemm.
 bool try_packed_conv(Plan* plan, ConvPlan* cp) {
   const std::int64_t rsc = cp->R * cp->S * cp->C;
@@ -840,6 +887,7 @@ bool try_packed_conv(Plan* plan, ConvPlan* cp) {
     c.pack_a = static_cast<int>(plan->bufs.size());
     c.pack_b = c.pack_a + 1;
     // materialised rows when a folded pixel is one 16-byte unit and a row a whole number of them
+    // (choose_band() may switch to band tiles once the output and epilogue are known)
     c.fold_rows = c.fold_c == 16 && c.fold_cv % 16 == 0 && !std::getenv("SB_FOLD_OVERLAP");
     const std::int64_t folded = c.fold_rows ? c.N * c.fold_u * c.W * c.fold_cv : c.N * c.fold_u * c.fold_v * c.fold_c;
     if (c.pack_k <= 1024 && folded < (1ll << 34) && !conv_igemm_unsupported(c)) {
@@ -1030,11 +1078,16 @@ void match_kernels(Plan* plan, const Program& p, const PlanOptions& opt) {
         st.launch.conv = cp;
         if (cp.fresh_output) st.launch.fused_fill_root = plan->bufs[cp.c_buf].root_index;
         if (!fuse_conv_epilogue(plan, s, p, opt)) fresh_scratch_output(plan, s);
+        choose_band(plan, &st.launch.conv);
+        cp = st.launch.conv;
         if (cp.fold_x)
           plan->notes.push_back("launch " + st.launch.path + ": small-channel conv phase-folded (" +
                                 std::to_string(cp.fold_x) + "x" + std::to_string(cp.fold_y) + ", " +
                                 std::to_string(cp.fold_c) + " bytes per folded pixel), packed to " +
-                                std::to_string(cp.fold_r) + " tap rows x " + std::to_string(cp.fold_cv));
+                                std::to_string(cp.fold_r) + " tap rows x " + std::to_string(cp.fold_cv) +
+                                (cp.fold_band ? ", band tiles of " + std::to_string(cp.fold_band) +
+                                                    " output rows stacked along N (overlapping-row descriptors)"
+                                              : std::string()));
         else
           plan->notes.push_back("launch " + st.launch.path + ": small-channel conv packed to " +
                                 std::to_string(cp.pack_k) + " taps x channels per pixel (gathered)");

@@ -165,6 +165,12 @@ struct ConvPlan {
   // fold_c - 1] (fold_cv bytes, 64-byte aligned TMA rows; ~2x the im2col rate of the
   // overlapping-stride view) instead of the folded pixels themselves
   bool fold_rows = false;
+  // fold_band (> 0, compact folded pixels): one tile = fold_band consecutive output rows x 128
+  // pixel columns; A = the (fold_r + fold_band - 1) folded rows the band needs, one bulk copy,
+  // read by UMMA descriptors whose rows overlap (row m at 16 m bytes, no swizzle); the band's
+  // output rows stacked along N against a banded filter [fold_r + band - 1][band * K][fold_cv]
+  // (block (r, p) = folded tap row r - p): N = band * K columns per MMA instead of K
+  std::int64_t fold_band = 0;
 };
 
 // Statement-DAG concurrency (schedule.cpp): independent steps on up to N streams.

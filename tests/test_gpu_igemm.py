@@ -193,6 +193,48 @@ def test_gather_stem_fused_vs_port(small_c_mode):
     np.testing.assert_array_equal(out["O"], ref["O"])
 
 
+BAND = [
+    # N, H, W, C, K, R, S, stride, pad, relu: strided small-channel convs into fresh i8 activations
+    (2, 32, 32, 3, 64, 7, 7, 2, 3, True),     # ResNet stem shape
+    (3, 28, 36, 3, 64, 7, 7, 2, 3, True),     # non-square, several images
+    (1, 224, 224, 3, 64, 7, 7, 2, 3, True),   # the full stem: 112-pixel rows in 128-row tiles
+    (2, 256, 250, 3, 64, 7, 7, 2, 3, False),  # 125-pixel rows (junk-row tail reads), no clamp
+    (2, 20, 20, 3, 128, 7, 7, 2, 3, True),    # K = 128: N = 256 per instruction, one store per row
+    (2, 16, 24, 3, 64, 5, 5, 2, 2, True),     # 3x3 folded taps (4 k-blocks)
+]
+
+
+@pytest.mark.parametrize("case", BAND, ids=lambda c: "x".join(map(str, c)))
+def test_band_fold_conv_exact(case):
+    """Band tiles (ConvPlan::fold_band): compact folded rows in shared memory read by
+    overlapping-row UMMA descriptors, two output rows stacked along N against the banded
+    filter, 4-D clipped TMA store -- bit-exact vs the exact restatement."""
+    import paper_1903_06498_b200 as sb
+    from paper_1903_06498_b200 import workloads as W
+    from intmodel import conv_layer_exact
+    N, H, Wd, C, K, R, S, st, pad, relu = case
+    text = W.conv_fused(N, H, Wd, C, K, R, S, st, pad, relu=relu)
+    plan = sb.parse_program(text).describe_plan()
+    assert "band tiles of 2 output rows" in plan, plan
+    prog, inp, out = run(text, seed=N + H + K)
+    exp = conv_layer_exact(inp["I"].reshape(N, H, Wd, C), inp["F"].reshape(R, S, K, C), inp["Bias"], st, pad, relu,
+                           None, 8, "cuda").cpu().numpy().ravel()
+    np.testing.assert_array_equal(out["O"], exp)
+
+
+def test_band_fold_off_matches(monkeypatch):
+    """SB_NO_BAND keeps the materialised-rows fold: same bytes as the band path."""
+    from paper_1903_06498_b200 import workloads as W
+    text = W.conv_fused(2, 30, 30, 3, 64, 7, 7, 2, 3)
+    _, _, out_band = run(text, seed=3)
+    monkeypatch.setenv("SB_NO_BAND", "1")
+    import paper_1903_06498_b200 as sb
+    plan = sb.parse_program(text).describe_plan()
+    assert "band tiles" not in plan and "phase-folded" in plan, plan
+    _, _, out_rows = run(text, seed=3)
+    np.testing.assert_array_equal(out_band["O"], out_rows["O"])
+
+
 @pytest.mark.parametrize("case", [(2, 16, 16, 64, 64, True), (3, 9, 11, 64, 128, True), (2, 14, 14, 64, 192, False)],
                          ids=lambda c: "x".join(map(str, c)))
 def test_resident_filter_conv_fused_i8(case):
