@@ -1343,7 +1343,8 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
   const bool tall = !kp.band && kp.epi_split && kp.tma_out != 1 && kp.N <= 128 && !(kp.epi_res && !kp.res_mma) &&
                     (kp.M + 2 * BM - 1) / (2 * BM) >= 2 * 148 && !std::getenv("SB_IG_MT1");
   // split i8 epilogue: two staging buffers per group when the ring keeps >= 3 stages
-  const bool stg4_ok = kp.epi_split && kp.tma_out == 2 && !std::getenv("SB_IG_STG2");
+  // (band mode: the ring depth matters more -- one bulk copy per tile with DRAM latency to hide)
+  const bool stg4_ok = kp.epi_split && kp.tma_out == 2 && !kp.band && !std::getenv("SB_IG_STG2");
   auto shape = [&](int bn, int mt) {
     if (stg4_ok) {
       kp.stg4 = 1;
