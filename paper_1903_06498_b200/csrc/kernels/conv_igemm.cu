@@ -108,6 +108,10 @@ struct IgKParams {
   long long bias_bound;
   int thr_always;  // fast8 with a clamp bound outside int32: always the threshold form
   int epi_pipe;    // fast8 epilogue with the next chunk's TMEM load in flight
+  // n-stationary: tiles_n > 1 with the grid a multiple of tiles_n, so CTA c only ever sees
+  // n-tile c % tiles_n and keeps that slice of the filter resident (b_res); res1: the
+  // tensor-core residual single-buffered (the smem the resident slice needs)
+  int nstat, res1;
   // band mode (ConvPlan::fold_band): tile t = output rows (img, band*(t % band_rpi) ..) x 128
   // columns; A = one bulk copy of band_bytes from the compact folded rows (band_rowb bytes
   // each, band_img per image) into a ring stage of band_stage bytes, read with overlapping-row
@@ -446,8 +450,8 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
         const int res_buf = TM * p.bn, hcount = (p.bn + 127) / 128;
         int it = 0;
         for (int t = blockIdx.x; t < tiles; t += gridDim.x, it++) {
-          const int b = it & 1;
-          mbar_wait(&rempty[b], ((it >> 1) & 1) ^ 1);
+          const int b = p.res1 ? 0 : it & 1;
+          mbar_wait(&rempty[b], (p.res1 ? it & 1 : (it >> 1) & 1) ^ 1);
           const int m0 = (t / p.tiles_n) * TM, n0 = (t % p.tiles_n) * p.bn;
           const int halves = min(p.bn, p.N - n0 + 127) / 128;
           if (issuer) {
@@ -470,8 +474,9 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
           int cb = 0, r = 0, s = 0;
           for (int kb = 0; kb < p.kblocks; kb++) {
             const std::uint32_t dst = smem_u32(bres + kb * stage_b);
-            if (p.gather) tma_load_4d(dst, &bmap, bfull, kb * p.bk, 0, 0, 0);
-            else tma_load_4d(dst, &bmap, bfull, cb * p.bk, 0, s, r);
+            const int nb0 = p.nstat ? static_cast<int>(blockIdx.x % p.tiles_n) * p.bn : 0;  // this CTA's slice
+            if (p.gather) tma_load_4d(dst, &bmap, bfull, kb * p.bk, nb0, 0, 0);
+            else tma_load_4d(dst, &bmap, bfull, cb * p.bk, nb0, s, r);
             if (++cb == p.cblocks) {
               cb = 0;
               if (++s == p.S) {
@@ -638,12 +643,13 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       }
       if (p.res_mma) {
         // + residual: D[:, 128 hh + n] += R[:, 128 hh + k] * I[n, k], four K = 32 steps per half
-        mbar_wait(&rfull[acc], (iter >> 1) & 1);
+        const int rb = p.res1 ? 0 : acc;
+        mbar_wait(&rfull[rb], p.res1 ? iter & 1 : (iter >> 1) & 1);
         tc_fence_after();
         const int halves = min(p.bn, nrem + 127) / 128;
         const std::uint32_t hi128 = (1024u >> 4) | (1u << 14) | (2u << 29);
         const std::uint32_t id128 = (p.idesc & ~(0x3Fu << 17)) | ((128u >> 3) << 17);
-        const std::uint32_t ra = smem_u32(base + p.res_off + acc * TM * p.bn), ib = smem_u32(base + p.ident_off);
+        const std::uint32_t ra = smem_u32(base + p.res_off + rb * TM * p.bn), ib = smem_u32(base + p.ident_off);
         const int hcount = (p.bn + 127) / 128;
         for (int sub = 0; sub < p.mt; sub++)
           for (int hh = 0; hh < halves; hh++)
@@ -652,7 +658,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
               if (issuer)
                 umma_i8(d + sub * p.bn + 128 * hh, (((ra + (sub * hcount + hh) * 16384) >> 4) | (1u << 16)) + ks * 2,
                         hi128, ((ib >> 4) | (1u << 16)) + ks * 2, hi128, id128, 1);
-        if (issuer) umma_commit(&rempty[acc]);
+        if (issuer) umma_commit(&rempty[rb]);
         __syncwarp();
       }
       if (issuer) umma_commit(&tfull[acc]);
@@ -1298,15 +1304,17 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     kp.tiles_m = (kp.M + BM * mt - 1) / (BM * mt);
     const int sboxes = kp.band && kp.vec_mod == 64 ? kp.band : bn / 128;  // 16 KB staging boxes per sub-tile
     const int stg = kp.tma_out == 1 ? kStgBytes : kp.tma_out == 2 ? (kp.stg4 ? 4 : 2) * mt * sboxes * 16384 : 0;
-    const int res = kp.epi_res ? 2 * BM * mt * bn : 0;
+    const int res = kp.epi_res ? (kp.res1 ? 1 : 2) * BM * mt * bn : 0;
     const int vec = kp.fast_clamp ? 2 * kVecBytes : kp.epi_vec ? kVecBytes : 0;
     const int tab = kp.gather ? (kp.kblocks * kp.bk * 6 + 15) / 16 * 16 : 0;
     const int ident = kp.res_mma ? 16384 : 0;
     // the filter stays resident when there is one n-tile and it is small (<= 96 KB)
     kp.bn_box = kp.N <= 64 ? 64 : bn;
-    const int bres = kp.tiles_n == 1 && kp.kblocks * kp.bn_box * g.bk <= 96 * 1024 && !std::getenv("SB_IG_NOBRES")
+    const int bres = (kp.tiles_n == 1 || kp.nstat) && kp.kblocks * kp.bn_box * g.bk <= 96 * 1024 &&
+                             !std::getenv("SB_IG_NOBRES")
                          ? kp.kblocks * kp.bn_box * g.bk : 0;
     kp.b_res = bres ? 1 : 0;
+    if (kp.nstat && !bres) return false;
     const int kstage = (BM * mt + (bres ? 0 : kp.bn_box)) * g.bk;  // one k-block's A (+ B)
     const int avail = std::min(kRingBytes, kSmemMax - 1024 - 512 - stg - res - vec - tab - bres - ident);
     // k-blocks per stage: up to 4 while three stages still fit (gather mode: 1)
@@ -1345,13 +1353,23 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
   // split i8 epilogue: two staging buffers per group when the ring keeps >= 3 stages
   // (band mode: the ring depth matters more -- one bulk copy per tile with DRAM latency to hide)
   const bool stg4_ok = kp.epi_split && kp.tma_out == 2 && !kp.band && !std::getenv("SB_IG_STG2");
+  // n-stationary resident filter slices when several n-tiles each fit (see IgKParams::nstat)
+  const bool nstat_ok = !kp.gather && !kp.band && !std::getenv("SB_IG_NONSTAT");
+  auto try_layout = [&](int bn, int mt, bool nstat, bool stg4, bool res1, int min_stages) {
+    kp.nstat = nstat ? 1 : 0;
+    kp.stg4 = stg4 ? 1 : 0;
+    kp.res1 = res1 ? 1 : 0;
+    return layout(bn, mt) && kp.stages >= min_stages;
+  };
   auto shape = [&](int bn, int mt) {
-    if (stg4_ok) {
-      kp.stg4 = 1;
-      if (layout(bn, mt) && kp.stages >= 3) return true;
+    const int tn = (kp.N + bn - 1) / bn;
+    if (nstat_ok && tn > 1 && tn <= 8) {
+      if (stg4_ok && try_layout(bn, mt, true, true, false, 3)) return true;
+      if (try_layout(bn, mt, true, false, false, 2)) return true;
+      if (kp.res_mma && try_layout(bn, mt, true, false, true, 2)) return true;
     }
-    kp.stg4 = 0;
-    return layout(bn, mt);
+    if (stg4_ok && try_layout(bn, mt, false, true, false, 3)) return true;
+    return try_layout(bn, mt, false, false, false, 0);
   };
   if (!(wide && shape(256, 1)) && !(tall && shape(128, 2)) && !shape(128, 1)) return cudaErrorNotSupported;
   // idesc: S32 accumulate, signed A/B, both K-major, N = 128, M = 128
@@ -1785,7 +1803,9 @@ cudaError_t launch_conv_igemm(const ConvPlan& cp, const ConvArgs& args, cudaStre
   if (kp.fast8 && std::getenv("SB_IG_NOPIPE")) kp.epi_pipe = 0;  // A/B switch, read per launch
   const int tiles = kp.tiles_m * kp.tiles_n;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(tiles < num_sms ? tiles : num_sms));
+  int grid = tiles < num_sms ? tiles : num_sms;
+  if (kp.nstat) grid = grid / kp.tiles_n * kp.tiles_n;  // CTA c keeps n-tile c % tiles_n
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
   cfg.blockDim = dim3(64 + 32 * kp.epi_warps + (kp.gather ? 256 : 96 + (kp.res_mma ? 32 : 0)));
   cfg.dynamicSmemBytes = static_cast<unsigned>(kp.smem);
   cfg.stream = s;
@@ -1804,8 +1824,8 @@ cudaError_t launch_conv_igemm(const ConvPlan& cp, const ConvArgs& args, cudaStre
   long long h[640 + 32 * 4 * 3 + 256 + 512];
   cudaStreamSynchronize(s);
   cudaMemcpy(h, tr, sizeof(h), cudaMemcpyDeviceToHost);
-  std::fprintf(stderr, "igemm M=%d N=%d kblocks=%d kpb=%d stages=%d b_res=%d split=%d tiles=%d\n", kp.M, kp.N, kp.kblocks,
-               kp.kpb, kp.stages, kp.b_res, kp.epi_split, tiles);
+  std::fprintf(stderr, "igemm M=%d N=%d kblocks=%d kpb=%d stages=%d b_res=%d nstat=%d res1=%d split=%d tiles=%d\n", kp.M, kp.N, kp.kblocks,
+               kp.kpb, kp.stages, kp.b_res, kp.nstat, kp.res1, kp.epi_split, tiles);
   if (kp.band && (kp.exp & 16)) {
     const unsigned char* b = reinterpret_cast<const unsigned char*>(h + 1280);
     std::fprintf(stderr, "band stage smem 0x%llx stage %lld rowb %lld bytes %d\n", h[1536], h[1537], kp.band_rowb, kp.band_bytes);
