@@ -70,6 +70,7 @@ struct ConvKParams {
   int debug_nofilt;       // timing experiments only
   int pdl;                // launched with programmatic stream serialization
   int filter_early;       // filter is immutable input: fetch before griddepcontrol.wait
+  int epi_pipe;           // TMA-store epilogue software-pipelined over 16-column TMEM loads
   // fused epilogue: out = wrap(max(acc + vec[k], lo)) (optional parts), int64 arithmetic
   int epi, epi_vec, epi_lo;
   long long lo;
@@ -167,6 +168,103 @@ __device__ __forceinline__ void tmem_ld32(std::uint32_t taddr, std::uint32_t (&v
         "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16_async(std::uint32_t taddr, std::uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld16(std::uint32_t (&v)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+                 "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15])
+               :
+               : "memory");
+}
+__device__ __forceinline__ uint4 lds128(std::uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+
+// One 16-column half (columns 32 h + 16 hf ..) of this thread's row: the fused transform
+// (EPI: + vec[k]; THR: acc >= t[k] ? acc + vec[k] : lo, exact for |acc| < 2^31 - 1) and the
+// staging store -- I8: 16 wrapped bytes into the SW64 row (64-channel boxes of 8 KB), else
+// 16 int32 into the SW128 row (32-channel boxes of 16 KB).
+template <bool I8, bool EPI, bool THR>
+__device__ __forceinline__ void tc_epi_half(const std::uint32_t (&v)[16], int h, int hf, std::uint32_t vaddr,
+                                            std::uint32_t taddr, std::uint32_t stg, int row, std::uint32_t lo32) {
+  std::uint32_t o[16];
+#pragma unroll
+  for (int q4 = 0; q4 < 4; q4++) {
+    const int col = h * 32 + hf * 16 + 4 * q4;
+    uint4 b4 = make_uint4(0, 0, 0, 0), t4 = make_uint4(0, 0, 0, 0);
+    if (EPI) b4 = lds128(vaddr + col * 4);
+    if (THR) t4 = lds128(taddr + col * 4);
+    const std::uint32_t bq[4] = {b4.x, b4.y, b4.z, b4.w}, tq[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      const std::uint32_t x = v[4 * q4 + e];
+      o[4 * q4 + e] = THR ? (static_cast<std::int32_t>(x) >= static_cast<std::int32_t>(tq[e]) ? x + bq[e] : lo32)
+                          : EPI ? x + bq[e] : x;
+    }
+  }
+  if (I8) {
+    std::uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++)
+      w[q] = __byte_perm(__byte_perm(o[4 * q], o[4 * q + 1], 0x0040), __byte_perm(o[4 * q + 2], o[4 * q + 3], 0x0040),
+                         0x5410);
+    const std::uint32_t a = stg + (h >> 1) * 8192 + row * 64 + ((((h & 1) * 2 + hf) ^ ((row >> 1) & 3)) << 4);
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]));
+  } else {
+    const std::uint32_t rb = stg + h * 16384 + row * 128;
+#pragma unroll
+    for (int q = 0; q < 4; q++)
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rb + (((hf * 4 + q) ^ (row & 7)) << 4)),
+                   "r"(o[4 * q]), "r"(o[4 * q + 1]), "r"(o[4 * q + 2]), "r"(o[4 * q + 3]));
+  }
+}
+
+// The tile's K accumulator columns of this thread's row, software-pipelined over two 16-column
+// TMEM buffers (half k+1 in flight while half k is transformed and staged).
+template <bool I8, bool EPI, bool THR>
+__device__ __forceinline__ void tc_epi_pipelined(std::uint32_t tbase, int K, std::uint32_t vaddr, std::uint32_t taddr,
+                                                 std::uint32_t stg, int row, std::uint32_t lo32) {
+  std::uint32_t va[16], vb[16];
+  const int chunks = K / 32;
+  if (K == 64) {
+    // the whole row at once: four loads in flight, one wait (the TMEM load latency, not the
+    // transform, bounds this short epilogue)
+    std::uint32_t vc[16], vd[16];
+    tmem_ld16_async(tbase, va);
+    tmem_ld16_async(tbase + 16, vb);
+    tmem_ld16_async(tbase + 32, vc);
+    tmem_ld16_async(tbase + 48, vd);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    tmem_wait_ld16(va);
+    tmem_wait_ld16(vb);
+    tmem_wait_ld16(vc);
+    tmem_wait_ld16(vd);
+    tc_epi_half<I8, EPI, THR>(va, 0, 0, vaddr, taddr, stg, row, lo32);
+    tc_epi_half<I8, EPI, THR>(vb, 0, 1, vaddr, taddr, stg, row, lo32);
+    tc_epi_half<I8, EPI, THR>(vc, 1, 0, vaddr, taddr, stg, row, lo32);
+    tc_epi_half<I8, EPI, THR>(vd, 1, 1, vaddr, taddr, stg, row, lo32);
+    return;
+  }
+  tmem_ld16_async(tbase, va);
+  for (int h = 0; h < chunks; h++) {
+    tmem_wait_ld16(va);
+    tmem_ld16_async(tbase + h * 32 + 16, vb);
+    tc_epi_half<I8, EPI, THR>(va, h, 0, vaddr, taddr, stg, row, lo32);
+    tmem_wait_ld16(vb);
+    if (h + 1 < chunks) tmem_ld16_async(tbase + (h + 1) * 32, va);
+    tc_epi_half<I8, EPI, THR>(vb, h, 1, vaddr, taddr, stg, row, lo32);
+  }
 }
 
 __device__ __forceinline__ std::uint32_t a_hi_for(std::uint32_t addr, int mode) {
@@ -286,7 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int x0 = (t % p.tiles_x) * p.TX;
         for (int cc = 0; cc < p.chunks; cc++) {
           mbar_wait(&empty[stage], phase ^ 1);
-          trace_at(p.trace, (t - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x));
+          if (t < static_cast<int>(blockIdx.x + 8 * gridDim.x)) trace_at(p.trace, (t - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x));
           mbar_expect_tx(&full[stage], p.strip_bytes);
           tma_load_4d(smem_u32(strips + stage * p.strip_bytes), &amap, &full[stage], cc * 64, p.v_off, x0 + p.u_off, n);
           if (!filter_issued) {
@@ -316,12 +414,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         int acc = iter & 1;
         std::uint32_t aphase = (iter >> 1) & 1;
         mbar_wait(&tempty[acc], aphase ^ 1);
-        if (issuer) trace_at(p.trace, 8 + iter);
+        if (issuer) { if (iter < 8) trace_at(p.trace, 8 + iter); }
         tc_fence_after();
         std::uint32_t dcol = tmem_base + static_cast<std::uint32_t>(acc * p.K);
         for (int cc = 0; cc < p.chunks; cc++) {
           mbar_wait(&full[stage], phase);
-          if (issuer) trace_at(p.trace, 16 + iter);
+          if (issuer) { if (iter < 8) trace_at(p.trace, 16 + iter); }
           tc_fence_after();
           const std::uint32_t sbase = smem_u32(strips + stage * p.strip_bytes);
           const std::uint32_t bbase = fsm_addr + static_cast<std::uint32_t>(cc) * p.filt_tap_bytes;
@@ -359,7 +457,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (issuer) umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
         __syncwarp();
-        if (issuer) trace_at(p.trace, 24 + iter);
+        if (issuer) { if (iter < 8) trace_at(p.trace, 24 + iter); }
       }
     }
   } else if (warp < 6 || (p.tma_out && p.nstg == 2 && !p.st_out)) {
@@ -378,11 +476,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int xl = row / p.P;
     const int y = row % p.P;
     int iter = 0;
-    if (p.epi_vec) {
-      // per-output-channel vector of the fused epilogue (e.g. the bias), as int32 in smem
+    if (p.epi) {
+      // per-output-channel vector of the fused epilogue (e.g. the bias; 0 without one), as
+      // int32 in smem, followed by the clamp thresholds
       for (int k = threadIdx.x - 64; k < p.K; k += ethreads) {
         long long a = p.vec_c + p.vec_k * k;
-        const int b = p.vec_kind == kI8 ? static_cast<const std::int8_t*>(p.vec)[a]
+        const int b = !p.epi_vec ? 0
+                      : p.vec_kind == kI8 ? static_cast<const std::int8_t*>(p.vec)[a]
                       : p.vec_kind == kI16 ? static_cast<const std::int16_t*>(p.vec)[a]
                                            : static_cast<const std::int32_t*>(p.vec)[a];
         vec_s[k] = b;
@@ -420,11 +520,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         asm volatile("bar.sync %0, 128;" ::"r"(gbar) : "memory");  // staging buffer sb is free again
         mbar_wait(&tfull[acc], aphase);
-        if (leader) trace_at(p.trace, 32 + iter);
+        if (leader) { if (iter < 8) trace_at(p.trace, 32 + iter); }
         tc_fence_after();
         std::uint8_t* stg = p.tma_out == 2 ? staging + static_cast<std::uint32_t>(sb * (halves / 2)) * 8192u
                                            : staging + static_cast<std::uint32_t>(sb * halves) * 16384u;
-        for (int h = 0; h < halves; h++) {
+        if (p.epi_pipe) {
+          const std::uint32_t tb = tmem_base + (static_cast<std::uint32_t>(quarter * 32) << 16) +
+                                   static_cast<std::uint32_t>(acc * p.K);
+          const std::uint32_t va = smem_u32(vec_s), ta = smem_u32(vec_s + p.K), sa = smem_u32(stg);
+          const std::uint32_t lo32 = static_cast<std::uint32_t>(p.lo);
+          if (p.tma_out == 2) {
+            if (p.epi && p.epi_lo) tc_epi_pipelined<true, true, true>(tb, p.K, va, ta, sa, row, lo32);
+            else if (p.epi) tc_epi_pipelined<true, true, false>(tb, p.K, va, ta, sa, row, lo32);
+            else tc_epi_pipelined<true, false, false>(tb, p.K, va, ta, sa, row, lo32);
+          } else {
+            if (p.epi && p.epi_lo) tc_epi_pipelined<false, true, true>(tb, p.K, va, ta, sa, row, lo32);
+            else if (p.epi) tc_epi_pipelined<false, true, false>(tb, p.K, va, ta, sa, row, lo32);
+            else tc_epi_pipelined<false, false, false>(tb, p.K, va, ta, sa, row, lo32);
+          }
+        }
+        for (int h = 0; h < (p.epi_pipe ? 0 : halves); h++) {
           std::uint32_t v[32];
           tmem_ld32(tmem_base + (static_cast<std::uint32_t>(quarter * 32) << 16) +
                         static_cast<std::uint32_t>(acc * p.K + h * 32),
@@ -537,7 +652,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                   : "memory");
           }
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          trace_at(p.trace, 40 + iter);
+          { if (iter < 8) trace_at(p.trace, 40 + iter); }
         }
       }
       if (leader) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -847,6 +962,7 @@ cudaError_t launch_conv_tc(const ConvPlan& cp, const ConvArgs& args, cudaStream_
   kp.pdl_wait = kp.pdl && args.pdl_mode == kPdlWait ? 1 : 0;
   kp.store_wait = kp.pdl && args.pdl_mode == kPdlLoadEarly ? 1 : 0;
   kp.filter_early = args.b_immutable ? 1 : 0;
+  kp.epi_pipe = kp.tma_out && !kp.st_out && !std::getenv("SB_TC_NOPIPE") ? 1 : 0;  // A/B switch, read per launch
   kp.epi = cp.epi ? 1 : 0;
   kp.epi_vec = cp.epi_vec ? 1 : 0;
   kp.epi_lo = cp.epi_lo ? 1 : 0;
