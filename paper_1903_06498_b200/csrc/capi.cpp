@@ -501,6 +501,14 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
       ctx->launches++;
       return;
     }
+    if (l.kernel == sb::KernelKind::GemmI8TC && l.gemm.limbs_a && l.gemm.limb_fused) {
+      const sb::GemmPlan& g = l.gemm;
+      cuda_check(sb::launch_limb_fused(g, ptr_of(g.a_buf), ptr_of(g.b_buf), ptr_of(g.planes_a), ptr_of(g.planes_b),
+                                       ptr_of(g.c_buf), ctx->stream, ctx->num_sms),
+                 "gemm_limb");
+      ctx->launches += 3;
+      return;
+    }
     if (l.kernel == sb::KernelKind::GemmI8TC && l.gemm.limbs_a) {
       const sb::GemmPlan& g = l.gemm;
       char* pa = static_cast<char*>(ptr_of(g.planes_a));

@@ -54,6 +54,11 @@ cudaError_t launch_gemm_f32(const GemmPlan& g, const void* a, const void* b, voi
 // byte-limb mode: split A/B into concatenated unsigned byte planes, and the final combine
 cudaError_t launch_limb_split(const GemmPlan& g, const void* a, const void* b, void* pa, void* pb, cudaStream_t s);
 cudaError_t launch_limb_combine(const GemmPlan& g, const void* sums, void* c, cudaStream_t s);
+// Fused byte-limb GEMM: planes (launch-internal split) + one kernel with the combine in its
+// epilogue; pa / pb hold limbs_a * M * limb_fused_kp(g) / limbs_b * N * limb_fused_kp(g) bytes.
+cudaError_t launch_limb_fused(const GemmPlan& g, const void* a, const void* b, void* pa, void* pb, void* c,
+                              cudaStream_t s, int num_sms);
+long long limb_fused_kp(const GemmPlan& g);
 // The u8 GEMM computing S_s inside a limb plan.
 GemmPlan limb_sum_plan(const GemmPlan& g, int s);
 long long limb_plane_bytes_a(const GemmPlan& g);

@@ -703,6 +703,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
+  __syncwarp();  // reconverge the single-lane role warps before the CTA barrier
   __syncthreads();
   if (threadIdx.x == 0) trace_at(p.trace, 50);
   if (warp == 1) {

@@ -16,7 +16,10 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -114,6 +117,20 @@ __device__ __forceinline__ void tmem_ld32(std::uint32_t taddr, std::uint32_t (&v
         "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16_async(std::uint32_t taddr, std::uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ bool elect_one_sync() {
+  std::uint32_t is;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(is));
+  return is != 0;
 }
 
 // SWIZZLE_128B descriptors (version 1, layout 2 in bits 61-63).
@@ -275,6 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (p.tma_out && leader) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
+  __syncwarp();  // reconverge the single-lane role warps before the CTA barrier
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
@@ -572,6 +590,423 @@ cudaError_t launch_limb_combine(const GemmPlan& g, const void* sums, void* c, cu
 }
 
 long long limb_plane_bytes_a(const GemmPlan& g) { return limb_a_off(g, limb_smax(g) + 1); }
+
+// ---- fused byte-limb GEMM ------------------------------------------------------------------
+// All output-byte sums in ONE kernel: per 128 x 128 output tile, TMEM holds S_0 .. S_smax
+// (128 columns each, 512 in all) and every 64-byte k-block of the la A planes and lb B planes
+// (u8, K-major [limb][rows][Kp], SW64) feeds the pairs (i, s - i) of every sum s.  The
+// epilogue combines C = sum_s S_s << 8s (mod 2^32) straight from TMEM into the output: no
+// sums buffer and no combine pass.  Split-K (ksplit > 1) runs k-chunks on separate CTAs that
+// add their partial C with red.global.add (wrap-around add: exact mod 2^32; the output was
+// zeroed first when it is fresh).
+
+namespace {
+
+constexpr int kLimbThreads = 256;  // warp 0: A loads, warp 1: MMA, warp 2: B loads, 4..7: epilogue
+constexpr int kLimbStages = 3;
+constexpr std::uint32_t kLimbPlane = 128 * 64;  // one plane's 128 rows x 64 bytes
+
+struct LimbKParams {
+  int M, N, Kp, la, lb, smax;
+  int tiles_m, tiles_n, ksplit, kb_per;  // k-blocks of 64 bytes per split chunk
+  int out_kind, fresh, atomic;
+  int tma_c;  // i32 output tile through swizzled staging: TMA store (fresh, one chunk) or TMA add
+  void* c;
+  long long ldc;
+  std::uint32_t idesc;
+  long long* trace;  // SB_LIMB_TRACE: per-CTA clock64 stamps [start, first stage, MMAs done, epilogue done]
+};
+
+__device__ __forceinline__ long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return static_cast<long long>(t);
+}
+
+__device__ __forceinline__ void tma_load_3d(std::uint32_t dst, const CUtensorMap* map, std::uint64_t* bar, int c0,
+                                            int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<std::uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kLimbThreads, 1)
+    gemm_limb_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
+                     const __grid_constant__ CUtensorMap cmap, const LimbKParams p) {
+  extern __shared__ __align__(1024) std::uint8_t smem_raw[];
+  std::uint8_t* base =
+      reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t{1023});
+  const std::uint32_t stage_bytes = (p.la + p.lb) * kLimbPlane;
+  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(base + kLimbStages * stage_bytes);
+  std::uint64_t* full = bars;
+  std::uint64_t* empty = bars + kLimbStages;
+  std::uint64_t* tfull = bars + 2 * kLimbStages;
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 2 * kLimbStages + 1);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int tile = blockIdx.x / p.ksplit, chunk = blockIdx.x % p.ksplit;
+  const int m0 = (tile / p.tiles_n) * 128, n0 = (tile % p.tiles_n) * 128;
+  const int kb0 = chunk * p.kb_per, kb1 = min(kb0 + p.kb_per, p.Kp / 64);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kLimbStages; s++) {
+      mbar_init(&full[s], 2);  // A and B producers each arrive with their bytes
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const std::uint32_t tmem_base = *tmem_slot;
+  if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 8] = gtime();
+  if (warp == 0 || warp == 2) {
+    if (lane == 0) {
+      const bool is_a = warp == 0;
+      const int np = is_a ? p.la : p.lb, r0 = is_a ? m0 : n0;
+      int stage = 0;
+      std::uint32_t phase = 0;
+      for (int kb = kb0; kb < kb1; kb++) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_expect_tx(&full[stage], np * kLimbPlane);
+        const std::uint32_t dst = smem_u32(base + stage * stage_bytes) + (is_a ? 0u : p.la * kLimbPlane);
+        // every limb plane in one box (limb is the outer box dimension: planes 8 KB apart)
+        tma_load_3d(dst, is_a ? &amap : &bmap, &full[stage], kb * 64, r0, 0);
+        if (++stage == kLimbStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    const bool issuer = elect_one_sync();
+    int stage = 0;
+    std::uint32_t phase = 0;
+    // SW64 K-major descriptors: SBO = 8 rows x 64 bytes, layout 4
+    const std::uint32_t hi = (512u >> 4) | (1u << 14) | (4u << 29);
+    for (int kb = kb0; kb < kb1; kb++) {
+      mbar_wait(&full[stage], phase);
+      tc_fence_after();
+      if (p.trace && issuer && kb == kb0) p.trace[blockIdx.x * 8 + 1] = gtime();
+      if (issuer) {
+        const std::uint32_t sb = smem_u32(base + stage * stage_bytes);
+        for (int ks = 0; ks < 2; ks++)
+          for (int s = 0; s <= p.smax; s++)
+            for (int i = 0; i <= s; i++) {
+              const int j = s - i;
+              if (i >= p.la || j >= p.lb) continue;
+              const std::uint32_t a = ((sb + i * kLimbPlane) >> 4) + ks * 2, b = ((sb + (p.la + j) * kLimbPlane) >> 4) + ks * 2;
+              // the first product of sum s in this CTA overwrites its accumulator
+              const bool first = kb == kb0 && ks == 0 && i == max(0, s - p.lb + 1);
+              umma_i8(tmem_base + s * 128, a | (1u << 16), hi, b | (1u << 16), hi, p.idesc, first ? 0u : 1u);
+            }
+        umma_commit(&empty[stage]);
+      }
+      __syncwarp();
+      if (++stage == kLimbStages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    if (issuer) umma_commit(tfull);
+    if (p.trace && issuer) p.trace[blockIdx.x * 8 + 2] = gtime();
+    __syncwarp();
+  } else if (warp >= 4) {
+    // epilogue: row m0 + 32 q + lane, 16 columns at a time: C = sum_s S_s << 8s
+    const int quarter = warp & 3, row = m0 + quarter * 32 + lane;
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+    if (p.trace && threadIdx.x == 128) p.trace[blockIdx.x * 8 + 3] = gtime();
+    const std::uint32_t lanes = static_cast<std::uint32_t>(quarter * 32) << 16;
+    for (int c16 = 0; c16 < 8; c16++) {
+      std::uint32_t v[4][16];
+#pragma unroll
+      for (int s = 0; s < 4; s++)
+        if (s <= p.smax) tmem_ld16_async(tmem_base + lanes + s * 128 + c16 * 16, v[s]);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      std::uint32_t o[16];
+#pragma unroll
+      for (int q = 0; q < 16; q++) {
+        std::uint32_t x = 0;
+#pragma unroll
+        for (int s = 0; s < 4; s++)
+          if (s <= p.smax) x += v[s][q] << (8 * s);
+        o[q] = x;
+      }
+      if (p.tma_c) {
+        // staging (the drained stage ring): 4 boxes of 32 columns x 128 rows, 128B swizzle
+        const int r = quarter * 32 + lane;
+        const std::uint32_t rb = smem_u32(base) + (c16 >> 1) * 16384 + r * 128;
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rb + ((((c16 & 1) * 4 + q) ^ (r & 7)) << 4)),
+                       "r"(o[4 * q]), "r"(o[4 * q + 1]), "r"(o[4 * q + 2]), "r"(o[4 * q + 3]));
+        continue;
+      }
+      const int n = n0 + c16 * 16;
+      if (row >= p.M || n >= p.N) continue;
+      const long long base_idx = static_cast<long long>(row) * p.ldc + n;
+      const int cnt = min(16, p.N - n);
+      if (p.out_kind == kI32 && p.atomic) {
+        std::uint32_t* d = static_cast<std::uint32_t*>(p.c) + base_idx;
+        for (int q = 0; q < cnt; q++) asm volatile("red.global.add.u32 [%0], %1;" ::"l"(d + q), "r"(o[q]) : "memory");
+      } else if (p.out_kind == kI32 && p.fresh && cnt == 16 && (base_idx & 3) == 0) {
+        uint4* d = reinterpret_cast<uint4*>(static_cast<std::uint32_t*>(p.c) + base_idx);
+#pragma unroll
+        for (int q = 0; q < 4; q++) d[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+      } else {
+        for (int q = 0; q < cnt; q++) {
+          if (p.out_kind == kI32) {
+            std::uint32_t* d = static_cast<std::uint32_t*>(p.c) + base_idx + q;
+            *d = p.fresh ? o[q] : *d + o[q];
+          } else if (p.out_kind == kI16) {
+            std::int16_t* d = static_cast<std::int16_t*>(p.c) + base_idx + q;
+            *d = static_cast<std::int16_t>(p.fresh ? o[q] : static_cast<std::uint32_t>(*d) + o[q]);
+          } else {
+            std::int8_t* d = static_cast<std::int8_t*>(p.c) + base_idx + q;
+            *d = static_cast<std::int8_t>(p.fresh ? o[q] : static_cast<std::uint32_t>(*d) + o[q]);
+          }
+        }
+      }
+    }
+    if (p.tma_c) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (threadIdx.x == 128) {
+        for (int h = 0; h < 4; h++) {
+          if (n0 + h * 32 >= p.N) break;
+          if (p.atomic)
+            asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                             reinterpret_cast<std::uint64_t>(&cmap)),
+                         "r"(smem_u32(base) + h * 16384), "r"(n0 + h * 32), "r"(m0)
+                         : "memory");
+          else
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                             reinterpret_cast<std::uint64_t>(&cmap)),
+                         "r"(smem_u32(base) + h * 16384), "r"(n0 + h * 32), "r"(m0)
+                         : "memory");
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      }
+    }
+    if (p.trace && threadIdx.x == 128) p.trace[blockIdx.x * 8 + 5] = gtime();
+  }
+  __syncwarp();  // the producer warps' other lanes wait for lane 0 (bar.sync is per warp)
+  tc_fence_before();
+  __syncthreads();
+  if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 8 + 4] = gtime();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+  }
+}
+
+// Unsigned byte planes [limb][rows][Kp] (K-major, zero past K) of a row-major source whose
+// k index is contiguous (A, or B stored [n][k]): one thread per 4 consecutive k.
+__global__ void limb_planes_kernel(const void* __restrict__ src, int kind, long long rows, long long K, long long Kp,
+                                   long long ld, long long off, int limbs, std::uint8_t* __restrict__ dst) {
+  const long long kq = Kp / 4, total = rows * kq;
+  for (long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; g < total;
+       g += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = g / kq, k = (g - r * kq) * 4;
+    std::uint32_t v[4];
+    const long long e0 = off + r * ld + k;
+    if (kind == kI32 && k + 4 <= K && (e0 & 3) == 0) {
+      const uint4 q = __ldg(reinterpret_cast<const uint4*>(static_cast<const std::int32_t*>(src) + e0));
+      v[0] = q.x;
+      v[1] = q.y;
+      v[2] = q.z;
+      v[3] = q.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; e++) v[e] = k + e < K ? elem_bits(src, kind, e0 + e) : 0u;
+    }
+    for (int i = 0; i < limbs; i++) {
+      const unsigned sel = static_cast<unsigned>(i | ((4 + i) << 4));
+      *reinterpret_cast<std::uint32_t*>(dst + (i * rows + r) * Kp + k) =
+          __byte_perm(__byte_perm(v[0], v[1], sel), __byte_perm(v[2], v[3], sel), 0x5410);
+    }
+  }
+}
+
+// Same for B stored [k][n] (n contiguous): 32 x 32 element tiles through shared memory so
+// both the reads (along n) and the plane writes (along k) are coalesced.
+__global__ void limb_planes_t_kernel(const void* __restrict__ src, int kind, long long N, long long K, long long Kp,
+                                     long long ldk, long long off, int limbs, std::uint8_t* __restrict__ dst) {
+  __shared__ std::uint32_t tile[32][33];
+  const long long tn = (N + 31) / 32, tk = (Kp + 31) / 32;
+  for (long long t = blockIdx.x; t < tn * tk; t += gridDim.x) {
+    const long long n0 = (t % tn) * 32, k0 = (t / tn) * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+      const long long k = k0 + r, n = n0 + threadIdx.x;
+      tile[r][threadIdx.x] = (k < K && n < N) ? elem_bits(src, kind, off + k * ldk + n) : 0u;
+    }
+    __syncthreads();
+    // write phase: thread (x, y) -> n = n0 + 4 y + x / 8 (8 passes of 32 rows... 4 per pass),
+    // k = k0 + 4 (x % 8): one 32-bit word of 4 consecutive k per limb
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    for (int q = tid; q < 32 * 8; q += blockDim.x * blockDim.y) {
+      const int rr = q / 8, kk = (q % 8) * 4;
+      const long long n = n0 + rr, k = k0 + kk;
+      if (n < N && k < Kp) {
+        const std::uint32_t x0 = tile[kk][rr], x1 = tile[kk + 1][rr], x2 = tile[kk + 2][rr], x3 = tile[kk + 3][rr];
+        for (int i = 0; i < limbs; i++) {
+          const unsigned sel = static_cast<unsigned>(i | ((4 + i) << 4));
+          *reinterpret_cast<std::uint32_t*>(dst + (i * N + n) * Kp + k) =
+              __byte_perm(__byte_perm(x0, x1, sel), __byte_perm(x2, x3, sel), 0x5410);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+struct LimbPrepared {
+  GemmPlan gp;
+  const void *pa, *pb;
+  void* c;
+  LimbKParams kp;
+  CUtensorMap amap, bmap, cmap;
+};
+std::mutex g_limb_mu;
+std::vector<LimbPrepared>* g_limb_prep = nullptr;
+
+}  // namespace
+
+long long limb_fused_kp(const GemmPlan& g) { return (g.K + 63) / 64 * 64; }
+
+cudaError_t launch_limb_fused(const GemmPlan& g, const void* a, const void* b, void* pa, void* pb, void* c,
+                              cudaStream_t s, int num_sms) {
+  const long long Kp = limb_fused_kp(g);
+  auto* A = static_cast<std::uint8_t*>(pa);
+  auto* B = static_cast<std::uint8_t*>(pb);
+  limb_planes_kernel<<<148 * 8, 256, 0, s>>>(a, g.a_kind, g.M, g.K, Kp, g.lda, g.a0, g.limbs_a, A);
+  if (g.b_kmajor)
+    limb_planes_kernel<<<148 * 8, 256, 0, s>>>(b, g.b_kind, g.N, g.K, Kp, g.ldb, g.b0, g.limbs_b, B);
+  else
+    limb_planes_t_kernel<<<148 * 8, dim3(32, 8), 0, s>>>(b, g.b_kind, g.N, g.K, Kp, g.ldb, g.b0, g.limbs_b, B);
+  const int ob = g.c_dtype == DType::I8 ? 1 : g.c_dtype == DType::I16 ? 2 : 4;
+  void* cc = static_cast<char*>(c) + g.c0 * ob;
+  LimbPrepared prep;
+  {
+    LimbPrepared* pr = nullptr;
+    std::lock_guard<std::mutex> lock(g_limb_mu);
+    if (!g_limb_prep) g_limb_prep = new std::vector<LimbPrepared>();
+    for (auto& e : *g_limb_prep)
+      if (e.pa == pa && e.pb == pb && e.c == cc && same(e.gp, g)) pr = &e;
+    if (!pr) {
+      if (g_limb_prep->size() >= 64) g_limb_prep->clear();
+      LimbPrepared f;
+      f.gp = g;
+      f.pa = pa;
+      f.pb = pb;
+      f.c = cc;
+      LimbKParams& kp = f.kp;
+      std::memset(&kp, 0, sizeof(kp));
+      kp.M = static_cast<int>(g.M);
+      kp.N = static_cast<int>(g.N);
+      kp.Kp = static_cast<int>(Kp);
+      kp.la = g.limbs_a;
+      kp.lb = g.limbs_b;
+      kp.smax = limb_smax(g);
+      kp.tiles_m = static_cast<int>((g.M + 127) / 128);
+      kp.tiles_n = static_cast<int>((g.N + 127) / 128);
+      const int kbs = static_cast<int>(Kp / 64), tiles = kp.tiles_m * kp.tiles_n;
+      // split-K (i32 outputs: red.global.add) while tiles alone leave SMs idle
+      kp.ksplit = 1;
+      if (g.c_dtype == DType::I32 && !std::getenv("SB_LIMB_NOSPLIT"))
+        while (kp.ksplit < 8 && tiles * kp.ksplit * 2 <= num_sms && kbs / (kp.ksplit * 2) >= 4) kp.ksplit *= 2;
+      kp.kb_per = (kbs + kp.ksplit - 1) / kp.ksplit;
+      kp.out_kind = ob == 1 ? kI8 : ob == 2 ? kI16 : kI32;
+      kp.fresh = g.fresh ? 1 : 0;
+      kp.atomic = kp.ksplit > 1 || !g.fresh ? 1 : 0;  // partial or accumulating tiles add into C
+      kp.tma_c = kp.out_kind == kI32 && g.ldc % 4 == 0 && reinterpret_cast<std::uintptr_t>(cc) % 16 == 0 ? 1 : 0;
+      if (!kp.tma_c) kp.ksplit = 1, kp.atomic = 0;
+      kp.c = cc;
+      kp.ldc = g.ldc;
+      // u8 x u8 -> s32, both K-major, N = 128, M = 128
+      kp.idesc = (2u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+      auto encode = get_encode();
+      if (!encode) return cudaErrorNotSupported;
+      cuuint32_t es[3] = {1, 1, 1};
+      cuuint64_t adim[3] = {static_cast<cuuint64_t>(Kp), static_cast<cuuint64_t>(g.M), static_cast<cuuint64_t>(g.limbs_a)};
+      cuuint64_t astr[2] = {static_cast<cuuint64_t>(Kp), static_cast<cuuint64_t>(Kp * g.M)};
+      cuuint32_t box[3] = {64, 128, static_cast<cuuint32_t>(g.limbs_a)};
+      if (encode(&f.amap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, pa, adim, astr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                 CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+          CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+      cuuint64_t bdim[3] = {static_cast<cuuint64_t>(Kp), static_cast<cuuint64_t>(g.N), static_cast<cuuint64_t>(g.limbs_b)};
+      cuuint64_t bstr[2] = {static_cast<cuuint64_t>(Kp), static_cast<cuuint64_t>(Kp * g.N)};
+      box[2] = static_cast<cuuint32_t>(g.limbs_b);
+      if (encode(&f.bmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, pb, bdim, bstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                 CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+          CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+      std::memset(&f.cmap, 0, sizeof(f.cmap));
+      if (kp.tma_c) {
+        cuuint64_t cdim[2] = {static_cast<cuuint64_t>(g.N), static_cast<cuuint64_t>(g.M)};
+        cuuint64_t cstr[1] = {static_cast<cuuint64_t>(g.ldc * 4)};
+        cuuint32_t cbox[2] = {32, 128};
+        if (encode(&f.cmap, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, cc, cdim, cstr, cbox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+            CUDA_SUCCESS)
+          return cudaErrorInvalidValue;
+      }
+      static bool attr = false;
+      if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(gemm_limb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        if (e != cudaSuccess) return e;
+        attr = true;
+      }
+      g_limb_prep->push_back(f);
+      pr = &g_limb_prep->back();
+    }
+    prep = *pr;
+  }
+  const LimbKParams& kp = prep.kp;
+  if (kp.atomic && kp.fresh && kp.ksplit > 1) {
+    // partial sums add into the output: start it from the identity
+    for (long long m = 0; m < g.M; m++) {
+      if (g.ldc == g.N) {
+        cudaError_t e = cudaMemsetAsync(cc, 0, static_cast<std::size_t>(g.M * g.N) * 4, s);
+        if (e != cudaSuccess) return e;
+        break;
+      }
+      cudaError_t e = cudaMemsetAsync(static_cast<std::uint32_t*>(cc) + m * g.ldc, 0, static_cast<std::size_t>(g.N) * 4, s);
+      if (e != cudaSuccess) return e;
+    }
+  }
+  const std::size_t smem = 1024 + kLimbStages * (kp.la + kp.lb) * kLimbPlane + 256;
+  const int grid = kp.tiles_m * kp.tiles_n * kp.ksplit;
+  static const bool tracing = std::getenv("SB_LIMB_TRACE") != nullptr;
+  if (!tracing) {
+    gemm_limb_kernel<<<grid, kLimbThreads, smem, s>>>(prep.amap, prep.bmap, prep.cmap, kp);
+    return cudaGetLastError();
+  }
+  LimbKParams kt = kp;
+  static long long* tr = nullptr;
+  if (!tr) cudaMalloc(&tr, 1024 * 8 * 8);
+  cudaMemsetAsync(tr, 0, 1024 * 8 * 8, s);
+  kt.trace = tr;
+  gemm_limb_kernel<<<grid, kLimbThreads, smem, s>>>(prep.amap, prep.bmap, prep.cmap, kt);
+  std::vector<long long> h(static_cast<std::size_t>(grid) * 8);
+  cudaStreamSynchronize(s);
+  cudaMemcpy(h.data(), tr, h.size() * 8, cudaMemcpyDeviceToHost);
+  long long t0 = h[0];
+  for (int b = 0; b < grid; b++) t0 = std::min(t0, h[b * 8]);
+  for (int b = 0; b < grid; b += grid / 8)
+    std::fprintf(stderr, "limb CTA %3d (ns): start %6lld first-stage %6lld mma-done %6lld epi-start %6lld epi-done %6lld end %6lld\n", b,
+                 h[b * 8] - t0, h[b * 8 + 1] - t0, h[b * 8 + 2] - t0, h[b * 8 + 3] - t0, h[b * 8 + 5] - t0, h[b * 8 + 4] - t0);
+  return cudaGetLastError();
+}
 
 // ---- 3xTF32 mode -----------------------------------------------------------------------
 // a = hi(a) + lo(a) with hi = tf32(a), lo = tf32(a - hi); A*B ~= hi*hi + hi*lo + lo*hi as

@@ -1128,11 +1128,20 @@ void match_kernels(Plan* plan, const Program& p, const PlanOptions& opt) {
           plan->bufs.push_back(b);
           return static_cast<int>(plan->bufs.size()) - 1;
         };
-        g.planes_a = scratch("limbs:" + plan->bufs[g.a_buf].name, kI8, limb_plane_bytes_a(g));
-        g.planes_b = scratch("limbs:" + plan->bufs[g.b_buf].name, kI8, limb_plane_bytes_b(g));
-        g.sums = scratch("limbsums:" + plan->bufs[g.c_buf].name, kI32, (limb_smax(g) + 1) * g.M * g.N);
-        plan->notes.push_back("launch " + st.launch.path + ": matmul exact modulo 2^" + std::to_string(g.limbs_a * 8) +
-                              " as " + std::to_string(limb_smax(g) + 1) + " u8 tensor-core GEMMs over byte limbs");
+        g.limb_fused = !std::getenv("SB_LIMB_UNFUSED");
+        if (g.limb_fused) {
+          g.planes_a = scratch("limbs:" + plan->bufs[g.a_buf].name, kI8, g.limbs_a * g.M * limb_fused_kp(g));
+          g.planes_b = scratch("limbs:" + plan->bufs[g.b_buf].name, kI8, g.limbs_b * g.N * limb_fused_kp(g));
+          plan->notes.push_back("launch " + st.launch.path + ": matmul exact modulo 2^" + std::to_string(g.limbs_a * 8) +
+                                " over byte limbs: " + std::to_string(limb_smax(g) + 1) +
+                                " u8 sums in TMEM of one tensor-core kernel, combined in its epilogue");
+        } else {
+          g.planes_a = scratch("limbs:" + plan->bufs[g.a_buf].name, kI8, limb_plane_bytes_a(g));
+          g.planes_b = scratch("limbs:" + plan->bufs[g.b_buf].name, kI8, limb_plane_bytes_b(g));
+          g.sums = scratch("limbsums:" + plan->bufs[g.c_buf].name, kI32, (limb_smax(g) + 1) * g.M * g.N);
+          plan->notes.push_back("launch " + st.launch.path + ": matmul exact modulo 2^" + std::to_string(g.limbs_a * 8) +
+                                " as " + std::to_string(limb_smax(g) + 1) + " u8 tensor-core GEMMs over byte limbs");
+        }
       }
       continue;
     }

@@ -95,6 +95,9 @@ struct GemmPlan {
   // concatenated along k (planes_a / planes_b), C (+)= sum_s S_s << 8s wrapped at the store
   int limbs_a = 0, limbs_b = 0, a_kind = 0, b_kind = 0;
   int planes_a = -1, planes_b = -1, sums = -1;  // scratch buffers
+  // fused (default): planes [limb][rows][Kp] and ONE kernel keeping every S_s in TMEM and
+  // combining them in its epilogue (gemm_tc.cu gemm_limb_kernel); else the per-sum GEMMs
+  bool limb_fused = false;
 };
 
 // Number of (i, j) limb pairs with i + j = s.

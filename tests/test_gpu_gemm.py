@@ -76,6 +76,8 @@ LIMB = [
     (128, 64, 48, "i32", "i16", True),
     (96, 112, 64, "i16", "i8", True),
     (33, 16, 16, "i32", "i32", True),
+    (256, 208, 2048, "i32", "i32", False),  # few tiles, long K: split-K partials added with red.global.add
+    (300, 128, 1008, "i16", "i32", True),   # K not a multiple of the 64-byte k-block (zero-padded planes)
 ]
 
 
@@ -85,6 +87,13 @@ def test_limb_gemm_vs_reference(case):
     text = (W.matmul_bt if bt else W.matmul)(M, N, K, in_dtype=dt, out_dtype=od)
     check(text, seed=M + N + K)
     check(text, seed=M + N + K + 1, provide_out=True)
+
+
+def test_limb_gemm_unfused_path(monkeypatch):
+    """SB_LIMB_UNFUSED keeps the per-sum GEMMs + combine pass: same bytes."""
+    monkeypatch.setenv("SB_LIMB_UNFUSED", "1")
+    text = W.matmul(130, 96, 80, in_dtype="i32", out_dtype="i32")
+    check(text, seed=5)
 
 
 def test_limb_gemm_config1_i32_exact():
