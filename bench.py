@@ -497,12 +497,17 @@ def sum_over_ranks(dist, world, dev, work):
 
 def traffic_of(cfg):
     """DRAM bytes (read + write) per launch of the dominant kernel from the committed ncu
-    capture (profiles/r02_traffic.json, written by tools/ncu_traffic.py), else None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as f:
-            return json.load(f)[cfg]["dram_bytes_per_launch"]
-    except Exception:
-        return None
+    capture: the steady-state one (profiles/r02_traffic_warm.json, `--cache-control none` on
+    launches after the set rotation, so earlier launches' dirty outputs are written back inside
+    the profiled ones; profiles/capture_r02_warm.sh), else the cold-cache one
+    (profiles/r02_traffic.json), else None."""
+    for name in ("r02_traffic_warm.json", "r02_traffic.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                return json.load(f)[cfg]["dram_bytes_per_launch"]
+        except Exception:
+            continue
+    return None
 
 
 def e2e_native(args, sb, np, torch, dist, world, ctx, prog, nbytes, in_names, out_names, work, unit, dev, local):
