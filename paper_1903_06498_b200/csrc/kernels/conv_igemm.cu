@@ -1361,17 +1361,22 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     kp.res1 = res1 ? 1 : 0;
     return layout(bn, mt) && kp.stages >= min_stages;
   };
-  auto shape = [&](int bn, int mt) {
+  const int max_tn = std::getenv("SB_IG_NSTAT8") ? 8 : 16;
+  auto shape_nstat = [&](int bn, int mt) {
     const int tn = (kp.N + bn - 1) / bn;
-    if (nstat_ok && tn > 1 && tn <= 8) {
-      if (stg4_ok && try_layout(bn, mt, true, true, false, 3)) return true;
-      if (try_layout(bn, mt, true, false, false, 2)) return true;
-      if (kp.res_mma && try_layout(bn, mt, true, false, true, 2)) return true;
-    }
+    if (!nstat_ok || tn < 2 || tn > max_tn) return false;
+    if (stg4_ok && try_layout(bn, mt, true, true, false, 3)) return true;
+    if (try_layout(bn, mt, true, false, false, 2)) return true;
+    return kp.res_mma && try_layout(bn, mt, true, false, true, 2);
+  };
+  auto shape = [&](int bn, int mt) {
     if (stg4_ok && try_layout(bn, mt, false, true, false, 3)) return true;
     return try_layout(bn, mt, false, false, false, 0);
   };
-  if (!(wide && shape(256, 1)) && !(tall && shape(128, 2)) && !shape(128, 1)) return cudaErrorNotSupported;
+  // n-stationary slices first (256-wide, then 128-wide tiles), then the streamed shapes
+  if (!(wide && shape_nstat(256, 1)) && !shape_nstat(128, 1) && !(wide && shape(256, 1)) && !(tall && shape(128, 2)) &&
+      !shape(128, 1))
+    return cudaErrorNotSupported;
   // idesc: S32 accumulate, signed A/B, both K-major, N = 128, M = 128
   kp.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
   // descriptor high word: SBO = 8 rows x row bytes, version 1, swizzle 128B (2) / 64B (4)

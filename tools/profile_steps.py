@@ -28,6 +28,10 @@ def program_text(which, batch):
         text = W.conv_fused(batch, 7, 7, 512, 2048, 1, 1, 1, 0, residual=True)
     elif which == "s3_1x1":
         text = W.conv_fused(batch, 14, 14, 256, 1024, 1, 1, 1, 0, residual=True)
+    elif which == "l24":
+        text = W.conv_fused(batch, 28, 28, 512, 1024, 1, 1, 2, 0, relu=False)
+    elif which == "l25":
+        text = W.conv_fused(batch, 28, 28, 512, 256, 1, 1, 1, 0)
     elif which == "l11":
         text = W.conv_fused(batch, 56, 56, 256, 512, 1, 1, 2, 0, relu=False)
     elif which == "s2_1x1":
