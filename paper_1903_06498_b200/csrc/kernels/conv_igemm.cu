@@ -120,6 +120,12 @@ struct IgKParams {
   long long band_rowb, band_img;
   const std::int8_t* band_src;
   std::uint32_t a_hi;
+  // strip mode (stride-1 3x3 over 64 channels into a fresh i8 activation): tile t = image
+  // t / strip_tx, output rows strip_rows * (t % strip_tx) .. (mt sub-tiles of 2 rows x 64-pixel
+  // pitch); A = ONE haloed strip (rows + 2, 64 pixels, 64 channels, SW64 4-D TMA box, zero
+  // outside the constraint window) per tile and the 9 taps are descriptor shifts of it
+  // ((i * 64 + j) * 64 bytes), so no input byte is fetched 9 times; 4-D clipped TMA store
+  int strip, strip_tx, strip_rows, strip_uoff, strip_voff, strip_stage;
   const void* vec;
   long long vec_k;
   long long lo;
@@ -367,8 +373,9 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
   const int TM = BM * p.mt;  // tile rows (output pixels)
   const std::uint32_t stage_a = TM * p.bk, stage_b = p.bn_box * p.bk;
   std::uint8_t* ring = base;                    // stages x (A | B), or stages x A with the filter resident
-  const std::uint32_t sstride = p.band ? static_cast<std::uint32_t>(p.band_stage)
-                                        : p.kpb * (stage_a + (p.b_res ? 0u : stage_b));
+  const std::uint32_t sstride = p.band    ? static_cast<std::uint32_t>(p.band_stage)
+                                 : p.strip ? static_cast<std::uint32_t>(p.strip_stage)
+                                           : p.kpb * (stage_a + (p.b_res ? 0u : stage_b));
   std::uint8_t* bres = base + p.bres_off;       // resident filter: kblocks x stage_b
   std::uint8_t* stg = base + p.stg_off;         // output staging: i32 4 x 16 KB quarters | i8 2 x 16 KB
   std::uint8_t* rstg = base + p.res_off;        // residual tiles (i8, 2 x 16 KB)
@@ -483,6 +490,25 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
                 s = 0;
                 r++;
               }
+            }
+          }
+        }
+      } else if (p.strip) {
+        // one haloed strip per tile (4-D TMA box, SW64)
+        if (pidx == 0) {
+          int stage = 0;
+          std::uint32_t phase = 0;
+          for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            if (issuer) {
+              const int img = t / p.strip_tx, x0 = (t - img * p.strip_tx) * p.strip_rows;
+              mbar_expect_tx(&full[stage], static_cast<std::uint32_t>(p.strip_stage));
+              tma_load_4d(smem_u32(ring + stage * sstride), &amap, &full[stage], 0, p.strip_voff, x0 + p.strip_uoff, img);
+            }
+            __syncwarp();
+            if (++stage == stages) {
+              stage = 0;
+              phase ^= 1;
             }
           }
         }
@@ -608,7 +634,22 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
           p.trace[1537] = static_cast<long long>(stage);
         }
 #endif
-        if (issuer && p.band) {
+        if (issuer && p.strip) {
+          // tap (i, j) of sub-tile sub: strip rows 2 sub + i .., shifted by j pixels (64 bytes
+          // each); SW64 descriptors, base offset 0 for every 64-byte row shift (conv_tc.cu)
+          const std::uint32_t sa0 = (sa >> 4) | (1u << 16);
+          for (int sub = 0; sub < p.mt; sub++) {
+            const std::uint32_t ds = d + sub * p.bn;
+#pragma unroll
+            for (int i = 0; i < 3; i++)
+#pragma unroll
+              for (int j = 0; j < 3; j++)
+#pragma unroll
+                for (int ks = 0; ks < 2; ks++)
+                  umma_i8(ds, sa0 + ((sub * 2 + i) * 64 + j) * 4 + ks * 2, hi, b0 + (i * 3 + j) * bs + ks * 2, hi, idesc,
+                          (i | j | ks) ? 1u : 0u);
+          }
+        } else if (issuer && p.band) {
           const std::uint32_t rs = static_cast<std::uint32_t>(p.band_rowb >> 4);
           // A descriptor low word: start | 16-byte stride between core matrices along K (a_hi)
           const std::uint32_t ab = (sa >> 4) | (1u << 16);
@@ -1101,6 +1142,19 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
                                  reinterpret_cast<std::uint64_t>(&cmap)),
                              "r"(smem_u32(stg + h * 16384)), "r"(n0 + h * 32), "r"(m0)
                              : "memory");
+          } else if (p.strip) {
+            // (k, pixel, row, image) per 128-row sub-tile (2 output rows x 64-pixel pitch):
+            // pixels past the row width and rows past the image are clipped
+            const int img = t / p.strip_tx, x0 = (t - img * p.strip_tx) * p.strip_rows;
+            for (int sub = 0; sub < p.mt; sub++)
+              for (int hh = 0; hh < p.bn / 128 || hh == 0; hh++) {
+                if (n0 + hh * 128 >= p.N) break;
+                asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                                 reinterpret_cast<std::uint64_t>(&cmap)),
+                             "r"(smem_u32(scur + (sub * hcnt + hh) * 16384)), "r"(n0 + hh * 128), "r"(0),
+                             "r"(x0 + sub * 2), "r"(img)
+                             : "memory");
+              }
           } else if (p.band) {
             // (k, row of the band, pixel, band index): pixels past the row width are clipped
             // one 16 KB box per band row
@@ -1295,6 +1349,12 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     kp.epi_split = kp.epi_warps == 8 && kp.tma_out != 1 && !std::getenv("SB_IG_NOSPLIT") ? 1 : 0;
     kp.bias_bound = T < INT_MAX ? INT_MAX - T : 0;
   }
+  // strip mode (see IgKParams::strip): stride-1 3x3 over exactly 64 channels, rows fit a
+  // 64-pixel pitch, fresh i8 output written by the TMA store, resident filter
+  if (!kp.gather && !cp.fold_band && cp.R == 3 && cp.S == 3 && cp.sx == 1 && cp.sy == 1 && cp.C == 64 &&
+      cp.W + 2 <= 64 && kp.tma_out == 2 && !cp.epi_res && cp.K <= 256 && !std::getenv("SB_IG_NOSTRIP") &&
+      cp.c_x == cp.W * cp.c_y && (cp.N == 1 || cp.c_n == cp.H * cp.c_x) && cp.c_y % 16 == 0)
+    kp.strip = 1;
   // dynamic smem: A/B ring (up to 128 KB) | resident filter | output staging | residual tiles |
   // vector | gather table | barriers, for tile width bn (false: does not fit)
   auto layout = [&](int bn, int mt) -> bool {
@@ -1319,14 +1379,20 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     const int avail = std::min(kRingBytes, kSmemMax - 1024 - 512 - stg - res - vec - tab - bres - ident);
     // k-blocks per stage: up to 4 while three stages still fit (gather mode: 1)
     kp.kpb = 1;
-    if (kp.band) kp.kpb = kp.kblocks;  // one bulk copy per tile feeds every k-block
+    if (kp.band || kp.strip) kp.kpb = kp.kblocks;  // one load per tile feeds every k-block
     else if (!kp.gather && !std::getenv("SB_IG_KPB1"))
       for (int c : {4, 3, 2})
         if (kp.kblocks % c == 0 && (std::getenv("SB_IG_KPB3") ? 3 : 2) * c * kstage <= avail) {
           kp.kpb = c;
           break;
         }
-    const int stage = kp.band ? kp.band_stage : kp.kpb * kstage;
+    if (kp.strip) {
+      kp.strip_rows = 2 * mt;
+      kp.strip_tx = static_cast<int>((cp.H + kp.strip_rows - 1) / kp.strip_rows);
+      kp.strip_stage = (kp.strip_rows + 2) * 64 * 64;
+      kp.tiles_m = static_cast<int>(cp.N) * kp.strip_tx;
+    }
+    const int stage = kp.band ? kp.band_stage : kp.strip ? kp.strip_stage : kp.kpb * kstage;
     if (avail < 2 * stage) return false;
     int ring = avail / stage * stage;
     kp.stages = std::min(16, ring / stage);
@@ -1354,7 +1420,7 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
   // (band mode: the ring depth matters more -- one bulk copy per tile with DRAM latency to hide)
   const bool stg4_ok = kp.epi_split && kp.tma_out == 2 && !kp.band && !std::getenv("SB_IG_STG2");
   // n-stationary resident filter slices when several n-tiles each fit (see IgKParams::nstat)
-  const bool nstat_ok = !kp.gather && !kp.band && !std::getenv("SB_IG_NONSTAT");
+  const bool nstat_ok = !kp.gather && !kp.band && !kp.strip && !std::getenv("SB_IG_NONSTAT");
   auto try_layout = [&](int bn, int mt, bool nstat, bool stg4, bool res1, int min_stages) {
     kp.nstat = nstat ? 1 : 0;
     kp.stg4 = stg4 ? 1 : 0;
@@ -1385,8 +1451,31 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
 
   std::memset(&out->amap, 0, sizeof(out->amap));
   if (kp.band && (kp.tma_out != 2 || !kp.b_res || kp.bn != kp.N || kp.mt != 1)) return cudaErrorNotSupported;
+  if (kp.strip && (!kp.b_res || kp.tiles_n != 1)) kp.strip = 0;  // (layout() ran with strip: redo without)
+  if (!kp.strip && kp.strip_stage) {
+    kp.strip_stage = 0;
+    if (!(wide && shape(256, 1)) && !(tall && shape(128, 2)) && !shape(128, 1)) return cudaErrorNotSupported;
+  }
   if (kp.band && reinterpret_cast<std::uintptr_t>(args.a) % 16) return cudaErrorMisalignedAddress;
-  if (!kp.gather && !kp.band) {
+  if (kp.strip) {
+    // A: the input window as (c, v, u, n) from the corner (u_lo, v_lo); box = haloed strip
+    const std::int8_t* abase = static_cast<const std::int8_t*>(args.a) + cp.a0 + cp.a_x * cp.u_lo + cp.a_y * cp.v_lo;
+    if (reinterpret_cast<std::uintptr_t>(abase) % 16 || cp.a_y % 16 || cp.a_x % 16 || cp.a_n % 16)
+      return cudaErrorMisalignedAddress;
+    cuuint64_t adim[4] = {64, static_cast<cuuint64_t>(cp.v_hi - cp.v_lo + 1), static_cast<cuuint64_t>(cp.u_hi - cp.u_lo + 1),
+                          static_cast<cuuint64_t>(cp.N)};
+    cuuint64_t astr[3] = {static_cast<cuuint64_t>(cp.a_y), static_cast<cuuint64_t>(cp.a_x),
+                          static_cast<cuuint64_t>(cp.a_n)};
+    cuuint32_t abox[4] = {64u, 64u, static_cast<cuuint32_t>(kp.strip_rows + 2), 1u};
+    cuuint32_t aes[4] = {1, 1, 1, 1};
+    kp.strip_uoff = static_cast<int>(cp.ox - cp.u_lo);
+    kp.strip_voff = static_cast<int>(cp.oy - cp.v_lo);
+    if (enc_tiled(&out->amap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<std::int8_t*>(abase), adim, astr, abox, aes,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  if (!kp.gather && !kp.band && !kp.strip) {
   // A: im2col over (c, v, u, n) from the window corner (u_lo, v_lo)
   const std::int8_t* abase = static_cast<const std::int8_t*>(args.a) + cp.a0 + cp.a_x * cp.u_lo + cp.a_y * cp.v_lo;
   if (reinterpret_cast<std::uintptr_t>(abase) % 16) return cudaErrorMisalignedAddress;
@@ -1422,6 +1511,17 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     cuuint64_t cstr[1] = {static_cast<cuuint64_t>(kp.ldc * 4)};
     cuuint32_t cbox[2] = {32, BM};
     if (enc_tiled(&out->cmap, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, kp.c, cdim, cstr, cbox, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  } else if (kp.tma_out == 2 && kp.strip) {
+    // (k, pixel, row, image), box (<= 128 channels, 64 pixels, 2 rows, 1): 128-byte padded rows
+    cuuint64_t cdim[4] = {static_cast<cuuint64_t>(cp.K), static_cast<cuuint64_t>(cp.W), static_cast<cuuint64_t>(cp.H),
+                          static_cast<cuuint64_t>(cp.N)};
+    cuuint64_t cstr[3] = {static_cast<cuuint64_t>(cp.c_y), static_cast<cuuint64_t>(cp.c_x),
+                          static_cast<cuuint64_t>(cp.N > 1 ? cp.c_n : cp.c_x * cp.H)};
+    cuuint32_t cbox[4] = {static_cast<cuuint32_t>(std::min<long long>(cp.K, 128)), 64, 2, 1};
+    if (enc_tiled(&out->cmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, kp.c, cdim, cstr, cbox, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;

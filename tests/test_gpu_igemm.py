@@ -222,6 +222,40 @@ def test_band_fold_conv_exact(case):
     np.testing.assert_array_equal(out["O"], exp)
 
 
+STRIP = [
+    # N, H, W, K, pad, relu: stride-1 3x3 over 64 channels into a fresh i8 activation
+    (2, 56, 56, 64, 1, True),      # the ResNet stage-1 shape
+    (3, 13, 17, 64, 1, True),      # odd rows (last strip clipped), 17-pixel rows in the 64 pitch
+    (2, 9, 62, 128, 1, False),     # widest row the pitch holds, K = 128, no clamp
+    (1, 20, 30, 256, 1, True),     # K = 256 (two store boxes per sub-tile)
+    (2, 10, 12, 64, 0, True),      # no padding (valid conv, different window corner)
+]
+
+
+@pytest.mark.parametrize("case", STRIP, ids=lambda c: "x".join(map(str, c)))
+def test_strip_conv_exact(case):
+    """Strip mode (IgKParams::strip): one haloed 4-D TMA strip per tile, the 9 taps as
+    descriptor shifts, 4-D clipped TMA store -- bit-exact vs the exact restatement."""
+    from paper_1903_06498_b200 import workloads as W
+    from intmodel import conv_layer_exact
+    N, H, Wd, K, pad, relu = case
+    text = W.conv_fused(N, H, Wd, 64, K, 3, 3, 1, pad, relu=relu)
+    prog, inp, out = run(text, seed=N + H + K + pad)
+    exp = conv_layer_exact(inp["I"].reshape(N, H, Wd, 64), inp["F"].reshape(3, 3, K, 64), inp["Bias"], 1, pad, relu,
+                           None, 8, "cuda").cpu().numpy().ravel()
+    np.testing.assert_array_equal(out["O"], exp)
+
+
+def test_strip_off_matches(monkeypatch):
+    """SB_IG_NOSTRIP keeps the im2col path: same bytes."""
+    from paper_1903_06498_b200 import workloads as W
+    text = W.conv_fused(2, 14, 14, 64, 64, 3, 3, 1, 1)
+    _, _, out_strip = run(text, seed=9)
+    monkeypatch.setenv("SB_IG_NOSTRIP", "1")
+    _, _, out_i2c = run(text, seed=9)
+    np.testing.assert_array_equal(out_strip["O"], out_i2c["O"])
+
+
 def test_band_fold_off_matches(monkeypatch):
     """SB_NO_BAND keeps the materialised-rows fold: same bytes as the band path."""
     from paper_1903_06498_b200 import workloads as W
