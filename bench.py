@@ -154,7 +154,7 @@ def spec(cfg, world, rank, args):
         n = args.batch or 32
         text = Wk.conv2d(n, 56, 56, 64, 64)
         s.update(text=text, flops=2.0 * Wk.conv_useful_macs(n, 56, 56, 64, 64), unit="GFLOP/s", bound="hbm",
-                 global_batch=n * world, images=n, dominant=("conv_i8_tc",),
+                 global_batch=n * world, images=n, dominant=("conv_i8_tc", "conv_igemm_tc"),
                  workload=f"BASELINE config 2: conv2d 3x3 NHWC 56x56x64->64, batch {n} per GPU, padding "
                           f"constraints, one Stripe block (i8 x i8 -> i32)",
                  cpu=dict(text=Wk.conv2d(1, 56, 56, 64, 64), work=2.0 * Wk.conv_useful_macs(1, 56, 56, 64, 64),
@@ -165,7 +165,7 @@ def spec(cfg, world, rank, args):
         piped = os.path.join(ROOT, "configs", f"c3_pipeline_b{n}.stripe")
         text = open(piped).read() if os.path.exists(piped) else Wk.conv_bias_relu(n, 56, 56, 64, 64)
         s.update(text=text, flops=2.0 * Wk.conv_useful_macs(n, 56, 56, 64, 64),
-                 unit="GFLOP/s", bound="hbm", global_batch=n * world, images=n, dominant=("conv_i8_tc",),
+                 unit="GFLOP/s", bound="hbm", global_batch=n * world, images=n, dominant=("conv_i8_tc", "conv_igemm_tc"),
                  workload=f"BASELINE config 3: fused conv3x3+bias+ReLU produced by the reference's "
                           f"tile_rewrite/fuse/localize/scalarize passes ({os.path.basename(piped) if os.path.exists(piped) else 'hand-built equivalent'}), "
                           f"56x56x64->64, batch {n} per GPU",
