@@ -1439,9 +1439,11 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     if (stg4_ok && try_layout(bn, mt, false, true, false, 3)) return true;
     return try_layout(bn, mt, false, false, false, 0);
   };
-  // n-stationary slices first (256-wide, then 128-wide tiles), then the streamed shapes
-  if (!(wide && shape_nstat(256, 1)) && !shape_nstat(128, 1) && !(wide && shape(256, 1)) && !(tall && shape(128, 2)) &&
-      !shape(128, 1))
+  // one 256-wide n-tile with the whole filter resident first, then n-stationary slices
+  // (256-wide, then 128-wide tiles), then the streamed shapes
+  const bool single_res = wide && (kp.N + 255) / 256 == 1 && shape(256, 1) && kp.b_res;
+  if (!single_res && !(wide && shape_nstat(256, 1)) && !shape_nstat(128, 1) && !(wide && shape(256, 1)) &&
+      !(tall && shape(128, 2)) && !shape(128, 1))
     return cudaErrorNotSupported;
   // idesc: S32 accumulate, signed A/B, both K-major, N = 128, M = 128
   kp.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
