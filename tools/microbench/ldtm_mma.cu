@@ -18,7 +18,7 @@ __device__ __forceinline__ uint64_t desc(uint32_t a, uint32_t lbo, uint32_t sbo,
   return d;
 }
 
-__global__ void k(int nmma, int nld, int N, long long* out) {
+__global__ void k(int nmma, int nld, int N, long long* out, long long* mma_out) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint32_t slot;
   __shared__ __align__(8) uint64_t bar;
@@ -44,13 +44,15 @@ __global__ void k(int nmma, int nld, int N, long long* out) {
     uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((128u >> 4) << 24);
     uint64_t ad = desc(smem_u32(base), 16, 1024, 2), bd = desc(smem_u32(base) + 64 * 1024, 16, 1024, 2);
     go = 1;
+    const long long m0 = clock64();
     for (int it = 0; it < nmma; it++)
       asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tm),
                    "l"(ad), "l"(bd), "r"(idesc), "r"(it));
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
     asm volatile("{\n.reg .pred P1;\nW:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n@P1 bra D;\nbra W;\nD:\n}" ::"r"(smem_u32(&bar)));
+    mma_out[blockIdx.x] = clock64() - m0;
   }
-  if (warp >= 4) {
+  if (warp >= 4 && nld > 0) {
     if (nmma > 0)
       while (go == 0) {
       }
@@ -76,13 +78,14 @@ __global__ void k(int nmma, int nld, int N, long long* out) {
 }
 
 int main() {
-  long long* d;
+  long long *d, *dm;
   cudaMalloc(&d, 4096 * 8);
+  cudaMalloc(&dm, 4096 * 8);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   for (int N : {64, 256})
     for (int nmma : {0, 2000}) {
       const int nld = 200;
-      k<<<148, 256, 100 * 1024>>>(nmma, nld, N, d);
+      k<<<148, 256, 100 * 1024>>>(nmma, nld, N, d, dm);
       cudaError_t e = cudaDeviceSynchronize();
       long long h[148 * 4];
       cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
@@ -90,6 +93,20 @@ int main() {
       for (int i = 0; i < 148 * 4; i++) avg += h[i];
       avg /= 148 * 4;
       printf("N=%3d MMAs running=%s: x16 tcgen05.ld + wait %.1f cycles  %s\n", N, nmma ? "yes" : "no ", avg / nld,
+             e == cudaSuccess ? "" : cudaGetErrorString(e));
+    }
+  // the other direction: MMA issue rate alone vs while four warps drain TMEM continuously
+  for (int N : {64, 128, 256})
+    for (int nld : {0, 100000}) {
+      const int nmma = 4000;
+      k<<<148, 256, 100 * 1024>>>(nmma, nld, N, d, dm);
+      cudaError_t e = cudaDeviceSynchronize();
+      long long h[148];
+      cudaMemcpy(h, dm, sizeof(h), cudaMemcpyDeviceToHost);
+      double avg = 0;
+      for (int i = 0; i < 148; i++) avg += h[i];
+      avg /= 148;
+      printf("N=%3d TMEM loads running=%s: %.1f cycles per MMA  %s\n", N, nld ? "yes" : "no ", avg / nmma,
              e == cudaSuccess ? "" : cudaGetErrorString(e));
     }
 }
