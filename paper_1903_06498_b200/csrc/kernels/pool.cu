@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "../kernels.hpp"
 
@@ -128,6 +129,83 @@ __global__ void __launch_bounds__(256) pool_kernel(const std::uint8_t* __restric
   }
 }
 
+// 3x3 / stride-2 windows (the ResNet stem pool): one thread folds a horizontal PAIR of output
+// pixels (y0, y0 + 1) of one channel vector; their windows share the middle column, so 15
+// vector loads (all in flight) serve 2 outputs instead of 18 -- a sixth less L1/L2 traffic.
+template <int KIND, bool MAX, typename IDX>
+__global__ void __launch_bounds__(256) pool_pair_kernel(const std::uint8_t* __restrict__ in, std::uint8_t* __restrict__ out,
+                                                        const PoolArgs p) {
+  const IDX CV = static_cast<IDX>(p.CV), W2 = static_cast<IDX>((p.W + 1) / 2), H = static_cast<IDX>(p.H);
+  const IDX total = static_cast<IDX>(p.N) * H * W2 * CV;
+  for (IDX g = blockIdx.x * static_cast<IDX>(blockDim.x) + threadIdx.x; g < total;
+       g += static_cast<IDX>(gridDim.x) * blockDim.x) {
+    const IDX q0 = g / CV, cv = g - q0 * CV;
+    const IDX q1 = q0 / W2;
+    const int y0 = 2 * static_cast<int>(q0 - q1 * W2);
+    const IDX n = q1 / H;
+    const int x = static_cast<int>(q1 - n * H);
+    const bool two = y0 + 1 < p.W;
+    uint4* o0 = reinterpret_cast<uint4*>(out + p.o0 + p.o_n * n + p.o_x * x + p.o_y * y0 + cv * 16);
+    uint4* o1 = reinterpret_cast<uint4*>(reinterpret_cast<std::uint8_t*>(o0) + p.o_y);
+    uint4 acc[2] = {p.fresh ? make_uint4(p.init, p.init, p.init, p.init) : *o0,
+                    p.fresh || !two ? make_uint4(p.init, p.init, p.init, p.init) : *o1};
+    std::uint32_t ev[2][4], od[2][4];
+    if (KIND == kI8) {
+#pragma unroll
+      for (int a = 0; a < 2; a++) {
+        const std::uint32_t a4[4] = {acc[a].x, acc[a].y, acc[a].z, acc[a].w};
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          ev[a][q] = sx_even(a4[q]);
+          od[a][q] = sx_odd(a4[q]);
+        }
+      }
+    }
+    auto fold_tap = [&](int a, const uint4 t) {
+      if (KIND == kI8) {
+        const std::uint32_t t4[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          ev[a][q] = mm16x2<MAX>(ev[a][q], sx_even(t4[q]));
+          od[a][q] = mm16x2<MAX>(od[a][q], sx_odd(t4[q]));
+        }
+      } else {
+        acc[a].x = fold<KIND, MAX>(acc[a].x, t.x);
+        acc[a].y = fold<KIND, MAX>(acc[a].y, t.y);
+        acc[a].z = fold<KIND, MAX>(acc[a].z, t.z);
+        acc[a].w = fold<KIND, MAX>(acc[a].w, t.w);
+      }
+    };
+    const std::uint8_t* ib = in + p.a0 + p.a_n * n + cv * 16;
+    const int u0 = 2 * x, v0 = 2 * y0;
+    uint4 t[15];
+    bool ok[15];
+#pragma unroll
+    for (int k = 0; k < 15; k++) {
+      const int u = u0 + k / 5, v = v0 + k % 5;
+      ok[k] = u >= p.u_lo && u <= p.u_hi && v >= p.v_lo && v <= p.v_hi && (k % 5 < 3 || two);
+      t[k] = ok[k] ? __ldg(reinterpret_cast<const uint4*>(ib + p.a_x * u + p.a_y * v)) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < 15; k++) {
+      if (!ok[k]) continue;
+      if (k % 5 <= 2) fold_tap(0, t[k]);
+      if (k % 5 >= 2) fold_tap(1, t[k]);
+    }
+#pragma unroll
+    for (int a = 0; a < 2; a++) {
+      if (KIND == kI8) {
+        std::uint32_t r[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) r[q] = __byte_perm(ev[a][q], od[a][q], 0x6240);
+        acc[a] = make_uint4(r[0], r[1], r[2], r[3]);
+      }
+    }
+    *o0 = acc[0];
+    if (two) *o1 = acc[1];
+  }
+}
+
 int esize(int kind) { return kind == kI8 ? 1 : kind == kI16 ? 2 : 4; }
 
 }  // namespace
@@ -178,6 +256,23 @@ cudaError_t launch_pool(const PoolPlan& pp, const void* in, void* out, cudaStrea
   auto* o = static_cast<std::uint8_t*>(out);
   const bool mx = pp.agg == static_cast<int>(Agg::Max);
   const bool small = total < (1ll << 31) - 148ll * 16 * 256;
+  if (pp.R == 3 && pp.S == 3 && pp.sx == 2 && pp.sy == 2 && !std::getenv("SB_POOL_SINGLE")) {
+    const long long pairs = a.N * a.H * ((a.W + 1) / 2) * a.CV;
+    const int pgrid = static_cast<int>(std::max<long long>(1, std::min<long long>((pairs + 255) / 256, 148 * 16)));
+    const auto* i = static_cast<const std::uint8_t*>(in);
+    auto* o = static_cast<std::uint8_t*>(out);
+    const bool mx = pp.agg == static_cast<int>(Agg::Max);
+#define SB_POOL2(K, M)                                                                      \
+  (small ? pool_pair_kernel<K, M, int><<<pgrid, 256, 0, s>>>(i, o, a)                      \
+         : pool_pair_kernel<K, M, long long><<<pgrid, 256, 0, s>>>(i, o, a))
+    switch (pp.kind) {
+      case kI8: mx ? SB_POOL2(kI8, true) : SB_POOL2(kI8, false); break;
+      case kI16: mx ? SB_POOL2(kI16, true) : SB_POOL2(kI16, false); break;
+      default: mx ? SB_POOL2(kI32, true) : SB_POOL2(kI32, false); break;
+    }
+#undef SB_POOL2
+    return cudaGetLastError();
+  }
 #define SB_POOL(K, M)                                                                      \
   (small ? pool_kernel<K, M, int><<<grid, 256, 0, s>>>(i, o, a)                           \
          : pool_kernel<K, M, long long><<<grid, 256, 0, s>>>(i, o, a))
