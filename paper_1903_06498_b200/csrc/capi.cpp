@@ -155,6 +155,9 @@ struct sb_context {
     for (auto& e : join_events)
       if (e) cudaEventDestroy(e);
     if (own) cudaStreamDestroy(own);
+    // teardown is best effort: a failing destroy must not surface later as the "last error"
+    // of an unrelated launch on this thread (non-sticky errors are consumed here)
+    cudaGetLastError();
   }
 };
 
@@ -960,6 +963,7 @@ int sb_execute_device(sb_context* ctx, sb_program* p, const sb_device_buffer* bu
     std::lock_guard<std::recursive_mutex> lock(ctx->mu);
     check_opts(opts);
     cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaGetLastError();  // a stale non-sticky error of an unrelated earlier runtime call is not ours
     const auto& prog = p->prog;
     std::vector<int> slot(prog.buffers.size(), -1);
     std::vector<int> flags(n);
@@ -1005,6 +1009,8 @@ namespace {
 int execute_host(sb_context* ctx, sb_program* p, sb_host_buffer* bufs, int n, const sb_exec_options* opts, bool async) {
   return guarded([&] {
     std::lock_guard<std::recursive_mutex> lock(ctx->mu);
+    cudaSetDevice(ctx->device);
+    cudaGetLastError();   // a stale non-sticky error of an unrelated earlier runtime call is not ours
     ctx->window.clear();  // host copies serialize the stream
     if (async)
       for (int i = 0; i < n; i++)
