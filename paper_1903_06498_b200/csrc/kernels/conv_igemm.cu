@@ -419,12 +419,14 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (p.res_mma) {
-    // identity B operand, K-major 128 x 128 with the 128B swizzle: row n has its 1 at byte n
+    // identity B operand 32 x 32, K-major without swizzle: core matrices of 8 rows x 16 bytes,
+    // the two along K 128 bytes apart (LBO), the four 8-row groups 256 bytes apart (SBO):
+    // byte (n, k) at (n / 8) 256 + (k / 16) 128 + (n % 8) 16 + k % 16, one where n == k
     uint4* id = reinterpret_cast<uint4*>(base + p.ident_off);
-    for (int u = threadIdx.x; u < 1024; u += blockDim.x) {
-      const int n = u >> 3, unit = (u & 7) ^ (n & 7);  // logical 16-byte unit of this physical slot
+    for (int u = threadIdx.x; u < 64; u += blockDim.x) {
+      const int grp = u >> 4, kc = (u >> 3) & 1, r = u & 7, n = grp * 8 + r;
       std::uint32_t w[4] = {0, 0, 0, 0};
-      if (unit == (n >> 4)) w[(n & 15) >> 2] = 1u << (8 * (n & 3));
+      if ((n >> 4) == kc) w[(n & 15) >> 2] = 1u << (8 * (n & 3));
       id[u] = make_uint4(w[0], w[1], w[2], w[3]);
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -683,22 +685,23 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
         }
       }
       if (p.res_mma) {
-        // + residual: D[:, 128 hh + n] += R[:, 128 hh + k] * I[n, k], four K = 32 steps per half
+        // + residual: D[:, 32 g + n] += R[:, 32 g + k] * I32[n, k], one N = 32 instruction per
+        // 32 output channels (the residual's K = 32 chunk g against the 32 x 32 identity)
         const int rb = p.res1 ? 0 : acc;
         mbar_wait(&rfull[rb], p.res1 ? iter & 1 : (iter >> 1) & 1);
         tc_fence_after();
-        const int halves = min(p.bn, nrem + 127) / 128;
+        const int groups = min(p.bn, nrem + 31) / 32;
         const std::uint32_t hi128 = (1024u >> 4) | (1u << 14) | (2u << 29);
-        const std::uint32_t id128 = (p.idesc & ~(0x3Fu << 17)) | ((128u >> 3) << 17);
+        const std::uint32_t id32 = (p.idesc & ~(0x3Fu << 17)) | ((32u >> 3) << 17);
         const std::uint32_t ra = smem_u32(base + p.res_off + rb * TM * p.bn), ib = smem_u32(base + p.ident_off);
+        const std::uint32_t ib_lo = (ib >> 4) | ((128u >> 4) << 16), ib_hi = (256u >> 4) | (1u << 14);
         const int hcount = (p.bn + 127) / 128;
         for (int sub = 0; sub < p.mt; sub++)
-          for (int hh = 0; hh < halves; hh++)
-#pragma unroll
-            for (int ks = 0; ks < 4; ks++)
-              if (issuer)
-                umma_i8(d + sub * p.bn + 128 * hh, (((ra + (sub * hcount + hh) * 16384) >> 4) | (1u << 16)) + ks * 2,
-                        hi128, ((ib >> 4) | (1u << 16)) + ks * 2, hi128, id128, 1);
+          for (int g = 0; g < groups; g++)
+            if (issuer)
+              umma_i8(d + sub * p.bn + 32 * g,
+                      (((ra + (sub * hcount + (g >> 2)) * 16384) >> 4) | (1u << 16)) + (g & 3) * 2, hi128, ib_lo, ib_hi,
+                      id32, 1);
         if (issuer) umma_commit(&rempty[rb]);
         __syncwarp();
       }
@@ -1367,7 +1370,7 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     const int res = kp.epi_res ? (kp.res1 ? 1 : 2) * BM * mt * bn : 0;
     const int vec = kp.fast_clamp ? 2 * kVecBytes : kp.epi_vec ? kVecBytes : 0;
     const int tab = kp.gather ? (kp.kblocks * kp.bk * 6 + 15) / 16 * 16 : 0;
-    const int ident = kp.res_mma ? 16384 : 0;
+    const int ident = kp.res_mma ? 1024 : 0;
     // the filter stays resident when there is one n-tile and it is small (<= 96 KB)
     kp.bn_box = kp.N <= 64 ? 64 : bn;
     const int bres = (kp.tiles_n == 1 || kp.nstat) && kp.kblocks * kp.bn_box * g.bk <= 96 * 1024 &&
@@ -1428,17 +1431,22 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     return layout(bn, mt) && kp.stages >= min_stages;
   };
   const int max_tn = std::getenv("SB_IG_NSTAT8") ? 8 : 16;
+  // the second staging buffer per epilogue group (stg4) only when the ring keeps >= 3 stages
+  // AND as many k-blocks per stage as without it (fewer, larger handshakes win: measured)
+  auto pick = [&](int bn, int mt, bool nstat, bool res1, int min_stages) {
+    if (!try_layout(bn, mt, nstat, false, res1, min_stages)) return false;
+    const int kpb2 = kp.kpb;
+    if (stg4_ok && try_layout(bn, mt, nstat, true, res1, 3) && (kp.kpb >= kpb2 || std::getenv("SB_IG_STG4_ANY")))
+      return true;
+    return try_layout(bn, mt, nstat, false, res1, min_stages);
+  };
   auto shape_nstat = [&](int bn, int mt) {
     const int tn = (kp.N + bn - 1) / bn;
     if (!nstat_ok || tn < 2 || tn > max_tn) return false;
-    if (stg4_ok && try_layout(bn, mt, true, true, false, 3)) return true;
-    if (try_layout(bn, mt, true, false, false, 2)) return true;
-    return kp.res_mma && try_layout(bn, mt, true, false, true, 2);
+    if (pick(bn, mt, true, false, 2)) return true;
+    return kp.res_mma && pick(bn, mt, true, true, 2);
   };
-  auto shape = [&](int bn, int mt) {
-    if (stg4_ok && try_layout(bn, mt, false, true, false, 3)) return true;
-    return try_layout(bn, mt, false, false, false, 0);
-  };
+  auto shape = [&](int bn, int mt) { return pick(bn, mt, false, false, 0); };
   // one 256-wide n-tile with the whole filter resident first, then n-stationary slices
   // (256-wide, then 128-wide tiles), then the streamed shapes
   const bool single_res = wide && (kp.N + 255) / 256 == 1 && shape(256, 1) && kp.b_res;

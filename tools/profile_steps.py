@@ -28,6 +28,8 @@ def program_text(which, batch):
         text = W.conv_fused(batch, 7, 7, 512, 2048, 1, 1, 1, 0, residual=True)
     elif which == "s3_1x1":
         text = W.conv_fused(batch, 14, 14, 256, 1024, 1, 1, 1, 0, residual=True)
+    elif which == "s2_3x3":
+        text = W.conv_fused(batch, 28, 28, 128, 128, 3, 3, 1, 1)
     elif which == "l24":
         text = W.conv_fused(batch, 28, 28, 512, 1024, 1, 1, 2, 0, relu=False)
     elif which == "l25":
