@@ -35,6 +35,7 @@
 // Development aid (make trace): per-tile timestamps of CTA 0 printed after each launch.
 #ifdef SB_TILE_TRACE
 #define EPI_EXP p.exp
+#define EXPB(b) (p.exp & (b))
 #include <cstdio>
 #define TILE_STAMP(slot, i) \
   do {                                                                            \
@@ -46,6 +47,7 @@
   } while (0)
 #else
 #define EPI_EXP 0
+#define EXPB(b) 0
 #define STAGE_STAMP(iter, st, k) \
   do {                           \
   } while (0)
@@ -524,12 +526,15 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
             if (issuer) {
               const int img = t / p.band_rpi, u = (t - img * p.band_rpi) * p.band;
               const std::int8_t* src = p.band_src + img * p.band_img + u * p.band_rowb;
+              if (EXPB(1)) mbar_arrive(&full[stage]);  // (trace builds: no A loads)
+              else {
               mbar_expect_tx(&full[stage], static_cast<std::uint32_t>(p.band_bytes));
               asm volatile(
                   "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                       smem_u32(ring + stage * sstride)),
                   "l"(reinterpret_cast<std::uint64_t>(src)), "r"(p.band_bytes), "r"(smem_u32(&full[stage]))
                   : "memory");
+              }
             }
             __syncwarp();
             if (++stage == stages) {
@@ -625,9 +630,6 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
         const std::uint32_t as = stage_a >> 4, bs = stage_b >> 4, hi = p.desc_hi;
         const bool first = kb0 == 0;
 #ifdef SB_TILE_TRACE
-        if (!(p.exp & 2))
-#endif
-#ifdef SB_TILE_TRACE
         if (issuer && p.band && blockIdx.x == 0 && iter == 0 && p.trace && (p.exp & 16)) {
           // debug: the first band stage as the MMA sees it (2 KB) and its descriptor fields
           const long long* src = reinterpret_cast<const long long*>(ring + stage * sstride);
@@ -636,7 +638,8 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
           p.trace[1537] = static_cast<long long>(stage);
         }
 #endif
-        if (issuer && p.strip) {
+        if (EXPB(2)) {  // (trace builds: no MMAs)
+        } else if (issuer && p.strip) {
           // tap (i, j) of sub-tile sub: strip rows 2 sub + i .., shifted by j pixels (64 bytes
           // each); SW64 descriptors, base offset 0 for every 64-byte row shift (conv_tc.cu)
           const std::uint32_t sa0 = (sa >> 4) | (1u << 16);
@@ -920,7 +923,8 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       const int nch = min(p.bn, p.N - n0 + 31) / 32;
       const int c_lo = split || hgroups == 1 ? 0 : (hgroup * nch) >> 1;
       const int c_hi = split || hgroups == 1 ? nch : ((hgroup + 1) * nch) >> 1;
-      if (fast8 && p.epi_pipe) {
+      if (EXPB(64)) {  // (trace builds: no epilogue math)
+      } else if (fast8 && p.epi_pipe) {
         const std::uint32_t tbase = tmem_base + (static_cast<std::uint32_t>(quarter * 32) << 16) +
                                     static_cast<std::uint32_t>(acc * p.mt * p.bn);
         const std::uint32_t vaddr = smem_u32(vec_s + n0), taddr = smem_u32(thr_s + n0);

@@ -16,6 +16,10 @@ CASES = [
     (2, 7, 7, 8, 3, 3, 1, 1, "max", "i16"),
     (1, 10, 6, 4, 3, 3, 2, 1, "min", "i32"),
     (3, 12, 12, 64, 5, 5, 3, 2, "max", "i8"),
+    # 3x3 / stride-2 i8: the row-strip kernel (odd and even sizes, no padding, min)
+    (3, 13, 10, 48, 3, 3, 2, 1, "min", "i8"),
+    (2, 15, 15, 32, 3, 3, 2, 0, "max", "i8"),
+    (5, 40, 38, 16, 3, 3, 2, 1, "max", "i8"),
 ]
 
 

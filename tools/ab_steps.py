@@ -2,7 +2,7 @@
 """In-process A/B of environment switches read at launch time: per-step device times of one
 program (sb_context_set_profile), variants interleaved so box and clock drift hit all alike.
 
-    python tools/ab_steps.py PROG BATCH REPS VAR[=VAL] [VAR...]    ('-' = no switch)
+    python tools/ab_steps.py PROG BATCH REPS VAR[=VAL][+VAR..] ...    ('-' = no switch)
 """
 import os
 import statistics
@@ -34,13 +34,15 @@ def main():
     run = ctx.bind_device(prog, bufs)
 
     def setv(v, on):
+        # one variant = "-" (no switch) or VAR[=VAL] switches joined by "+"
         if v == "-":
             return
-        k, _, val = v.partition("=")
-        if on:
-            os.environ[k] = val or "1"
-        else:
-            os.environ.pop(k, None)
+        for one in v.split("+"):
+            k, _, val = one.partition("=")
+            if on:
+                os.environ[k] = val or "1"
+            else:
+                os.environ.pop(k, None)
 
     res = {v: {} for v in variants}
     with torch.cuda.stream(s):

@@ -1,0 +1,147 @@
+// Per-tile cadence of the conv kernels' MMA warp, one CTA per SM: a tile = NM tcgen05.mma
+// kind::i8 (M = 128, N) into accumulator acc = tile & 1, then tcgen05.commit -> tfull[acc].
+// mode 0: MMAs + commits only; mode 1: + wait tempty[acc] (released by an epilogue warp that
+// waits tfull[acc] and arrives at once); mode 2: + a 4-stage full/empty ring fed by a producer
+// warp that only arrives; mode 3: mode 2 + the epilogue warp holds the accumulator HOLD cycles.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -o mma_cadence mma_cadence.cu && ./mma_cadence
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint64_t desc(uint32_t a, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  return (uint64_t)((a >> 4) & 0x3FFF) | (uint64_t)((lbo >> 4) & 0x3FFF) << 16 | (uint64_t)((sbo >> 4) & 0x3FFF) << 32 |
+         (uint64_t)1 << 46 | (uint64_t)layout << 61;
+}
+__device__ __forceinline__ void wait(uint64_t* b, uint32_t ph) {
+  asm volatile(
+      "{\n.reg .pred P1;\nWAIT_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n@P1 bra DONE_%=;\nbra "
+      "WAIT_%=;\nDONE_%=:\n}" ::"r"(smem_u32(b)),
+      "r"(ph), "r"(0x989680u)
+      : "memory");
+}
+__device__ __forceinline__ void arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
+template <int NM>
+__global__ void k(int tiles, int N, int mode, int hold, int var, long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint32_t slot;
+  __shared__ __align__(8) uint64_t tfull[2], tempty[2], full[4], empty[4];
+  uint8_t* base = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
+  for (int i = threadIdx.x; i < 100 * 1024; i += blockDim.x) base[i] = (uint8_t)(i * 7);
+  const int warp = threadIdx.x / 32;
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&slot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; i++) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tfull[i])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tempty[i])));
+    }
+    for (int i = 0; i < 4; i++) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[i])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&empty[i])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tm = slot;
+  const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((128u >> 4) << 24);
+  long long t0 = clock64();
+  if (warp == 0 && mode >= 2) {
+    int s = 0;
+    uint32_t ph = 0;
+    for (int t = 0; t < tiles; t++) {
+      wait(&empty[s], ph ^ 1);
+      arrive(&full[s]);
+      if (++s == 4) s = 0, ph ^= 1;
+    }
+  } else if (warp == 1) {
+    int s = 0;
+    uint32_t ph = 0;
+    const uint32_t a = smem_u32(base), b = smem_u32(base) + 48 * 1024;
+    uint64_t ads[NM], bds[NM];
+#pragma unroll
+    for (int q = 0; q < NM; q++) {
+      ads[q] = desc(a + (q >> 1) * 2048 + ((var & 32) ? 0 : (q & 1) * 32), 16, 128, 0);
+      bds[q] = desc(b + (q >> 1) * 4096 + ((var & 16) ? 0 : (q & 1) * 32), 16, 1024, 2);
+    }
+    for (int t = 0; t < tiles; t++) {
+      const int acc = t & 1;
+      if (mode >= 1) wait(&tempty[acc], ((t >> 1) & 1) ^ 1);
+      if (mode >= 2) wait(&full[s], ph);
+      if (!(var & 64)) asm volatile("tcgen05.fence::after_thread_sync;");
+      if (threadIdx.x == 32) {
+        // variant bits: 1 precomputed descriptors, 2 no per-tile commit, 4 one accumulator,
+        // 8 always accumulate, 16 (with 1) B k-steps without the +32 B start offset, 32 the same for A,
+        // 64 no tcgen05.fence::after_thread_sync per tile, 128 no __syncwarp per tile
+        const uint32_t dcol = (var & 4) ? tm : tm + acc * 256;
+#pragma unroll
+        for (int q = 0; q < NM; q++) {
+          const uint64_t ad = (var & 1) ? ads[q] : desc(a + (q >> 1) * 2048 + (q & 1) * 32, 16, 128, 0);
+          const uint64_t bd = (var & 1) ? bds[q] : desc(b + (q >> 1) * 4096 + (q & 1) * 32, 16, 1024, 2);
+          asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(
+                           dcol),
+                       "l"(ad), "l"(bd), "r"(idesc), "r"((var & 8) ? 1 : q));
+        }
+        if (mode >= 2) commit(&empty[s]);
+        if (!(var & 2) || t == tiles - 1) commit(&tfull[acc]);
+      }
+      if (!(var & 128)) __syncwarp();
+      if (mode >= 2 && ++s == 4) s = 0, ph ^= 1;
+    }
+    if (threadIdx.x == 32) {
+      wait(&tfull[(tiles - 1) & 1], (var & 2) ? 0 : ((tiles - 1) >> 1) & 1);
+      out[blockIdx.x] = clock64() - t0;
+    }
+  } else if (warp == 2 && mode >= 1) {
+    for (int t = 0; t < tiles; t++) {
+      const int acc = t & 1;
+      wait(&tfull[acc], (t >> 1) & 1);
+      if (hold) {
+        const long long h0 = clock64();
+        while (clock64() - h0 < hold) {
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      if (threadIdx.x == 64) arrive(&tempty[acc]);
+      __syncwarp();
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(512));
+}
+
+int main(int argc, char** argv) {
+  long long* d;
+  cudaMalloc(&d, 1024 * 8);
+  cudaFuncSetAttribute(k<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
+  cudaFuncSetAttribute(k<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
+  // one configuration per process (argv: NM N mode), so a fault names its configuration
+  const int nm = argc > 1 ? atoi(argv[1]) : 10, N = argc > 2 ? atoi(argv[2]) : 128, mode = argc > 3 ? atoi(argv[3]) : 0,
+            var = argc > 4 ? atoi(argv[4]) : 0;
+  const int tiles = 2000, hold = mode == 3 ? 1000 : 0;
+  cudaMemset(d, 0, 1024 * 8);
+  if (nm == 10) k<10><<<148, 96, 110 * 1024>>>(tiles, N, mode, hold, var, d);
+  else k<4><<<148, 96, 110 * 1024>>>(tiles, N, mode, hold, var, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h[148];
+  cudaMemcpy(h, d, 148 * 8, cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < 148; i++) avg += h[i];
+  avg /= 148;
+  const double ideal = nm * (N == 64 ? 48.0 : N == 128 ? 64.0 : 128.0);
+  printf("NM=%2d N=%3d mode %d var %2d: %7.1f cycles/tile (ideal %5.0f) %s\n", nm, N, mode, var, avg / tiles, ideal,
+         e == cudaSuccess ? "" : cudaGetErrorString(e));
+}
