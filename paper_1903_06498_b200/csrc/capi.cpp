@@ -447,12 +447,16 @@ void run_plan(sb_context* ctx, const Compiled* c, const std::vector<void*>& root
       } else if (l.conv.packed && l.conv.fold_x) {
         // phase-folded small-channel conv: fold the input and the filter, then the stride-1
         // im2col conv over the folded copy (packed_view)
+        // (band_raw: the conv's producer warps fold the raw rows themselves)
         void* fa = ptr_of(l.conv.pack_a);
         void* pb = ptr_of(l.conv.pack_b);
-        cuda_check(sb::launch_conv_fold(l.conv, a.a, fa, ctx->stream), "conv_fold");
+        if (!l.conv.band_raw) {
+          cuda_check(sb::launch_conv_fold(l.conv, a.a, fa, ctx->stream), "conv_fold");
+          ctx->launches++;
+          a.a = fa;
+        }
         cuda_check(sb::launch_conv_pack_filter(l.conv, a.b, pb, ctx->stream), "conv_pack_filter");
-        ctx->launches += 2;
-        a.a = fa;
+        ctx->launches++;
         a.b = pb;
         cuda_check(sb::launch_conv_igemm(sb::packed_view(l.conv), a, ctx->stream, ctx->num_sms), "conv_igemm");
       } else if (l.conv.packed) {

@@ -46,8 +46,12 @@
     if (p.trace && blockIdx.x == 0 && (iter) < 32 && (st) < 4) p.trace[640 + ((iter)*4 + (st)) * 3 + (k)] = clock64(); \
   } while (0)
 #else
-#define EPI_EXP 0
-#define EXPB(b) 0
+// (SB_EXP_CONST: compile-time knock-out bits for experiment builds, see tools/exp_build.sh)
+#ifndef SB_EXP_CONST
+#define SB_EXP_CONST 0
+#endif
+#define EPI_EXP SB_EXP_CONST
+#define EXPB(b) (SB_EXP_CONST & (b))
 #define STAGE_STAMP(iter, st, k) \
   do {                           \
   } while (0)
@@ -59,6 +63,7 @@
 namespace sb {
 namespace {
 
+constexpr int kRawStages = 4;        // band_raw: raw-row stages in flight (cp.async groups)
 constexpr int kThreadsGather = 448;  // + 8 warps gathering A tiles (small-channel convs), 2 per row
 constexpr int BM = 128, BN = 128;
 constexpr int kRingBytes = 192 * 1024;  // A+B stage ring (cap)
@@ -122,6 +127,15 @@ struct IgKParams {
   long long band_rowb, band_img;
   const std::int8_t* band_src;
   std::uint32_t a_hi;
+  // band_raw (ConvPlan::band_raw): no folded copy; four producer warps cp.async each band's
+  // 2 * kblocks raw input rows (raw_chunks 16-byte chunks of the valid columns, zero-filled
+  // outside [r_ulo, r_uhi]) into a ring of kRawStages raw stages (raw_rp bytes per row, the
+  // valid bytes from raw_col0, zero padding either side written once), then build the band's
+  // folded rows from them: folded pixel (j, V) = raw rows 2j, 2j+1, 6 bytes each from window
+  // column 2V, then 4 zero bytes
+  int band_raw, raw_rp, raw_col0, raw_chunks, raw_stage, raw_off, raw_fv;
+  long long r_an, r_ax, r_a0;
+  int r_ulo, r_uhi, r_vlo;
   // strip mode (stride-1 3x3 over 64 channels into a fresh i8 activation): tile t = image
   // t / strip_tx, output rows strip_rows * (t % strip_tx) .. (mt sub-tiles of 2 rows x 64-pixel
   // pitch); A = ONE haloed strip (rows + 2, 64 pixels, 64 channels, SW64 4-D TMA box, zero
@@ -280,7 +294,7 @@ __device__ __forceinline__ uint4 lds128(std::uint32_t a) {
 template <bool THR, bool RES>
 __device__ __forceinline__ void epi8_half(const std::uint32_t (&v)[16], int sub, int h, int hf, std::uint32_t vaddr,
                                           std::uint32_t taddr, std::uint32_t raddr, std::uint32_t saddr, int hcnt,
-                                          int hsh, int sw, std::uint32_t lo32u, std::int32_t lo8) {
+                                          int hsh, int sw, std::uint32_t lo32u, std::int32_t lo8, int exp = 0) {
   // 16 KB staging box and swizzled 16-byte unit of this half: 128-byte rows hold 1 << hsh
   // 32-column chunks (hsh = 2; band mode with 64 channels: hsh = 1, one band row per box)
   const std::uint32_t box = (sub * hcnt + (h >> hsh)) * 16384;
@@ -292,7 +306,7 @@ __device__ __forceinline__ void epi8_half(const std::uint32_t (&v)[16], int sub,
 #pragma unroll
   for (int q4 = 0; q4 < 4; q4++) {
     const int col = h * 32 + hf * 16 + 4 * q4;
-    const uint4 b4 = lds128(vaddr + col * 4);
+    const uint4 b4 = (exp & 1024) ? make_uint4(col, col, col, col) : lds128(vaddr + col * 4);  // (trace: no vector loads)
     const std::uint32_t bq[4] = {b4.x, b4.y, b4.z, b4.w};
     uint4 t4 = make_uint4(0, 0, 0, 0);
     if (THR) t4 = lds128(taddr + col * 4);
@@ -311,6 +325,9 @@ __device__ __forceinline__ void epi8_half(const std::uint32_t (&v)[16], int sub,
     }
     w[q4] = __byte_perm(__byte_perm(o[0], o[1], 0x0040), __byte_perm(o[2], o[3], 0x0040), 0x5410);
   }
+  if (exp & 512) {  // (trace: no staging stores; keep the values live)
+    if ((w[0] ^ w[1] ^ w[2] ^ w[3]) == 0x12345678u) asm volatile("st.shared.b32 [%0], %1;" ::"r"(saddr), "r"(w[0]));
+  } else
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(saddr + box + unit), "r"(w[0]), "r"(w[1]), "r"(w[2]),
                "r"(w[3]));
 }
@@ -332,6 +349,9 @@ __device__ __forceinline__ void epi8_pipelined(std::uint32_t tbase, int bn, int 
   if (total <= 0) return;
   std::uint32_t va[16], vb[16];
   // chunk (sub, h): half 0 in va, half 1 in vb; the next chunk's column advanced incrementally
+  if (exp & 256) {  // (trace: no TMEM loads)
+    for (int q = 0; q < 16; q++) va[q] = vb[q] = q * 977u;
+  } else
   tmem_ld16_async(tbase + c_lo * 32, va);
   int sub = 0, h = c_lo;
   for (int c = 0; c < total; c++) {
@@ -341,12 +361,16 @@ __device__ __forceinline__ void epi8_pipelined(std::uint32_t tbase, int bn, int 
       nsub++;
     }
     const std::uint32_t col = tbase + sub * bn + h * 32;
-    tmem_wait_ld16(va);
-    tmem_ld16_async(col + 16, vb);
-    epi8_half<THR, RES>(va, sub, h, 0, vaddr, taddr, raddr, saddr, hcnt, hsh, sw, lo32u, lo8);
-    tmem_wait_ld16(vb);
-    if (c + 1 < total) tmem_ld16_async(tbase + nsub * bn + nh * 32, va);
-    epi8_half<THR, RES>(vb, sub, h, 1, vaddr, taddr, raddr, saddr, hcnt, hsh, sw, lo32u, lo8);
+    if (!(exp & 256)) {
+      tmem_wait_ld16(va);
+      tmem_ld16_async(col + 16, vb);
+    }
+    epi8_half<THR, RES>(va, sub, h, 0, vaddr, taddr, raddr, saddr, hcnt, hsh, sw, lo32u, lo8, exp);
+    if (!(exp & 256)) {
+      tmem_wait_ld16(vb);
+      if (c + 1 < total) tmem_ld16_async(tbase + nsub * bn + nh * 32, va);
+    }
+    epi8_half<THR, RES>(vb, sub, h, 1, vaddr, taddr, raddr, saddr, hcnt, hsh, sw, lo32u, lo8, exp);
     sub = nsub;
     h = nh;
   }
@@ -456,7 +480,69 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       if (p.pdl_wait && !(p.b_early && do_b && p.b_res)) asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory");
       const int nchains = p.gather ? 1 : 2, chain = p.gather ? 0 : pidx >> 1;
       const int PQ = p.P * p.Q;
-      if (pidx == 4) {
+      if (p.band_raw && pidx != 1) {
+        // band_raw fold producers: warps pidx 0, 2, 3, 4 (128 threads, named barrier 5)
+        const int tt = (pidx == 0 ? 0 : pidx - 1) * 32 + lane;
+        std::uint8_t* raw = base + p.raw_off;
+        const int rrows = 2 * p.kblocks, rp = p.raw_rp, c16 = p.raw_rp / 16;
+        auto tbar = [] { asm volatile("bar.sync 5, 128;" ::: "memory"); };
+        // padding bytes of every raw row (outside the copied chunks): zero once
+        for (int i = tt; i < kRawStages * rrows * c16; i += 128) {
+          const int r = i / c16, b = (i - r * c16) * 16;
+          const int rs = r / rrows;
+          if (b < p.raw_col0 || b >= p.raw_col0 + p.raw_chunks * 16)
+            *reinterpret_cast<uint4*>(raw + rs * p.raw_stage + (r - rs * rrows) * rp + b) = make_uint4(0, 0, 0, 0);
+        }
+        // copy role: thread tt owns chunk ch0 of rows r0, r0 + rstep, ... (no per-chunk division)
+        const int rstep = 128 / p.raw_chunks, r0 = tt / p.raw_chunks, ch0 = tt - r0 * p.raw_chunks;
+        auto issue = [&](int k) {  // raw rows of this CTA's k-th tile into raw stage k % kRawStages
+          const int t = static_cast<int>(blockIdx.x) + k * static_cast<int>(gridDim.x);
+          if (t < tiles && r0 < rstep && !EXPB(65536)) {
+            const int img = t / p.band_rpi, U0 = (t - img * p.band_rpi) * p.band;
+            const std::uint32_t dst0 = smem_u32(raw + (k % kRawStages) * p.raw_stage) + p.raw_col0 + ch0 * 16;
+            const std::int8_t* src0 = p.band_src + p.r_a0 + p.r_an * img + 3ll * p.r_vlo + ch0 * 16;
+            for (int r = r0; r < rrows; r += rstep) {
+              const int u = 2 * U0 + r;
+              const bool ok = u >= p.r_ulo && u <= p.r_uhi;
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst0 + r * rp),
+                           "l"(src0 + p.r_ax * (ok ? u : p.r_ulo)), "r"(ok ? 16 : 0)
+                           : "memory");
+            }
+          }
+          asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        for (int k = 0; k < kRawStages - 1; k++) issue(k);
+        int stage = 0;
+        std::uint32_t phase = 0;
+        const int s0 = p.raw_col0 - 3 * p.r_vlo;
+        for (int k = 0, t = blockIdx.x; t < tiles; k++, t += gridDim.x) {
+          issue(k + kRawStages - 1);
+          asm volatile("cp.async.wait_group %0;" ::"n"(kRawStages - 1) : "memory");
+          tbar();  // tile k's raw rows have landed (every thread's chunks)
+          mbar_wait(&empty[stage], phase ^ 1);
+          const std::uint32_t rs = smem_u32(raw + (k % kRawStages) * p.raw_stage);
+          const std::uint32_t dst = smem_u32(ring + stage * sstride);
+          for (int j = 0; j < p.kblocks && !EXPB(32768); j++)
+          for (int V = tt; V < p.raw_fv; V += 128) {
+            const std::uint32_t a = rs + 2 * j * rp + s0 + 6 * V, a4 = a & ~3u, sh = (a & 3u) * 8;
+            const std::uint32_t x0 = lds32(a4), x1 = lds32(a4 + 4), x2 = lds32(a4 + 8);
+            const std::uint32_t y0 = lds32(a4 + rp), y1 = lds32(a4 + rp + 4), y2 = lds32(a4 + rp + 8);
+            const std::uint32_t lo0 = __funnelshift_r(x0, x1, sh), hi0 = __funnelshift_r(x1, x2, sh);
+            const std::uint32_t lo1 = __funnelshift_r(y0, y1, sh), hi1 = __funnelshift_r(y1, y2, sh);
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst + j * static_cast<std::uint32_t>(p.band_rowb) + V * 16),
+                         "r"(lo0), "r"((hi0 & 0xFFFFu) | (lo1 << 16)), "r"((lo1 >> 16) | (hi1 << 16)), "r"(0u)
+                         : "memory");
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
+          tbar();
+          if (tt == 0) mbar_arrive(&full[stage]);
+          if (++stage == stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+      } else if (pidx == 4) {
         // residual tiles for the tensor-core add, double-buffered by tile parity
         const int res_buf = TM * p.bn, hcount = (p.bn + 127) / 128;
         int it = 0;
@@ -655,10 +741,12 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
                           (i | j | ks) ? 1u : 0u);
           }
         } else if (issuer && p.band) {
-          const std::uint32_t rs = static_cast<std::uint32_t>(p.band_rowb >> 4);
+          const std::uint32_t rs = EXPB(8192) ? 128u : static_cast<std::uint32_t>(p.band_rowb >> 4);  // (8192: aligned rows)
           // A descriptor low word: start | 16-byte stride between core matrices along K (a_hi)
           const std::uint32_t ab = (sa >> 4) | (1u << 16);
-          if (p.kblocks == 5 && ksteps == 2) issue_band<5, 2>(d, ab, rs, p.a_hi, b0, bs, hi, idesc);
+          if (EXPB(4096)) issue_band<5, 2>(d, ab, rs, (128u >> 4) | (1u << 14) | (2u << 29), b0, bs, hi, idesc);  // (A as SW128)
+          else if (EXPB(16384)) issue_band<5, 2>(d, ab, rs, p.a_hi, ab, rs, p.a_hi, idesc);  // (B = A's layout)
+          else if (p.kblocks == 5 && ksteps == 2) issue_band<5, 2>(d, ab, rs, p.a_hi, b0, bs, hi, idesc);
           else
             for (int j = 0; j < p.kblocks; j++)
               for (int ks = 0; ks < ksteps; ks++)
@@ -1165,7 +1253,7 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
           } else if (p.band) {
             // (k, row of the band, pixel, band index): pixels past the row width are clipped
             // one 16 KB box per band row
-            for (int hh = 0; hh < p.band; hh++)
+            for (int hh = 0; hh < p.band && !EXPB(2048); hh++)
               asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
                                reinterpret_cast<std::uint64_t>(&cmap)),
                            "r"(smem_u32(scur + hh * 16384)), "r"(0), "r"(hh), "r"(0), "r"(t)
@@ -1241,7 +1329,9 @@ bool same(const ConvPlan& x, const ConvPlan& y) {
          x.b_j == y.b_j && x.b_k == y.b_k && x.b0 == y.b0 && x.c_n == y.c_n && x.c_x == y.c_x && x.c_y == y.c_y &&
          x.c0 == y.c0 && x.c_dtype == y.c_dtype && x.fresh_output == y.fresh_output && x.epi == y.epi &&
          x.epi_vec == y.epi_vec && x.epi_lo == y.epi_lo && x.vec_k == y.vec_k && x.vec_c == y.vec_c && x.lo == y.lo &&
-         x.epi_res == y.epi_res && x.res_c0 == y.res_c0 && x.res_pix == y.res_pix;
+         x.epi_res == y.epi_res && x.res_c0 == y.res_c0 && x.res_pix == y.res_pix && x.fold_band == y.fold_band &&
+         x.band_raw == y.band_raw && x.raw_a_n == y.raw_a_n && x.raw_a_x == y.raw_a_x && x.raw_a0 == y.raw_a0 &&
+         x.raw_u_lo == y.raw_u_lo && x.raw_u_hi == y.raw_u_hi && x.raw_v_lo == y.raw_v_lo && x.raw_v_hi == y.raw_v_hi;
 }
 
 int kind_of(DType d) { return d == DType::I8 ? kI8 : d == DType::I16 ? kI16 : kI32; }
@@ -1290,6 +1380,21 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     kp.band_stage = (kp.band_bytes + 1023) / 1024 * 1024;
     kp.band_src = static_cast<const std::int8_t*>(args.a);
     kp.vec_mod = static_cast<int>(cp.K / band);
+    if (cp.band_raw) {
+      kp.band_raw = 1;
+      kp.raw_fv = static_cast<int>(cp.fold_v);
+      kp.raw_chunks = static_cast<int>((cp.raw_v_hi - cp.raw_v_lo + 1) * 3 / 16);
+      kp.raw_col0 = static_cast<int>((3 * cp.raw_v_lo + 15) / 16 * 16);
+      // bytes read per row: up to window column 2 fold_v - 1 plus the 12-byte word window
+      kp.raw_rp = (kp.raw_col0 + 6 * kp.raw_fv + 16 + 15) / 16 * 16;
+      kp.raw_stage = (2 * kp.kblocks * kp.raw_rp + 127) / 128 * 128;
+      kp.r_an = cp.raw_a_n;
+      kp.r_ax = cp.raw_a_x;
+      kp.r_a0 = cp.raw_a0;
+      kp.r_ulo = static_cast<int>(cp.raw_u_lo);
+      kp.r_uhi = static_cast<int>(cp.raw_u_hi);
+      kp.r_vlo = static_cast<int>(cp.raw_v_lo);
+    }
     kp.M = static_cast<int>(cp.N * kp.band_rpi * BM);
     // K-major, no swizzle: core matrices of 8 rows x 16 bytes (rows 16 bytes apart), LBO (low
     // word, 16 bytes) between core matrices along K, SBO (high word, 128 bytes) between 8-row
@@ -1375,6 +1480,7 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     const int vec = kp.fast_clamp ? 2 * kVecBytes : kp.epi_vec ? kVecBytes : 0;
     const int tab = kp.gather ? (kp.kblocks * kp.bk * 6 + 15) / 16 * 16 : 0;
     const int ident = kp.res_mma ? 1024 : 0;
+    const int rawb = kp.band_raw ? kRawStages * kp.raw_stage : 0;
     // the filter stays resident when there is one n-tile and it is small (<= 96 KB)
     kp.bn_box = kp.N <= 64 ? 64 : bn;
     const int bres = (kp.tiles_n == 1 || kp.nstat) && kp.kblocks * kp.bn_box * g.bk <= 96 * 1024 &&
@@ -1383,7 +1489,7 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     kp.b_res = bres ? 1 : 0;
     if (kp.nstat && !bres) return false;
     const int kstage = (BM * mt + (bres ? 0 : kp.bn_box)) * g.bk;  // one k-block's A (+ B)
-    const int avail = std::min(kRingBytes, kSmemMax - 1024 - 512 - stg - res - vec - tab - bres - ident);
+    const int avail = std::min(kRingBytes, kSmemMax - 1024 - 512 - stg - res - vec - tab - bres - ident - rawb);
     // k-blocks per stage: up to 4 while three stages still fit (gather mode: 1)
     kp.kpb = 1;
     if (kp.band || kp.strip) kp.kpb = kp.kblocks;  // one load per tile feeds every k-block
@@ -1412,7 +1518,8 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     ring += ident;
     kp.vec_off = ring + stg + res;
     kp.tab_off = ring + stg + res + vec;
-    kp.bar_off = kp.tab_off + tab;
+    kp.raw_off = kp.tab_off + tab;
+    kp.bar_off = kp.raw_off + rawb;
     kp.smem = 1024 + kp.bar_off + 512;
     return true;
   };
@@ -1925,7 +2032,7 @@ cudaError_t launch_conv_igemm(const ConvPlan& cp, const ConvArgs& args, cudaStre
   int grid = tiles < num_sms ? tiles : num_sms;
   if (kp.nstat) grid = grid / kp.tiles_n * kp.tiles_n;  // CTA c keeps n-tile c % tiles_n
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
-  cfg.blockDim = dim3(64 + 32 * kp.epi_warps + (kp.gather ? 256 : 96 + (kp.res_mma ? 32 : 0)));
+  cfg.blockDim = dim3(64 + 32 * kp.epi_warps + (kp.gather ? 256 : 96 + (kp.res_mma || kp.band_raw ? 32 : 0)));
   cfg.dynamicSmemBytes = static_cast<unsigned>(kp.smem);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];

@@ -859,9 +859,28 @@ void choose_band(Plan* plan, ConvPlan* cp) {
   b.fold_band = 2;
   b.fold_rows = false;
   b.pack_k = (b.fold_r + b.fold_band - 1) * b.fold_cv * b.fold_band;
+  // opt-in (SB_BAND_RAW=1): the fold moves into the conv's producer warps when the raw rows are
+  // 16-byte aligned runs of 3-byte pixels (one cp.async chunk per 16 bytes of a row).  Bit-exact,
+  // but measured slower (stem 568 vs 441 us at b1024 including the separate fold): the copies and
+  // the in-shared-memory transform contend with the N = 128 MMAs for shared-memory bandwidth
+  // (knocking either out recovers ~130-150 us), while the separate fold runs at HBM speed.
+  const std::int64_t row_bytes = (c.v_hi - c.v_lo + 1) * c.a_y;
+  b.band_raw = c.fold_x == 2 && c.fold_y == 2 && c.C == 3 && c.a_y == 3 && c.a_x % 16 == 0 && c.a_n % 16 == 0 &&
+               ((c.a0 + c.a_x * c.u_lo + c.a_y * c.v_lo) % 16 + 16) % 16 == 0 && row_bytes % 16 == 0 &&
+               row_bytes <= 128 * 16 && c.v_lo >= 0 && c.v_lo <= 64 && c.u_lo >= 0 && c.fold_v <= 128 &&
+               std::getenv("SB_BAND_RAW") != nullptr;
+  if (b.band_raw) {
+    b.raw_a_n = c.a_n;
+    b.raw_a_x = c.a_x;
+    b.raw_a0 = c.a0;
+    b.raw_u_lo = c.u_lo;
+    b.raw_u_hi = c.u_hi;
+    b.raw_v_lo = c.v_lo;
+    b.raw_v_hi = c.v_hi;
+  }
   if (conv_igemm_unsupported(b)) return;
   *cp = b;
-  plan->bufs[b.pack_a].elements = b.N * b.fold_u * b.fold_v * b.fold_c + 128 * 16 + 64;
+  plan->bufs[b.pack_a].elements = b.band_raw ? 16 : b.N * b.fold_u * b.fold_v * b.fold_c + 128 * 16 + 64;
   plan->bufs[b.pack_b].elements = b.K * b.pack_k;
 }
 
@@ -1086,7 +1105,9 @@ void match_kernels(Plan* plan, const Program& p, const PlanOptions& opt) {
                                 std::to_string(cp.fold_c) + " bytes per folded pixel), packed to " +
                                 std::to_string(cp.fold_r) + " tap rows x " + std::to_string(cp.fold_cv) +
                                 (cp.fold_band ? ", band tiles of " + std::to_string(cp.fold_band) +
-                                                    " output rows stacked along N (overlapping-row descriptors)"
+                                                    " output rows stacked along N (overlapping-row descriptors)" +
+                                                    (cp.band_raw ? std::string(", folded in the producer warps from the raw rows")
+                                                                 : std::string())
                                               : std::string()));
         else
           plan->notes.push_back("launch " + st.launch.path + ": small-channel conv packed to " +

@@ -174,6 +174,12 @@ struct ConvPlan {
   // output rows stacked along N against a banded filter [fold_r + band - 1][band * K][fold_cv]
   // (block (r, p) = folded tap row r - p): N = band * K columns per MMA instead of K
   std::int64_t fold_band = 0;
+  // band_raw (with fold_band, the 2x2-folded 3-channel stem): no folded copy -- the conv's
+  // producer warps build each band's folded rows in shared memory from the raw input rows
+  // (raw_* = the unfolded input's geometry: a_n, a_x, a0, window [u_lo, u_hi] x [v_lo, v_hi],
+  // 3-byte pixels)
+  bool band_raw = false;
+  std::int64_t raw_a_n = 0, raw_a_x = 0, raw_a0 = 0, raw_u_lo = 0, raw_u_hi = 0, raw_v_lo = 0, raw_v_hi = 0;
 };
 
 // Statement-DAG concurrency (schedule.cpp): independent steps on up to N streams.

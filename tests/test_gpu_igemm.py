@@ -201,6 +201,11 @@ BAND = [
     (2, 256, 250, 3, 64, 7, 7, 2, 3, False),  # 125-pixel rows (junk-row tail reads), no clamp
     (2, 20, 20, 3, 128, 7, 7, 2, 3, True),    # K = 128: N = 256 per instruction, one store per row
     (2, 16, 24, 3, 64, 5, 5, 2, 2, True),     # 3x3 folded taps (4 k-blocks)
+    # rows of whole 16-byte chunks (band_raw-eligible; see test_band_raw_matches_folded)
+    (2, 64, 48, 3, 64, 7, 7, 2, 3, True),
+    (2, 20, 32, 3, 128, 7, 7, 2, 3, True),    # K = 128
+    (2, 16, 32, 3, 64, 5, 5, 2, 2, True),     # 5x5 / pad 2: 4 folded rows, 8 raw rows per band
+    (1, 36, 16, 3, 64, 7, 7, 2, 3, False),    # 8-pixel output rows, no clamp
 ]
 
 
@@ -254,6 +259,24 @@ def test_strip_off_matches(monkeypatch):
     monkeypatch.setenv("SB_IG_NOSTRIP", "1")
     _, _, out_i2c = run(text, seed=9)
     np.testing.assert_array_equal(out_strip["O"], out_i2c["O"])
+
+
+@pytest.mark.parametrize("shape", [(2, 32, 32), (3, 64, 48), (1, 224, 224)], ids=lambda c: "x".join(map(str, c)))
+def test_band_raw_matches_folded(monkeypatch, shape):
+    """band_raw (SB_BAND_RAW=1: the fold inside the conv's producer warps) writes the same bytes
+    as the default band path over a materialised folded copy."""
+    import paper_1903_06498_b200 as sb
+    from paper_1903_06498_b200 import workloads as W
+    N, H, Wd = shape
+    text = W.conv_fused(N, H, Wd, 3, 64, 7, 7, 2, 3)
+    monkeypatch.setenv("SB_BAND_RAW", "1")  # opt-in (measured slower than the separate fold)
+    assert "folded in the producer warps" in sb.parse_program(text).describe_plan()
+    _, _, out_raw = run(text, seed=H)
+    monkeypatch.delenv("SB_BAND_RAW")
+    plan = sb.parse_program(text).describe_plan()
+    assert "band tiles" in plan and "producer warps" not in plan, plan
+    _, _, out_fold = run(text, seed=H)
+    np.testing.assert_array_equal(out_raw["O"], out_fold["O"])
 
 
 def test_band_fold_off_matches(monkeypatch):
