@@ -68,6 +68,9 @@ struct ConvKParams {
   int store_wait;         // loads start at once; the epilogue waits for the predecessor before storing
   int cluster;            // CTAs per thread-block cluster (filter multicast)
   int debug_nofilt;       // timing experiments only
+  int filt_par;           // filter boxes issued by the 8 epilogue warps at kernel start (one TMA
+                          // issue costs a thread ~260 cycles: 9+ boxes from the producer delayed
+                          // the second strip by ~1.5 us)
   int pdl;                // launched with programmatic stream serialization
   int filter_early;       // filter is immutable input: fetch before griddepcontrol.wait
   int epi_pipe;           // TMA-store epilogue software-pipelined over 16-column TMEM loads
@@ -303,6 +306,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tempty[a], 128);
     }
     mbar_init(fready, 1);
+    if (p.filt_par) mbar_expect_tx(fready, p.filt_bytes);  // the single arrival; boxes land later
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -320,6 +324,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   const std::uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) trace_at(p.trace, 49);
+  if (p.filt_par && warp >= 2 && lane == 0) {
+    // filter boxes spread over the epilogue warps (idle until the first accumulator lands)
+    const int e = warp - 2, ne = kThreads / 32 - 2;
+    int idx = 0;
+    for (int i = 0; i < p.R; i++)
+      for (int j = 0; j < p.S; j++)
+        for (int cc = 0; cc < p.chunks; cc++, idx++)
+          if (idx % ne == e)
+            tma_load_4d(smem_u32(fsm) + ((i * p.S + j) * p.chunks + cc) * p.filt_tap_bytes, &fmap, fready, cc * 64, 0,
+                        j, i);
+  }
   // the next kernel in the stream may start its prologue as soon as SMs free up
   // Dependents are released only after this grid's own griddepcontrol.wait returned (then
   // the predecessor has completed), so at most this launch and its successor overlap: the
@@ -366,12 +381,12 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
       };
-      bool filter_issued = false;
+      bool filter_issued = p.filt_par != 0;
       if (p.pdl_wait) {
         // Programmatic dependent launch: this prologue overlapped the previous kernel's tail.
         // An immutable filter (a root `in` buffer nothing in the plan writes) may be fetched
         // before the dependency resolves; the activations only after it.
-        if (p.filter_early) {
+        if (p.filter_early && !filter_issued) {
           load_filter();
           filter_issued = true;
         }
@@ -963,6 +978,11 @@ cudaError_t launch_conv_tc(const ConvPlan& cp, const ConvArgs& args, cudaStream_
   kp.pdl_wait = kp.pdl && args.pdl_mode == kPdlWait ? 1 : 0;
   kp.store_wait = kp.pdl && args.pdl_mode == kPdlLoadEarly ? 1 : 0;
   kp.filter_early = args.b_immutable ? 1 : 0;
+  // (a filter another launch may still be writing keeps the producer's post-wait fetch)
+  kp.filt_par = kp.cluster == 1 && !kp.debug_nofilt && (!kp.pdl_wait || kp.filter_early) &&
+                        !std::getenv("SB_TC_FILT_SERIAL")
+                    ? 1
+                    : 0;  // A/B switch, read per launch
   kp.epi_pipe = kp.tma_out && !kp.st_out && !std::getenv("SB_TC_NOPIPE") ? 1 : 0;  // A/B switch, read per launch
   kp.epi = cp.epi ? 1 : 0;
   kp.epi_vec = cp.epi_vec ? 1 : 0;

@@ -128,12 +128,14 @@ int main(int argc, char** argv) {
   cudaMalloc(&d, 1024 * 8);
   cudaFuncSetAttribute(k<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
   cudaFuncSetAttribute(k<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
+  cudaFuncSetAttribute(k<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
   // one configuration per process (argv: NM N mode), so a fault names its configuration
   const int nm = argc > 1 ? atoi(argv[1]) : 10, N = argc > 2 ? atoi(argv[2]) : 128, mode = argc > 3 ? atoi(argv[3]) : 0,
             var = argc > 4 ? atoi(argv[4]) : 0;
   const int tiles = 2000, hold = mode == 3 ? 1000 : 0;
   cudaMemset(d, 0, 1024 * 8);
   if (nm == 10) k<10><<<148, 96, 110 * 1024>>>(tiles, N, mode, hold, var, d);
+  else if (nm == 8) k<8><<<148, 96, 110 * 1024>>>(tiles, N, mode, hold, var, d);
   else k<4><<<148, 96, 110 * 1024>>>(tiles, N, mode, hold, var, d);
   cudaError_t e = cudaDeviceSynchronize();
   long long h[148];
