@@ -261,18 +261,6 @@ __device__ __forceinline__ void tmem_wait_ld16(std::uint32_t (&v)[16]) {
                : "memory");
 }
 
-// One ring stage's MMAs, fully unrolled (compile-time KPB k-blocks x KS 32-byte k-steps):
-// descriptors advance by constants, so the issue is a straight run of uniform adds + UTCIMMA.
-template <int KPB, int KS>
-__device__ __forceinline__ void issue_stage(std::uint32_t d, std::uint32_t a0, std::uint32_t a_step, std::uint32_t b0,
-                                            std::uint32_t b_step, std::uint32_t hi, std::uint32_t idesc, bool first) {
-#pragma unroll
-  for (int j = 0; j < KPB; j++)
-#pragma unroll
-    for (int ks = 0; ks < KS; ks++)
-      umma_i8(d, a0 + j * a_step + ks * 2, hi, b0 + j * b_step + ks * 2, hi, idesc, (first && j == 0 && ks == 0) ? 0u : 1u);
-}
-
 // i8 TMA-store epilogue of one tile, software-pipelined: chunk c+1's TMEM load is in flight
 // while chunk c is transformed and staged (tcgen05.wait::ld waits for every outstanding load,
 // so the next load is issued right after the wait that makes chunk c valid).  Chunks run over
@@ -374,19 +362,6 @@ __device__ __forceinline__ void epi8_pipelined(std::uint32_t tbase, int bn, int 
     sub = nsub;
     h = nh;
   }
-}
-
-// band mode: KB k-blocks (folded rows) x KS k-steps; A rows overlap (a_hi: no swizzle), B is
-// the resident banded filter (b_hi: its TMA swizzle)
-template <int KB, int KS>
-__device__ __forceinline__ void issue_band(std::uint32_t d, std::uint32_t a0, std::uint32_t a_step, std::uint32_t a_hi,
-                                           std::uint32_t b0, std::uint32_t b_step, std::uint32_t b_hi,
-                                           std::uint32_t idesc) {
-#pragma unroll
-  for (int j = 0; j < KB; j++)
-#pragma unroll
-    for (int ks = 0; ks < KS; ks++)
-      umma_i8(d, a0 + j * a_step + ks * 2, a_hi, b0 + j * b_step + ks * 2, b_hi, idesc, (j == 0 && ks == 0) ? 0u : 1u);
 }
 
 __global__ void __launch_bounds__(kThreadsGather, 1)
@@ -695,6 +670,9 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
       mbar_wait(bfull, 0);
       tc_fence_after();
     }
+    // shared-memory bases as integers once: the per-stage descriptor arithmetic then stays
+    // in uniform registers (no vector-register round trip per MMA)
+    const std::uint32_t ring_s = smem_u32(ring), bres_s = smem_u32(bres);
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, iter++) {
       const int acc = iter & 1;
       mbar_wait(&tempty[acc], ((iter >> 1) & 1) ^ 1);
@@ -710,9 +688,9 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (issuer) STAGE_STAMP(iter, kb0 / p.kpb, 1);
-        const std::uint32_t sa = smem_u32(ring + stage * sstride);
+        const std::uint32_t sa = ring_s + stage * sstride;
         const std::uint32_t a0 = (sa >> 4) | (1u << 16);
-        const std::uint32_t b0 = ((p.b_res ? smem_u32(bres + kb0 * stage_b) : sa + p.kpb * stage_a) >> 4) | (1u << 16);
+        const std::uint32_t b0 = ((p.b_res ? bres_s + kb0 * stage_b : sa + p.kpb * stage_a) >> 4) | (1u << 16);
         const std::uint32_t as = stage_a >> 4, bs = stage_b >> 4, hi = p.desc_hi;
         const bool first = kb0 == 0;
 #ifdef SB_TILE_TRACE
@@ -725,45 +703,47 @@ __global__ void __launch_bounds__(kThreadsGather, 1)
         }
 #endif
         if (EXPB(2)) {  // (trace builds: no MMAs)
-        } else if (issuer && p.strip) {
-          // tap (i, j) of sub-tile sub: strip rows 2 sub + i .., shifted by j pixels (64 bytes
-          // each); SW64 descriptors, base offset 0 for every 64-byte row shift (conv_tc.cu)
-          const std::uint32_t sa0 = (sa >> 4) | (1u << 16);
-          for (int sub = 0; sub < p.mt; sub++) {
-            const std::uint32_t ds = d + sub * p.bn;
-#pragma unroll
-            for (int i = 0; i < 3; i++)
+        } else if (issuer) {
+          // rolled issue: only the innermost k-steps unrolled, descriptors advanced by adds, so
+          // few 64-bit descriptor pairs are live in uniform registers at once (fully unrolled
+          // runs of 16-18 MMAs spilled uniform registers through vector ones: stage-1 3x3
+          // 166 -> 145 us at b1024)
+          if (p.strip) {
+            // tap (i, j) of sub-tile sub: strip rows 2 sub + i .., shifted by j pixels (64 bytes
+            // each); SW64 descriptors, base offset 0 for every 64-byte row shift (conv_tc.cu)
+            const std::uint32_t sa0 = (sa >> 4) | (1u << 16);
+#pragma unroll 1
+            for (int q = 0; q < p.mt * 3; q++) {
+              const int sub = q / 3, i = q - sub * 3;
+              const std::uint32_t ds = d + sub * p.bn, ar = sa0 + (sub * 2 + i) * 256, br = b0 + i * 3 * bs;
 #pragma unroll
               for (int j = 0; j < 3; j++)
 #pragma unroll
                 for (int ks = 0; ks < 2; ks++)
-                  umma_i8(ds, sa0 + ((sub * 2 + i) * 64 + j) * 4 + ks * 2, hi, b0 + (i * 3 + j) * bs + ks * 2, hi, idesc,
-                          (i | j | ks) ? 1u : 0u);
-          }
-        } else if (issuer && p.band) {
-          const std::uint32_t rs = EXPB(8192) ? 128u : static_cast<std::uint32_t>(p.band_rowb >> 4);  // (8192: aligned rows)
-          // A descriptor low word: start | 16-byte stride between core matrices along K (a_hi)
-          const std::uint32_t ab = (sa >> 4) | (1u << 16);
-          if (EXPB(4096)) issue_band<5, 2>(d, ab, rs, (128u >> 4) | (1u << 14) | (2u << 29), b0, bs, hi, idesc);  // (A as SW128)
-          else if (EXPB(16384)) issue_band<5, 2>(d, ab, rs, p.a_hi, ab, rs, p.a_hi, idesc);  // (B = A's layout)
-          else if (p.kblocks == 5 && ksteps == 2) issue_band<5, 2>(d, ab, rs, p.a_hi, b0, bs, hi, idesc);
-          else
+                  umma_i8(ds, ar + j * 4 + ks * 2, hi, br + j * bs + ks * 2, hi, idesc, (i | j | ks) ? 1u : 0u);
+            }
+          } else if (p.band) {
+            // folded row j of the band (overlapping-row A, a_hi) against banded filter block j
+            const std::uint32_t rs = static_cast<std::uint32_t>(p.band_rowb >> 4), ab = (sa >> 4) | (1u << 16);
+#pragma unroll 1
             for (int j = 0; j < p.kblocks; j++)
-              for (int ks = 0; ks < ksteps; ks++)
+#pragma unroll
+              for (int ks = 0; ks < 2; ks++)
                 umma_i8(d, ab + j * rs + ks * 2, p.a_hi, b0 + j * bs + ks * 2, hi, idesc, (j | ks) ? 1u : 0u);
-        } else if (issuer) {
-          // sub-tile sub: rows 128 sub .. of every k-block's A, accumulator columns + sub * bn
-          for (int sub = 0; sub < p.mt; sub++) {
-            const std::uint32_t ds = d + sub * p.bn, as0 = a0 + sub * ((BM * p.bk) >> 4);
-            switch (p.kpb * 8 + ksteps) {
-              case 1 * 8 + 2: issue_stage<1, 2>(ds, as0, as, b0, bs, hi, idesc, first); break;
-              case 1 * 8 + 4: issue_stage<1, 4>(ds, as0, as, b0, bs, hi, idesc, first); break;
-              case 2 * 8 + 2: issue_stage<2, 2>(ds, as0, as, b0, bs, hi, idesc, first); break;
-              case 2 * 8 + 4: issue_stage<2, 4>(ds, as0, as, b0, bs, hi, idesc, first); break;
-              case 3 * 8 + 2: issue_stage<3, 2>(ds, as0, as, b0, bs, hi, idesc, first); break;
-              case 3 * 8 + 4: issue_stage<3, 4>(ds, as0, as, b0, bs, hi, idesc, first); break;
-              case 4 * 8 + 2: issue_stage<4, 2>(ds, as0, as, b0, bs, hi, idesc, first); break;
-              default: issue_stage<4, 4>(ds, as0, as, b0, bs, hi, idesc, first); break;
+          } else {
+            // sub-tile sub: rows 128 sub .. of every k-block's A, accumulator columns + sub * bn
+#pragma unroll 1
+            for (int q = 0; q < p.mt * p.kpb; q++) {
+              const int sub = q / p.kpb, j = q - sub * p.kpb;
+              const std::uint32_t ds = d + sub * p.bn, ar = a0 + sub * ((BM * p.bk) >> 4) + j * as, br = b0 + j * bs;
+              const bool f = first && j == 0;
+              if (ksteps == 2) {
+#pragma unroll
+                for (int ks = 0; ks < 2; ks++) umma_i8(ds, ar + ks * 2, hi, br + ks * 2, hi, idesc, (f && ks == 0) ? 0u : 1u);
+              } else {
+#pragma unroll
+                for (int ks = 0; ks < 4; ks++) umma_i8(ds, ar + ks * 2, hi, br + ks * 2, hi, idesc, (f && ks == 0) ? 0u : 1u);
+              }
             }
           }
         }
