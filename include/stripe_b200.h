@@ -46,7 +46,8 @@ enum {
   SB_ERR_UNSUPPORTED = 9,        /* outside this executor's contract (e.g. observers) */
   SB_ERR_CUDA = 10,              /* CUDA runtime / driver failure */
   SB_ERR_NCCL = 11,              /* NCCL failure (split aggregations) */
-  SB_ERR_INVALID = 12            /* bad argument at the ABI */
+  SB_ERR_INVALID = 12,           /* bad argument at the ABI */
+  SB_ERR_PASS = 13               /* PassError{code} "InvalidTile"/"NotTileable" (passes.h, tile.cpp:104-133) */
 };
 
 /* Element dtypes (bit widths; ir.h:25) plus the fp32 extension. */
@@ -114,6 +115,27 @@ int sb_program_output_aggregation(const sb_program* p, const char* name, int* ag
  * constraints), the reference's count_valid_points (tile.cpp:338-370) evaluated on the
  * device in closed form per innermost row. */
 int sb_count_valid_points(sb_context* ctx, const sb_program* p, const char* block_path, int64_t* count);
+/* TileCostReport (passes.h:42-50); excluded = 1 for "MemCap". */
+typedef struct sb_tile_report {
+  int64_t lines_total;
+  int64_t useful_ops;
+  int64_t tile_elements;
+  int32_t excluded;
+} sb_tile_report;
+/* tile_cost(block, parse_tile_shape(tiles), CacheModel{line}, mem_cap) (passes.h:60-67,
+ * tile.cpp:380-455) of the block at `block_path`, evaluated on the device: same report, same
+ * PassError codes (SB_ERR_PASS, sb_last_error "InvalidTile: ..."/"NotTileable: ...").
+ * `interleaved` = TileShape::interleaved.  line <= 4096 elements. */
+int sb_tile_cost(sb_context* ctx, const sb_program* p, const char* block_path, const char* tiles, int interleaved,
+                 int64_t line, int64_t mem_cap, sb_tile_report* out);
+/* autotile(block, CacheModel{line}, AutotileOptions{mem_cap, power_of_two}) (passes.h:85-89,
+ * tile.cpp:475-535): the exhaustive divisor (or power-of-two) search, every candidate's lines
+ * counted on the device.  *found = 0 when every candidate exceeds the cap (the reference's
+ * "NoFeasibleTile" warning); otherwise `chosen` gets TileShape::to_string ("m:32,n:64", names
+ * sorted), *len its length.  The caller applies the reference's tile_rewrite to it. */
+int sb_autotile(sb_context* ctx, const sb_program* p, const char* block_path, int64_t line, int64_t mem_cap,
+                int power_of_two, char* chosen, size_t cap, size_t* len, int* found, sb_tile_report* report,
+                int64_t* candidates, int64_t* excluded);
 /* Split-aggregation sharding: a copy of `p` whose ranged index `index` in the
  * block at dot path `block_path` ("" = root, "0", "0.1", ...) runs over [lo, hi) only.
  * Shards' outputs combine with the output's aggregation (all-reduce sum/max/min/prod). */

@@ -133,6 +133,8 @@ class Ref:
             L.sr_tile_rewrite.argtypes = [_vp, _cp, _cp, _cp, _sz, _cp, _sz]
             L.sr_pipeline.argtypes = [_vp, _cp, _cp, _sz, _cp, _sz]
             L.sr_useful_ops.argtypes = [_vp, _cp, ctypes.POINTER(_i64), _cp, _sz]
+            L.sr_tile_cost.argtypes = [_vp, _cp, _cp, _i32, _i64, _i64, _i64, _vp, _cp, _sz]
+            L.sr_autotile.argtypes = [_vp, _cp, _i64, _i64, _i32, _cp, _sz, _vp, _cp, _sz]
             cls._lib = L
         return cls._lib
 
@@ -211,6 +213,31 @@ class Ref:
         if cls.lib().sr_useful_ops(p.h, path.encode(), ctypes.byref(v), err, len(err)):
             raise OracleError(err.value.decode())
         return v.value
+
+    @classmethod
+    def tile_cost(cls, text: str, path: str, tiles: str, line: int, mem_cap: int, interleaved: bool = False,
+                  hint: int = -1):
+        """tile_cost (tile.cpp:380-455) -> (lines_total, useful_ops, tile_elements, excluded)."""
+        p = cls.parse(text)
+        err = ctypes.create_string_buffer(4096)
+        out = np.zeros(4, dtype=np.int64)
+        if cls.lib().sr_tile_cost(p.h, path.encode(), tiles.encode(), int(interleaved), line, mem_cap, hint,
+                                  out.ctypes.data, err, len(err)):
+            raise OracleError(err.value.decode())
+        return int(out[0]), int(out[1]), int(out[2]), bool(out[3])
+
+    @classmethod
+    def autotile(cls, text: str, path: str, line: int, mem_cap: int, power_of_two: bool = False):
+        """autotile (tile.cpp:475-535) -> (chosen text or None, (lines, ops, tile_elements), candidates, excluded)."""
+        p = cls.parse(text)
+        err = ctypes.create_string_buffer(4096)
+        buf = ctypes.create_string_buffer(4096)
+        out = np.zeros(6, dtype=np.int64)
+        if cls.lib().sr_autotile(p.h, path.encode(), line, mem_cap, int(power_of_two), buf, len(buf),
+                                 out.ctypes.data, err, len(err)):
+            raise OracleError(err.value.decode())
+        return (buf.value.decode() if out[5] else None, (int(out[0]), int(out[1]), int(out[2])), int(out[3]),
+                int(out[4]))
 
     @classmethod
     def pipeline(cls, text: str, hwcfg: str) -> str:

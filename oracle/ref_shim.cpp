@@ -261,6 +261,47 @@ int sr_useful_ops(void* p, const char* path, std::int64_t* out, char* err, std::
   });
 }
 
+// tile_cost (tile.cpp:380-455) of the block at `path`; hint < 0: no useful_ops hint.
+// out = {lines_total, useful_ops, tile_elements, excluded}.
+int sr_tile_cost(void* p, const char* path, const char* tiles, int interleaved, std::int64_t line,
+                 std::int64_t mem_cap, std::int64_t hint, std::int64_t* out, char* err, std::size_t ecap) {
+  return guarded(err, ecap, [&] {
+    const Program& prog = *static_cast<Program*>(p);
+    const Block* blk = block_at_path(&prog.root, path);
+    if (!blk) throw std::runtime_error("bad block path");
+    TileShape ts = parse_tile_shape(tiles);
+    ts.interleaved = interleaved != 0;
+    CacheModel cm{line, std::int64_t{1} << 40};
+    TileCostReport r = hint < 0 ? tile_cost(*blk, ts, cm, mem_cap) : tile_cost(*blk, ts, cm, mem_cap, hint);
+    out[0] = r.lines_total;
+    out[1] = r.useful_ops;
+    out[2] = r.tile_elements;
+    out[3] = r.excluded ? 1 : 0;
+  });
+}
+
+// autotile (tile.cpp:475-535); chosen gets TileShape::to_string() ("" when none feasible).
+// out = {lines_total, useful_ops, tile_elements, candidates, excluded, found}.
+int sr_autotile(void* p, const char* path, std::int64_t line, std::int64_t mem_cap, int power_of_two,
+                char* chosen, std::size_t cap, std::int64_t* out, char* err, std::size_t ecap) {
+  return guarded(err, ecap, [&] {
+    const Program& prog = *static_cast<Program*>(p);
+    const Block* blk = block_at_path(&prog.root, path);
+    if (!blk) throw std::runtime_error("bad block path");
+    AutotileOptions opts;
+    opts.mem_cap = mem_cap;
+    opts.power_of_two = power_of_two != 0;
+    AutotileResult r = autotile(*blk, CacheModel{line, std::int64_t{1} << 40}, opts);
+    put(r.chosen ? r.chosen->to_string() : std::string(), chosen, cap);
+    out[0] = r.report.lines_total;
+    out[1] = r.report.useful_ops;
+    out[2] = r.report.tile_elements;
+    out[3] = r.candidates;
+    out[4] = r.excluded;
+    out[5] = r.chosen ? 1 : 0;
+  });
+}
+
 // apply_pipeline (passes.cpp:905-1023) with a .hwcfg text.
 int sr_pipeline(void* p, const char* hwcfg, char* buf, std::size_t cap, char* err,
                 std::size_t ecap) {

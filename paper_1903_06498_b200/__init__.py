@@ -35,7 +35,7 @@ SB_BUF_PREPARE = 1
 STATUS_NAMES = [
     "Ok", "MissingBuffer", "UnknownIntrinsic", "UnknownSpecial", "UndefinedTemp",
     "OutOfBoundsAccess", "UnboundIndex", "SyntaxError", "ScopeError", "Unsupported",
-    "CudaError", "NcclError", "Invalid",
+    "CudaError", "NcclError", "Invalid", "PassError",
 ]
 
 # Every symbol include/stripe_b200.h declares (checked by tests/test_abi.py).
@@ -44,6 +44,7 @@ EXPORTED = [
     "sb_program_parse", "sb_program_free", "sb_program_print", "sb_program_buffer_count",
     "sb_program_buffer_info", "sb_program_output_identity", "sb_program_describe_plan",
     "sb_program_output_aggregation", "sb_program_restrict_index", "sb_program_check_split", "sb_count_valid_points",
+    "sb_tile_cost", "sb_autotile",
     "sb_context_create", "sb_context_destroy", "sb_context_set_stream", "sb_context_stream",
     "sb_context_sync", "sb_context_launch_count", "sb_context_set_profile", "sb_context_profile_read", "sb_device_alloc", "sb_device_free",
     "sb_host_alloc_pinned", "sb_host_free_pinned", "sb_execute", "sb_execute_device", "sb_execute_async",
@@ -54,6 +55,28 @@ EXPORTED = [
 class HostBuffer(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char_p), ("carrier", ctypes.c_int32), ("flags", ctypes.c_int32),
                 ("data", ctypes.c_void_p), ("count", ctypes.c_int64)]
+
+
+class TileReport(ctypes.Structure):
+    """TileCostReport (passes.h:42-50): cost() = lines_total / useful_ops; excluded = "MemCap"."""
+    _fields_ = [("lines_total", ctypes.c_int64), ("useful_ops", ctypes.c_int64), ("tile_elements", ctypes.c_int64),
+                ("_excluded", ctypes.c_int32)]
+
+    @property
+    def excluded(self):
+        return "MemCap" if self._excluded else None
+
+    def as_tuple(self):
+        return (self.lines_total, self.useful_ops, self.tile_elements, bool(self._excluded))
+
+
+class AutotileResult:
+    """AutotileResult (passes.h:76-83) without the rewritten block: apply the reference's
+    tile_rewrite to `chosen` (TileShape::to_string text, or None when every candidate was
+    excluded: the reference's NoFeasibleTile warning)."""
+
+    def __init__(self, chosen, report, candidates, excluded):
+        self.chosen, self.report, self.candidates, self.excluded = chosen, report, candidates, excluded
 
 
 class DeviceBuffer(ctypes.Structure):
@@ -91,6 +114,10 @@ def lib() -> ctypes.CDLL:
         L.sb_program_restrict_index.argtypes = [vp, ctypes.c_char_p, ctypes.c_char_p, i64, i64, ctypes.POINTER(vp)]
         L.sb_program_check_split.argtypes = [vp, ctypes.c_char_p, ctypes.c_char_p]
         L.sb_count_valid_points.argtypes = [vp, vp, ctypes.c_char_p, ctypes.POINTER(i64)]
+        L.sb_tile_cost.argtypes = [vp, vp, ctypes.c_char_p, ctypes.c_char_p, i32, i64, i64, ctypes.POINTER(TileReport)]
+        L.sb_autotile.argtypes = [vp, vp, ctypes.c_char_p, i64, i64, i32, ctypes.c_char_p, ctypes.c_size_t,
+                                  ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(i32), ctypes.POINTER(TileReport),
+                                  ctypes.POINTER(i64), ctypes.POINTER(i64)]
         L.sb_program_describe_plan.argtypes = [vp, i32, i32, ctypes.c_char_p, ctypes.c_size_t,
                                                ctypes.POINTER(ctypes.c_size_t)]
         L.sb_context_create.argtypes = [i32, ctypes.POINTER(vp)]
@@ -132,6 +159,8 @@ def _check(rc: int) -> None:
     if rc != 0:
         msg = lib().sb_last_error().decode(errors="replace")
         code = STATUS_NAMES[rc] if 0 <= rc < len(STATUS_NAMES) else "Invalid"
+        if code == "PassError":  # PassError{code}: InvalidTile / NotTileable (passes.h)
+            code = msg.split(":", 1)[0]
         raise ExecError(code, msg)
 
 
@@ -212,6 +241,27 @@ class Program:
         _check(lib().sb_count_valid_points((ctx or default_context(0)).handle, self._h, block_path.encode(),
                                            ctypes.byref(v)))
         return v.value
+
+    def tile_cost(self, block_path: str, tiles: str, line: int, mem_cap: int, interleaved: bool = False,
+                  ctx: "Context" = None) -> TileReport:
+        """tile_cost(block, parse_tile_shape(tiles), CacheModel{line}, mem_cap) (tile.cpp:380-455),
+        line counts on the device (sb_tile_cost)."""
+        r = TileReport()
+        _check(lib().sb_tile_cost((ctx or default_context(0)).handle, self._h, block_path.encode(), tiles.encode(),
+                                  int(interleaved), line, mem_cap, ctypes.byref(r)))
+        return r
+
+    def autotile(self, block_path: str, line: int, mem_cap: int, power_of_two: bool = False,
+                 ctx: "Context" = None) -> AutotileResult:
+        """autotile(block, CacheModel{line}, AutotileOptions{mem_cap, power_of_two}) (tile.cpp:475-535):
+        every candidate evaluated on the device (sb_autotile)."""
+        buf = ctypes.create_string_buffer(4096)
+        n, found, r = ctypes.c_size_t(), ctypes.c_int32(), TileReport()
+        cands, excl = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().sb_autotile((ctx or default_context(0)).handle, self._h, block_path.encode(), line, mem_cap,
+                                 int(power_of_two), buf, len(buf), ctypes.byref(n), ctypes.byref(found),
+                                 ctypes.byref(r), ctypes.byref(cands), ctypes.byref(excl)))
+        return AutotileResult(buf.value.decode() if found.value else None, r, cands.value, excl.value)
 
     def describe_plan(self, fresh_outputs: bool = False, tensor_cores: bool = True, fp32_mode: int = 0) -> str:
         n = ctypes.c_size_t()

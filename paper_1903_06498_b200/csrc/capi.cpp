@@ -24,6 +24,7 @@
 #include "../../include/stripe_b200.h"
 #include "ir.hpp"
 #include "kernels.hpp"
+#include "tilecost.hpp"
 #include "plan.hpp"
 
 namespace {
@@ -37,7 +38,8 @@ int status_of(const std::string& code) {
       {"OutOfBoundsAccess", SB_ERR_OUT_OF_BOUNDS}, {"UnboundIndex", SB_ERR_UNBOUND_INDEX},
       {"SyntaxError", SB_ERR_SYNTAX},             {"ScopeError", SB_ERR_SCOPE},
       {"Unsupported", SB_ERR_UNSUPPORTED},        {"CudaError", SB_ERR_CUDA},
-      {"NcclError", SB_ERR_NCCL},                 {"Invalid", SB_ERR_INVALID}};
+      {"NcclError", SB_ERR_NCCL},                 {"Invalid", SB_ERR_INVALID},
+      {"InvalidTile", SB_ERR_PASS},               {"NotTileable", SB_ERR_PASS}};
   auto it = m.find(code);
   return it == m.end() ? SB_ERR_INVALID : it->second;
 }
@@ -728,8 +730,8 @@ const char* sb_status_name(int s) {
   static const char* names[] = {"Ok",           "MissingBuffer",  "UnknownIntrinsic", "UnknownSpecial",
                                 "UndefinedTemp", "OutOfBoundsAccess", "UnboundIndex",   "SyntaxError",
                                 "ScopeError",   "Unsupported",    "CudaError",        "NcclError",
-                                "Invalid"};
-  return s >= 0 && s <= 12 ? names[s] : "Invalid";
+                                "Invalid",      "PassError"};
+  return s >= 0 && s <= 13 ? names[s] : "Invalid";
 }
 
 int sb_program_parse(const char* text, sb_program** out) {
@@ -777,20 +779,68 @@ int sb_program_output_aggregation(const sb_program* p, const char* name, int* ag
   return guarded([&] { *agg = static_cast<int>(sb::output_aggregation(p->prog, name)); });
 }
 
+namespace {
+const sb::Block* block_at(const sb_program* p, const char* block_path) {
+  const sb::Block* b = &p->prog.root;
+  std::string path = block_path ? block_path : "";
+  std::stringstream ss(path);
+  std::string part;
+  while (!path.empty() && std::getline(ss, part, '.')) {
+    const std::size_t k = static_cast<std::size_t>(std::stoll(part));
+    if (k >= b->stmts.size() || b->stmts[k].kind != sb::StmtKind::Block)
+      throw sb::Error("Unsupported", "no block at path '" + path + "'");
+    b = b->stmts[k].block.get();
+  }
+  return b;
+}
+
+void put_report(const sb::TileReport& r, sb_tile_report* out) {
+  out->lines_total = r.lines_total;
+  out->useful_ops = r.useful_ops;
+  out->tile_elements = r.tile_elements;
+  out->excluded = r.excluded ? 1 : 0;
+}
+}  // namespace
+
+int sb_tile_cost(sb_context* ctx, const sb_program* p, const char* block_path, const char* tiles, int interleaved,
+                 int64_t line, int64_t mem_cap, sb_tile_report* out) {
+  return guarded([&] {
+    if (!out) throw sb::Error("Invalid", "null report");
+    std::lock_guard<std::recursive_mutex> lock(ctx->mu);
+    cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const auto shape = sb::parse_tile_shape_text(tiles ? tiles : "");
+    sb::TileCoster tc(*block_at(p, block_path), line, mem_cap, ctx->stream);
+    put_report(tc.tile_cost(shape, interleaved != 0), out);
+  });
+}
+
+int sb_autotile(sb_context* ctx, const sb_program* p, const char* block_path, int64_t line, int64_t mem_cap,
+                int power_of_two, char* chosen, size_t cap, size_t* len, int* found, sb_tile_report* report,
+                int64_t* candidates, int64_t* excluded) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lock(ctx->mu);
+    cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    sb::TileCoster tc(*block_at(p, block_path), line, mem_cap, ctx->stream);
+    const sb::AutotileResult r = tc.autotile(power_of_two != 0);
+    const std::string text = r.found ? tc.shape_text(r.chosen) : "";
+    if (len) *len = text.size();
+    if (chosen && cap) {
+      const std::size_t n = std::min(cap - 1, text.size());
+      std::memcpy(chosen, text.data(), n);
+      chosen[n] = 0;
+    }
+    if (found) *found = r.found ? 1 : 0;
+    if (report) put_report(r.report, report);
+    if (candidates) *candidates = r.candidates;
+    if (excluded) *excluded = r.excluded;
+  });
+}
+
 int sb_count_valid_points(sb_context* ctx, const sb_program* p, const char* block_path, int64_t* count) {
   return guarded([&] {
     std::lock_guard<std::recursive_mutex> lock(ctx->mu);
     cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
-    const sb::Block* b = &p->prog.root;
-    std::string path = block_path ? block_path : "";
-    std::stringstream ss(path);
-    std::string part;
-    while (!path.empty() && std::getline(ss, part, '.')) {
-      const std::size_t k = static_cast<std::size_t>(std::stoll(part));
-      if (k >= b->stmts.size() || b->stmts[k].kind != sb::StmtKind::Block)
-        throw sb::Error("Unsupported", "no block at path '" + path + "'");
-      b = b->stmts[k].block.get();
-    }
+    const sb::Block* b = block_at(p, block_path);
     // the reference's definition: the block's own ranged indexes, its own constraints
     std::vector<long long> ranges;
     std::vector<std::string> names;

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 #include "desc.hpp"
 #include "plan.hpp"
@@ -75,6 +76,21 @@ cudaError_t launch_gemm_tc(const GemmPlan& g, const GemmArgs& args, cudaStream_t
 cudaError_t launch_count_points(int nd, const long long* ranges, int nc, const long long* cons_c,
                                 const long long* cons_k, void* scratch, unsigned long long* h_out, cudaStream_t s);
 std::size_t count_points_scratch_bytes();
+
+// Distinct cache lines per tile for every residue of the tile base (kernels/tilecost.cu): one
+// (candidate, refinement) item of tile_cost (tile.cpp:413-453).  F = cst + one value from each
+// axis list (len[a] values at val_off, axis 0 fastest); run != 0: the last axis is the unit-step
+// run [v, v + len - 1] given by its single stored value v.  Per-q min/max slots live in shared
+// memory (scratch_off < 0) or at scratch_off words of the global scratch (2 * nq words).
+constexpr int kTileMaxAxes = 32;
+struct TileLineItem {
+  long long cst, qbase, prefixes, scratch_off;
+  int nq, naxes, run, val_off;
+  int len[kTileMaxAxes];
+};
+int tile_lines_smem_q();
+cudaError_t launch_tile_lines(const std::vector<TileLineItem>& items, const std::vector<long long>& values,
+                              long long scratch_words, int L, std::vector<long long>* counts, cudaStream_t s);
 
 // Windowed max/min over constraint-bounded taps, 16-byte channel vectors (kernels/pool.cu).
 const char* pool_unsupported(const PoolPlan& pp);

@@ -27,7 +27,7 @@ def test_symbol_exported(sym):
 def test_status_names_match_reference_codes():
     L = sb.lib()
     assert L.sb_abi_version() == 1
-    names = [L.sb_status_name(i).decode() for i in range(13)]
+    names = [L.sb_status_name(i).decode() for i in range(14)]
     assert names == sb.STATUS_NAMES
     for code in ["MissingBuffer", "UnknownIntrinsic", "UnknownSpecial", "UndefinedTemp", "OutOfBoundsAccess",
                  "UnboundIndex", "SyntaxError", "ScopeError"]:
