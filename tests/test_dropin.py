@@ -63,3 +63,29 @@ def test_reference_side_dropin_concurrent_threads(tmp_path):
     lines = [l for l in r.stdout.splitlines() if "threads=" in l]
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert len(lines) >= len(files) - 1 and all(l.startswith("OK") for l in lines), r.stdout
+
+
+@pytest.mark.gpu
+def test_reference_side_autotile(tmp_path):
+    """stripe::b200::autotile (device line counts + the reference's tile_rewrite) against
+    stripe::autotile on block 0 of small programs, divisor and power-of-two spaces: same chosen
+    shape, report, candidate counts, rewritten block text and exception codes (tile.cpp:475-535)."""
+    if not gpu_available():
+        pytest.skip("no B200")
+    if not os.path.exists(BIN):
+        pytest.skip("oracle/_ref/dropin_test not built (needs /root/reference at build time)")
+    from paper_1903_06498_b200 import workloads as W
+    progs = {"mm": W.matmul(16, 12, 20), "conv": W.conv2d(1, 8, 8, 4, 4), "pool": W.pool2d(2, 9, 9, 4)}
+    for c in corpus():
+        if c.name.startswith(("fx_", "rnd_text_0", "gen_", "tile_")) and c.name not in ("fx_place2",):
+            progs[c.name] = c.text
+    files = []
+    for name, text in progs.items():
+        p = tmp_path / f"{name}.stripe"
+        p.write_text(text)
+        files.append(str(p))
+    r = subprocess.run([BIN, "--seed", "5", "--autotile", "8:512"] + files, capture_output=True, text=True,
+                       timeout=900)
+    lines = [l for l in r.stdout.splitlines() if " autotile " in l]
+    assert r.returncode == 0, "\n".join(l for l in r.stdout.splitlines() if not l.startswith("OK"))[-3000:]
+    assert len(lines) >= 2 * (len(files) - 6) and all(l.startswith("OK") for l in lines), r.stdout[-3000:]
