@@ -1449,6 +1449,7 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     kp.strip = 1;
   // dynamic smem: A/B ring (up to 128 KB) | resident filter | output staging | residual tiles |
   // vector | gather table | barriers, for tile width bn (false: does not fit)
+  const int bres_cap = (std::getenv("SB_IG_BRES_KB") ? std::atoi(std::getenv("SB_IG_BRES_KB")) : 96) * 1024;
   auto layout = [&](int bn, int mt) -> bool {
     kp.bn = bn;
     kp.mt = mt;
@@ -1463,7 +1464,7 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
     const int rawb = kp.band_raw ? kRawStages * kp.raw_stage : 0;
     // the filter stays resident when there is one n-tile and it is small (<= 96 KB)
     kp.bn_box = kp.N <= 64 ? 64 : bn;
-    const int bres = (kp.tiles_n == 1 || kp.nstat) && kp.kblocks * kp.bn_box * g.bk <= 96 * 1024 &&
+    const int bres = (kp.tiles_n == 1 || kp.nstat) && kp.kblocks * kp.bn_box * g.bk <= bres_cap &&
                              !std::getenv("SB_IG_NOBRES")
                          ? kp.kblocks * kp.bn_box * g.bk : 0;
     kp.b_res = bres ? 1 : 0;

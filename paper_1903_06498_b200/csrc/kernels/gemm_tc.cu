@@ -46,6 +46,10 @@ struct GemmKParams {
   int tf32;  // kind::tf32 (fp32 accumulators, f32 output)
   int bk_el;  // k-block width in elements (128 bytes)
   int pdl_wait;
+  // split-K over a CTA pair (cluster of 2, opt-in): rank r runs k-blocks [r * kb_per, (r + 1) * kb_per);
+  // rank 1 parks its partial tile in its own staging buffer, rank 0 adds it over DSMEM in the
+  // epilogue and stores the sum (no zero fill, no atomics, no second pass)
+  int ksplit, kb_per;
 };
 
 __device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
@@ -127,6 +131,45 @@ __device__ __forceinline__ void tmem_ld16_async(std::uint32_t taddr, std::uint32
         "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
 }
+__device__ __forceinline__ std::uint32_t cluster_rank() {
+  std::uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ std::uint32_t cluster_id() {
+  std::uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ std::uint32_t cluster_count() {
+  std::uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of this CTA's shared variable `a` in cluster CTA `rank`
+__device__ __forceinline__ std::uint32_t peer_addr(std::uint32_t a, std::uint32_t rank) {
+  std::uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_peer(std::uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(std::uint64_t* bar, std::uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra DONEC_%=;\n\t"
+      "bra WAITC_%=;\n\t"
+      "DONEC_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ bool elect_one_sync() {
   std::uint32_t is;
   asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(is));
@@ -152,9 +195,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   std::uint64_t* empty = bars + kStages;
   std::uint64_t* tfull = bars + 2 * kStages;
   std::uint64_t* tempty = bars + 2 * kStages + 2;
-  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 2 * kStages + 4);
+  std::uint64_t* peer_full = bars + 2 * kStages + 4;   // rank 0: rank 1's partial tile is staged
+  std::uint64_t* peer_empty = bars + 2 * kStages + 5;  // rank 1: rank 0 has read it
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 2 * kStages + 6);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int tiles = p.tiles_m * p.tiles_n;
+  const bool split = p.ksplit > 1;
+  const std::uint32_t rank = split ? cluster_rank() : 0;
+  const int t_first = split ? static_cast<int>(cluster_id()) : static_cast<int>(blockIdx.x);
+  const int t_step = split ? static_cast<int>(cluster_count()) : static_cast<int>(gridDim.x);
+  const int kb_lo = split ? static_cast<int>(rank) * p.kb_per : 0;
+  const int kb_hi = split ? min(p.kblocks, kb_lo + p.kb_per) : p.kblocks;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; s++) {
@@ -165,6 +216,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 128);
     }
+    mbar_init(peer_full, 128);
+    mbar_init(peer_empty, 128);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -174,6 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (split) cluster_sync_all();  // the peer's barriers are initialised before any remote arrive
   tc_fence_after();
   const std::uint32_t tmem_base = *tmem_slot;
   // dependents are released after this grid's wait (see conv_tc.cu)
@@ -184,9 +238,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (p.pdl_wait) asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory");
       int stage = 0;
       std::uint32_t phase = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int t = t_first; t < tiles; t += t_step) {
         const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * BN;
-        for (int kb = 0; kb < p.kblocks; kb++) {
+        for (int kb = kb_lo; kb < kb_hi; kb++) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], kStageA + kStageB);
           tma_load_2d(smem_u32(sa + stage * kStageA), &amap, &full[stage], kb * p.bk_el, m0);
@@ -203,12 +257,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0, iter = 0;
       std::uint32_t phase = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x, iter++) {
+      for (int t = t_first; t < tiles; t += t_step, iter++) {
         const int acc = iter & 1;
         mbar_wait(&tempty[acc], ((iter >> 1) & 1) ^ 1);
         tc_fence_after();
         const std::uint32_t d = tmem_base + static_cast<std::uint32_t>(acc * BN);
-        for (int kb = 0; kb < p.kblocks; kb++) {
+        for (int kb = kb_lo; kb < kb_hi; kb++) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const std::uint32_t a0 = (smem_u32(sa + stage * kStageA) >> 4) | (1u << 16);
@@ -218,8 +272,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             // A: +32 bytes along the 128-byte K row; B: K-major +32 bytes, N-major +32 rows (4 KB)
             std::uint32_t b_lo = p.b_kmajor ? (((bsm + ks * 32) >> 4) | (1u << 16))
                                             : (((bsm + ks * 32 * 128) >> 4) | ((static_cast<std::uint32_t>(BK * 128) >> 4) << 16));
-            if (p.tf32) umma_tf32(d, a0 + ks * 2, kHiSW128, b_lo, kHiSW128, p.idesc, (kb | ks) != 0);
-            else umma_i8(d, a0 + ks * 2, kHiSW128, b_lo, kHiSW128, p.idesc, (kb | ks) != 0);
+            const std::uint32_t accum = (kb != kb_lo || ks != 0) ? 1u : 0u;
+            if (p.tf32) umma_tf32(d, a0 + ks * 2, kHiSW128, b_lo, kHiSW128, p.idesc, accum);
+            else umma_i8(d, a0 + ks * 2, kHiSW128, b_lo, kHiSW128, p.idesc, accum);
           }
           umma_commit(&empty[stage]);
           if (++stage == kStages) {
@@ -235,9 +290,30 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = quarter * 32 + lane;
     const bool leader = threadIdx.x == 64;
     int iter = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, iter++) {
+    for (int t = t_first; t < tiles; t += t_step, iter++) {
       const int acc = iter & 1;
       const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * BN;
+      if (split && rank == 1) {
+        // park the partial tile in the own staging buffer (same swizzled layout rank 0 uses)
+        if (iter > 0) mbar_wait_cluster(peer_empty, (iter - 1) & 1);
+        mbar_wait(&tfull[acc], (iter >> 1) & 1);
+        tc_fence_after();
+        for (int h = 0; h < BN / 32; h++) {
+          std::uint32_t v[32];
+          tmem_ld32(tmem_base + (static_cast<std::uint32_t>(quarter * 32) << 16) +
+                        static_cast<std::uint32_t>(acc * BN + h * 32),
+                    v);
+          const std::uint32_t rbase = smem_u32(stg + h * 16384 + row * 128);
+#pragma unroll
+          for (int q = 0; q < 8; q++)
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rbase + ((q ^ (row & 7)) << 4)),
+                         "r"(v[4 * q]), "r"(v[4 * q + 1]), "r"(v[4 * q + 2]), "r"(v[4 * q + 3]));
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        mbar_arrive_peer(peer_addr(smem_u32(peer_full), 0));
+        continue;
+      }
       if (p.tma_out) {
         if (leader) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -250,6 +326,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                   v);
         if (p.tma_out) {
           std::uint32_t rbase = smem_u32(stg + h * 16384 + row * 128);
+          if (split) {  // + rank 1's partial, read over DSMEM at the same swizzled address
+            if (h == 0) mbar_wait_cluster(peer_full, iter & 1);
+            const std::uint32_t pbase = peer_addr(rbase, 1);
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+              std::uint32_t w0, w1, w2, w3;
+              asm volatile("ld.shared::cluster.v4.b32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(w0), "=r"(w1), "=r"(w2), "=r"(w3)
+                           : "r"(pbase + ((q ^ (row & 7)) << 4)));
+              v[4 * q] += w0;
+              v[4 * q + 1] += w1;
+              v[4 * q + 2] += w2;
+              v[4 * q + 3] += w3;
+            }
+            if (h == BN / 32 - 1) mbar_arrive_peer(peer_addr(smem_u32(peer_empty), 1));
+          }
 #pragma unroll
           for (int q = 0; q < 8; q++)
             asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rbase + ((q ^ (row & 7)) << 4)),
@@ -291,6 +383,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     if (p.tma_out && leader) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    // rank 1 stays resident until rank 0 has read its last partial tile
+    if (split && rank == 1 && iter > 0) mbar_wait_cluster(peer_empty, (iter - 1) & 1);
   }
   __syncwarp();  // reconverge the single-lane role warps before the CTA barrier
   __syncthreads();
@@ -1135,16 +1229,34 @@ cudaError_t launch_gemm_tc(const GemmPlan& g, const GemmArgs& args, cudaStream_t
   kp.pdl = args.pdl_mode != kPdlOff ? 1 : 0;
   kp.pdl_wait = args.pdl_mode == kPdlWait ? 1 : 0;
   int tiles = kp.tiles_m * kp.tiles_n;
+  // split-K over CTA pairs while the tiles alone leave at least half the SMs idle: opt-in
+  // (SB_GEMM_SPLIT=1), measured slower at config 1 (1024^3: 11.2 vs 7.8 us per pipelined step,
+  // 17.5 vs 13.4 us per launch; the pair's DSMEM hand-off serialises both epilogues)
+  kp.ksplit = 1;
+  if (kp.tma_out && !kp.tf32 && kp.kblocks >= 2 && 2 * tiles <= num_sms && std::getenv("SB_GEMM_SPLIT")) {
+    kp.ksplit = 2;
+    kp.kb_per = (kp.kblocks + 1) / 2;
+  }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(tiles < num_sms ? tiles : num_sms));
+  const int ctas = kp.ksplit * tiles;
+  cfg.gridDim = dim3(static_cast<unsigned>(kp.ksplit > 1 ? ctas : (tiles < num_sms ? tiles : num_sms)));
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (kp.pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na++].val.programmaticStreamSerializationAllowed = 1;
+  }
+  if (kp.ksplit > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na++].val.clusterDim.z = 1;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = kp.pdl ? 1 : 0;
+  cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, gemm_i8_tc_kernel, prep.amap, prep.bmap, prep.cmap, kp);
 }
 

@@ -38,7 +38,8 @@ def check(text, seed=3, provide_out=False):
     np.testing.assert_array_equal(got["C"], exp["C"])
 
 
-@pytest.mark.parametrize("mnk", [(64, 64, 64), (256, 128, 512), (200, 176, 320), (130, 304, 48), (3, 16, 16)],
+@pytest.mark.parametrize("mnk", [(64, 64, 64), (256, 128, 512), (200, 176, 320), (130, 304, 48), (3, 16, 16),
+                                 (128, 128, 384), (1008, 608, 1008), (130, 1104, 4096)],
                          ids=lambda s: "x".join(map(str, s)))
 def test_matmul_i8_to_i32(mnk):
     check(W.matmul(*mnk, in_dtype="i8", out_dtype="i32"))
@@ -47,6 +48,15 @@ def test_matmul_i8_to_i32(mnk):
 @pytest.mark.parametrize("od", ["i8", "i16"])
 def test_matmul_narrow_outputs_wrap(od):
     check(W.matmul(128, 128, 256, in_dtype="i8", out_dtype=od))
+
+
+@pytest.mark.parametrize("mnk", [(256, 128, 512), (128, 128, 384), (1008, 608, 1008), (1024, 1024, 1024)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_matmul_pair_split_path(monkeypatch, mnk):
+    """The opt-in CTA-pair split-K (SB_GEMM_SPLIT: rank 1's partial tile added over DSMEM by
+    rank 0) stays bit-exact, odd k-block counts included."""
+    monkeypatch.setenv("SB_GEMM_SPLIT", "1")
+    check(W.matmul(*mnk, in_dtype="i8", out_dtype="i32"))
 
 
 def test_matmul_b_k_major():

@@ -22,6 +22,12 @@ def program_text(which, batch):
         text = W.conv_fused(batch, 14, 14, 256, 256, 3, 3, 1, 1)
     elif which == "s3_1024":
         text = W.conv_fused(batch, 14, 14, 1024, 256, 1, 1, 1, 0)
+    elif which == "l44":
+        text = W.conv_fused(batch, 14, 14, 1024, 512, 1, 1, 1, 0)
+    elif which == "l43":
+        text = W.conv_fused(batch, 14, 14, 1024, 2048, 1, 1, 2, 0, relu=False)
+    elif which == "l47":
+        text = W.conv_fused(batch, 7, 7, 2048, 512, 1, 1, 1, 0)
     elif which == "s4_3x3":
         text = W.conv_fused(batch, 7, 7, 512, 512, 3, 3, 1, 1)
     elif which == "s4_1x1":
