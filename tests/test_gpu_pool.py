@@ -20,6 +20,10 @@ CASES = [
     (3, 13, 10, 48, 3, 3, 2, 1, "min", "i8"),
     (2, 15, 15, 32, 3, 3, 2, 0, "max", "i8"),
     (5, 40, 38, 16, 3, 3, 2, 1, "max", "i8"),
+    # 3x3 / stride-2, other widths and a single-window image
+    (2, 17, 19, 8, 3, 3, 2, 1, "max", "i16"),
+    (2, 33, 9, 4, 3, 3, 2, 1, "min", "i32"),
+    (1, 3, 3, 16, 3, 3, 2, 1, "max", "i8"),
 ]
 
 
@@ -46,6 +50,31 @@ def test_pool_vs_port(case):
     store = {"I": sb.Buffer(prog.buffers["I"].dtype, x.copy())}
     sb.prepare_outputs(prog, store)
     o0 = store["O"].data.copy()
+    sb.execute(prog, store)
+    ref = reference_execute(text, {"I": x, "O": o0})
+    np.testing.assert_array_equal(store["O"].data, ref["O"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kernel", ["pair", "single"])
+@pytest.mark.parametrize("case", [c for c in CASES if c[4:7] == (3, 3, 2)], ids=lambda c: "x".join(map(str, c)))
+def test_pool_3x3s2_accumulates_into_existing(case, kernel, monkeypatch):
+    """max/min into an output that already holds values (no fill absorbed): the pair kernel
+    and the per-pixel kernel (SB_POOL_SINGLE)."""
+    if not gpu_available():
+        pytest.skip("no B200")
+    if kernel == "single":
+        monkeypatch.setenv("SB_POOL_SINGLE", "1")
+    import paper_1903_06498_b200 as sb
+    from paper_1903_06498_b200 import workloads as W
+    text = W.pool2d(*case)
+    prog = sb.parse_program(text)
+    bits = int(prog.buffers["I"].dtype)
+    rng = np.random.default_rng(7 + sum(case[:4]))
+    lim = 1 << (bits - 1)
+    x = rng.integers(-lim, lim, prog.buffers["I"].elements, dtype=np.int64)
+    o0 = rng.integers(-lim, lim, prog.buffers["O"].elements, dtype=np.int64)
+    store = {"I": sb.Buffer(prog.buffers["I"].dtype, x.copy()), "O": sb.Buffer(prog.buffers["O"].dtype, o0.copy())}
     sb.execute(prog, store)
     ref = reference_execute(text, {"I": x, "O": o0})
     np.testing.assert_array_equal(store["O"].data, ref["O"])
