@@ -1660,6 +1660,13 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
+  if (std::getenv("SB_IG_SHOW"))  // development aid: the chosen layout per prepared conv
+    std::fprintf(stderr,
+                 "igemm M=%d N=%d C=%lld R=%lld bn=%d mt=%d tiles=%dx%d kblocks=%d kpb=%d stages=%d b_res=%d nstat=%d "
+                 "stg4=%d res1=%d res_mma=%d split=%d band=%d strip=%d gather=%d tma_out=%d smem=%d\n",
+                 kp.M, kp.N, static_cast<long long>(cp.C), static_cast<long long>(cp.R), kp.bn, kp.mt, kp.tiles_m,
+                 kp.tiles_n, kp.kblocks, kp.kpb, kp.stages, kp.b_res, kp.nstat, kp.stg4, kp.res1, kp.res_mma,
+                 kp.epi_split, kp.band, kp.strip, kp.gather, kp.tma_out, kp.smem);
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(conv_igemm_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
