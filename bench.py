@@ -191,11 +191,22 @@ def spec(cfg, world, rank, args):
         M = 1024
         lo, hi = Wk.shard_range(M, world, rank)
         m = hi - lo
-        s.update(text=Wk.matmul(m, 1024, 1024, in_dtype=dt, out_dtype="i32"), flops=2.0 * m * 1024 * 1024,
+        if world == 1:
+            # "as one autotiled Stripe block": the reference's tile_rewrite of the shape the device
+            # autotile search chose (configs/c1_autotile.json, tests/golden/make_pipeline_programs.py)
+            with open(os.path.join(ROOT, "configs", f"c1_autotiled_{dt}.stripe")) as f:
+                text = f.read()
+            with open(os.path.join(ROOT, "configs", "c1_autotile.json")) as f:
+                shape = json.load(f)[dt]["chosen"]
+            what = f"one block autotiled on the B200 to {shape} (1331 candidates), rewritten by the reference's tile_rewrite"
+        else:
+            text = Wk.matmul(m, 1024, 1024, in_dtype=dt, out_dtype="i32")
+            what = f"rows sharded ({m} on this rank)"
+        s.update(text=text, flops=2.0 * m * 1024 * 1024,
                  unit="GFLOP/s", bound="tensor", scaling="strong", global_batch=M, images=m,
                  dominant=("gemm_i8_tc",),
                  workload=f"BASELINE config 1: matmul C[i,j] += A[i,k]*B[k,j] 1024^3 ({dt} x {dt} -> i32, exact), "
-                          f"rows sharded ({m} on this rank)",
+                          f"{what}",
                  cpu=dict(text=Wk.matmul(64, 1024, 1024, in_dtype=dt, out_dtype="i32"), work=2.0 * 64 * 1024 * 1024,
                           what="64 rows of config 1 per thread (a row shard; 16 threads = the whole matmul)",
                           seed=1001))

@@ -16,8 +16,15 @@ configs/c2_partition_n8.stripe -- config 2 after `pass partition block=0 index=n
 (tile.cpp:644-691): the batch index split into 8 disjoint banks (Location.bank = n), the
 reference's own work-splitting construct and the multi-GPU shard carrier.
 
+configs/c1_autotiled_{i8,i32}.stripe -- config 1 "as one autotiled Stripe block": the 1024^3
+matmul block tiled by the reference's tile_rewrite with the shape the DEVICE autotile search
+chose (configs/c1_autotile.json, written on a B200 by tools/c1_autotile.py: sb_autotile over
+all 1331 divisor candidates under configs/b200_matmul.hwcfg's SMEM model, 128-element lines,
+cap 232448 elements; the reference's own search does not finish at this size).
+
     python tests/golden/make_pipeline_programs.py [N ...]
 """
+import json
 import os
 import sys
 
@@ -53,6 +60,13 @@ if __name__ == "__main__":
         with open(os.path.join(CONFIGS, f"c3_pipeline_b{n}.stripe"), "w") as f:
             f.write(make(n))
         print("wrote c3", n)
+    with open(os.path.join(CONFIGS, "c1_autotile.json")) as f:
+        chosen = json.load(f)
+    for dt in ("i8", "i32"):
+        text = Ref.tile_rewrite(W.matmul(1024, 1024, 1024, in_dtype=dt, out_dtype="i32"), "0", chosen[dt]["chosen"])
+        with open(os.path.join(CONFIGS, f"c1_autotiled_{dt}.stripe"), "w") as f:
+            f.write(text)
+        print("wrote c1 autotiled", dt, chosen[dt]["chosen"])
     for n in (32, 8):
         with open(os.path.join(CONFIGS, f"c2_partition_n8_b{n}.stripe"), "w") as f:
             f.write(Ref.pipeline(W.conv2d(n, 56, 56, 64, 64), PARTITION))

@@ -129,3 +129,27 @@ def test_limb_gemm_config1_i32_exact():
     c = (ll + (mid << 16)) & 0xFFFFFFFF
     c = torch.where(c >= 2**31, c - 2**32, c).cpu().numpy().ravel()
     np.testing.assert_array_equal(store["C"].data, c)
+
+
+@pytest.mark.parametrize("dt", ["i8", "i32"])
+def test_config1_autotiled_program_exact(dt):
+    """BASELINE config 1 as one autotiled Stripe block (configs/c1_autotiled_*.stripe: the
+    reference's tile_rewrite of the device autotile choice) collapses onto the tensor-core GEMM
+    and equals the exact int64 product wrapped to i32."""
+    import os
+    import paper_1903_06498_b200 as sb
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with open(os.path.join(root, "configs", f"c1_autotiled_{dt}.stripe")) as f:
+        text = f.read()
+    p = sb.parse_program(text)
+    assert "gemm_i8_tc" in p.describe_plan(True)
+    bits = 8 if dt == "i8" else 32
+    rng = np.random.default_rng(11)
+    a = rng.integers(-(1 << (bits - 1)), 1 << (bits - 1), (1024, 1024), dtype=np.int64)
+    b = rng.integers(-(1 << (bits - 1)), 1 << (bits - 1), (1024, 1024), dtype=np.int64)
+    store = {"A": sb.Buffer(p.buffers["A"].dtype, a.ravel().copy()), "B": sb.Buffer(p.buffers["B"].dtype, b.ravel().copy())}
+    sb.prepare_outputs(p, store)
+    sb.execute(p, store)
+    # exact product modulo 2^32 (uint64 wrap-around arithmetic), as the reference's i32 store wraps
+    exp = (a.astype(np.uint64) @ b.astype(np.uint64)).astype(np.uint32).astype(np.int32).astype(np.int64)
+    np.testing.assert_array_equal(store["C"].data.reshape(1024, 1024), exp)
