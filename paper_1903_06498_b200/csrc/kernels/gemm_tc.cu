@@ -30,9 +30,9 @@ namespace sb {
 namespace {
 
 constexpr int kThreads = 192;
-constexpr int kStages = 4;
+constexpr int kStages = 4;  // ring depth of 128-wide tiles (3 for 256-wide tiles: same smem)
 constexpr int BM = 128, BN = 128, BK = 128;
-constexpr std::uint32_t kStageA = BM * BK, kStageB = BK * BN;  // bytes (i8)
+constexpr std::uint32_t kStageA = BM * BK;  // bytes (i8); a B stage is BK * bn
 
 struct GemmKParams {
   int M, N, K;
@@ -50,6 +50,9 @@ struct GemmKParams {
   // rank 1 parks its partial tile in its own staging buffer, rank 0 adds it over DSMEM in the
   // epilogue and stores the sum (no zero fill, no atomics, no second pass)
   int ksplit, kb_per;
+  // tile width 128 or 256 (N = 256 MMAs: 85 instead of 64 MACs per staged byte, for problems
+  // with at least two 128 x 256 tiles per SM), ring depth
+  int bn, stages;
 };
 
 __device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
@@ -187,10 +190,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) std::uint8_t smem_raw[];
   std::uint8_t* base =
       reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t{1023});
-  std::uint8_t* sa = base;                              // kStages x 16 KB
-  std::uint8_t* sbm = sa + kStages * kStageA;           // kStages x 16 KB
-  std::uint8_t* stg = sbm + kStages * kStageB;          // 64 KB output staging (4 x 16 KB column quarters)
-  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(stg + BM * BN * 4);
+  const int bn = p.bn, nst = p.stages;
+  const std::uint32_t stage_b = static_cast<std::uint32_t>(BK * bn);
+  std::uint8_t* sa = base;                              // stages x 16 KB
+  std::uint8_t* sbm = sa + nst * kStageA;               // stages x (16 | 32) KB
+  std::uint8_t* stg = sbm + nst * stage_b;              // 64 KB output staging (4 x 16 KB column quarters)
+  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(stg + BM * 128 * 4);
   std::uint64_t* full = bars;
   std::uint64_t* empty = bars + kStages;
   std::uint64_t* tfull = bars + 2 * kStages;
@@ -198,6 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   std::uint64_t* peer_full = bars + 2 * kStages + 4;   // rank 0: rank 1's partial tile is staged
   std::uint64_t* peer_empty = bars + 2 * kStages + 5;  // rank 1: rank 0 has read it
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 2 * kStages + 6);
+  const std::uint32_t tmem_cols = static_cast<std::uint32_t>(2 * bn);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int tiles = p.tiles_m * p.tiles_n;
   const bool split = p.ksplit > 1;
@@ -208,7 +214,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int kb_hi = split ? min(p.kblocks, kb_lo + p.kb_per) : p.kblocks;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; s++) {
+    for (int s = 0; s < nst; s++) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -222,7 +228,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(256));
+                 "r"(tmem_cols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -239,14 +245,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       std::uint32_t phase = 0;
       for (int t = t_first; t < tiles; t += t_step) {
-        const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * BN;
+        const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * bn;
         for (int kb = kb_lo; kb < kb_hi; kb++) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], kStageA + kStageB);
+          mbar_expect_tx(&full[stage], kStageA + stage_b);
           tma_load_2d(smem_u32(sa + stage * kStageA), &amap, &full[stage], kb * p.bk_el, m0);
-          if (p.b_kmajor) tma_load_2d(smem_u32(sbm + stage * kStageB), &bmap, &full[stage], kb * p.bk_el, n0);
-          else tma_load_2d(smem_u32(sbm + stage * kStageB), &bmap, &full[stage], n0, kb * p.bk_el);
-          if (++stage == kStages) {
+          if (p.b_kmajor) {
+            tma_load_2d(smem_u32(sbm + stage * stage_b), &bmap, &full[stage], kb * p.bk_el, n0);
+          } else {  // 128-element MN blocks of BK k-rows each (LBO = 16 KB in the descriptor)
+            for (int j = 0; j < bn / 128; j++)
+              tma_load_2d(smem_u32(sbm + stage * stage_b + j * 16384), &bmap, &full[stage], n0 + j * 128, kb * p.bk_el);
+          }
+          if (++stage == nst) {
             stage = 0;
             phase ^= 1;
           }
@@ -261,12 +271,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int acc = iter & 1;
         mbar_wait(&tempty[acc], ((iter >> 1) & 1) ^ 1);
         tc_fence_after();
-        const std::uint32_t d = tmem_base + static_cast<std::uint32_t>(acc * BN);
+        const std::uint32_t d = tmem_base + static_cast<std::uint32_t>(acc * bn);
         for (int kb = kb_lo; kb < kb_hi; kb++) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const std::uint32_t a0 = (smem_u32(sa + stage * kStageA) >> 4) | (1u << 16);
-          const std::uint32_t bsm = smem_u32(sbm + stage * kStageB);
+          const std::uint32_t bsm = smem_u32(sbm + stage * stage_b);
 #pragma unroll
           for (int ks = 0; ks < BK / 32; ks++) {
             // A: +32 bytes along the 128-byte K row; B: K-major +32 bytes, N-major +32 rows (4 KB)
@@ -277,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             else umma_i8(d, a0 + ks * 2, kHiSW128, b_lo, kHiSW128, p.idesc, accum);
           }
           umma_commit(&empty[stage]);
-          if (++stage == kStages) {
+          if (++stage == nst) {
             stage = 0;
             phase ^= 1;
           }
@@ -292,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int iter = 0;
     for (int t = t_first; t < tiles; t += t_step, iter++) {
       const int acc = iter & 1;
-      const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * BN;
+      const int m0 = (t / p.tiles_n) * BM, n0 = (t % p.tiles_n) * bn;
       if (split && rank == 1) {
         // park the partial tile in the own staging buffer (same swizzled layout rank 0 uses)
         if (iter > 0) mbar_wait_cluster(peer_empty, (iter - 1) & 1);
@@ -301,7 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int h = 0; h < BN / 32; h++) {
           std::uint32_t v[32];
           tmem_ld32(tmem_base + (static_cast<std::uint32_t>(quarter * 32) << 16) +
-                        static_cast<std::uint32_t>(acc * BN + h * 32),
+                        static_cast<std::uint32_t>(acc * bn + h * 32),
                     v);
           const std::uint32_t rbase = smem_u32(stg + h * 16384 + row * 128);
 #pragma unroll
@@ -320,12 +330,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       mbar_wait(&tfull[acc], (iter >> 1) & 1);
       tc_fence_after();
-      for (int h = 0; h < BN / 32; h++) {
+      for (int h = 0; h < bn / 32; h++) {
         std::uint32_t v[32];
-        tmem_ld32(tmem_base + (static_cast<std::uint32_t>(quarter * 32) << 16) + static_cast<std::uint32_t>(acc * BN + h * 32),
+        tmem_ld32(tmem_base + (static_cast<std::uint32_t>(quarter * 32) << 16) + static_cast<std::uint32_t>(acc * bn + h * 32),
                   v);
+        if (p.tma_out && h > 0 && (h & 3) == 0) {
+          // 256-wide tiles: the first 128 columns go out before the staging is reused
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (leader) {
+            for (int q = 0; q < 4; q++)
+              asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                               reinterpret_cast<std::uint64_t>(&cmap)),
+                           "r"(smem_u32(stg + q * 16384)), "r"(n0 + (h - 4 + q) * 32), "r"(m0)
+                           : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+        }
         if (p.tma_out) {
-          std::uint32_t rbase = smem_u32(stg + h * 16384 + row * 128);
+          std::uint32_t rbase = smem_u32(stg + (h & 3) * 16384 + row * 128);
           if (split) {  // + rank 1's partial, read over DSMEM at the same swizzled address
             if (h == 0) mbar_wait_cluster(peer_full, iter & 1);
             const std::uint32_t pbase = peer_addr(rbase, 1);
@@ -373,10 +398,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (leader) {
-          for (int h = 0; h < BN / 32; h++)
+          const int hq0 = bn / 32 - 4;  // the last 128 columns are still staged
+          for (int q = 0; q < 4; q++)
             asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                              reinterpret_cast<std::uint64_t>(&cmap)),
-                         "r"(smem_u32(stg + h * 16384)), "r"(n0 + h * 32), "r"(m0)
+                         "r"(smem_u32(stg + q * 16384)), "r"(n0 + (hq0 + q) * 32), "r"(m0)
                          : "memory");
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
@@ -390,7 +416,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(256));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols));
   }
 }
 
@@ -406,7 +432,8 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-constexpr std::size_t kSmem = 1024 + kStages * (kStageA + kStageB) + BM * BN * 4 + 256;
+std::size_t smem_bytes(int bn, int stages) { return 1024 + stages * (kStageA + BK * bn) + BM * 128 * 4 + 256; }
+constexpr std::size_t kSmemMax = 1024 + 3 * (BM * BK + BK * 256) + BM * 128 * 4 + 256;
 
 struct Prepared {
   GemmPlan gp;
@@ -424,7 +451,7 @@ bool same(const GemmPlan& x, const GemmPlan& y) {
 std::mutex g_mu;
 std::vector<Prepared>* g_prep = nullptr;
 
-cudaError_t prepare(const GemmPlan& g, const GemmArgs& args, Prepared* out) {
+cudaError_t prepare(const GemmPlan& g, const GemmArgs& args, Prepared* out, int num_sms) {
   out->gp = g;
   out->a = args.a;
   out->b = args.b;
@@ -441,7 +468,12 @@ cudaError_t prepare(const GemmPlan& g, const GemmArgs& args, Prepared* out) {
   kp.tf32 = g.tf32x3 ? 1 : 0;
   kp.bk_el = bk_el;
   kp.tiles_m = static_cast<int>((g.M + BM - 1) / BM);
-  kp.tiles_n = static_cast<int>((g.N + BN - 1) / BN);
+  // 256-wide tiles when every SM still gets at least two of them (SB_GEMM_BN=128|256 forces)
+  const long long wide_tiles = static_cast<long long>(kp.tiles_m) * ((g.N + 255) / 256);
+  kp.bn = !g.tf32x3 && g.N >= 256 && wide_tiles >= 2ll * num_sms ? 256 : 128;
+  if (const char* f = std::getenv("SB_GEMM_BN")) kp.bn = !g.tf32x3 && std::atoi(f) == 256 ? 256 : 128;
+  kp.stages = kp.bn == 256 ? 3 : kStages;
+  kp.tiles_n = static_cast<int>((g.N + kp.bn - 1) / kp.bn);
   kp.kblocks = static_cast<int>((g.K + bk_el - 1) / bk_el);
   kp.b_kmajor = g.b_kmajor ? 1 : 0;
   kp.fresh = g.fresh ? 1 : 0;
@@ -452,8 +484,8 @@ cudaError_t prepare(const GemmPlan& g, const GemmArgs& args, Prepared* out) {
                reinterpret_cast<std::uintptr_t>(kp.c) % 16 == 0;
   // idesc: S32 accumulate, signed A/B, A K-major, B K- or MN-major, N = 128, M = 128
   const std::uint32_t sgn = g.unsigned_ab ? 0u : 1u;  // atype/btype: 0 = U8, 1 = S8
-  kp.idesc = (2u << 4) | (sgn << 7) | (sgn << 10) | ((kp.b_kmajor ? 0u : 1u) << 16) | ((128u >> 3) << 17) |
-             ((128u >> 4) << 24);
+  kp.idesc = (2u << 4) | (sgn << 7) | (sgn << 10) | ((kp.b_kmajor ? 0u : 1u) << 16) |
+             ((static_cast<std::uint32_t>(kp.bn) >> 3) << 17) | ((128u >> 4) << 24);
   if (g.tf32x3)  // D = F32 (1), A = B = TF32 (2), both K-major
     kp.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
   const CUtensorMapDataType ttype = g.tf32x3 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT8;
@@ -474,11 +506,11 @@ cudaError_t prepare(const GemmPlan& g, const GemmArgs& args, Prepared* out) {
     bdim[0] = static_cast<cuuint64_t>(g.K);
     bdim[1] = static_cast<cuuint64_t>(g.N);
     bbox[0] = static_cast<cuuint32_t>(bk_el);
-    bbox[1] = BN;
-  } else {
+    bbox[1] = static_cast<cuuint32_t>(kp.bn);
+  } else {  // 128-element MN boxes (one 128-byte swizzle span); 256-wide tiles load two
     bdim[0] = static_cast<cuuint64_t>(g.N);
     bdim[1] = static_cast<cuuint64_t>(g.K);
-    bbox[0] = BN;
+    bbox[0] = 128;
     bbox[1] = BK;
   }
   if (encode(&out->bmap, ttype, 2, const_cast<std::int8_t*>(b), bdim, bstr, bbox, es,
@@ -498,7 +530,7 @@ cudaError_t prepare(const GemmPlan& g, const GemmArgs& args, Prepared* out) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(gemm_i8_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kSmem));
+                                         static_cast<int>(std::max(kSmemMax, smem_bytes(128, kStages))));
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -1218,7 +1250,7 @@ cudaError_t launch_gemm_tc(const GemmPlan& g, const GemmArgs& args, cudaStream_t
     if (!pr) {
       if (g_prep->size() >= 256) g_prep->clear();
       Prepared fresh;
-      cudaError_t err = prepare(g, args, &fresh);
+      cudaError_t err = prepare(g, args, &fresh, num_sms);
       if (err != cudaSuccess) return err;
       g_prep->push_back(fresh);
       pr = &g_prep->back();
@@ -1233,7 +1265,7 @@ cudaError_t launch_gemm_tc(const GemmPlan& g, const GemmArgs& args, cudaStream_t
   // (SB_GEMM_SPLIT=1), measured slower at config 1 (1024^3: 11.2 vs 7.8 us per pipelined step,
   // 17.5 vs 13.4 us per launch; the pair's DSMEM hand-off serialises both epilogues)
   kp.ksplit = 1;
-  if (kp.tma_out && !kp.tf32 && kp.kblocks >= 2 && 2 * tiles <= num_sms && std::getenv("SB_GEMM_SPLIT")) {
+  if (kp.tma_out && !kp.tf32 && kp.bn == 128 && kp.kblocks >= 2 && 2 * tiles <= num_sms && std::getenv("SB_GEMM_SPLIT")) {
     kp.ksplit = 2;
     kp.kb_per = (kp.kblocks + 1) / 2;
   }
@@ -1241,7 +1273,7 @@ cudaError_t launch_gemm_tc(const GemmPlan& g, const GemmArgs& args, cudaStream_t
   const int ctas = kp.ksplit * tiles;
   cfg.gridDim = dim3(static_cast<unsigned>(kp.ksplit > 1 ? ctas : (tiles < num_sms ? tiles : num_sms)));
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = kSmem;
+  cfg.dynamicSmemBytes = smem_bytes(kp.bn, kp.stages);
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   int na = 0;

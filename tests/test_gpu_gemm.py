@@ -59,6 +59,42 @@ def test_matmul_pair_split_path(monkeypatch, mnk):
     check(W.matmul(*mnk, in_dtype="i8", out_dtype="i32"))
 
 
+def check_exact_np(text, a_shape, b_shape, bt=False, seed=5):
+    """Large shapes: the exact int64 product (numpy) wrapped to i32 is the reference's value
+    (i8 x i8 products summed in int64, stored with i32 wrap; interp.cpp / ir.cpp:79-97)."""
+    import paper_1903_06498_b200 as sb
+    p = sb.parse_program(text)
+    assert "gemm_i8_tc" in p.describe_plan(True)
+    rng = np.random.default_rng(seed)
+    a = rng.integers(-128, 128, a_shape, dtype=np.int64)
+    b = rng.integers(-128, 128, b_shape, dtype=np.int64)
+    store = {"A": sb.Buffer(p.buffers["A"].dtype, a.ravel().copy()), "B": sb.Buffer(p.buffers["B"].dtype, b.ravel().copy())}
+    sb.prepare_outputs(p, store)
+    sb.execute(p, store)
+    exp = (a @ (b.T if bt else b)).astype(np.int32).astype(np.int64)
+    np.testing.assert_array_equal(store["C"].data.reshape(exp.shape), exp)
+
+
+@pytest.mark.parametrize("shape", [(2048, 4864, 256, "n"), (2048, 4800, 384, "n"), (2048, 4864, 256, "k"),
+                                   (1920, 5120, 128, "n")], ids=lambda s: "x".join(map(str, s)))
+def test_matmul_wide_tiles(shape):
+    """128 x 256 tiles (N = 256 MMAs, two 128-element MN boxes of B per stage or one 256-row
+    K-major box, the staged i32 output stored in two 128-column halves), chosen when every SM
+    gets at least two of them; ragged N included."""
+    M, N, K, major = shape
+    if major == "n":
+        check_exact_np(W.matmul(M, N, K, in_dtype="i8", out_dtype="i32"), (M, K), (K, N))
+    else:
+        check_exact_np(W.matmul_bt(M, N, K), (M, K), (N, K), bt=True)
+
+
+def test_matmul_wide_tiles_forced_and_accumulating(monkeypatch):
+    monkeypatch.setenv("SB_GEMM_BN", "256")
+    check(W.matmul(384, 512, 256, in_dtype="i8", out_dtype="i32"))
+    check(W.matmul(256, 768, 128, in_dtype="i8", out_dtype="i32"), provide_out=True)
+    check(W.matmul(128, 400, 256, in_dtype="i8", out_dtype="i16"))
+
+
 def test_matmul_b_k_major():
     check(W.matmul_bt(192, 160, 256))
 
