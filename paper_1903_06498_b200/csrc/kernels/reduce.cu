@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <limits>
 
 #include "../kernels.hpp"
@@ -118,6 +119,85 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceArgs a) {
   }
 }
 
+// Short reductions (rcount <= 8: max-pool windows, small sums) over index spaces that fit
+// 32 bits: 32-bit index math (64-bit div/mod costs several times the instructions the
+// loads themselves take at 16 bytes per thread) and all rcount vector loads in flight before
+// the fold.  The offsets come straight from the serial dims (no shared-memory table).
+constexpr int kShortR = 8;
+
+template <int AGG, typename TI, typename TO>
+__global__ void __launch_bounds__(256) reduce_short_kernel(const ReduceArgs a) {
+  constexpr int V = Vec16<TI>::N;
+  int roff[kShortR];
+#pragma unroll
+  for (int r = 0; r < kShortR; r++) {
+    int rest = r, off = 0;
+    for (int i = a.nr - 1; i >= 0; i--) {
+      off += (rest % static_cast<int>(a.rrange[i])) * static_cast<int>(a.rstep[i]);
+      rest /= static_cast<int>(a.rrange[i]);
+    }
+    roff[r] = off;
+  }
+  const TI* in = static_cast<const TI*>(a.in);
+  TO* out = static_cast<TO*>(a.out);
+  const int nvec = static_cast<int>(a.prange[0] / V);
+  const int total = static_cast<int>(a.pcount / V);
+  for (int lin = blockIdx.x * blockDim.x + threadIdx.x; lin < total; lin += gridDim.x * blockDim.x) {
+    int rest = lin / nvec;
+    const int c0 = (lin - rest * nvec) * V;
+    int ib = static_cast<int>(a.in_c) + c0, ob = static_cast<int>(a.out_c) + c0;
+    for (int i = 1; i < a.np; i++) {
+      const int pr = static_cast<int>(a.prange[i]);
+      const int q = rest / pr;
+      const int c = rest - q * pr;
+      rest = q;
+      ib += c * static_cast<int>(a.pin[i]);
+      ob += c * static_cast<int>(a.pout[i]);
+    }
+    int4 w[kShortR];  // raw 16-byte vectors, all loads in flight before the fold
+#pragma unroll
+    for (int r = 0; r < kShortR; r++)
+      if (r < a.rcount) w[r] = __ldg(reinterpret_cast<const int4*>(in + ib + roff[r]));
+    std::int64_t acc[V];
+#pragma unroll
+    for (int l = 0; l < V; l++) acc[l] = a.fresh ? a.identity : static_cast<std::int64_t>(out[ob + l]);
+#pragma unroll
+    for (int r = 0; r < kShortR; r++)
+      if (r < a.rcount) {
+        const TI* x = reinterpret_cast<const TI*>(&w[r]);
+#pragma unroll
+        for (int l = 0; l < V; l++) acc[l] = agg<AGG, TO>(acc[l], x[l]);
+      }
+    constexpr int per16 = 16 / sizeof(TO);
+#pragma unroll
+    for (int q = 0; q < V / per16; q++) {
+      int4 w;
+      TO* st = reinterpret_cast<TO*>(&w);
+#pragma unroll
+      for (int l = 0; l < per16; l++) st[l] = static_cast<TO>(acc[q * per16 + l]);
+      *reinterpret_cast<int4*>(out + ob + q * per16) = w;
+    }
+  }
+}
+
+// whether every index reduce_short_kernel forms fits a positive int
+bool short_ok(const ReduceArgs& a, int V) {
+  if (a.rcount < 1 || a.rcount > kShortR || std::getenv("SB_REDUCE_LONG")) return false;
+  const std::int64_t lim = (1ll << 31) - 1;
+  std::int64_t in_hi = a.in_c + a.prange[0], out_hi = a.out_c + a.prange[0], r_hi = 0;
+  if (a.in_c < 0 || a.out_c < 0 || a.pcount / V > lim) return false;
+  for (int i = 1; i < a.np; i++) {
+    if (a.pin[i] < 0 || a.pout[i] < 0) return false;
+    in_hi += (a.prange[i] - 1) * a.pin[i];
+    out_hi += (a.prange[i] - 1) * a.pout[i];
+  }
+  for (int i = 0; i < a.nr; i++) {
+    if (a.rstep[i] < 0) return false;
+    r_hi += (a.rrange[i] - 1) * a.rstep[i];
+  }
+  return in_hi + r_hi + V < lim && out_hi + V < lim;
+}
+
 // Few outputs, long reductions (the ResNet global sum: 16K vectors x 49 rows): a block is 32
 // output vectors x kSplit row phases; each thread folds rows r = phase (mod kSplit) into
 // an identity-started accumulator, then the kSplit partials are folded in shared memory.
@@ -215,6 +295,14 @@ cudaError_t dispatch_out(const ReduceArgs& a, int grid, std::size_t smem, cudaSt
       case kI8: reduce_split_kernel<AGG, TI, std::int8_t><<<sgrid, 256, ssmem, s>>>(a); break;
       case kI16: reduce_split_kernel<AGG, TI, std::int16_t><<<sgrid, 256, ssmem, s>>>(a); break;
       default: reduce_split_kernel<AGG, TI, std::int32_t><<<sgrid, 256, ssmem, s>>>(a); break;
+    }
+    return cudaGetLastError();
+  }
+  if (short_ok(a, V)) {
+    switch (a.out_kind) {
+      case kI8: reduce_short_kernel<AGG, TI, std::int8_t><<<grid, 256, 0, s>>>(a); break;
+      case kI16: reduce_short_kernel<AGG, TI, std::int16_t><<<grid, 256, 0, s>>>(a); break;
+      default: reduce_short_kernel<AGG, TI, std::int32_t><<<grid, 256, 0, s>>>(a); break;
     }
     return cudaGetLastError();
   }

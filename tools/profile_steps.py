@@ -52,6 +52,10 @@ def program_text(which, batch):
         text = W.pool2d(batch, 112, 112, 64)
     elif which == "l1x1":
         text = W.conv_fused(batch, 56, 56, 64, 64, 1, 1, 1, 0)
+    elif which == "c4a":
+        text = W.maxpool2x2(batch, 112, 112, 64)
+    elif which == "c4b":
+        text = W.global_sum(batch, 7, 7, 2048)
     elif which == "c2":
         text = W.conv2d(32, 56, 56, 64, 64)
     else:
