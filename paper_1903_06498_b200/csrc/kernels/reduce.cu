@@ -92,7 +92,18 @@ __global__ void __launch_bounds__(256) reduce_kernel(const ReduceArgs a) {
       for (int l = 0; l < V; l++) acc[l] = out[ob + l];
     }
     int r = 0;
-    // two independent loads in flight per iteration
+    // four independent loads in flight per iteration
+    for (; r + 3 < a.rcount; r += 4) {
+      int4 w[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) w[u] = __ldg(reinterpret_cast<const int4*>(in + ib + roff[r + u]));
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const TI* x = reinterpret_cast<const TI*>(&w[u]);
+#pragma unroll
+        for (int l = 0; l < V; l++) acc[l] = agg<AGG, TO>(acc[l], x[l]);
+      }
+    }
     for (; r + 1 < a.rcount; r += 2) {
       TI x[V], y[V];
       load16<TI>(in + ib + roff[r], x);
@@ -253,13 +264,27 @@ __global__ void __launch_bounds__(256) reduce_split_kernel(const ReduceArgs a) {
     std::int64_t acc[V];
 #pragma unroll
     for (int l = 0; l < V; l++) acc[l] = agg_identity<AGG, TO>();
-    if (live)
-      for (int r = phase; r < a.rcount; r += kSplit) {
+    if (live) {
+      // four rows of this phase per step, their loads in flight before the folds
+      int r = phase;
+      for (; r + 3 * kSplit < a.rcount; r += 4 * kSplit) {
+        int4 w[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) w[u] = __ldg(reinterpret_cast<const int4*>(in + ib + roff[r + u * kSplit]));
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const TI* x = reinterpret_cast<const TI*>(&w[u]);
+#pragma unroll
+          for (int l = 0; l < V; l++) acc[l] = agg<AGG, TO>(acc[l], x[l]);
+        }
+      }
+      for (; r < a.rcount; r += kSplit) {
         TI x[V];
         load16<TI>(in + ib + roff[r], x);
 #pragma unroll
         for (int l = 0; l < V; l++) acc[l] = agg<AGG, TO>(acc[l], x[l]);
       }
+    }
 #pragma unroll
     for (int l = 0; l < V; l++) part[threadIdx.x * V + l] = acc[l];
     __syncthreads();

@@ -56,6 +56,8 @@ def program_text(which, batch):
         text = W.maxpool2x2(batch, 112, 112, 64)
     elif which == "c4b":
         text = W.global_sum(batch, 7, 7, 2048)
+    elif which == "gsum_i8":  # C5's global sum (7x7, 2048 channels, i8)
+        text = W.global_sum(batch, 7, 7, 2048, in_dtype="i8", out_dtype="i8")
     elif which == "c2":
         text = W.conv2d(32, 56, 56, 64, 64)
     else:
