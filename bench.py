@@ -526,6 +526,9 @@ def e2e_native(args, sb, np, torch, dist, world, ctx, prog, nbytes, in_names, ou
     from pinned host memory and its outputs out; step i's D2H overlaps step i+1's H2D."""
     ctx.set_stream(None)
     ctxs = [ctx, sb.Context(local)]
+    ordered = not os.environ.get("SB_E2E_UNORDERED")
+    for c_ in ctxs:  # one step's kernels at a time; copies overlap the other step's kernels
+        c_.set_kernel_order(ordered)
     pins, hosts = [], []
     for _ in ctxs:
         host = {}
@@ -563,7 +566,8 @@ def e2e_native(args, sb, np, torch, dist, world, ctx, prog, nbytes, in_names, ou
     return {"value": round(tot * steps / float(te.item()) / 1e9, 3), "unit": unit, "h2d_bytes_per_step": int(sum(nbytes[n] for n in in_names)),
             "d2h_bytes_per_step": int(sum(nbytes[n] for n in out_names)), "steps": steps,
             "api": "sb_execute_async, native-width pinned host buffers",
-            "timer": "host wall clock from the first sb_execute_async to the last context sync (2 contexts)"}
+            "timer": "host wall clock from the first sb_execute_async to the last context sync (2 contexts)",
+            "kernel_order": ordered}
 
 
 def e2e_dropin(args, sb, np, torch, dist, world, ctx, prog, in_names, out_names, work, unit, dev):

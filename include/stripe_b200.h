@@ -159,6 +159,12 @@ void sb_context_destroy(sb_context* ctx);
 /* Launch on an external cudaStream_t (e.g. torch's current stream); NULL = own stream. */
 int sb_context_set_stream(sb_context* ctx, void* cuda_stream);
 void* sb_context_stream(sb_context* ctx);
+/* Kernel order across contexts (host-buffer executes, sb_execute / sb_execute_async): while
+ * enabled, this context's kernels start only after the kernels of the previous execute of any
+ * ordered context on the same device; its host<->device copies are not held back.  Two
+ * contexts ping-ponging steps then overlap one step's copies with the other's kernels
+ * without running both steps' kernels at once. */
+int sb_context_set_kernel_order(sb_context* ctx, int enable);
 /* Waits for the stream and reports any device-side error (OutOfBoundsAccess ...). */
 int sb_context_sync(sb_context* ctx);
 /* Number of kernels this library launched on the context so far. */

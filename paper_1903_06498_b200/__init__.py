@@ -46,6 +46,7 @@ EXPORTED = [
     "sb_program_output_aggregation", "sb_program_restrict_index", "sb_program_check_split", "sb_count_valid_points",
     "sb_tile_cost", "sb_autotile",
     "sb_context_create", "sb_context_destroy", "sb_context_set_stream", "sb_context_stream",
+    "sb_context_set_kernel_order",
     "sb_context_sync", "sb_context_launch_count", "sb_context_set_profile", "sb_context_profile_read", "sb_device_alloc", "sb_device_free",
     "sb_host_alloc_pinned", "sb_host_free_pinned", "sb_execute", "sb_execute_device", "sb_execute_async",
     "sb_graph_begin", "sb_graph_end", "sb_graph_launch", "sb_graph_free",
@@ -124,6 +125,7 @@ def lib() -> ctypes.CDLL:
         L.sb_context_destroy.argtypes = [vp]
         L.sb_context_destroy.restype = None
         L.sb_context_set_stream.argtypes = [vp, vp]
+        L.sb_context_set_kernel_order.argtypes = [vp, i32]
         L.sb_context_stream.argtypes = [vp]
         L.sb_context_stream.restype = vp
         L.sb_context_sync.argtypes = [vp]
@@ -353,6 +355,10 @@ class Context:
 
     def sync(self) -> None:
         _check(lib().sb_context_sync(self._h))
+
+    def set_kernel_order(self, enable: bool) -> None:
+        """sb_context_set_kernel_order: kernels queue behind other ordered contexts' kernels."""
+        _check(lib().sb_context_set_kernel_order(self._h, int(enable)))
 
     def set_profile(self, enable: bool) -> None:
         _check(lib().sb_context_set_profile(self._h, int(enable)))

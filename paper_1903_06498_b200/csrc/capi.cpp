@@ -130,6 +130,10 @@ struct sb_context {
   cudaEvent_t aux_fork = nullptr, aux_join[4] = {};
   std::vector<std::pair<void*, std::size_t>> roots;  // host-path device buffers
   std::vector<std::pair<void*, std::size_t>> pinned;  // host-path staging
+  // sb_context_set_kernel_order: this context's kernel phases queue behind the last kernel
+  // phase of every other ordered context on the device (its copies do not)
+  bool ordered = false;
+  cudaEvent_t kernels_done = nullptr;
   bool profile = false;      // per-step device times (sb_context_set_profile)
   std::string profile_text;  // "step ms kernel path points" lines since the last read
 
@@ -171,10 +175,22 @@ std::atomic<std::uint64_t> g_next_plan_id{1};
 
 }  // namespace
 
+// Device-wide order of the kernel phases of ordered contexts (sb_context_set_kernel_order).
+struct KernelOrder {
+  std::mutex mu;
+  cudaEvent_t last = nullptr;  // the kernels_done event of the last ordered kernel phase
+};
+KernelOrder g_kernel_order[64];
+
 sb_context::~sb_context() {
   {
     std::lock_guard<std::mutex> lock(g_registry_mu);
     g_contexts.erase(this);
+  }
+  if (kernels_done) {
+    std::lock_guard<std::mutex> lock(g_kernel_order[device & 63].mu);
+    if (g_kernel_order[device & 63].last == kernels_done) g_kernel_order[device & 63].last = nullptr;
+    cudaEventDestroy(kernels_done);
   }
   body_dtor();
 }
@@ -955,6 +971,16 @@ int sb_context_set_stream(sb_context* ctx, void* s) {
 
 void* sb_context_stream(sb_context* ctx) { return ctx->stream; }
 
+int sb_context_set_kernel_order(sb_context* ctx, int enable) {
+  return guarded([&] {
+    std::lock_guard<std::recursive_mutex> lock(ctx->mu);
+    cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (enable && !ctx->kernels_done)
+      cuda_check(cudaEventCreateWithFlags(&ctx->kernels_done, cudaEventDisableTiming), "cudaEventCreate(order)");
+    ctx->ordered = enable != 0;
+  });
+}
+
 int sb_context_sync(sb_context* ctx) {
   return guarded([&] {
     std::lock_guard<std::recursive_mutex> lock(ctx->mu);
@@ -1131,9 +1157,22 @@ int execute_host(sb_context* ctx, sb_program* p, sb_host_buffer* bufs, int n, co
                  "H2D");
     }
     {
-      // reuse the device path for prepare-fills + plan execution
+      // reuse the device path for prepare-fills + plan execution; an ordered context's
+      // kernels wait for the previous ordered kernel phase on this device (two contexts
+      // ping-ponging steps then overlap copies with kernels without running two steps'
+      // kernels at once, which would split L2 between their activations)
+      std::unique_lock<std::mutex> order;
+      if (ctx->ordered) {
+        KernelOrder& ko = g_kernel_order[ctx->device & 63];
+        order = std::unique_lock<std::mutex>(ko.mu);
+        if (ko.last) cuda_check(cudaStreamWaitEvent(ctx->stream, ko.last, 0), "cudaStreamWaitEvent(order)");
+      }
       int rc = sb_execute_device(ctx, p, dev.data(), static_cast<int>(nr), opts);
       if (rc != SB_OK) throw sb::Error(sb_status_name(rc), g_last_error);
+      if (ctx->ordered) {
+        cuda_check(cudaEventRecord(ctx->kernels_done, ctx->stream), "cudaEventRecord(order)");
+        g_kernel_order[ctx->device & 63].last = ctx->kernels_done;
+      }
     }
     for (std::size_t r = 0; r < nr; r++) {
       const auto& b = prog.buffers[r];

@@ -146,7 +146,8 @@ def test_fused_epilogue_int64_semantics_near_overflow():
     np.testing.assert_array_equal(got["O"], exp["O"])
 
 
-def test_async_two_context_pingpong_matches_sync():
+@pytest.mark.parametrize("ordered", [False, True])
+def test_async_two_context_pingpong_matches_sync(ordered):
     """sb_execute_async on two contexts (the bench's e2e pattern) gives the sync results."""
     import ctypes
 
@@ -155,6 +156,8 @@ def test_async_two_context_pingpong_matches_sync():
     text = W.conv2d(4, 10, 10, 64, 64)
     prog = sb.parse_program(text)
     ctxs = [sb.Context(0), sb.Context(0)]
+    for c in ctxs:  # sb_context_set_kernel_order: kernels one step at a time, copies overlap
+        c.set_kernel_order(ordered)
     pins = []
 
     def pinned(n, ct):
