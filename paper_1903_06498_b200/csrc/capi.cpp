@@ -17,6 +17,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <thread>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -1086,6 +1087,47 @@ int sb_execute_device(sb_context* ctx, sb_program* p, const sb_device_buffer* bu
 }  // extern "C"
 
 namespace {
+// int64 carriers <-> native width on the host (the drop-in boundary's BufferStore, interp.h:14-17):
+// memory-bound loops split over host threads for large buffers.
+template <typename F>
+void parallel_elems(std::int64_t n, F&& f) {
+  const std::int64_t kMin = 1 << 20;
+  unsigned hw = std::thread::hardware_concurrency();
+  int nt = static_cast<int>(std::min<std::int64_t>(std::max(1u, std::min(hw, 16u)), (n + kMin - 1) / kMin));
+  if (nt <= 1) {
+    f(0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  const std::int64_t chunk = (n + nt - 1) / nt;
+  for (int t = 1; t < nt; t++) {
+    const std::int64_t lo = t * chunk, hi = std::min(n, lo + chunk);
+    if (lo < hi) th.emplace_back([&f, lo, hi] { f(lo, hi); });
+  }
+  f(0, std::min(n, chunk));
+  for (auto& x : th) x.join();
+}
+
+void narrow_from_i64(const std::int64_t* in, void* out, int kind, std::int64_t n) {
+  parallel_elems(n, [&](std::int64_t lo, std::int64_t hi) {
+    switch (kind) {
+      case sb::kI8: for (std::int64_t e = lo; e < hi; e++) static_cast<std::int8_t*>(out)[e] = static_cast<std::int8_t>(in[e]); break;
+      case sb::kI16: for (std::int64_t e = lo; e < hi; e++) static_cast<std::int16_t*>(out)[e] = static_cast<std::int16_t>(in[e]); break;
+      default: for (std::int64_t e = lo; e < hi; e++) static_cast<std::int32_t*>(out)[e] = static_cast<std::int32_t>(in[e]); break;
+    }
+  });
+}
+
+void widen_to_i64(const void* in, std::int64_t* out, int kind, std::int64_t n) {
+  parallel_elems(n, [&](std::int64_t lo, std::int64_t hi) {
+    switch (kind) {
+      case sb::kI8: for (std::int64_t e = lo; e < hi; e++) out[e] = static_cast<const std::int8_t*>(in)[e]; break;
+      case sb::kI16: for (std::int64_t e = lo; e < hi; e++) out[e] = static_cast<const std::int16_t*>(in)[e]; break;
+      default: for (std::int64_t e = lo; e < hi; e++) out[e] = static_cast<const std::int32_t*>(in)[e]; break;
+    }
+  });
+}
+
 int execute_host(sb_context* ctx, sb_program* p, sb_host_buffer* bufs, int n, const sb_exec_options* opts, bool async) {
   return guarded([&] {
     std::lock_guard<std::recursive_mutex> lock(ctx->mu);
@@ -1142,15 +1184,8 @@ int execute_host(sb_context* ctx, sb_program* p, sb_host_buffer* bufs, int n, co
           cuda_check(cudaMallocHost(&ctx->pinned[r].first, bytes), "cudaMallocHost");
           ctx->pinned[r].second = bytes;
         }
-        const auto* in = static_cast<const std::int64_t*>(hb.data);
         void* st = ctx->pinned[r].first;
-        for (std::int64_t e = 0; e < b.elements; e++) {
-          switch (kind) {
-            case sb::kI8: static_cast<std::int8_t*>(st)[e] = static_cast<std::int8_t>(in[e]); break;
-            case sb::kI16: static_cast<std::int16_t*>(st)[e] = static_cast<std::int16_t>(in[e]); break;
-            default: static_cast<std::int32_t*>(st)[e] = static_cast<std::int32_t>(in[e]); break;
-          }
-        }
+        narrow_from_i64(static_cast<const std::int64_t*>(hb.data), st, kind, b.elements);
         src = st;
       }
       cuda_check(cudaMemcpyAsync(ptrs[r], src, b.elements * kind_bytes(kind), cudaMemcpyHostToDevice, ctx->stream),
@@ -1201,15 +1236,7 @@ int execute_host(sb_context* ctx, sb_program* p, sb_host_buffer* bufs, int n, co
       sb_host_buffer& hb = bufs[slot[r]];
       if (hb.carrier != SB_CARRIER_I64) continue;
       int kind = c->plan.bufs[r].kind;
-      auto* out = static_cast<std::int64_t*>(hb.data);
-      const void* st = ctx->pinned[r].first;
-      for (std::int64_t e = 0; e < b.elements; e++) {
-        switch (kind) {
-          case sb::kI8: out[e] = static_cast<const std::int8_t*>(st)[e]; break;
-          case sb::kI16: out[e] = static_cast<const std::int16_t*>(st)[e]; break;
-          default: out[e] = static_cast<const std::int32_t*>(st)[e]; break;
-        }
-      }
+      widen_to_i64(ctx->pinned[r].first, static_cast<std::int64_t*>(hb.data), kind, b.elements);
     }
   });
 }
