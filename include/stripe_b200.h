@@ -141,6 +141,20 @@ int sb_autotile(sb_context* ctx, const sb_program* p, const char* block_path, in
  * Shards' outputs combine with the output's aggregation (all-reduce sum/max/min/prod). */
 int sb_program_restrict_index(const sb_program* p, const char* block_path, const char* index, int64_t lo,
                               int64_t hi, sb_program** out);
+/* The split-aggregation combine over NCCL (the reference has no split,
+ * tile.cpp:668-685): every rank runs its shard (sb_program_restrict_index) into fresh
+ * outputs, then sb_split_allreduce all-reduces each output's partials in place on the
+ * context stream with the output's aggregation (add -> sum, max -> max, min -> min,
+ * mul -> prod; integer wrap exact; i16 reduced as i32).  `data` = the output's device buffer
+ * at native width, `count` its element count.  NCCL (libnccl.so.2) is loaded at first use;
+ * the communicator is any ncclComm_t, or one from sb_nccl_comm_init with the 128-byte id
+ * sb_nccl_unique_id made on rank 0 and broadcast by the caller.  SB_ERR_NCCL on NCCL
+ * failures. */
+int sb_nccl_unique_id(char* id /* [128] */);
+int sb_nccl_comm_init(sb_context* ctx, int nranks, const char* id, int rank, void** comm);
+int sb_nccl_comm_destroy(void* comm);
+int sb_split_allreduce(sb_context* ctx, const sb_program* p, const char* name, void* data, int64_t count,
+                       void* nccl_comm);
 /* SB_OK when splitting ranged `index` of the block at `block_path` across shards and
  * combining the shards' outputs with each output's aggregation is exact; otherwise
  * SB_ERR_UNSUPPORTED with the reason (an assigned output, a store whose aggregation differs

@@ -44,7 +44,8 @@ EXPORTED = [
     "sb_program_parse", "sb_program_free", "sb_program_print", "sb_program_buffer_count",
     "sb_program_buffer_info", "sb_program_output_identity", "sb_program_describe_plan",
     "sb_program_output_aggregation", "sb_program_restrict_index", "sb_program_check_split", "sb_count_valid_points",
-    "sb_tile_cost", "sb_autotile",
+    "sb_tile_cost", "sb_autotile", "sb_nccl_unique_id", "sb_nccl_comm_init", "sb_nccl_comm_destroy",
+    "sb_split_allreduce",
     "sb_context_create", "sb_context_destroy", "sb_context_set_stream", "sb_context_stream",
     "sb_context_set_kernel_order",
     "sb_context_sync", "sb_context_launch_count", "sb_context_set_profile", "sb_context_profile_read", "sb_device_alloc", "sb_device_free",
@@ -115,6 +116,10 @@ def lib() -> ctypes.CDLL:
         L.sb_program_restrict_index.argtypes = [vp, ctypes.c_char_p, ctypes.c_char_p, i64, i64, ctypes.POINTER(vp)]
         L.sb_program_check_split.argtypes = [vp, ctypes.c_char_p, ctypes.c_char_p]
         L.sb_count_valid_points.argtypes = [vp, vp, ctypes.c_char_p, ctypes.POINTER(i64)]
+        L.sb_nccl_unique_id.argtypes = [ctypes.c_char_p]
+        L.sb_nccl_comm_init.argtypes = [vp, i32, ctypes.c_char_p, i32, ctypes.POINTER(vp)]
+        L.sb_nccl_comm_destroy.argtypes = [vp]
+        L.sb_split_allreduce.argtypes = [vp, vp, ctypes.c_char_p, vp, i64, vp]
         L.sb_tile_cost.argtypes = [vp, vp, ctypes.c_char_p, ctypes.c_char_p, i32, i64, i64, ctypes.POINTER(TileReport)]
         L.sb_autotile.argtypes = [vp, vp, ctypes.c_char_p, i64, i64, i32, ctypes.c_char_p, ctypes.c_size_t,
                                   ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(i32), ctypes.POINTER(TileReport),

@@ -896,6 +896,48 @@ int sb_count_valid_points(sb_context* ctx, const sb_program* p, const char* bloc
   });
 }
 
+int sb_nccl_unique_id(char* id) {
+  return guarded([&] {
+    if (!id) throw sb::Error("Invalid", "null id buffer");
+    char buf[128];
+    sb::nccl_unique_id(buf);
+    std::memcpy(id, buf, 128);
+  });
+}
+
+int sb_nccl_comm_init(sb_context* ctx, int nranks, const char* id, int rank, void** comm) {
+  return guarded([&] {
+    if (!id || !comm || nranks < 1 || rank < 0 || rank >= nranks) throw sb::Error("Invalid", "bad communicator arguments");
+    std::lock_guard<std::recursive_mutex> lock(ctx->mu);
+    cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    *comm = sb::nccl_comm_init(nranks, id, rank);
+  });
+}
+
+int sb_nccl_comm_destroy(void* comm) {
+  return guarded([&] {
+    if (comm) sb::nccl_comm_destroy(comm);
+  });
+}
+
+int sb_split_allreduce(sb_context* ctx, const sb_program* p, const char* name, void* data, int64_t count,
+                       void* nccl_comm) {
+  return guarded([&] {
+    if (!name || !nccl_comm || (count > 0 && !data)) throw sb::Error("Invalid", "null argument");
+    const int r = p->prog.buffer_index(name);
+    if (r < 0) throw sb::Error("MissingBuffer", std::string("no buffer '") + name + "'");
+    const auto& b = p->prog.buffers[r];
+    if (b.dir == sb::Dir::In) throw sb::Error("Unsupported", std::string("'") + name + "' is an input");
+    if (count != b.elements)
+      throw sb::Error("MissingBuffer", "buffer '" + b.name + "' has " + std::to_string(count) + " elements, expected " +
+                                           std::to_string(b.elements));
+    std::lock_guard<std::recursive_mutex> lock(ctx->mu);
+    cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    ctx->window.clear();  // a collective is a serialization point of the stream
+    sb::split_allreduce(nccl_comm, data, count, b.dtype, sb::output_aggregation(p->prog, name), ctx->stream);
+  });
+}
+
 int sb_program_restrict_index(const sb_program* p, const char* block_path, const char* index, int64_t lo, int64_t hi,
                               sb_program** out) {
   return guarded([&] {

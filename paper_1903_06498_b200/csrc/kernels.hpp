@@ -88,6 +88,11 @@ struct TileLineItem {
   int nq, naxes, run, val_off;
   int len[kTileMaxAxes];
 };
+// Split-aggregation combine over NCCL (kernels/collective.cu; NCCL loaded at first use).
+void nccl_unique_id(char (&id)[128]);
+void* nccl_comm_init(int nranks, const char* id, int rank);
+void nccl_comm_destroy(void* comm);
+void split_allreduce(void* comm, void* data, long long count, DType dt, Agg agg, cudaStream_t s);
 int tile_lines_smem_q();
 cudaError_t launch_tile_lines(const std::vector<TileLineItem>& items, const std::vector<long long>& values,
                               long long scratch_words, int L, std::vector<long long>* counts, cudaStream_t s);

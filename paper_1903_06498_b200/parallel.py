@@ -47,3 +47,40 @@ def allreduce_outputs(program: Program, outputs: Dict[str, object], group=None) 
         dist.all_reduce(t, op=getattr(dist.ReduceOp, AGG_OPS[agg]), group=group)
         if t.dtype == torch.int64 and int(decl.dtype) in (8, 16, 32):
             t.copy_(torch.from_numpy(_wrap(t.cpu().numpy(), int(decl.dtype))).to(t.device))
+
+
+class NcclComm:
+    """An NCCL communicator made through the C ABI (sb_nccl_unique_id on rank 0, broadcast
+    with torch.distributed -- gloo or nccl -- then sb_nccl_comm_init on every rank)."""
+
+    def __init__(self, ctx, group=None):
+        import ctypes
+
+        import torch.distributed as dist
+
+        from . import _check, lib
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        uid = ctypes.create_string_buffer(128)
+        if rank == 0:
+            _check(lib().sb_nccl_unique_id(uid))
+        box = [uid.raw]
+        if world > 1:
+            dist.broadcast_object_list(box, src=0, group=group)
+        h = ctypes.c_void_p()
+        _check(lib().sb_nccl_comm_init(ctx.handle, world, box[0], rank, ctypes.byref(h)))
+        self.handle, self.ctx, self.world, self.rank = h.value, ctx, world, rank
+
+    def close(self):
+        from . import _check, lib
+        if self.handle:
+            _check(lib().sb_nccl_comm_destroy(self.handle))
+            self.handle = None
+
+
+def allreduce_outputs_device(ctx, program: Program, outputs: Dict[str, tuple], comm: NcclComm) -> None:
+    """The C-ABI combine (sb_split_allreduce): outputs name -> (device_ptr, count) at native
+    width, reduced in place on ctx's stream with each output's aggregation over NCCL."""
+    from . import _check, lib
+    for name, (ptr, count) in outputs.items():
+        _check(lib().sb_split_allreduce(ctx.handle, program.handle, name.encode(), ptr, count, comm.handle))
