@@ -438,7 +438,8 @@ def run_ours(args):
         ach = dflops / (dom_ms / 1e3) / 1e12 if dom_ms else None
         roof = {"bound": "tensor", "achieved": round(ach, 2) if ach else None, "peak": round(pk["int8_tops"], 1),
                 "unit": "TFLOP/s", "frac": round(ach / pk["int8_tops"], 4) if ach else None,
-                "traffic": None, "peak_kind": pk["int8_kind"], "kernel": "+".join(dom),
+                "traffic": c5_traffic() if sp["cfg"] == "c5" else traffic_of(sp["cfg"]), "peak_kind": pk["int8_kind"],
+                "kernel": "+".join(dom),
                 "kernel_ms_per_step": round(dom_ms, 5), "launches_per_step": dom_launches,
                 "algorithmic_ops_per_step": dflops,
                 "network": {"achieved": round(work / (ms_per_step / 1e3) / 1e12, 2),
@@ -504,6 +505,16 @@ def sum_over_ranks(dist, world, dev, work):
     if world > 1:
         dist.all_reduce(t)
     return float(t.item())
+
+
+def c5_traffic():
+    """DRAM bytes per step of C5's conv family from the committed ncu capture of one b1024 step
+    (profiles/r02_c5_traffic.json: 26.8 GB against 28.0 GB algorithmic), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_c5_traffic.json")) as f:
+            return json.load(f)["c5"]["dram_bytes_per_step"]
+    except Exception:
+        return None
 
 
 def traffic_of(cfg):
