@@ -57,7 +57,8 @@ struct ConvKParams {
   int out_kind;           // kI8 / kI16 / kI32
   int fresh;              // overwrite (prepare_outputs identity fused) vs accumulate into O
   int tma_out;            // fresh i32 output: swizzled staging + TMA stores
-  int nstg;               // staging buffers (1 or 2)
+  int nstg;               // staging buffers (1, 2, or 4 = two per epilogue group)
+  int stages;             // strip ring depth (<= kStages; 3 when four staging buffers need the room)
   std::uint32_t staging_bytes, strip_bytes, filt_bytes, filt_tap_bytes;
   std::uint32_t tmem_cols;
   std::uint32_t idesc;
@@ -282,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   std::uint8_t* staging =
       reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t{1023});
   std::uint8_t* strips = staging + p.staging_bytes;
-  std::uint8_t* fsm = strips + kStages * p.strip_bytes + 1024;  // +slack: junk rows read past a strip
+  std::uint8_t* fsm = strips + p.stages * p.strip_bytes + 1024;  // +slack: junk rows read past a strip
   std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(fsm + p.filt_bytes);
   std::uint64_t* full = bars;
   std::uint64_t* empty = bars + kStages;
@@ -297,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) trace_at(p.trace, 48);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; s++) {
+    for (int s = 0; s < p.stages; s++) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -406,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             load_filter();
             filter_issued = true;
           }
-          if (++stage == kStages) {
+          if (++stage == p.stages) {
             stage = 0;
             phase ^= 1;
           }
@@ -465,7 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (issuer) umma_commit(&empty[stage]);  // smem slot free once these MMAs retire
           __syncwarp();
-          if (++stage == kStages) {
+          if (++stage == p.stages) {
             stage = 0;
             phase ^= 1;
           }
@@ -475,13 +476,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (issuer) { if (iter < 8) trace_at(p.trace, 24 + iter); }
       }
     }
-  } else if (warp < 6 || (p.tma_out && p.nstg == 2 && !p.st_out)) {
+  } else if (warp < 6 || (p.tma_out && p.nstg >= 2 && !p.st_out)) {
     // ---------------- epilogue: warps 2..5, or 2..9 as two groups ----------------
     // With two staging buffers the eight warps form two independent groups of four (one
     // per TMEM lane quarter each): group g owns accumulator g, staging buffer g, its own
     // named barrier and store leader, and tiles blockIdx.x + g*grid, + 2*grid, ... -- the two
     // groups' per-tile chains (TMEM drain, staging, barrier, TMA store) overlap.
-    const bool split = p.tma_out && p.nstg == 2 && !p.st_out;
+    const bool split = p.tma_out && p.nstg >= 2 && !p.st_out;
     const int eg = split ? (warp - 2) >> 2 : 0;
     const int gbar = eg ? 3 : 1;
     const int ethreads = split ? 256 : 128;
@@ -528,9 +529,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int t = blockIdx.x + eg * gridDim.x; t < p.tiles; t += tstep, iter += split ? 2 : 1) {
         int acc = iter & 1;
         std::uint32_t aphase = (iter >> 1) & 1;
-        int sb = p.nstg == 2 ? (iter & 1) : 0;  // split: iter & 1 == eg, the group's own buffer
+        // split: iter & 1 == eg, the group's own buffer; with four buffers the group alternates
+        // between its two, so tile t's TMA store drains while t + 2*grid is staged
+        int sb = p.nstg == 4 ? eg * 2 + ((iter >> 1) & 1) : p.nstg == 2 ? (iter & 1) : 0;
         if (leader) {
-          if (p.nstg == 2 && !split) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          if ((p.nstg == 2 && !split) || p.nstg == 4) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
           else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         }
         asm volatile("bar.sync %0, 128;" ::"r"(gbar) : "memory");  // staging buffer sb is free again
@@ -749,7 +752,7 @@ int pitch_for(std::int64_t W, std::int64_t S) {
 }
 
 std::size_t smem_bytes(const ConvKParams& kp) {
-  return 1024 /*align*/ + kp.staging_bytes + kStages * kp.strip_bytes + 1024 + kp.filt_bytes + 256 +
+  return 1024 /*align*/ + kp.staging_bytes + kp.stages * kp.strip_bytes + 1024 + kp.filt_bytes + 256 +
          static_cast<std::size_t>(kp.K) * 8;
 }
 
@@ -785,10 +788,27 @@ bool fill_params(const ConvPlan& cp, ConvKParams* kp) {
   if (kp->fresh && kp->out_kind == kI8 && cp.K % 64 == 0 && cp.c_y % 16 == 0 && cp.c_x % 16 == 0 &&
       cp.c_n % 16 == 0 && cp.c0 % 16 == 0)
     kp->tma_out = 2;
+  kp->stages = kStages;
+  auto stg_bytes = [&](int n) {
+    return kp->tma_out == 1 ? static_cast<std::uint32_t>(n * (cp.K / 32) * 16384)
+           : kp->tma_out == 2 ? static_cast<std::uint32_t>(n * (cp.K / 64) * 8192)
+                              : 0u;
+  };
   kp->nstg = 2;
-  kp->staging_bytes = kp->tma_out == 1   ? static_cast<std::uint32_t>(kp->nstg * (cp.K / 32) * 16384)
-                      : kp->tma_out == 2 ? static_cast<std::uint32_t>(kp->nstg * (cp.K / 64) * 8192)
-                                         : 0;
+  kp->staging_bytes = stg_bytes(2);
+  if (kp->tma_out && !std::getenv("SB_CONV_STG2")) {
+    // two staging buffers per epilogue group (a three-stage strip ring makes the room): a
+    // group stages tile t + 2*grid while tile t's TMA store still reads its other buffer
+    // (C3 37.8 -> 32.1-32.8 us, C2 10.45 -> 10.05-10.15 us; SB_CONV_STG2 = one per group)
+    kp->nstg = 4;
+    kp->stages = 3;
+    kp->staging_bytes = stg_bytes(4);
+    if (smem_bytes(*kp) > 220 * 1024) {
+      kp->nstg = 2;
+      kp->stages = kStages;
+      kp->staging_bytes = stg_bytes(2);
+    }
+  }
   if (kp->tma_out && smem_bytes(*kp) > 220 * 1024) {
     kp->nstg = 1;
     kp->staging_bytes = static_cast<std::uint32_t>(kp->tma_out == 2 ? (cp.K / 64) * 8192 : (cp.K / 32) * 16384);
