@@ -1513,7 +1513,8 @@ cudaError_t prepare(const ConvPlan& cp, const ConvArgs& args, Prepared* out) {
                     (kp.M + 2 * BM - 1) / (2 * BM) >= 2 * 148 && !std::getenv("SB_IG_MT1");
   // split i8 epilogue: two staging buffers per group when the ring keeps >= 3 stages
   // (band mode: the ring depth matters more -- one bulk copy per tile with DRAM latency to hide)
-  const bool stg4_ok = kp.epi_split && kp.tma_out == 2 && !kp.band && !std::getenv("SB_IG_STG2");
+  const bool stg4_ok = kp.epi_split && kp.tma_out == 2 && (!kp.band || std::getenv("SB_IG_BAND_STG4")) &&
+                       !std::getenv("SB_IG_STG2");
   // n-stationary resident filter slices when several n-tiles each fit (see IgKParams::nstat)
   const bool nstat_ok = !kp.gather && !kp.band && !kp.strip && !std::getenv("SB_IG_NONSTAT");
   auto try_layout = [&](int bn, int mt, bool nstat, bool stg4, bool res1, int min_stages) {
