@@ -356,7 +356,12 @@ cudaError_t launch_reduce(const ReduceArgs& a, cudaStream_t s) {
   const int V = reduce_vec_lanes(a.in_kind);
   std::int64_t threads = a.pcount / V;
   std::int64_t g = (threads + 255) / 256;
-  if (g > 148 * 16) g = 148 * 16;
+  // blocks per SM: 16 for the table-driven kernels; the short-window kernel (all loads of a
+  // window in flight per thread) streams better with 8 (C4a 106 -> 103 us, tools/ab_steps.py)
+  const int per_sm = std::getenv("SB_REDUCE_GRID") ? std::atoi(std::getenv("SB_REDUCE_GRID"))
+                     : (a.rcount >= 1 && a.rcount <= kShortR) ? 8 : 16;
+  const std::int64_t cap = 148ll * per_sm;
+  if (g > cap) g = cap;
   if (g < 1) g = 1;
   std::size_t smem = static_cast<std::size_t>(a.rcount) * sizeof(std::int64_t);
   switch (a.agg) {
