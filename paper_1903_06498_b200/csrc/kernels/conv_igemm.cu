@@ -1882,7 +1882,11 @@ cudaError_t launch_conv_fold(const ConvPlan& cp, const void* a, void* f, cudaStr
   const auto* in = static_cast<const std::int8_t*>(a);
   const int lo_u = static_cast<int>(cp.u_lo), hi_u = static_cast<int>(cp.u_hi);
   const int lo_v = static_cast<int>(cp.v_lo), hi_v = static_cast<int>(cp.v_hi);
-  const int blocks = static_cast<int>(std::min<long long>((pixels + 255) / 256, 148 * 32));
+  // one thread per folded pixel, no grid-stride cap: the stem fold (12.8 M pixels at b1024)
+  // streams better with every block in flight (stem step 437.9 -> 431.9 us against 32 blocks
+  // per SM); SB_FOLD_GRID=<blocks per SM> caps it
+  const long long fold_cap = 148ll * (std::getenv("SB_FOLD_GRID") ? std::atoi(std::getenv("SB_FOLD_GRID")) : 4096);
+  const int blocks = static_cast<int>(std::min<long long>((pixels + 255) / 256, fold_cap));
   const int Q = static_cast<int>(cp.W), NB = static_cast<int>(cp.fold_cv / 16);
   auto fixed = [&](auto kern) {
     kern<<<blocks, 256, 0, s>>>(in, static_cast<uint4*>(f), static_cast<int>(pixels), static_cast<int>(cp.fold_u),
